@@ -1,0 +1,174 @@
+"""ctypes wrapper over oracle/liboracle.so — TEST INFRASTRUCTURE ONLY.
+
+Allowed importers: tests/, __graft_entry__.smoke(), bench.py (cpu_baseline / --impl reference).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+INT_ARRAYS = {"source_index", "rect", "isect_tile", "isect_depth_bits", "isect_src", "tile_begin", "tile_end",
+              "grid", "n_contrib", "last_idx"}
+
+
+def build():
+    subprocess.check_call(["make", "-s", "-C", _HERE])
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        _LIB = C.CDLL(path)
+        for suf in ("f32", "f64"):
+            for name in ("orc_scene_new", "orc_view_camera", "orc_view_lidar"):
+                getattr(_LIB, f"{name}_{suf}").restype = C.c_void_p
+            getattr(_LIB, f"orc_scene_error_{suf}").restype = C.c_char_p
+            for name in ("orc_scene_array", "orc_view_array"):
+                getattr(_LIB, f"{name}_{suf}").restype = C.c_int64
+            ct = C.c_float if suf == "f32" else C.c_double
+            for name in ("orc_pixel_capture_offset", "orc_wrap_pi", "orc_wrap_two_pi", "orc_sigmoid"):
+                getattr(_LIB, f"{name}_{suf}").restype = ct
+            getattr(_LIB, f"orc_pixel_capture_offset_{suf}").argtypes = [C.c_int, C.c_int, ct, ct]
+            getattr(_LIB, f"orc_wrap_pi_{suf}").argtypes = [ct]
+            getattr(_LIB, f"orc_wrap_two_pi_{suf}").argtypes = [ct]
+            getattr(_LIB, f"orc_sigmoid_{suf}").argtypes = [ct]
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _suf(dtype):
+    return "f32" if np.dtype(dtype) == np.float32 else "f64"
+
+
+class OracleScene:
+    def __init__(self, scene, dtype=np.float32):
+        self.dtype = np.dtype(dtype)
+        self.suf = _suf(dtype)
+        self.L = lib()
+        s = scene.astype(self.dtype)
+        self.n, self.d_f = s.n, s.d_f
+        self.h = C.c_void_p(getattr(self.L, f"orc_scene_new_{self.suf}")(
+            C.c_int64(s.n), C.c_int(s.d_f), _p(s.mean), _p(s.scale_log), _p(s.quat), _p(s.opacity_logit), _p(s.color),
+            _p(s.feature), _p(s.actor_id)))
+        self.tracks = list(scene.tracks)
+        for tr in scene.tracks:
+            f = lambda a: np.ascontiguousarray(a, np.float64)
+            st, R, t, po, vl, va, vo = f(tr.stamps), f(tr.R), f(tr.t), f(tr.pose_offset), f(tr.vel_lin), f(tr.vel_ang), f(tr.vel_offset)
+            getattr(self.L, f"orc_scene_add_track_{self.suf}")(self.h, C.c_int(len(st)), _p(st), _p(R), _p(t), _p(po),
+                                                            _p(vl), _p(va), _p(vo), C.c_int(int(tr.init_velocity_from_poses)))
+
+    def __del__(self):
+        try:
+            getattr(self.L, f"orc_scene_free_{self.suf}")(self.h)
+        except Exception:
+            pass
+
+    def zero_grads(self):
+        getattr(self.L, f"orc_scene_zero_grads_{self.suf}")(self.h)
+
+    def array(self, name):
+        fn = getattr(self.L, f"orc_scene_array_{self.suf}")
+        n = fn(self.h, name.encode(), None)
+        if n < 0:
+            raise KeyError(name)
+        dt = np.float64 if name.startswith("actor_") else self.dtype
+        out = np.empty(n, dt)
+        fn(self.h, name.encode(), _p(out))
+        return out
+
+    def grads(self):
+        g = {k: self.array(k) for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_color", "d_feature")}
+        g["d_mean"] = g["d_mean"].reshape(-1, 3)
+        g["d_scale_log"] = g["d_scale_log"].reshape(-1, 3)
+        g["d_quat"] = g["d_quat"].reshape(-1, 4)
+        g["d_color"] = g["d_color"].reshape(-1, 3)
+        g["d_feature"] = g["d_feature"].reshape(self.n, -1)
+        g["actors"] = [dict(d_pose_offset=self.array(f"actor_d_pose_offset:{a}").reshape(-1, 6),
+                            d_vel_offset=self.array(f"actor_d_vel_offset:{a}")) for a in range(len(self.tracks))]
+        return g
+
+    def actor_velocity(self, a):
+        v = self.array(f"actor_vel:{a}")
+        return v[:3], v[3:]
+
+    def render_camera(self, cam, settings, t_scene=0.0, workers=1, stop_after=0):
+        h = getattr(self.L, f"orc_view_camera_{self.suf}")(
+            self.h, C.c_double(t_scene), _p(cam.packed(self.dtype)), _p(settings.packed(self.dtype)), C.c_int(workers),
+            C.c_int(stop_after))
+        if not h:
+            raise RuntimeError(getattr(self.L, f"orc_scene_error_{self.suf}")(self.h).decode())
+        return OracleView(self, C.c_void_p(h), True, cam.width * cam.height)
+
+    def render_lidar(self, lidar, rayset, settings, t_scene=0.0, workers=1, stop_after=0):
+        rays = np.ascontiguousarray(rayset.rays, self.dtype)
+        rb = np.ascontiguousarray(rayset.begin, np.int64)
+        re = np.ascontiguousarray(rayset.end, np.int64)
+        elev = lidar.elev(self.dtype)
+        h = getattr(self.L, f"orc_view_lidar_{self.suf}")(
+            self.h, C.c_double(t_scene), _p(lidar.packed(self.dtype)), _p(elev), C.c_int(len(elev)),
+            _p(settings.packed(self.dtype)), _p(rays), C.c_int64(len(rays)), _p(rb), _p(re), C.c_int64(len(rb)),
+            C.c_int(workers), C.c_int(stop_after))
+        if not h:
+            raise RuntimeError(getattr(self.L, f"orc_scene_error_{self.suf}")(self.h).decode())
+        return OracleView(self, C.c_void_p(h), False, len(rays))
+
+
+class OracleView:
+    def __init__(self, scene, h, camera, P):
+        self.scene, self.h, self.camera, self.P = scene, h, camera, P
+        self.L, self.suf, self.dtype = scene.L, scene.suf, scene.dtype
+
+    def __del__(self):
+        try:
+            getattr(self.L, f"orc_view_free_{self.suf}")(self.h)
+        except Exception:
+            pass
+
+    def array(self, name):
+        fn = getattr(self.L, f"orc_view_array_{self.suf}")
+        n = fn(self.h, name.encode(), None)
+        if n < 0:
+            raise KeyError(name)
+        out = np.empty(n, np.int64 if name in INT_ARRAYS else self.dtype)
+        fn(self.h, name.encode(), _p(out))
+        return out
+
+    def backward(self, g_blend16, g_alpha, workers=1):
+        gb = np.ascontiguousarray(g_blend16, self.dtype)
+        ga = np.ascontiguousarray(g_alpha, self.dtype)
+        assert gb.size == 16 * self.P and ga.size == self.P
+        getattr(self.L, f"orc_view_backward_{self.suf}")(self.h, _p(gb), _p(ga), C.c_int(workers))
+
+    def brute_force(self, early_exit=True):
+        blend = np.empty((self.P, 16), self.dtype)
+        alpha = np.empty(self.P, self.dtype)
+        nc = np.empty(self.P, np.int64)
+        getattr(self.L, f"orc_view_brute_{self.suf}")(self.h, C.c_int(int(early_exit)), _p(blend), _p(alpha), _p(nc))
+        return blend, alpha, nc
+
+    def ms(self):
+        return self.array("ms").astype(np.float64)
+
+
+def detmath_eval(fn, x, y=None):
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.zeros_like(x) if y is None else np.ascontiguousarray(y, np.float32)
+    out = np.empty_like(x)
+    lib().orc_detmath_eval(C.c_int(fn), _p(x), _p(y), _p(out), C.c_int64(x.size))
+    return out
+
+
+def hardware_threads():
+    return int(lib().orc_hardware_threads())

@@ -1,0 +1,639 @@
+"""Pins the CPU oracle against SPEC.md's worked examples.
+
+The reference ships no tests or goldens; these known-answer cases are the only pins the
+reference itself provides for this path. CPU only.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle_py as op
+from paper_2411_16816_b200 import synth
+from paper_2411_16816_b200.model import CameraModel, LidarModel, RasterSettings, RaySet, Scene
+
+ST = RasterSettings()
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+@pytest.fixture(scope="module")
+def L(oracle_lib):
+    return oracle_lib
+
+
+def one_gaussian_scene(mean, scale_log=(0, 0, 0), quat=(1, 0, 0, 0), opacity_logit=20.0, color=(0.2, 0.5, 0.7), d_f=13):
+    f = np.arange(1, d_f + 1, dtype=np.float64)[None, :] / 10.0
+    return Scene(np.array([mean], np.float64), np.array([scale_log], np.float64), np.array([quat], np.float64),
+                 np.array([opacity_logit], np.float64), np.array([color], np.float64), f, np.zeros(1, np.int32))
+
+
+# ---- KA1: covariance_from_scale_quat ------------------------------------------
+def test_ka1_covariance(L):
+    out = np.zeros(9)
+    L.orc_covariance_from_scale_quat_f64(_p(np.zeros(3)), _p(np.array([1.0, 0, 0, 0])), _p(out))
+    assert np.allclose(out.reshape(3, 3), np.eye(3), atol=1e-15)
+    L.orc_covariance_from_scale_quat_f64(_p(np.array([np.log(2.0), 0, 0])), _p(np.array([1.0, 0, 0, 0])), _p(out))
+    assert np.allclose(out.reshape(3, 3), np.diag([4.0, 1, 1]), atol=1e-12)
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        sl, q = rng.normal(0, 0.7, 3), rng.normal(0, 1, 4)
+        L.orc_covariance_from_scale_quat_f64(_p(sl), _p(q), _p(out))
+        ev = np.sort(np.linalg.eigvalsh(out.reshape(3, 3)))
+        assert np.allclose(ev, np.sort(np.exp(sl) ** 2), rtol=1e-10)
+
+
+# ---- KA2: compose_at_time -----------------------------------------------------
+def test_ka2_compose_static_and_actor(L):
+    sc = synth.make_scene(100, seed=3)
+    o = op.OracleScene(sc, np.float64)
+    v = o.render_camera(synth.make_camera(64, 64), ST, t_scene=0.37, stop_after=1)
+    assert np.array_equal(v.array("mean_w").reshape(-1, 3), sc.mean.astype(np.float64))
+    assert np.all(v.array("vel_dyn_w") == 0)
+    # actor translating 1 m/s along x, Gaussian at box origin: t advanced 1 s => shift (1,0,0)
+    from paper_2411_16816_b200.model import ActorTrack
+    tr = ActorTrack(stamps=[0.0, 1.0], R=np.stack([np.eye(3)] * 2), t=np.array([[5.0, 0, 0], [6.0, 0, 0]]),
+                    init_velocity_from_poses=True)
+    s1 = one_gaussian_scene((0, 0, 0))
+    s1.actor_id[:] = 1
+    s1.tracks.append(tr)
+    o = op.OracleScene(s1, np.float64)
+    m0 = o.render_camera(synth.make_camera(64, 64), ST, t_scene=0.0, stop_after=1).array("mean_w")
+    m1 = o.render_camera(synth.make_camera(64, 64), ST, t_scene=1.0, stop_after=1).array("mean_w")
+    assert np.allclose(m1 - m0, [1, 0, 0], atol=1e-12)
+    # rotating at (0,0,pi/2) rad/s, Gaussian at actor-frame (1,0,0) => |v_dyn| = pi/2
+    a = np.pi / 2
+    Rz = lambda th: np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1.0]])
+    tr = ActorTrack(stamps=[0.0, 1.0], R=np.stack([Rz(0), Rz(a)]), t=np.zeros((2, 3)), init_velocity_from_poses=True)
+    s2 = one_gaussian_scene((1, 0, 0))
+    s2.actor_id[:] = 1
+    s2.tracks.append(tr)
+    o = op.OracleScene(s2, np.float64)
+    view = o.render_camera(synth.make_camera(64, 64), ST, t_scene=0.5, stop_after=1)
+    vd = view.array("vel_dyn_w")
+    assert abs(np.linalg.norm(vd) - np.pi / 2) < 1e-9
+    # v_dyn matches central finite differences of composed positions
+    dt = 1e-4
+    mp = o.render_camera(synth.make_camera(64, 64), ST, t_scene=0.5 + dt, stop_after=1).array("mean_w")
+    mm = o.render_camera(synth.make_camera(64, 64), ST, t_scene=0.5 - dt, stop_after=1).array("mean_w")
+    assert np.allclose((mp - mm) / (2 * dt), vd, atol=1e-5)
+
+
+def test_unknown_actor_is_hard_error(L):
+    s = one_gaussian_scene((0, 0, 5))
+    s.actor_id[:] = 3
+    o = op.OracleScene(s, np.float64)
+    with pytest.raises(RuntimeError, match="unknown actor_id 3"):
+        o.render_camera(synth.make_camera(64, 64), ST)
+
+
+# ---- KA3: camera projection -------------------------------------------------
+def test_ka3_camera_projection(L):
+    cam = CameraModel(fx=120.0, fy=120.0, cx=50.0, cy=40.0, width=100, height=80)
+    sig = 0.2
+    s = one_gaussian_scene((0, 0, 4.0), scale_log=(np.log(sig),) * 3)
+    v = op.OracleScene(s, np.float64).render_camera(cam, ST, stop_after=1)
+    assert np.allclose(v.array("mean2d"), [50.0, 40.0])
+    assert np.allclose(v.array("cov2d").reshape(2, 2), (120.0 * sig / 4.0) ** 2 * np.eye(2), rtol=1e-12)
+    # random Gaussian: cov2d == J Sigma J^T with J from central differences
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        mu = np.array([rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(3, 8)])
+        sl, q = rng.normal(-2, 0.3, 3), rng.normal(0, 1, 4)
+        s = one_gaussian_scene(mu, sl, q)
+        v = op.OracleScene(s, np.float64).render_camera(cam, ST, stop_after=1)
+        if len(v.array("source_index")) == 0:
+            continue
+        cov = np.zeros(9)
+        L.orc_covariance_from_scale_quat_f64(_p(sl), _p(q), _p(cov))
+        proj = lambda p: np.array([cam.fx * p[0] / p[2] + cam.cx, cam.fy * p[1] / p[2] + cam.cy])
+        h = 1e-6
+        J = np.stack([(proj(mu + h * e) - proj(mu - h * e)) / (2 * h) for e in np.eye(3)], 1)
+        assert np.allclose(v.array("cov2d").reshape(2, 2), J @ cov.reshape(3, 3) @ J.T, rtol=1e-6)
+
+
+# ---- KA4: lidar projection + Eq. 11 -----------------------------------------
+def test_ka4_spherical(L):
+    sph, J = np.zeros(3), np.zeros(9)
+    L.orc_spherical_f64(_p(np.array([1.0, 0, 0])), _p(sph), _p(J))
+    assert np.allclose(sph, [0, 0, 1])
+    assert np.allclose(J.reshape(3, 3), [[0, 1, 0], [0, 0, 1], [1, 0, 0]])
+    L.orc_spherical_f64(_p(np.array([1.0, 1.0, np.sqrt(2.0)])), _p(sph), _p(J))
+    assert np.allclose(sph, [np.pi / 4, np.pi / 4, 2.0])
+    rng = np.random.default_rng(2)
+
+    def f(p):
+        r = np.linalg.norm(p)
+        return np.array([np.arctan2(p[1], p[0]), np.arcsin(p[2] / r), r])
+    for _ in range(1000):
+        p = rng.normal(0, 5, 3)
+        if p[0] < 0.5:
+            p[0] = abs(p[0]) + 0.5     # stay away from the atan2 branch cut for the FD
+        L.orc_spherical_f64(_p(p), _p(sph), _p(J))
+        h = 1e-6
+        Jn = np.stack([(f(p + h * e) - f(p - h * e)) / (2 * h) for e in np.eye(3)], 1)
+        assert np.allclose(J.reshape(3, 3), Jn, rtol=1e-6, atol=1e-8)
+
+
+def test_spherical_jacobian_point_grad_fd(L):
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        p, gJ = rng.normal(0, 4, 3) + np.array([6.0, 0, 0]), rng.normal(0, 1, 9)
+        out, sph, J = np.zeros(3), np.zeros(3), np.zeros(9)
+        L.orc_spherical_jacobian_point_grad_f64(_p(p), _p(gJ), _p(out))
+        h = 1e-6
+        num = np.zeros(3)
+        for k, e in enumerate(np.eye(3)):
+            Jp, Jm = np.zeros(9), np.zeros(9)
+            L.orc_spherical_f64(_p(p + h * e), _p(sph), _p(Jp))
+            L.orc_spherical_f64(_p(p - h * e), _p(sph), _p(Jm))
+            num[k] = np.dot(gJ, (Jp - Jm) / (2 * h))
+        assert np.allclose(out, num, rtol=1e-5, atol=1e-8)
+
+
+# ---- KA5: velocities --------------------------------------------------------
+def test_ka5_pixel_velocity(L):
+    f, z = 100.0, 5.0
+    s = one_gaussian_scene((0, 0, z), scale_log=(-3,) * 3)
+    cam = CameraModel(fx=f, fy=f, cx=50, cy=50, width=100, height=100)
+    v = op.OracleScene(s, np.float64).render_camera(cam, ST, stop_after=1)
+    assert np.all(v.array("velocity") == 0)
+    cam.vel_lin = np.array([0, 0, 1.0])
+    v = op.OracleScene(s, np.float64).render_camera(cam, ST, stop_after=1)
+    assert np.allclose(v.array("velocity")[:2], 0)           # focus of expansion
+    cam.vel_lin, cam.vel_ang = np.zeros(3), np.array([0, 0.3, 0])
+    v = op.OracleScene(s, np.float64).render_camera(cam, ST, stop_after=1)
+    assert np.allclose(v.array("velocity")[:2], [-f * 0.3, 0])
+
+
+# ---- KA6: velocity-expanded AABB --------------------------------------------
+def test_ka6_aabb(L):
+    f, z = 100.0, 10.0
+    # Sigma^I = diag(4,1) <= sigma_c = (z/f) * (2, 1) px; dilation 0
+    s = one_gaussian_scene((0, 0, z), scale_log=(np.log(0.2), np.log(0.1), np.log(0.1)))
+    cam = CameraModel(fx=f, fy=f, cx=50, cy=50, width=100, height=100)
+    st0 = RasterSettings(dilation=0.0)
+    v = op.OracleScene(s, np.float64).render_camera(cam, st0, stop_after=1)
+    ab = v.array("aabb")
+    assert np.allclose([ab[2] - 50, ab[3] - 50], [6, 3])
+    cam.shutter_duration, cam.vel_ang = 0.1, np.array([0, -0.1, 0])   # v^I = (+10, 0) px/s
+    v = op.OracleScene(s, np.float64).render_camera(cam, st0, stop_after=1)
+    assert np.allclose(v.array("velocity")[:2], [10, 0])
+    assert np.allclose(v.array("aabb")[2] - 50, 6.5)
+    cam.shutter_duration = 0.0
+    v = op.OracleScene(s, np.float64).render_camera(cam, st0, stop_after=1)
+    assert np.allclose(v.array("aabb")[2] - 50, 6.0)
+
+
+# ---- KA7: image tiles -------------------------------------------------------
+def test_ka7_image_tile_range(L):
+    out = np.zeros(4, np.int32)
+    L.orc_image_tile_range_f64(_p(np.array([0.0, 0.0])), _p(np.array([15.9, 15.9])), 8, 8, _p(out))
+    assert list(out) == [0, 1, 0, 1]
+    L.orc_image_tile_range_f64(_p(np.array([15.5, 0.0])), _p(np.array([16.5, 1.0])), 8, 8, _p(out))
+    assert list(out) == [0, 2, 0, 1]
+    L.orc_image_tile_range_f64(_p(np.array([-40.0, -40.0])), _p(np.array([-20.0, -20.0])), 8, 8, _p(out))
+    assert (out[1] - out[0]) * (out[3] - out[2]) == 0
+
+
+# ---- KA8: azimuth tiles -----------------------------------------------------
+ELEV16 = np.deg2rad(np.linspace(-15, 15, 16))
+
+
+def test_ka8_azimuth_tiles(L):
+    sp, m2, b = np.zeros(2), np.zeros(2, np.int32), np.zeros(8)
+    L.orc_lidar_grid_f64(C.c_double(np.deg2rad(0.2)), _p(ELEV16), 16, _p(sp), _p(m2), _p(b))
+    assert m2[0] == 57 and m2[1] == 2
+    assert np.isclose(np.rad2deg(sp[0]), 6.4) and np.isclose(np.rad2deg(sp[1]), 364.8)
+    out = np.zeros(4, np.int32)
+    d = np.deg2rad
+    L.orc_lidar_tile_range_f64(C.c_double(d(0.2)), _p(ELEV16), 16, _p(np.array([d(1.0), 0.0])), _p(np.array([d(5.0), 0.0])), _p(out))
+    assert (out[0], out[1]) == (0, 1)
+    L.orc_lidar_tile_range_f64(C.c_double(d(0.2)), _p(ELEV16), 16, _p(np.array([d(-2.0), 0.0])), _p(np.array([d(2.0), 0.0])), _p(out))
+    assert (out[0], out[1]) == (-2, 1)
+    assert [(x + 57) % 57 for x in range(out[0], out[1])] == [55, 56, 0]
+
+
+def test_p2_azimuth_wrap_vs_dense_sampling(L):
+    """wrapped tile columns == dense sampling at res/4, 10k random AABBs."""
+    rng = np.random.default_rng(5)
+    res = np.deg2rad(0.2)
+    span, m_phi = 32 * res, 57
+    out = np.zeros(4, np.int32)
+    n_checked = 0
+    for _ in range(10000):
+        c = rng.uniform(0, 2 * np.pi)
+        half = rng.uniform(0.0005, 0.2) if rng.random() < 0.9 else rng.uniform(0.2, 1.5)
+        lo, hi = c - half, c + half
+        L.orc_lidar_tile_range_f64(C.c_double(res), _p(ELEV16), 16, _p(np.array([lo, 0.0])), _p(np.array([hi, 0.0])), _p(out))
+        got = {(x + m_phi) % m_phi for x in range(out[0], out[1])}
+        samples = np.arange(lo, hi, res / 4)
+        want = set((np.floor(np.mod(samples, 2 * np.pi) / span)).astype(int).tolist())
+        # the paper's formulas are conservative: they must cover every sampled column and may add the
+        # overlap column (phi_max > 360 deg) or one neighbour at an exact boundary
+        assert want <= got, (lo, hi, want, got)
+        assert len(got - want) <= 2
+        n_checked += 1
+    assert n_checked == 10000
+
+
+# ---- KA9: elevation rows ----------------------------------------------------
+def test_ka9_elevation_rows(L):
+    b = np.deg2rad(np.array([-15.0, -5.0, 0.0, 3.0, 6.0]))
+    out = np.zeros(2, np.int32)
+    L.orc_elevation_rows_f64(_p(b), 5, C.c_double(np.deg2rad(-6.0)), C.c_double(np.deg2rad(1.0)), _p(out))
+    assert (out[0], out[1]) == (1, 4)          # rows 1..3: the rows touching boundaries -5 and 0
+    L.orc_elevation_rows_f64(_p(b), 5, C.c_double(np.deg2rad(-4.0)), C.c_double(np.deg2rad(-1.0)), _p(out))
+    assert (out[0], out[1]) == (2, 3)          # strictly inside row 2
+    L.orc_elevation_rows_f64(_p(b), 5, C.c_double(np.deg2rad(-40.0)), C.c_double(np.deg2rad(40.0)), _p(out))
+    assert (out[0], out[1]) == (0, 6)
+
+
+# ---- KA10: sorted worklist --------------------------------------------------
+def test_ka10_worklist_matches_filter_then_sort(L):
+    sc = synth.make_scene(1000, seed=7, r_max=30)
+    cam = synth.make_camera(width=256, height=128)
+    for dt in (np.float32, np.float64):
+        v = op.OracleScene(sc, dt).render_camera(cam, ST, stop_after=2)
+        tiles, depth, src = v.array("isect_tile"), v.array("isect_depth_bits"), v.array("isect_src")
+        rect = v.array("rect").reshape(-1, 4)
+        sidx = v.array("source_index")
+        dk = v.array("depth_key")
+        assert len(tiles) == int(((rect[:, 1] - rect[:, 0]) * (rect[:, 3] - rect[:, 2])).sum())   # duplication exactness
+        tx, ty = v.array("grid")
+        tb, te = v.array("tile_begin"), v.array("tile_end")
+        for t in range(tx * ty):
+            x, y = t % tx, t // tx
+            inside = (rect[:, 0] <= x) & (x < rect[:, 1]) & (rect[:, 2] <= y) & (y < rect[:, 3])
+            want = sorted(zip(dk[inside].tolist(), sidx[inside].tolist()))
+            got = src[tb[t]:te[t]].tolist()
+            assert got == [w[1] for w in want]
+            assert np.all(tiles[tb[t]:te[t]] == t)
+
+
+# ---- KA12: pixel capture offset ---------------------------------------------
+def test_ka12_capture_offset(L):
+    f = L.orc_pixel_capture_offset_f64
+    assert f(50, 100, 0.1, 0.0) == 0.0
+    assert np.isclose(f(0, 100, 0.1, 0.0), -0.05)
+    assert np.isclose(f(99, 100, 0.1, 0.0), 0.049)
+    assert np.isclose(f(50, 100, 0.1, 0.002), 0.002)
+
+
+# ---- KA13: evaluate_alpha ---------------------------------------------------
+def _splat(mx, my, vx, vy, cov, s, rho_o):
+    d = cov + s * np.eye(2)
+    c = np.linalg.inv(d)
+    det_ratio = np.sqrt(np.linalg.det(cov) / np.linalg.det(d))
+    return np.array([mx, my, vx, vy, 0.0, c[0, 0], c[0, 1] + c[1, 0], c[1, 1], det_ratio * rho_o, 1.0])
+
+
+def test_ka13_alpha(L):
+    a = C.c_double(0)
+    sp = _splat(3.0, 4.0, 0, 0, np.eye(2), 0.3, 1.0)
+    assert L.orc_evaluate_alpha_f64(_p(sp), C.c_double(3.0), C.c_double(4.0), C.c_double(0.0), _p(ST.packed(np.float64)), 0, C.byref(a)) == 1
+    assert np.isclose(a.value, 10.0 / 13.0)
+    sp = _splat(3.0, 4.0, 0, 0, np.eye(2), 0.3, 0.5)
+    assert L.orc_evaluate_alpha_f64(_p(sp), C.c_double(13.0), C.c_double(4.0), C.c_double(0.0), _p(ST.packed(np.float64)), 0, C.byref(a)) == 0
+    sp = _splat(3.0, 4.0, 10.0, 0, np.eye(2), 0.3, 1.0)
+    assert L.orc_evaluate_alpha_f64(_p(sp), C.c_double(3.1), C.c_double(4.0), C.c_double(0.01), _p(ST.packed(np.float64)), 0, C.byref(a)) == 1
+    assert np.isclose(a.value, 10.0 / 13.0)
+    # lidar: azimuth difference wraps (common.hpp:41-46)
+    sp = _splat(0.001, 0.0, 0, 0, 1e-4 * np.eye(2), 1e-6, 1.0)
+    assert L.orc_evaluate_alpha_f64(_p(sp), C.c_double(2 * np.pi - 0.001), C.c_double(0.0), C.c_double(0.0), _p(ST.packed(np.float64)), 1, C.byref(a)) == 1
+    assert L.orc_evaluate_alpha_f64(_p(sp), C.c_double(2 * np.pi - 0.001), C.c_double(0.0), C.c_double(0.0), _p(ST.packed(np.float64)), 0, C.byref(a)) == 0
+
+
+# ---- KA14: camera rasterization ---------------------------------------------
+def test_ka14_camera_raster(L):
+    cam = CameraModel(fx=100.0, fy=100.0, cx=32.5, cy=32.5, width=64, height=64)
+    empty = Scene(*[np.zeros((0, k)) for k in (3, 3, 4)], np.zeros(0), np.zeros((0, 3)), np.zeros((0, 13)), np.zeros(0, np.int32))
+    v = op.OracleScene(empty, np.float64).render_camera(cam, ST)
+    assert np.all(v.array("blend") == 0) and np.all(v.array("alpha") == 0)
+    # one Gaussian centred on pixel (32,32)'s centre (32.5, 32.5)
+    z = 5.0
+    s = one_gaussian_scene((0.0, 0.0, z), scale_log=(np.log(0.05),) * 3, opacity_logit=1.0)
+    v = op.OracleScene(s, np.float64).render_camera(cam, ST)
+    cov = (100.0 * 0.05 / z) ** 2
+    a0 = np.sqrt(cov * cov / ((cov + 0.3) ** 2)) / (1 + np.exp(-1.0))
+    px = v.array("blend").reshape(64, 64, 16)[32, 32]
+    assert np.allclose(px[:3], a0 * np.array([0.2, 0.5, 0.7]), rtol=1e-9)
+    assert np.allclose(px[3:16], a0 * np.arange(1, 14) / 10.0, rtol=1e-9)
+    assert np.isclose(v.array("alpha").reshape(64, 64)[32, 32], a0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tiled_equals_brute_force_camera(L, seed):
+    """<=500 Gaussians, 64x64, max-abs <= 1e-5 in fast32 (here: identical op order => exact)."""
+    sc = synth.make_scene(500, seed=100 + seed, r_min=2.0, r_max=15.0, scale_mean=0.15)
+    cam = synth.make_camera(width=64, height=64, f=1000.0 * 1920 / 64 * 0.05)
+    for dt in (np.float32, np.float64):
+        v = op.OracleScene(sc, dt).render_camera(cam, ST)
+        assert v.array("n_contrib").sum() > 0
+        b, a, nc = v.brute_force()
+        assert np.abs(b - v.array("blend").reshape(-1, 16)).max() <= 1e-5
+        assert np.abs(a - v.array("alpha")).max() <= 1e-5
+        assert np.array_equal(nc, v.array("n_contrib"))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_tiled_equals_brute_force_lidar(L, seed):
+    sc = synth.make_scene(500, seed=200 + seed, r_min=2.0, r_max=12.0, scale_mean=0.25)
+    lid = synth.lidar32()
+    lid.vel_lin, lid.vel_ang = np.array([8.0, 1.0, 0.0]), np.array([0.0, 0.0, 0.4])
+    rays = synth.grid_rays(lid)
+    for dt in (np.float32, np.float64):
+        v = op.OracleScene(sc, dt).render_lidar(lid, rays, ST)
+        assert v.array("n_contrib").sum() > 0
+        b, a, nc = v.brute_force()
+        assert np.abs(b - v.array("blend").reshape(-1, 16)).max() <= 1e-5
+        assert np.array_equal(nc, v.array("n_contrib"))
+
+
+# ---- KA15: lidar rasterization ----------------------------------------------
+def _flat_lidar(n_beams=8, res=2 * np.pi / 64):
+    return LidarModel(elevation_channels=np.linspace(-0.2, 0.2, n_beams), azimuth_resolution=res, scan_duration=0.1,
+                      beam_divergence_h=3e-3, beam_divergence_v=3e-3)
+
+
+def _scene_from_rows(rows, d_f=13):
+    n = len(rows)
+    mean = np.array([r[0] for r in rows], np.float64)
+    sl = np.array([[np.log(r[1])] * 3 for r in rows])
+    q = np.tile([1.0, 0, 0, 0], (n, 1))
+    ol = np.array([r[2] for r in rows], np.float64)
+    return Scene(mean, sl, q, ol, np.full((n, 3), 0.5), np.ones((n, d_f)), np.zeros(n, np.int32))
+
+
+def test_ka15_lidar_median_expected(L):
+    lid = _flat_lidar()
+    rays = synth.grid_rays(lid)
+    # ray closest to azimuth of bin 0 centre and beam 4
+    phi, om = rays.rays[:, 0].astype(np.float64), rays.rays[:, 1].astype(np.float64)
+    k = int(np.argmin(np.abs(phi - phi.min()) + np.abs(om - np.sort(np.unique(om))[4])))
+    d = np.array([np.cos(om[k]) * np.cos(phi[k]), np.cos(om[k]) * np.sin(phi[k]), np.sin(om[k])])
+    logit = lambda p: np.log(p / (1 - p))
+    # big, so det_ratio ~ 1 and alpha ~ o at the centre: alphas .4 then .5
+    sc = _scene_from_rows([(5.0 * d, 0.5, logit(0.4)), (10.0 * d, 1.0, logit(0.5))])
+    lid_static = lid
+    v = op.OracleScene(sc, np.float64).render_lidar(lid_static, rays, ST)
+    px = v.array("blend").reshape(-1, 16)[k]
+    T = v.array("t_final")[k]
+    assert abs(T - 0.3) < 2e-3
+    assert px[14] == pytest.approx(10.0, abs=1e-9)     # median on the second surface
+    assert 5.0 < px[13] < 10.0                         # expected strictly between
+    assert v.array("n_contrib")[k] == 2
+    # one Gaussian crossing 0.5 alone => median = its r
+    sc = _scene_from_rows([(7.0 * d, 0.7, logit(0.8))])
+    v = op.OracleScene(sc, np.float64).render_lidar(lid_static, rays, ST)
+    assert v.array("blend").reshape(-1, 16)[k][14] == pytest.approx(7.0, abs=1e-9)
+    # rolling shutter on range: v_r = 2 m/s => r + 2 t_l
+    lid.vel_lin = -2.0 * d       # sensor receding => Gaussian relative radial velocity +2
+    v = op.OracleScene(sc, np.float64).render_lidar(lid, rays, ST)
+    t_l = float(rays.rays[k, 2])
+    assert v.array("blend").reshape(-1, 16)[k][14] == pytest.approx(7.0 + 2.0 * t_l, abs=1e-6)
+
+
+# ---- KA11 / P2: ray-to-tile mapping of the synthetic sweeps -----------------
+def test_ka11_grid_rays_fill_tiles_exactly():
+    for lid in (synth.lidar32(), synth.lidar128()):
+        rs = synth.grid_rays(lid)
+        m_phi, m_omega = lid.grid()
+        cnt = rs.end - rs.begin
+        assert len(cnt) == m_phi * m_omega and cnt.max() <= 256 and cnt.sum() == len(rs.rays)
+        span = 32 * float(np.float32(lid.azimuth_resolution))
+        col = np.floor(rs.rays[:, 0].astype(np.float64) / span).astype(int)
+        tile_of = np.repeat(np.arange(len(cnt)), cnt)
+        assert np.array_equal(tile_of % m_phi, col)
+        assert np.array_equal(tile_of // m_phi, rs.beam // 8)
+    assert np.all((synth.grid_rays(synth.lidar32()).end - synth.grid_rays(synth.lidar32()).begin) == 256)
+
+
+# ---- P1: yaw equivariance -------------------------------------------------------
+def test_p1_yaw_equivariance(L):
+    sc = synth.make_scene(300, seed=9, r_max=40)
+    a = 0.7
+    Rz = np.array([[np.cos(a), -np.sin(a), 0], [np.sin(a), np.cos(a), 0], [0, 0, 1.0]])
+    lid0 = synth.lidar128(yaw=0.0, moving=False)
+    lid0.t = np.zeros(3)
+    lid1 = synth.lidar128(yaw=0.0, moving=False)
+    lid1.t = np.zeros(3)
+    sc1 = Scene(sc.mean.astype(np.float64) @ Rz.T, sc.scale_log, sc.quat, sc.opacity_logit, sc.color, sc.feature, sc.actor_id)
+    # rotate the Gaussians' orientation too: q' = q_z(a) * q
+    qz = np.array([np.cos(a / 2), 0, 0, np.sin(a / 2)])
+    q = sc.quat.astype(np.float64)
+    w0, x0, y0, z0 = qz
+    sc1.quat = np.stack([w0 * q[:, 0] - z0 * q[:, 3], w0 * q[:, 1] - z0 * q[:, 2], w0 * q[:, 2] + z0 * q[:, 1],
+                         w0 * q[:, 3] + z0 * q[:, 0]], 1)
+    v0 = op.OracleScene(sc, np.float64).render_lidar(lid0, synth.grid_rays(lid0), ST, stop_after=1)
+    v1 = op.OracleScene(sc1, np.float64).render_lidar(lid1, synth.grid_rays(lid1), ST, stop_after=1)
+    assert np.array_equal(v0.array("source_index"), v1.array("source_index"))
+    m0, m1 = v0.array("mean2d").reshape(-1, 2), v1.array("mean2d").reshape(-1, 2)
+    assert np.allclose(np.mod(m0[:, 0] + a, 2 * np.pi), m1[:, 0], atol=1e-9)
+    assert np.allclose(m0[:, 1], m1[:, 1], atol=1e-9)
+    assert np.allclose(v0.array("depth_key"), v1.array("depth_key"), atol=1e-9)
+    e0 = np.linalg.eigvalsh(v0.array("cov2d").reshape(-1, 2, 2))
+    e1 = np.linalg.eigvalsh(v1.array("cov2d").reshape(-1, 2, 2))
+    assert np.allclose(e0, e1, rtol=1e-7, atol=1e-15)
+
+
+# ---- P3: rolling-shutter null test + transmittance / early-exit properties --
+def test_p3_rolling_shutter_null_and_early_exit(L):
+    sc = synth.make_scene(400, seed=11, r_min=2.0, r_max=15.0, scale_mean=0.15)
+    cam_rs = synth.make_camera(width=64, height=64, f=1500.0, moving=False, shutter=0.03)
+    cam_no = synth.make_camera(width=64, height=64, f=1500.0, moving=False, shutter=0.0)
+    o = op.OracleScene(sc, np.float64)
+    a, b = o.render_camera(cam_rs, ST), o.render_camera(cam_no, ST)
+    assert np.abs(a.array("blend") - b.array("blend")).max() <= 1e-7
+    st_off = RasterSettings(transmittance_min=0.0)
+    c = o.render_camera(cam_rs, st_off)
+    assert np.abs(a.array("blend") - c.array("blend")).max() <= 1e-3
+    assert np.all(a.array("alpha") >= 0) and np.all(a.array("alpha") <= 1)
+
+
+# ---- detmath: fp32 transcendentals are accurate and the bit patterns are stable ---------------
+def test_detmath_accuracy():
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-80, 80, 200000).astype(np.float32)
+    e = op.detmath_eval(0, x)
+    ref = np.exp(x.astype(np.float64))
+    assert np.max(np.abs(e - ref) / ref) < 3e-7
+    x = rng.uniform(-30, 30, 100000).astype(np.float32)
+    s = op.detmath_eval(1, x)
+    assert np.max(np.abs(s - 1 / (1 + np.exp(-x.astype(np.float64))))) < 2e-7
+    yy, xx = rng.normal(0, 10, 200000).astype(np.float32), rng.normal(0, 10, 200000).astype(np.float32)
+    at = op.detmath_eval(2, xx, yy)
+    assert np.max(np.abs(at - np.arctan2(yy.astype(np.float64), xx.astype(np.float64)))) < 6e-7
+    x = rng.uniform(-1, 1, 200000).astype(np.float32)
+    asn = op.detmath_eval(3, x)
+    assert np.max(np.abs(asn - np.arcsin(x.astype(np.float64)))) < 4e-7
+    assert op.detmath_eval(0, np.array([0.0], np.float32))[0] == 1.0
+    assert op.detmath_eval(2, np.array([-1.0], np.float32), np.array([0.0], np.float32))[0] == np.float32(np.pi)
+
+
+# ---- KA16: backward ---------------------------------------------------------
+def _loss_camera(sc, cam, gb, ga, t_scene=0.0):
+    v = op.OracleScene(sc, np.float64).render_camera(cam, ST, t_scene=t_scene)
+    return float((v.array("blend").reshape(-1, 16) * gb).sum() + (v.array("alpha") * ga).sum())
+
+
+def _loss_lidar(sc, lid, rays, gb, ga, t_scene=0.0):
+    v = op.OracleScene(sc, np.float64).render_lidar(lid, rays, ST, t_scene=t_scene)
+    b = v.array("blend").reshape(-1, 16)
+    return float((b[:, :14] * gb[:, :14]).sum() + (v.array("alpha") * ga).sum())
+
+
+def _fd_check(loss_fn, sc, grads, rng, n_probe=6, h=1e-6, tol=1e-3):
+    names = {"mean": "d_mean", "scale_log": "d_scale_log", "quat": "d_quat", "opacity_logit": "d_opacity_logit",
+             "color": "d_color", "feature": "d_feature"}
+    for field, gname in names.items():
+        arr = getattr(sc, field)
+        g = grads[gname].reshape(arr.shape)
+        scale = np.abs(g).max()
+        if scale == 0:
+            continue
+        flat = np.argsort(-np.abs(g).ravel())[:n_probe]
+        for idx in flat:
+            idx = np.unravel_index(idx, arr.shape)
+            old = arr[idx]
+            arr[idx] = old + h
+            lp = loss_fn(sc)
+            arr[idx] = old - h
+            lm = loss_fn(sc)
+            arr[idx] = old
+            num = (lp - lm) / (2 * h)
+            assert abs(num - g[idx]) <= tol * max(abs(num), 1e-3 * scale) + 1e-7, (field, idx, num, g[idx])
+
+
+def _f64_scene(sc):
+    return Scene(*[np.ascontiguousarray(a, np.float64) for a in (sc.mean, sc.scale_log, sc.quat, sc.opacity_logit, sc.color, sc.feature)],
+                 sc.actor_id, list(sc.tracks))
+
+
+def test_ka16_backward_camera_fd(L):
+    rng = np.random.default_rng(21)
+    sc = _f64_scene(synth.make_scene(10, seed=31, r_min=3.0, r_max=6.0, scale_mean=0.3))
+    sc.mean[:, 1] *= 0.15
+    sc.mean[:, 2] = rng.uniform(1.0, 2.0, 10)
+    cam = synth.make_camera(width=48, height=32, f=1000.0, moving=True, shutter=0.03)
+    gb, ga = rng.normal(0, 1, (48 * 32, 16)), rng.normal(0, 1, 48 * 32)
+    o = op.OracleScene(sc, np.float64)
+    v = o.render_camera(cam, ST)
+    assert v.array("n_contrib").sum() > 50
+    # zero upstream => zero grads
+    v.backward(np.zeros_like(gb), np.zeros_like(ga))
+    assert all(np.all(x == 0) for k, x in o.grads().items() if k != "actors")
+    o.zero_grads()
+    v.backward(gb, ga)
+    grads = o.grads()
+    _fd_check(lambda s: _loss_camera(s, cam, gb, ga), sc, grads, rng)
+    # sensor grads: velocities and the camera time offset
+    sg = v.array("sensor_grads")
+    h = 1e-6
+    for k in range(3):
+        for name, off in (("vel_lin", 0), ("vel_ang", 3)):
+            vec = getattr(cam, name)
+            old = vec[k]
+            vec[k] = old + h
+            lp = _loss_camera(sc, cam, gb, ga)
+            vec[k] = old - h
+            lm = _loss_camera(sc, cam, gb, ga)
+            vec[k] = old
+            num = (lp - lm) / (2 * h)
+            assert abs(num - sg[off + k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(sg[:6]).max()) + 1e-7, (name, k, num, sg[off + k])
+    old = cam.time_offset
+    cam.time_offset = old + h
+    lp = _loss_camera(sc, cam, gb, ga)
+    cam.time_offset = old - h
+    lm = _loss_camera(sc, cam, gb, ga)
+    cam.time_offset = old
+    assert abs((lp - lm) / (2 * h) - sg[6]) <= 1e-3 * abs(sg[6]) + 1e-6
+
+
+def test_ka16_backward_lidar_fd(L):
+    rng = np.random.default_rng(22)
+    sc = _f64_scene(synth.make_scene(10, seed=32, r_min=3.0, r_max=6.0, scale_mean=0.3))
+    sc.mean[:, 2] = rng.uniform(-0.5, 1.0, 10)
+    lid = _flat_lidar(n_beams=16, res=2 * np.pi / 128)
+    lid.vel_lin, lid.vel_ang = np.array([5.0, 1.0, 0.2]), np.array([0.0, 0.05, 0.3])
+    rays = synth.grid_rays(lid)
+    P = len(rays.rays)
+    gb, ga = rng.normal(0, 1, (P, 16)), rng.normal(0, 1, P)
+    gb[:, 14:] = 0
+    o = op.OracleScene(sc, np.float64)
+    v = o.render_lidar(lid, rays, ST)
+    assert v.array("n_contrib").sum() > 50
+    v.backward(gb, ga)
+    grads = o.grads()
+    _fd_check(lambda s: _loss_lidar(s, lid, rays, gb, ga), sc, grads, rng)
+    sg = v.array("sensor_grads")
+    h = 1e-6
+    for k in range(3):
+        for name, off in (("vel_lin", 0), ("vel_ang", 3)):
+            vec = getattr(lid, name)
+            old = vec[k]
+            vec[k] = old + h
+            lp = _loss_lidar(sc, lid, rays, gb, ga)
+            vec[k] = old - h
+            lm = _loss_lidar(sc, lid, rays, gb, ga)
+            vec[k] = old
+            num = (lp - lm) / (2 * h)
+            assert abs(num - sg[off + k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(sg[:6]).max()) + 1e-7, (name, k, num, sg[off + k])
+
+
+def test_ka16_expected_range_monotone(L):
+    """d(expected range)/d(range-direction mean) > 0 for a single contributor."""
+    lid = _flat_lidar()
+    rays = synth.grid_rays(lid)
+    k = 100
+    phi, om = float(rays.rays[k, 0]), float(rays.rays[k, 1])
+    d = np.array([np.cos(om) * np.cos(phi), np.cos(om) * np.sin(phi), np.sin(om)])
+    sc = _scene_from_rows([(6.0 * d, 0.6, 0.0)])
+    o = op.OracleScene(sc, np.float64)
+    v = o.render_lidar(lid, rays, ST)
+    gb = np.zeros((len(rays.rays), 16))
+    gb[k, 13] = 1.0
+    v.backward(gb, np.zeros(len(rays.rays)))
+    assert float(o.grads()["d_mean"][0] @ d) > 0
+
+
+def test_backward_dynamic_actor_fd(L):
+    """Actor pose / velocity offset gradients (scene.hpp:420-453) against finite differences."""
+    rng = np.random.default_rng(23)
+    sc = _f64_scene(synth.make_scene(40, seed=33, n_actors=1, dynamic_fraction=0.5, r_min=3.0, r_max=6.0, scale_mean=0.2))
+    tr = sc.tracks[0]
+    # put the actor in front of the camera
+    tr.t[:] = np.array([[5.0, -0.3, 1.2], [5.2, 0.0, 1.3], [5.4, 0.3, 1.4]])
+    cam = synth.make_camera(width=48, height=32, f=300.0, moving=True, shutter=0.03)
+    gb, ga = rng.normal(0, 1, (48 * 32, 16)), rng.normal(0, 1, 48 * 32)
+    t_scene = 0.04
+    o = op.OracleScene(sc, np.float64)
+    v = o.render_camera(cam, ST, t_scene=t_scene)
+    dyn_visible = np.isin(v.array("source_index"), np.nonzero(sc.actor_id)[0]).sum()
+    assert dyn_visible > 3
+    v.backward(gb, ga)
+    g = o.grads()
+    _fd_check(lambda s: _loss_camera(s, cam, gb, ga, t_scene), sc, g, rng, n_probe=3)
+    h = 1e-6
+    ga_pose, ga_vel = g["actors"][0]["d_pose_offset"], g["actors"][0]["d_vel_offset"]
+    assert np.abs(ga_pose).max() > 0 and np.abs(ga_vel).max() > 0
+    for (i, k) in [(1, 0), (1, 2), (2, 1), (1, 3), (1, 5), (2, 4), (0, 0), (0, 4)]:
+        old = tr.pose_offset[i, k]
+        tr.pose_offset[i, k] = old + h
+        lp = _loss_camera(sc, cam, gb, ga, t_scene)
+        tr.pose_offset[i, k] = old - h
+        lm = _loss_camera(sc, cam, gb, ga, t_scene)
+        tr.pose_offset[i, k] = old
+        num = (lp - lm) / (2 * h)
+        assert abs(num - ga_pose[i, k]) <= 2e-3 * max(abs(num), 1e-3 * np.abs(ga_pose).max()) + 1e-6, (i, k, num, ga_pose[i, k])
+    for k in range(6):
+        old = tr.vel_offset[k]
+        tr.vel_offset[k] = old + h
+        lp = _loss_camera(sc, cam, gb, ga, t_scene)
+        tr.vel_offset[k] = old - h
+        lm = _loss_camera(sc, cam, gb, ga, t_scene)
+        tr.vel_offset[k] = old
+        num = (lp - lm) / (2 * h)
+        assert abs(num - ga_vel[k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(ga_vel).max()) + 1e-6, (k, num, ga_vel[k])
