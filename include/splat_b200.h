@@ -1,0 +1,190 @@
+/* splat_b200.h — C ABI of libsplat_b200.so: the B200 (sm_100a) implementation of SplatAD's
+ * differentiable camera + lidar Gaussian rasterizer hot path
+ *     compose -> project -> tile-bin + sort -> composite   and the reverse.
+ *
+ * Plain pointers and sizes only; no C++/torch types. Every entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj/include/splat/, or SPEC.md for the
+ * two modules the reference only specifies). INTEGRATION.md shows the reference-side binding.
+ *
+ * Conventions
+ *  - All per-Gaussian arrays use the reference's physical layout (Eigen column-major kxN ==
+ *    N rows of k contiguous floats): mean/scale_log/color 3 floats, quat 4 floats (w,x,y,z),
+ *    feature d_f floats per Gaussian (scene.hpp:11-19).
+ *  - Rotation matrices are 9 floats ROW-major.
+ *  - Every call returns 0 on success or a negative SPLATB200_E* code; splatb200_last_error()
+ *    gives the message. Errors the reference raises as C++ exceptions keep their text
+ *    ("unknown actor_id 7" scene.hpp:176-177,297-298; "actor track has no poses" scene.hpp:242).
+ *  - A ctx is bound to one device and one stream; calls on a ctx are stream-ordered and not
+ *    thread-safe. Different ctxs are independent.
+ *  - There is no CPU fallback: without a CUDA device ctx_create fails.
+ */
+#ifndef SPLAT_B200_H_
+#define SPLAT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPLATB200_OK 0
+#define SPLATB200_EINVAL -1      /* bad argument */
+#define SPLATB200_ECUDA -2       /* CUDA runtime error */
+#define SPLATB200_EOUTOFRANGE -3 /* std::out_of_range in the reference (unknown actor_id) */
+#define SPLATB200_ERUNTIME -4    /* std::runtime_error in the reference (empty track, backward without forward) */
+#define SPLATB200_ENOMEM -5
+
+#define SPLATB200_MAX_CHANNELS 16 /* 3 colour + D_f <= 13 features */
+#define SPLATB200_TILE 16
+#define SPLATB200_NPHI 32
+#define SPLATB200_NOMEGA 8
+
+typedef struct splatb200_ctx splatb200_ctx;
+typedef struct splatb200_view splatb200_view;
+
+/* projection.hpp:7-15 RasterSettings<float> */
+typedef struct {
+  float dilation, alpha_clamp, alpha_min, qform_max, transmittance_min, near_plane, lidar_min_range;
+} splatb200_raster_settings;
+
+/* scene.hpp:98-137 CameraModel<float> (embedding belongs to the decoder: out of scope) */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float R[9], t[3];          /* pose: world -> sensor */
+  float vel_lin[3], vel_ang[3];
+  float shutter_duration, time_offset, timestamp;
+} splatb200_camera;
+
+/* scene.hpp:139-168 LidarModel<float> */
+typedef struct {
+  const float* elevation_channels; /* host pointer, n_beams strictly increasing radians */
+  int32_t n_beams;
+  float azimuth_resolution, scan_duration, beam_divergence_h, beam_divergence_v;
+  float R[9], t[3];
+  float vel_lin[3], vel_ang[3];
+  float timestamp, max_range;
+} splatb200_lidar;
+
+/* scene.hpp:50-96 ActorTrack<double>: actor poses are per-actor host work and stay in double */
+typedef struct {
+  int32_t n_poses;
+  const double* stamps;      /* n_poses, strictly increasing */
+  const double* R;           /* n_poses x 9 row-major, actor -> world */
+  const double* t;           /* n_poses x 3 */
+  const double* pose_offset; /* n_poses x 6: translation (world) 0-2, rotvec (actor frame) 3-5 */
+  double vel_lin[3], vel_ang[3];
+  double vel_offset[6];
+  int32_t init_velocity_from_poses; /* non-zero: ignore vel_lin/vel_ang, use scene.hpp:70-83 */
+} splatb200_actor_track;
+
+/* projection.hpp:207-222 SensorGrads<float> (d_embedding: decoder, out of scope) */
+typedef struct {
+  float d_vel_lin[3], d_vel_ang[3], d_time_offset;
+} splatb200_sensor_grads;
+
+/* counts of one forward pass */
+typedef struct {
+  int64_t n_gaussians;     /* N */
+  int64_t n_visible;       /* V: |project_*()| */
+  int64_t n_intersections; /* I: duplicated (Gaussian, tile) pairs */
+  int64_t n_queries;       /* P: pixels or rays */
+  int32_t tiles_x, tiles_y;
+} splatb200_view_stats;
+
+/* ---- context ------------------------------------------------------------------------------- */
+int splatb200_ctx_create(int device, void* cuda_stream /* cudaStream_t or NULL */, splatb200_ctx** out);
+void splatb200_ctx_destroy(splatb200_ctx* ctx);
+const char* splatb200_last_error(const splatb200_ctx* ctx); /* ctx may be NULL: last create error */
+int splatb200_ctx_sync(splatb200_ctx* ctx);
+/* number of kernels launched by this ctx since creation (bench.py's gpu_launches) */
+int64_t splatb200_ctx_launch_count(const splatb200_ctx* ctx);
+
+/* ---- scene: GaussianSet + SceneGraph (scene.hpp:11-45, 171-187) ------------------------------ */
+/* host arrays are copied to the device; actor_id is validated lazily against the tracks at
+ * compose time exactly like scene.hpp:297-298 */
+int splatb200_scene_upload(splatb200_ctx* ctx, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
+                           const float* quat, const float* opacity_logit, const float* color, const float* feature,
+                           const int32_t* actor_id);
+/* zero-copy variant: DEVICE pointers owned by the caller (e.g. optimiser state); must outlive use */
+int splatb200_scene_bind_device(splatb200_ctx* ctx, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
+                                const float* quat, const float* opacity_logit, const float* color,
+                                const float* feature, const int32_t* actor_id, int32_t max_actor_id);
+/* SceneGraph::tracks; actor k (1-based) = tracks[k-1] */
+int splatb200_scene_set_tracks(splatb200_ctx* ctx, int32_t n_tracks, const splatb200_actor_track* tracks);
+/* ActorTrack::init_velocity_from_poses result / stored velocities (lin 3, ang 3; without vel_offset) */
+int splatb200_scene_actor_velocity(splatb200_ctx* ctx, int32_t track, double out6[6]);
+
+/* ---- SceneParamGrads (scene.hpp:325-363) ----------------------------------------------------- */
+/* one contiguous device buffer of 27*N floats (d_f = 13):
+ *   [d_mean 3N | d_scale_log 3N | d_quat 4N | d_opacity_logit N | d_color 3N | d_feature d_f*N]
+ * backward ACCUMULATES (+=) like the reference (scene.hpp:394-456); zero explicitly. */
+int splatb200_grads_zero(splatb200_ctx* ctx);
+int64_t splatb200_grads_size(const splatb200_ctx* ctx);            /* number of floats */
+float* splatb200_grads_device_ptr(splatb200_ctx* ctx);             /* for ncclAllReduce */
+int splatb200_grads_bind_device(splatb200_ctx* ctx, float* dev, int64_t n_floats); /* caller-owned buffer */
+int splatb200_grads_download(splatb200_ctx* ctx, float* d_mean, float* d_scale_log, float* d_quat,
+                             float* d_opacity_logit, float* d_color, float* d_feature);
+/* SceneParamGrads::ActorGrad: d_pose_offset (n_poses x 6) and d_vel_offset (6), double */
+int splatb200_grads_download_actor(splatb200_ctx* ctx, int32_t track, double* d_pose_offset, double* d_vel_offset6);
+
+/* ---- views: one sensor render ---------------------------------------------------------------- */
+int splatb200_view_create_camera(splatb200_ctx* ctx, const splatb200_camera* cam,
+                                 const splatb200_raster_settings* settings, splatb200_view** out);
+/* rays: n_rays x 3 floats (azimuth in [0,2pi), elevation, capture-time offset t_l), grouped per
+ * tile: tile t owns rays [ray_begin[t], ray_end[t]) (SPEC.md:230-238 assign_points_to_tiles
+ * output); n_tiles must equal M_phi*M_omega. Host pointers, copied. */
+int splatb200_view_create_lidar(splatb200_ctx* ctx, const splatb200_lidar* lidar,
+                                const splatb200_raster_settings* settings, const float* rays, int64_t n_rays,
+                                const int64_t* ray_begin, const int64_t* ray_end, int64_t n_tiles,
+                                splatb200_view** out);
+void splatb200_view_destroy(splatb200_view* v);
+/* update sensor pose / velocities / time offset between frames without re-creating buffers */
+int splatb200_view_set_camera(splatb200_view* v, const splatb200_camera* cam);
+int splatb200_view_set_lidar_pose(splatb200_view* v, const float R[9], const float t[3], const float vel_lin[3],
+                                  const float vel_ang[3]);
+/* lidar tile grid: M_phi, M_omega */
+int splatb200_lidar_grid(const splatb200_lidar* lidar, int32_t* m_phi, int32_t* m_omega);
+
+/* compose_at_time (scene.hpp:273-308) + project_camera / project_lidar (projection.hpp:88-118,
+ * 140-174) + image/lidar tile ranges and build_sorted_worklist +
+ * rasterize_camera / rasterize_lidar, stream-ordered.
+ * stop_after: 0 = everything, 1 = after projection, 2 = after tiling/sort. */
+int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t stop_after);
+int splatb200_view_stats_get(splatb200_view* v, splatb200_view_stats* out); /* syncs */
+
+/* Rendered outputs, DEVICE pointers valid until the next forward on this view.
+ *   blend:  P x 16 floats, query-major (ChannelImage physical layout, common.hpp:104-116):
+ *           camera: rgb(3) + feature(13); lidar: feature(13), [13] expected range, [14] median range,
+ *           [15] accumulated opacity
+ *   alpha:  P accumulated opacity (1 - T)
+ *   n_contrib: P int32 number of blended Gaussians */
+const float* splatb200_view_blend(splatb200_view* v);
+const float* splatb200_view_alpha(splatb200_view* v);
+const int32_t* splatb200_view_n_contrib(splatb200_view* v);
+
+/* rasterizer backward + project_*_backward (projection.hpp:250-288, 322-357) +
+ * compose_backward (scene.hpp:386-458). g_blend16: P x 16, g_alpha: P (DEVICE pointers).
+ * Lidar: slots 14 (median) and 15 carry no gradient; the accumulated-opacity gradient is g_alpha.
+ * Accumulates into the ctx's SceneParamGrads and this view's SensorGrads. */
+int splatb200_view_backward(splatb200_view* v, const float* g_blend16, const float* g_alpha);
+int splatb200_view_sensor_grads(splatb200_view* v, splatb200_sensor_grads* out); /* syncs */
+
+/* Host-buffer convenience (the end-to-end path): upstream grads come from HOST memory, outputs go
+ * to HOST memory; copies are issued on the ctx stream. Any pointer may be NULL to skip it. */
+int splatb200_view_download(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib);
+int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, const float* g_alpha);
+
+/* Introspection for parity tests: copy a named intermediate to host. Returns the element count
+ * (call with dst = NULL to size), or a negative error. int64 arrays: source_index, rect (x0,x1,y0,y1
+ * per visible Gaussian, un-wrapped), isect_tile, isect_depth_bits, isect_src, tile_begin, tile_end,
+ * n_contrib, last_idx. float arrays: mean2d(2), depth_key, cov2d(4), velocity(3), aabb(4), conic(4),
+ * det_ratio, mu_sensor(3), rel_vel_sensor(3), blend(16), alpha, t_final, range_blend — projected
+ * fields are compacted in ascending source_index like the reference's std::vector<ProjectedGaussian>
+ * (projection.hpp:115,171). */
+int64_t splatb200_view_array(splatb200_view* v, const char* name, void* dst);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLAT_B200_H_ */

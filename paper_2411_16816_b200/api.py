@@ -1,0 +1,365 @@
+"""Host-side mirror of the reference's operator interface for the hot path, over the C ABI of
+libsplat_b200.so (include/splat_b200.h). ctypes only: no torch, no numpy math on the data path.
+
+Reference names (under /root/reference/proj/include/splat/):
+  compose_at_time      scene.hpp:273-308      project_camera / project_lidar  projection.hpp:88-118 / 140-174
+  compose_backward     scene.hpp:386-458      project_*_backward              projection.hpp:250-288 / 322-357
+  rasterize_camera / rasterize_lidar / backward
+There is NO CPU fallback: importing works anywhere (so that the symbol table can be checked on a CPU
+box), but creating a Context without a CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .model import CameraModel, LidarModel, RasterSettings, RaySet, Scene
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsplat_b200.so")
+_LIB = None
+
+INT_ARRAYS = {"source_index", "rect", "isect_tile", "isect_depth_bits", "isect_src", "tile_begin", "tile_end",
+              "grid", "n_contrib", "last_idx"}
+
+# every symbol include/splat_b200.h declares
+SYMBOLS = [
+    "splatb200_ctx_create", "splatb200_ctx_destroy", "splatb200_last_error", "splatb200_ctx_sync",
+    "splatb200_ctx_launch_count", "splatb200_scene_upload", "splatb200_scene_bind_device",
+    "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
+    "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
+    "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_lidar_grid",
+    "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
+    "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
+    "splatb200_view_backward_host", "splatb200_view_array",
+]
+
+
+class SplatError(RuntimeError):
+    pass
+
+
+class SettingsPOD(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("dilation", "alpha_clamp", "alpha_min", "qform_max", "transmittance_min",
+                                         "near_plane", "lidar_min_range")]
+
+
+class CameraPOD(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32),
+                ("height", C.c_int32), ("R", C.c_float * 9), ("t", C.c_float * 3), ("vel_lin", C.c_float * 3),
+                ("vel_ang", C.c_float * 3), ("shutter_duration", C.c_float), ("time_offset", C.c_float),
+                ("timestamp", C.c_float)]
+
+
+class LidarPOD(C.Structure):
+    _fields_ = [("elevation_channels", C.POINTER(C.c_float)), ("n_beams", C.c_int32), ("azimuth_resolution", C.c_float),
+                ("scan_duration", C.c_float), ("beam_divergence_h", C.c_float), ("beam_divergence_v", C.c_float),
+                ("R", C.c_float * 9), ("t", C.c_float * 3), ("vel_lin", C.c_float * 3), ("vel_ang", C.c_float * 3),
+                ("timestamp", C.c_float), ("max_range", C.c_float)]
+
+
+class TrackPOD(C.Structure):
+    _fields_ = [("n_poses", C.c_int32), ("stamps", C.POINTER(C.c_double)), ("R", C.POINTER(C.c_double)),
+                ("t", C.POINTER(C.c_double)), ("pose_offset", C.POINTER(C.c_double)), ("vel_lin", C.c_double * 3),
+                ("vel_ang", C.c_double * 3), ("vel_offset", C.c_double * 6), ("init_velocity_from_poses", C.c_int32)]
+
+
+class SensorGradsPOD(C.Structure):
+    _fields_ = [("d_vel_lin", C.c_float * 3), ("d_vel_ang", C.c_float * 3), ("d_time_offset", C.c_float)]
+
+
+class StatsPOD(C.Structure):
+    _fields_ = [("n_gaussians", C.c_int64), ("n_visible", C.c_int64), ("n_intersections", C.c_int64),
+                ("n_queries", C.c_int64), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32)]
+
+
+def lib():
+    """Load libsplat_b200.so. Raises if it has not been built: the product path never falls back."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise SplatError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                             "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.splatb200_last_error.restype = C.c_char_p
+        L.splatb200_last_error.argtypes = [C.c_void_p]
+        for n in ("splatb200_ctx_launch_count", "splatb200_grads_size", "splatb200_view_array"):
+            getattr(L, n).restype = C.c_int64
+        for n in ("splatb200_grads_device_ptr", "splatb200_view_blend", "splatb200_view_alpha", "splatb200_view_n_contrib"):
+            getattr(L, n).restype = C.c_void_p
+        L.splatb200_ctx_destroy.restype = None
+        L.splatb200_view_destroy.restype = None
+        L.splatb200_ctx_launch_count.argtypes = [C.c_void_p]
+        L.splatb200_grads_size.argtypes = [C.c_void_p]
+        L.splatb200_grads_device_ptr.argtypes = [C.c_void_p]
+        L.splatb200_ctx_destroy.argtypes = [C.c_void_p]
+        L.splatb200_view_destroy.argtypes = [C.c_void_p]
+        L.splatb200_ctx_sync.argtypes = [C.c_void_p]
+        L.splatb200_grads_zero.argtypes = [C.c_void_p]
+        for n in ("splatb200_view_blend", "splatb200_view_alpha", "splatb200_view_n_contrib"):
+            getattr(L, n).argtypes = [C.c_void_p]
+        L.splatb200_view_array.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        L.splatb200_view_forward.argtypes = [C.c_void_p, C.c_float, C.c_int32]
+        L.splatb200_view_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_view_backward_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_view_download.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_view_stats_get.argtypes = [C.c_void_p, C.c_void_p]
+        L.splatb200_view_sensor_grads.argtypes = [C.c_void_p, C.c_void_p]
+        L.splatb200_view_set_camera.argtypes = [C.c_void_p, C.c_void_p]
+        L.splatb200_view_set_lidar_pose.argtypes = [C.c_void_p] + [C.c_void_p] * 4
+        L.splatb200_grads_bind_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.splatb200_grads_download.argtypes = [C.c_void_p] * 7
+        L.splatb200_grads_download_actor.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        L.splatb200_scene_actor_velocity.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.splatb200_scene_upload.argtypes = [C.c_void_p, C.c_int64, C.c_int32] + [C.c_void_p] * 7
+        L.splatb200_scene_bind_device.argtypes = [C.c_void_p, C.c_int64, C.c_int32] + [C.c_void_p] * 7 + [C.c_int32]
+        L.splatb200_scene_set_tracks.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.splatb200_view_create_camera.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_view_create_lidar.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                                  C.c_void_p, C.c_int64, C.c_void_p]
+        L.splatb200_ctx_create.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
+        L.splatb200_lidar_grid.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        _LIB = L
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, np.float32)
+
+
+def _settings_pod(st: RasterSettings) -> SettingsPOD:
+    return SettingsPOD(*[np.float32(getattr(st, n)) for n, _ in SettingsPOD._fields_])
+
+
+def _fill3(dst, src, n):
+    for k, x in enumerate(np.asarray(src, np.float64).reshape(n).astype(np.float32)):
+        dst[k] = x
+
+
+def _camera_pod(cam: CameraModel) -> CameraPOD:
+    p = CameraPOD(fx=np.float32(cam.fx), fy=np.float32(cam.fy), cx=np.float32(cam.cx), cy=np.float32(cam.cy),
+                  width=cam.width, height=cam.height, shutter_duration=np.float32(cam.shutter_duration),
+                  time_offset=np.float32(cam.time_offset), timestamp=np.float32(cam.timestamp))
+    _fill3(p.R, cam.R, 9); _fill3(p.t, cam.t, 3); _fill3(p.vel_lin, cam.vel_lin, 3); _fill3(p.vel_ang, cam.vel_ang, 3)
+    return p
+
+
+def _lidar_pod(lid: LidarModel):
+    elev = _f32(lid.elevation_channels)
+    p = LidarPOD(elevation_channels=elev.ctypes.data_as(C.POINTER(C.c_float)), n_beams=len(elev),
+                 azimuth_resolution=np.float32(lid.azimuth_resolution), scan_duration=np.float32(lid.scan_duration),
+                 beam_divergence_h=np.float32(lid.beam_divergence_h), beam_divergence_v=np.float32(lid.beam_divergence_v),
+                 timestamp=np.float32(lid.timestamp), max_range=np.float32(lid.max_range))
+    _fill3(p.R, lid.R, 9); _fill3(p.t, lid.t, 3); _fill3(p.vel_lin, lid.vel_lin, 3); _fill3(p.vel_ang, lid.vel_ang, 3)
+    return p, elev
+
+
+class Context:
+    """One (GPU, stream): owns the device copy of a SceneGraph and its SceneParamGrads."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.L = lib()
+        h = C.c_void_p()
+        rc = self.L.splatb200_ctx_create(C.c_int(device), C.c_void_p(stream), C.byref(h))
+        if rc != 0:
+            raise SplatError(f"splatb200_ctx_create failed ({rc}): {self.L.splatb200_last_error(None).decode()}")
+        self.h = h
+        self.n = 0
+        self.d_f = 0
+        self.n_tracks = 0
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.splatb200_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc < 0:
+            msg = self.L.splatb200_last_error(self.h).decode()
+            if rc == -3:
+                raise IndexError(msg)          # std::out_of_range in the reference
+            raise SplatError(f"[{rc}] {msg}")
+        return rc
+
+    def sync(self):
+        self._check(self.L.splatb200_ctx_sync(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.L.splatb200_ctx_launch_count(self.h))
+
+    # ---- SceneGraph ---------------------------------------------------------------------------
+    def upload_scene(self, scene: Scene):
+        s = scene.astype(np.float32)
+        self.n, self.d_f = s.n, s.d_f
+        self._check(self.L.splatb200_scene_upload(self.h, s.n, s.d_f, _p(s.mean), _p(s.scale_log), _p(s.quat),
+                                                  _p(s.opacity_logit), _p(s.color), _p(s.feature), _p(s.actor_id)))
+        self.set_tracks(scene.tracks)
+
+    def bind_scene_device(self, n, d_f, mean, scale_log, quat, opacity_logit, color, feature, actor_id, max_actor_id=0):
+        """Zero-copy: arguments are raw device addresses (e.g. torch.Tensor.data_ptr())."""
+        self.n, self.d_f = int(n), int(d_f)
+        self._check(self.L.splatb200_scene_bind_device(self.h, n, d_f, mean, scale_log, quat, opacity_logit, color,
+                                                       feature, actor_id, max_actor_id))
+
+    def set_tracks(self, tracks):
+        arr = (TrackPOD * max(1, len(tracks)))()
+        keep = []
+        for k, tr in enumerate(tracks):
+            f = lambda a: np.ascontiguousarray(a, np.float64)
+            st, R, t, po = f(tr.stamps), f(tr.R), f(tr.t), f(tr.pose_offset)
+            keep += [st, R, t, po]
+            dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+            arr[k].n_poses = len(st)
+            arr[k].stamps, arr[k].R, arr[k].t, arr[k].pose_offset = dp(st), dp(R), dp(t), dp(po)
+            for j in range(3):
+                arr[k].vel_lin[j] = float(tr.vel_lin[j]); arr[k].vel_ang[j] = float(tr.vel_ang[j])
+            for j in range(6):
+                arr[k].vel_offset[j] = float(tr.vel_offset[j])
+            arr[k].init_velocity_from_poses = int(tr.init_velocity_from_poses)
+        self._check(self.L.splatb200_scene_set_tracks(self.h, len(tracks), C.byref(arr)))
+        self.n_tracks = len(tracks)
+        self.track_poses = [len(tr.stamps) for tr in tracks]
+
+    def actor_velocity(self, a):
+        out = np.zeros(6)
+        self._check(self.L.splatb200_scene_actor_velocity(self.h, a, _p(out)))
+        return out[:3], out[3:]
+
+    # ---- SceneParamGrads ----------------------------------------------------------------------
+    def zero_grads(self):
+        self._check(self.L.splatb200_grads_zero(self.h))
+
+    @property
+    def grads_size(self) -> int:
+        return int(self.L.splatb200_grads_size(self.h))
+
+    @property
+    def grads_device_ptr(self) -> int:
+        return int(self.L.splatb200_grads_device_ptr(self.h) or 0)
+
+    def bind_grads_device(self, ptr: int, n_floats: int):
+        self._check(self.L.splatb200_grads_bind_device(self.h, C.c_void_p(ptr), n_floats))
+
+    def grads(self):
+        n, d_f = self.n, self.d_f
+        g = dict(d_mean=np.zeros((n, 3), np.float32), d_scale_log=np.zeros((n, 3), np.float32),
+                 d_quat=np.zeros((n, 4), np.float32), d_opacity_logit=np.zeros(n, np.float32),
+                 d_color=np.zeros((n, 3), np.float32), d_feature=np.zeros((n, d_f), np.float32))
+        self._check(self.L.splatb200_grads_download(self.h, _p(g["d_mean"]), _p(g["d_scale_log"]), _p(g["d_quat"]),
+                                                    _p(g["d_opacity_logit"]), _p(g["d_color"]), _p(g["d_feature"])))
+        g["actors"] = []
+        for a in range(self.n_tracks):
+            dp, dv = np.zeros((self.track_poses[a], 6)), np.zeros(6)
+            self._check(self.L.splatb200_grads_download_actor(self.h, a, _p(dp), _p(dv)))
+            g["actors"].append(dict(d_pose_offset=dp, d_vel_offset=dv))
+        return g
+
+    # ---- views --------------------------------------------------------------------------------
+    def camera_view(self, cam: CameraModel, settings: RasterSettings) -> "View":
+        h = C.c_void_p()
+        pod, st = _camera_pod(cam), _settings_pod(settings)
+        self._check(self.L.splatb200_view_create_camera(self.h, C.byref(pod), C.byref(st), C.byref(h)))
+        return View(self, h, True, cam.width * cam.height)
+
+    def lidar_view(self, lidar: LidarModel, rayset: RaySet, settings: RasterSettings) -> "View":
+        h = C.c_void_p()
+        (pod, elev), st = _lidar_pod(lidar), _settings_pod(settings)
+        rays = _f32(rayset.rays)
+        rb, re = np.ascontiguousarray(rayset.begin, np.int64), np.ascontiguousarray(rayset.end, np.int64)
+        self._check(self.L.splatb200_view_create_lidar(self.h, C.byref(pod), C.byref(st), _p(rays), len(rays), _p(rb),
+                                                       _p(re), len(rb), C.byref(h)))
+        return View(self, h, False, len(rays))
+
+    # reference-shaped one-shot calls: compose + project + bin + composite for one sensor
+    def render_camera(self, cam, settings, t_scene=0.0, stop_after=0) -> "View":
+        v = self.camera_view(cam, settings)
+        v.forward(t_scene, stop_after)
+        return v
+
+    def render_lidar(self, lidar, rayset, settings, t_scene=0.0, stop_after=0) -> "View":
+        v = self.lidar_view(lidar, rayset, settings)
+        v.forward(t_scene, stop_after)
+        return v
+
+
+class View:
+    def __init__(self, ctx: Context, h, camera: bool, P: int):
+        self.ctx, self.h, self.camera, self.P, self.L = ctx, h, camera, P, ctx.L
+
+    def close(self):
+        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
+            self.L.splatb200_view_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_camera(self, cam: CameraModel):
+        pod = _camera_pod(cam)
+        self.ctx._check(self.L.splatb200_view_set_camera(self.h, C.byref(pod)))
+
+    def set_lidar_pose(self, lidar: LidarModel):
+        R, t, vl, va = (_f32(np.asarray(x, np.float64).ravel()) for x in (lidar.R, lidar.t, lidar.vel_lin, lidar.vel_ang))
+        self.ctx._check(self.L.splatb200_view_set_lidar_pose(self.h, _p(R), _p(t), _p(vl), _p(va)))
+
+    def forward(self, t_scene=0.0, stop_after=0):
+        self.ctx._check(self.L.splatb200_view_forward(self.h, C.c_float(t_scene), stop_after))
+
+    def stats(self) -> dict:
+        s = StatsPOD()
+        self.ctx._check(self.L.splatb200_view_stats_get(self.h, C.byref(s)))
+        return {n: int(getattr(s, n)) for n, _ in StatsPOD._fields_}
+
+    def array(self, name):
+        n = self.ctx._check(self.L.splatb200_view_array(self.h, name.encode(), None))
+        out = np.empty(n, np.int64 if name in INT_ARRAYS else np.float32)
+        self.ctx._check(self.L.splatb200_view_array(self.h, name.encode(), _p(out)))
+        return out
+
+    # device pointers of the rendered outputs
+    @property
+    def blend_ptr(self):
+        return int(self.L.splatb200_view_blend(self.h))
+
+    @property
+    def alpha_ptr(self):
+        return int(self.L.splatb200_view_alpha(self.h))
+
+    def backward_device(self, g_blend16_ptr: int, g_alpha_ptr: int):
+        self.ctx._check(self.L.splatb200_view_backward(self.h, C.c_void_p(g_blend16_ptr), C.c_void_p(g_alpha_ptr)))
+
+    def backward(self, g_blend16, g_alpha):
+        """Host-buffer backward (the end-to-end path)."""
+        gb, ga = _f32(g_blend16), _f32(g_alpha)
+        assert gb.size == 16 * self.P and ga.size == self.P
+        self.ctx._check(self.L.splatb200_view_backward_host(self.h, _p(gb), _p(ga)))
+        self.ctx.sync()   # gb / ga are pageable temporaries
+
+    def backward_host_async(self, gb: np.ndarray, ga: np.ndarray):
+        self.ctx._check(self.L.splatb200_view_backward_host(self.h, _p(gb), _p(ga)))
+
+    def download(self, blend16=None, alpha=None, n_contrib=None):
+        self.ctx._check(self.L.splatb200_view_download(self.h, _p(blend16), _p(alpha), _p(n_contrib)))
+
+    def sensor_grads(self):
+        s = SensorGradsPOD()
+        self.ctx._check(self.L.splatb200_view_sensor_grads(self.h, C.byref(s)))
+        return np.array(list(s.d_vel_lin) + list(s.d_vel_ang) + [s.d_time_offset], np.float32)

@@ -1,0 +1,868 @@
+// capi.cu — the C ABI of libsplat_b200.so (include/splat_b200.h): context, scene, views and the
+// stream-ordered stage pipeline  project -> scan -> emit keys -> radix sort -> tile ranges ->
+// composite, and its reverse. Host code only; the kernels live in forward.cu / binning.cu /
+// raster_bwd.cu / project_bwd.cu.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/splat_b200.h"
+#include "kernels.h"
+#include "so3_host.h"
+
+using namespace sb;
+
+namespace {
+std::string g_create_error;
+
+template <class T> void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+}  // namespace
+
+struct splatb200_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // scene
+  int64_t n = 0;
+  int d_f = 0;
+  bool owns_scene = false;
+  float *mean = nullptr, *scale_log = nullptr, *quat = nullptr, *opacity_logit = nullptr, *color = nullptr,
+        *feature = nullptr;
+  int32_t* actor_id = nullptr;
+  std::map<int, int64_t> actor_first;  // distinct actor id -> first Gaussian using it (upload path)
+  int bound_max_actor = 0;             // bind path
+  std::vector<sbh::Track> tracks;
+
+  // SceneParamGrads
+  float* grads = nullptr;
+  bool owns_grads = false;
+  int64_t grads_floats = 0;
+  std::vector<std::vector<double>> actor_d_pose;  // per track 6 x n_poses
+  std::vector<std::vector<double>> actor_d_vel;   // per track 6
+  std::vector<splatb200_view*> views;
+
+  int fail(int code, const std::string& m) {
+    err = m;
+    return code;
+  }
+  ParamGradDev pg() const {
+    ParamGradDev g;
+    g.d_mean = grads;
+    g.d_scale_log = grads + 3 * n;
+    g.d_quat = grads + 6 * n;
+    g.d_opacity_logit = grads + 10 * n;
+    g.d_color = grads + 11 * n;
+    g.d_feature = grads + 14 * n;
+    return g;
+  }
+  SceneDev scene_dev(const ActorState* d_actors) const {
+    SceneDev s;
+    s.n = n; s.d_f = d_f; s.mean = mean; s.scale_log = scale_log; s.quat = quat; s.opacity_logit = opacity_logit;
+    s.color = color; s.feature = feature; s.actor_id = actor_id; s.actors = d_actors; s.n_actors = (int)tracks.size();
+    return s;
+  }
+};
+
+struct splatb200_view {
+  splatb200_ctx* ctx = nullptr;
+  Sensor s;
+  int64_t n_alloc = 0;  // Gaussians the per-source buffers are sized for
+  ProjDev proj{};
+  int64_t* offsets = nullptr;
+  void* scan_temp = nullptr;
+  size_t scan_temp_bytes = 0;
+  float* rg = nullptr;
+  // intersections
+  int64_t isect_cap = 0;
+  uint64_t *keys0 = nullptr, *keys1 = nullptr;
+  uint32_t *vals0 = nullptr, *vals1 = nullptr;
+  void* sort_temp = nullptr;
+  size_t sort_temp_bytes = 0;
+  int sorted_sel = 0;
+  uint32_t *tile_begin = nullptr, *tile_end = nullptr;
+  // queries
+  int64_t P = 0, n_tiles = 0;
+  float* rays = nullptr;
+  int64_t *ray_begin = nullptr, *ray_end = nullptr;
+  RasterOutDev out{};
+  float *g_blend_stage = nullptr, *g_alpha_stage = nullptr;
+  float* sensor_grads = nullptr;  // 6 + d_time_offset
+  // actors
+  ActorState* d_actors = nullptr;
+  int d_actors_cap = 0;
+  float* actor_acc = nullptr;
+  int actor_acc_cap = 0;
+  std::vector<sbh::Interp> poses;
+  bool actor_pending = false;
+  // state
+  int64_t I = 0;
+  int stage = 0;  // 0 nothing, 1 projected, 2 sorted, 3 rasterized
+  float t_scene = 0.0f;
+  int64_t* h_total = nullptr;  // pinned
+
+  const uint64_t* keys() const { return sorted_sel ? keys1 : keys0; }
+  const uint32_t* vals() const { return sorted_sel ? vals1 : vals0; }
+};
+
+#define CU_TRY(ctx, call)                                                                             \
+  do {                                                                                                \
+    cudaError_t e__ = (call);                                                                         \
+    if (e__ != cudaSuccess)                                                                           \
+      return (ctx)->fail(SPLATB200_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__));        \
+  } while (0)
+
+#define CHECK_LAUNCH(ctx, what)                                                                       \
+  do {                                                                                                \
+    cudaError_t e__ = cudaGetLastError();                                                             \
+    if (e__ != cudaSuccess) return (ctx)->fail(SPLATB200_ECUDA, std::string(what) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+namespace {
+
+void free_scene(splatb200_ctx* c) {
+  if (c->owns_scene) {
+    dfree(c->mean); dfree(c->scale_log); dfree(c->quat); dfree(c->opacity_logit); dfree(c->color); dfree(c->feature);
+    dfree(c->actor_id);
+  }
+  c->mean = c->scale_log = c->quat = c->opacity_logit = c->color = c->feature = nullptr;
+  c->actor_id = nullptr;
+  c->owns_scene = false;
+  if (c->owns_grads) dfree(c->grads);
+  c->grads = nullptr;
+  c->owns_grads = false;
+}
+
+int alloc_grads(splatb200_ctx* c) {
+  c->grads_floats = (int64_t)(14 + c->d_f) * c->n;
+  CU_TRY(c, cudaMalloc(&c->grads, sizeof(float) * (size_t)std::max<int64_t>(1, c->grads_floats)));
+  c->owns_grads = true;
+  CU_TRY(c, cudaMemsetAsync(c->grads, 0, sizeof(float) * (size_t)c->grads_floats, c->stream));
+  return SPLATB200_OK;
+}
+
+void reset_actor_grads(splatb200_ctx* c) {
+  c->actor_d_pose.assign(c->tracks.size(), {});
+  c->actor_d_vel.assign(c->tracks.size(), std::vector<double>(6, 0.0));
+  for (size_t a = 0; a < c->tracks.size(); ++a) c->actor_d_pose[a].assign(6 * (size_t)c->tracks[a].n_poses(), 0.0);
+}
+
+// Fold a view's device-side per-actor sums into the host-side ActorGrad slots (scene.hpp:424-453).
+int finalize_actor_grads(splatb200_view* v) {
+  splatb200_ctx* c = v->ctx;
+  if (!v->actor_pending) return SPLATB200_OK;
+  const size_t na = c->tracks.size();
+  std::vector<float> acc(kActorAccStride * na);
+  CU_TRY(c, cudaMemcpyAsync(acc.data(), v->actor_acc, sizeof(float) * acc.size(), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  CU_TRY(c, cudaMemsetAsync(v->actor_acc, 0, sizeof(float) * acc.size(), c->stream));
+  if (c->actor_d_pose.size() != na) reset_actor_grads(c);
+  for (size_t a = 0; a < na && a < v->poses.size(); ++a) {
+    const float* p = &acc[kActorAccStride * a];
+    for (int k = 0; k < 6; ++k) c->actor_d_vel[a][k] += (double)p[6 + k];
+    sbh::V3 g_mu{{p[0], p[1], p[2]}}, g_psi{{p[3], p[4], p[5]}};
+    sbh::pose_offset_backward(c->tracks[a], v->poses[a], g_mu, g_psi, c->actor_d_pose[a].data());
+  }
+  v->actor_pending = false;
+  return SPLATB200_OK;
+}
+
+void free_view_buffers(splatb200_view* v) {
+  dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
+  dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
+  dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
+  dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end);
+  dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
+  if (v->h_total) cudaFreeHost(v->h_total);
+  v->h_total = nullptr;
+}
+
+int ensure_source_buffers(splatb200_view* v) {
+  splatb200_ctx* c = v->ctx;
+  if (v->n_alloc == c->n && v->proj.count) return SPLATB200_OK;
+  dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
+  dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
+  const size_t n = (size_t)std::max<int64_t>(1, c->n);
+  CU_TRY(c, cudaMalloc(&v->proj.geomA, sizeof(float4) * n));
+  CU_TRY(c, cudaMalloc(&v->proj.geomB, sizeof(float4) * n));
+  CU_TRY(c, cudaMalloc(&v->proj.geomC, sizeof(float2) * n));
+  CU_TRY(c, cudaMalloc(&v->proj.feat, sizeof(float4) * 4 * n));
+  CU_TRY(c, cudaMalloc(&v->proj.rect, sizeof(int4) * n));
+  CU_TRY(c, cudaMalloc(&v->proj.count, sizeof(uint32_t) * (n + 1)));
+  CU_TRY(c, cudaMemsetAsync(v->proj.count, 0, sizeof(uint32_t) * (n + 1), c->stream));
+  CU_TRY(c, cudaMalloc(&v->offsets, sizeof(int64_t) * (n + 1)));
+  v->scan_temp_bytes = scan_temp_bytes(c->n);
+  CU_TRY(c, cudaMalloc(&v->scan_temp, v->scan_temp_bytes));
+  CU_TRY(c, cudaMalloc(&v->rg, sizeof(float) * kRasterGradStride * n));
+  CU_TRY(c, cudaMemsetAsync(v->rg, 0, sizeof(float) * kRasterGradStride * n, c->stream));
+  v->n_alloc = c->n;
+  return SPLATB200_OK;
+}
+
+int ensure_isect_capacity(splatb200_view* v, int64_t total) {
+  splatb200_ctx* c = v->ctx;
+  if (total <= v->isect_cap) return SPLATB200_OK;
+  dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
+  const int64_t cap = total + total / 4 + 1024;
+  CU_TRY(c, cudaMalloc(&v->keys0, sizeof(uint64_t) * (size_t)cap));
+  CU_TRY(c, cudaMalloc(&v->keys1, sizeof(uint64_t) * (size_t)cap));
+  CU_TRY(c, cudaMalloc(&v->vals0, sizeof(uint32_t) * (size_t)cap));
+  CU_TRY(c, cudaMalloc(&v->vals1, sizeof(uint32_t) * (size_t)cap));
+  v->sort_temp_bytes = sort_temp_bytes(cap);
+  CU_TRY(c, cudaMalloc(&v->sort_temp, v->sort_temp_bytes));
+  v->isect_cap = cap;
+  return SPLATB200_OK;
+}
+
+void fill_settings(Sensor& s, const splatb200_raster_settings& st) {
+  s.alpha_clamp = st.alpha_clamp; s.alpha_min = st.alpha_min; s.qform_max = st.qform_max;
+  s.transmittance_min = st.transmittance_min; s.near_plane = st.near_plane; s.lidar_min_range = st.lidar_min_range;
+}
+
+void fill_pose(Sensor& s, const float* R, const float* t, const float* vl, const float* va) {
+  for (int k = 0; k < 9; ++k) s.R[k] = R[k];
+  for (int k = 0; k < 3; ++k) { s.t[k] = t[k]; s.vel_lin[k] = vl[k]; s.vel_ang[k] = va[k]; }
+}
+
+int alloc_query_buffers(splatb200_view* v) {
+  splatb200_ctx* c = v->ctx;
+  const size_t P = (size_t)std::max<int64_t>(1, v->P), T = (size_t)std::max<int64_t>(1, v->n_tiles);
+  CU_TRY(c, cudaMalloc(&v->out.blend, sizeof(float) * 16 * P));
+  CU_TRY(c, cudaMalloc(&v->out.alpha, sizeof(float) * P));
+  CU_TRY(c, cudaMalloc(&v->out.t_final, sizeof(float) * P));
+  CU_TRY(c, cudaMalloc(&v->out.range_blend, sizeof(float) * P));
+  CU_TRY(c, cudaMalloc(&v->out.n_contrib, sizeof(int32_t) * P));
+  CU_TRY(c, cudaMalloc(&v->out.last_idx, sizeof(int32_t) * P));
+  CU_TRY(c, cudaMalloc(&v->tile_begin, sizeof(uint32_t) * T));
+  CU_TRY(c, cudaMalloc(&v->tile_end, sizeof(uint32_t) * T));
+  CU_TRY(c, cudaMalloc(&v->sensor_grads, sizeof(float) * 8));
+  CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, c->stream));
+  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t)));
+  return SPLATB200_OK;
+}
+
+int lidar_grid_of(float az_res, int n_beams, int* m_phi, int* m_omega) {
+  // M_phi = ceil(360deg / (N_phi res_phi)), evaluated in double with a 1e-4-tile guard so
+  // that resolutions dividing the circle exactly do not spawn a sliver column from the fp32 rounding of res_phi.
+  *m_phi = (int)std::ceil(6.283185307179586476925 / ((double)kNphi * (double)az_res) - 1e-4);
+  *m_omega = (n_beams + kNomega - 1) / kNomega;
+  return 0;
+}
+
+}  // namespace
+
+// ---- context ------------------------------------------------------------------------------------
+extern "C" int splatb200_ctx_create(int device, void* cuda_stream, splatb200_ctx** out) {
+  if (!out) return SPLATB200_EINVAL;
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    g_create_error = std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "device count is 0") +
+                     " (libsplat_b200 has no CPU fallback)";
+    return SPLATB200_ECUDA;
+  }
+  if (device < 0 || device >= count) {
+    g_create_error = "device index out of range";
+    return SPLATB200_EINVAL;
+  }
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    return SPLATB200_ECUDA;
+  }
+  auto* c = new splatb200_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  *out = c;
+  return SPLATB200_OK;
+}
+
+extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  while (!c->views.empty()) splatb200_view_destroy(c->views.back());
+  free_scene(c);
+  delete c;
+}
+
+extern "C" const char* splatb200_last_error(const splatb200_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+extern "C" int splatb200_ctx_sync(splatb200_ctx* c) {
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
+extern "C" int64_t splatb200_ctx_launch_count(const splatb200_ctx* c) { return c->launches; }
+
+// ---- scene --------------------------------------------------------------------------------------
+extern "C" int splatb200_scene_upload(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
+                                      const float* quat, const float* opacity_logit, const float* color,
+                                      const float* feature, const int32_t* actor_id) {
+  if (n < 0 || d_f < 0 || d_f > 13) return c->fail(SPLATB200_EINVAL, "scene_upload: need n >= 0 and 0 <= d_f <= 13");
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  free_scene(c);
+  c->n = n;
+  c->d_f = d_f;
+  c->owns_scene = true;
+  const size_t m = (size_t)std::max<int64_t>(1, n);
+  auto up = [&](float*& dst, const float* src, int width) -> cudaError_t {
+    cudaError_t e = cudaMalloc(&dst, sizeof(float) * m * (size_t)std::max(1, width));
+    if (e != cudaSuccess || n == 0 || width == 0) return e;
+    return cudaMemcpyAsync(dst, src, sizeof(float) * (size_t)n * width, cudaMemcpyHostToDevice, c->stream);
+  };
+  CU_TRY(c, up(c->mean, mean, 3));
+  CU_TRY(c, up(c->scale_log, scale_log, 3));
+  CU_TRY(c, up(c->quat, quat, 4));
+  CU_TRY(c, up(c->opacity_logit, opacity_logit, 1));
+  CU_TRY(c, up(c->color, color, 3));
+  CU_TRY(c, up(c->feature, feature, d_f));
+  CU_TRY(c, cudaMalloc(&c->actor_id, sizeof(int32_t) * m));
+  if (n) CU_TRY(c, cudaMemcpyAsync(c->actor_id, actor_id, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+  c->actor_first.clear();
+  for (int64_t i = 0; i < n; ++i)
+    if (actor_id[i] != 0) c->actor_first.emplace(actor_id[i], i);
+  c->bound_max_actor = 0;
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  for (auto* v : c->views) v->stage = 0;
+  return alloc_grads(c);
+}
+
+extern "C" int splatb200_scene_bind_device(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean,
+                                           const float* scale_log, const float* quat, const float* opacity_logit,
+                                           const float* color, const float* feature, const int32_t* actor_id,
+                                           int32_t max_actor_id) {
+  if (n < 0 || d_f < 0 || d_f > 13) return c->fail(SPLATB200_EINVAL, "scene_bind_device: need n >= 0 and 0 <= d_f <= 13");
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  float* keep_grads = c->owns_grads ? nullptr : c->grads;
+  const int64_t keep_floats = c->grads_floats;
+  free_scene(c);
+  c->n = n;
+  c->d_f = d_f;
+  c->mean = const_cast<float*>(mean); c->scale_log = const_cast<float*>(scale_log); c->quat = const_cast<float*>(quat);
+  c->opacity_logit = const_cast<float*>(opacity_logit); c->color = const_cast<float*>(color);
+  c->feature = const_cast<float*>(feature); c->actor_id = const_cast<int32_t*>(actor_id);
+  c->actor_first.clear();
+  c->bound_max_actor = max_actor_id;
+  for (auto* v : c->views) v->stage = 0;
+  if (keep_grads && keep_floats == (int64_t)(14 + d_f) * n) {
+    c->grads = keep_grads;
+    c->grads_floats = keep_floats;
+    return SPLATB200_OK;
+  }
+  return alloc_grads(c);
+}
+
+extern "C" int splatb200_scene_set_tracks(splatb200_ctx* c, int32_t n_tracks, const splatb200_actor_track* tracks) {
+  if (n_tracks < 0) return c->fail(SPLATB200_EINVAL, "negative track count");
+  for (auto* v : c->views) {
+    int rc = finalize_actor_grads(v);
+    if (rc) return rc;
+    v->stage = 0;
+  }
+  c->tracks.clear();
+  for (int a = 0; a < n_tracks; ++a) {
+    const auto& t = tracks[a];
+    sbh::Track tk;
+    const int np = t.n_poses;
+    tk.stamps.assign(t.stamps, t.stamps + np);
+    tk.R.assign(t.R, t.R + 9 * np);
+    tk.t.assign(t.t, t.t + 3 * np);
+    if (t.pose_offset) tk.pose_offset.assign(t.pose_offset, t.pose_offset + 6 * np);
+    else tk.pose_offset.assign(6 * (size_t)np, 0.0);
+    for (int k = 0; k < 3; ++k) { tk.vel_lin[k] = t.vel_lin[k]; tk.vel_ang[k] = t.vel_ang[k]; }
+    for (int k = 0; k < 6; ++k) tk.vel_offset[k] = t.vel_offset[k];
+    if (t.init_velocity_from_poses) tk.init_velocity_from_poses();
+    c->tracks.push_back(std::move(tk));
+  }
+  reset_actor_grads(c);
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_scene_actor_velocity(splatb200_ctx* c, int32_t track, double out6[6]) {
+  if (track < 0 || track >= (int)c->tracks.size()) return c->fail(SPLATB200_EINVAL, "track index out of range");
+  for (int k = 0; k < 3; ++k) { out6[k] = c->tracks[track].vel_lin[k]; out6[3 + k] = c->tracks[track].vel_ang[k]; }
+  return SPLATB200_OK;
+}
+
+// ---- grads --------------------------------------------------------------------------------------
+extern "C" int splatb200_grads_zero(splatb200_ctx* c) {
+  if (c->grads) CU_TRY(c, cudaMemsetAsync(c->grads, 0, sizeof(float) * (size_t)c->grads_floats, c->stream));
+  for (auto* v : c->views) {
+    if (v->actor_pending) {
+      CU_TRY(c, cudaMemsetAsync(v->actor_acc, 0, sizeof(float) * kActorAccStride * c->tracks.size(), c->stream));
+      v->actor_pending = false;
+    }
+  }
+  reset_actor_grads(c);
+  return SPLATB200_OK;
+}
+extern "C" int64_t splatb200_grads_size(const splatb200_ctx* c) { return c->grads_floats; }
+extern "C" float* splatb200_grads_device_ptr(splatb200_ctx* c) { return c->grads; }
+extern "C" int splatb200_grads_bind_device(splatb200_ctx* c, float* dev, int64_t n_floats) {
+  if (n_floats != (int64_t)(14 + c->d_f) * c->n) return c->fail(SPLATB200_EINVAL, "grads_bind_device: size must be (14 + d_f) * N floats");
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->owns_grads) dfree(c->grads);
+  c->grads = dev;
+  c->owns_grads = false;
+  c->grads_floats = n_floats;
+  return SPLATB200_OK;
+}
+extern "C" int splatb200_grads_download(splatb200_ctx* c, float* d_mean, float* d_scale_log, float* d_quat,
+                                        float* d_opacity_logit, float* d_color, float* d_feature) {
+  const ParamGradDev g = c->pg();
+  const size_t n = (size_t)c->n;
+  auto dl = [&](float* dst, const float* src, size_t w) -> cudaError_t {
+    if (!dst || n * w == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, sizeof(float) * n * w, cudaMemcpyDeviceToHost, c->stream);
+  };
+  CU_TRY(c, dl(d_mean, g.d_mean, 3));
+  CU_TRY(c, dl(d_scale_log, g.d_scale_log, 3));
+  CU_TRY(c, dl(d_quat, g.d_quat, 4));
+  CU_TRY(c, dl(d_opacity_logit, g.d_opacity_logit, 1));
+  CU_TRY(c, dl(d_color, g.d_color, 3));
+  CU_TRY(c, dl(d_feature, g.d_feature, (size_t)c->d_f));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+extern "C" int splatb200_grads_download_actor(splatb200_ctx* c, int32_t track, double* d_pose_offset, double* d_vel_offset6) {
+  if (track < 0 || track >= (int)c->tracks.size()) return c->fail(SPLATB200_EINVAL, "track index out of range");
+  for (auto* v : c->views) {
+    int rc = finalize_actor_grads(v);
+    if (rc) return rc;
+  }
+  if (d_pose_offset) std::memcpy(d_pose_offset, c->actor_d_pose[track].data(), sizeof(double) * c->actor_d_pose[track].size());
+  if (d_vel_offset6) std::memcpy(d_vel_offset6, c->actor_d_vel[track].data(), sizeof(double) * 6);
+  return SPLATB200_OK;
+}
+
+// ---- views --------------------------------------------------------------------------------------
+extern "C" int splatb200_view_set_camera(splatb200_view* v, const splatb200_camera* cam) {
+  splatb200_ctx* c = v->ctx;
+  if (!v->s.is_camera) return c->fail(SPLATB200_EINVAL, "view is not a camera");
+  if (cam->width != v->s.width || cam->height != v->s.height) return c->fail(SPLATB200_EINVAL, "camera size is fixed per view");
+  v->s.fx = cam->fx; v->s.fy = cam->fy; v->s.cx = cam->cx; v->s.cy = cam->cy;
+  fill_pose(v->s, cam->R, cam->t, cam->vel_lin, cam->vel_ang);
+  v->s.shutter = cam->shutter_duration;
+  v->s.time_offset = cam->time_offset;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_set_lidar_pose(splatb200_view* v, const float R[9], const float t[3], const float vel_lin[3],
+                                             const float vel_ang[3]) {
+  if (v->s.is_camera) return v->ctx->fail(SPLATB200_EINVAL, "view is not a lidar");
+  fill_pose(v->s, R, t, vel_lin, vel_ang);
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_create_camera(splatb200_ctx* c, const splatb200_camera* cam,
+                                            const splatb200_raster_settings* st, splatb200_view** out) {
+  if (!cam || !st || !out) return c->fail(SPLATB200_EINVAL, "null argument");
+  if (cam->width < 1 || cam->height < 1) return c->fail(SPLATB200_EINVAL, "camera needs W, H >= 1");
+  CU_TRY(c, cudaSetDevice(c->device));
+  auto* v = new splatb200_view();
+  v->ctx = c;
+  std::memset(&v->s, 0, sizeof(Sensor));
+  v->s.is_camera = 1;
+  v->s.width = cam->width; v->s.height = cam->height;
+  fill_settings(v->s, *st);
+  v->s.dilation = st->dilation;
+  v->s.tiles_x = (cam->width + kTile - 1) / kTile;
+  v->s.tiles_y = (cam->height + kTile - 1) / kTile;
+  v->P = (int64_t)cam->width * cam->height;
+  v->n_tiles = (int64_t)v->s.tiles_x * v->s.tiles_y;
+  c->views.push_back(v);
+  int rc = splatb200_view_set_camera(v, cam);
+  if (!rc) rc = alloc_query_buffers(v);
+  if (rc) {
+    splatb200_view_destroy(v);
+    return rc;
+  }
+  *out = v;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_lidar_grid(const splatb200_lidar* l, int32_t* m_phi, int32_t* m_omega) {
+  int a, b;
+  lidar_grid_of(l->azimuth_resolution, l->n_beams, &a, &b);
+  if (m_phi) *m_phi = a;
+  if (m_omega) *m_omega = b;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_create_lidar(splatb200_ctx* c, const splatb200_lidar* l, const splatb200_raster_settings* st,
+                                           const float* rays, int64_t n_rays, const int64_t* ray_begin,
+                                           const int64_t* ray_end, int64_t n_tiles, splatb200_view** out) {
+  if (!l || !st || !out || n_rays < 0) return c->fail(SPLATB200_EINVAL, "null argument");
+  if (l->n_beams < 1 || !(l->azimuth_resolution > 0.0f)) return c->fail(SPLATB200_EINVAL, "lidar needs beams and res_phi > 0");
+  CU_TRY(c, cudaSetDevice(c->device));
+  int m_phi, m_omega;
+  lidar_grid_of(l->azimuth_resolution, l->n_beams, &m_phi, &m_omega);
+  if (m_omega - 1 > kMaxBoundaries) return c->fail(SPLATB200_EINVAL, "too many beams");
+  if (n_tiles != (int64_t)m_phi * m_omega) return c->fail(SPLATB200_EINVAL, "n_tiles must equal M_phi * M_omega");
+  auto* v = new splatb200_view();
+  v->ctx = c;
+  std::memset(&v->s, 0, sizeof(Sensor));
+  v->s.is_camera = 0;
+  fill_settings(v->s, *st);
+  fill_pose(v->s, l->R, l->t, l->vel_lin, l->vel_ang);
+  v->s.shutter = l->scan_duration;
+  v->s.dilation = l->beam_divergence_h * l->beam_divergence_v;  // scene.hpp:152, projection.hpp:149
+  v->s.elev_min = l->elevation_channels[0];
+  v->s.elev_max = l->elevation_channels[l->n_beams - 1];
+  v->s.tiles_x = m_phi;
+  v->s.tiles_y = m_omega;
+  v->s.span = (float)kNphi * l->azimuth_resolution;
+  v->s.phi_max = (float)m_phi * v->s.span;
+  v->s.n_boundaries = m_omega - 1;
+  for (int k = 1; k < m_omega; ++k)  // midway between channels 8k-1 and 8k
+    v->s.boundaries[k - 1] = 0.5f * (l->elevation_channels[kNomega * k - 1] + l->elevation_channels[kNomega * k]);
+  v->P = n_rays;
+  v->n_tiles = n_tiles;
+  c->views.push_back(v);
+  int rc = alloc_query_buffers(v);
+  auto fin = [&](int code) {
+    splatb200_view_destroy(v);
+    return code;
+  };
+  if (rc) return fin(rc);
+  const size_t P = (size_t)std::max<int64_t>(1, n_rays);
+  if (cudaMalloc(&v->rays, sizeof(float) * 3 * P) != cudaSuccess || cudaMalloc(&v->ray_begin, sizeof(int64_t) * n_tiles) != cudaSuccess ||
+      cudaMalloc(&v->ray_end, sizeof(int64_t) * n_tiles) != cudaSuccess)
+    return fin(c->fail(SPLATB200_ENOMEM, "cudaMalloc rays"));
+  if (n_rays) cudaMemcpyAsync(v->rays, rays, sizeof(float) * 3 * (size_t)n_rays, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(v->ray_begin, ray_begin, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(v->ray_end, ray_end, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fin(c->fail(SPLATB200_ECUDA, "ray upload failed"));
+  *out = v;
+  return SPLATB200_OK;
+}
+
+extern "C" void splatb200_view_destroy(splatb200_view* v) {
+  if (!v) return;
+  splatb200_ctx* c = v->ctx;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  finalize_actor_grads(v);
+  free_view_buffers(v);
+  for (size_t k = 0; k < c->views.size(); ++k)
+    if (c->views[k] == v) {
+      c->views.erase(c->views.begin() + k);
+      break;
+    }
+  delete v;
+}
+
+// compose_at_time's host part: actor validation (scene.hpp:297-298) and pose interpolation
+// (scene.hpp:283-285), then the per-actor state upload.
+static int prepare_actors(splatb200_view* v, float t_scene) {
+  splatb200_ctx* c = v->ctx;
+  const int na = (int)c->tracks.size();
+  int rc = finalize_actor_grads(v);
+  if (rc) return rc;
+  v->poses.clear();
+  try {
+    for (const auto& tk : c->tracks) v->poses.push_back(sbh::interpolate_pose(tk, (double)t_scene));
+  } catch (const std::runtime_error& e) {
+    return c->fail(SPLATB200_ERUNTIME, e.what());
+  }
+  int bad = 0;
+  int64_t bad_at = -1;
+  for (const auto& kv : c->actor_first)
+    if ((kv.first < 0 || kv.first > na) && (bad_at < 0 || kv.second < bad_at)) { bad = kv.first; bad_at = kv.second; }
+  if (bad_at >= 0) return c->fail(SPLATB200_EOUTOFRANGE, "unknown actor_id " + std::to_string(bad));
+  if (c->bound_max_actor > na) return c->fail(SPLATB200_EOUTOFRANGE, "unknown actor_id " + std::to_string(c->bound_max_actor));
+  if (na == 0) return SPLATB200_OK;
+  if (v->d_actors_cap < na) {
+    dfree(v->d_actors);
+    CU_TRY(c, cudaMalloc(&v->d_actors, sizeof(ActorState) * na));
+    v->d_actors_cap = na;
+  }
+  if (v->actor_acc_cap < na) {
+    dfree(v->actor_acc);
+    CU_TRY(c, cudaMalloc(&v->actor_acc, sizeof(float) * kActorAccStride * na));
+    CU_TRY(c, cudaMemsetAsync(v->actor_acc, 0, sizeof(float) * kActorAccStride * na, c->stream));
+    v->actor_acc_cap = na;
+  }
+  std::vector<ActorState> st(na);
+  for (int a = 0; a < na; ++a) {
+    const auto& ip = v->poses[a];
+    const auto& tk = c->tracks[a];
+    for (int k = 0; k < 9; ++k) st[a].R[k] = (float)ip.R.a[k];
+    for (int k = 0; k < 3; ++k) {
+      st[a].t[k] = (float)ip.t.a[k];
+      st[a].v[k] = (float)(tk.vel_lin[k] + tk.vel_offset[k]);      // scene.hpp:61
+      st[a].w[k] = (float)(tk.vel_ang[k] + tk.vel_offset[3 + k]);  // scene.hpp:62
+    }
+  }
+  // the previous frame's kernels may still read d_actors: order the overwrite after them
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  CU_TRY(c, cudaMemcpy(v->d_actors, st.data(), sizeof(ActorState) * na, cudaMemcpyHostToDevice));
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t stop_after) {
+  splatb200_ctx* c = v->ctx;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (!c->mean && c->n > 0) return c->fail(SPLATB200_EINVAL, "no scene uploaded");
+  v->stage = 0;
+  v->t_scene = t_scene;
+  int rc = prepare_actors(v, t_scene);
+  if (rc) return rc;
+  rc = ensure_source_buffers(v);
+  if (rc) return rc;
+  v->s.d_f = c->d_f;
+  v->s.channels = v->s.is_camera ? 3 + c->d_f : c->d_f;
+  cudaStream_t st = c->stream;
+  const SceneDev sc = c->scene_dev(v->d_actors);
+  CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, st));
+
+  launch_project(v->s, sc, v->proj, st);
+  CHECK_LAUNCH(c, "k_project");
+  c->launches += c->n > 0;
+  launch_scan_counts(v->proj.count, v->offsets, c->n, v->scan_temp, v->scan_temp_bytes, st);
+  CHECK_LAUNCH(c, "scan");
+  c->launches += 2;
+  CU_TRY(c, cudaMemcpyAsync(v->h_total, v->offsets + c->n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU_TRY(c, cudaStreamSynchronize(st));
+  v->I = *v->h_total;
+  v->stage = 1;
+  if (stop_after == 1) return SPLATB200_OK;
+  if (v->I > 0x7fffffffLL) return c->fail(SPLATB200_ENOMEM, "more than 2^31-1 intersections in one view");
+  rc = ensure_isect_capacity(v, v->I);
+  if (rc) return rc;
+
+  launch_emit_keys(c->n, v->I, v->offsets, v->proj, v->s.tiles_x, v->s.is_camera ? 0 : 1, v->keys0, v->vals0, st);
+  CHECK_LAUNCH(c, "k_emit_keys");
+  int tile_bits = 1;
+  while ((1LL << tile_bits) < v->n_tiles) ++tile_bits;
+  v->sorted_sel = 0;
+  if (v->I > 0) {
+    v->sorted_sel = launch_sort_pairs(v->keys0, v->keys1, v->vals0, v->vals1, v->I, 32 + tile_bits, v->sort_temp,
+                                      v->sort_temp_bytes, st);
+    CHECK_LAUNCH(c, "radix sort");
+    c->launches += 1 + 2 + (32 + tile_bits + 7) / 8;
+  }
+  CU_TRY(c, cudaMemsetAsync(v->tile_begin, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
+  CU_TRY(c, cudaMemsetAsync(v->tile_end, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
+  launch_tile_ranges(v->I, v->keys(), v->tile_begin, v->tile_end, st);
+  CHECK_LAUNCH(c, "k_tile_ranges");
+  c->launches += v->I > 0;
+  v->stage = 2;
+  if (stop_after == 2) return SPLATB200_OK;
+
+  launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out, st);
+  CHECK_LAUNCH(c, "k_raster_fwd");
+  c->launches += 1;
+  v->stage = 3;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_stats_get(splatb200_view* v, splatb200_view_stats* out) {
+  splatb200_ctx* c = v->ctx;
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "stats before forward");
+  std::vector<uint32_t> cnt((size_t)c->n);
+  if (c->n) CU_TRY(c, cudaMemcpyAsync(cnt.data(), v->proj.count, sizeof(uint32_t) * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  int64_t vis = 0;
+  for (uint32_t x : cnt) vis += x != 0;
+  out->n_gaussians = c->n;
+  out->n_visible = vis;
+  out->n_intersections = v->I;
+  out->n_queries = v->P;
+  out->tiles_x = v->s.tiles_x;
+  out->tiles_y = v->s.tiles_y;
+  return SPLATB200_OK;
+}
+
+extern "C" const float* splatb200_view_blend(splatb200_view* v) { return v->out.blend; }
+extern "C" const float* splatb200_view_alpha(splatb200_view* v) { return v->out.alpha; }
+extern "C" const int32_t* splatb200_view_n_contrib(splatb200_view* v) { return v->out.n_contrib; }
+
+extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16, const float* g_alpha) {
+  splatb200_ctx* c = v->ctx;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
+  if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
+  cudaStream_t st = c->stream;
+  RasterGradDev rg{v->rg};
+  const ParamGradDev pg = c->pg();
+  if (v->I > 0) {
+    launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out,
+                      g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
+    CHECK_LAUNCH(c, "k_raster_bwd");
+    c->launches += 1;
+  }
+  launch_project_bwd(v->s, c->scene_dev(v->d_actors), v->proj, rg, pg, v->sensor_grads, v->actor_acc, st);
+  CHECK_LAUNCH(c, "k_project_bwd");
+  c->launches += c->n > 0;
+  if (!c->tracks.empty()) v->actor_pending = true;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_sensor_grads(splatb200_view* v, splatb200_sensor_grads* out) {
+  splatb200_ctx* c = v->ctx;
+  float h[8];
+  CU_TRY(c, cudaMemcpyAsync(h, v->sensor_grads, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < 3; ++k) { out->d_vel_lin[k] = h[k]; out->d_vel_ang[k] = h[3 + k]; }
+  out->d_time_offset = h[6];
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_download(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib) {
+  splatb200_ctx* c = v->ctx;
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "download before forward");
+  const size_t P = (size_t)v->P;
+  if (blend16 && P) CU_TRY(c, cudaMemcpyAsync(blend16, v->out.blend, sizeof(float) * 16 * P, cudaMemcpyDeviceToHost, c->stream));
+  if (alpha && P) CU_TRY(c, cudaMemcpyAsync(alpha, v->out.alpha, sizeof(float) * P, cudaMemcpyDeviceToHost, c->stream));
+  if (n_contrib && P) CU_TRY(c, cudaMemcpyAsync(n_contrib, v->out.n_contrib, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, const float* g_alpha) {
+  splatb200_ctx* c = v->ctx;
+  if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
+  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  if (!v->g_blend_stage) {
+    CU_TRY(c, cudaMalloc(&v->g_blend_stage, sizeof(float) * 16 * P));
+    CU_TRY(c, cudaMalloc(&v->g_alpha_stage, sizeof(float) * P));
+  }
+  CU_TRY(c, cudaMemcpyAsync(v->g_blend_stage, g_blend16, sizeof(float) * 16 * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(v->g_alpha_stage, g_alpha, sizeof(float) * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
+  return splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
+}
+
+// ---- introspection ------------------------------------------------------------------------------
+namespace {
+template <class T> int fetch(splatb200_ctx* c, std::vector<T>& h, const T* d, size_t n) {
+  h.resize(n);
+  if (n) CU_TRY(c, cudaMemcpyAsync(h.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+}  // namespace
+
+extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, void* dst) {
+  splatb200_ctx* c = v->ctx;
+  const std::string name(name_c ? name_c : "");
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "view_array before forward");
+  const size_t N = (size_t)c->n;
+
+  struct Field { const char* name; int off, width; };
+  static const Field dump_fields[] = {{"mean2d", 1, 2}, {"depth_key", 3, 1}, {"cov2d", 4, 4}, {"velocity", 8, 3},
+                                      {"aabb", 11, 4}, {"conic", 15, 4}, {"det_ratio", 19, 1}, {"mu_sensor", 20, 3},
+                                      {"rel_vel_sensor", 23, 3}};
+  static const Field scene_fields[] = {{"opacity", 26, 1}, {"mean_w", 27, 3}, {"vel_dyn_w", 30, 3}, {"cov_w", 33, 9}};
+  const Field* df = nullptr;
+  bool per_scene = false;
+  for (const auto& f : dump_fields) if (name == f.name) df = &f;
+  for (const auto& f : scene_fields) if (name == f.name) { df = &f; per_scene = true; }
+
+  if (df || name == "source_index" || name == "rect") {
+    std::vector<uint32_t> cnt;
+    int rc = fetch(c, cnt, v->proj.count, N);
+    if (rc) return rc;
+    std::vector<int64_t> vis;
+    for (size_t i = 0; i < N; ++i) if (cnt[i]) vis.push_back((int64_t)i);
+    if (name == "source_index") {
+      if (dst) std::memcpy(dst, vis.data(), sizeof(int64_t) * vis.size());
+      return (int64_t)vis.size();
+    }
+    if (name == "rect") {
+      std::vector<int4> r;
+      rc = fetch(c, r, v->proj.rect, N);
+      if (rc) return rc;
+      if (dst) {
+        int64_t* d = (int64_t*)dst;
+        for (size_t k = 0; k < vis.size(); ++k) {
+          const int4 q = r[vis[k]];
+          d[4 * k] = q.x; d[4 * k + 1] = q.y; d[4 * k + 2] = q.z; d[4 * k + 3] = q.w;
+        }
+      }
+      return (int64_t)vis.size() * 4;
+    }
+    const size_t rows = per_scene ? N : vis.size();
+    if (!dst) return (int64_t)rows * df->width;
+    float* dump = nullptr;
+    CU_TRY(c, cudaMalloc(&dump, sizeof(float) * kDumpStride * std::max<size_t>(1, N)));
+    cudaMemsetAsync(dump, 0, sizeof(float) * kDumpStride * N, c->stream);
+    launch_project_dump(v->s, c->scene_dev(v->d_actors), dump, c->stream);
+    std::vector<float> h;
+    rc = fetch(c, h, dump, (size_t)kDumpStride * N);
+    cudaFree(dump);
+    if (rc) return rc;
+    float* d = (float*)dst;
+    for (size_t k = 0; k < rows; ++k) {
+      const size_t i = per_scene ? k : (size_t)vis[k];
+      for (int w = 0; w < df->width; ++w) d[k * df->width + w] = h[i * kDumpStride + df->off + w];
+    }
+    return (int64_t)rows * df->width;
+  }
+
+  if (name == "isect_tile" || name == "isect_depth_bits" || name == "isect_src") {
+    if (v->stage < 2) return c->fail(SPLATB200_ERUNTIME, "worklist not built");
+    if (!dst) return v->I;
+    int64_t* d = (int64_t*)dst;
+    if (name == "isect_src") {
+      std::vector<uint32_t> h;
+      int rc = fetch(c, h, v->vals(), (size_t)v->I);
+      if (rc) return rc;
+      for (int64_t k = 0; k < v->I; ++k) d[k] = h[k];
+    } else {
+      std::vector<uint64_t> h;
+      int rc = fetch(c, h, v->keys(), (size_t)v->I);
+      if (rc) return rc;
+      const bool tile = name == "isect_tile";
+      for (int64_t k = 0; k < v->I; ++k) d[k] = tile ? (int64_t)(h[k] >> 32) : (int64_t)(h[k] & 0xffffffffull);
+    }
+    return v->I;
+  }
+  if (name == "tile_begin" || name == "tile_end") {
+    if (v->stage < 2) return c->fail(SPLATB200_ERUNTIME, "worklist not built");
+    if (!dst) return v->n_tiles;
+    std::vector<uint32_t> h;
+    int rc = fetch(c, h, name == "tile_begin" ? v->tile_begin : v->tile_end, (size_t)v->n_tiles);
+    if (rc) return rc;
+    for (int64_t k = 0; k < v->n_tiles; ++k) ((int64_t*)dst)[k] = h[k];
+    return v->n_tiles;
+  }
+  if (name == "grid") {
+    if (dst) { ((int64_t*)dst)[0] = v->s.tiles_x; ((int64_t*)dst)[1] = v->s.tiles_y; }
+    return 2;
+  }
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "not rasterized");
+  const size_t P = (size_t)v->P;
+  if (name == "n_contrib" || name == "last_idx") {
+    if (!dst) return v->P;
+    std::vector<int32_t> h;
+    int rc = fetch(c, h, name == "n_contrib" ? v->out.n_contrib : v->out.last_idx, P);
+    if (rc) return rc;
+    for (size_t k = 0; k < P; ++k) ((int64_t*)dst)[k] = h[k];
+    return v->P;
+  }
+  const float* src = nullptr;
+  size_t cnt = P;
+  if (name == "blend") { src = v->out.blend; cnt = 16 * P; }
+  else if (name == "alpha") src = v->out.alpha;
+  else if (name == "t_final") src = v->out.t_final;
+  else if (name == "range_blend") src = v->out.range_blend;
+  if (!src) return c->fail(SPLATB200_EINVAL, "unknown array name " + name);
+  if (dst && cnt) {
+    CU_TRY(c, cudaMemcpyAsync(dst, src, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  return (int64_t)cnt;
+}

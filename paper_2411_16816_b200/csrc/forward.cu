@@ -1,0 +1,264 @@
+// forward.cu — forward kernels of the hot path (compiled with --fmad=false, see splat_device.cuh).
+//
+//   k_project<camera|lidar>   compose_at_time + project_camera/project_lidar fused, one thread per
+//                             Gaussian: scene.hpp:273-308, projection.hpp:88-118 / 140-174, plus the
+//                             tile rectangle and the packed compositing record.
+//   k_emit_keys               duplication: one (tile_id << 32 | depth_bits, source_index) pair per
+//                             intersection.
+//   k_tile_ranges             per-tile [begin, end) slices of the sorted worklist.
+//   k_raster_fwd<camera|lidar> per-tile front-to-back compositing (Eq. 3-6).
+#include "kernels.h"
+#include "raster_common.cuh"
+
+namespace sb {
+
+// ------------------------------------------------------------------------------------------------
+// K1/K2: fused compose + projection + tile rectangle
+// ------------------------------------------------------------------------------------------------
+template <bool kCamera>
+__global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sc.n) return;
+  Fwd f;
+  compose_one(sc, i, f);
+  if (kCamera) project_camera_one(s, f);
+  else project_lidar_one(s, f);
+  if (!f.visible) {
+    p.count[i] = 0u;
+    return;
+  }
+  const int4 r = kCamera ? image_tile_range(f, s.tiles_x, s.tiles_y) : lidar_tile_range(f, s);
+  const int w = r.y - r.x, h = r.w - r.z;
+  p.count[i] = (w > 0 && h > 0) ? (uint32_t)w * (uint32_t)h : 0u;
+  p.rect[i] = r;
+  p.geomA[i] = make_float4(f.mean2d[0], f.mean2d[1], f.vel[0], f.vel[1]);
+  p.geomB[i] = make_float4(f.conic[0], f.conic[1] + f.conic[2], f.conic[3], f.det_ratio * f.opacity);
+  p.geomC[i] = make_float2(f.depth, f.vel[2]);
+  float ch[kChannels];
+#pragma unroll
+  for (int k = 0; k < kChannels; ++k) ch[k] = 0.0f;
+  int o = 0;
+  if (kCamera) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ch[o++] = sc.color[3 * i + k];
+  }
+  for (int k = 0; k < sc.d_f; ++k) ch[o + k] = sc.feature[(int64_t)sc.d_f * i + k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p.feat[4 * i + k] = make_float4(ch[4 * k], ch[4 * k + 1], ch[4 * k + 2], ch[4 * k + 3]);
+}
+
+void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st) {
+  if (sc.n == 0) return;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
+  if (s.is_camera) k_project<true><<<blocks, threads, 0, st>>>(s, sc, p);
+  else k_project<false><<<blocks, threads, 0, st>>>(s, sc, p);
+}
+
+// ------------------------------------------------------------------------------------------------
+// K3: key generation. One thread per intersection; the owning Gaussian is found by binary search in
+// the exclusive scan of the per-Gaussian tile counts, which makes the kernel insensitive to the
+// heavy-tailed counts (a grazing Gaussian can cover all 8,160 tiles) and keeps the key stream in
+// ascending source order, so that a stable sort yields the (tile, depth, source_index) order.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_emit_keys(int64_t n, int64_t total, const int64_t* __restrict__ offsets,
+                                                   const int4* __restrict__ rect, const float2* __restrict__ geomC,
+                                                   int tiles_x, int wrap_x, uint64_t* __restrict__ keys,
+                                                   uint32_t* __restrict__ vals) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int64_t lo = 0, hi = n;  // invariant: offsets[lo] <= e < offsets[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (offsets[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  const int4 r = rect[lo];
+  const int w = r.y - r.x;
+  const int local = (int)(e - offsets[lo]);
+  const int y = r.z + local / w;
+  int x = r.x + local % w;
+  if (wrap_x) x = ((x % tiles_x) + tiles_x) % tiles_x;
+  const uint32_t tile = (uint32_t)(y * tiles_x + x);
+  keys[e] = ((uint64_t)tile << 32) | (uint64_t)__float_as_uint(geomC[lo].x);
+  vals[e] = (uint32_t)lo;
+}
+
+void launch_emit_keys(int64_t n, int64_t total, const int64_t* offsets, const ProjDev& p, int tiles_x, int wrap_x,
+                      uint64_t* keys, uint32_t* vals, cudaStream_t st) {
+  if (total == 0) return;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  k_emit_keys<<<blocks, 256, 0, st>>>(n, total, offsets, p.rect, p.geomC, tiles_x, wrap_x, keys, vals);
+}
+
+__global__ void __launch_bounds__(256) k_tile_ranges(int64_t total, const uint64_t* __restrict__ keys,
+                                                     uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t t = (uint32_t)(keys[e] >> 32);
+  if (e == 0 || (uint32_t)(keys[e - 1] >> 32) != t) tile_begin[t] = (uint32_t)e;
+  if (e == total - 1 || (uint32_t)(keys[e + 1] >> 32) != t) tile_end[t] = (uint32_t)(e + 1);
+}
+
+void launch_tile_ranges(int64_t total, const uint64_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st) {
+  if (total == 0) return;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  k_tile_ranges<<<blocks, 256, 0, st>>>(total, keys, tile_begin, tile_end);
+}
+
+// ------------------------------------------------------------------------------------------------
+// K5/K6: forward compositing. One CTA of 256 threads per tile: 16x16 pixels, or up to 256 rays of
+// a 32x8 lidar tile (more than 256 rays => additional passes over the list). The tile's
+// depth-sorted slice is staged through shared memory 256 Gaussians at a time (each thread fetches one
+// 112-byte record with 7 128-bit loads); every thread then walks the batch front to back with
+// broadcast shared-memory reads. The batch loop ends when every query of the tile has saturated
+// (T < transmittance_min), detected with one __syncthreads_and per batch.
+// ------------------------------------------------------------------------------------------------
+template <bool kCamera>
+__global__ void __launch_bounds__(256)
+k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
+             const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
+             const float* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
+             RasterOutDev out) {
+  __shared__ float4 sA[256];
+  __shared__ float4 sB[256];
+  __shared__ float2 sC[256];
+  __shared__ float4 sF[256 * 4];
+
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const uint32_t lb = tile_begin[tile], le = tile_end[tile];
+
+  int64_t q_begin = 0, q_end = 1;  // camera: single pass
+  if (!kCamera) { q_begin = ray_begin[tile]; q_end = ray_end[tile]; }
+
+  for (int64_t q_base = q_begin; q_base < q_end; q_base += 256) {
+    bool inside;
+    int64_t pix;
+    float qx, qy, t;
+    if (kCamera) {
+      const int px = (tile % s.tiles_x) * kTile + (tid & 15);
+      const int py = (tile / s.tiles_x) * kTile + (tid >> 4);
+      inside = px < s.width && py < s.height;
+      pix = (int64_t)py * s.width + px;
+      qx = (float)px + 0.5f;
+      qy = (float)py + 0.5f;
+      t = ((float)py / (float)s.height - 0.5f) * s.shutter + s.time_offset;  // Eq. 3
+    } else {
+      pix = q_base + tid;
+      inside = pix < q_end;
+      qx = qy = t = 0.0f;
+      if (inside) { qx = rays[3 * pix]; qy = rays[3 * pix + 1]; t = rays[3 * pix + 2]; }
+    }
+
+    float T = 1.0f, range_acc = 0.0f, median = 0.0f;
+    bool med_found = false;
+    int n_contrib = 0, last_idx = 0;
+    float acc[kChannels];
+#pragma unroll
+    for (int k = 0; k < kChannels; ++k) acc[k] = 0.0f;
+    bool done = !inside;
+
+    for (uint32_t base = lb; base < le; base += 256) {
+      if (__syncthreads_and(done)) break;
+      const uint32_t idx = base + tid;
+      if (idx < le) {
+        const uint32_t src = vals[idx];
+        sA[tid] = p.geomA[src];
+        sB[tid] = p.geomB[src];
+        if (!kCamera) sC[tid] = p.geomC[src];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sF[4 * tid + k] = p.feat[4 * (size_t)src + k];
+      }
+      __syncthreads();
+      const int cnt = min(256u, le - base);
+      if (!done) {
+        for (int j = 0; j < cnt; ++j) {
+          AlphaEval ev;
+          if (!evaluate_alpha<!kCamera>(sA[j], sB[j], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) continue;
+          const float w = __fmul_rn(ev.alpha, T);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 f4 = sF[4 * j + k];
+            acc[4 * k] = __fmaf_rn(f4.x, w, acc[4 * k]);
+            acc[4 * k + 1] = __fmaf_rn(f4.y, w, acc[4 * k + 1]);
+            acc[4 * k + 2] = __fmaf_rn(f4.z, w, acc[4 * k + 2]);
+            acc[4 * k + 3] = __fmaf_rn(f4.w, w, acc[4 * k + 3]);
+          }
+          T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
+          ++n_contrib;
+          last_idx = (int)(base - lb) + j + 1;
+          if (!kCamera) {
+            const float2 c = sC[j];
+            const float r_rs = __fmaf_rn(c.y, t, c.x);
+            range_acc = __fmaf_rn(r_rs, w, range_acc);
+            if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
+          }
+          if (T < s.transmittance_min) { done = true; break; }
+        }
+      }
+    }
+
+    if (inside) {
+      const float A = __fsub_rn(1.0f, T);
+      if (!kCamera) {
+        acc[13] = (A > 1e-6f) ? __fdiv_rn(range_acc, A) : range_acc;
+        acc[14] = median;
+        acc[15] = A;
+        out.range_blend[pix] = range_acc;
+      }
+      float4* o4 = reinterpret_cast<float4*>(out.blend + 16 * pix);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+      out.alpha[pix] = A;
+      out.t_final[pix] = T;
+      out.n_contrib[pix] = n_contrib;
+      out.last_idx[pix] = last_idx;
+    }
+    __syncthreads();  // shared staging is reused by the next ray pass
+  }
+}
+
+void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
+                       const uint32_t* tile_end, const float* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                       const RasterOutDev& out, cudaStream_t st) {
+  const int tiles = s.tiles_x * s.tiles_y;
+  if (tiles == 0) return;
+  if (s.is_camera) k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, out);
+  else k_raster_fwd<false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, out);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Introspection (parity tests only, not on the hot path): the full ProjectedGaussian / ComposedScene
+// record of every Gaussian, recomputed with the identical instruction sequence as k_project.
+// Layout per Gaussian (kDumpStride floats): visible, mean2d 2, depth, cov2d 4, velocity 3, aabb 4,
+// conic 4, det_ratio, mu_sensor 3, rel_vel_sensor 3, opacity, mean_w 3, vel_dyn_w 3, cov_w 9.
+// ------------------------------------------------------------------------------------------------
+template <bool kCamera>
+__global__ void __launch_bounds__(256) k_project_dump(const __grid_constant__ Sensor s, SceneDev sc, float* __restrict__ d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sc.n) return;
+  Fwd f;
+  compose_one(sc, i, f);
+  if (kCamera) project_camera_one(s, f);
+  else project_lidar_one(s, f);
+  float* o = d + (size_t)kDumpStride * i;
+  o[0] = f.visible ? 1.0f : 0.0f;
+  o[26] = f.opacity;
+  for (int k = 0; k < 3; ++k) { o[27 + k] = f.mean_w[k]; o[30 + k] = f.vel_dyn_w[k]; }
+  for (int k = 0; k < 9; ++k) o[33 + k] = f.cov_w[k];
+  if (!f.visible) return;
+  o[1] = f.mean2d[0]; o[2] = f.mean2d[1]; o[3] = f.depth;
+  for (int k = 0; k < 4; ++k) { o[4 + k] = f.cov2d[k]; o[15 + k] = f.conic[k]; }
+  for (int k = 0; k < 3; ++k) { o[8 + k] = f.vel[k]; o[20 + k] = f.mu[k]; o[23 + k] = f.u[k]; }
+  o[11] = f.lo[0]; o[12] = f.lo[1]; o[13] = f.hi[0]; o[14] = f.hi[1];
+  o[19] = f.det_ratio;
+}
+void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st) {
+  if (sc.n == 0) return;
+  const unsigned blocks = (unsigned)((sc.n + 255) / 256);
+  if (s.is_camera) k_project_dump<true><<<blocks, 256, 0, st>>>(s, sc, dump);
+  else k_project_dump<false><<<blocks, 256, 0, st>>>(s, sc, dump);
+}
+
+}  // namespace sb

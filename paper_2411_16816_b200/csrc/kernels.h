@@ -1,0 +1,72 @@
+// kernels.h — host-callable launchers of the sm_100a kernels (one per stage of the hot path).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "splat_device.cuh"
+
+namespace sb {
+
+struct RasterOutDev {
+  float* blend;        // P x 16
+  float* alpha;        // P
+  float* t_final;      // P  saved terminal transmittance
+  float* range_blend;  // P  lidar: un-normalised sum w r_rs
+  int32_t* n_contrib;  // P
+  int32_t* last_idx;   // P  1-based tile-local list position of the last blended Gaussian
+};
+
+// Raw per-Gaussian sums of the compositing backward, indexed by source index; consumed (and re-zeroed)
+// by the projection backward. 10 floats per Gaussian: conic (3), mean2d (2), velocity (3), rho, range.
+struct RasterGradDev {
+  float* g;  // N x 10, zero between backward calls
+};
+constexpr int kRasterGradStride = 10;
+
+// SceneParamGrads (scene.hpp:325-363) as one contiguous device buffer.
+struct ParamGradDev {
+  float* d_mean;
+  float* d_scale_log;
+  float* d_quat;
+  float* d_opacity_logit;
+  float* d_color;
+  float* d_feature;
+};
+
+// Per-actor accumulators filled by the projection/compose backward, finished on the host with the
+// SO(3) Jacobians (scene.hpp:428-453): g_mu_w (3), g_psi (3), d_vel_offset (6).
+constexpr int kActorAccStride = 12;
+
+// forward.cu
+void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st);
+void launch_emit_keys(int64_t n, int64_t total, const int64_t* offsets, const ProjDev& p, int tiles_x, int wrap_x,
+                      uint64_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_tile_ranges(int64_t total, const uint64_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st);
+void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
+                       const uint32_t* tile_end, const float* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                       const RasterOutDev& out, cudaStream_t st);
+constexpr int kDumpStride = 42;
+void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
+
+// binning.cu (device scan + radix sort)
+size_t scan_temp_bytes(int64_t n);
+void launch_scan_counts(const uint32_t* count, int64_t* offsets /* n + 1 */, int64_t n, void* temp, size_t temp_bytes,
+                        cudaStream_t st);
+void launch_scan_i64(const int64_t* in, int64_t* out /* n + 1 */, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
+size_t sort_temp_bytes(int64_t n);
+// sorts (keys, vals) by the low `key_bits` bits, stable; returns which buffer holds the result (0 / 1)
+int launch_sort_pairs(uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int key_bits,
+                      void* temp, size_t temp_bytes, cudaStream_t st);
+
+// raster_bwd.cu
+void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
+                       const uint32_t* tile_end, const float* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                       const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha, const RasterGradDev& rg,
+                       const ParamGradDev& pg, float* d_time_offset, cudaStream_t st);
+
+// project_bwd.cu
+void launch_project_bwd(const Sensor& s, const SceneDev& sc, const ProjDev& p, const RasterGradDev& rg,
+                        const ParamGradDev& pg, float* sensor_grads6, float* actor_acc, cudaStream_t st);
+
+}  // namespace sb
