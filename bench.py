@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the SplatAD camera + lidar rasterizer hot path on B200.
+
+Metric (BASELINE.json): lidar Mrays/s + camera MPix/s, forward+backward, next to the CPU path.
+
+One "step" = one FRAME of the north-star workload: a 128-beam 360-degree lidar sweep (1800 azimuth bins,
+non-uniform elevations, rolling shutter) plus a 1920x1080 rolling-shutter camera over a 1M-Gaussian
+synthetic scene (`synth-v1`), each rendered forward + backward through the C ABI of
+libsplat_b200.so (compose -> project -> tile-bin + radix sort -> composite, and the reverse).
+`value` = (rays + pixels) of all ranks / step time, in Mqueries/s; the per-sensor rates are in `breakdown`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W]            the sm_100a path
+  python bench.py --impl reference ...                           the reference's CPU path (the oracle port)
+
+N > 1 (torchrun, one rank per GPU): the scene is replicated, rank r renders frame r (ego pose advanced
+1.5 m and camera yawed 60 degrees per frame: independent frames, no data-path collective), and the
+per-Gaussian SceneParamGrads buffer (27 N floats) is all-reduced with NCCL every step — "weak" scaling.
+
+oracle/ is used here only as the CPU baseline (cpu_baseline leg, --impl reference), never on the GPU path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+N_GAUSS = 1_000_000
+SCENE_SEED = 3
+METRIC = "lidar Mrays/s + camera MPix/s, fwd+bwd (one frame = 128-beam lidar sweep + 1920x1080 RS camera, 1M Gaussians)"
+UNIT = "Mqueries/s"
+
+
+def frame_sensors(frame: int):
+    """Frame `frame` of the drive: ego advanced 1.5 m per frame, camera k of a 6-camera rig (yaw k*60 deg)."""
+    from paper_2411_16816_b200 import synth
+    x = 1.5 * frame
+    lid = synth.lidar128(position=(x, 0.0, 1.8))
+    cam = synth.make_camera(position=(x, 0.0, 1.5), yaw=(frame % 6) * np.pi / 3.0)
+    return lid, cam
+
+
+def workload_config(world: int):
+    return {
+        "workload": "north-star frame: synth-v1 scene N=1,000,000 static Gaussians (d_f=13), lidar-128 "
+                    "(1800 bins, non-uniform elevation, 0.1 s sweep, moving sensor) + 1920x1080 pinhole camera "
+                    "(30 ms rolling shutter, moving sensor), forward+backward incl. features/intensity/ray-drop, "
+                    "expected+median range",
+        "n_gaussians": N_GAUSS, "lidar_rays": 128 * 1800, "camera_pixels": 1920 * 1080,
+        "frames_per_step": world, "parallelism": f"frames x{world} (scene replicated, grads all-reduced)" if world > 1 else "single GPU",
+        "l2_policy": "inputs larger than L2 (scene 112 MB + per-view records and worklists > 500 MB, L2 126 MB); no explicit flush",
+    }
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks (B200_PROFILING.md: sample nvidia-smi DURING the timed region)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows, self.proc, self.thread = [], None, None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                                          "-i", str(index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def stop(self, t0: float, t1: float):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()          # the exact PID we started
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        rows = [r for (t, r) in self.rows if t0 - 0.05 <= t <= t1 + 0.15] or [r for (_, r) in self.rows]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1])); pw.append(float(f[2]))
+            except Exception:
+                continue
+            for k, nm in enumerate(names):
+                if len(f) > 3 + k and f[3 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------------------
+# algorithmic bytes
+# ------------------------------------------------------------------------------------------------
+def stage_bytes(stats: dict, camera: bool):
+    """Compulsory HBM bytes of each stage of one sensor render (fp32): every input read once, every
+    output written once; the radix sort as one read + one write of (key 8 B + value 4 B)."""
+    N, V, I, P = stats["n_gaussians"], stats["n_visible"], stats["n_intersections"], stats["n_queries"]
+    T = stats["tiles_x"] * stats["tiles_y"]
+    b_out = 72 if camera else 80       # camera: 16 ch + alpha + count; lidar: 12 B ray in + 68 B out
+    b_gin = 68 if camera else 60
+    return {
+        "project": 48 * N + 48 * V + 64 * V + 16 * V + 4 * N,     # raw params in; geom + feat record, rect, count out
+        "scan": 4 * N + 8 * N,
+        "emit_keys": 12 * V + 8 * V + 12 * I,
+        "sort": 24 * I,
+        "tile_ranges": 8 * I + 8 * T,
+        "raster_fwd": 116 * I + 8 * T + P * b_out,
+        "raster_bwd": 116 * I + 8 * T + P * (b_out + b_gin) + 104 * V,
+        "project_bwd": 104 * V + 48 * V + 48 * N + 108 * N,
+    }
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU path (the oracle port of the reference's compose/project + SPEC tiling/rasterizer)
+# ------------------------------------------------------------------------------------------------
+class CpuFrame:
+    """One frame on the host cores with the reference's threading primitive (parallel_chunks, common.hpp:72-90)."""
+
+    def __init__(self, scene, quarter: bool):
+        from oracle import oracle_py as op
+        from paper_2411_16816_b200 import synth
+        from paper_2411_16816_b200.model import RasterSettings, RaySet
+        self.op, self.st = op, RasterSettings()
+        self.osc = op.OracleScene(scene, np.float32)
+        self.workers = max(1, op.hardware_threads())
+        lid, cam = frame_sensors(0)
+        rays = synth.grid_rays(lid)
+        if quarter:
+            # bounded sample: the middle quarter band of the image (rows 405..674: same intrinsics, principal point
+            # and rolling-shutter timing of those rows) and the first 15 of the 57 azimuth tile columns of the sweep
+            h = cam.height // 4
+            cam.cy = cam.cy - (cam.height - h) / 2.0
+            cam.height = h
+            cam.shutter_duration = cam.shutter_duration / 4.0
+            m_phi, m_omega = lid.grid()
+            keep = np.zeros(len(rays.begin), bool)
+            for row in range(m_omega):
+                keep[row * m_phi: row * m_phi + 15] = True
+            parts, begin, end, cur = [], [], [], 0
+            for t in range(len(rays.begin)):
+                begin.append(cur)
+                if keep[t]:
+                    seg = rays.rays[rays.begin[t]:rays.end[t]]
+                    parts.append(seg)
+                    cur += len(seg)
+                end.append(cur)
+            rays = RaySet(rays=np.concatenate(parts), begin=np.array(begin, np.int64), end=np.array(end, np.int64))
+        self.lid, self.cam, self.rays = lid, cam, rays
+        self.P_l, self.P_c = len(rays.rays), cam.width * cam.height
+        self.gl = synth.upstream(self.P_l, seed=11)
+        self.gl[0][:, 14:] = 0
+        self.gc = synth.upstream(self.P_c, seed=12)
+        self.sample = ("middle 1920x270 band of the camera image + 15 of 57 azimuth tile columns of the lidar sweep "
+                       f"({self.P_c} px + {self.P_l} rays), all 1M Gaussians projected") if quarter else \
+                      f"the full frame ({self.P_c} px + {self.P_l} rays)"
+
+    def step(self):
+        """returns (seconds lidar, seconds camera)"""
+        self.osc.zero_grads()
+        t0 = time.perf_counter()
+        v = self.osc.render_lidar(self.lid, self.rays, self.st, workers=self.workers)
+        v.backward(self.gl[0], self.gl[1], workers=self.workers)
+        t1 = time.perf_counter()
+        del v
+        t2 = time.perf_counter()
+        v = self.osc.render_camera(self.cam, self.st, workers=self.workers)
+        v.backward(self.gc[0], self.gc[1], workers=self.workers)
+        t3 = time.perf_counter()
+        del v
+        return t1 - t0, t3 - t2
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2411_16816_b200 import synth
+    scene = synth.make_scene(N_GAUSS, seed=SCENE_SEED)
+    total = args.steps + args.warmup
+    budget_s = 150.0
+    frame = CpuFrame(scene, quarter=False)
+    times, done = [], 0
+    t_first = None
+    if args.ref_sample != "quarter" and total > 0:
+        tl, tc = frame.step()
+        t_first = tl + tc
+        done = 1
+        if done > args.warmup:
+            times.append((tl, tc))
+    if args.ref_sample == "quarter" or (args.ref_sample == "auto" and t_first is not None and t_first * (total - 1) > budget_s):
+        # the full frame does not fit the time budget K + W times: restart on the bounded sample
+        frame = CpuFrame(scene, quarter=True)
+        times, done = [], 0
+    while done < total:
+        tl, tc = frame.step()
+        done += 1
+        if done > args.warmup:
+            times.append((tl, tc))
+    times = times[-args.steps:] if args.steps > 0 else []
+    tl = float(np.mean([a for a, _ in times])) if times else float("nan")
+    tc = float(np.mean([b for _, b in times])) if times else float("nan")
+    value = (frame.P_l + frame.P_c) / (tl + tc) / 1e6
+    cfg = workload_config(1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * (tl + tc), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+        "breakdown": {"lidar_mrays_s": frame.P_l / tl / 1e6, "camera_mpix_s": frame.P_c / tc / 1e6},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": frame.workers, "kind": "port", "sample": frame.sample,
+                         "note": "CPU oracle (restatement of scene.hpp/projection.hpp + SPEC tiling/rasterizer; the reference "
+                                 "headers need Eigen, which is not vendored), fp32, parallel_chunks over all host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------
+# the sm_100a path
+# ------------------------------------------------------------------------------------------------
+def pinned(shape, dtype):
+    import torch
+    t = torch.empty(shape, dtype=dtype, pin_memory=True)
+    return t, t.numpy()
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_16816_b200 import api, synth
+    from paper_2411_16816_b200.model import RasterSettings, Scene
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the sm_100a path has no CPU fallback; use --impl reference for the CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(device=dev)
+    st = RasterSettings()
+
+    with torch.cuda.stream(stream):
+        ctx = api.Context(local, stream.cuda_stream)
+        scene = synth.make_scene(N_GAUSS, seed=SCENE_SEED)
+        # host-side (pinned) copy of the GaussianSet: the e2e path uploads it every step
+        keep, arrs = [], []
+        for a in (scene.mean, scene.scale_log, scene.quat, scene.opacity_logit, scene.color, scene.feature):
+            t, v = pinned(a.shape, torch.float32)
+            v[...] = a
+            keep.append(t); arrs.append(v)
+        t_id, v_id = pinned(scene.actor_id.shape, torch.int32)
+        v_id[...] = scene.actor_id
+        keep.append(t_id)
+        pscene = Scene(*arrs, v_id, [])
+        ctx.upload_scene(pscene)
+        n_grad = ctx.grads_size
+        grads_t = torch.zeros(n_grad, dtype=torch.float32, device=dev)
+        ctx.bind_grads_device(grads_t.data_ptr(), n_grad)
+
+        lid, cam = frame_sensors(rank)
+        rays = synth.grid_rays(lid)
+        vl = ctx.lidar_view(lid, rays, st)
+        vc = ctx.camera_view(cam, st)
+        P_l, P_c = vl.P, vc.P
+        # upstream gradients: N(0,1) (seeded), pinned on the host and resident on the device
+        g_host, g_dev = {}, {}
+        for name, P, seed in (("l", P_l, 11), ("c", P_c, 12)):
+            gb, ga = synth.upstream(P, seed=seed)
+            if name == "l":
+                gb[:, 14:] = 0
+            tb, vb = pinned(gb.shape, torch.float32); vb[...] = gb
+            ta, va = pinned(ga.shape, torch.float32); va[...] = ga
+            g_host[name] = (tb, ta, vb, va)
+            g_dev[name] = (tb.to(dev, non_blocking=True), ta.to(dev, non_blocking=True))
+        # pinned host outputs of the e2e path
+        out_host = {}
+        for name, P in (("l", P_l), ("c", P_c)):
+            tb, vb = pinned((P, 16), torch.float32)
+            ta, va = pinned((P,), torch.float32)
+            tn, vn = pinned((P,), torch.int32)
+            out_host[name] = (tb, ta, tn, vb, va, vn)
+        gh_t, gh = pinned((n_grad,), torch.float32)
+        n = N_GAUSS
+        gh_parts = [gh[0:3 * n], gh[3 * n:6 * n], gh[6 * n:10 * n], gh[10 * n:11 * n], gh[11 * n:14 * n], gh[14 * n:]]
+        stream.synchronize()
+
+        def barrier():
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+
+        def step_device():
+            """inputs resident in HBM: scene, rays, upstream gradients"""
+            ctx.zero_grads()
+            vl.forward(0.0)
+            vl.backward_device(g_dev["l"][0].data_ptr(), g_dev["l"][1].data_ptr())
+            vc.forward(0.0)
+            vc.backward_device(g_dev["c"][0].data_ptr(), g_dev["c"][1].data_ptr())
+            if world > 1:
+                dist.all_reduce(grads_t)
+
+        def step_e2e():
+            """the reference-facing call with HOST buffers: GaussianSet up, rendered images down, upstream
+            gradients up, SceneParamGrads down — all inside the timed region, from/to pinned memory"""
+            ctx.upload_scene(pscene)
+            ctx.zero_grads()
+            for name, v in (("l", vl), ("c", vc)):
+                v.forward(0.0)
+                _, _, _, vb, va, vn = out_host[name]
+                v.download(vb, va, vn)
+                _, _, gb, ga = g_host[name]
+                v.backward_host_async(gb, ga)
+            if world > 1:
+                dist.all_reduce(grads_t)
+            ctx.grads_into(*gh_parts)
+
+        def timed(fn, steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            t0 = time.time()
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+            barrier()
+            t1 = time.time()
+            ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            return float(ms.item()), t0, t1
+
+        # ---- device-resident timing ------------------------------------------------------------
+        for _ in range(max(args.warmup, 0)):
+            step_device()
+        ctx.set_profiling(True)
+        l0, ll0 = ctx.launch_count, ctx.library_launch_count
+        sampler = ClockSampler(local) if rank == 0 else None
+        ms_dev, t0, t1 = timed(step_device, args.steps)
+        clocks = sampler.stop(t0, t1) if sampler else None
+        launches, lib_launches = ctx.launch_count - l0, ctx.library_launch_count - ll0
+        stage_l, stage_c = vl.stage_ms(), vc.stage_ms()
+        ctx.set_profiling(False)
+        stats_l, stats_c = vl.stats(), vc.stats()
+
+        # per-sensor rates (each sensor's fwd+bwd timed alone, device-resident)
+        def only(v, g):
+            def f():
+                v.forward(0.0)
+                v.backward_device(g[0].data_ptr(), g[1].data_ptr())
+            return f
+        k_br = max(1, min(args.steps, 5))
+        ms_l, _, _ = timed(only(vl, g_dev["l"]), k_br)
+        ms_c, _, _ = timed(only(vc, g_dev["c"]), k_br)
+
+        # ---- end to end through the host-buffer API -------------------------------------------
+        for _ in range(min(max(args.warmup, 1), 3)):
+            step_e2e()
+        ms_e2e, _, _ = timed(step_e2e, args.steps)
+        checksum = float(np.abs(gh[:1024]).sum())   # the downloaded result is really there
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    queries = (P_l + P_c) * world
+    per_step = ms_dev / args.steps
+    value = queries / (per_step * 1e-3) / 1e6
+    e2e_value = queries / (ms_e2e / args.steps * 1e-3) / 1e6
+    h2d = 112 * N_GAUSS + 68 * (P_l + P_c)
+    d2h = 72 * (P_l + P_c) + 4 * n_grad
+
+    # roofline of the dominant kernel
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    cand = []
+    for sensor, stg, sts, camera in (("lidar", stage_l, stats_l, False), ("camera", stage_c, stats_c, True)):
+        by = stage_bytes(sts, camera)
+        for k, ms in stg.items():
+            cand.append((ms, sensor, k, by[k]))
+    cand.sort(reverse=True)
+    ms_k, sensor_k, stage_k, bytes_k = cand[0]
+    kernel_name = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project", "project_bwd": "k_project_bwd",
+                   "emit_keys": "k_emit_keys", "sort": "cub::DeviceRadixSort", "scan": "cub::DeviceScan",
+                   "tile_ranges": "k_tile_ranges"}[stage_k] + ("<camera>" if sensor_k == "camera" else "<lidar>")
+    achieved = bytes_k / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")   # per-launch dram bytes from the committed ncu --set full capture
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(kernel_name)
+        except Exception:
+            traffic = None
+    stage_total = sum(stage_l.values()) + sum(stage_c.values())
+    frame_bytes = sum(stage_bytes(stats_l, False).values()) + sum(stage_bytes(stats_c, True).values())
+    roofline = {
+        "bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+        "kernel_ms": ms_k, "kernel_bytes": bytes_k, "kernel_share_of_step": ms_k / stage_total if stage_total else None,
+        "frame_algorithmic_bytes": frame_bytes, "frame_frac": frame_bytes / (per_step * 1e-3) / 1e9 / peak,
+        "stage_ms": {"lidar": stage_l, "camera": stage_c},
+        "note": "compositing is fp32-issue bound (~120 flop/B, SURVEY.md §8(d)), so its HBM fraction is low by construction; "
+                "frame_frac = algorithmic bytes of the whole frame / step time / peak",
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(world),
+        "breakdown": {"lidar_mrays_s": P_l / (ms_l / k_br * 1e-3) / 1e6, "camera_mpix_s": P_c / (ms_c / k_br * 1e-3) / 1e6,
+                      "lidar_ms": ms_l / k_br, "camera_ms": ms_c / k_br,
+                      "lidar": stats_l, "camera": stats_c},
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": ms_e2e / args.steps, "result_checksum": checksum},
+        "gpu_launches": launches, "library_launches": lib_launches,
+        "roofline": roofline,
+    }
+
+    if world == 1 and not args.no_cpu:
+        fr = CpuFrame(scene, quarter=False)
+        tl, tc = fr.step()
+        line["cpu_baseline"] = {"value": (fr.P_l + fr.P_c) / (tl + tc) / 1e6, "unit": UNIT, "cores": fr.workers, "kind": "port",
+                                "sample": fr.sample + ", one run", "lidar_mrays_s": fr.P_l / tl / 1e6,
+                                "camera_mpix_s": fr.P_c / tc / 1e6, "seconds": tl + tc}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-sample", default="auto", choices=["auto", "full", "quarter"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -97,8 +97,18 @@ int splatb200_ctx_create(int device, void* cuda_stream /* cudaStream_t or NULL *
 void splatb200_ctx_destroy(splatb200_ctx* ctx);
 const char* splatb200_last_error(const splatb200_ctx* ctx); /* ctx may be NULL: last create error */
 int splatb200_ctx_sync(splatb200_ctx* ctx);
-/* number of kernels launched by this ctx since creation (bench.py's gpu_launches) */
+/* number of hand-written kernels launched by this ctx since creation (bench.py's gpu_launches), and
+ * the number of library (CUB scan / radix sort) kernels launched beside them */
 int64_t splatb200_ctx_launch_count(const splatb200_ctx* ctx);
+int64_t splatb200_ctx_library_launch_count(const splatb200_ctx* ctx);
+/* per-stage CUDA-event timing on the ctx stream (off by default). Stages: 0 project, 1 scan, 2 emit_keys,
+ * 3 sort, 4 tile_ranges, 5 raster_fwd, 6 raster_bwd, 7 project_bwd. set_profiling(1) resets the running
+ * sums; stage_ms returns the MEAN milliseconds per launch of each stage over every forward / backward of
+ * the view since then (syncs). Event pairs are folded into the sums at the forward pass's own
+ * synchronisation point, so enabling profiling adds no host-device synchronisation to a timed region.
+ * This is the measurement hook bench.py's roofline uses. */
+int splatb200_ctx_set_profiling(splatb200_ctx* ctx, int32_t on);
+int splatb200_view_stage_ms(splatb200_view* v, float out_ms[8]);
 
 /* ---- scene: GaussianSet + SceneGraph (scene.hpp:11-45, 171-187) ------------------------------ */
 /* host arrays are copied to the device; actor_id is validated lazily against the tracks at

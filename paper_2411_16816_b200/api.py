@@ -27,7 +27,8 @@ INT_ARRAYS = {"source_index", "rect", "isect_tile", "isect_depth_bits", "isect_s
 # every symbol include/splat_b200.h declares
 SYMBOLS = [
     "splatb200_ctx_create", "splatb200_ctx_destroy", "splatb200_last_error", "splatb200_ctx_sync",
-    "splatb200_ctx_launch_count", "splatb200_scene_upload", "splatb200_scene_bind_device",
+    "splatb200_ctx_launch_count", "splatb200_ctx_library_launch_count",
+    "splatb200_ctx_set_profiling", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_bind_device",
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
@@ -86,13 +87,17 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.splatb200_last_error.restype = C.c_char_p
         L.splatb200_last_error.argtypes = [C.c_void_p]
-        for n in ("splatb200_ctx_launch_count", "splatb200_grads_size", "splatb200_view_array"):
+        for n in ("splatb200_ctx_launch_count", "splatb200_ctx_library_launch_count", "splatb200_grads_size",
+                  "splatb200_view_array"):
             getattr(L, n).restype = C.c_int64
         for n in ("splatb200_grads_device_ptr", "splatb200_view_blend", "splatb200_view_alpha", "splatb200_view_n_contrib"):
             getattr(L, n).restype = C.c_void_p
         L.splatb200_ctx_destroy.restype = None
         L.splatb200_view_destroy.restype = None
         L.splatb200_ctx_launch_count.argtypes = [C.c_void_p]
+        L.splatb200_ctx_library_launch_count.argtypes = [C.c_void_p]
+        L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
+        L.splatb200_view_stage_ms.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_grads_size.argtypes = [C.c_void_p]
         L.splatb200_grads_device_ptr.argtypes = [C.c_void_p]
         L.splatb200_ctx_destroy.argtypes = [C.c_void_p]
@@ -202,6 +207,13 @@ class Context:
     def launch_count(self) -> int:
         return int(self.L.splatb200_ctx_launch_count(self.h))
 
+    @property
+    def library_launch_count(self) -> int:
+        return int(self.L.splatb200_ctx_library_launch_count(self.h))
+
+    def set_profiling(self, on: bool):
+        self._check(self.L.splatb200_ctx_set_profiling(self.h, int(on)))
+
     # ---- SceneGraph ---------------------------------------------------------------------------
     def upload_scene(self, scene: Scene):
         s = scene.astype(np.float32)
@@ -254,6 +266,11 @@ class Context:
 
     def bind_grads_device(self, ptr: int, n_floats: int):
         self._check(self.L.splatb200_grads_bind_device(self.h, C.c_void_p(ptr), n_floats))
+
+    def grads_into(self, d_mean, d_scale_log, d_quat, d_opacity_logit, d_color, d_feature):
+        """Download SceneParamGrads into caller-owned (e.g. pinned) float32 arrays; None skips a group."""
+        self._check(self.L.splatb200_grads_download(self.h, _p(d_mean), _p(d_scale_log), _p(d_quat), _p(d_opacity_logit),
+                                                    _p(d_color), _p(d_feature)))
 
     def grads(self):
         n, d_f = self.n, self.d_f
@@ -322,6 +339,13 @@ class View:
 
     def forward(self, t_scene=0.0, stop_after=0):
         self.ctx._check(self.L.splatb200_view_forward(self.h, C.c_float(t_scene), stop_after))
+
+    STAGES = ("project", "scan", "emit_keys", "sort", "tile_ranges", "raster_fwd", "raster_bwd", "project_bwd")
+
+    def stage_ms(self) -> dict:
+        out = np.zeros(8, np.float32)
+        self.ctx._check(self.L.splatb200_view_stage_ms(self.h, _p(out)))
+        return dict(zip(self.STAGES, out.astype(float).tolist()))
 
     def stats(self) -> dict:
         s = StatsPOD()

@@ -27,7 +27,9 @@ struct splatb200_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string err;
-  int64_t launches = 0;
+  int64_t launches = 0;      // hand-written kernels
+  int64_t lib_launches = 0;  // CUB scan / radix-sort kernels
+  bool profiling = false;
 
   // scene
   int64_t n = 0;
@@ -106,6 +108,11 @@ struct splatb200_view {
   int stage = 0;  // 0 nothing, 1 projected, 2 sorted, 3 rasterized
   float t_scene = 0.0f;
   int64_t* h_total = nullptr;  // pinned
+  // per-stage CUDA events (ctx profiling): project, scan, emit_keys, sort, tile_ranges, raster_fwd, raster_bwd, project_bwd
+  cudaEvent_t ev[8][2] = {};
+  bool ev_valid[8] = {};   // recorded, not yet harvested
+  double ev_sum_ms[8] = {};
+  int64_t ev_count[8] = {};
 
   const uint64_t* keys() const { return sorted_sel ? keys1 : keys0; }
   const uint32_t* vals() const { return sorted_sel ? vals1 : vals0; }
@@ -183,7 +190,40 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
+  for (auto& e : v->ev)
+    for (auto& x : e)
+      if (x) { cudaEventDestroy(x); x = nullptr; }
 }
+
+// Fold every recorded-and-completed event pair into the running sums. Only called right after a
+// stream synchronisation, so cudaEventElapsedTime never blocks and the timed region is not perturbed.
+void harvest_stage_events(splatb200_view* v) {
+  for (int k = 0; k < 8; ++k) {
+    if (!v->ev_valid[k]) continue;
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, v->ev[k][0], v->ev[k][1]) == cudaSuccess) {
+      v->ev_sum_ms[k] += ms;
+      v->ev_count[k] += 1;
+    }
+    v->ev_valid[k] = false;
+  }
+}
+
+struct StageTimer {
+  splatb200_view* v;
+  int stage;
+  StageTimer(splatb200_view* view, int st) : v(view), stage(st) {
+    if (!v->ctx->profiling) return;
+    for (int k = 0; k < 2; ++k)
+      if (!v->ev[stage][k]) cudaEventCreate(&v->ev[stage][k]);
+    cudaEventRecord(v->ev[stage][0], v->ctx->stream);
+  }
+  ~StageTimer() {
+    if (!v->ctx->profiling) return;
+    cudaEventRecord(v->ev[stage][1], v->ctx->stream);
+    v->ev_valid[stage] = true;
+  }
+};
 
 int ensure_source_buffers(splatb200_view* v) {
   splatb200_ctx* c = v->ctx;
@@ -304,21 +344,47 @@ extern "C" int splatb200_ctx_sync(splatb200_ctx* c) {
 
 extern "C" int64_t splatb200_ctx_launch_count(const splatb200_ctx* c) { return c->launches; }
 
+extern "C" int64_t splatb200_ctx_library_launch_count(const splatb200_ctx* c) { return c->lib_launches; }
+
+extern "C" int splatb200_ctx_set_profiling(splatb200_ctx* c, int32_t on) {
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  c->profiling = on != 0;
+  for (auto* v : c->views)
+    for (int k = 0; k < 8; ++k) { v->ev_valid[k] = false; v->ev_sum_ms[k] = 0.0; v->ev_count[k] = 0; }
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_stage_ms(splatb200_view* v, float out_ms[8]) {
+  splatb200_ctx* c = v->ctx;
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  harvest_stage_events(v);
+  for (int k = 0; k < 8; ++k) out_ms[k] = v->ev_count[k] ? (float)(v->ev_sum_ms[k] / (double)v->ev_count[k]) : 0.0f;
+  return SPLATB200_OK;
+}
+
 // ---- scene --------------------------------------------------------------------------------------
 extern "C" int splatb200_scene_upload(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
                                       const float* quat, const float* opacity_logit, const float* color,
                                       const float* feature, const int32_t* actor_id) {
   if (n < 0 || d_f < 0 || d_f > 13) return c->fail(SPLATB200_EINVAL, "scene_upload: need n >= 0 and 0 <= d_f <= 13");
   CU_TRY(c, cudaSetDevice(c->device));
-  CU_TRY(c, cudaStreamSynchronize(c->stream));
-  free_scene(c);
-  c->n = n;
-  c->d_f = d_f;
-  c->owns_scene = true;
+  // Same shape as the resident scene (the per-iteration case: parameters change, sizes do not): keep the
+  // device buffers and the SceneParamGrads buffer (owned or bound), only refresh the contents.
+  const bool reuse = c->owns_scene && c->n == n && c->d_f == d_f && c->grads;
+  if (!reuse) {
+    CU_TRY(c, cudaStreamSynchronize(c->stream));
+    free_scene(c);
+    c->n = n;
+    c->d_f = d_f;
+    c->owns_scene = true;
+  }
   const size_t m = (size_t)std::max<int64_t>(1, n);
   auto up = [&](float*& dst, const float* src, int width) -> cudaError_t {
-    cudaError_t e = cudaMalloc(&dst, sizeof(float) * m * (size_t)std::max(1, width));
-    if (e != cudaSuccess || n == 0 || width == 0) return e;
+    if (!reuse) {
+      cudaError_t e = cudaMalloc(&dst, sizeof(float) * m * (size_t)std::max(1, width));
+      if (e != cudaSuccess) return e;
+    }
+    if (n == 0 || width == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, sizeof(float) * (size_t)n * width, cudaMemcpyHostToDevice, c->stream);
   };
   CU_TRY(c, up(c->mean, mean, 3));
@@ -327,15 +393,16 @@ extern "C" int splatb200_scene_upload(splatb200_ctx* c, int64_t n, int32_t d_f, 
   CU_TRY(c, up(c->opacity_logit, opacity_logit, 1));
   CU_TRY(c, up(c->color, color, 3));
   CU_TRY(c, up(c->feature, feature, d_f));
-  CU_TRY(c, cudaMalloc(&c->actor_id, sizeof(int32_t) * m));
+  if (!reuse) CU_TRY(c, cudaMalloc(&c->actor_id, sizeof(int32_t) * m));
   if (n) CU_TRY(c, cudaMemcpyAsync(c->actor_id, actor_id, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
   c->actor_first.clear();
   for (int64_t i = 0; i < n; ++i)
     if (actor_id[i] != 0) c->actor_first.emplace(actor_id[i], i);
   c->bound_max_actor = 0;
+  // host arrays are borrowed for the duration of the call only (pageable or pinned)
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   for (auto* v : c->views) v->stage = 0;
-  return alloc_grads(c);
+  return reuse ? SPLATB200_OK : alloc_grads(c);
 }
 
 extern "C" int splatb200_scene_bind_device(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean,
@@ -628,14 +695,21 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   const SceneDev sc = c->scene_dev(v->d_actors);
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, st));
 
-  launch_project(v->s, sc, v->proj, st);
+  {
+    StageTimer tm(v, 0);
+    launch_project(v->s, sc, v->proj, st);
+  }
   CHECK_LAUNCH(c, "k_project");
   c->launches += c->n > 0;
-  launch_scan_counts(v->proj.count, v->offsets, c->n, v->scan_temp, v->scan_temp_bytes, st);
+  {
+    StageTimer tm(v, 1);
+    launch_scan_counts(v->proj.count, v->offsets, c->n, v->scan_temp, v->scan_temp_bytes, st);
+  }
   CHECK_LAUNCH(c, "scan");
-  c->launches += 2;
+  c->lib_launches += 2;
   CU_TRY(c, cudaMemcpyAsync(v->h_total, v->offsets + c->n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaStreamSynchronize(st));
+  if (c->profiling) harvest_stage_events(v);  // previous step's events have all completed by now
   v->I = *v->h_total;
   v->stage = 1;
   if (stop_after == 1) return SPLATB200_OK;
@@ -643,26 +717,37 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   rc = ensure_isect_capacity(v, v->I);
   if (rc) return rc;
 
-  launch_emit_keys(c->n, v->I, v->offsets, v->proj, v->s.tiles_x, v->s.is_camera ? 0 : 1, v->keys0, v->vals0, st);
+  {
+    StageTimer tm(v, 2);
+    launch_emit_keys(c->n, v->I, v->offsets, v->proj, v->s.tiles_x, v->s.is_camera ? 0 : 1, v->keys0, v->vals0, st);
+  }
   CHECK_LAUNCH(c, "k_emit_keys");
+  c->launches += v->I > 0;
   int tile_bits = 1;
   while ((1LL << tile_bits) < v->n_tiles) ++tile_bits;
   v->sorted_sel = 0;
   if (v->I > 0) {
+    StageTimer tm(v, 3);
     v->sorted_sel = launch_sort_pairs(v->keys0, v->keys1, v->vals0, v->vals1, v->I, 32 + tile_bits, v->sort_temp,
                                       v->sort_temp_bytes, st);
     CHECK_LAUNCH(c, "radix sort");
-    c->launches += 1 + 2 + (32 + tile_bits + 7) / 8;
+    c->lib_launches += 1 + 2 + (32 + tile_bits + 7) / 8;
   }
   CU_TRY(c, cudaMemsetAsync(v->tile_begin, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
   CU_TRY(c, cudaMemsetAsync(v->tile_end, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
-  launch_tile_ranges(v->I, v->keys(), v->tile_begin, v->tile_end, st);
+  {
+    StageTimer tm(v, 4);
+    launch_tile_ranges(v->I, v->keys(), v->tile_begin, v->tile_end, st);
+  }
   CHECK_LAUNCH(c, "k_tile_ranges");
   c->launches += v->I > 0;
   v->stage = 2;
   if (stop_after == 2) return SPLATB200_OK;
 
-  launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out, st);
+  {
+    StageTimer tm(v, 5);
+    launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out, st);
+  }
   CHECK_LAUNCH(c, "k_raster_fwd");
   c->launches += 1;
   v->stage = 3;
@@ -699,12 +784,16 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
   RasterGradDev rg{v->rg};
   const ParamGradDev pg = c->pg();
   if (v->I > 0) {
+    StageTimer tm(v, 6);
     launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out,
                       g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
     CHECK_LAUNCH(c, "k_raster_bwd");
     c->launches += 1;
   }
-  launch_project_bwd(v->s, c->scene_dev(v->d_actors), v->proj, rg, pg, v->sensor_grads, v->actor_acc, st);
+  {
+    StageTimer tm(v, 7);
+    launch_project_bwd(v->s, c->scene_dev(v->d_actors), v->proj, rg, pg, v->sensor_grads, v->actor_acc, st);
+  }
   CHECK_LAUNCH(c, "k_project_bwd");
   c->launches += c->n > 0;
   if (!c->tracks.empty()) v->actor_pending = true;
