@@ -185,6 +185,33 @@ int splatb200_view_sensor_grads(splatb200_view* v, splatb200_sensor_grads* out);
 int splatb200_view_download(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib);
 int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, const float* g_alpha);
 
+/* ---- reference-granularity entry points --------------------------------------------------------
+ * One call per function the reference ships as code, HOST buffers in and out, for callers that switch
+ * function by function (include/splat_b200.hpp wraps them in the reference's own types). All need a
+ * forward(stop_after >= 1) on the view first; none is on the hot path. */
+/* ComposedScene (scene.hpp:261-271) of compose_at_time (scene.hpp:273-308): N rows each, cov_w 9 floats
+ * row-major; any pointer may be NULL */
+int splatb200_view_composed(splatb200_view* v, float* mean_w, float* cov_w, float* vel_dyn_w, float* opacity);
+/* std::vector<ProjectedGaussian> of project_camera / project_lidar (projection.hpp:28-40, 88-118, 140-174),
+ * ascending source_index. Returns V (call with NULLs to size). fields25 per entry: mean2d 2, depth_key,
+ * cov2d 4 row-major, velocity 3, aabb lo 2 + hi 2, conic 4 row-major, det_ratio, mu_sensor 3, rel_vel_sensor 3 */
+int64_t splatb200_view_projected(splatb200_view* v, int64_t* source_index, float* fields25);
+/* project_camera_backward / project_lidar_backward (projection.hpp:250-288, 322-357) over projected positions
+ * [begin, end). g_mean2d (2), g_range (1), g_cov2d (4 row-major), g_velocity (3) have V rows indexed by projected
+ * POSITION k, exactly what the shipped consumers read (projection.hpp:257-268, 329-344); NULL = zeros.
+ * ComposeGrads (scene.hpp:313-323) g_mean_w (3), g_cov_w (9), g_vel_dyn_w (3) have N rows by source index and are
+ * ACCUMULATED (+=); SensorGrads d_vel_lin / d_vel_ang accumulate in the view (splatb200_view_sensor_grads). */
+int splatb200_view_project_backward(splatb200_view* v, const float* g_mean2d, const float* g_range, const float* g_cov2d,
+                                    const float* g_velocity, int64_t begin, int64_t end, float* g_mean_w, float* g_cov_w,
+                                    float* g_vel_dyn_w);
+/* compose_backward (scene.hpp:386-458) over source indices [begin, end): ComposeGrads + g_opacity (activated,
+ * N rows) in, accumulated into the ctx's SceneParamGrads (d_mean, d_scale_log, d_quat, d_opacity_logit, ActorGrad) */
+int splatb200_view_compose_backward(splatb200_view* v, const float* g_mean_w, const float* g_cov_w, const float* g_vel_dyn_w,
+                                    const float* g_opacity, int64_t begin, int64_t end);
+/* both fused over the whole projected list: ProjectedGrads (projection.hpp:178-205) -> SceneParamGrads */
+int splatb200_view_backward_projected(splatb200_view* v, const float* g_mean2d, const float* g_range, const float* g_cov2d,
+                                      const float* g_velocity, const float* g_opacity);
+
 /* Introspection for parity tests: copy a named intermediate to host. Returns the element count
  * (call with dst = NULL to size), or a negative error. int64 arrays: source_index, rect (x0,x1,y0,y1
  * per visible Gaussian, un-wrapped), isect_tile, isect_depth_bits, isect_src, tile_begin, tile_end,

@@ -35,7 +35,8 @@ SYMBOLS = [
     "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
-    "splatb200_view_backward_host", "splatb200_view_array",
+    "splatb200_view_backward_host", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
+    "splatb200_view_project_backward", "splatb200_view_compose_backward", "splatb200_view_backward_projected",
 ]
 
 
@@ -107,6 +108,12 @@ def lib():
         for n in ("splatb200_view_blend", "splatb200_view_alpha", "splatb200_view_n_contrib"):
             getattr(L, n).argtypes = [C.c_void_p]
         L.splatb200_view_array.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        L.splatb200_view_projected.restype = C.c_int64
+        L.splatb200_view_projected.argtypes = [C.c_void_p] * 3
+        L.splatb200_view_composed.argtypes = [C.c_void_p] * 5
+        L.splatb200_view_project_backward.argtypes = [C.c_void_p] * 5 + [C.c_int64, C.c_int64] + [C.c_void_p] * 3
+        L.splatb200_view_compose_backward.argtypes = [C.c_void_p] * 5 + [C.c_int64, C.c_int64]
+        L.splatb200_view_backward_projected.argtypes = [C.c_void_p] * 6
         L.splatb200_view_forward.argtypes = [C.c_void_p, C.c_float, C.c_int32]
         L.splatb200_view_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_backward_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -382,6 +389,45 @@ class View:
 
     def download(self, blend16=None, alpha=None, n_contrib=None):
         self.ctx._check(self.L.splatb200_view_download(self.h, _p(blend16), _p(alpha), _p(n_contrib)))
+
+    # ---- reference-granularity calls (host buffers) ----------------------------------------------
+    PROJECTED_FIELDS = (("mean2d", 0, 2), ("depth_key", 2, 1), ("cov2d", 3, 4), ("velocity", 7, 3), ("aabb", 10, 4),
+                        ("conic", 14, 4), ("det_ratio", 18, 1), ("mu_sensor", 19, 3), ("rel_vel_sensor", 22, 3))
+
+    def projected(self) -> dict:
+        """project_camera / project_lidar result: dict of arrays, V rows in ascending source_index."""
+        V = self.ctx._check(self.L.splatb200_view_projected(self.h, None, None))
+        src, f = np.zeros(V, np.int64), np.zeros((V, 25), np.float32)
+        self.ctx._check(self.L.splatb200_view_projected(self.h, _p(src), _p(f)))
+        out = {"source_index": src}
+        for name, off, w in self.PROJECTED_FIELDS:
+            out[name] = f[:, off:off + w].copy()
+        return out
+
+    def composed(self) -> dict:
+        n = self.ctx.n
+        out = dict(mean_w=np.zeros((n, 3), np.float32), cov_w=np.zeros((n, 9), np.float32),
+                   vel_dyn_w=np.zeros((n, 3), np.float32), opacity=np.zeros(n, np.float32))
+        self.ctx._check(self.L.splatb200_view_composed(self.h, _p(out["mean_w"]), _p(out["cov_w"]), _p(out["vel_dyn_w"]),
+                                                       _p(out["opacity"])))
+        return out
+
+    def project_backward(self, g_mean2d, g_range, g_cov2d, g_velocity, begin, end, compose_grads: dict):
+        """project_*_backward over projected positions [begin, end); accumulates into compose_grads (N-row arrays)."""
+        a = [None if x is None else _f32(x) for x in (g_mean2d, g_range, g_cov2d, g_velocity)]
+        cg = compose_grads
+        self.ctx._check(self.L.splatb200_view_project_backward(self.h, *[_p(x) for x in a], begin, end, _p(cg["g_mean_w"]),
+                                                               _p(cg["g_cov_w"]), _p(cg["g_vel_dyn_w"])))
+
+    def compose_backward(self, compose_grads: dict, g_opacity, begin, end):
+        cg = compose_grads
+        go = None if g_opacity is None else _f32(g_opacity)
+        self.ctx._check(self.L.splatb200_view_compose_backward(self.h, _p(cg["g_mean_w"]), _p(cg["g_cov_w"]),
+                                                               _p(cg["g_vel_dyn_w"]), _p(go), begin, end))
+
+    def backward_projected(self, g_mean2d, g_range, g_cov2d, g_velocity, g_opacity):
+        a = [None if x is None else _f32(x) for x in (g_mean2d, g_range, g_cov2d, g_velocity, g_opacity)]
+        self.ctx._check(self.L.splatb200_view_backward_projected(self.h, *[_p(x) for x in a]))
 
     def sensor_grads(self):
         s = SensorGradsPOD()

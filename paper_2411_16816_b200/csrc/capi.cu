@@ -834,6 +834,192 @@ extern "C" int splatb200_view_backward_host(splatb200_view* v, const float* g_bl
   return splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
 }
 
+// ---- reference-granularity entry points ------------------------------------------------------------
+// The functions the reference ships as code, one call each, HOST buffers in and out. Not the hot path
+// (the fused forward/backward above is); these exist so that a caller written against
+// splat/scene.hpp + splat/projection.hpp can switch function by function (include/splat_b200.hpp).
+namespace {
+
+int visible_list(splatb200_view* v, std::vector<int64_t>& vis) {
+  splatb200_ctx* c = v->ctx;
+  std::vector<uint32_t> cnt((size_t)c->n);
+  if (c->n) CU_TRY(c, cudaMemcpyAsync(cnt.data(), v->proj.count, sizeof(uint32_t) * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  vis.clear();
+  for (size_t i = 0; i < cnt.size(); ++i)
+    if (cnt[i]) vis.push_back((int64_t)i);
+  return SPLATB200_OK;
+}
+
+struct DevScratch {
+  float* p = nullptr;
+  ~DevScratch() { if (p) cudaFree(p); }
+};
+
+int run_dump(splatb200_view* v, std::vector<float>& h) {
+  splatb200_ctx* c = v->ctx;
+  const size_t N = (size_t)c->n;
+  DevScratch d;
+  CU_TRY(c, cudaMalloc(&d.p, sizeof(float) * kDumpStride * std::max<size_t>(1, N)));
+  CU_TRY(c, cudaMemsetAsync(d.p, 0, sizeof(float) * kDumpStride * N, c->stream));
+  launch_project_dump(v->s, c->scene_dev(v->d_actors), d.p, c->stream);
+  CHECK_LAUNCH(c, "k_project_dump");
+  h.resize((size_t)kDumpStride * N);
+  if (N) CU_TRY(c, cudaMemcpyAsync(h.data(), d.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
+}  // namespace
+
+extern "C" int splatb200_view_composed(splatb200_view* v, float* mean_w, float* cov_w, float* vel_dyn_w, float* opacity) {
+  splatb200_ctx* c = v->ctx;
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "view_composed before forward");
+  std::vector<float> h;
+  int rc = run_dump(v, h);
+  if (rc) return rc;
+  for (int64_t i = 0; i < c->n; ++i) {
+    const float* o = &h[(size_t)kDumpStride * i];
+    if (opacity) opacity[i] = o[26];
+    for (int k = 0; k < 3; ++k) {
+      if (mean_w) mean_w[3 * i + k] = o[27 + k];
+      if (vel_dyn_w) vel_dyn_w[3 * i + k] = o[30 + k];
+    }
+    if (cov_w) for (int k = 0; k < 9; ++k) cov_w[9 * i + k] = o[33 + k];
+  }
+  return SPLATB200_OK;
+}
+
+extern "C" int64_t splatb200_view_projected(splatb200_view* v, int64_t* source_index, float* fields25) {
+  splatb200_ctx* c = v->ctx;
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "view_projected before forward");
+  std::vector<int64_t> vis;
+  int rc = visible_list(v, vis);
+  if (rc) return rc;
+  if (source_index) std::memcpy(source_index, vis.data(), sizeof(int64_t) * vis.size());
+  if (fields25) {
+    std::vector<float> h;
+    rc = run_dump(v, h);
+    if (rc) return rc;
+    for (size_t k = 0; k < vis.size(); ++k) std::memcpy(fields25 + 25 * k, &h[(size_t)kDumpStride * vis[k] + 1], sizeof(float) * 25);
+  }
+  return (int64_t)vis.size();
+}
+
+namespace {
+
+// scatter ProjectedGrads rows [begin, end) (indexed by projected position) to source index and upload
+int upload_projected_grads(splatb200_view* v, const std::vector<int64_t>& vis, int64_t begin, int64_t end, const float* g_mean2d,
+                           const float* g_range, const float* g_cov2d, const float* g_velocity, const float* g_opacity,
+                           DevScratch& d) {
+  splatb200_ctx* c = v->ctx;
+  const size_t N = (size_t)c->n;
+  std::vector<float> h((size_t)kProjGradStride * std::max<size_t>(1, N), 0.0f);
+  for (int64_t k = begin; k < end; ++k) {
+    float* q = &h[(size_t)kProjGradStride * vis[k]];
+    if (g_mean2d) { q[0] = g_mean2d[2 * k]; q[1] = g_mean2d[2 * k + 1]; }
+    if (g_range) q[2] = g_range[k];
+    if (g_cov2d) for (int e = 0; e < 4; ++e) q[3 + e] = g_cov2d[4 * k + e];
+    if (g_velocity) for (int e = 0; e < 3; ++e) q[7 + e] = g_velocity[3 * k + e];
+  }
+  if (g_opacity) for (size_t i = 0; i < N; ++i) h[(size_t)kProjGradStride * i + 10] = g_opacity[i];
+  CU_TRY(c, cudaMalloc(&d.p, sizeof(float) * h.size()));
+  CU_TRY(c, cudaMemcpyAsync(d.p, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));  // h is a local
+  return SPLATB200_OK;
+}
+
+}  // namespace
+
+extern "C" int splatb200_view_project_backward(splatb200_view* v, const float* g_mean2d, const float* g_range,
+                                               const float* g_cov2d, const float* g_velocity, int64_t begin, int64_t end,
+                                               float* g_mean_w, float* g_cov_w, float* g_vel_dyn_w) {
+  splatb200_ctx* c = v->ctx;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
+  std::vector<int64_t> vis;
+  int rc = visible_list(v, vis);
+  if (rc) return rc;
+  if (begin < 0 || end > (int64_t)vis.size() || begin > end) return c->fail(SPLATB200_EINVAL, "project_backward: [begin, end) outside the projected list");
+  if (begin == end) return SPLATB200_OK;
+  DevScratch pgin, cg;
+  rc = upload_projected_grads(v, vis, begin, end, g_mean2d, g_range, g_cov2d, g_velocity, nullptr, pgin);
+  if (rc) return rc;
+  const size_t N = (size_t)c->n;
+  CU_TRY(c, cudaMalloc(&cg.p, sizeof(float) * kComposeGradStride * N));
+  CU_TRY(c, cudaMemsetAsync(cg.p, 0, sizeof(float) * kComposeGradStride * N, c->stream));
+  launch_project_bwd_mode(kProjOnly, v->s, c->scene_dev(v->d_actors), v->proj, c->pg(), v->sensor_grads, v->actor_acc, pgin.p,
+                          cg.p, vis[begin], vis[end - 1] + 1, c->stream);
+  CHECK_LAUNCH(c, "k_project_bwd<proj-only>");
+  c->launches += 1;
+  std::vector<float> h((size_t)kComposeGradStride * N);
+  CU_TRY(c, cudaMemcpyAsync(h.data(), cg.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int64_t k = begin; k < end; ++k) {  // accumulate (+=) like the reference (projection.hpp:283-286)
+    const int64_t i = vis[k];
+    const float* o = &h[(size_t)kComposeGradStride * i];
+    for (int e = 0; e < 3; ++e) {
+      if (g_mean_w) g_mean_w[3 * i + e] += o[e];
+      if (g_vel_dyn_w) g_vel_dyn_w[3 * i + e] += o[12 + e];
+    }
+    if (g_cov_w) for (int e = 0; e < 9; ++e) g_cov_w[9 * i + e] += o[3 + e];
+  }
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_compose_backward(splatb200_view* v, const float* g_mean_w, const float* g_cov_w,
+                                               const float* g_vel_dyn_w, const float* g_opacity, int64_t begin, int64_t end) {
+  splatb200_ctx* c = v->ctx;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
+  if (begin < 0 || end > c->n || begin > end) return c->fail(SPLATB200_EINVAL, "compose_backward: [begin, end) outside the scene");
+  if (begin == end) return SPLATB200_OK;
+  const size_t N = (size_t)c->n;
+  std::vector<float> hc((size_t)kComposeGradStride * N, 0.0f), hp((size_t)kProjGradStride * N, 0.0f);
+  for (int64_t i = begin; i < end; ++i) {
+    float* o = &hc[(size_t)kComposeGradStride * i];
+    for (int e = 0; e < 3; ++e) {
+      if (g_mean_w) o[e] = g_mean_w[3 * i + e];
+      if (g_vel_dyn_w) o[12 + e] = g_vel_dyn_w[3 * i + e];
+    }
+    if (g_cov_w) for (int e = 0; e < 9; ++e) o[3 + e] = g_cov_w[9 * i + e];
+    if (g_opacity) hp[(size_t)kProjGradStride * i + 10] = g_opacity[i];
+  }
+  DevScratch cg, pgin;
+  CU_TRY(c, cudaMalloc(&cg.p, sizeof(float) * hc.size()));
+  CU_TRY(c, cudaMalloc(&pgin.p, sizeof(float) * hp.size()));
+  CU_TRY(c, cudaMemcpyAsync(cg.p, hc.data(), sizeof(float) * hc.size(), cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(pgin.p, hp.data(), sizeof(float) * hp.size(), cudaMemcpyHostToDevice, c->stream));
+  launch_project_bwd_mode(kComposeOnly, v->s, c->scene_dev(v->d_actors), v->proj, c->pg(), v->sensor_grads, v->actor_acc,
+                          pgin.p, cg.p, begin, end, c->stream);
+  CHECK_LAUNCH(c, "k_project_bwd<compose-only>");
+  c->launches += 1;
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (!c->tracks.empty()) v->actor_pending = true;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_backward_projected(splatb200_view* v, const float* g_mean2d, const float* g_range,
+                                                 const float* g_cov2d, const float* g_velocity, const float* g_opacity) {
+  splatb200_ctx* c = v->ctx;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
+  if (c->n == 0) return SPLATB200_OK;
+  std::vector<int64_t> vis;
+  int rc = visible_list(v, vis);
+  if (rc) return rc;
+  DevScratch pgin;
+  rc = upload_projected_grads(v, vis, 0, (int64_t)vis.size(), g_mean2d, g_range, g_cov2d, g_velocity, g_opacity, pgin);
+  if (rc) return rc;
+  launch_project_bwd_mode(kFromProjected, v->s, c->scene_dev(v->d_actors), v->proj, c->pg(), v->sensor_grads, v->actor_acc,
+                          pgin.p, nullptr, 0, c->n, c->stream);
+  CHECK_LAUNCH(c, "k_project_bwd<from-projected>");
+  c->launches += 1;
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (!c->tracks.empty()) v->actor_pending = true;
+  return SPLATB200_OK;
+}
+
 // ---- introspection ------------------------------------------------------------------------------
 namespace {
 template <class T> int fetch(splatb200_ctx* c, std::vector<T>& h, const T* d, size_t n) {

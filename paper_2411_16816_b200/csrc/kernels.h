@@ -66,6 +66,12 @@ void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
                        const ParamGradDev& pg, float* d_time_offset, cudaStream_t st);
 
 // project_bwd.cu
+enum BwdMode { kFused = 0, kFromProjected = 1, kProjOnly = 2, kComposeOnly = 3 };
+constexpr int kProjGradStride = 11;     // g_mean2d 2, g_range, g_cov2d 4, g_velocity 3, g_opacity
+constexpr int kComposeGradStride = 15;  // g_mean_w 3, g_cov_w 9, g_vel_dyn_w 3
+void launch_project_bwd_mode(int mode, const Sensor& s, const SceneDev& sc, const ProjDev& p, const ParamGradDev& pg,
+                             float* sensor_grads6, float* actor_acc, const float* pgin, float* cg, int64_t i_lo,
+                             int64_t i_hi, cudaStream_t st);
 void launch_project_bwd(const Sensor& s, const SceneDev& sc, const ProjDev& p, const RasterGradDev& rg,
                         const ParamGradDev& pg, float* sensor_grads6, float* actor_acc, cudaStream_t st);
 

@@ -91,20 +91,43 @@ __device__ __forceinline__ float block_sum_256(float v, float* s_red /* 8 */) {
   return tot;
 }
 
-template <bool kCamera>
+// Modes of the per-Gaussian backward kernel. kFused is the hot path; the other three expose the
+// reference's function granularity through the C ABI (include/splat_b200.h "reference-granularity
+// backward"): ProjectedGrads in (projection.hpp:178-205), ComposeGrads in/out (scene.hpp:313-323).
+//   kFused          raw compositing sums -> ProjectedGrads -> project_*_backward -> compose_backward
+//   kFromProjected  ProjectedGrads (pgin) -> project_*_backward -> compose_backward
+//   kProjOnly       ProjectedGrads (pgin) -> project_*_backward -> ComposeGrads written to cg
+//   kComposeOnly    ComposeGrads (cg) + g_opacity (pgin slot 10) -> compose_backward
+// pgin: N x 11 floats by source index (g_mean2d 2, g_range, g_cov2d 4 row-major, g_velocity 3, g_opacity);
+// cg:   N x 15 floats by source index (g_mean_w 3, g_cov_w 9 row-major, g_vel_dyn_w 3).
+template <bool kCamera, int kMode>
 __global__ void __launch_bounds__(256)
 k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGradDev rg, ParamGradDev pg,
-              float* __restrict__ sensor_grads6, float* __restrict__ actor_acc) {
+              float* __restrict__ sensor_grads6, float* __restrict__ actor_acc, const float* __restrict__ pgin,
+              float* __restrict__ cg, int64_t i_lo, int64_t i_hi) {
   __shared__ float s_red[8];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float sg[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};  // d_vel_lin, d_vel_ang
-  const bool live = i < sc.n && p.count[i] != 0u;
+  const bool in_range = i < sc.n && i >= i_lo && i < i_hi;
+  const bool live = in_range && (kMode == kComposeOnly || p.count[i] != 0u);
   if (live) {
     Fwd f;
     compose_one(sc, i, f);
+    float g_opacity = 0.0f;
+    float g_mean_w[3], g_vdyn_w[3], g_cov_w[9], tmp9[9];
+    if (kMode == kComposeOnly) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { g_mean_w[k] = cg[kComposeGradStride * i + k]; g_vdyn_w[k] = cg[kComposeGradStride * i + 12 + k]; }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) g_cov_w[k] = cg[kComposeGradStride * i + 3 + k];
+      g_opacity = pgin[kProjGradStride * i + 10];
+    } else {
     if (kCamera) project_camera_one(s, f);
     else project_lidar_one(s, f);
 
+    float G2[2][2];
+    float gm[3], gv[3];   // g_mean2d + g_range, g_velocity
+    if (kMode == kFused) {
     float r[kRasterGradStride];
 #pragma unroll
     for (int k = 0; k < kRasterGradStride; ++k) {
@@ -113,11 +136,11 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     }
     // ---- (1) raw sums -> ProjectedGrads -------------------------------------------------------
     const float g_rho = r[8];
-    const float g_opacity = f.det_ratio * g_rho;
+    g_opacity = f.det_ratio * g_rho;
     const float g_dr = f.opacity * g_rho;
     const float C[2][2] = {{f.conic[0], f.conic[1]}, {f.conic[2], f.conic[3]}};
     const float Gc[2][2] = {{r[0], r[1]}, {r[1], r[2]}};
-    float CtG[2][2], G2[2][2];
+    float CtG[2][2];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -134,11 +157,20 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     G2[0][0] = gcov[0][0];
     G2[0][1] = G2[1][0] = 0.5f * (gcov[0][1] + gcov[1][0]);
     G2[1][1] = gcov[1][1];
+    gm[0] = r[3]; gm[1] = r[4]; gm[2] = kCamera ? 0.0f : r[9];
+    gv[0] = r[5]; gv[1] = r[6]; gv[2] = kCamera ? 0.0f : r[7];
+    } else {  // ProjectedGrads handed in (projection.hpp:257-268 / 329-344)
+      const float* q = pgin + kProjGradStride * i;
+      G2[0][0] = q[3];
+      G2[0][1] = G2[1][0] = 0.5f * (q[4] + q[5]);
+      G2[1][1] = q[6];
+      gm[0] = q[0]; gm[1] = q[1]; gm[2] = kCamera ? 0.0f : q[2];
+      gv[0] = q[7]; gv[1] = q[8]; gv[2] = kCamera ? 0.0f : q[9];
+      g_opacity = q[10];
+    }
 
     // ---- (2) projection backward --------------------------------------------------------------
     constexpr int ROWS = kCamera ? 2 : 3;
-    const float gm[3] = {r[3], r[4], kCamera ? 0.0f : r[9]};   // g_mean2d, g_range
-    const float gv[3] = {r[5], r[6], kCamera ? 0.0f : r[7]};   // g_velocity
     float g_mu[3], GJ[2 * 3], g_cov_s[9], g_J[ROWS * 3], g_u[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -182,12 +214,19 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     cross3(s.vel_ang, g_u, wxg);
 #pragma unroll
     for (int k = 0; k < 3; ++k) { sg[k] = -g_u[k]; sg[3 + k] = -mxg[k]; g_mu[k] += wxg[k]; }
-    float g_mean_w[3], g_vdyn_w[3], g_cov_w[9], tmp9[9];
     mat_t_vec(s.R, g_mu, g_mean_w);
     mat_t_vec(s.R, g_u, g_vdyn_w);
+    if (!f.dynamic) g_vdyn_w[0] = g_vdyn_w[1] = g_vdyn_w[2] = 0.0f;  // projection.hpp:245, 283
     mat_mul_tn(s.R, g_cov_s, tmp9);
     mat_mul(tmp9, s.R, g_cov_w);
+    }  // kMode != kComposeOnly
 
+    if (kMode == kProjOnly) {  // ComposeGrads out (scene.hpp:313-323)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { cg[kComposeGradStride * i + k] = g_mean_w[k]; cg[kComposeGradStride * i + 12 + k] = g_vdyn_w[k]; }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) cg[kComposeGradStride * i + 3 + k] = g_cov_w[k];
+    } else {
     // ---- (3) compose backward -----------------------------------------------------------------
     pg.d_opacity_logit[i] += g_opacity * f.opacity * (1.0f - f.opacity);
     float g_cov_local[9], d_mean[3];
@@ -254,6 +293,7 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     for (int k = 0; k < 3; ++k) pg.d_scale_log[3 * i + k] += gsl[k];
 #pragma unroll
     for (int k = 0; k < 4; ++k) pg.d_quat[4 * i + k] += gq[k];
+    }  // kMode != kProjOnly
   }
   // SensorGrads d_vel_lin / d_vel_ang: block reduction, one atomic per block and component
 #pragma unroll
@@ -267,8 +307,30 @@ void launch_project_bwd(const Sensor& s, const SceneDev& sc, const ProjDev& p, c
                         const ParamGradDev& pg, float* sensor_grads6, float* actor_acc, cudaStream_t st) {
   if (sc.n == 0) return;
   const unsigned blocks = (unsigned)((sc.n + 255) / 256);
-  if (s.is_camera) k_project_bwd<true><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc);
-  else k_project_bwd<false><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc);
+  if (s.is_camera)
+    k_project_bwd<true, kFused><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc, nullptr, nullptr, 0, sc.n);
+  else
+    k_project_bwd<false, kFused><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc, nullptr, nullptr, 0, sc.n);
+}
+
+void launch_project_bwd_mode(int mode, const Sensor& s, const SceneDev& sc, const ProjDev& p, const ParamGradDev& pg,
+                             float* sensor_grads6, float* actor_acc, const float* pgin, float* cg, int64_t i_lo,
+                             int64_t i_hi, cudaStream_t st) {
+  if (sc.n == 0) return;
+  const unsigned blocks = (unsigned)((sc.n + 255) / 256);
+  RasterGradDev rg{nullptr};
+#define SB_LAUNCH(CAM, MODE) \
+  k_project_bwd<CAM, MODE><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc, pgin, cg, i_lo, i_hi)
+  if (s.is_camera) {
+    if (mode == kFromProjected) SB_LAUNCH(true, kFromProjected);
+    else if (mode == kProjOnly) SB_LAUNCH(true, kProjOnly);
+    else SB_LAUNCH(true, kComposeOnly);
+  } else {
+    if (mode == kFromProjected) SB_LAUNCH(false, kFromProjected);
+    else if (mode == kProjOnly) SB_LAUNCH(false, kProjOnly);
+    else SB_LAUNCH(false, kComposeOnly);
+  }
+#undef SB_LAUNCH
 }
 
 }  // namespace sb
