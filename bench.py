@@ -282,7 +282,9 @@ def run_b200(args):
         grads_t = torch.zeros(n_grad, dtype=torch.float32, device=dev)
         ctx.bind_grads_device(grads_t.data_ptr(), n_grad)
 
-        lid, cam = frame_sensors(rank)
+        from paper_2411_16816_b200 import dist as sdist
+        (frame,) = sdist.assign_frames(world, world, rank)      # one frame per rank and step: weak scaling
+        lid, cam = frame_sensors(frame)
         rays = synth.grid_rays(lid)
         vl = ctx.lidar_view(lid, rays, st)
         vc = ctx.camera_view(cam, st)
@@ -321,8 +323,7 @@ def run_b200(args):
             vl.backward_device(g_dev["l"][0].data_ptr(), g_dev["l"][1].data_ptr())
             vc.forward(0.0)
             vc.backward_device(g_dev["c"][0].data_ptr(), g_dev["c"][1].data_ptr())
-            if world > 1:
-                dist.all_reduce(grads_t)
+            sdist.allreduce_grads(grads_t)
 
         def step_e2e():
             """the reference-facing call with HOST buffers: GaussianSet up, rendered images down, upstream
@@ -335,8 +336,7 @@ def run_b200(args):
                 v.download(vb, va, vn)
                 _, _, gb, ga = g_host[name]
                 v.backward_host_async(gb, ga)
-            if world > 1:
-                dist.all_reduce(grads_t)
+            sdist.allreduce_grads(grads_t)
             ctx.grads_into(*gh_parts)
 
         def timed(fn, steps):
