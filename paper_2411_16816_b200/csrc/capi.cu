@@ -2,6 +2,8 @@
 // stream-ordered stage pipeline  project -> scan -> emit keys -> radix sort -> tile ranges ->
 // composite, and its reverse. Host code only; the kernels live in forward.cu / binning.cu /
 // raster_bwd.cu / project_bwd.cu.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -91,8 +93,9 @@ struct splatb200_view {
   uint32_t *tile_begin = nullptr, *tile_end = nullptr;
   // queries
   int64_t P = 0, n_tiles = 0;
-  float* rays = nullptr;
+  float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
   int64_t *ray_begin = nullptr, *ray_end = nullptr;
+  uint32_t* tile_order = nullptr;  // optional CTA -> tile permutation
   RasterOutDev out{};
   float *g_blend_stage = nullptr, *g_alpha_stage = nullptr;
   float* sensor_grads = nullptr;  // 6 + d_time_offset
@@ -184,7 +187,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
   dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
-  dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end);
+  dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end); dfree(v->tile_order);
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
   dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
@@ -605,10 +608,41 @@ extern "C" int splatb200_view_create_lidar(splatb200_ctx* c, const splatb200_lid
   };
   if (rc) return fin(rc);
   const size_t P = (size_t)std::max<int64_t>(1, n_rays);
-  if (cudaMalloc(&v->rays, sizeof(float) * 3 * P) != cudaSuccess || cudaMalloc(&v->ray_begin, sizeof(int64_t) * n_tiles) != cudaSuccess ||
+  if (n_rays > 0xffffffffLL) return fin(c->fail(SPLATB200_EINVAL, "more than 2^32-1 rays in one view"));
+  for (int64_t t = 0; t < n_tiles; ++t)
+    if (ray_begin[t] < 0 || ray_end[t] < ray_begin[t] || ray_end[t] > n_rays)
+      return fin(c->fail(SPLATB200_EINVAL, "ray_begin/ray_end must delimit slices of the ray array"));
+  // Within a tile the rays are re-ordered azimuth-major (then by elevation), so that 32 consecutive positions — one
+  // warp of the compositing kernels — form a compact patch (4 azimuth bins x 8 beams on a grid sweep) that per-warp
+  // culling can exploit. The original index travels in .w; outputs keep the caller's ray order.
+  std::vector<float4> packed(P);
+  {
+    std::vector<std::pair<std::pair<float, float>, int64_t>> keyed;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+      const int64_t b = ray_begin[t], e = ray_end[t];
+      if (e <= b) continue;
+      keyed.clear();
+      const float ref = rays[3 * b];
+      for (int64_t r = b; r < e; ++r) {
+        float rel = std::fmod(rays[3 * r] - ref, 6.283185307179586f);   // wrap to (-pi, pi] around the tile's first ray
+        if (rel > 3.14159265358979f) rel -= 6.283185307179586f;
+        if (rel <= -3.14159265358979f) rel += 6.283185307179586f;
+        keyed.push_back({{rel, rays[3 * r + 1]}, r});
+      }
+      std::stable_sort(keyed.begin(), keyed.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (int64_t k = 0; k < e - b; ++k) {
+        const int64_t r = keyed[(size_t)k].second;
+        const uint32_t bits = (uint32_t)r;
+        float w;
+        std::memcpy(&w, &bits, 4);
+        packed[(size_t)(b + k)] = make_float4(rays[3 * r], rays[3 * r + 1], rays[3 * r + 2], w);
+      }
+    }
+  }
+  if (cudaMalloc(&v->rays, sizeof(float4) * P) != cudaSuccess || cudaMalloc(&v->ray_begin, sizeof(int64_t) * n_tiles) != cudaSuccess ||
       cudaMalloc(&v->ray_end, sizeof(int64_t) * n_tiles) != cudaSuccess)
     return fin(c->fail(SPLATB200_ENOMEM, "cudaMalloc rays"));
-  if (n_rays) cudaMemcpyAsync(v->rays, rays, sizeof(float) * 3 * (size_t)n_rays, cudaMemcpyHostToDevice, c->stream);
+  if (n_rays) cudaMemcpyAsync(v->rays, packed.data(), sizeof(float4) * (size_t)n_rays, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(v->ray_begin, ray_begin, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(v->ray_end, ray_end, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fin(c->fail(SPLATB200_ECUDA, "ray upload failed"));
@@ -746,7 +780,8 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
 
   {
     StageTimer tm(v, 5);
-    launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out, st);
+    launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
+                      v->out, st);
   }
   CHECK_LAUNCH(c, "k_raster_fwd");
   c->launches += 1;
@@ -785,8 +820,8 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
   const ParamGradDev pg = c->pg();
   if (v->I > 0) {
     StageTimer tm(v, 6);
-    launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->out,
-                      g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
+    launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
+                      v->out, g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
     CHECK_LAUNCH(c, "k_raster_bwd");
     c->launches += 1;
   }

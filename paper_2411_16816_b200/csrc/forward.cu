@@ -107,26 +107,37 @@ void launch_tile_ranges(int64_t total, const uint64_t* keys, uint32_t* tile_begi
 }
 
 // ------------------------------------------------------------------------------------------------
-// K5/K6: forward compositing. One CTA of 256 threads per tile: 16x16 pixels, or up to 256 rays of
-// a 32x8 lidar tile (more than 256 rays => additional passes over the list). The tile's
-// depth-sorted slice is staged through shared memory 256 Gaussians at a time (each thread fetches one
-// 112-byte record with 7 128-bit loads); every thread then walks the batch front to back with
-// broadcast shared-memory reads. The batch loop ends when every query of the tile has saturated
-// (T < transmittance_min), detected with one __syncthreads_and per batch.
+// K5/K6: forward compositing. One CTA of 256 threads per tile: 16x16 pixels, or up to 256 rays of a
+// 32x8 lidar tile (more than 256 rays => additional passes over the list). Each warp owns
+// a compact patch of 32 queries (camera: 8x4 pixels; lidar: 32 consecutive rays of the per-tile
+// azimuth-major order, i.e. 4 azimuth bins x 8 beams of a grid sweep).
+//
+// The tile's depth-sorted slice is staged through shared memory 256 Gaussians at a time. The staging
+// thread tests its Gaussian against the 8 patch boxes (raster_common.cuh: a rigorous lower bound of the
+// fp32 quadratic form, so no blended pair is ever dropped) and fetches the 112-byte record only if some
+// patch can see it; every warp compacts the batch to its own visible entries with ballots and walks
+// those front to back with broadcast shared-memory reads. The evaluation itself is the exact IEEE
+// sequence of the oracle, so contributor counts stay bit-identical. The batch loop ends when every
+// query of the tile has saturated (T < transmittance_min): one __syncthreads_and per batch; a warp whose
+// 32 queries have all saturated stops evaluating on its own.
 // ------------------------------------------------------------------------------------------------
 template <bool kCamera>
 __global__ void __launch_bounds__(256)
 k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
-             const float* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
-             RasterOutDev out) {
+             const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
+             const uint32_t* __restrict__ tile_order, RasterOutDev out) {
   __shared__ float4 sA[256];
   __shared__ float4 sB[256];
   __shared__ float2 sC[256];
   __shared__ float4 sF[256 * 4];
+  __shared__ uint8_t sMask[256];
+  __shared__ uint8_t sList[8][256];
+  __shared__ PatchBox sBox[8];
 
-  const int tile = blockIdx.x;
+  const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
 
   int64_t q_begin = 0, q_end = 1;  // camera: single pass
@@ -137,19 +148,25 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     int64_t pix;
     float qx, qy, t;
     if (kCamera) {
-      const int px = (tile % s.tiles_x) * kTile + (tid & 15);
-      const int py = (tile / s.tiles_x) * kTile + (tid >> 4);
+      const int px = (tile % s.tiles_x) * kTile + (warp & 1) * 8 + (lane & 7);
+      const int py = (tile / s.tiles_x) * kTile + (warp >> 1) * 4 + (lane >> 3);
       inside = px < s.width && py < s.height;
       pix = (int64_t)py * s.width + px;
       qx = (float)px + 0.5f;
       qy = (float)py + 0.5f;
       t = ((float)py / (float)s.height - 0.5f) * s.shutter + s.time_offset;  // Eq. 3
     } else {
-      pix = q_base + tid;
-      inside = pix < q_end;
+      const int64_t pos = q_base + tid;
+      inside = pos < q_end;
       qx = qy = t = 0.0f;
-      if (inside) { qx = rays[3 * pix]; qy = rays[3 * pix + 1]; t = rays[3 * pix + 2]; }
+      pix = 0;
+      if (inside) {
+        const float4 r = rays[pos];
+        qx = r.x; qy = r.y; t = r.z;
+        pix = (int64_t)__float_as_uint(r.w);  // original ray index
+      }
     }
+    warp_patch_box<!kCamera>(inside, qx, qy, t, lane, &sBox[warp]);
 
     float T = 1.0f, range_acc = 0.0f, median = 0.0f;
     bool med_found = false;
@@ -158,44 +175,54 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
 #pragma unroll
     for (int k = 0; k < kChannels; ++k) acc[k] = 0.0f;
     bool done = !inside;
+    __syncthreads();  // patch boxes visible
 
     for (uint32_t base = lb; base < le; base += 256) {
       if (__syncthreads_and(done)) break;
       const uint32_t idx = base + tid;
+      uint32_t mask = 0u;
       if (idx < le) {
         const uint32_t src = vals[idx];
-        sA[tid] = p.geomA[src];
-        sB[tid] = p.geomB[src];
-        if (!kCamera) sC[tid] = p.geomC[src];
+        const float4 gA = p.geomA[src], gB = p.geomB[src];
+        mask = patch_mask<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min);
+        if (mask) {
+          sA[tid] = gA;
+          sB[tid] = gB;
+          if (!kCamera) sC[tid] = p.geomC[src];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) sF[4 * tid + k] = p.feat[4 * (size_t)src + k];
-      }
-      __syncthreads();
-      const int cnt = min(256u, le - base);
-      if (!done) {
-        for (int j = 0; j < cnt; ++j) {
-          AlphaEval ev;
-          if (!evaluate_alpha<!kCamera>(sA[j], sB[j], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) continue;
-          const float w = __fmul_rn(ev.alpha, T);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float4 f4 = sF[4 * j + k];
-            acc[4 * k] = __fmaf_rn(f4.x, w, acc[4 * k]);
-            acc[4 * k + 1] = __fmaf_rn(f4.y, w, acc[4 * k + 1]);
-            acc[4 * k + 2] = __fmaf_rn(f4.z, w, acc[4 * k + 2]);
-            acc[4 * k + 3] = __fmaf_rn(f4.w, w, acc[4 * k + 3]);
-          }
-          T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
-          ++n_contrib;
-          last_idx = (int)(base - lb) + j + 1;
-          if (!kCamera) {
-            const float2 c = sC[j];
-            const float r_rs = __fmaf_rn(c.y, t, c.x);
-            range_acc = __fmaf_rn(r_rs, w, range_acc);
-            if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
-          }
-          if (T < s.transmittance_min) { done = true; break; }
+          for (int k = 0; k < 4; ++k) sF[4 * tid + k] = p.feat[4 * (size_t)src + k];
         }
+      }
+      sMask[tid] = (uint8_t)mask;
+      __syncthreads();
+      if (__all_sync(0xffffffffu, done)) continue;  // this warp's 32 queries have saturated
+      const int cnt = min(256u, le - base);
+      const int n_w = warp_compact(sMask, cnt, warp, lane, sList[warp]);
+      for (int k = 0; k < n_w; ++k) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const int j = sList[warp][k];
+        if (done) continue;
+        AlphaEval ev;
+        if (!evaluate_alpha<!kCamera>(sA[j], sB[j], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) continue;
+        const float w = __fmul_rn(ev.alpha, T);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 f4 = sF[4 * j + c];
+          acc[4 * c] = __fmaf_rn(f4.x, w, acc[4 * c]);
+          acc[4 * c + 1] = __fmaf_rn(f4.y, w, acc[4 * c + 1]);
+          acc[4 * c + 2] = __fmaf_rn(f4.z, w, acc[4 * c + 2]);
+          acc[4 * c + 3] = __fmaf_rn(f4.w, w, acc[4 * c + 3]);
+        }
+        T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
+        ++n_contrib;
+        last_idx = (int)(base - lb) + j + 1;
+        if (!kCamera) {
+          const float2 c = sC[j];
+          const float r_rs = __fmaf_rn(c.y, t, c.x);
+          range_acc = __fmaf_rn(r_rs, w, range_acc);
+          if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
+        }
+        if (T < s.transmittance_min) done = true;
       }
     }
 
@@ -215,17 +242,19 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       out.n_contrib[pix] = n_contrib;
       out.last_idx[pix] = last_idx;
     }
-    __syncthreads();  // shared staging is reused by the next ray pass
+    __syncthreads();  // shared staging and patch boxes are reused by the next ray pass
   }
 }
 
 void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
-                       const uint32_t* tile_end, const float* rays, const int64_t* ray_begin, const int64_t* ray_end,
-                       const RasterOutDev& out, cudaStream_t st) {
+                       const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                       const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st) {
   const int tiles = s.tiles_x * s.tiles_y;
   if (tiles == 0) return;
-  if (s.is_camera) k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, out);
-  else k_raster_fwd<false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, out);
+  if (s.is_camera)
+    k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order, out);
+  else
+    k_raster_fwd<false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order, out);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -43,9 +43,12 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
 void launch_emit_keys(int64_t n, int64_t total, const int64_t* offsets, const ProjDev& p, int tiles_x, int wrap_x,
                       uint64_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_tile_ranges(int64_t total, const uint64_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st);
+// rays: one float4 per ray POSITION (azimuth, elevation, t_l, bit pattern of the original ray index), tile-major and
+// azimuth-major inside a tile (prepared at view creation); tile_order: optional CTA -> tile permutation (longest
+// worklists first), nullptr = identity
 void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
-                       const uint32_t* tile_end, const float* rays, const int64_t* ray_begin, const int64_t* ray_end,
-                       const RasterOutDev& out, cudaStream_t st);
+                       const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                       const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st);
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 
@@ -61,8 +64,8 @@ int launch_sort_pairs(uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_
 
 // raster_bwd.cu
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
-                       const uint32_t* tile_end, const float* rays, const int64_t* ray_begin, const int64_t* ray_end,
-                       const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha, const RasterGradDev& rg,
+                       const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                       const uint32_t* tile_order, const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha, const RasterGradDev& rg,
                        const ParamGradDev& pg, float* d_time_offset, cudaStream_t st);
 
 // project_bwd.cu

@@ -51,4 +51,130 @@ __device__ __forceinline__ bool evaluate_alpha(const float4 gA /* mx my vx vy */
   return true;
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// Per-warp conservative culling (shared by the forward and backward compositing kernels).
+//
+// A CTA owns a tile; each of its 8 warps owns a compact PATCH of 32 queries (camera: 8x4 pixels; lidar:
+// 32 rays consecutive in the per-tile azimuth-major order prepared at view creation, i.e. 4 azimuth
+// bins x 8 beams on a grid sweep). When a batch of 256 Gaussians is staged, the staging thread tests its
+// Gaussian against the 8 patch boxes and publishes an 8-bit mask; every warp then compacts the batch to
+// the entries whose bit is set (order preserved) and walks only those.
+//
+// The test must NEVER drop a pair the exact per-query fp32 evaluation would blend, because contributor
+// counts are a bit-exact parity gate. It is therefore a rigorous bound, not a heuristic:
+//   * the set of fp32-computed offsets d = q - (m + v t) over the patch is enclosed in a box with centre
+//     dc and half-extents H that include the rolling-shutter travel and the rounding of m + v t and q - m;
+//   * for a positive semi-definite conic, sqrt(Q) is a norm:  sqrt(Q(d)) >= sqrt(Q(dc)) - sqrt(Qabs(H));
+//   * the fp32 evaluation of Q differs from the exact one by at most ~4 ulp of the sum of term magnitudes
+//     M <= a DX^2 + c DY^2 + |b2| DX DY; a margin of 2^-18 M (64 ulp) covers that, the cull's own
+//     arithmetic and the rounding of the conic entries;
+//   * the pair is dropped only if that lower bound exceeds qform_max, or the alpha it allows is below
+//     alpha_min (with a 1% margin). A conic that is not certifiably PSD, a non-finite value, or a lidar
+//     offset box that reaches the +-pi seam keeps the pair.
+// Ill-conditioned grazing footprints (|d| ~ 1e5 px, M ~ 1e10) get a margin far above qform_max and are
+// simply never culled — their per-query evaluation is rounding noise that must be reproduced, not bounded.
+// ------------------------------------------------------------------------------------------------
+struct PatchBox {
+  float cx, cy, hx, hy, tc, th;
+  int enabled;  // 0: the warp's queries are too spread out (or absent) to cull against
+  int pad;
+};
+
+constexpr float kCullGamma = 3.814697265625e-06f;   // 2^-18
+constexpr float kSlackUlp = 4.76837158203125e-07f;  // 2^-21
+
+template <bool kLidar>
+__device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB, const PatchBox* __restrict__ box,
+                                               float qform_max, float alpha_min) {
+  const float a = gB.x, b2 = gB.y, c = gB.z, rho = gB.w;
+  const float ab2 = fabsf(b2);
+  // certified PSD: 4ac >= b2^2 with rounding slack on both sides
+  const bool psd = a > 0.0f && c > 0.0f && (4.0f * a * c * (1.0f - 1e-6f) - b2 * b2 * (1.0f + 1e-6f) >= 0.0f);
+  if (!psd) return 0xffu;
+  // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min)
+  float qmax = qform_max;
+  if (alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qmax = fminf(qmax, 2.0f * __logf(rho * 1.01f / alpha_min) + 0.02f);
+  uint32_t mask = 0u;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const PatchBox b = box[p];
+    bool keep = true;
+    if (b.enabled) {
+      const float mxc = fmaf(gA.z, b.tc, gA.x), myc = fmaf(gA.w, b.tc, gA.y);
+      float dcx = b.cx - mxc;
+      if (kLidar) dcx = wrap_pi(dcx);
+      const float dcy = b.cy - myc;
+      const float tmax = fabsf(b.tc) + b.th;
+      const float Hx = b.hx + fabsf(gA.z) * b.th + kSlackUlp * (fabsf(gA.x) + fabsf(gA.z) * tmax + fabsf(b.cx) + b.hx + 8.0f);
+      const float Hy = b.hy + fabsf(gA.w) * b.th + kSlackUlp * (fabsf(gA.y) + fabsf(gA.w) * tmax + fabsf(b.cy) + b.hy + 8.0f);
+      const float DX = fabsf(dcx) + Hx, DY = fabsf(dcy) + Hy;
+      const bool seam = kLidar && !(DX < kPi - 1e-3f);
+      const float E = kCullGamma * (a * DX * DX + c * DY * DY + ab2 * DX * DY);
+      const float Qc = a * dcx * dcx + b2 * dcx * dcy + c * dcy * dcy;
+      const float R2 = a * Hx * Hx + ab2 * Hx * Hy + c * Hy * Hy;
+      const float s = sqrtf(fmaxf(Qc - E, 0.0f)) - sqrtf(R2) * (1.0f + 1e-5f);
+      // fp32 qf >= lb for every query of the patch (lb may be negative: rounding can push qf below zero)
+      const float lb = (s > 0.0f ? s * s * (1.0f - 1e-5f) : 0.0f) - E;
+      const bool cull = !seam && lb > qmax;
+      keep = !cull;
+    }
+    if (keep) mask |= 1u << p;
+  }
+  return mask;
+}
+
+// Bounding box of the warp's queries (lanes with `inside`), written by lane 0. Lidar azimuths are measured
+// relative to the first valid lane's azimuth so that a patch straddling 0 / 2 pi stays compact.
+template <bool kLidar>
+__device__ __forceinline__ void warp_patch_box(bool inside, float qx, float qy, float t, int lane, PatchBox* out) {
+  const unsigned act = __ballot_sync(0xffffffffu, inside);
+  PatchBox b;
+  b.cx = b.cy = b.hx = b.hy = b.tc = b.th = 0.0f;
+  b.enabled = 0;
+  b.pad = 0;
+  if (act != 0u) {
+    const int first = __ffs(act) - 1;
+    const float ref = __shfl_sync(0xffffffffu, qx, first);
+    float rx = kLidar ? wrap_pi(qx - ref) : qx;
+    const float big = 3.0e38f;
+    float x0 = inside ? rx : big, x1 = inside ? rx : -big;
+    float y0 = inside ? qy : big, y1 = inside ? qy : -big;
+    float t0 = inside ? t : big, t1 = inside ? t : -big;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o)); x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+      y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o)); y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+      t0 = fminf(t0, __shfl_xor_sync(0xffffffffu, t0, o)); t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, o));
+    }
+    // centre / half-extent, padded by a few ulp so the box certainly contains every query
+    b.cx = 0.5f * (x0 + x1); b.hx = 0.5f * (x1 - x0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(x0) + fabsf(x1)) + 1e-30f;
+    b.cy = 0.5f * (y0 + y1); b.hy = 0.5f * (y1 - y0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(y0) + fabsf(y1)) + 1e-30f;
+    b.tc = 0.5f * (t0 + t1); b.th = 0.5f * (t1 - t0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
+    b.enabled = 1;
+    if (kLidar) {
+      b.cx += ref;                             // back to absolute azimuth (any 2 pi offset is removed by wrap_pi later)
+      b.hx += 1e-6f * (fabsf(ref) + 8.0f);
+      if (!(b.hx < 0.5f * kPi)) b.enabled = 0;  // rays all around the circle: nothing to cull against
+    }
+    if (!(b.hx == b.hx && b.hy == b.hy && b.th == b.th)) b.enabled = 0;
+  }
+  if (lane == 0) *out = b;
+}
+
+// Order-preserving compaction of the batch entries whose mask has this warp's bit. Returns the count.
+__device__ __forceinline__ int warp_compact(const uint8_t* __restrict__ sMask, int cnt, int warp, int lane,
+                                            uint8_t* __restrict__ list) {
+  int n = 0;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const int j = c0 + lane;
+    const bool bit = j < cnt && ((sMask[j] >> warp) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    if (bit) list[n + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)j;
+    n += __popc(bal);
+  }
+  __syncwarp();
+  return n;
+}
+
 }  // namespace sb
