@@ -119,10 +119,10 @@ def stage_bytes(stats: dict, camera: bool):
     b_gin = 68 if camera else 60
     return {
         "project": 48 * N + 48 * V + 64 * V + 16 * V + 4 * N,     # raw params in; geom + feat record, rect, count out
-        "scan": 4 * N + 8 * N,
-        "emit_keys": 12 * V + 8 * V + 12 * I,
-        "sort": 24 * I,
-        "tile_ranges": 8 * I + 8 * T,
+        "depth_sort_scan": 16 * N + 4 * N + 8 * N,          # (key, index) pairs read + written once; counts in, offsets out
+        "emit": 28 * V + 8 * I,                              # offsets + order + rect per visible Gaussian; (tile, index) out
+        "tile_sort": 16 * I,                                 # (tile, index) pairs read + written once
+        "tile_ranges": 4 * I + 8 * T,
         "raster_fwd": 116 * I + 8 * T + P * b_out,
         "raster_bwd": 116 * I + 8 * T + P * (b_out + b_gin) + 104 * V,
         "project_bwd": 104 * V + 48 * V + 48 * N + 108 * N,
@@ -411,7 +411,7 @@ def run_b200(args):
     cand.sort(reverse=True)
     ms_k, sensor_k, stage_k, bytes_k = cand[0]
     kernel_name = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project", "project_bwd": "k_project_bwd",
-                   "emit_keys": "k_emit_keys", "sort": "cub::DeviceRadixSort", "scan": "cub::DeviceScan",
+                   "emit": "k_emit", "tile_sort": "cub::DeviceRadixSort", "depth_sort_scan": "cub::DeviceRadixSort+DeviceScan",
                    "tile_ranges": "k_tile_ranges"}[stage_k] + ("<camera>" if sensor_k == "camera" else "<lidar>")
     achieved = bytes_k / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
     traffic = None

@@ -347,7 +347,7 @@ class View:
     def forward(self, t_scene=0.0, stop_after=0):
         self.ctx._check(self.L.splatb200_view_forward(self.h, C.c_float(t_scene), stop_after))
 
-    STAGES = ("project", "scan", "emit_keys", "sort", "tile_ranges", "raster_fwd", "raster_bwd", "project_bwd")
+    STAGES = ("project", "depth_sort_scan", "emit", "tile_sort", "tile_ranges", "raster_fwd", "raster_bwd", "project_bwd")
 
     def stage_ms(self) -> dict:
         out = np.zeros(8, np.float32)

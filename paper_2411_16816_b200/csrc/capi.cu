@@ -85,8 +85,13 @@ struct splatb200_view {
   float* rg = nullptr;
   // intersections
   int64_t isect_cap = 0;
-  uint64_t *keys0 = nullptr, *keys1 = nullptr;
-  uint32_t *vals0 = nullptr, *vals1 = nullptr;
+  uint32_t *keys0 = nullptr, *keys1 = nullptr;  // tile ids
+  uint32_t *vals0 = nullptr, *vals1 = nullptr;  // source indices
+  // depth sort of the Gaussians (N + 1 entries each; [n] is padding)
+  uint32_t *dkey_alt = nullptr, *order0 = nullptr, *order1 = nullptr;
+  void* dsort_temp = nullptr;
+  size_t dsort_temp_bytes = 0;
+  int order_sel = 0;
   void* sort_temp = nullptr;
   size_t sort_temp_bytes = 0;
   int sorted_sel = 0;
@@ -117,7 +122,8 @@ struct splatb200_view {
   double ev_sum_ms[8] = {};
   int64_t ev_count[8] = {};
 
-  const uint64_t* keys() const { return sorted_sel ? keys1 : keys0; }
+  const uint32_t* keys() const { return sorted_sel ? keys1 : keys0; }
+  const uint32_t* order() const { return order_sel ? order1 : order0; }
   const uint32_t* vals() const { return sorted_sel ? vals1 : vals0; }
 };
 
@@ -186,6 +192,7 @@ int finalize_actor_grads(splatb200_view* v) {
 void free_view_buffers(splatb200_view* v) {
   dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
   dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
+  dfree(v->proj.dkey); dfree(v->dkey_alt); dfree(v->order0); dfree(v->order1); dfree(v->dsort_temp);
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
   dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end); dfree(v->tile_order);
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
@@ -233,6 +240,7 @@ int ensure_source_buffers(splatb200_view* v) {
   if (v->n_alloc == c->n && v->proj.count) return SPLATB200_OK;
   dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
   dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
+  dfree(v->proj.dkey); dfree(v->dkey_alt); dfree(v->order0); dfree(v->order1); dfree(v->dsort_temp);
   const size_t n = (size_t)std::max<int64_t>(1, c->n);
   CU_TRY(c, cudaMalloc(&v->proj.geomA, sizeof(float4) * n));
   CU_TRY(c, cudaMalloc(&v->proj.geomB, sizeof(float4) * n));
@@ -241,6 +249,14 @@ int ensure_source_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->proj.rect, sizeof(int4) * n));
   CU_TRY(c, cudaMalloc(&v->proj.count, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMemsetAsync(v->proj.count, 0, sizeof(uint32_t) * (n + 1), c->stream));
+  CU_TRY(c, cudaMalloc(&v->proj.dkey, sizeof(uint32_t) * (n + 1)));
+  CU_TRY(c, cudaMalloc(&v->dkey_alt, sizeof(uint32_t) * (n + 1)));
+  CU_TRY(c, cudaMalloc(&v->order0, sizeof(uint32_t) * (n + 1)));
+  CU_TRY(c, cudaMalloc(&v->order1, sizeof(uint32_t) * (n + 1)));
+  launch_iota((int64_t)n + 1, v->order0, c->stream);  // [n] = n: the scan's padding element
+  launch_iota((int64_t)n + 1, v->order1, c->stream);
+  v->dsort_temp_bytes = sort_temp_bytes((int64_t)n);
+  CU_TRY(c, cudaMalloc(&v->dsort_temp, v->dsort_temp_bytes));
   CU_TRY(c, cudaMalloc(&v->offsets, sizeof(int64_t) * (n + 1)));
   v->scan_temp_bytes = scan_temp_bytes(c->n);
   CU_TRY(c, cudaMalloc(&v->scan_temp, v->scan_temp_bytes));
@@ -255,8 +271,8 @@ int ensure_isect_capacity(splatb200_view* v, int64_t total) {
   if (total <= v->isect_cap) return SPLATB200_OK;
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
   const int64_t cap = total + total / 4 + 1024;
-  CU_TRY(c, cudaMalloc(&v->keys0, sizeof(uint64_t) * (size_t)cap));
-  CU_TRY(c, cudaMalloc(&v->keys1, sizeof(uint64_t) * (size_t)cap));
+  CU_TRY(c, cudaMalloc(&v->keys0, sizeof(uint32_t) * (size_t)cap));
+  CU_TRY(c, cudaMalloc(&v->keys1, sizeof(uint32_t) * (size_t)cap));
   CU_TRY(c, cudaMalloc(&v->vals0, sizeof(uint32_t) * (size_t)cap));
   CU_TRY(c, cudaMalloc(&v->vals1, sizeof(uint32_t) * (size_t)cap));
   v->sort_temp_bytes = sort_temp_bytes(cap);
@@ -737,9 +753,18 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   c->launches += c->n > 0;
   {
     StageTimer tm(v, 1);
-    launch_scan_counts(v->proj.count, v->offsets, c->n, v->scan_temp, v->scan_temp_bytes, st);
+    // depth order of the Gaussians (stable: ties in ascending source index), then offsets in that order
+    v->order_sel = 0;
+    if (c->n > 0) {
+      launch_iota(c->n, v->order0, st);
+      v->order_sel = launch_sort_pairs(v->proj.dkey, v->dkey_alt, v->order0, v->order1, c->n, 32, v->dsort_temp,
+                                       v->dsort_temp_bytes, st);
+      c->launches += 1;
+      c->lib_launches += 1 + 2 + 4;
+    }
+    launch_scan_counts(v->proj.count, v->order(), v->offsets, c->n, v->scan_temp, v->scan_temp_bytes, st);
   }
-  CHECK_LAUNCH(c, "scan");
+  CHECK_LAUNCH(c, "depth sort + scan");
   c->lib_launches += 2;
   CU_TRY(c, cudaMemcpyAsync(v->h_total, v->offsets + c->n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaStreamSynchronize(st));
@@ -753,19 +778,19 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
 
   {
     StageTimer tm(v, 2);
-    launch_emit_keys(c->n, v->I, v->offsets, v->proj, v->s.tiles_x, v->s.is_camera ? 0 : 1, v->keys0, v->vals0, st);
+    launch_emit(c->n, v->I, v->offsets, v->order(), v->proj, v->s.tiles_x, v->s.is_camera ? 0 : 1, v->keys0, v->vals0, st);
   }
-  CHECK_LAUNCH(c, "k_emit_keys");
+  CHECK_LAUNCH(c, "k_emit");
   c->launches += v->I > 0;
   int tile_bits = 1;
   while ((1LL << tile_bits) < v->n_tiles) ++tile_bits;
   v->sorted_sel = 0;
   if (v->I > 0) {
     StageTimer tm(v, 3);
-    v->sorted_sel = launch_sort_pairs(v->keys0, v->keys1, v->vals0, v->vals1, v->I, 32 + tile_bits, v->sort_temp,
+    v->sorted_sel = launch_sort_pairs(v->keys0, v->keys1, v->vals0, v->vals1, v->I, tile_bits, v->sort_temp,
                                       v->sort_temp_bytes, st);
     CHECK_LAUNCH(c, "radix sort");
-    c->lib_launches += 1 + 2 + (32 + tile_bits + 7) / 8;
+    c->lib_launches += 1 + 2 + (tile_bits + 7) / 8;
   }
   CU_TRY(c, cudaMemsetAsync(v->tile_begin, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
   CU_TRY(c, cudaMemsetAsync(v->tile_end, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
@@ -1131,12 +1156,22 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
       int rc = fetch(c, h, v->vals(), (size_t)v->I);
       if (rc) return rc;
       for (int64_t k = 0; k < v->I; ++k) d[k] = h[k];
-    } else {
-      std::vector<uint64_t> h;
+    } else if (name == "isect_tile") {
+      std::vector<uint32_t> h;
       int rc = fetch(c, h, v->keys(), (size_t)v->I);
       if (rc) return rc;
-      const bool tile = name == "isect_tile";
-      for (int64_t k = 0; k < v->I; ++k) d[k] = tile ? (int64_t)(h[k] >> 32) : (int64_t)(h[k] & 0xffffffffull);
+      for (int64_t k = 0; k < v->I; ++k) d[k] = h[k];
+    } else {  // the depth half of the reference's sort key: fp32 bits of the owner's depth_key
+      std::vector<uint32_t> h;
+      std::vector<float2> gc;
+      int rc = fetch(c, h, v->vals(), (size_t)v->I);
+      if (!rc) rc = fetch(c, gc, (const float2*)v->proj.geomC, N);
+      if (rc) return rc;
+      for (int64_t k = 0; k < v->I; ++k) {
+        uint32_t bits;
+        std::memcpy(&bits, &gc[h[k]].x, 4);
+        d[k] = bits;
+      }
     }
     return v->I;
   }

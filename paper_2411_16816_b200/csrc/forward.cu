@@ -3,8 +3,8 @@
 //   k_project<camera|lidar>   compose_at_time + project_camera/project_lidar fused, one thread per
 //                             Gaussian: scene.hpp:273-308, projection.hpp:88-118 / 140-174, plus the
 //                             tile rectangle and the packed compositing record.
-//   k_emit_keys               duplication: one (tile_id << 32 | depth_bits, source_index) pair per
-//                             intersection.
+//   k_emit                    duplication: one (tile_id, source_index) pair per intersection, emitted in depth
+//                             order.
 //   k_tile_ranges             per-tile [begin, end) slices of the sorted worklist.
 //   k_raster_fwd<camera|lidar> per-tile front-to-back compositing (Eq. 3-6).
 #include "kernels.h"
@@ -25,11 +25,14 @@ __global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor 
   else project_lidar_one(s, f);
   if (!f.visible) {
     p.count[i] = 0u;
+    p.dkey[i] = 0xffffffffu;
     return;
   }
   const int4 r = kCamera ? image_tile_range(f, s.tiles_x, s.tiles_y) : lidar_tile_range(f, s);
   const int w = r.y - r.x, h = r.w - r.z;
-  p.count[i] = (w > 0 && h > 0) ? (uint32_t)w * (uint32_t)h : 0u;
+  const uint32_t cnt = (w > 0 && h > 0) ? (uint32_t)w * (uint32_t)h : 0u;
+  p.count[i] = cnt;
+  p.dkey[i] = cnt ? __float_as_uint(f.depth) : 0xffffffffu;  // depth > 0: the bit pattern orders like the value
   p.rect[i] = r;
   p.geomA[i] = make_float4(f.mean2d[0], f.mean2d[1], f.vel[0], f.vel[1]);
   p.geomB[i] = make_float4(f.conic[0], f.conic[1] + f.conic[2], f.conic[3], f.det_ratio * f.opacity);
@@ -56,54 +59,95 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
 }
 
 // ------------------------------------------------------------------------------------------------
-// K3: key generation. One thread per intersection; the owning Gaussian is found by binary search in
-// the exclusive scan of the per-Gaussian tile counts, which makes the kernel insensitive to the
-// heavy-tailed counts (a grazing Gaussian can cover all 8,160 tiles) and keeps the key stream in
-// ascending source order, so that a stable sort yields the (tile, depth, source_index) order.
+// K3: duplication. The worklist order the reference specifies is (tile_id, depth_key, source_index)
+// (SPEC.md:220-228). It is produced with two narrow sorts instead of one wide one:
+//   1. the Gaussians are sorted by depth once (32-bit keys over N entries, stable => ties in ascending
+//      source index; culled Gaussians carry the key 0xffffffff and end up behind every visible one);
+//   2. the intersections are emitted in that order, each Gaussian's tiles in row-major order;
+//   3. the intersections are sorted by tile id alone — ceil(log2 T) bits, 2 radix passes instead of the
+//      6 a tile|depth key needs — which, being stable, leaves every tile's slice in (depth, source) order.
+// k_emit: one CTA per kEmitChunk consecutive intersections. Because every depth-sorted entry in front of
+// the culled tail owns >= 1 intersection, the chunk spans at most kEmitChunk + 1 Gaussians: their
+// offsets are staged in shared memory (relative to the chunk) and each thread locates the owner of its
+// intersections by binary search there — insensitive to the heavy-tailed counts (a grazing Gaussian can
+// cover all 8,160 tiles of a 1080p image).
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_emit_keys(int64_t n, int64_t total, const int64_t* __restrict__ offsets,
-                                                   const int4* __restrict__ rect, const float2* __restrict__ geomC,
-                                                   int tiles_x, int wrap_x, uint64_t* __restrict__ keys,
-                                                   uint32_t* __restrict__ vals) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
-  int64_t lo = 0, hi = n;  // invariant: offsets[lo] <= e < offsets[hi]
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (offsets[mid] <= e) lo = mid;
-    else hi = mid;
+constexpr int kEmitChunk = 2048;
+
+__global__ void __launch_bounds__(256)
+k_emit(int64_t n, int64_t total, const int64_t* __restrict__ offsets /* n + 1, over the depth-sorted order */,
+       const uint32_t* __restrict__ order /* depth-sorted position -> source index */, const int4* __restrict__ rect,
+       int tiles_x, int wrap_x, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  __shared__ int s_off[kEmitChunk + 2];
+  __shared__ int64_t s_k0;
+  const int64_t e0 = (int64_t)blockIdx.x * kEmitChunk;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int64_t lo = 0, hi = n;  // invariant: offsets[lo] <= e0 < offsets[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (offsets[mid] <= e0) lo = mid;
+      else hi = mid;
+    }
+    s_k0 = lo;
   }
-  const int4 r = rect[lo];
-  const int w = r.y - r.x;
-  const int local = (int)(e - offsets[lo]);
-  const int y = r.z + local / w;
-  int x = r.x + local % w;
-  if (wrap_x) x = ((x % tiles_x) + tiles_x) % tiles_x;
-  const uint32_t tile = (uint32_t)(y * tiles_x + x);
-  keys[e] = ((uint64_t)tile << 32) | (uint64_t)__float_as_uint(geomC[lo].x);
-  vals[e] = (uint32_t)lo;
+  __syncthreads();
+  const int64_t k0 = s_k0;
+  const int span = (int)min((int64_t)(kEmitChunk + 2), n + 1 - k0);
+  for (int x = tid; x < span; x += 256) {
+    const int64_t rel = offsets[k0 + x] - e0;
+    s_off[x] = (int)min(rel, (int64_t)(kEmitChunk + 1));  // only values <= kEmitChunk matter
+  }
+  __syncthreads();
+  const int chunk = (int)min((int64_t)kEmitChunk, total - e0);
+  for (int x = tid; x < chunk; x += 256) {
+    int lo = 0, hi = span - 1;  // s_off[lo] <= x < s_off[hi]  (s_off[span-1] > x: the span covers the chunk)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= x) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t src = order[k0 + lo];
+    const int4 r = rect[src];
+    const int w = r.y - r.x;
+    const int local = x - s_off[lo];
+    const int y = r.z + local / w;
+    int xx = r.x + local % w;
+    if (wrap_x) xx = ((xx % tiles_x) + tiles_x) % tiles_x;
+    keys[e0 + x] = (uint32_t)(y * tiles_x + xx);
+    vals[e0 + x] = src;
+  }
 }
 
-void launch_emit_keys(int64_t n, int64_t total, const int64_t* offsets, const ProjDev& p, int tiles_x, int wrap_x,
-                      uint64_t* keys, uint32_t* vals, cudaStream_t st) {
+void launch_emit(int64_t n, int64_t total, const int64_t* offsets, const uint32_t* order, const ProjDev& p, int tiles_x,
+                 int wrap_x, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
   if (total == 0) return;
-  const unsigned blocks = (unsigned)((total + 255) / 256);
-  k_emit_keys<<<blocks, 256, 0, st>>>(n, total, offsets, p.rect, p.geomC, tiles_x, wrap_x, keys, vals);
+  const unsigned blocks = (unsigned)((total + kEmitChunk - 1) / kEmitChunk);
+  k_emit<<<blocks, 256, 0, st>>>(n, total, offsets, order, p.rect, tiles_x, wrap_x, keys, vals);
 }
 
-__global__ void __launch_bounds__(256) k_tile_ranges(int64_t total, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) k_tile_ranges(int64_t total, const uint32_t* __restrict__ keys,
                                                      uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= total) return;
-  const uint32_t t = (uint32_t)(keys[e] >> 32);
-  if (e == 0 || (uint32_t)(keys[e - 1] >> 32) != t) tile_begin[t] = (uint32_t)e;
-  if (e == total - 1 || (uint32_t)(keys[e + 1] >> 32) != t) tile_end[t] = (uint32_t)(e + 1);
+  const uint32_t t = keys[e];
+  if (e == 0 || keys[e - 1] != t) tile_begin[t] = (uint32_t)e;
+  if (e == total - 1 || keys[e + 1] != t) tile_end[t] = (uint32_t)(e + 1);
 }
 
-void launch_tile_ranges(int64_t total, const uint64_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st) {
+void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st) {
   if (total == 0) return;
   const unsigned blocks = (unsigned)((total + 255) / 256);
   k_tile_ranges<<<blocks, 256, 0, st>>>(total, keys, tile_begin, tile_end);
+}
+
+__global__ void __launch_bounds__(256) k_iota(int64_t n, uint32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)i;
+}
+void launch_iota(int64_t n, uint32_t* out, cudaStream_t st) {
+  if (n == 0) return;
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, out);
 }
 
 // ------------------------------------------------------------------------------------------------

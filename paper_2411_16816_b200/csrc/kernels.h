@@ -40,9 +40,10 @@ constexpr int kActorAccStride = 12;
 
 // forward.cu
 void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st);
-void launch_emit_keys(int64_t n, int64_t total, const int64_t* offsets, const ProjDev& p, int tiles_x, int wrap_x,
-                      uint64_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_tile_ranges(int64_t total, const uint64_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st);
+void launch_emit(int64_t n, int64_t total, const int64_t* offsets, const uint32_t* order, const ProjDev& p, int tiles_x,
+                 int wrap_x, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st);
+void launch_iota(int64_t n, uint32_t* out, cudaStream_t st);
 // rays: one float4 per ray POSITION (azimuth, elevation, t_l, bit pattern of the original ray index), tile-major and
 // azimuth-major inside a tile (prepared at view creation); tile_order: optional CTA -> tile permutation (longest
 // worklists first), nullptr = identity
@@ -54,12 +55,13 @@ void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaS
 
 // binning.cu (device scan + radix sort)
 size_t scan_temp_bytes(int64_t n);
-void launch_scan_counts(const uint32_t* count, int64_t* offsets /* n + 1 */, int64_t n, void* temp, size_t temp_bytes,
-                        cudaStream_t st);
+// offsets[k] = sum_{k' < k} count[order[k']] for k in [0, n]; order = depth-sorted position -> source index
+void launch_scan_counts(const uint32_t* count, const uint32_t* order, int64_t* offsets /* n + 1 */, int64_t n, void* temp,
+                        size_t temp_bytes, cudaStream_t st);
 void launch_scan_i64(const int64_t* in, int64_t* out /* n + 1 */, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
 size_t sort_temp_bytes(int64_t n);
 // sorts (keys, vals) by the low `key_bits` bits, stable; returns which buffer holds the result (0 / 1)
-int launch_sort_pairs(uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int key_bits,
+int launch_sort_pairs(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int key_bits,
                       void* temp, size_t temp_bytes, cudaStream_t st);
 
 // raster_bwd.cu

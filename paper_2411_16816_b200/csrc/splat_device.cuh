@@ -82,6 +82,7 @@ struct ProjDev {
   float4* feat;     // 4 x float4 per Gaussian: camera rgb+feature, lidar feature (zero padded)
   int4* rect;       // x0, x1, y0, y1 (lidar x un-wrapped)
   uint32_t* count;  // tiles touched; 0 <=> culled
+  uint32_t* dkey;   // fp32 bits of the (positive) depth key; 0xffffffff for culled Gaussians: the depth-sort key
 };
 
 __device__ __forceinline__ float wrap_two_pi(float a) {  // common.hpp:34-38
