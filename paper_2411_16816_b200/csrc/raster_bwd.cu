@@ -1,9 +1,9 @@
 // raster_bwd.cu — compositing backward.
 //
-// One CTA per tile, the same query->thread mapping as the forward kernel. Each thread restarts from
-// its saved terminal transmittance and walks the tile's list back to front, recomputing
-// alpha with the very same instruction sequence as the forward pass (raster_common.cuh), so it
-// revisits exactly the Gaussians that were blended.
+// One CTA per tile, the same query->thread mapping, per-warp patches and conservative culling as the
+// forward kernel (raster_common.cuh). Each thread restarts from its saved terminal transmittance
+// and walks its warp's compacted list back to front, recomputing alpha with the very same
+// instruction sequence as the forward pass, so it revisits exactly the Gaussians that were blended.
 //
 // With w_i = alpha_i T_i, out_c = sum_i f_ic w_i, A = 1 - T_final:
 //   dL/df_ic     = w_i g_c
@@ -12,32 +12,112 @@
 // For lidar the rolling-shutter range r_rs = r + v_r t is one more blended channel whose upstream is
 // dL/d(range_blend); expected = range_blend / A feeds both.
 //
-// Reduction to per-Gaussian gradients (north_star (4): warp-aggregated atomics): the 26 per-pair
-// values are reduced over the 32 lanes of a warp with a transposing butterfly (31 shuffles: after
-// step k each lane keeps half of its values), which leaves value l on lane l; 26 lanes then issue
-// ONE shared-memory atomic each into the batch's accumulator, and the accumulator is flushed to
-// global memory with one RED per (tile, Gaussian, value) at the end of the batch. Warps in which no
-// lane blends the Gaussian skip everything after the ballot.
+// Reduction of the 26 per-pair values to per-Gaussian gradients, in two phases per warp:
+//   A (lane = query): the sequential part. For every list entry that some lane blends, each lane computes
+//     only THREE scalars — w, dL/dsigma (sigma = qf / 2) and its dL/drho term — and parks them in a
+//     [slot][lane] shared-memory panel (stride 33: conflict-free both ways). Every other one of the 26
+//     values is a product of one of those scalars with per-query data (g_c, t, g_D) or per-Gaussian data
+//     (conic, mean, velocity).
+//   B (lane = Gaussian): when the panel holds kChunk entries (or the batch ends) the roles flip: lanes are
+//     spread over the parked entries (32 / E lanes per entry, E = capacity rounded up to a power of two),
+//     each lane loops over its share of the 32 queries — query data is read as shared-memory broadcasts —
+//     and accumulates the 26 sums of ITS Gaussian in registers; log2(32 / E) shuffle steps join the lanes
+//     of one entry. This replaces a 31-shuffle transposing butterfly per (warp, Gaussian) and costs about
+//     half the instructions.
+// The panel carries its own copy of each parked Gaussian's record, so it survives batch boundaries and is
+// (almost) always drained full. The 26 sums of a (warp, Gaussian) leave as 26 fire-and-forget global REDs
+// (north_star (4): warp-aggregated atomics — 32 queries are folded into one RED per value). Shared-memory
+// float atomics are NOT used: on sm_100a they compile to a compare-and-swap spin loop (ATOMS.CAST.SPIN),
+// which the first version of this kernel showed to be the bottleneck (profiles/).
 #include "kernels.h"
 #include "raster_common.cuh"
 
 namespace sb {
 
-constexpr int kRed = 26;  // 16 channel grads + conic 3 + mean2d 2 + vel 3 + rho + range
+constexpr int kRed = 26;     // 16 channel grads + conic 3 + mean2d 2 + vel 3 + rho + range
+constexpr int kBatch = 256;  // Gaussians staged per batch
+constexpr int kChunk = 16;   // panel capacity per warp
+constexpr int kPanelStride = 33;
+constexpr int kPxStride = 20;  // qx qy t g_D | g_out[16]
 
-// In: v[0..31] per lane. Out: v[0] on lane l = sum over lanes of v[l].
-__device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane) {
+struct WarpScratch {
+  float w[kChunk * kPanelStride];
+  float gs[kChunk * kPanelStride];
+  float gr[kChunk * kPanelStride];
+  float px[32 * kPxStride];
+  float4 gA[kChunk], gB[kChunk];  // the parked Gaussians' records
+  uint32_t src[kChunk];
+};
+
+// Phase B for `n` parked entries (1 <= n <= kChunk).
+template <bool kCamera>
+__device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int lane, int d_f, const RasterGradDev& rg,
+                                             const ParamGradDev& pg, float& dt_local) {
+  int E = 1;  // capacity: smallest power of two >= n
+  while (E < n) E <<= 1;
+  const int e = lane & (E - 1);
+  const int g = lane / E;  // which share of the queries
+  const bool active = e < n;
+  const float4 gA = ws.gA[active ? e : 0], gB = ws.gB[active ? e : 0];
+  float acc[kRed];
 #pragma unroll
-  for (int half = 16; half >= 1; half >>= 1) {
-    const bool hi = (lane & half) != 0;
+  for (int c = 0; c < kRed; ++c) acc[c] = 0.0f;
+  float dt = 0.0f;
+  const int row = e * kPanelStride;
+  for (int pp = 0; pp < E; ++pp) {  // 32 / (32 / E) queries per lane
+    const int q = g * E + pp;
+    const float w = ws.w[row + q], gs = ws.gs[row + q], gr = ws.gr[row + q];
+    const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);  // qx qy t g_D
 #pragma unroll
-    for (int k = 0; k < half; ++k) {
-      const float send = hi ? v[k] : v[k + half];
-      const float keep = hi ? v[k + half] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const float4 gq = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride + 4 + 4 * c4]);
+      acc[4 * c4] = fmaf(w, gq.x, acc[4 * c4]);
+      acc[4 * c4 + 1] = fmaf(w, gq.y, acc[4 * c4 + 1]);
+      acc[4 * c4 + 2] = fmaf(w, gq.z, acc[4 * c4 + 2]);
+      acc[4 * c4 + 3] = fmaf(w, gq.w, acc[4 * c4 + 3]);
+    }
+    const float t = q0.z;
+    if (!kCamera) {
+      const float gw = q0.w * w;  // g_D w
+      acc[25] += gw;               // d/d range
+      acc[23] = fmaf(gw, t, acc[23]);  // d/d v_r
+    }
+    float dx = q0.x - fmaf(gA.z, t, gA.x);
+    if (!kCamera) dx = wrap_pi(dx);
+    const float dy = q0.y - fmaf(gA.w, t, gA.y);
+    const float hx = 0.5f * gs * dx, hy = 0.5f * gs * dy;
+    acc[16] = fmaf(hx, dx, acc[16]);
+    acc[17] = fmaf(hx, dy, acc[17]);
+    acc[18] = fmaf(hy, dy, acc[18]);
+    const float gdx = gs * fmaf(0.5f * gB.y, dy, gB.x * dx);
+    const float gdy = gs * fmaf(0.5f * gB.y, dx, gB.z * dy);
+    acc[19] -= gdx;
+    acc[20] -= gdy;
+    acc[21] = fmaf(-t, gdx, acc[21]);
+    acc[22] = fmaf(-t, gdy, acc[22]);
+    acc[24] += gr;
+    if (kCamera) dt -= fmaf(gA.z, gdx, gA.w * gdy);
+  }
+  // join the 32 / E lanes that worked on the same entry
+  for (int o = E; o < 32; o <<= 1) {
+#pragma unroll
+    for (int c = 0; c < kRed; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  }
+  if (active) dt_local += dt;
+  if (active && g == 0) {  // one RED per (warp, Gaussian, value)
+    const size_t src = ws.src[e];
+    float* f0 = kCamera ? pg.d_color + 3 * src : pg.d_feature + (size_t)d_f * src;
+    float* f1 = pg.d_feature + (size_t)d_f * src - (kCamera ? 3 : 0);
+    float* r0 = rg.g + kRasterGradStride * src - 16;
+#pragma unroll
+    for (int c = 0; c < kRed; ++c) {
+      if (acc[c] != 0.0f) {
+        float* dst = (c >= 16) ? r0 + c : ((kCamera && c < 3) ? f0 + c : f1 + c);
+        atomicAdd(dst, acc[c]);
+      }
     }
   }
-  return v[0];
+  __syncwarp();
 }
 
 template <bool kCamera>
@@ -48,26 +128,25 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
              const uint32_t* __restrict__ tile_order, RasterOutDev fwd, const float* __restrict__ g_blend16,
              const float* __restrict__ g_alpha, RasterGradDev rg, ParamGradDev pg, float* __restrict__ d_time_offset) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float4* sA = reinterpret_cast<float4*>(smem_raw);  // 256
-  float4* sB = sA + 256;                             // 256
-  float4* sF = sB + 256;                             // 1024
-  float2* sC = reinterpret_cast<float2*>(sF + 1024); // 256
-  float* sG = reinterpret_cast<float*>(sC + 256);    // 256 * kRed
-  uint32_t* sSrc = reinterpret_cast<uint32_t*>(sG + 256 * kRed);  // 256
-  uint8_t* sMask = reinterpret_cast<uint8_t*>(sSrc + 256);        // 256
-  uint8_t* sListAll = sMask + 256;                                // 8 x 256
-  PatchBox* sBox = reinterpret_cast<PatchBox*>(sListAll + 8 * 256);  // 8
+  float4* sA = reinterpret_cast<float4*>(smem_raw);                    // kBatch
+  float4* sB = sA + kBatch;                                            // kBatch
+  float4* sF = sB + kBatch;                                            // 4 kBatch
+  float2* sC = reinterpret_cast<float2*>(sF + 4 * kBatch);             // kBatch
+  uint32_t* sSrc = reinterpret_cast<uint32_t*>(sC + kBatch);           // kBatch
+  PatchBox* sBox = reinterpret_cast<PatchBox*>(sSrc + kBatch);         // 8
+  WarpScratch* sWs = reinterpret_cast<WarpScratch*>(sBox + 8);         // 8
+  uint8_t* sMask = reinterpret_cast<uint8_t*>(sWs + 8);                // kBatch
+  uint8_t* sListAll = sMask + kBatch;                                  // 8 x kBatch
   __shared__ int s_max_last;
   __shared__ float s_dt[8];
 
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  uint8_t* sList = sListAll + 256 * warp;
+  uint8_t* sList = sListAll + kBatch * warp;
+  WarpScratch& ws = sWs[warp];
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
   if (le <= lb) return;
-
-  for (int x = tid; x < 256 * kRed; x += 256) sG[x] = 0.0f;
 
   int64_t q_begin = 0, q_end = 1;
   if (!kCamera) { q_begin = ray_begin[tile]; q_end = ray_end[tile]; }
@@ -129,6 +208,15 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     }
     float S = 0.0f;  // sum_c g_c * suffix_c (+ g_D * suffix_r)
 
+    // per-query data for phase B (read there as broadcasts)
+    {
+      float* row = &ws.px[lane * kPxStride];
+      *reinterpret_cast<float4*>(row) = make_float4(qx, qy, t, g_D);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        *reinterpret_cast<float4*>(row + 4 + 4 * k) = make_float4(g_out[4 * k], g_out[4 * k + 1], g_out[4 * k + 2], g_out[4 * k + 3]);
+    }
+
     // warp and block maxima of `last`
     if (tid == 0) s_max_last = 0;
     __syncthreads();
@@ -136,12 +224,13 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
     if (lane == 0 && warp_last > 0) atomicMax(&s_max_last, warp_last);
-    __syncthreads();  // also publishes the patch boxes
+    __syncthreads();  // also publishes the patch boxes and the per-query rows
     const int max_last = s_max_last;
+    int n_slots = 0;  // parked entries (warp-uniform); the panel persists across batches
 
-    for (int batch = (max_last - 1) / 256; batch >= 0 && max_last > 0; --batch) {
-      const int bstart = batch * 256;
-      const int cnt = min(256, max_last - bstart);
+    for (int batch = (max_last - 1) / kBatch; batch >= 0 && max_last > 0; --batch) {
+      const int bstart = batch * kBatch;
+      const int cnt = min(kBatch, max_last - bstart);
       uint32_t mask = 0u;
       if (tid < cnt) {
         const uint32_t src = vals[lb + bstart + tid];
@@ -159,7 +248,6 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       sMask[tid] = (uint8_t)mask;
       __syncthreads();
 
-      bool touched = false;
       if (warp_last > bstart) {
         const int n_w = warp_compact(sMask, cnt, warp, lane, sList);
         for (int k = n_w - 1; k >= 0; --k) {
@@ -167,23 +255,15 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           const int pos = bstart + jj;
           AlphaEval ev;
           bool valid = false;
-          float4 gA, gB;
-          if (pos < last) {
-            gA = sA[jj];
-            gB = sB[jj];
-            valid = evaluate_alpha<!kCamera>(gA, gB, qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
-          }
+          if (pos < last) valid = evaluate_alpha<!kCamera>(sA[jj], sB[jj], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
           if (!__any_sync(0xffffffffu, valid)) continue;
-          touched = true;
 
-          float v[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = 0.0f;
+          float w = 0.0f, g_sigma = 0.0f, g_rho = 0.0f;
           if (valid) {
             const float one_m = 1.0f - ev.alpha;
             const float inv = 1.0f / one_m;
             T = T * inv;  // transmittance in front of this Gaussian
-            const float w = ev.alpha * T;
+            w = ev.alpha * T;
             float dotgf = 0.0f;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -193,55 +273,41 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
               dotgf = fmaf(g_out[4 * c + 2], f4.z, dotgf);
               dotgf = fmaf(g_out[4 * c + 3], f4.w, dotgf);
             }
-#pragma unroll
-            for (int c = 0; c < kChannels; ++c) v[c] = w * g_out[c];
             if (!kCamera) {
               const float2 c2 = sC[jj];
-              const float r_rs = fmaf(c2.y, t, c2.x);
-              dotgf = fmaf(g_D, r_rs, dotgf);
-              v[25] = g_D * w;      // d/d range
-              v[23] = g_D * w * t;  // d/d v_r
+              dotgf = fmaf(g_D, fmaf(c2.y, t, c2.x), dotgf);  // r_rs = r + v_r t
             }
             const float g_a = dotgf * T + (K - S) * inv;
             S = fmaf(w, dotgf, S);
-            if (!ev.clamped) {  // alpha == alpha_clamp is constant in every parameter
-              const float g_sigma = -ev.alpha * g_a;  // alpha = rho exp(-sigma), sigma = qf / 2
-              const float gdx = g_sigma * (gB.x * ev.dx + 0.5f * gB.y * ev.dy);
-              const float gdy = g_sigma * (gB.z * ev.dy + 0.5f * gB.y * ev.dx);
-              v[16] = g_sigma * 0.5f * ev.dx * ev.dx;
-              v[17] = g_sigma * 0.5f * ev.dx * ev.dy;
-              v[18] = g_sigma * 0.5f * ev.dy * ev.dy;
-              v[19] = -gdx;
-              v[20] = -gdy;
-              v[21] = -t * gdx;
-              v[22] = -t * gdy;
-              v[24] = ev.gauss * g_a;  // d/d rho
-              dt_local -= gA.z * gdx + gA.w * gdy;
+            if (!ev.clamped) {            // alpha == alpha_clamp is constant in every parameter
+              g_sigma = -ev.alpha * g_a;  // alpha = rho exp(-sigma), sigma = qf / 2
+              g_rho = ev.gauss * g_a;
             }
           }
-          const float r = warp_transpose_reduce(v, lane);
-          if (lane < kRed && r != 0.0f) atomicAdd(&sG[jj * kRed + lane], r);
-        }
-      }
-      // flush the batch accumulator: one RED per (tile, Gaussian, value); skipped when no warp blended anything
-      if (__syncthreads_or(touched)) {
-        for (int x = tid; x < cnt * kRed; x += 256) {
-          const float val = sG[x];
-          if (val != 0.0f) {
-            const int jj = x / kRed, l = x - jj * kRed;
-            const size_t src = sSrc[jj];
-            float* dst;
-            if (l >= 16) dst = rg.g + kRasterGradStride * src + (l - 16);
-            else if (kCamera) dst = (l < 3) ? pg.d_color + 3 * src + l : pg.d_feature + (size_t)s.d_f * src + (l - 3);
-            else dst = pg.d_feature + (size_t)s.d_f * src + l;
-            atomicAdd(dst, val);
-            sG[x] = 0.0f;
+          const int o = n_slots * kPanelStride + lane;
+          ws.w[o] = w;
+          ws.gs[o] = g_sigma;
+          ws.gr[o] = g_rho;
+          if (lane == 0) {
+            ws.gA[n_slots] = sA[jj];
+            ws.gB[n_slots] = sB[jj];
+            ws.src[n_slots] = sSrc[jj];
+          }
+          if (++n_slots == kChunk) {
+            __syncwarp();
+            reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local);
+            n_slots = 0;
           }
         }
-        __syncthreads();
       }
+      __syncthreads();  // every warp is done with the staged batch
     }
-    __syncthreads();  // patch boxes / staging are reused by the next ray pass
+    if (n_slots > 0) {  // drain what is left of this pass
+      __syncwarp();
+      reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local);
+      n_slots = 0;
+    }
+    __syncthreads();  // patch boxes / staging / per-query rows are reused by the next ray pass
   }
 
   if (kCamera) {  // SensorGrads.d_time_offset (projection.hpp:210)
@@ -257,7 +323,8 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   }
 }
 
-constexpr size_t kBwdSmem = 256 * 16 * 2 + 1024 * 16 + 256 * 8 + 256 * kRed * 4 + 256 * 4 + 256 + 8 * 256 + 8 * sizeof(PatchBox);
+constexpr size_t kBwdSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBatch * 4 + 8 * sizeof(PatchBox) +
+                            8 * sizeof(WarpScratch) + kBatch + 8 * kBatch;
 
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,

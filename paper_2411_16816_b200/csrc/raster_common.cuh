@@ -84,20 +84,21 @@ struct PatchBox {
 constexpr float kCullGamma = 3.814697265625e-06f;   // 2^-18
 constexpr float kSlackUlp = 4.76837158203125e-07f;  // 2^-21
 
-template <bool kLidar>
+// Tests patches [kP0, kP0 + kNP) of the 8; returns their bits (in place: bit p for patch p).
+template <bool kLidar, int kP0 = 0, int kNP = 8>
 __device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB, const PatchBox* __restrict__ box,
                                                float qform_max, float alpha_min) {
   const float a = gB.x, b2 = gB.y, c = gB.z, rho = gB.w;
   const float ab2 = fabsf(b2);
   // certified PSD: 4ac >= b2^2 with rounding slack on both sides
   const bool psd = a > 0.0f && c > 0.0f && (4.0f * a * c * (1.0f - 1e-6f) - b2 * b2 * (1.0f + 1e-6f) >= 0.0f);
-  if (!psd) return 0xffu;
+  if (!psd) return ((1u << kNP) - 1u) << kP0;
   // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min)
   float qmax = qform_max;
   if (alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qmax = fminf(qmax, 2.0f * __logf(rho * 1.01f / alpha_min) + 0.02f);
   uint32_t mask = 0u;
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
+  for (int p = kP0; p < kP0 + kNP; ++p) {
     const PatchBox b = box[p];
     bool keep = true;
     if (b.enabled) {
