@@ -100,7 +100,8 @@ struct splatb200_view {
   int64_t P = 0, n_tiles = 0;
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
   int64_t *ray_begin = nullptr, *ray_end = nullptr;
-  uint32_t* tile_order = nullptr;  // optional CTA -> tile permutation
+  uint32_t* tile_order = nullptr;  // CTA -> tile permutation (longest worklists first), rebuilt every forward
+  uint32_t* to_vals0 = nullptr;
   RasterOutDev out{};
   float *g_blend_stage = nullptr, *g_alpha_stage = nullptr;
   float* sensor_grads = nullptr;  // 6 + d_time_offset
@@ -194,7 +195,9 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
   dfree(v->proj.dkey); dfree(v->dkey_alt); dfree(v->order0); dfree(v->order1); dfree(v->dsort_temp);
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
-  dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end); dfree(v->tile_order);
+  dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end);
+  dfree(v->to_vals0);
+  v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
   dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
@@ -302,6 +305,7 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->out.last_idx, sizeof(int32_t) * P));
   CU_TRY(c, cudaMalloc(&v->tile_begin, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->tile_end, sizeof(uint32_t) * T));
+  CU_TRY(c, cudaMalloc(&v->to_vals0, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->sensor_grads, sizeof(float) * 8));
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, c->stream));
   CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t)));
@@ -797,6 +801,13 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   {
     StageTimer tm(v, 4);
     launch_tile_ranges(v->I, v->keys(), v->tile_begin, v->tile_end, st);
+    // CTA -> tile permutation for the compositing kernels
+    v->tile_order = nullptr;
+    if (v->I > 0 && v->n_tiles > 1) {
+      launch_tile_order((int)v->n_tiles, v->tile_begin, v->tile_end, v->to_vals0, st);
+      v->tile_order = v->to_vals0;
+      c->launches += 1;
+    }
   }
   CHECK_LAUNCH(c, "k_tile_ranges");
   c->launches += v->I > 0;

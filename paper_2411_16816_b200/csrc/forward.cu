@@ -141,6 +141,38 @@ void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begi
   k_tile_ranges<<<blocks, 256, 0, st>>>(total, keys, tile_begin, tile_end);
 }
 
+// CTA -> tile permutation: longest worklists first, so that the last wave of compositing CTAs is the cheapest.
+// One CTA, counting sort over 256 length buckets (order inside a bucket is irrelevant).
+__global__ void __launch_bounds__(1024) k_tile_order(int n_tiles, const uint32_t* __restrict__ tile_begin,
+                                                     const uint32_t* __restrict__ tile_end, uint32_t* __restrict__ order) {
+  __shared__ unsigned s_max;
+  __shared__ unsigned s_hist[256];
+  const int tid = threadIdx.x;
+  if (tid == 0) s_max = 1u;
+  if (tid < 256) s_hist[tid] = 0u;
+  __syncthreads();
+  unsigned m = 0u;
+  for (int t = tid; t < n_tiles; t += 1024) m = max(m, tile_end[t] - tile_begin[t]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) atomicMax(&s_max, m);
+  __syncthreads();
+  const float scale = 255.0f / (float)s_max;
+  for (int t = tid; t < n_tiles; t += 1024) atomicAdd(&s_hist[255 - (int)((float)(tile_end[t] - tile_begin[t]) * scale)], 1u);
+  __syncthreads();
+  if (tid == 0) {  // exclusive scan of 256 counters
+    unsigned run = 0u;
+    for (int b = 0; b < 256; ++b) { const unsigned c = s_hist[b]; s_hist[b] = run; run += c; }
+  }
+  __syncthreads();
+  for (int t = tid; t < n_tiles; t += 1024)
+    order[atomicAdd(&s_hist[255 - (int)((float)(tile_end[t] - tile_begin[t]) * scale)], 1u)] = (uint32_t)t;
+}
+void launch_tile_order(int n_tiles, const uint32_t* tile_begin, const uint32_t* tile_end, uint32_t* order, cudaStream_t st) {
+  if (n_tiles == 0) return;
+  k_tile_order<<<1, 1024, 0, st>>>(n_tiles, tile_begin, tile_end, order);
+}
+
 __global__ void __launch_bounds__(256) k_iota(int64_t n, uint32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (uint32_t)i;
@@ -166,7 +198,7 @@ void launch_iota(int64_t n, uint32_t* out, cudaStream_t st) {
 // 32 queries have all saturated stops evaluating on its own.
 // ------------------------------------------------------------------------------------------------
 template <bool kCamera>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, kCamera ? 4 : 3)
 k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
              const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
@@ -242,12 +274,8 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       if (__all_sync(0xffffffffu, done)) continue;  // this warp's 32 queries have saturated
       const int cnt = min(256u, le - base);
       const int n_w = warp_compact(sMask, cnt, warp, lane, sList[warp]);
-      for (int k = 0; k < n_w; ++k) {
-        if (__all_sync(0xffffffffu, done)) break;
-        const int j = sList[warp][k];
-        if (done) continue;
-        AlphaEval ev;
-        if (!evaluate_alpha<!kCamera>(sA[j], sB[j], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) continue;
+      const uint8_t* lst = sList[warp];
+      auto blend = [&](int j, const AlphaEval& ev) {
         const float w = __fmul_rn(ev.alpha, T);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -267,6 +295,38 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
         }
         if (T < s.transmittance_min) done = true;
+      };
+      if (kCamera) {
+        // the camera kernel is issue-bound: the plain loop has the fewest instructions
+        for (int k = 0; k < n_w; ++k) {
+          if ((k & 3) == 0 && __all_sync(0xffffffffu, done)) break;
+          const int j = lst[k];
+          AlphaEval ev;
+          if (!done && evaluate_alpha<false>(sA[j], sB[j], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j, ev);
+        }
+      } else {
+        // the lidar kernel is latency-bound (wrap + fewer resident warps' worth of work per tile): two entries per
+        // iteration with independent quadratic forms, next pair's records fetched before the current pair is blended
+        int j0 = 0, j1 = 0;
+        float4 a0, b0, a1, b1;
+        if (n_w > 0) {
+          j0 = lst[0];
+          j1 = lst[n_w > 1 ? 1 : 0];
+          a0 = sA[j0]; b0 = sB[j0]; a1 = sA[j1]; b1 = sB[j1];
+        }
+        for (int k = 0; k < n_w; k += 2) {
+          if ((k & 7) == 0 && __all_sync(0xffffffffu, done)) break;
+          const bool has1 = k + 1 < n_w;
+          const int jn0 = lst[min(k + 2, n_w - 1)], jn1 = lst[min(k + 3, n_w - 1)];  // clamped: always a valid slot
+          const float4 an0 = sA[jn0], bn0 = sB[jn0], an1 = sA[jn1], bn1 = sB[jn1];
+          float dx0, dy0, dx1, dy1;
+          const float qf0 = alpha_qform<true>(a0, b0, qx, qy, t, dx0, dy0);
+          const float qf1 = alpha_qform<true>(a1, b1, qx, qy, t, dx1, dy1);
+          AlphaEval ev;
+          if (!done && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j0, ev);
+          if (has1 && !done && alpha_finish(qf1, b1.w, dx1, dy1, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j1, ev);
+          j0 = jn0; j1 = jn1; a0 = an0; b0 = bn0; a1 = an1; b1 = bn1;
+        }
       }
     }
 

@@ -44,6 +44,7 @@ void launch_emit(int64_t n, int64_t total, const int64_t* offsets, const uint32_
                  int wrap_x, uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st);
 void launch_iota(int64_t n, uint32_t* out, cudaStream_t st);
+void launch_tile_order(int n_tiles, const uint32_t* tile_begin, const uint32_t* tile_end, uint32_t* order, cudaStream_t st);
 // rays: one float4 per ray POSITION (azimuth, elevation, t_l, bit pattern of the original ray index), tile-major and
 // azimuth-major inside a tile (prepared at view creation); tile_order: optional CTA -> tile permutation (longest
 // worklists first), nullptr = identity

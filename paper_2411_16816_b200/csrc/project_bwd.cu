@@ -105,7 +105,6 @@ __global__ void __launch_bounds__(256)
 k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGradDev rg, ParamGradDev pg,
               float* __restrict__ sensor_grads6, float* __restrict__ actor_acc, const float* __restrict__ pgin,
               float* __restrict__ cg, int64_t i_lo, int64_t i_hi) {
-  __shared__ float s_red[8];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float sg[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};  // d_vel_lin, d_vel_ang
   const bool in_range = i < sc.n && i >= i_lo && i < i_hi;
@@ -295,11 +294,25 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     for (int k = 0; k < 4; ++k) pg.d_quat[4 * i + k] += gq[k];
     }  // kMode != kProjOnly
   }
-  // SensorGrads d_vel_lin / d_vel_ang: block reduction, one atomic per block and component
+  // SensorGrads d_vel_lin / d_vel_ang: warp shuffles, one shared-memory hop, one atomic per block and component
+  if (kMode == kComposeOnly) return;  // compose_backward has no sensor terms
+  if (!__syncthreads_or(live)) return;
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    const float tot = block_sum_256(sg[k], s_red);
-    if (threadIdx.x == 0 && tot != 0.0f) atomicAdd(sensor_grads6 + k, tot);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) sg[k] += __shfl_xor_sync(0xffffffffu, sg[k], o);
+  }
+  __shared__ float s_sg[8][6];
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s_sg[threadIdx.x >> 5][k] = sg[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    float tot = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += s_sg[w][threadIdx.x];
+    if (tot != 0.0f) atomicAdd(sensor_grads6 + threadIdx.x, tot);
   }
 }
 

@@ -64,6 +64,7 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
   for (int c = 0; c < kRed; ++c) acc[c] = 0.0f;
   float dt = 0.0f;
   const int row = e * kPanelStride;
+#pragma unroll 2
   for (int pp = 0; pp < E; ++pp) {  // 32 / (32 / E) queries per lane
     const int q = g * E + pp;
     const float w = ws.w[row + q], gs = ws.gs[row + q], gr = ws.gr[row + q];
@@ -250,14 +251,8 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
 
       if (warp_last > bstart) {
         const int n_w = warp_compact(sMask, cnt, warp, lane, sList);
-        for (int k = n_w - 1; k >= 0; --k) {
-          const int jj = sList[k];
-          const int pos = bstart + jj;
-          AlphaEval ev;
-          bool valid = false;
-          if (pos < last) valid = evaluate_alpha<!kCamera>(sA[jj], sB[jj], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
-          if (!__any_sync(0xffffffffu, valid)) continue;
-
+        // park one list entry (phase A); `valid`: this lane blended it in the forward pass
+        auto park = [&](int jj, bool valid, const AlphaEval& ev) {
           float w = 0.0f, g_sigma = 0.0f, g_rho = 0.0f;
           if (valid) {
             const float one_m = 1.0f - ev.alpha;
@@ -298,6 +293,20 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
             reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local);
             n_slots = 0;
           }
+        };
+        // two entries per iteration: independent quadratic forms (ILP), parked in back-to-front order
+        for (int k = n_w - 1; k >= 0; k -= 2) {
+          const bool has1 = k >= 1;
+          const int j0 = sList[k], j1 = sList[has1 ? k - 1 : k];
+          const float4 a0 = sA[j0], b0 = sB[j0], a1 = sA[j1], b1 = sB[j1];
+          float dx0, dy0, dx1, dy1;
+          const float qf0 = alpha_qform<!kCamera>(a0, b0, qx, qy, t, dx0, dy0);
+          const float qf1 = alpha_qform<!kCamera>(a1, b1, qx, qy, t, dx1, dy1);
+          AlphaEval ev;
+          bool valid = (bstart + j0 < last) && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
+          if (__any_sync(0xffffffffu, valid)) park(j0, valid, ev);
+          valid = has1 && (bstart + j1 < last) && alpha_finish(qf1, b1.w, dx1, dy1, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
+          if (__any_sync(0xffffffffu, valid)) park(j1, valid, ev);
         }
       }
       __syncthreads();  // every warp is done with the staged batch

@@ -31,19 +31,25 @@ struct AlphaEval {
   bool clamped;
 };
 
+// Step 1 of evaluate_alpha: the offsets and the quadratic form (branch-free apart from the lidar wrap), so that two
+// list entries can be evaluated side by side for instruction-level parallelism.
 template <bool kLidar>
-__device__ __forceinline__ bool evaluate_alpha(const float4 gA /* mx my vx vy */, const float4 gB /* a b2 c rho */,
-                                               float qx, float qy, float t, float qform_max, float alpha_clamp,
-                                               float alpha_min, AlphaEval& o) {
+__device__ __forceinline__ float alpha_qform(const float4 gA /* mx my vx vy */, const float4 gB /* a b2 c rho */, float qx,
+                                             float qy, float t, float& dx, float& dy) {
   const float mx = __fmaf_rn(gA.z, t, gA.x);
   const float my = __fmaf_rn(gA.w, t, gA.y);
-  float dx = __fsub_rn(qx, mx);
+  dx = __fsub_rn(qx, mx);
   if (kLidar) dx = wrap_pi(dx);
-  const float dy = __fsub_rn(qy, my);
-  const float qf = __fmaf_rn(gB.x, __fmul_rn(dx, dx), __fmaf_rn(gB.z, __fmul_rn(dy, dy), __fmul_rn(gB.y, __fmul_rn(dx, dy))));
+  dy = __fsub_rn(qy, my);
+  return __fmaf_rn(gB.x, __fmul_rn(dx, dx), __fmaf_rn(gB.z, __fmul_rn(dy, dy), __fmul_rn(gB.y, __fmul_rn(dx, dy))));
+}
+
+// Step 2: thresholds, exp, clamp. Returns false if the pair is skipped.
+__device__ __forceinline__ bool alpha_finish(float qf, float rho, float dx, float dy, float qform_max, float alpha_clamp,
+                                             float alpha_min, AlphaEval& o) {
   if (!(qf <= qform_max)) return false;
   const float gauss = detmath::exp(__fmul_rn(-0.5f, qf));
-  float alpha = __fmul_rn(gB.w, gauss);
+  float alpha = __fmul_rn(rho, gauss);
   const bool clamped = alpha > alpha_clamp;
   if (clamped) alpha = alpha_clamp;
   if (!(alpha >= alpha_min)) return false;
@@ -51,6 +57,14 @@ __device__ __forceinline__ bool evaluate_alpha(const float4 gA /* mx my vx vy */
   return true;
 }
 
+template <bool kLidar>
+__device__ __forceinline__ bool evaluate_alpha(const float4 gA /* mx my vx vy */, const float4 gB /* a b2 c rho */,
+                                               float qx, float qy, float t, float qform_max, float alpha_clamp,
+                                               float alpha_min, AlphaEval& o) {
+  float dx, dy;
+  const float qf = alpha_qform<kLidar>(gA, gB, qx, qy, t, dx, dy);
+  return alpha_finish(qf, gB.w, dx, dy, qform_max, alpha_clamp, alpha_min, o);
+}
 
 // ------------------------------------------------------------------------------------------------
 // Per-warp conservative culling (shared by the forward and backward compositing kernels).
@@ -76,10 +90,19 @@ __device__ __forceinline__ bool evaluate_alpha(const float4 gA /* mx my vx vy */
 // simply never culled — their per-query evaluation is rounding noise that must be reproduced, not bounded.
 // ------------------------------------------------------------------------------------------------
 struct PatchBox {
-  float cx, cy, hx, hy, tc, th;
-  int enabled;  // 0: the warp's queries are too spread out (or absent) to cull against
+  float cx, cy, tc;
+  float hx2, hy2;  // half-extents plus the query-side rounding slack: h + 2^-21 (|c| + h)
+  float th2;       // th + 2^-21 (|tc| + th): multiplies |v| (travel during the patch's time span + slack on v t)
+  int enabled;     // 0: the warp's queries are too spread out (or absent) to cull against
   int pad;
 };
+
+// sqrt rounded up: MUFU.SQRT (2^-22 relative error) padded by 2^-20
+__device__ __forceinline__ float sqrt_up(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r * 1.000001f;
+}
 
 constexpr float kCullGamma = 3.814697265625e-06f;   // 2^-18
 constexpr float kSlackUlp = 4.76837158203125e-07f;  // 2^-21
@@ -96,6 +119,8 @@ __device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB,
   // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min)
   float qmax = qform_max;
   if (alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qmax = fminf(qmax, 2.0f * __logf(rho * 1.01f / alpha_min) + 0.02f);
+  const float avx = fabsf(gA.z), avy = fabsf(gA.w);
+  const float slack_x = kSlackUlp * (fabsf(gA.x) + 8.0f), slack_y = kSlackUlp * (fabsf(gA.y) + 8.0f);
   uint32_t mask = 0u;
 #pragma unroll
   for (int p = kP0; p < kP0 + kNP; ++p) {
@@ -106,18 +131,22 @@ __device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB,
       float dcx = b.cx - mxc;
       if (kLidar) dcx = wrap_pi(dcx);
       const float dcy = b.cy - myc;
-      const float tmax = fabsf(b.tc) + b.th;
-      const float Hx = b.hx + fabsf(gA.z) * b.th + kSlackUlp * (fabsf(gA.x) + fabsf(gA.z) * tmax + fabsf(b.cx) + b.hx + 8.0f);
-      const float Hy = b.hy + fabsf(gA.w) * b.th + kSlackUlp * (fabsf(gA.y) + fabsf(gA.w) * tmax + fabsf(b.cy) + b.hy + 8.0f);
+      // half-extents of the offset box: query box + rolling-shutter travel + rounding slack
+      const float Hx = fmaf(avx, b.th2, b.hx2) + slack_x;
+      const float Hy = fmaf(avy, b.th2, b.hy2) + slack_y;
       const float DX = fabsf(dcx) + Hx, DY = fabsf(dcy) + Hy;
       const bool seam = kLidar && !(DX < kPi - 1e-3f);
-      const float E = kCullGamma * (a * DX * DX + c * DY * DY + ab2 * DX * DY);
-      const float Qc = a * dcx * dcx + b2 * dcx * dcy + c * dcy * dcy;
-      const float R2 = a * Hx * Hx + ab2 * Hx * Hy + c * Hy * Hy;
-      const float s = sqrtf(fmaxf(Qc - E, 0.0f)) - sqrtf(R2) * (1.0f + 1e-5f);
-      // fp32 qf >= lb for every query of the patch (lb may be negative: rounding can push qf below zero)
-      const float lb = (s > 0.0f ? s * s * (1.0f - 1e-5f) : 0.0f) - E;
-      const bool cull = !seam && lb > qmax;
+      const float E = kCullGamma * fmaf(a * DX, DX, fmaf(c * DY, DY, ab2 * DX * DY));
+      const float Qc = fmaf(a * dcx, dcx, fmaf(c * dcy, dcy, b2 * dcx * dcy));
+      const float R2 = fmaf(a * Hx, Hx, fmaf(c * Hy, Hy, ab2 * Hx * Hy));
+      // cull <=> sqrt(A) - sqrt(R2) k > sqrt(q),  A = max(Qc - E, 0), q = max(qmax + E, 0) (1 + 2e-5), k = 1 + 1e-5
+      //      <=> A > R2 k^2 + q + 2 k sqrt(R2 q)   (both sides >= 0); the approximate sqrt is padded upwards
+      const float A = fmaxf(Qc - E, 0.0f);
+      const float qe = qmax + E;
+      const float q = fmaxf(qe, 0.0f) * (1.0f + 2e-5f);
+      const float rhs = fmaf(2.00004f, sqrt_up(R2 * q), fmaf(R2, 1.00003f, q));
+      // qe < 0: even qf = -E (the lowest value rounding allows) is beyond the alpha cut-off
+      const bool cull = !seam && ((A > rhs) || (qe < 0.0f));
       keep = !cull;
     }
     if (keep) mask |= 1u << p;
@@ -131,7 +160,7 @@ template <bool kLidar>
 __device__ __forceinline__ void warp_patch_box(bool inside, float qx, float qy, float t, int lane, PatchBox* out) {
   const unsigned act = __ballot_sync(0xffffffffu, inside);
   PatchBox b;
-  b.cx = b.cy = b.hx = b.hy = b.tc = b.th = 0.0f;
+  b.cx = b.cy = b.tc = b.hx2 = b.hy2 = b.th2 = 0.0f;
   b.enabled = 0;
   b.pad = 0;
   if (act != 0u) {
@@ -149,16 +178,22 @@ __device__ __forceinline__ void warp_patch_box(bool inside, float qx, float qy, 
       t0 = fminf(t0, __shfl_xor_sync(0xffffffffu, t0, o)); t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, o));
     }
     // centre / half-extent, padded by a few ulp so the box certainly contains every query
-    b.cx = 0.5f * (x0 + x1); b.hx = 0.5f * (x1 - x0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(x0) + fabsf(x1)) + 1e-30f;
-    b.cy = 0.5f * (y0 + y1); b.hy = 0.5f * (y1 - y0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(y0) + fabsf(y1)) + 1e-30f;
-    b.tc = 0.5f * (t0 + t1); b.th = 0.5f * (t1 - t0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
+    b.cx = 0.5f * (x0 + x1);
+    b.cy = 0.5f * (y0 + y1);
+    b.tc = 0.5f * (t0 + t1);
+    float hx = 0.5f * (x1 - x0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(x0) + fabsf(x1)) + 1e-30f;
+    const float hy = 0.5f * (y1 - y0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(y0) + fabsf(y1)) + 1e-30f;
+    const float th = 0.5f * (t1 - t0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
     b.enabled = 1;
     if (kLidar) {
       b.cx += ref;                             // back to absolute azimuth (any 2 pi offset is removed by wrap_pi later)
-      b.hx += 1e-6f * (fabsf(ref) + 8.0f);
-      if (!(b.hx < 0.5f * kPi)) b.enabled = 0;  // rays all around the circle: nothing to cull against
+      hx += 1e-6f * (fabsf(ref) + 8.0f);
+      if (!(hx < 0.5f * kPi)) b.enabled = 0;   // rays all around the circle: nothing to cull against
     }
-    if (!(b.hx == b.hx && b.hy == b.hy && b.th == b.th)) b.enabled = 0;
+    b.hx2 = hx + kSlackUlp * (fabsf(b.cx) + hx);
+    b.hy2 = hy + kSlackUlp * (fabsf(b.cy) + hy);
+    b.th2 = th + kSlackUlp * (fabsf(b.tc) + th);
+    if (!(b.hx2 == b.hx2 && b.hy2 == b.hy2 && b.th2 == b.th2)) b.enabled = 0;
   }
   if (lane == 0) *out = b;
 }
