@@ -100,16 +100,50 @@ __device__ __forceinline__ float block_sum_256(float v, float* s_red /* 8 */) {
 //   kComposeOnly    ComposeGrads (cg) + g_opacity (pgin slot 10) -> compose_backward
 // pgin: N x 11 floats by source index (g_mean2d 2, g_range, g_cov2d 4 row-major, g_velocity 3, g_opacity);
 // cg:   N x 15 floats by source index (g_mean_w 3, g_cov_w 9 row-major, g_vel_dyn_w 3).
+constexpr int kBwdSpan = 512;  // Gaussians per CTA
+
 template <bool kCamera, int kMode>
 __global__ void __launch_bounds__(256)
 k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGradDev rg, ParamGradDev pg,
               float* __restrict__ sensor_grads6, float* __restrict__ actor_acc, const float* __restrict__ pgin,
               float* __restrict__ cg, int64_t i_lo, int64_t i_hi) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // Each CTA owns kBwdSpan consecutive Gaussians. The live ones (visible for this sensor, inside [i_lo, i_hi)) are
+  // compacted into a shared list first, so that whole warps are busy even when a camera sees a quarter of the scene,
+  // while the accesses stay within a kBwdSpan-Gaussian window (coalescing friendly, unlike a gather through the depth order).
+  __shared__ int s_list[kBwdSpan];
+  __shared__ int s_warp_cnt[8];
+  __shared__ int s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kBwdSpan;
   float sg[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};  // d_vel_lin, d_vel_ang
-  const bool in_range = i < sc.n && i >= i_lo && i < i_hi;
-  const bool live = in_range && (kMode == kComposeOnly || p.count[i] != 0u);
-  if (live) {
+  {
+    // thread t looks at kBwdSpan / 256 consecutive Gaussians (keeps the list in ascending order)
+    int mine[4];
+    int n_mine = 0;
+#pragma unroll
+    for (int r = 0; r < kBwdSpan / 256; ++r) {
+      const int64_t j = base + (int64_t)tid * (kBwdSpan / 256) + r;
+      const bool ok = j < sc.n && j >= i_lo && j < i_hi && (kMode == kComposeOnly || p.count[j] != 0u);
+      if (ok) mine[n_mine++] = (int)(j - base);
+    }
+    int incl = n_mine;  // inclusive scan over the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_warp_cnt[warp] = incl;
+    __syncthreads();
+    int off = incl - n_mine;
+    for (int w = 0; w < warp; ++w) off += s_warp_cnt[w];
+    for (int r = 0; r < n_mine; ++r) s_list[off + r] = mine[r];
+    if (tid == 255) s_total = off + n_mine;
+    __syncthreads();
+  }
+  const int total = s_total;
+  for (int slot = tid; slot < total; slot += 256) {
+  const int64_t i = base + s_list[slot];
+  {
     Fwd f;
     compose_one(sc, i, f);
     float g_opacity = 0.0f;
@@ -212,7 +246,7 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     cross3(f.mu, g_u, mxg);
     cross3(s.vel_ang, g_u, wxg);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { sg[k] = -g_u[k]; sg[3 + k] = -mxg[k]; g_mu[k] += wxg[k]; }
+    for (int k = 0; k < 3; ++k) { sg[k] -= g_u[k]; sg[3 + k] -= mxg[k]; g_mu[k] += wxg[k]; }
     mat_t_vec(s.R, g_mu, g_mean_w);
     mat_t_vec(s.R, g_u, g_vdyn_w);
     if (!f.dynamic) g_vdyn_w[0] = g_vdyn_w[1] = g_vdyn_w[2] = 0.0f;  // projection.hpp:245, 283
@@ -294,9 +328,9 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     for (int k = 0; k < 4; ++k) pg.d_quat[4 * i + k] += gq[k];
     }  // kMode != kProjOnly
   }
+  }  // compacted list
   // SensorGrads d_vel_lin / d_vel_ang: warp shuffles, one shared-memory hop, one atomic per block and component
-  if (kMode == kComposeOnly) return;  // compose_backward has no sensor terms
-  if (!__syncthreads_or(live)) return;
+  if (kMode == kComposeOnly || total == 0) return;  // compose_backward has no sensor terms
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
 #pragma unroll
@@ -319,7 +353,7 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
 void launch_project_bwd(const Sensor& s, const SceneDev& sc, const ProjDev& p, const RasterGradDev& rg,
                         const ParamGradDev& pg, float* sensor_grads6, float* actor_acc, cudaStream_t st) {
   if (sc.n == 0) return;
-  const unsigned blocks = (unsigned)((sc.n + 255) / 256);
+  const unsigned blocks = (unsigned)((sc.n + kBwdSpan - 1) / kBwdSpan);
   if (s.is_camera)
     k_project_bwd<true, kFused><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc, nullptr, nullptr, 0, sc.n);
   else
@@ -330,7 +364,7 @@ void launch_project_bwd_mode(int mode, const Sensor& s, const SceneDev& sc, cons
                              float* sensor_grads6, float* actor_acc, const float* pgin, float* cg, int64_t i_lo,
                              int64_t i_hi, cudaStream_t st) {
   if (sc.n == 0) return;
-  const unsigned blocks = (unsigned)((sc.n + 255) / 256);
+  const unsigned blocks = (unsigned)((sc.n + kBwdSpan - 1) / kBwdSpan);
   RasterGradDev rg{nullptr};
 #define SB_LAUNCH(CAM, MODE) \
   k_project_bwd<CAM, MODE><<<blocks, 256, 0, st>>>(s, sc, p, rg, pg, sensor_grads6, actor_acc, pgin, cg, i_lo, i_hi)

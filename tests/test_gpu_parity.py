@@ -414,3 +414,70 @@ def test_multi_sensor_accumulation_and_reuse(ctx, op):
             ov = o.render_camera(cam, ST, workers=8)
             ov.backward(gb, ga, workers=8)
     grads_close(ctx.grads(), o64.grads(), o32.grads(), what="multi-sensor ")
+
+
+# ---- BASELINE.json full sizes ------------------------------------------------------------------------
+def _worklist_invariants(v, n_tiles):
+    """Size-independent properties of the sorted worklist: tiles ascending, depth ascending inside a
+    tile, source index ascending among equal depths; tile ranges partition the list."""
+    tile, depth, src = v.array("isect_tile"), v.array("isect_depth_bits"), v.array("isect_src")
+    tb, te = v.array("tile_begin"), v.array("tile_end")
+    assert len(tile) == v.stats()["n_intersections"]
+    if len(tile) == 0:
+        return
+    dt = np.diff(tile)
+    assert (dt >= 0).all()
+    same_tile = dt == 0
+    dd = np.diff(depth)
+    assert (dd[same_tile] >= 0).all()
+    ties = same_tile & (dd == 0)
+    assert (np.diff(src)[ties] > 0).all()
+    nonempty = te > tb
+    assert int((te - tb).sum()) == len(tile)
+    assert (tile[tb[nonempty]] == np.flatnonzero(nonempty)).all() and (tile[te[nonempty] - 1] == np.flatnonzero(nonempty)).all()
+    assert tile.max() < n_tiles
+
+
+@pytest.mark.parametrize("sensor", ["lidar128", "camera1080p"])
+def test_full_size_1m_gaussians(ctx, op, sensor):
+    """BASELINE configs 2/3 at the north-star size (1M Gaussians): worklist and contributor counts bit-exact against the
+    oracle, plus the size-independent properties: sortedness, 0 <= alpha <= 1, backward linear in the upstream
+    gradient, zero upstream => zero gradients, accumulation (+=)."""
+    n = 1_000_000
+    sc = synth.make_scene(n, seed=3)
+    ctx.upload_scene(sc)
+    if sensor == "lidar128":
+        lid = synth.lidar128()
+        rays = synth.grid_rays(lid)
+        gv = ctx.render_lidar(lid, rays, ST)
+        ov = op.OracleScene(sc, np.float32).render_lidar(lid, rays, ST, workers=op.hardware_threads())
+    else:
+        cam = synth.make_camera()
+        gv = ctx.render_camera(cam, ST)
+        ov = op.OracleScene(sc, np.float32).render_camera(cam, ST, workers=op.hardware_threads())
+    st = gv.stats()
+    _worklist_invariants(gv, st["tiles_x"] * st["tiles_y"])
+    for f in ("source_index", "isect_tile", "isect_src", "tile_begin", "tile_end", "n_contrib", "last_idx"):
+        assert np.array_equal(gv.array(f), ov.array(f)), f
+    assert_render_close(gv, ov, sensor == "lidar128")
+    a = gv.array("alpha")
+    assert a.min() >= 0.0 and a.max() <= 1.0
+    # backward: linearity / zero / accumulation
+    gb, ga = synth.upstream(gv.P, seed=1)
+    if sensor == "lidar128":
+        gb[:, 14:] = 0
+    ctx.zero_grads()
+    gv.backward(np.zeros_like(gb), np.zeros_like(ga))
+    assert all(np.all(x == 0) for k, x in ctx.grads().items() if k != "actors")
+    gv.backward(gb, ga)
+    g1 = ctx.grads()
+    ctx.zero_grads()
+    gv.backward(2.0 * gb, 2.0 * ga)
+    g2 = ctx.grads()
+    for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_color", "d_feature"):
+        x, y = g2[k].reshape(n, -1).astype(np.float64), 2.0 * g1[k].reshape(n, -1).astype(np.float64)
+        if np.abs(y).max() == 0:        # lidar renders no colour
+            assert np.abs(x).max() == 0, k
+            continue
+        rel = np.abs(x - y).max(1) / np.maximum(np.abs(y).max(1), 1e-3 * np.abs(y).max())
+        assert np.quantile(rel, 0.99) <= 1e-3 and np.isfinite(x).all(), (k, np.quantile(rel, 0.99))
