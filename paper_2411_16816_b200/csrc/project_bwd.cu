@@ -100,7 +100,7 @@ __device__ __forceinline__ float block_sum_256(float v, float* s_red /* 8 */) {
 //   kComposeOnly    ComposeGrads (cg) + g_opacity (pgin slot 10) -> compose_backward
 // pgin: N x 11 floats by source index (g_mean2d 2, g_range, g_cov2d 4 row-major, g_velocity 3, g_opacity);
 // cg:   N x 15 floats by source index (g_mean_w 3, g_cov_w 9 row-major, g_vel_dyn_w 3).
-constexpr int kBwdSpan = 512;  // Gaussians per CTA
+constexpr int kBwdSpan = 1024;  // Gaussians per CTA
 
 template <bool kCamera, int kMode>
 __global__ void __launch_bounds__(256)
