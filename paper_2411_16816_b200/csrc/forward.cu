@@ -100,22 +100,56 @@ k_emit(int64_t n, int64_t total, const int64_t* __restrict__ offsets /* n + 1, o
   }
   __syncthreads();
   const int chunk = (int)min((int64_t)kEmitChunk, total - e0);
-  for (int x = tid; x < chunk; x += 256) {
-    int lo = 0, hi = span - 1;  // s_off[lo] <= x < s_off[hi]  (s_off[span-1] > x: the span covers the chunk)
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= x) lo = mid;
-      else hi = mid;
+  // each thread emits kEmitChunk / 256 CONSECUTIVE intersections: one binary search, then a linear walk
+  constexpr int kPer = kEmitChunk / 256;
+  const int x0 = tid * kPer;
+  if (x0 >= chunk) return;
+  int lo = 0, hi = span - 1;  // s_off[lo] <= x0 < s_off[hi]  (s_off[span-1] > x: the span covers the chunk)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_off[mid] <= x0) lo = mid;
+    else hi = mid;
+  }
+  uint32_t src = order[k0 + lo];
+  int4 r = rect[src];
+  int w = r.y - r.x;
+  int next = s_off[lo + 1];
+  uint32_t kk[kPer], vv[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int x = x0 + u;
+    if (x < chunk) {
+      while (x >= next) {  // advance to the owner of x (zero-count entries cannot occur before the culled tail)
+        ++lo;
+        next = s_off[lo + 1];
+        src = order[k0 + lo];
+        r = rect[src];
+        w = r.y - r.x;
+      }
+      const int local = x - s_off[lo];
+      const int y = r.z + local / w;
+      int xx = r.x + local % w;
+      if (wrap_x) xx = ((xx % tiles_x) + tiles_x) % tiles_x;
+      kk[u] = (uint32_t)(y * tiles_x + xx);
+      vv[u] = src;
+    } else {
+      kk[u] = 0u;
+      vv[u] = 0u;
     }
-    const uint32_t src = order[k0 + lo];
-    const int4 r = rect[src];
-    const int w = r.y - r.x;
-    const int local = x - s_off[lo];
-    const int y = r.z + local / w;
-    int xx = r.x + local % w;
-    if (wrap_x) xx = ((xx % tiles_x) + tiles_x) % tiles_x;
-    keys[e0 + x] = (uint32_t)(y * tiles_x + xx);
-    vals[e0 + x] = src;
+  }
+  if (x0 + kPer <= chunk) {  // full group: 128-bit stores (e0 and x0 are multiples of 8)
+    uint4* k4 = reinterpret_cast<uint4*>(keys + e0 + x0);
+    uint4* v4 = reinterpret_cast<uint4*>(vals + e0 + x0);
+#pragma unroll
+    for (int u = 0; u < kPer; u += 4) {
+      k4[u / 4] = make_uint4(kk[u], kk[u + 1], kk[u + 2], kk[u + 3]);
+      v4[u / 4] = make_uint4(vv[u], vv[u + 1], vv[u + 2], vv[u + 3]);
+    }
+  } else {
+    for (int u = 0; u < kPer && x0 + u < chunk; ++u) {
+      keys[e0 + x0 + u] = kk[u];
+      vals[e0 + x0 + u] = vv[u];
+    }
   }
 }
 
@@ -126,18 +160,33 @@ void launch_emit(int64_t n, int64_t total, const int64_t* offsets, const uint32_
   k_emit<<<blocks, 256, 0, st>>>(n, total, offsets, order, p.rect, tiles_x, wrap_x, keys, vals);
 }
 
+// Four keys per thread (one 128-bit load); a boundary between keys e-1 and e closes tile keys[e-1] and opens keys[e].
 __global__ void __launch_bounds__(256) k_tile_ranges(int64_t total, const uint32_t* __restrict__ keys,
                                                      uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
-  const uint32_t t = keys[e];
-  if (e == 0 || keys[e - 1] != t) tile_begin[t] = (uint32_t)e;
-  if (e == total - 1 || keys[e + 1] != t) tile_end[t] = (uint32_t)(e + 1);
+  const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (e0 >= total) return;
+  uint32_t k[5];  // k[0] = key before the group
+  k[0] = e0 > 0 ? keys[e0 - 1] : 0xffffffffu;
+  if (e0 + 4 <= total) {
+    const uint4 q = *reinterpret_cast<const uint4*>(keys + e0);
+    k[1] = q.x; k[2] = q.y; k[3] = q.z; k[4] = q.w;
+  } else {
+    for (int u = 0; u < 4; ++u) k[1 + u] = e0 + u < total ? keys[e0 + u] : 0xffffffffu;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t e = e0 + u;
+    if (e < total && k[u] != k[u + 1]) {
+      tile_begin[k[u + 1]] = (uint32_t)e;
+      if (e > 0) tile_end[k[u]] = (uint32_t)e;
+    }
+  }
+  if (e0 + 4 >= total) tile_end[keys[total - 1]] = (uint32_t)total;
 }
 
 void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st) {
   if (total == 0) return;
-  const unsigned blocks = (unsigned)((total + 255) / 256);
+  const unsigned blocks = (unsigned)((total + 1023) / 1024);
   k_tile_ranges<<<blocks, 256, 0, st>>>(total, keys, tile_begin, tile_end);
 }
 
