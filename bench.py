@@ -120,9 +120,8 @@ def stage_bytes(stats: dict, camera: bool):
     return {
         "project": 48 * N + 48 * V + 64 * V + 16 * V + 4 * N,     # raw params in; geom + feat record, rect, count out
         "depth_sort_scan": 16 * N + 4 * N + 8 * N,          # (key, index) pairs read + written once; counts in, offsets out
-        "emit": 28 * V + 8 * I,                              # offsets + order + rect per visible Gaussian; (tile, index) out
-        "tile_sort": 16 * I,                                 # (tile, index) pairs read + written once
-        "tile_ranges": 4 * I + 8 * T,
+        "tile_counts": 20 * V + 4 * N + 12 * T,              # count per Gaussian, rect per visible one; tile ranges + order out
+        "tile_sort": 28 * V + 8 * I,                         # offsets + order + rect per visible Gaussian in; sorted list out
         "raster_fwd": 116 * I + 8 * T + P * b_out,
         "raster_bwd": 116 * I + 8 * T + P * (b_out + b_gin) + 104 * V,
         "project_bwd": 104 * V + 48 * V + 48 * N + 108 * N,
@@ -411,8 +410,8 @@ def run_b200(args):
     cand.sort(reverse=True)
     ms_k, sensor_k, stage_k, bytes_k = cand[0]
     kernel_name = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project", "project_bwd": "k_project_bwd",
-                   "emit": "k_emit", "tile_sort": "cub::DeviceRadixSort", "depth_sort_scan": "cub::DeviceRadixSort+DeviceScan",
-                   "tile_ranges": "k_tile_ranges"}[stage_k] + ("<camera>" if sensor_k == "camera" else "<lidar>")
+                   "tile_counts": "k_tile_hist+k_tile_scan", "tile_sort": "k_radix_pass",
+                   "depth_sort_scan": "k_radix_pass+k_count_scan"}[stage_k] + ("<camera>" if sensor_k == "camera" else "<lidar>")
     achieved = bytes_k / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")   # per-launch dram bytes from the committed ncu --set full capture

@@ -101,8 +101,8 @@ int splatb200_ctx_sync(splatb200_ctx* ctx);
  * the number of library (CUB scan / radix sort) kernels launched beside them */
 int64_t splatb200_ctx_launch_count(const splatb200_ctx* ctx);
 int64_t splatb200_ctx_library_launch_count(const splatb200_ctx* ctx);
-/* per-stage CUDA-event timing on the ctx stream (off by default). Stages: 0 project, 1 depth sort + scan, 2 emit,
- * 3 tile sort, 4 tile_ranges, 5 raster_fwd, 6 raster_bwd, 7 project_bwd. set_profiling(1) resets the running
+/* per-stage CUDA-event timing on the ctx stream (off by default). Stages: 0 project, 1 depth sort + scan, 2 tile counts
+ * (tile ranges from the rectangles), 3 tile sort (duplication fused into its first pass), 4 unused, 5 raster_fwd, 6 raster_bwd, 7 project_bwd. set_profiling(1) resets the running
  * sums; stage_ms returns the MEAN milliseconds per launch of each stage over every forward / backward of
  * the view since then (syncs). Event pairs are folded into the sums at the forward pass's own
  * synchronisation point, so enabling profiling adds no host-device synchronisation to a timed region.

@@ -347,12 +347,12 @@ class View:
     def forward(self, t_scene=0.0, stop_after=0):
         self.ctx._check(self.L.splatb200_view_forward(self.h, C.c_float(t_scene), stop_after))
 
-    STAGES = ("project", "depth_sort_scan", "emit", "tile_sort", "tile_ranges", "raster_fwd", "raster_bwd", "project_bwd")
+    STAGES = ("project", "depth_sort_scan", "tile_counts", "tile_sort", "_unused", "raster_fwd", "raster_bwd", "project_bwd")
 
     def stage_ms(self) -> dict:
         out = np.zeros(8, np.float32)
         self.ctx._check(self.L.splatb200_view_stage_ms(self.h, _p(out)))
-        return dict(zip(self.STAGES, out.astype(float).tolist()))
+        return {k: v for k, v in zip(self.STAGES, out.astype(float).tolist()) if not k.startswith("_")}
 
     def stats(self) -> dict:
         s = StatsPOD()

@@ -30,7 +30,7 @@ struct splatb200_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;      // hand-written kernels
-  int64_t lib_launches = 0;  // CUB scan / radix-sort kernels
+  int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
 
   // scene
@@ -79,9 +79,9 @@ struct splatb200_view {
   Sensor s;
   int64_t n_alloc = 0;  // Gaussians the per-source buffers are sized for
   ProjDev proj{};
-  int64_t* offsets = nullptr;
-  void* scan_temp = nullptr;
-  size_t scan_temp_bytes = 0;
+  uint32_t* offsets = nullptr;  // n + 1: exclusive scan of the tile counts in depth order, [n] = total (mod 2^32)
+  int64_t* d_total = nullptr;   // the number of intersections as counted from the tile rectangles (64-bit)
+  void* tile_ws = nullptr;     // tile-rectangle difference array + digit histograms of the tile sort
   float* rg = nullptr;
   // intersections
   int64_t isect_cap = 0;
@@ -123,7 +123,6 @@ struct splatb200_view {
   double ev_sum_ms[8] = {};
   int64_t ev_count[8] = {};
 
-  const uint32_t* keys() const { return sorted_sel ? keys1 : keys0; }
   const uint32_t* order() const { return order_sel ? order1 : order0; }
   const uint32_t* vals() const { return sorted_sel ? vals1 : vals0; }
 };
@@ -192,11 +191,11 @@ int finalize_actor_grads(splatb200_view* v) {
 
 void free_view_buffers(splatb200_view* v) {
   dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
-  dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
+  dfree(v->proj.count); dfree(v->offsets); dfree(v->rg);
   dfree(v->proj.dkey); dfree(v->dkey_alt); dfree(v->order0); dfree(v->order1); dfree(v->dsort_temp);
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
   dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end);
-  dfree(v->to_vals0);
+  dfree(v->to_vals0); dfree(v->tile_ws); dfree(v->d_total);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
   dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
@@ -242,7 +241,7 @@ int ensure_source_buffers(splatb200_view* v) {
   splatb200_ctx* c = v->ctx;
   if (v->n_alloc == c->n && v->proj.count) return SPLATB200_OK;
   dfree(v->proj.geomA); dfree(v->proj.geomB); dfree(v->proj.geomC); dfree(v->proj.feat); dfree(v->proj.rect);
-  dfree(v->proj.count); dfree(v->offsets); dfree(v->scan_temp); dfree(v->rg);
+  dfree(v->proj.count); dfree(v->offsets); dfree(v->rg);
   dfree(v->proj.dkey); dfree(v->dkey_alt); dfree(v->order0); dfree(v->order1); dfree(v->dsort_temp);
   const size_t n = (size_t)std::max<int64_t>(1, c->n);
   CU_TRY(c, cudaMalloc(&v->proj.geomA, sizeof(float4) * n));
@@ -256,13 +255,9 @@ int ensure_source_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->dkey_alt, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMalloc(&v->order0, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMalloc(&v->order1, sizeof(uint32_t) * (n + 1)));
-  launch_iota((int64_t)n + 1, v->order0, c->stream);  // [n] = n: the scan's padding element
-  launch_iota((int64_t)n + 1, v->order1, c->stream);
-  v->dsort_temp_bytes = sort_temp_bytes((int64_t)n);
+  v->dsort_temp_bytes = depth_sort_temp_bytes((int64_t)n);
   CU_TRY(c, cudaMalloc(&v->dsort_temp, v->dsort_temp_bytes));
-  CU_TRY(c, cudaMalloc(&v->offsets, sizeof(int64_t) * (n + 1)));
-  v->scan_temp_bytes = scan_temp_bytes(c->n);
-  CU_TRY(c, cudaMalloc(&v->scan_temp, v->scan_temp_bytes));
+  CU_TRY(c, cudaMalloc(&v->offsets, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMalloc(&v->rg, sizeof(float) * kRasterGradStride * n));
   CU_TRY(c, cudaMemsetAsync(v->rg, 0, sizeof(float) * kRasterGradStride * n, c->stream));
   v->n_alloc = c->n;
@@ -278,7 +273,7 @@ int ensure_isect_capacity(splatb200_view* v, int64_t total) {
   CU_TRY(c, cudaMalloc(&v->keys1, sizeof(uint32_t) * (size_t)cap));
   CU_TRY(c, cudaMalloc(&v->vals0, sizeof(uint32_t) * (size_t)cap));
   CU_TRY(c, cudaMalloc(&v->vals1, sizeof(uint32_t) * (size_t)cap));
-  v->sort_temp_bytes = sort_temp_bytes(cap);
+  v->sort_temp_bytes = tile_sort_temp_bytes(cap, v->n_tiles);
   CU_TRY(c, cudaMalloc(&v->sort_temp, v->sort_temp_bytes));
   v->isect_cap = cap;
   return SPLATB200_OK;
@@ -306,9 +301,11 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->tile_begin, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->tile_end, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->to_vals0, sizeof(uint32_t) * T));
+  CU_TRY(c, cudaMalloc(&v->tile_ws, tile_hist_bytes(v->s.tiles_x, v->s.tiles_y)));
+  CU_TRY(c, cudaMalloc(&v->d_total, sizeof(int64_t)));
   CU_TRY(c, cudaMalloc(&v->sensor_grads, sizeof(float) * 8));
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, c->stream));
-  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t)));
+  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t) * 2));
   return SPLATB200_OK;
 }
 
@@ -755,62 +752,46 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   }
   CHECK_LAUNCH(c, "k_project");
   c->launches += c->n > 0;
+  const int wrap_x = v->s.is_camera ? 0 : 1;
+  {
+    // per-tile list lengths straight from the tile rectangles: tile ranges, compositing CTA order, sort histograms
+    StageTimer tm(v, 2);
+    c->launches += launch_tile_counts(c->n, v->proj, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin, v->tile_end,
+                                      v->to_vals0, v->d_total, st);
+    v->tile_order = v->to_vals0;
+  }
+  CHECK_LAUNCH(c, "k_tile_hist / k_tile_scan");
   {
     StageTimer tm(v, 1);
     // depth order of the Gaussians (stable: ties in ascending source index), then offsets in that order
     v->order_sel = 0;
-    if (c->n > 0) {
-      launch_iota(c->n, v->order0, st);
-      v->order_sel = launch_sort_pairs(v->proj.dkey, v->dkey_alt, v->order0, v->order1, c->n, 32, v->dsort_temp,
-                                       v->dsort_temp_bytes, st);
-      c->launches += 1;
-      c->lib_launches += 1 + 2 + 4;
-    }
-    launch_scan_counts(v->proj.count, v->order(), v->offsets, c->n, v->scan_temp, v->scan_temp_bytes, st);
+    c->launches += launch_depth_sort_scan(v->proj.dkey, v->dkey_alt, v->order0, v->order1, v->proj.count, v->offsets, c->n,
+                                          v->dsort_temp, v->dsort_temp_bytes, st);
   }
   CHECK_LAUNCH(c, "depth sort + scan");
-  c->lib_launches += 2;
-  CU_TRY(c, cudaMemcpyAsync(v->h_total, v->offsets + c->n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  v->h_total[1] = 0;
+  CU_TRY(c, cudaMemcpyAsync(v->h_total, v->d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU_TRY(c, cudaMemcpyAsync(v->h_total + 1, v->offsets + c->n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaStreamSynchronize(st));
   if (c->profiling) harvest_stage_events(v);  // previous step's events have all completed by now
-  v->I = *v->h_total;
+  v->I = v->h_total[0];
   v->stage = 1;
   if (stop_after == 1) return SPLATB200_OK;
-  if (v->I > 0x7fffffffLL) return c->fail(SPLATB200_ENOMEM, "more than 2^31-1 intersections in one view");
+  if (v->I >= (1LL << 30)) return c->fail(SPLATB200_ENOMEM, "2^30 or more intersections in one view");
+  if ((int64_t)(uint32_t)v->h_total[1] != v->I)
+    return c->fail(SPLATB200_ERUNTIME, "tile histogram and count scan disagree on the number of intersections");
   rc = ensure_isect_capacity(v, v->I);
   if (rc) return rc;
 
-  {
-    StageTimer tm(v, 2);
-    launch_emit(c->n, v->I, v->offsets, v->order(), v->proj, v->s.tiles_x, v->s.is_camera ? 0 : 1, v->keys0, v->vals0, st);
-  }
-  CHECK_LAUNCH(c, "k_emit");
-  c->launches += v->I > 0;
-  int tile_bits = 1;
-  while ((1LL << tile_bits) < v->n_tiles) ++tile_bits;
   v->sorted_sel = 0;
   if (v->I > 0) {
     StageTimer tm(v, 3);
-    v->sorted_sel = launch_sort_pairs(v->keys0, v->keys1, v->vals0, v->vals1, v->I, tile_bits, v->sort_temp,
-                                      v->sort_temp_bytes, st);
-    CHECK_LAUNCH(c, "radix sort");
-    c->lib_launches += 1 + 2 + (tile_bits + 7) / 8;
+    int nl = 0;
+    v->sorted_sel = launch_tile_sort(c->n, v->I, v->offsets, v->order(), v->proj, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws,
+                                     v->keys0, v->keys1, v->vals0, v->vals1, v->sort_temp, v->sort_temp_bytes, &nl, st);
+    CHECK_LAUNCH(c, "tile sort");
+    c->launches += nl;
   }
-  CU_TRY(c, cudaMemsetAsync(v->tile_begin, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
-  CU_TRY(c, cudaMemsetAsync(v->tile_end, 0, sizeof(uint32_t) * (size_t)v->n_tiles, st));
-  {
-    StageTimer tm(v, 4);
-    launch_tile_ranges(v->I, v->keys(), v->tile_begin, v->tile_end, st);
-    // CTA -> tile permutation for the compositing kernels
-    v->tile_order = nullptr;
-    if (v->I > 0 && v->n_tiles > 1) {
-      launch_tile_order((int)v->n_tiles, v->tile_begin, v->tile_end, v->to_vals0, st);
-      v->tile_order = v->to_vals0;
-      c->launches += 1;
-    }
-  }
-  CHECK_LAUNCH(c, "k_tile_ranges");
-  c->launches += v->I > 0;
   v->stage = 2;
   if (stop_after == 2) return SPLATB200_OK;
 
@@ -1168,10 +1149,14 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
       if (rc) return rc;
       for (int64_t k = 0; k < v->I; ++k) d[k] = h[k];
     } else if (name == "isect_tile") {
-      std::vector<uint32_t> h;
-      int rc = fetch(c, h, v->keys(), (size_t)v->I);
+      // the last sort pass writes source indices only; the tile of a list position follows from the tile ranges
+      std::vector<uint32_t> tb, te;
+      int rc = fetch(c, tb, v->tile_begin, (size_t)v->n_tiles);
+      if (!rc) rc = fetch(c, te, v->tile_end, (size_t)v->n_tiles);
       if (rc) return rc;
-      for (int64_t k = 0; k < v->I; ++k) d[k] = h[k];
+      for (int64_t k = 0; k < v->I; ++k) d[k] = -1;
+      for (int64_t t = 0; t < v->n_tiles; ++t)
+        for (uint32_t k = tb[t]; k < te[t] && (int64_t)k < v->I; ++k) d[k] = t;
     } else {  // the depth half of the reference's sort key: fp32 bits of the owner's depth_key
       std::vector<uint32_t> h;
       std::vector<float2> gc;

@@ -3,9 +3,7 @@
 //   k_project<camera|lidar>   compose_at_time + project_camera/project_lidar fused, one thread per
 //                             Gaussian: scene.hpp:273-308, projection.hpp:88-118 / 140-174, plus the
 //                             tile rectangle and the packed compositing record.
-//   k_emit                    duplication: one (tile_id, source_index) pair per intersection, emitted in depth
-//                             order.
-//   k_tile_ranges             per-tile [begin, end) slices of the sorted worklist.
+//   (tile binning — depth sort, duplication, tile sort, tile ranges — lives in binning.cu)
 //   k_raster_fwd<camera|lidar> per-tile front-to-back compositing (Eq. 3-6).
 #include "kernels.h"
 #include "raster_common.cuh"
@@ -56,179 +54,6 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
   const unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
   if (s.is_camera) k_project<true><<<blocks, threads, 0, st>>>(s, sc, p);
   else k_project<false><<<blocks, threads, 0, st>>>(s, sc, p);
-}
-
-// ------------------------------------------------------------------------------------------------
-// K3: duplication. The worklist order the reference specifies is (tile_id, depth_key, source_index)
-// (SPEC.md:220-228). It is produced with two narrow sorts instead of one wide one:
-//   1. the Gaussians are sorted by depth once (32-bit keys over N entries, stable => ties in ascending
-//      source index; culled Gaussians carry the key 0xffffffff and end up behind every visible one);
-//   2. the intersections are emitted in that order, each Gaussian's tiles in row-major order;
-//   3. the intersections are sorted by tile id alone — ceil(log2 T) bits, 2 radix passes instead of the
-//      6 a tile|depth key needs — which, being stable, leaves every tile's slice in (depth, source) order.
-// k_emit: one CTA per kEmitChunk consecutive intersections. Because every depth-sorted entry in front of
-// the culled tail owns >= 1 intersection, the chunk spans at most kEmitChunk + 1 Gaussians: their
-// offsets are staged in shared memory (relative to the chunk) and each thread locates the owner of its
-// intersections by binary search there — insensitive to the heavy-tailed counts (a grazing Gaussian can
-// cover all 8,160 tiles of a 1080p image).
-// ------------------------------------------------------------------------------------------------
-constexpr int kEmitChunk = 2048;
-
-__global__ void __launch_bounds__(256)
-k_emit(int64_t n, int64_t total, const int64_t* __restrict__ offsets /* n + 1, over the depth-sorted order */,
-       const uint32_t* __restrict__ order /* depth-sorted position -> source index */, const int4* __restrict__ rect,
-       int tiles_x, int wrap_x, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  __shared__ int s_off[kEmitChunk + 2];
-  __shared__ int64_t s_k0;
-  const int64_t e0 = (int64_t)blockIdx.x * kEmitChunk;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    int64_t lo = 0, hi = n;  // invariant: offsets[lo] <= e0 < offsets[hi]
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (offsets[mid] <= e0) lo = mid;
-      else hi = mid;
-    }
-    s_k0 = lo;
-  }
-  __syncthreads();
-  const int64_t k0 = s_k0;
-  const int span = (int)min((int64_t)(kEmitChunk + 2), n + 1 - k0);
-  for (int x = tid; x < span; x += 256) {
-    const int64_t rel = offsets[k0 + x] - e0;
-    s_off[x] = (int)min(rel, (int64_t)(kEmitChunk + 1));  // only values <= kEmitChunk matter
-  }
-  __syncthreads();
-  const int chunk = (int)min((int64_t)kEmitChunk, total - e0);
-  // each thread emits kEmitChunk / 256 CONSECUTIVE intersections: one binary search, then a linear walk
-  constexpr int kPer = kEmitChunk / 256;
-  const int x0 = tid * kPer;
-  if (x0 >= chunk) return;
-  int lo = 0, hi = span - 1;  // s_off[lo] <= x0 < s_off[hi]  (s_off[span-1] > x: the span covers the chunk)
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (s_off[mid] <= x0) lo = mid;
-    else hi = mid;
-  }
-  uint32_t src = order[k0 + lo];
-  int4 r = rect[src];
-  int w = r.y - r.x;
-  int next = s_off[lo + 1];
-  uint32_t kk[kPer], vv[kPer];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int x = x0 + u;
-    if (x < chunk) {
-      while (x >= next) {  // advance to the owner of x (zero-count entries cannot occur before the culled tail)
-        ++lo;
-        next = s_off[lo + 1];
-        src = order[k0 + lo];
-        r = rect[src];
-        w = r.y - r.x;
-      }
-      const int local = x - s_off[lo];
-      const int y = r.z + local / w;
-      int xx = r.x + local % w;
-      if (wrap_x) xx = ((xx % tiles_x) + tiles_x) % tiles_x;
-      kk[u] = (uint32_t)(y * tiles_x + xx);
-      vv[u] = src;
-    } else {
-      kk[u] = 0u;
-      vv[u] = 0u;
-    }
-  }
-  if (x0 + kPer <= chunk) {  // full group: 128-bit stores (e0 and x0 are multiples of 8)
-    uint4* k4 = reinterpret_cast<uint4*>(keys + e0 + x0);
-    uint4* v4 = reinterpret_cast<uint4*>(vals + e0 + x0);
-#pragma unroll
-    for (int u = 0; u < kPer; u += 4) {
-      k4[u / 4] = make_uint4(kk[u], kk[u + 1], kk[u + 2], kk[u + 3]);
-      v4[u / 4] = make_uint4(vv[u], vv[u + 1], vv[u + 2], vv[u + 3]);
-    }
-  } else {
-    for (int u = 0; u < kPer && x0 + u < chunk; ++u) {
-      keys[e0 + x0 + u] = kk[u];
-      vals[e0 + x0 + u] = vv[u];
-    }
-  }
-}
-
-void launch_emit(int64_t n, int64_t total, const int64_t* offsets, const uint32_t* order, const ProjDev& p, int tiles_x,
-                 int wrap_x, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
-  if (total == 0) return;
-  const unsigned blocks = (unsigned)((total + kEmitChunk - 1) / kEmitChunk);
-  k_emit<<<blocks, 256, 0, st>>>(n, total, offsets, order, p.rect, tiles_x, wrap_x, keys, vals);
-}
-
-// Four keys per thread (one 128-bit load); a boundary between keys e-1 and e closes tile keys[e-1] and opens keys[e].
-__global__ void __launch_bounds__(256) k_tile_ranges(int64_t total, const uint32_t* __restrict__ keys,
-                                                     uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end) {
-  const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (e0 >= total) return;
-  uint32_t k[5];  // k[0] = key before the group
-  k[0] = e0 > 0 ? keys[e0 - 1] : 0xffffffffu;
-  if (e0 + 4 <= total) {
-    const uint4 q = *reinterpret_cast<const uint4*>(keys + e0);
-    k[1] = q.x; k[2] = q.y; k[3] = q.z; k[4] = q.w;
-  } else {
-    for (int u = 0; u < 4; ++u) k[1 + u] = e0 + u < total ? keys[e0 + u] : 0xffffffffu;
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t e = e0 + u;
-    if (e < total && k[u] != k[u + 1]) {
-      tile_begin[k[u + 1]] = (uint32_t)e;
-      if (e > 0) tile_end[k[u]] = (uint32_t)e;
-    }
-  }
-  if (e0 + 4 >= total) tile_end[keys[total - 1]] = (uint32_t)total;
-}
-
-void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st) {
-  if (total == 0) return;
-  const unsigned blocks = (unsigned)((total + 1023) / 1024);
-  k_tile_ranges<<<blocks, 256, 0, st>>>(total, keys, tile_begin, tile_end);
-}
-
-// CTA -> tile permutation: longest worklists first, so that the last wave of compositing CTAs is the cheapest.
-// One CTA, counting sort over 256 length buckets (order inside a bucket is irrelevant).
-__global__ void __launch_bounds__(1024) k_tile_order(int n_tiles, const uint32_t* __restrict__ tile_begin,
-                                                     const uint32_t* __restrict__ tile_end, uint32_t* __restrict__ order) {
-  __shared__ unsigned s_max;
-  __shared__ unsigned s_hist[256];
-  const int tid = threadIdx.x;
-  if (tid == 0) s_max = 1u;
-  if (tid < 256) s_hist[tid] = 0u;
-  __syncthreads();
-  unsigned m = 0u;
-  for (int t = tid; t < n_tiles; t += 1024) m = max(m, tile_end[t] - tile_begin[t]);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((tid & 31) == 0) atomicMax(&s_max, m);
-  __syncthreads();
-  const float scale = 255.0f / (float)s_max;
-  for (int t = tid; t < n_tiles; t += 1024) atomicAdd(&s_hist[255 - (int)((float)(tile_end[t] - tile_begin[t]) * scale)], 1u);
-  __syncthreads();
-  if (tid == 0) {  // exclusive scan of 256 counters
-    unsigned run = 0u;
-    for (int b = 0; b < 256; ++b) { const unsigned c = s_hist[b]; s_hist[b] = run; run += c; }
-  }
-  __syncthreads();
-  for (int t = tid; t < n_tiles; t += 1024)
-    order[atomicAdd(&s_hist[255 - (int)((float)(tile_end[t] - tile_begin[t]) * scale)], 1u)] = (uint32_t)t;
-}
-void launch_tile_order(int n_tiles, const uint32_t* tile_begin, const uint32_t* tile_end, uint32_t* order, cudaStream_t st) {
-  if (n_tiles == 0) return;
-  k_tile_order<<<1, 1024, 0, st>>>(n_tiles, tile_begin, tile_end, order);
-}
-
-__global__ void __launch_bounds__(256) k_iota(int64_t n, uint32_t* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (uint32_t)i;
-}
-void launch_iota(int64_t n, uint32_t* out, cudaStream_t st) {
-  if (n == 0) return;
-  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, out);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -40,11 +40,6 @@ constexpr int kActorAccStride = 12;
 
 // forward.cu
 void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st);
-void launch_emit(int64_t n, int64_t total, const int64_t* offsets, const uint32_t* order, const ProjDev& p, int tiles_x,
-                 int wrap_x, uint32_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_tile_ranges(int64_t total, const uint32_t* keys, uint32_t* tile_begin, uint32_t* tile_end, cudaStream_t st);
-void launch_iota(int64_t n, uint32_t* out, cudaStream_t st);
-void launch_tile_order(int n_tiles, const uint32_t* tile_begin, const uint32_t* tile_end, uint32_t* order, cudaStream_t st);
 // rays: one float4 per ray POSITION (azimuth, elevation, t_l, bit pattern of the original ray index), tile-major and
 // azimuth-major inside a tile (prepared at view creation); tile_order: optional CTA -> tile permutation (longest
 // worklists first), nullptr = identity
@@ -54,16 +49,23 @@ void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 
-// binning.cu (device scan + radix sort)
-size_t scan_temp_bytes(int64_t n);
-// offsets[k] = sum_{k' < k} count[order[k']] for k in [0, n]; order = depth-sorted position -> source index
-void launch_scan_counts(const uint32_t* count, const uint32_t* order, int64_t* offsets /* n + 1 */, int64_t n, void* temp,
-                        size_t temp_bytes, cudaStream_t st);
-void launch_scan_i64(const int64_t* in, int64_t* out /* n + 1 */, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
-size_t sort_temp_bytes(int64_t n);
-// sorts (keys, vals) by the low `key_bits` bits, stable; returns which buffer holds the result (0 / 1)
-int launch_sort_pairs(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int key_bits,
-                      void* temp, size_t temp_bytes, cudaStream_t st);
+// binning.cu (hand-written radix sort, scans, tile histogram — no library kernels)
+size_t depth_sort_temp_bytes(int64_t n);
+// stable sort of (dkey, position) by the 32-bit key; the sorted source indices land in order0 (dkey, dkey_alt, order1
+// are scratch), then offsets[k] = sum_{k' < k} count[order0[k']] for k in [0, n]. Returns the number of kernels launched.
+int launch_depth_sort_scan(uint32_t* dkey, uint32_t* dkey_alt, uint32_t* order0, uint32_t* order1, const uint32_t* count,
+                           uint32_t* offsets, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
+size_t tile_hist_bytes(int tiles_x, int tiles_y);
+// per-tile list lengths from the tile rectangles -> tile_begin / tile_end (0, 0 for an empty tile), the CTA -> tile
+// permutation (longest lists first), *total (device) and the digit histograms the tile sort needs (kept in tile_ws)
+int launch_tile_counts(int64_t n, const ProjDev& p, int tiles_x, int tiles_y, int wrap_x, void* tile_ws, uint32_t* tile_begin,
+                       uint32_t* tile_end, uint32_t* tile_order, int64_t* total, cudaStream_t st);
+size_t tile_sort_temp_bytes(int64_t cap, int64_t n_tiles);
+// duplication (one (tile id, source index) pair per intersection, generated in depth order inside the first pass) +
+// stable sort by tile id. Returns which of vals0 / vals1 holds the sorted source indices.
+int launch_tile_sort(int64_t n, int64_t total, const uint32_t* offsets, const uint32_t* order, const ProjDev& p, int tiles_x,
+                     int tiles_y, int wrap_x, const void* tile_ws, uint32_t* keys0, uint32_t* keys1, uint32_t* vals0,
+                     uint32_t* vals1, void* temp, size_t temp_bytes, int* launches, cudaStream_t st);
 
 // raster_bwd.cu
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
