@@ -67,6 +67,12 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   return base + inc - v;
 }
 
+// tile rectangle -> rectangle on the grid of 2^shift x 2^shift-tile blocks
+__device__ __forceinline__ int4 coarse_rect(int4 r, int shift) {
+  const int up = (1 << shift) - 1;
+  return make_int4(r.x >> shift, (r.y + up) >> shift, r.z >> shift, (r.w + up) >> shift);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------------
@@ -108,7 +114,8 @@ struct EmitSrc {
   const uint32_t* offsets; // n + 1, exclusive scan of the tile counts over the depth-sorted order (I < 2^30)
   const uint32_t* order;   // depth-sorted position -> source index
   const int4* rect;
-  int tiles_x, wrap_x;
+  int tiles_x, wrap_x;     // grid the keys are generated on (the coarse grid if shift > 0)
+  int shift;
 };
 
 constexpr int kStagePad = kRTile + kRTile / 16;  // staging index x + (x >> 4): conflict-free blocked writes, striped reads
@@ -164,7 +171,7 @@ k_radix_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ 
         else h = mid;
       }
       uint32_t src = em.order[k0 + l];
-      int4 r = em.rect[src];
+      int4 r = coarse_rect(em.rect[src], em.shift);
       int w = r.y - r.x;
       int next = s_off[l + 1];
       const int local = x0 - s_off[l];
@@ -180,7 +187,7 @@ k_radix_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ 
             ++l;
             next = s_off[l + 1];
             src = em.order[k0 + l];
-            r = em.rect[src];
+            r = coarse_rect(em.rect[src], em.shift);
             w = r.y - r.x;
             lx = 0; ly = 0;
             xw = wrapped(r.x);
@@ -390,20 +397,21 @@ k_count_scan(const uint32_t* __restrict__ count, const uint32_t* __restrict__ or
 // directly or adds a large rectangle to a 2-D difference array (4 REDs); k_tile_scan prefix-sums the latter and adds
 // the two. Each tile's two counters live in their own 128-byte line (kTileStride ints): L2 serialises atomics per line,
 // and 1,000 lidar tiles packed into 32 lines made this kernel 0.6 ms.
+// `shift` > 0 counts on the coarse grid of 2^shift x 2^shift tiles (the first level of the camera's two-level binning).
 // ------------------------------------------------------------------------------------------------
 constexpr int kTileStride = 32;  // ints per tile slot: [0] difference array, [1] direct count
 constexpr int kDirectMax = 4;    // rectangles of up to this many tiles are counted directly
 
 __global__ void __launch_bounds__(256)
-k_tile_hist(int64_t n, const uint32_t* __restrict__ count, const int4* __restrict__ rect, int tiles_x, int wrap_x,
+k_tile_hist(int64_t n, const uint32_t* __restrict__ count, const int4* __restrict__ rect, int shift, int tiles_x, int wrap_x,
             int* __restrict__ slots /* (tiles_y + 1) x (tiles_x + 1) x kTileStride */) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint32_t cnt = count[i];
-  if (cnt == 0u) return;
-  const int4 r = rect[i];
+  if (count[i] == 0u) return;
+  const int4 r = coarse_rect(rect[i], shift);
   const int W = tiles_x + 1;
   const int w = r.y - r.x;
+  const uint32_t cnt = (uint32_t)w * (uint32_t)(r.w - r.z);
   const int x0 = wrap_x ? ((r.x % tiles_x) + tiles_x) % tiles_x : r.x;  // lidar: columns are x mod M_phi, width <= M_phi
   if (cnt <= (uint32_t)kDirectMax) {
     for (int y = r.z; y < r.w; ++y) {
@@ -425,18 +433,20 @@ k_tile_hist(int64_t n, const uint32_t* __restrict__ count, const int4* __restric
   else { add(x0, tiles_x); add(0, x0 + w - tiles_x); }
 }
 
-// One CTA: 2-D prefix sum of the difference array (in place), exclusive scan over the tiles -> tile_begin / tile_end
-// (0, 0 for an empty tile, like the oracle), the digit histograms of the tile sort's passes, the total, and the
-// CTA -> tile permutation of the compositing kernels (longest lists first: counting sort over 256 length buckets).
+// One CTA: gathers the slots into a compact array (shared memory when the grid fits, a global scratch otherwise),
+// 2-D prefix sum of the difference array, exclusive scan over the tiles -> tile_begin / tile_end (0, 0 for an empty
+// tile, like the oracle), the digit histograms of the tile sort's passes, the total, and the CTA -> tile permutation of
+// the compositing kernels (longest lists first: counting sort over 256 length buckets).
 struct TilePasses {
   int n_pass;
   int shift[4], bits[4];
 };
 
 __global__ void __launch_bounds__(1024)
-k_tile_scan(int tiles_x, int tiles_y, int* __restrict__ slots, uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end,
-            uint32_t* __restrict__ hist /* n_pass x 256 */, TilePasses tp, uint32_t* __restrict__ tile_order,
-            int64_t* __restrict__ total_out) {
+k_tile_scan(int tiles_x, int tiles_y, const int* __restrict__ slots, int* __restrict__ gscratch /* 2 T ints or null */,
+            uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end, uint32_t* __restrict__ hist /* n_pass x 256 or null */,
+            TilePasses tp, uint32_t* __restrict__ tile_order /* or null */, int64_t* __restrict__ total_out) {
+  extern __shared__ int s_dyn[];
   __shared__ unsigned long long s_wsum[32];
   __shared__ uint32_t s_hist[4 * kRMaxBins];
   __shared__ unsigned s_max;
@@ -444,74 +454,60 @@ k_tile_scan(int tiles_x, int tiles_y, int* __restrict__ slots, uint32_t* __restr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = tiles_x + 1;
   const int T = tiles_x * tiles_y;
+  int* a = gscratch ? gscratch : s_dyn;  // T: difference array -> list lengths
+  int* dir = a + T;                       // T: directly counted rectangles
   for (int i = tid; i < 4 * kRMaxBins; i += 1024) s_hist[i] = 0u;
   if (tid < 256) s_len[tid] = 0u;
   if (tid == 0) s_max = 1u;
-  // rows: a warp per row, 8 x 32 columns loaded before the scans so that the loads overlap
+  for (int t = tid; t < T; t += 1024) {
+    const size_t g = (size_t)((t / tiles_x) * W + (t % tiles_x)) * kTileStride;
+    a[t] = slots[g];
+    dir[t] = slots[g + 1];
+  }
+  __syncthreads();
+  // rows: a warp per row, 32 columns per step
   for (int y = warp; y < tiles_y; y += 32) {
     int carry = 0;
-    for (int xb = 0; xb < tiles_x; xb += 256) {
-      int v[8];
+    for (int xb = 0; xb < tiles_x; xb += 32) {
+      const int x = xb + lane;
+      int v = x < tiles_x ? a[y * tiles_x + x] : 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int x = xb + 32 * k + lane;
-        v[k] = x < tiles_x ? slots[(size_t)(y * W + x) * kTileStride] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int x = xb + 32 * k + lane;
-        int a = v[k];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, a, o);
-          if (lane >= o) a += u;
-        }
-        a += carry;
-        if (x < tiles_x) slots[(size_t)(y * W + x) * kTileStride] = a;
-        carry = __shfl_sync(0xffffffffu, a, 31);
-      }
+      v += carry;
+      if (x < tiles_x) a[y * tiles_x + x] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
     }
   }
   __syncthreads();
-  // columns: a warp per column, 8 x 32 rows per step
+  // columns: a warp per column, 32 rows per step; the directly counted rectangles are folded in on the way
   for (int x = warp; x < tiles_x; x += 32) {
     int carry = 0;
-    for (int yb = 0; yb < tiles_y; yb += 256) {
-      int v[8];
+    for (int yb = 0; yb < tiles_y; yb += 32) {
+      const int y = yb + lane;
+      int v = y < tiles_y ? a[y * tiles_x + x] : 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int y = yb + 32 * k + lane;
-        v[k] = y < tiles_y ? slots[(size_t)(y * W + x) * kTileStride] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int y = yb + 32 * k + lane;
-        int a = v[k];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, a, o);
-          if (lane >= o) a += u;
-        }
-        a += carry;
-        // fold the directly counted rectangles in: slot [0] now holds the tile's list length
-        if (y < tiles_y) slots[(size_t)(y * W + x) * kTileStride] = a + slots[(size_t)(y * W + x) * kTileStride + 1];
-        carry = __shfl_sync(0xffffffffu, a, 31);
-      }
+      v += carry;
+      if (y < tiles_y) a[y * tiles_x + x] = v + dir[y * tiles_x + x];
+      carry = __shfl_sync(0xffffffffu, v, 31);
     }
   }
   __syncthreads();
-  // exclusive scan over the tiles (row-major ids): each thread owns a run of consecutive tiles, 8 at a time in registers
+  // exclusive scan over the tiles (row-major ids): each thread owns a run of consecutive tiles
   const int per = (T + 1023) / 1024;
   const int t0 = tid * per, t1 = min(T, t0 + per);
-  auto len_of = [&](int t) { return (unsigned)slots[(size_t)((t / tiles_x) * W + (t % tiles_x)) * kTileStride]; };
   unsigned long long mine = 0ull;
   unsigned mx = 0u;
-  for (int tb = t0; tb < t1; tb += 8) {
-    unsigned c[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = tb + k < t1 ? len_of(tb + k) : 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) { mine += c[k]; mx = max(mx, c[k]); }
+  for (int t = t0; t < t1; ++t) {
+    const unsigned c = (unsigned)a[t];
+    mine += c;
+    mx = max(mx, c);
   }
   unsigned long long inc = mine;
 #pragma unroll
@@ -533,39 +529,93 @@ k_tile_scan(int tiles_x, int tiles_y, int* __restrict__ slots, uint32_t* __restr
   if (tid == 0) *total_out = (int64_t)total;
   const float scale = 255.0f / (float)s_max;
   unsigned long long run = base + inc - mine;
-  for (int tb = t0; tb < t1; tb += 8) {
-    unsigned c[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = tb + k < t1 ? len_of(tb + k) : 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = tb + k;
-      if (t < t1) {
-        tile_begin[t] = c[k] ? (uint32_t)run : 0u;
-        tile_end[t] = c[k] ? (uint32_t)(run + c[k]) : 0u;
-        run += c[k];
-        if (c[k]) {
-          for (int p = 0; p < tp.n_pass; ++p)
-            atomicAdd(&s_hist[p * kRMaxBins + (((uint32_t)t >> tp.shift[p]) & ((1u << tp.bits[p]) - 1u))], c[k]);
-        }
-        atomicAdd(&s_len[255 - (int)((float)c[k] * scale)], 1u);
-      }
+  for (int t = t0; t < t1; ++t) {
+    const unsigned c = (unsigned)a[t];
+    tile_begin[t] = c ? (uint32_t)run : 0u;
+    tile_end[t] = c ? (uint32_t)(run + c) : 0u;
+    run += c;
+    if (c && hist) {
+      for (int p = 0; p < tp.n_pass; ++p)
+        atomicAdd(&s_hist[p * kRMaxBins + (((uint32_t)t >> tp.shift[p]) & ((1u << tp.bits[p]) - 1u))], c);
     }
+    atomicAdd(&s_len[255 - (int)((float)c * scale)], 1u);
   }
   __syncthreads();
-  for (int i = tid; i < tp.n_pass * kRMaxBins; i += 1024) hist[i] = s_hist[i];
+  if (hist)
+    for (int i = tid; i < tp.n_pass * kRMaxBins; i += 1024) hist[i] = s_hist[i];
+  if (!tile_order) return;
   if (tid == 0) {  // exclusive scan of the 256 length buckets
     unsigned r = 0u;
     for (int b = 0; b < 256; ++b) { const unsigned c = s_len[b]; s_len[b] = r; r += c; }
   }
   __syncthreads();
-  for (int tb = t0; tb < t1; tb += 8) {
-    unsigned c[8];
+  for (int t = t0; t < t1; ++t)
+    tile_order[atomicAdd(&s_len[255 - (int)((float)(unsigned)a[t] * scale)], 1u)] = (uint32_t)t;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Second level of the camera's binning: one CTA per 8 x 8-tile block walks the block's depth-ordered list (the
+// output of the coarse sort) once and appends every Gaussian to the lists of the tiles its rectangle covers. Warp w
+// owns tile row w of the block: its 8 list cursors live in registers, list order is kept by ballot ranks, and every
+// store instruction writes a run of consecutive source indices. A Gaussian covering all 8,160 tiles of a 1080p image
+// is handled as 135 coarse entries + 8,160 four-byte stores instead of 8,160 sorted key-value pairs.
+// ------------------------------------------------------------------------------------------------
+constexpr int kSuperShift = 3;
+constexpr int kSuper = 1 << kSuperShift;
+
+__global__ void __launch_bounds__(256)
+k_expand(int stiles_x, int tiles_x, int tiles_y, const uint32_t* __restrict__ super_begin, const uint32_t* __restrict__ super_end,
+         const uint32_t* __restrict__ cvals, const int4* __restrict__ rect, const uint32_t* __restrict__ tile_begin,
+         const uint32_t* __restrict__ super_order, uint32_t* __restrict__ vals) {
+  __shared__ uint32_t s_src[256];
+  __shared__ unsigned long long s_mask[256];
+  const int st = super_order ? (int)super_order[blockIdx.x] : (int)blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lb = super_begin[st], le = super_end[st];
+  if (le <= lb) return;
+  const int bx = (st % stiles_x) * kSuper, by = (st / stiles_x) * kSuper;
+  uint32_t pos[kSuper];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = tb + k < t1 ? len_of(tb + k) : 0u;
+  for (int c = 0; c < kSuper; ++c) {
+    const int tx = bx + c, ty = by + warp;
+    pos[c] = (tx < tiles_x && ty < tiles_y) ? tile_begin[ty * tiles_x + tx] : 0u;
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  // software pipeline: the next chunk's (source index -> rectangle) gather is in flight while this one is expanded
+  uint32_t src_n = 0u;
+  int4 r_n = make_int4(0, 0, 0, 0);
+  if (lb + tid < le) { src_n = cvals[lb + tid]; r_n = rect[src_n]; }
+  for (uint32_t base = lb; base < le; base += 256) {
+    const int cnt = (int)min(256u, le - base);
+    unsigned long long m = 0ull;
+    if (tid < cnt) {
+      const int xlo = max(r_n.x - bx, 0), xhi = min(r_n.y - bx, kSuper);
+      const int ylo = max(r_n.z - by, 0), yhi = min(r_n.w - by, kSuper);
+      if (xlo < xhi && ylo < yhi) {
+        const unsigned long long xbits = ((1u << xhi) - 1u) & ~((1u << xlo) - 1u);
+        const unsigned long long rows_hi = yhi >= kSuper ? ~0ull : ((1ull << (8 * yhi)) - 1ull);
+        const unsigned long long rows_lo = (1ull << (8 * ylo)) - 1ull;
+        m = (xbits * 0x0101010101010101ull) & rows_hi & ~rows_lo;
+      }
+    }
+    s_src[tid] = src_n;
+    s_mask[tid] = m;
+    __syncthreads();
+    const uint32_t nxt = base + 256 + tid;
+    if (nxt < le) { src_n = cvals[nxt]; r_n = rect[src_n]; }
+    for (int k = 0; k < cnt; k += 32) {
+      const int e = k + lane;
+      const uint32_t m8 = e < cnt ? (uint32_t)(s_mask[e] >> (8 * warp)) & 0xffu : 0u;
+      const uint32_t src = s_src[e & 255];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (tb + k < t1) tile_order[atomicAdd(&s_len[255 - (int)((float)c[k] * scale)], 1u)] = (uint32_t)(tb + k);
+      for (int c = 0; c < kSuper; ++c) {
+        const bool bit = (m8 >> c) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, bit);
+        if (bit) vals[pos[c] + __popc(b & lt)] = src;
+        pos[c] += __popc(b);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -587,6 +637,24 @@ void launch_pass(const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t*
   k_radix_pass<kSrc, kWriteKeys><<<(unsigned)radix_tiles(n), kRThreads, kRadixSmem, st>>>(ki, vi, ko, vo, n, shift, bits, hist,
                                                                                           state, ticket, err, em);
 }
+
+// passes of a tile-id sort: ceil(bits / 8) passes of (almost) equal width
+TilePasses tile_passes(int64_t n_tiles) {
+  int bits = 1;
+  while ((1LL << bits) < n_tiles) ++bits;
+  TilePasses tp{};
+  tp.n_pass = (bits + 7) / 8;
+  int shift = 0;
+  for (int p = 0; p < tp.n_pass; ++p) {
+    const int b = (bits - shift + (tp.n_pass - p) - 1) / (tp.n_pass - p);
+    tp.shift[p] = shift;
+    tp.bits[p] = b;
+    shift += b;
+  }
+  return tp;
+}
+
+constexpr size_t kScanSmemMax = 200 * 1024;
 }  // namespace
 
 // workspace of the depth sort + count scan over n Gaussians
@@ -622,41 +690,44 @@ int launch_depth_sort_scan(uint32_t* dkey, uint32_t* dkey_alt, uint32_t* order0,
   return 6;  // kernels launched
 }
 
-// passes of the tile-id sort: ceil(bits / 8) passes of (almost) equal width
-static TilePasses tile_passes(int64_t n_tiles) {
-  int bits = 1;
-  while ((1LL << bits) < n_tiles) ++bits;
-  TilePasses tp{};
-  tp.n_pass = (bits + 7) / 8;
-  int shift = 0;
-  for (int p = 0; p < tp.n_pass; ++p) {
-    const int b = (bits - shift + (tp.n_pass - p) - 1) / (tp.n_pass - p);
-    tp.shift[p] = shift;
-    tp.bits[p] = b;
-    shift += b;
-  }
-  return tp;
-}
+int super_shift() { return kSuperShift; }
 
+// Workspace of launch_tile_counts for a grid of tiles_x x tiles_y tiles: padded slots, compact scratch, histograms.
 static size_t tile_slot_bytes(int tiles_x, int tiles_y) {
   return sizeof(int) * kTileStride * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1);
 }
-size_t tile_hist_bytes(int tiles_x, int tiles_y) { return tile_slot_bytes(tiles_x, tiles_y) + sizeof(uint32_t) * 4 * 256 + 64; }
+static size_t tile_scratch_bytes(int tiles_x, int tiles_y) { return sizeof(int) * 2 * (size_t)tiles_x * (size_t)tiles_y; }
+size_t tile_hist_bytes(int tiles_x, int tiles_y) {
+  return tile_slot_bytes(tiles_x, tiles_y) + tile_scratch_bytes(tiles_x, tiles_y) + sizeof(uint32_t) * 4 * 256 + 64;
+}
+static const uint32_t* tile_ws_hist(const void* ws, int tiles_x, int tiles_y) {
+  return (const uint32_t*)((const char*)ws + tile_slot_bytes(tiles_x, tiles_y) + tile_scratch_bytes(tiles_x, tiles_y));
+}
 
-// tile_ws: tile_hist_bytes(); fills tile_begin / tile_end / tile_order and *total (device), keeps the pass histograms
-int launch_tile_counts(int64_t n, const ProjDev& p, int tiles_x, int tiles_y, int wrap_x, void* tile_ws, uint32_t* tile_begin,
-                       uint32_t* tile_end, uint32_t* tile_order, int64_t* total, cudaStream_t st) {
-  const size_t diff_bytes = tile_slot_bytes(tiles_x, tiles_y);
-  cudaMemsetAsync(tile_ws, 0, diff_bytes, st);
-  int* diff = (int*)tile_ws;
-  uint32_t* hist = (uint32_t*)((char*)tile_ws + diff_bytes);
+// Per-tile list lengths on the grid of 2^shift-tile blocks (shift 0: the tiles themselves) from the tile rectangles
+// -> tile_begin / tile_end (0, 0 for an empty tile), the CTA -> tile permutation (longest lists first; optional),
+// *total (device) and the digit histograms a sort by tile id needs (kept in tile_ws).
+int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int tiles_y, int wrap_x, void* tile_ws,
+                       uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, cudaStream_t st) {
+  const size_t slot_bytes = tile_slot_bytes(tiles_x, tiles_y);
+  cudaMemsetAsync(tile_ws, 0, slot_bytes, st);
+  int* slots = (int*)tile_ws;
+  int* scratch = (int*)((char*)tile_ws + slot_bytes);
+  uint32_t* hist = (uint32_t*)tile_ws_hist(tile_ws, tiles_x, tiles_y);
   int launches = 0;
   if (n > 0) {
-    k_tile_hist<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p.count, p.rect, tiles_x, wrap_x, diff);
+    k_tile_hist<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p.count, p.rect, shift, tiles_x, wrap_x, slots);
     ++launches;
   }
-  k_tile_scan<<<1, 1024, 0, st>>>(tiles_x, tiles_y, diff, tile_begin, tile_end, hist, tile_passes((int64_t)tiles_x * tiles_y),
-                                  tile_order, total);
+  const size_t smem = tile_scratch_bytes(tiles_x, tiles_y);
+  const bool in_smem = smem <= kScanSmemMax;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmemMax);
+    attr = true;
+  }
+  k_tile_scan<<<1, 1024, in_smem ? smem : 0, st>>>(tiles_x, tiles_y, slots, in_smem ? nullptr : scratch, tile_begin, tile_end, hist,
+                                                   tile_passes((int64_t)tiles_x * tiles_y), tile_order, total);
   return launches + 1;
 }
 
@@ -667,22 +738,23 @@ size_t tile_sort_temp_bytes(int64_t cap, int64_t n_tiles) {
   return sizeof(uint32_t) * words + 64;
 }
 
-// Emits the (tile id, source index) stream in depth order and sorts it by tile id (stable). Returns which of
-// vals0 / vals1 holds the sorted source indices (0 / 1); *launches receives the kernel count.
-int launch_tile_sort(int64_t n, int64_t total, const uint32_t* offsets, const uint32_t* order, const ProjDev& p, int tiles_x,
-                     int tiles_y, int wrap_x, const void* tile_ws, uint32_t* keys0, uint32_t* keys1, uint32_t* vals0,
+// Emits the (tile id, source index) stream in depth order and sorts it by tile id (stable), on the grid of
+// 2^shift-tile blocks. Returns which of vals0 / vals1 holds the sorted source indices (0 / 1); *launches receives the
+// kernel count. tile_ws: the workspace launch_tile_counts filled for the same grid.
+int launch_tile_sort(int64_t n, int64_t total, const uint32_t* offsets, const uint32_t* order, const ProjDev& p, int shift,
+                     int tiles_x, int tiles_y, int wrap_x, const void* tile_ws, uint32_t* keys0, uint32_t* keys1, uint32_t* vals0,
                      uint32_t* vals1, void* temp, size_t temp_bytes, int* launches, cudaStream_t st) {
   *launches = 0;
   if (total <= 0) return 0;
   const TilePasses tp = tile_passes((int64_t)tiles_x * tiles_y);
-  const uint32_t* hist = (const uint32_t*)((const char*)tile_ws + tile_slot_bytes(tiles_x, tiles_y));
+  const uint32_t* hist = tile_ws_hist(tile_ws, tiles_x, tiles_y);
   const size_t tiles = (size_t)radix_tiles(total);
   size_t words = kHdrWords;
   for (int q = 0; q < tp.n_pass; ++q) words += tiles << tp.bits[q];
   cudaMemsetAsync(temp, 0, std::min(temp_bytes, sizeof(uint32_t) * words), st);
   uint32_t* hdr = (uint32_t*)temp;
   uint32_t* state = hdr + kHdrWords;
-  EmitSrc em{n, offsets, order, p.rect, tiles_x, wrap_x};
+  EmitSrc em{n, offsets, order, p.rect, tiles_x, wrap_x, shift};
   uint32_t* k[2] = {keys0, keys1};
   uint32_t* v[2] = {vals0, vals1};
   int cur = 0;  // buffer holding the current pass's input (pass 0 has none)
@@ -702,6 +774,15 @@ int launch_tile_sort(int64_t n, int64_t total, const uint32_t* offsets, const ui
     ++*launches;
   }
   return cur;
+}
+
+// Second level of the two-level binning: expands the block lists (cvals, sorted by block) into the tile lists.
+void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, const uint32_t* super_begin, const uint32_t* super_end,
+                   const uint32_t* cvals, const ProjDev& p, const uint32_t* tile_begin, const uint32_t* super_order, uint32_t* vals,
+                   cudaStream_t st) {
+  const int blocks = stiles_x * stiles_y;
+  if (blocks <= 0) return;
+  k_expand<<<blocks, 256, 0, st>>>(stiles_x, tiles_x, tiles_y, super_begin, super_end, cvals, p.rect, tile_begin, super_order, vals);
 }
 
 }  // namespace sb

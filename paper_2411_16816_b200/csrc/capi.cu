@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -96,6 +97,15 @@ struct splatb200_view {
   size_t sort_temp_bytes = 0;
   int sorted_sel = 0;
   uint32_t *tile_begin = nullptr, *tile_end = nullptr;
+  // two-level binning (cameras): lists per block of 8 x 8 tiles first, expanded into the tile lists
+  bool two_level = false;
+  int stiles_x = 0, stiles_y = 0;
+  uint32_t *super_begin = nullptr, *super_end = nullptr, *super_order = nullptr;
+  void* tile_ws_c = nullptr;
+  int64_t* d_total_c = nullptr;
+  uint32_t* vals_fine = nullptr;  // the tile lists (two-level mode; otherwise the sorted vals0 / vals1)
+  int64_t fine_cap = 0;
+  int64_t I_sort = 0;             // entries the radix sort handles: block-level intersections, or I
   // queries
   int64_t P = 0, n_tiles = 0;
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
@@ -124,7 +134,8 @@ struct splatb200_view {
   int64_t ev_count[8] = {};
 
   const uint32_t* order() const { return order_sel ? order1 : order0; }
-  const uint32_t* vals() const { return sorted_sel ? vals1 : vals0; }
+  const uint32_t* vals() const { return two_level ? vals_fine : (sorted_sel ? vals1 : vals0); }
+  const uint32_t* sorted_vals() const { return sorted_sel ? vals1 : vals0; }
 };
 
 #define CU_TRY(ctx, call)                                                                             \
@@ -196,6 +207,8 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
   dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end);
   dfree(v->to_vals0); dfree(v->tile_ws); dfree(v->d_total);
+  dfree(v->super_begin); dfree(v->super_end); dfree(v->super_order); dfree(v->tile_ws_c); dfree(v->d_total_c);
+  dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
   dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
@@ -251,6 +264,12 @@ int ensure_source_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->proj.rect, sizeof(int4) * n));
   CU_TRY(c, cudaMalloc(&v->proj.count, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMemsetAsync(v->proj.count, 0, sizeof(uint32_t) * (n + 1), c->stream));
+  dfree(v->proj.ccount);
+  v->proj.cshift = 0;
+  if (v->two_level) {
+    CU_TRY(c, cudaMalloc(&v->proj.ccount, sizeof(uint32_t) * (n + 1)));
+    v->proj.cshift = super_shift();
+  }
   CU_TRY(c, cudaMalloc(&v->proj.dkey, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMalloc(&v->dkey_alt, sizeof(uint32_t) * (n + 1)));
   CU_TRY(c, cudaMalloc(&v->order0, sizeof(uint32_t) * (n + 1)));
@@ -264,18 +283,26 @@ int ensure_source_buffers(splatb200_view* v) {
   return SPLATB200_OK;
 }
 
-int ensure_isect_capacity(splatb200_view* v, int64_t total) {
+// n_sort: entries the radix sort handles (block-level intersections in two-level mode, else = n_fine)
+int ensure_isect_capacity(splatb200_view* v, int64_t n_sort, int64_t n_fine) {
   splatb200_ctx* c = v->ctx;
-  if (total <= v->isect_cap) return SPLATB200_OK;
-  dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
-  const int64_t cap = total + total / 4 + 1024;
-  CU_TRY(c, cudaMalloc(&v->keys0, sizeof(uint32_t) * (size_t)cap));
-  CU_TRY(c, cudaMalloc(&v->keys1, sizeof(uint32_t) * (size_t)cap));
-  CU_TRY(c, cudaMalloc(&v->vals0, sizeof(uint32_t) * (size_t)cap));
-  CU_TRY(c, cudaMalloc(&v->vals1, sizeof(uint32_t) * (size_t)cap));
-  v->sort_temp_bytes = tile_sort_temp_bytes(cap, v->n_tiles);
-  CU_TRY(c, cudaMalloc(&v->sort_temp, v->sort_temp_bytes));
-  v->isect_cap = cap;
+  if (n_sort > v->isect_cap) {
+    dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
+    const int64_t cap = n_sort + n_sort / 4 + 1024;
+    CU_TRY(c, cudaMalloc(&v->keys0, sizeof(uint32_t) * (size_t)cap));
+    CU_TRY(c, cudaMalloc(&v->keys1, sizeof(uint32_t) * (size_t)cap));
+    CU_TRY(c, cudaMalloc(&v->vals0, sizeof(uint32_t) * (size_t)cap));
+    CU_TRY(c, cudaMalloc(&v->vals1, sizeof(uint32_t) * (size_t)cap));
+    v->sort_temp_bytes = tile_sort_temp_bytes(cap, v->two_level ? (int64_t)v->stiles_x * v->stiles_y : v->n_tiles);
+    CU_TRY(c, cudaMalloc(&v->sort_temp, v->sort_temp_bytes));
+    v->isect_cap = cap;
+  }
+  if (v->two_level && n_fine > v->fine_cap) {
+    dfree(v->vals_fine);
+    const int64_t cap = n_fine + n_fine / 4 + 1024;
+    CU_TRY(c, cudaMalloc(&v->vals_fine, sizeof(uint32_t) * (size_t)cap));
+    v->fine_cap = cap;
+  }
   return SPLATB200_OK;
 }
 
@@ -303,9 +330,20 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->to_vals0, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->tile_ws, tile_hist_bytes(v->s.tiles_x, v->s.tiles_y)));
   CU_TRY(c, cudaMalloc(&v->d_total, sizeof(int64_t)));
+  if (v->two_level) {
+    const int sh = super_shift();
+    v->stiles_x = (v->s.tiles_x + (1 << sh) - 1) >> sh;
+    v->stiles_y = (v->s.tiles_y + (1 << sh) - 1) >> sh;
+    const size_t Ts = (size_t)std::max(1, v->stiles_x * v->stiles_y);
+    CU_TRY(c, cudaMalloc(&v->super_begin, sizeof(uint32_t) * Ts));
+    CU_TRY(c, cudaMalloc(&v->super_end, sizeof(uint32_t) * Ts));
+    CU_TRY(c, cudaMalloc(&v->super_order, sizeof(uint32_t) * Ts));
+    CU_TRY(c, cudaMalloc(&v->tile_ws_c, tile_hist_bytes(v->stiles_x, v->stiles_y)));
+    CU_TRY(c, cudaMalloc(&v->d_total_c, sizeof(int64_t)));
+  }
   CU_TRY(c, cudaMalloc(&v->sensor_grads, sizeof(float) * 8));
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, c->stream));
-  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t) * 2));
+  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t) * 3));
   return SPLATB200_OK;
 }
 
@@ -569,6 +607,7 @@ extern "C" int splatb200_view_create_camera(splatb200_ctx* c, const splatb200_ca
   v->s.tiles_y = (cam->height + kTile - 1) / kTile;
   v->P = (int64_t)cam->width * cam->height;
   v->n_tiles = (int64_t)v->s.tiles_x * v->s.tiles_y;
+  v->two_level = std::getenv("SPLATB200_ONE_LEVEL") == nullptr;  // cameras bin in two levels (debug switch: one level)
   c->views.push_back(v);
   int rc = splatb200_view_set_camera(v, cam);
   if (!rc) rc = alloc_query_buffers(v);
@@ -753,42 +792,58 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   CHECK_LAUNCH(c, "k_project");
   c->launches += c->n > 0;
   const int wrap_x = v->s.is_camera ? 0 : 1;
+  const int sh = v->two_level ? super_shift() : 0;
   {
     // per-tile list lengths straight from the tile rectangles: tile ranges, compositing CTA order, sort histograms
     StageTimer tm(v, 2);
-    c->launches += launch_tile_counts(c->n, v->proj, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin, v->tile_end,
+    c->launches += launch_tile_counts(c->n, v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin, v->tile_end,
                                       v->to_vals0, v->d_total, st);
     v->tile_order = v->to_vals0;
+    if (v->two_level)  // the same on the grid of 8 x 8-tile blocks: block ranges, expansion CTA order, sort histograms
+      c->launches += launch_tile_counts(c->n, v->proj, sh, v->stiles_x, v->stiles_y, 0, v->tile_ws_c, v->super_begin,
+                                        v->super_end, v->super_order, v->d_total_c, st);
   }
   CHECK_LAUNCH(c, "k_tile_hist / k_tile_scan");
   {
     StageTimer tm(v, 1);
     // depth order of the Gaussians (stable: ties in ascending source index), then offsets in that order
     v->order_sel = 0;
-    c->launches += launch_depth_sort_scan(v->proj.dkey, v->dkey_alt, v->order0, v->order1, v->proj.count, v->offsets, c->n,
-                                          v->dsort_temp, v->dsort_temp_bytes, st);
+    c->launches += launch_depth_sort_scan(v->proj.dkey, v->dkey_alt, v->order0, v->order1,
+                                          v->two_level ? v->proj.ccount : v->proj.count, v->offsets, c->n, v->dsort_temp,
+                                          v->dsort_temp_bytes, st);
   }
   CHECK_LAUNCH(c, "depth sort + scan");
   v->h_total[1] = 0;
+  v->h_total[2] = 0;
   CU_TRY(c, cudaMemcpyAsync(v->h_total, v->d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaMemcpyAsync(v->h_total + 1, v->offsets + c->n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (v->two_level) CU_TRY(c, cudaMemcpyAsync(v->h_total + 2, v->d_total_c, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaStreamSynchronize(st));
   if (c->profiling) harvest_stage_events(v);  // previous step's events have all completed by now
   v->I = v->h_total[0];
+  v->I_sort = v->two_level ? v->h_total[2] : v->I;
   v->stage = 1;
   if (stop_after == 1) return SPLATB200_OK;
   if (v->I >= (1LL << 30)) return c->fail(SPLATB200_ENOMEM, "2^30 or more intersections in one view");
-  if ((int64_t)(uint32_t)v->h_total[1] != v->I)
+  if ((int64_t)(uint32_t)v->h_total[1] != v->I_sort)
     return c->fail(SPLATB200_ERUNTIME, "tile histogram and count scan disagree on the number of intersections");
-  rc = ensure_isect_capacity(v, v->I);
+  rc = ensure_isect_capacity(v, v->I_sort, v->I);
   if (rc) return rc;
 
   v->sorted_sel = 0;
   if (v->I > 0) {
     StageTimer tm(v, 3);
     int nl = 0;
-    v->sorted_sel = launch_tile_sort(c->n, v->I, v->offsets, v->order(), v->proj, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws,
-                                     v->keys0, v->keys1, v->vals0, v->vals1, v->sort_temp, v->sort_temp_bytes, &nl, st);
+    if (!v->two_level) {
+      v->sorted_sel = launch_tile_sort(c->n, v->I, v->offsets, v->order(), v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x,
+                                       v->tile_ws, v->keys0, v->keys1, v->vals0, v->vals1, v->sort_temp, v->sort_temp_bytes, &nl, st);
+    } else {
+      v->sorted_sel = launch_tile_sort(c->n, v->I_sort, v->offsets, v->order(), v->proj, sh, v->stiles_x, v->stiles_y, 0,
+                                       v->tile_ws_c, v->keys0, v->keys1, v->vals0, v->vals1, v->sort_temp, v->sort_temp_bytes, &nl, st);
+      launch_expand(v->stiles_x, v->stiles_y, v->s.tiles_x, v->s.tiles_y, v->super_begin, v->super_end, v->sorted_vals(), v->proj,
+                    v->tile_begin, v->super_order, v->vals_fine, st);
+      ++nl;
+    }
     CHECK_LAUNCH(c, "tile sort");
     c->launches += nl;
   }

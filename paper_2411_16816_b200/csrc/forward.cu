@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor 
   else project_lidar_one(s, f);
   if (!f.visible) {
     p.count[i] = 0u;
+    if (p.ccount) p.ccount[i] = 0u;
     p.dkey[i] = 0xffffffffu;
     return;
   }
@@ -30,6 +31,11 @@ __global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor 
   const int w = r.y - r.x, h = r.w - r.z;
   const uint32_t cnt = (w > 0 && h > 0) ? (uint32_t)w * (uint32_t)h : 0u;
   p.count[i] = cnt;
+  if (p.ccount) {  // blocks of 2^cshift x 2^cshift tiles the rectangle touches (first level of the two-level binning)
+    const int up = (1 << p.cshift) - 1;
+    const int cw = ((r.y + up) >> p.cshift) - (r.x >> p.cshift), ch = ((r.w + up) >> p.cshift) - (r.z >> p.cshift);
+    p.ccount[i] = cnt ? (uint32_t)cw * (uint32_t)ch : 0u;
+  }
   p.dkey[i] = cnt ? __float_as_uint(f.depth) : 0xffffffffu;  // depth > 0: the bit pattern orders like the value
   p.rect[i] = r;
   p.geomA[i] = make_float4(f.mean2d[0], f.mean2d[1], f.vel[0], f.vel[1]);

@@ -83,6 +83,8 @@ struct ProjDev {
   int4* rect;       // x0, x1, y0, y1 (lidar x un-wrapped)
   uint32_t* count;  // tiles touched; 0 <=> culled
   uint32_t* dkey;   // fp32 bits of the (positive) depth key; 0xffffffff for culled Gaussians: the depth-sort key
+  uint32_t* ccount; // two-level binning (camera): blocks of 2^cshift x 2^cshift tiles touched; null otherwise
+  int cshift;
 };
 
 __device__ __forceinline__ float wrap_two_pi(float a) {  // common.hpp:34-38
