@@ -445,7 +445,8 @@ struct TilePasses {
 __global__ void __launch_bounds__(1024)
 k_tile_scan(int tiles_x, int tiles_y, const int* __restrict__ slots, int* __restrict__ gscratch /* 2 T ints or null */,
             uint32_t* __restrict__ tile_begin, uint32_t* __restrict__ tile_end, uint32_t* __restrict__ hist /* n_pass x 256 or null */,
-            TilePasses tp, uint32_t* __restrict__ tile_order /* or null */, int64_t* __restrict__ total_out) {
+            TilePasses tp, uint32_t* __restrict__ tile_order /* or null */, int64_t* __restrict__ total_out,
+            uint32_t* __restrict__ seg_first /* T + 1 or null: exclusive scan of ceil(length / seg_len) */, int seg_len) {
   extern __shared__ int s_dyn[];
   __shared__ unsigned long long s_wsum[32];
   __shared__ uint32_t s_hist[4 * kRMaxBins];
@@ -527,6 +528,31 @@ k_tile_scan(int tiles_x, int tiles_y, const int* __restrict__ slots, int* __rest
     total += v;
   }
   if (tid == 0) *total_out = (int64_t)total;
+  if (seg_first) {  // segments of the lists (two-level binning): a second scan over the same runs
+    __syncthreads();
+    unsigned long long segs = 0ull;
+    for (int t = t0; t < t1; ++t) segs += ((unsigned)a[t] + (unsigned)seg_len - 1u) / (unsigned)seg_len;
+    unsigned long long sinc = segs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, sinc, o);
+      if (lane >= o) sinc += u;
+    }
+    if (lane == 31) s_wsum[warp] = sinc;
+    __syncthreads();
+    unsigned long long sbase = 0ull, stotal = 0ull;
+    for (int w = 0; w < 32; ++w) {
+      const unsigned long long v = s_wsum[w];
+      if (w < warp) sbase += v;
+      stotal += v;
+    }
+    unsigned long long srun = sbase + sinc - segs;
+    for (int t = t0; t < t1; ++t) {
+      seg_first[t] = (uint32_t)srun;
+      srun += ((unsigned)a[t] + (unsigned)seg_len - 1u) / (unsigned)seg_len;
+    }
+    if (tid == 0) seg_first[T] = (uint32_t)stotal;
+  }
   const float scale = 255.0f / (float)s_max;
   unsigned long long run = base + inc - mine;
   for (int t = t0; t < t1; ++t) {
@@ -554,43 +580,62 @@ k_tile_scan(int tiles_x, int tiles_y, const int* __restrict__ slots, int* __rest
 }
 
 // ------------------------------------------------------------------------------------------------
-// Second level of the camera's binning: one CTA per 8 x 8-tile block walks the block's depth-ordered list (the
-// output of the coarse sort) once and appends every Gaussian to the lists of the tiles its rectangle covers. Warp w
-// owns tile row w of the block: its 8 list cursors live in registers, list order is kept by ballot ranks, and every
-// store instruction writes a run of consecutive source indices. A Gaussian covering all 8,160 tiles of a 1080p image
-// is handled as 135 coarse entries + 8,160 four-byte stores instead of 8,160 sorted key-value pairs.
+// Second level of the camera's binning: the depth-ordered list of every 8 x 8-tile block (the output of the coarse
+// sort) is cut into segments of 1,024 entries; one CTA per segment appends its Gaussians to the lists of the tiles
+// their rectangles cover. A Gaussian covering all 8,160 tiles of a 1080p image costs 135 coarse entries + 8,160
+// four-byte stores instead of 8,160 sorted key-value pairs.
+//   1. gather (source index -> rectangle) and turn each rectangle into a 64-bit tile mask of the block;
+//   2. count the segment's entries per tile (per-lane adds, one warp reduction per tile);
+//   3. publish the 64 counts and look back over the preceding segments of the same block (decoupled look-back)
+//      -> the segment's first position in each of the 64 tile lists;
+//   4. warp w owns tile row w: ballot ranks keep the list order, every store instruction writes a run of
+//      consecutive positions of one tile list.
 // ------------------------------------------------------------------------------------------------
 constexpr int kSuperShift = 3;
 constexpr int kSuper = 1 << kSuperShift;
+constexpr int kSeg = 1024;
 
 __global__ void __launch_bounds__(256)
-k_expand(int stiles_x, int tiles_x, int tiles_y, const uint32_t* __restrict__ super_begin, const uint32_t* __restrict__ super_end,
+k_expand(int stiles_x, int n_super, int tiles_x, int tiles_y, const uint32_t* __restrict__ super_begin,
+         const uint32_t* __restrict__ super_end, const uint32_t* __restrict__ seg_first /* n_super + 1 */,
          const uint32_t* __restrict__ cvals, const int4* __restrict__ rect, const uint32_t* __restrict__ tile_begin,
-         const uint32_t* __restrict__ super_order, uint32_t* __restrict__ vals) {
-  __shared__ uint32_t s_src[256];
-  __shared__ unsigned long long s_mask[256];
-  const int st = super_order ? (int)super_order[blockIdx.x] : (int)blockIdx.x;
+         uint32_t* __restrict__ state /* segments x 64 */, uint32_t* __restrict__ ticket, uint32_t* __restrict__ err,
+         uint32_t* __restrict__ vals) {
+  __shared__ uint32_t s_src[kSeg];
+  __shared__ unsigned long long s_mask[kSeg];
+  __shared__ uint32_t s_cnt[64], s_cursor[64];
+  __shared__ uint32_t s_seg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lb = super_begin[st], le = super_end[st];
-  if (le <= lb) return;
-  const int bx = (st % stiles_x) * kSuper, by = (st / stiles_x) * kSuper;
-  uint32_t pos[kSuper];
-#pragma unroll
-  for (int c = 0; c < kSuper; ++c) {
-    const int tx = bx + c, ty = by + warp;
-    pos[c] = (tx < tiles_x && ty < tiles_y) ? tile_begin[ty * tiles_x + tx] : 0u;
+  if (tid == 0) s_seg = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t seg = s_seg;
+  if (seg >= seg_first[n_super]) return;
+  // block owning this segment: seg_first[st] <= seg < seg_first[st + 1] (256-ary search)
+  int lo = 0, hi = n_super;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 255) / 256;
+    const int idx = lo + (tid + 1) * step;
+    const int c = __syncthreads_count(idx < hi && seg_first[idx] <= seg);
+    lo += c * step;
+    hi = min(hi, lo + step);
   }
-  const uint32_t lt = (1u << lane) - 1u;
-  // software pipeline: the next chunk's (source index -> rectangle) gather is in flight while this one is expanded
-  uint32_t src_n = 0u;
-  int4 r_n = make_int4(0, 0, 0, 0);
-  if (lb + tid < le) { src_n = cvals[lb + tid]; r_n = rect[src_n]; }
-  for (uint32_t base = lb; base < le; base += 256) {
-    const int cnt = (int)min(256u, le - base);
+  const int st = lo;
+  const uint32_t j = seg - seg_first[st];  // segment index inside the block's list
+  const uint32_t lb = super_begin[st] + j * kSeg;
+  const int cnt = (int)min((uint32_t)kSeg, super_end[st] - lb);
+  const int bx = (st % stiles_x) * kSuper, by = (st / stiles_x) * kSuper;
+
+  // 1. gather + masks
+#pragma unroll
+  for (int u = 0; u < kSeg / 256; ++u) {
+    const int e = u * 256 + tid;
+    uint32_t src = 0u;
     unsigned long long m = 0ull;
-    if (tid < cnt) {
-      const int xlo = max(r_n.x - bx, 0), xhi = min(r_n.y - bx, kSuper);
-      const int ylo = max(r_n.z - by, 0), yhi = min(r_n.w - by, kSuper);
+    if (e < cnt) {
+      src = cvals[lb + e];
+      const int4 r = rect[src];
+      const int xlo = max(r.x - bx, 0), xhi = min(r.y - bx, kSuper);
+      const int ylo = max(r.z - by, 0), yhi = min(r.w - by, kSuper);
       if (xlo < xhi && ylo < yhi) {
         const unsigned long long xbits = ((1u << xhi) - 1u) & ~((1u << xlo) - 1u);
         const unsigned long long rows_hi = yhi >= kSuper ? ~0ull : ((1ull << (8 * yhi)) - 1ull);
@@ -598,24 +643,83 @@ k_expand(int stiles_x, int tiles_x, int tiles_y, const uint32_t* __restrict__ su
         m = (xbits * 0x0101010101010101ull) & rows_hi & ~rows_lo;
       }
     }
-    s_src[tid] = src_n;
-    s_mask[tid] = m;
-    __syncthreads();
-    const uint32_t nxt = base + 256 + tid;
-    if (nxt < le) { src_n = cvals[nxt]; r_n = rect[src_n]; }
-    for (int k = 0; k < cnt; k += 32) {
-      const int e = k + lane;
-      const uint32_t m8 = e < cnt ? (uint32_t)(s_mask[e] >> (8 * warp)) & 0xffu : 0u;
-      const uint32_t src = s_src[e & 255];
+    s_src[e] = src;
+    s_mask[e] = m;
+  }
+  __syncthreads();
+
+  // 2. per-tile counts of the segment: warp w counts tile row w
+  const int ksteps = (cnt + 31) >> 5;
+  {
+    uint32_t acc[kSuper];
 #pragma unroll
-      for (int c = 0; c < kSuper; ++c) {
-        const bool bit = (m8 >> c) & 1u;
-        const unsigned b = __ballot_sync(0xffffffffu, bit);
-        if (bit) vals[pos[c] + __popc(b & lt)] = src;
-        pos[c] += __popc(b);
-      }
+    for (int c = 0; c < kSuper; ++c) acc[c] = 0u;
+    for (int k = 0; k < ksteps; ++k) {
+      const uint32_t m8 = (uint32_t)(s_mask[k * 32 + lane] >> (8 * warp)) & 0xffu;
+#pragma unroll
+      for (int c = 0; c < kSuper; ++c) acc[c] += (m8 >> c) & 1u;
     }
-    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < kSuper; ++c) {
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, acc[c]);
+      if (lane == c) s_cnt[warp * kSuper + c] = tot;
+    }
+  }
+  __syncthreads();
+
+  // 3. first position of the segment in each tile list
+  if (tid < 64) {
+    const uint32_t mine = s_cnt[tid];
+    uint32_t excl = 0u;
+    if (j == 0) {
+      st_volatile(&state[(size_t)seg * 64 + tid], kFlagPrefix | mine);
+    } else {
+      st_volatile(&state[(size_t)seg * 64 + tid], kFlagAgg | mine);
+      int64_t t = (int64_t)seg - 1;
+      const int64_t t_first = (int64_t)seg - (int64_t)j;  // first segment of this block
+      uint32_t spins = 0u;
+      bool done = false;
+      while (!done) {
+        uint32_t w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = (t - u >= t_first) ? ld_volatile(&state[(size_t)(t - u) * 64 + tid]) : kFlagPrefix;
+        bool stall = false;
+        int used = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!done && !stall) {
+            const uint32_t f = w[u] >> 30;
+            if (f == 0u) stall = true;
+            else { excl += w[u] & kValMask; ++used; done = f != 1u; }
+          }
+        }
+        t -= used;
+        if (stall && ++spins > kSpinLimit) { *err = 1u; done = true; }
+      }
+      st_volatile(&state[(size_t)seg * 64 + tid], kFlagPrefix | (excl + mine));
+    }
+    const int tx = bx + (tid & 7), ty = by + (tid >> 3);
+    s_cursor[tid] = excl + ((tx < tiles_x && ty < tiles_y) ? tile_begin[ty * tiles_x + tx] : 0u);
+  }
+  __syncthreads();
+
+  // 4. append: warp w walks the segment for tile row w
+  uint32_t pos[kSuper];
+#pragma unroll
+  for (int c = 0; c < kSuper; ++c) pos[c] = s_cursor[warp * kSuper + c];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int k = 0; k < ksteps; ++k) {
+    const int e = k * 32 + lane;
+    const uint32_t m8 = (uint32_t)(s_mask[e] >> (8 * warp)) & 0xffu;  // 0 beyond cnt
+    const uint32_t src = s_src[e];
+#pragma unroll
+    for (int c = 0; c < kSuper; ++c) {
+      const uint32_t bit = (m8 >> c) & 1u;
+      const unsigned b = __ballot_sync(0xffffffffu, bit != 0u);
+      const uint32_t rank = __popc(b & lt);
+      if (bit) vals[pos[c] + rank] = src;
+      pos[c] += __shfl_sync(0xffffffffu, rank + bit, 31);  // = popc(b), without a second trip through the XU pipe
+    }
   }
 }
 
@@ -708,7 +812,8 @@ static const uint32_t* tile_ws_hist(const void* ws, int tiles_x, int tiles_y) {
 // -> tile_begin / tile_end (0, 0 for an empty tile), the CTA -> tile permutation (longest lists first; optional),
 // *total (device) and the digit histograms a sort by tile id needs (kept in tile_ws).
 int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int tiles_y, int wrap_x, void* tile_ws,
-                       uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, cudaStream_t st) {
+                       uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, uint32_t* seg_first,
+                       cudaStream_t st) {
   const size_t slot_bytes = tile_slot_bytes(tiles_x, tiles_y);
   cudaMemsetAsync(tile_ws, 0, slot_bytes, st);
   int* slots = (int*)tile_ws;
@@ -727,7 +832,7 @@ int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int 
     attr = true;
   }
   k_tile_scan<<<1, 1024, in_smem ? smem : 0, st>>>(tiles_x, tiles_y, slots, in_smem ? nullptr : scratch, tile_begin, tile_end, hist,
-                                                   tile_passes((int64_t)tiles_x * tiles_y), tile_order, total);
+                                                   tile_passes((int64_t)tiles_x * tiles_y), tile_order, total, seg_first, kSeg);
   return launches + 1;
 }
 
@@ -777,12 +882,20 @@ int launch_tile_sort(int64_t n, int64_t total, const uint32_t* offsets, const ui
 }
 
 // Second level of the two-level binning: expands the block lists (cvals, sorted by block) into the tile lists.
-void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, const uint32_t* super_begin, const uint32_t* super_end,
-                   const uint32_t* cvals, const ProjDev& p, const uint32_t* tile_begin, const uint32_t* super_order, uint32_t* vals,
-                   cudaStream_t st) {
-  const int blocks = stiles_x * stiles_y;
-  if (blocks <= 0) return;
-  k_expand<<<blocks, 256, 0, st>>>(stiles_x, tiles_x, tiles_y, super_begin, super_end, cvals, p.rect, tile_begin, super_order, vals);
+// n_coarse: block-level intersections (bounds the number of segments); state: expand_temp_bytes().
+size_t expand_temp_bytes(int64_t cap_coarse, int n_super) {
+  return sizeof(uint32_t) * (kHdrWords + 64 * (size_t)(cap_coarse / kSeg + n_super + 1));
+}
+void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, int64_t n_coarse, const uint32_t* super_begin,
+                   const uint32_t* super_end, const uint32_t* seg_first, const uint32_t* cvals, const ProjDev& p,
+                   const uint32_t* tile_begin, void* temp, uint32_t* vals, cudaStream_t st) {
+  const int n_super = stiles_x * stiles_y;
+  if (n_super <= 0 || n_coarse <= 0) return;
+  const int64_t max_segs = n_coarse / kSeg + n_super;
+  cudaMemsetAsync(temp, 0, sizeof(uint32_t) * (kHdrWords + 64 * (size_t)max_segs), st);
+  uint32_t* hdr = (uint32_t*)temp;
+  k_expand<<<(unsigned)max_segs, 256, 0, st>>>(stiles_x, n_super, tiles_x, tiles_y, super_begin, super_end, seg_first, cvals, p.rect,
+                                               tile_begin, hdr + kHdrWords, hdr, hdr + 16, vals);
 }
 
 }  // namespace sb

@@ -100,7 +100,8 @@ struct splatb200_view {
   // two-level binning (cameras): lists per block of 8 x 8 tiles first, expanded into the tile lists
   bool two_level = false;
   int stiles_x = 0, stiles_y = 0;
-  uint32_t *super_begin = nullptr, *super_end = nullptr, *super_order = nullptr;
+  uint32_t *super_begin = nullptr, *super_end = nullptr, *seg_first = nullptr;
+  void* expand_temp = nullptr;
   void* tile_ws_c = nullptr;
   int64_t* d_total_c = nullptr;
   uint32_t* vals_fine = nullptr;  // the tile lists (two-level mode; otherwise the sorted vals0 / vals1)
@@ -207,7 +208,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->keys0); dfree(v->keys1); dfree(v->vals0); dfree(v->vals1); dfree(v->sort_temp);
   dfree(v->tile_begin); dfree(v->tile_end); dfree(v->rays); dfree(v->ray_begin); dfree(v->ray_end);
   dfree(v->to_vals0); dfree(v->tile_ws); dfree(v->d_total);
-  dfree(v->super_begin); dfree(v->super_end); dfree(v->super_order); dfree(v->tile_ws_c); dfree(v->d_total_c);
+  dfree(v->super_begin); dfree(v->super_end); dfree(v->seg_first); dfree(v->expand_temp); dfree(v->tile_ws_c); dfree(v->d_total_c);
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
@@ -295,6 +296,10 @@ int ensure_isect_capacity(splatb200_view* v, int64_t n_sort, int64_t n_fine) {
     CU_TRY(c, cudaMalloc(&v->vals1, sizeof(uint32_t) * (size_t)cap));
     v->sort_temp_bytes = tile_sort_temp_bytes(cap, v->two_level ? (int64_t)v->stiles_x * v->stiles_y : v->n_tiles);
     CU_TRY(c, cudaMalloc(&v->sort_temp, v->sort_temp_bytes));
+    if (v->two_level) {
+      dfree(v->expand_temp);
+      CU_TRY(c, cudaMalloc(&v->expand_temp, expand_temp_bytes(cap, v->stiles_x * v->stiles_y)));
+    }
     v->isect_cap = cap;
   }
   if (v->two_level && n_fine > v->fine_cap) {
@@ -337,7 +342,7 @@ int alloc_query_buffers(splatb200_view* v) {
     const size_t Ts = (size_t)std::max(1, v->stiles_x * v->stiles_y);
     CU_TRY(c, cudaMalloc(&v->super_begin, sizeof(uint32_t) * Ts));
     CU_TRY(c, cudaMalloc(&v->super_end, sizeof(uint32_t) * Ts));
-    CU_TRY(c, cudaMalloc(&v->super_order, sizeof(uint32_t) * Ts));
+    CU_TRY(c, cudaMalloc(&v->seg_first, sizeof(uint32_t) * (Ts + 1)));
     CU_TRY(c, cudaMalloc(&v->tile_ws_c, tile_hist_bytes(v->stiles_x, v->stiles_y)));
     CU_TRY(c, cudaMalloc(&v->d_total_c, sizeof(int64_t)));
   }
@@ -797,11 +802,11 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     // per-tile list lengths straight from the tile rectangles: tile ranges, compositing CTA order, sort histograms
     StageTimer tm(v, 2);
     c->launches += launch_tile_counts(c->n, v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin, v->tile_end,
-                                      v->to_vals0, v->d_total, st);
+                                      v->to_vals0, v->d_total, nullptr, st);
     v->tile_order = v->to_vals0;
     if (v->two_level)  // the same on the grid of 8 x 8-tile blocks: block ranges, expansion CTA order, sort histograms
       c->launches += launch_tile_counts(c->n, v->proj, sh, v->stiles_x, v->stiles_y, 0, v->tile_ws_c, v->super_begin,
-                                        v->super_end, v->super_order, v->d_total_c, st);
+                                        v->super_end, nullptr, v->d_total_c, v->seg_first, st);
   }
   CHECK_LAUNCH(c, "k_tile_hist / k_tile_scan");
   {
@@ -840,8 +845,8 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     } else {
       v->sorted_sel = launch_tile_sort(c->n, v->I_sort, v->offsets, v->order(), v->proj, sh, v->stiles_x, v->stiles_y, 0,
                                        v->tile_ws_c, v->keys0, v->keys1, v->vals0, v->vals1, v->sort_temp, v->sort_temp_bytes, &nl, st);
-      launch_expand(v->stiles_x, v->stiles_y, v->s.tiles_x, v->s.tiles_y, v->super_begin, v->super_end, v->sorted_vals(), v->proj,
-                    v->tile_begin, v->super_order, v->vals_fine, st);
+      launch_expand(v->stiles_x, v->stiles_y, v->s.tiles_x, v->s.tiles_y, v->I_sort, v->super_begin, v->super_end, v->seg_first,
+                    v->sorted_vals(), v->proj, v->tile_begin, v->expand_temp, v->vals_fine, st);
       ++nl;
     }
     CHECK_LAUNCH(c, "tile sort");

@@ -61,17 +61,20 @@ size_t tile_hist_bytes(int tiles_x, int tiles_y);
 // tile_begin / tile_end (0, 0 for an empty tile), the CTA -> tile permutation (longest lists first; may be null),
 // *total (device) and the digit histograms a sort by tile id needs (kept in tile_ws)
 int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int tiles_y, int wrap_x, void* tile_ws,
-                       uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, cudaStream_t st);
+                       uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, uint32_t* seg_first,
+                       cudaStream_t st);
 size_t tile_sort_temp_bytes(int64_t cap, int64_t n_tiles);
 // duplication (one (tile id, source index) pair per intersection, generated in depth order inside the first pass) +
 // stable sort by tile id, on the grid of 2^shift-tile blocks. Returns which of vals0 / vals1 holds the sorted indices.
 int launch_tile_sort(int64_t n, int64_t total, const uint32_t* offsets, const uint32_t* order, const ProjDev& p, int shift,
                      int tiles_x, int tiles_y, int wrap_x, const void* tile_ws, uint32_t* keys0, uint32_t* keys1, uint32_t* vals0,
                      uint32_t* vals1, void* temp, size_t temp_bytes, int* launches, cudaStream_t st);
-// second level: block lists (sorted by block id, depth order inside) -> tile lists
-void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, const uint32_t* super_begin, const uint32_t* super_end,
-                   const uint32_t* cvals, const ProjDev& p, const uint32_t* tile_begin, const uint32_t* super_order, uint32_t* vals,
-                   cudaStream_t st);
+// second level: block lists (sorted by block id, depth order inside), cut into segments (seg_first from
+// launch_tile_counts on the block grid) -> tile lists
+size_t expand_temp_bytes(int64_t cap_coarse, int n_super);
+void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, int64_t n_coarse, const uint32_t* super_begin,
+                   const uint32_t* super_end, const uint32_t* seg_first, const uint32_t* cvals, const ProjDev& p,
+                   const uint32_t* tile_begin, void* temp, uint32_t* vals, cudaStream_t st);
 
 // raster_bwd.cu
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
