@@ -106,6 +106,8 @@ struct splatb200_view {
   int64_t* d_total_c = nullptr;
   uint32_t* vals_fine = nullptr;  // the tile lists (two-level mode; otherwise the sorted vals0 / vals1)
   int64_t fine_cap = 0;
+  int64_t hit_cap = 0;            // out.hit: one byte per tile-list entry
+  bool multi_pass = false;        // some lidar tile holds more than 256 rays
   int64_t I_sort = 0;             // entries the radix sort handles: block-level intersections, or I
   // queries
   int64_t P = 0, n_tiles = 0;
@@ -212,7 +214,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -301,6 +303,12 @@ int ensure_isect_capacity(splatb200_view* v, int64_t n_sort, int64_t n_fine) {
       CU_TRY(c, cudaMalloc(&v->expand_temp, expand_temp_bytes(cap, v->stiles_x * v->stiles_y)));
     }
     v->isect_cap = cap;
+  }
+  if (n_fine > v->hit_cap) {
+    dfree(v->out.hit);
+    const int64_t cap = n_fine + n_fine / 4 + 1024;
+    CU_TRY(c, cudaMalloc(&v->out.hit, (size_t)cap));
+    v->hit_cap = cap;
   }
   if (v->two_level && n_fine > v->fine_cap) {
     dfree(v->vals_fine);
@@ -673,6 +681,8 @@ extern "C" int splatb200_view_create_lidar(splatb200_ctx* c, const splatb200_lid
   for (int64_t t = 0; t < n_tiles; ++t)
     if (ray_begin[t] < 0 || ray_end[t] < ray_begin[t] || ray_end[t] > n_rays)
       return fin(c->fail(SPLATB200_EINVAL, "ray_begin/ray_end must delimit slices of the ray array"));
+  for (int64_t t = 0; t < n_tiles; ++t)
+    if (ray_end[t] - ray_begin[t] > 256) v->multi_pass = true;  // several passes over a tile's list
   // Within a tile the rays are re-ordered azimuth-major (then by elevation), so that 32 consecutive positions — one
   // warp of the compositing kernels — form a compact patch (4 azimuth bins x 8 beams on a grid sweep) that per-warp
   // culling can exploit. The original index travels in .w; outputs keep the caller's ray order.
@@ -855,6 +865,8 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   v->stage = 2;
   if (stop_after == 2) return SPLATB200_OK;
 
+  v->out.hit_or = v->multi_pass ? 1 : 0;
+  if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
   {
     StageTimer tm(v, 5);
     launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,

@@ -89,6 +89,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   __shared__ float4 sF[256 * 4];
   __shared__ uint8_t sMask[256];
   __shared__ uint8_t sList[8][256];
+  __shared__ __align__(8) uint8_t sHit[8][256];  // [warp][batch entry]: some lane of the warp blended it
   __shared__ PatchBox sBox[8];
 
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
@@ -133,14 +134,28 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     bool done = !inside;
     __syncthreads();  // patch boxes visible
 
+    // the hit bytes of a batch are folded and written once every warp is through it, i.e. after the next barrier
+    int64_t pending = -1;  // list position of the batch whose hit bytes are still in shared memory (CTA-uniform)
+    auto flush_hits = [&]() {
+      if (pending >= 0 && (uint32_t)pending + tid < le) {
+        uint32_t h = 0u;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) h |= (uint32_t)(sHit[w][tid] != 0) << w;
+        uint8_t* dst = out.hit + pending + tid;
+        *dst = out.hit_or ? (uint8_t)(*dst | h) : (uint8_t)h;
+      }
+      pending = -1;
+    };
     for (uint32_t base = lb; base < le; base += 256) {
-      if (__syncthreads_and(done)) break;
+      const bool all_done = __syncthreads_and(done);
+      flush_hits();
+      if (all_done) break;
       const uint32_t idx = base + tid;
-      uint32_t mask = 0u;
+      uint32_t mask = 0u, wrapm = 0u;
       if (idx < le) {
         const uint32_t src = vals[idx];
         const float4 gA = p.geomA[src], gB = p.geomB[src];
-        mask = patch_mask<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min);
+        mask = patch_mask<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min, &wrapm);
         if (mask) {
           sA[tid] = gA;
           sB[tid] = gB;
@@ -150,8 +165,12 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         }
       }
       sMask[tid] = (uint8_t)mask;
-      __syncthreads();
+      // lidar: does any (entry, patch) pair of this batch need the azimuth wrap? (rare: tiles at the seam)
+      const bool wrap = kCamera ? (__syncthreads(), false) : __syncthreads_or((mask & wrapm) != 0u) != 0;
+      reinterpret_cast<uint2*>(sHit[warp])[lane] = make_uint2(0u, 0u);  // 256 bytes per warp
+      pending = (int64_t)base;
       if (__all_sync(0xffffffffu, done)) continue;  // this warp's 32 queries have saturated
+      __syncwarp();
       const int cnt = min(256u, le - base);
       const int n_w = warp_compact(sMask, cnt, warp, lane, sList[warp]);
       const uint8_t* lst = sList[warp];
@@ -168,6 +187,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
         ++n_contrib;
         last_idx = (int)(base - lb) + j + 1;
+        sHit[warp][j] = 1;
         if (!kCamera) {
           const float2 c = sC[j];
           const float r_rs = __fmaf_rn(c.y, t, c.x);
@@ -200,8 +220,8 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           const int jn0 = lst[min(k + 2, n_w - 1)], jn1 = lst[min(k + 3, n_w - 1)];  // clamped: always a valid slot
           const float4 an0 = sA[jn0], bn0 = sB[jn0], an1 = sA[jn1], bn1 = sB[jn1];
           float dx0, dy0, dx1, dy1;
-          const float qf0 = alpha_qform<true>(a0, b0, qx, qy, t, dx0, dy0);
-          const float qf1 = alpha_qform<true>(a1, b1, qx, qy, t, dx1, dy1);
+          const float qf0 = alpha_qform<true>(a0, b0, qx, qy, t, dx0, dy0, wrap);
+          const float qf1 = alpha_qform<true>(a1, b1, qx, qy, t, dx1, dy1, wrap);
           AlphaEval ev;
           if (!done && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j0, ev);
           if (has1 && !done && alpha_finish(qf1, b1.w, dx1, dy1, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j1, ev);
@@ -227,6 +247,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       out.last_idx[pix] = last_idx;
     }
     __syncthreads();  // shared staging and patch boxes are reused by the next ray pass
+    flush_hits();     // the last batch of a list that ended before every query saturated
   }
 }
 

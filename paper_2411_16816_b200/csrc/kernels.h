@@ -15,6 +15,9 @@ struct RasterOutDev {
   float* range_blend;  // P  lidar: un-normalised sum w r_rs
   int32_t* n_contrib;  // P
   int32_t* last_idx;   // P  1-based tile-local list position of the last blended Gaussian
+  uint8_t* hit;        // I  per list entry: bit w set if some query of warp w of the tile's CTA blended it (saved for
+                       //    the backward pass, which then revisits only those entries)
+  int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
 };
 
 // Raw per-Gaussian sums of the compositing backward, indexed by source index; consumed (and re-zeroed)

@@ -176,8 +176,6 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         pix = (int64_t)__float_as_uint(r.w);
       }
     }
-    warp_patch_box<!kCamera>(inside, qx, qy, t, lane, &sBox[warp]);
-
     int last = 0;
     float T = 1.0f, K = 0.0f, g_D = 0.0f;
     float g_out[kChannels];
@@ -232,15 +230,15 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     for (int batch = (max_last - 1) / kBatch; batch >= 0 && max_last > 0; --batch) {
       const int bstart = batch * kBatch;
       const int cnt = min(kBatch, max_last - bstart);
+      // the forward pass saved, per list entry, which warps blended it: only those entries are staged and revisited
       uint32_t mask = 0u;
       if (tid < cnt) {
-        const uint32_t src = vals[lb + bstart + tid];
-        const float4 gA = p.geomA[src], gB = p.geomB[src];
-        mask = patch_mask<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min);
+        mask = fwd.hit[lb + bstart + tid];
         if (mask) {
+          const uint32_t src = vals[lb + bstart + tid];
           sSrc[tid] = src;
-          sA[tid] = gA;
-          sB[tid] = gB;
+          sA[tid] = p.geomA[src];
+          sB[tid] = p.geomB[src];
           if (!kCamera) sC[tid] = p.geomC[src];
 #pragma unroll
           for (int k = 0; k < 4; ++k) sF[4 * tid + k] = p.feat[4 * (size_t)src + k];

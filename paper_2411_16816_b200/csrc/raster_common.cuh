@@ -33,13 +33,15 @@ struct AlphaEval {
 
 // Step 1 of evaluate_alpha: the offsets and the quadratic form (branch-free apart from the lidar wrap), so that two
 // list entries can be evaluated side by side for instruction-level parallelism.
+// `wrap` (lidar only, warp-uniform): false when the staging pass has certified |qx - mx| < pi for every query of the warp
+// and every entry of the batch, so that wrap_pi would return its argument unchanged (see patch_mask).
 template <bool kLidar>
 __device__ __forceinline__ float alpha_qform(const float4 gA /* mx my vx vy */, const float4 gB /* a b2 c rho */, float qx,
-                                             float qy, float t, float& dx, float& dy) {
+                                             float qy, float t, float& dx, float& dy, bool wrap = true) {
   const float mx = __fmaf_rn(gA.z, t, gA.x);
   const float my = __fmaf_rn(gA.w, t, gA.y);
   dx = __fsub_rn(qx, mx);
-  if (kLidar) dx = wrap_pi(dx);
+  if (kLidar && wrap) dx = wrap_pi(dx);
   dy = __fsub_rn(qy, my);
   return __fmaf_rn(gB.x, __fmul_rn(dx, dx), __fmaf_rn(gB.z, __fmul_rn(dy, dy), __fmul_rn(gB.y, __fmul_rn(dx, dy))));
 }
@@ -83,7 +85,12 @@ __device__ __forceinline__ bool evaluate_alpha(const float4 gA /* mx my vx vy */
 //   * the fp32 evaluation of Q differs from the exact one by at most ~4 ulp of the sum of term magnitudes
 //     M <= a DX^2 + c DY^2 + |b2| DX DY; a margin of 2^-18 M (64 ulp) covers that, the cull's own
 //     arithmetic and the rounding of the conic entries;
-//   * the pair is dropped only if that lower bound exceeds qform_max, or the alpha it allows is below
+//   * a second lower bound handles boxes much larger than the footprint, where the norm bound is weak (a lidar patch
+//     of 8 beams spans 1-6 degrees, a footprint 0.5): minimising the exact Q over one coordinate gives
+//     Q(d) >= dx^2 det4 / (4c) and Q(d) >= dy^2 det4 / (4a) with det4 = 4ac - b2^2, so the distance of the box from the
+//     Gaussian's centre along either axis bounds Q from below (the "3 sigma slab" test, in exact arithmetic);
+//     det4 is taken from the certified-PSD expression, i.e. rounded towards zero;
+//   * the pair is dropped only if a lower bound exceeds qform_max, or the alpha it allows is below
 //     alpha_min (with a 1% margin). A conic that is not certifiably PSD, a non-finite value, or a lidar
 //     offset box that reaches the +-pi seam keeps the pair.
 // Ill-conditioned grazing footprints (|d| ~ 1e5 px, M ~ 1e10) get a margin far above qform_max and are
@@ -94,7 +101,7 @@ struct PatchBox {
   float hx2, hy2;  // half-extents plus the query-side rounding slack: h + 2^-21 (|c| + h)
   float th2;       // th + 2^-21 (|tc| + th): multiplies |v| (travel during the patch's time span + slack on v t)
   int enabled;     // 0: the warp's queries are too spread out (or absent) to cull against
-  int pad;
+  int straddle;    // lidar: some query lies >= pi away from the first one (the patch crosses 0 / 2 pi): always wrap
 };
 
 // sqrt rounded up: MUFU.SQRT (2^-22 relative error) padded by 2^-20
@@ -108,28 +115,39 @@ constexpr float kCullGamma = 3.814697265625e-06f;   // 2^-18
 constexpr float kSlackUlp = 4.76837158203125e-07f;  // 2^-21
 
 // Tests patches [kP0, kP0 + kNP) of the 8; returns their bits (in place: bit p for patch p).
+// *wrapmask (lidar): bit p set if some query of patch p may need the azimuth wrap for this Gaussian, i.e. the raw
+// difference qx - mx is not certified to lie inside (-pi, pi).
 template <bool kLidar, int kP0 = 0, int kNP = 8>
 __device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB, const PatchBox* __restrict__ box,
-                                               float qform_max, float alpha_min) {
+                                               float qform_max, float alpha_min, uint32_t* wrapmask = nullptr) {
+  if (wrapmask) *wrapmask = ((1u << kNP) - 1u) << kP0;
   const float a = gB.x, b2 = gB.y, c = gB.z, rho = gB.w;
   const float ab2 = fabsf(b2);
   // certified PSD: 4ac >= b2^2 with rounding slack on both sides
-  const bool psd = a > 0.0f && c > 0.0f && (4.0f * a * c * (1.0f - 1e-6f) - b2 * b2 * (1.0f + 1e-6f) >= 0.0f);
+  const float det4 = 4.0f * a * c * (1.0f - 1e-6f) - b2 * b2 * (1.0f + 1e-6f);  // <= the exact 4ac - b2^2
+  const bool psd = a > 0.0f && c > 0.0f && det4 >= 0.0f;
   if (!psd) return ((1u << kNP) - 1u) << kP0;
+  // slab bounds: Q >= dx^2 kx and Q >= dy^2 ky, both factors rounded down
+  const float kx = __fdiv_rd(det4, 4.0f * c) * (1.0f - 1e-5f), ky = __fdiv_rd(det4, 4.0f * a) * (1.0f - 1e-5f);
   // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min)
   float qmax = qform_max;
   if (alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qmax = fminf(qmax, 2.0f * __logf(rho * 1.01f / alpha_min) + 0.02f);
   const float avx = fabsf(gA.z), avy = fabsf(gA.w);
   const float slack_x = kSlackUlp * (fabsf(gA.x) + 8.0f), slack_y = kSlackUlp * (fabsf(gA.y) + 8.0f);
-  uint32_t mask = 0u;
+  uint32_t mask = 0u, wm = 0u;
 #pragma unroll
   for (int p = kP0; p < kP0 + kNP; ++p) {
     const PatchBox b = box[p];
     bool keep = true;
+    bool needw = true;
     if (b.enabled) {
       const float mxc = fmaf(gA.z, b.tc, gA.x), myc = fmaf(gA.w, b.tc, gA.y);
       float dcx = b.cx - mxc;
-      if (kLidar) dcx = wrap_pi(dcx);
+      if (kLidar) {
+        // every query's raw difference lies within Hx of dcx (when the patch does not straddle the seam)
+        needw = b.straddle || !(fabsf(dcx) + fmaf(fabsf(gA.z), b.th2, b.hx2) + kSlackUlp * (fabsf(gA.x) + 8.0f) < kPi - 1e-3f);
+        dcx = wrap_pi(dcx);
+      }
       const float dcy = b.cy - myc;
       // half-extents of the offset box: query box + rolling-shutter travel + rounding slack
       const float Hx = fmaf(avx, b.th2, b.hx2) + slack_x;
@@ -141,16 +159,21 @@ __device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB,
       const float R2 = fmaf(a * Hx, Hx, fmaf(c * Hy, Hy, ab2 * Hx * Hy));
       // cull <=> sqrt(A) - sqrt(R2) k > sqrt(q),  A = max(Qc - E, 0), q = max(qmax + E, 0) (1 + 2e-5), k = 1 + 1e-5
       //      <=> A > R2 k^2 + q + 2 k sqrt(R2 q)   (both sides >= 0); the approximate sqrt is padded upwards
+      // box-to-centre gaps; the extra slack covers the roundings of this very computation (dcx, Hx, the difference)
+      const float gx = fmaxf(fabsf(dcx) - Hx - slack_x, 0.0f), gy = fmaxf(fabsf(dcy) - Hy - slack_y, 0.0f);
+      const float slab = fmaxf(gx * gx * kx, gy * gy * ky) * (1.0f - 1e-5f);
       const float A = fmaxf(Qc - E, 0.0f);
       const float qe = qmax + E;
       const float q = fmaxf(qe, 0.0f) * (1.0f + 2e-5f);
       const float rhs = fmaf(2.00004f, sqrt_up(R2 * q), fmaf(R2, 1.00003f, q));
       // qe < 0: even qf = -E (the lowest value rounding allows) is beyond the alpha cut-off
-      const bool cull = !seam && ((A > rhs) || (qe < 0.0f));
+      const bool cull = !seam && ((A > rhs) || (qe < 0.0f) || (slab > qe * (1.0f + 1e-5f)));
       keep = !cull;
     }
     if (keep) mask |= 1u << p;
+    if (needw) wm |= 1u << p;
   }
+  if (kLidar && wrapmask) *wrapmask = wm;
   return mask;
 }
 
@@ -162,10 +185,11 @@ __device__ __forceinline__ void warp_patch_box(bool inside, float qx, float qy, 
   PatchBox b;
   b.cx = b.cy = b.tc = b.hx2 = b.hy2 = b.th2 = 0.0f;
   b.enabled = 0;
-  b.pad = 0;
+  b.straddle = 1;
   if (act != 0u) {
     const int first = __ffs(act) - 1;
     const float ref = __shfl_sync(0xffffffffu, qx, first);
+    b.straddle = kLidar ? (__any_sync(0xffffffffu, inside && !(fabsf(qx - ref) < kPi - 1e-3f)) ? 1 : 0) : 0;
     float rx = kLidar ? wrap_pi(qx - ref) : qx;
     const float big = 3.0e38f;
     float x0 = inside ? rx : big, x1 = inside ? rx : -big;
