@@ -214,7 +214,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -343,6 +343,10 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->to_vals0, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->tile_ws, tile_hist_bytes(v->s.tiles_x, v->s.tiles_y)));
   CU_TRY(c, cudaMalloc(&v->d_total, sizeof(int64_t)));
+  if (std::getenv("SPLATB200_STATS")) {  // debug counters of the compositing kernels (read through view_array "raster_stats")
+    CU_TRY(c, cudaMalloc(&v->out.stats, sizeof(unsigned long long) * 4));
+    CU_TRY(c, cudaMemsetAsync(v->out.stats, 0, sizeof(unsigned long long) * 4, c->stream));
+  }
   if (v->two_level) {
     const int sh = super_shift();
     v->stiles_x = (v->s.tiles_x + (1 << sh) - 1) >> sh;
@@ -1251,6 +1255,17 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
     if (rc) return rc;
     for (int64_t k = 0; k < v->n_tiles; ++k) ((int64_t*)dst)[k] = h[k];
     return v->n_tiles;
+  }
+  if (name == "raster_stats") {  // cumulative since view creation; zeros unless SPLATB200_STATS is set
+    if (dst) {
+      unsigned long long h[4] = {0, 0, 0, 0};
+      if (v->out.stats) {
+        CU_TRY(c, cudaMemcpyAsync(h, v->out.stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CU_TRY(c, cudaStreamSynchronize(c->stream));
+      }
+      for (int k = 0; k < 4; ++k) ((int64_t*)dst)[k] = (int64_t)h[k];
+    }
+    return 4;
   }
   if (name == "grid") {
     if (dst) { ((int64_t*)dst)[0] = v->s.tiles_x; ((int64_t*)dst)[1] = v->s.tiles_y; }

@@ -174,6 +174,10 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       const int cnt = min(256u, le - base);
       const int n_w = warp_compact(sMask, cnt, warp, lane, sList[warp]);
       const uint8_t* lst = sList[warp];
+      if (out.stats && lane == 0) {
+        atomicAdd(&out.stats[1], (unsigned long long)n_w);
+        if (warp == 0) atomicAdd(&out.stats[0], (unsigned long long)cnt);
+      }
       auto blend = [&](int j, const AlphaEval& ev) {
         const float w = __fmul_rn(ev.alpha, T);
 #pragma unroll

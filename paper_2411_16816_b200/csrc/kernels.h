@@ -18,6 +18,7 @@ struct RasterOutDev {
   uint8_t* hit;        // I  per list entry: bit w set if some query of warp w of the tile's CTA blended it (saved for
                        //    the backward pass, which then revisits only those entries)
   int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
+  unsigned long long* stats;  // debug (SPLATB200_STATS=1), else null: [0] staged entries, [1] per-warp survivors of the cull
 };
 
 // Raw per-Gaussian sums of the compositing backward, indexed by source index; consumed (and re-zeroed)
