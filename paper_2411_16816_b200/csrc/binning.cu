@@ -366,14 +366,25 @@ k_count_scan(const uint32_t* __restrict__ count, const uint32_t* __restrict__ or
       st_volatile(&state[0], kFlagPrefix | total);
     } else {
       st_volatile(&state[tile], kFlagAgg | total);
+      int64_t t = (int64_t)tile - 1;
       uint32_t spins = 0u;
-      for (int64_t t = (int64_t)tile - 1; t >= 0; --t) {
-        uint32_t w;
-        while (((w = ld_volatile(&state[t])) >> 30) == 0u) {
-          if (++spins > kSpinLimit) { *err = 1u; break; }
+      bool done = false;
+      while (!done) {  // 8 preceding tiles per step (independent loads)
+        uint32_t w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = (t - u >= 0) ? ld_volatile(&state[t - u]) : kFlagPrefix;
+        bool stall = false;
+        int used = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!done && !stall) {
+            const uint32_t f = w[u] >> 30;
+            if (f == 0u) stall = true;
+            else { excl += w[u] & kValMask; ++used; done = f != 1u; }
+          }
         }
-        excl += w & kValMask;
-        if ((w >> 30) != 1u) break;
+        t -= used;
+        if (stall && ++spins > kSpinLimit) { *err = 1u; done = true; }
       }
       st_volatile(&state[tile], kFlagPrefix | ((excl + total) & kValMask));
     }

@@ -33,6 +33,8 @@ struct splatb200_ctx {
   int64_t launches = 0;      // hand-written kernels
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
+  cudaStream_t aux = nullptr;  // independent small kernels of the binning stage run beside the depth sort
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // scene
   int64_t n = 0;
@@ -240,15 +242,16 @@ void harvest_stage_events(splatb200_view* v) {
 struct StageTimer {
   splatb200_view* v;
   int stage;
-  StageTimer(splatb200_view* view, int st) : v(view), stage(st) {
+  cudaStream_t s;
+  StageTimer(splatb200_view* view, int st, cudaStream_t stream = nullptr) : v(view), stage(st), s(stream ? stream : view->ctx->stream) {
     if (!v->ctx->profiling) return;
     for (int k = 0; k < 2; ++k)
       if (!v->ev[stage][k]) cudaEventCreate(&v->ev[stage][k]);
-    cudaEventRecord(v->ev[stage][0], v->ctx->stream);
+    cudaEventRecord(v->ev[stage][0], s);
   }
   ~StageTimer() {
     if (!v->ctx->profiling) return;
-    cudaEventRecord(v->ev[stage][1], v->ctx->stream);
+    cudaEventRecord(v->ev[stage][1], s);
     v->ev_valid[stage] = true;
   }
 };
@@ -397,6 +400,13 @@ extern "C" int splatb200_ctx_create(int device, void* cuda_stream, splatb200_ctx
   auto* c = new splatb200_ctx();
   c->device = device;
   c->stream = (cudaStream_t)cuda_stream;
+  if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    g_create_error = "cannot create the auxiliary stream";
+    delete c;
+    return SPLATB200_ECUDA;
+  }
   *out = c;
   return SPLATB200_OK;
 }
@@ -407,6 +417,9 @@ extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
   cudaStreamSynchronize(c->stream);
   while (!c->views.empty()) splatb200_view_destroy(c->views.back());
   free_scene(c);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
@@ -813,23 +826,37 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   const int wrap_x = v->s.is_camera ? 0 : 1;
   const int sh = v->two_level ? super_shift() : 0;
   {
-    // per-tile list lengths straight from the tile rectangles: tile ranges, compositing CTA order, sort histograms
-    StageTimer tm(v, 2);
-    c->launches += launch_tile_counts(c->n, v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin, v->tile_end,
-                                      v->to_vals0, v->d_total, nullptr, st);
-    v->tile_order = v->to_vals0;
-    if (v->two_level)  // the same on the grid of 8 x 8-tile blocks: block ranges, expansion CTA order, sort histograms
-      c->launches += launch_tile_counts(c->n, v->proj, sh, v->stiles_x, v->stiles_y, 0, v->tile_ws_c, v->super_begin,
-                                        v->super_end, nullptr, v->d_total_c, v->seg_first, st);
-  }
-  CHECK_LAUNCH(c, "k_tile_hist / k_tile_scan");
-  {
-    StageTimer tm(v, 1);
-    // depth order of the Gaussians (stable: ties in ascending source index), then offsets in that order
-    v->order_sel = 0;
-    c->launches += launch_depth_sort_scan(v->proj.dkey, v->dkey_alt, v->order0, v->order1,
-                                          v->two_level ? v->proj.ccount : v->proj.count, v->offsets, c->n, v->dsort_temp,
-                                          v->dsort_temp_bytes, st);
+    // Per-tile list lengths straight from the tile rectangles (tile ranges, compositing CTA order, sort histograms).
+    // Independent of the depth sort; running the two side by side on separate streams was measured and gains nothing
+    // (both are chains of small kernels that already fill the SM slots; the fork/join events cost what the overlap saves).
+    const bool fork = false;
+    cudaStream_t ts = st;
+    if (fork) {
+      CU_TRY(c, cudaEventRecord(c->ev_fork, st));
+      CU_TRY(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    }
+    {
+      StageTimer tm(v, 2, ts);
+      c->launches += launch_tile_counts(c->n, v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin,
+                                        v->tile_end, v->to_vals0, v->d_total, nullptr, ts);
+      v->tile_order = v->to_vals0;
+      if (v->two_level)  // the same on the grid of 8 x 8-tile blocks: block ranges, list segments, sort histograms
+        c->launches += launch_tile_counts(c->n, v->proj, sh, v->stiles_x, v->stiles_y, 0, v->tile_ws_c, v->super_begin,
+                                          v->super_end, nullptr, v->d_total_c, v->seg_first, ts);
+    }
+    CHECK_LAUNCH(c, "k_tile_hist / k_tile_scan");
+    {
+      StageTimer tm(v, 1);
+      // depth order of the Gaussians (stable: ties in ascending source index), then offsets in that order
+      v->order_sel = 0;
+      c->launches += launch_depth_sort_scan(v->proj.dkey, v->dkey_alt, v->order0, v->order1,
+                                            v->two_level ? v->proj.ccount : v->proj.count, v->offsets, c->n, v->dsort_temp,
+                                            v->dsort_temp_bytes, st);
+    }
+    if (fork) {
+      CU_TRY(c, cudaEventRecord(c->ev_join, c->aux));
+      CU_TRY(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+    }
   }
   CHECK_LAUNCH(c, "depth sort + scan");
   v->h_total[1] = 0;
