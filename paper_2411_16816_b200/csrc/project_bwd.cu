@@ -103,7 +103,7 @@ __device__ __forceinline__ float block_sum_256(float v, float* s_red /* 8 */) {
 constexpr int kBwdSpan = 1024;  // Gaussians per CTA
 
 template <bool kCamera, int kMode>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGradDev rg, ParamGradDev pg,
               float* __restrict__ sensor_grads6, float* __restrict__ actor_acc, const float* __restrict__ pgin,
               float* __restrict__ cg, int64_t i_lo, int64_t i_hi) {
@@ -163,10 +163,9 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     if (kMode == kFused) {
     float r[kRasterGradStride];
 #pragma unroll
-    for (int k = 0; k < kRasterGradStride; ++k) {
-      r[k] = rg.g[kRasterGradStride * i + k];
-      rg.g[kRasterGradStride * i + k] = 0.0f;  // leave the scratch buffer zero for the next backward
-    }
+    for (int k = 0; k < kRasterGradStride; ++k) r[k] = rg.g[kRasterGradStride * i + k];  // all loads first: independent
+#pragma unroll
+    for (int k = 0; k < kRasterGradStride; ++k) rg.g[kRasterGradStride * i + k] = 0.0f;  // scratch zero for the next backward
     // ---- (1) raw sums -> ProjectedGrads -------------------------------------------------------
     const float g_rho = r[8];
     g_opacity = f.det_ratio * g_rho;
@@ -261,7 +260,7 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
       for (int k = 0; k < 9; ++k) cg[kComposeGradStride * i + 3 + k] = g_cov_w[k];
     } else {
     // ---- (3) compose backward -----------------------------------------------------------------
-    pg.d_opacity_logit[i] += g_opacity * f.opacity * (1.0f - f.opacity);
+    atomicAdd(&pg.d_opacity_logit[i], g_opacity * f.opacity * (1.0f - f.opacity));  // REDs: no load latency on the += slots
     float g_cov_local[9], d_mean[3];
     if (!f.dynamic) {
 #pragma unroll
@@ -319,13 +318,13 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
       }
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) pg.d_mean[3 * i + k] += d_mean[k];
+    for (int k = 0; k < 3; ++k) atomicAdd(&pg.d_mean[3 * i + k], d_mean[k]);
     float gsl[3], gq[4];
     covariance_backward(f, g_cov_local, gsl, gq);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) pg.d_scale_log[3 * i + k] += gsl[k];
+    for (int k = 0; k < 3; ++k) atomicAdd(&pg.d_scale_log[3 * i + k], gsl[k]);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) pg.d_quat[4 * i + k] += gq[k];
+    for (int k = 0; k < 4; ++k) atomicAdd(&pg.d_quat[4 * i + k], gq[k]);
     }  // kMode != kProjOnly
   }
   }  // compacted list
