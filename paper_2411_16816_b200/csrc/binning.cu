@@ -27,8 +27,8 @@ namespace sb {
 
 namespace {
 
-constexpr int kRThreads = 256;
-constexpr int kRItems = 16;
+constexpr int kRThreads = 512;
+constexpr int kRItems = 8;
 constexpr int kRTile = kRThreads * kRItems;  // 4,096 items per CTA
 constexpr int kRWarps = kRThreads / 32;
 constexpr int kRMaxBins = 256;
@@ -45,6 +45,7 @@ __device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned lo
 }
 
 // Exclusive scan of one value per thread over a 256-thread CTA; `total` receives the CTA sum. s_warp: 8 words.
+template <int kWarps = kRWarps>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t inc = v;
@@ -58,7 +59,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   __syncthreads();
   uint32_t base = 0u, tot = 0u;
 #pragma unroll
-  for (int w = 0; w < kRWarps; ++w) {
+  for (int w = 0; w < kWarps; ++w) {
     const uint32_t c = s_warp[w];
     if (w < warp) base += c;
     tot += c;
@@ -122,7 +123,7 @@ constexpr int kStagePad = kRTile + kRTile / 16;  // staging index x + (x >> 4): 
 constexpr size_t kRadixSmem = sizeof(uint32_t) * (2 * kStagePad + (kRTile + 2));
 
 template <int kSrc, bool kWriteKeys>
-__global__ void __launch_bounds__(kRThreads, 3)
+__global__ void __launch_bounds__(kRThreads, 2)
 k_radix_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
              uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ hist,
              uint32_t* __restrict__ state, uint32_t* __restrict__ ticket, uint32_t* __restrict__ err, EmitSrc em) {
@@ -147,7 +148,7 @@ k_radix_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ 
     // (a) owner of the tile's first intersection: 256-ary search, offsets[k0] <= e0 < offsets[k0 + 1]
     int64_t lo = 0, hi = em.n;
     while (hi - lo > 1) {
-      const int64_t step = (hi - lo + 255) / 256;
+      const int64_t step = (hi - lo + kRThreads - 1) / kRThreads;
       const int64_t idx = lo + (int64_t)(tid + 1) * step;
       const int c = __syncthreads_count(idx < hi && (int64_t)em.offsets[idx] <= e0);
       lo += (int64_t)c * step;
@@ -336,7 +337,7 @@ constexpr int kSTile = 256 * kSItems;
 __global__ void __launch_bounds__(256)
 k_count_scan(const uint32_t* __restrict__ count, const uint32_t* __restrict__ order, int64_t n, uint32_t* __restrict__ offsets,
              uint32_t* __restrict__ state, uint32_t* __restrict__ ticket, uint32_t* __restrict__ err) {
-  __shared__ uint32_t s_warp[kRWarps];
+  __shared__ uint32_t s_warp[8];
   __shared__ uint32_t s_tile, s_base;
   __shared__ uint32_t s_out[kSTile + kSTile / 8];  // index j + (j >> 3): blocked writes, striped reads, no conflicts
   const int tid = threadIdx.x;
@@ -359,7 +360,7 @@ k_count_scan(const uint32_t* __restrict__ count, const uint32_t* __restrict__ or
 #pragma unroll
   for (int u = 0; u < kSItems; ++u) mine += c[u];
   uint32_t total;
-  const uint32_t excl_in_tile = block_excl_scan(mine, s_warp, total);
+  const uint32_t excl_in_tile = block_excl_scan<8>(mine, s_warp, total);
   if (tid == 0) {
     uint32_t excl = 0u;
     if (tile == 0) {
