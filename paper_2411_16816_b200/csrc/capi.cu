@@ -216,7 +216,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -344,6 +344,8 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->tile_begin, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->tile_end, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->to_vals0, sizeof(uint32_t) * T));
+  CU_TRY(c, cudaMalloc(&v->out.tile_wrap, T));
+  CU_TRY(c, cudaMemsetAsync(v->out.tile_wrap, 1, T, c->stream));
   CU_TRY(c, cudaMalloc(&v->tile_ws, tile_hist_bytes(v->s.tiles_x, v->s.tiles_y)));
   CU_TRY(c, cudaMalloc(&v->d_total, sizeof(int64_t)));
   if (std::getenv("SPLATB200_STATS")) {  // debug counters of the compositing kernels (read through view_array "raster_stats")

@@ -99,6 +99,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
 
   int64_t q_begin = 0, q_end = 1;  // camera: single pass
   if (!kCamera) { q_begin = ray_begin[tile]; q_end = ray_end[tile]; }
+  bool any_wrap = false;  // lidar, CTA-uniform: some batch needed the azimuth wrap
 
   for (int64_t q_base = q_begin; q_base < q_end; q_base += 256) {
     bool inside;
@@ -167,6 +168,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       sMask[tid] = (uint8_t)mask;
       // lidar: does any (entry, patch) pair of this batch need the azimuth wrap? (rare: tiles at the seam)
       const bool wrap = kCamera ? (__syncthreads(), false) : __syncthreads_or((mask & wrapm) != 0u) != 0;
+      any_wrap |= wrap;
       reinterpret_cast<uint2*>(sHit[warp])[lane] = make_uint2(0u, 0u);  // 256 bytes per warp
       pending = (int64_t)base;
       if (__all_sync(0xffffffffu, done)) continue;  // this warp's 32 queries have saturated
@@ -253,6 +255,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     __syncthreads();  // shared staging and patch boxes are reused by the next ray pass
     flush_hits();     // the last batch of a list that ended before every query saturated
   }
+  if (!kCamera && tid == 0) out.tile_wrap[tile] = any_wrap ? 1 : 0;
 }
 
 void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,

@@ -18,6 +18,8 @@ struct RasterOutDev {
   uint8_t* hit;        // I  per list entry: bit w set if some query of warp w of the tile's CTA blended it (saved for
                        //    the backward pass, which then revisits only those entries)
   int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
+  uint8_t* tile_wrap;  // T  lidar: 1 if some batch of the tile could not certify |azimuth difference| < pi (seam tiles);
+                       //    the backward skips the wrap elsewhere. Written by the forward.
   unsigned long long* stats;  // debug (SPLATB200_STATS=1), else null: [0] staged entries, [1] per-warp survivors of the cull
 };
 

@@ -52,7 +52,7 @@ struct WarpScratch {
 // Phase B for `n` parked entries (1 <= n <= kChunk).
 template <bool kCamera>
 __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int lane, int d_f, const RasterGradDev& rg,
-                                             const ParamGradDev& pg, float& dt_local) {
+                                             const ParamGradDev& pg, float& dt_local, bool wrap) {
   int E = 1;  // capacity: smallest power of two >= n
   while (E < n) E <<= 1;
   const int e = lane & (E - 1);
@@ -86,7 +86,7 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
       acc[23] = fmaf(gw, t, acc[23]);  // d/d v_r
     }
     float dx = q0.x - fmaf(gA.z, t, gA.x);
-    if (!kCamera) dx = wrap_pi(dx);
+    if (!kCamera && wrap) dx = wrap_pi(dx);
     const float dy = q0.y - fmaf(gA.w, t, gA.y);
     const float hx = 0.5f * gs * dx, hy = 0.5f * gs * dy;
     acc[16] = fmaf(hx, dx, acc[16]);
@@ -151,6 +151,8 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   WarpScratch& ws = sWs[warp];
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
   if (le <= lb) return;
+  // lidar: the forward pass certified, per tile, whether any azimuth difference can leave (-pi, pi) (raster_common.cuh)
+  const bool wrap = kCamera ? false : fwd.tile_wrap[tile] != 0;
 
   int64_t q_begin = 0, q_end = 1;
   if (!kCamera) { q_begin = ray_begin[tile]; q_end = ray_end[tile]; }
@@ -289,7 +291,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           }
           if (++n_slots == kChunk) {
             __syncwarp();
-            reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local);
+            reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
             n_slots = 0;
           }
         };
@@ -299,8 +301,8 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           const int j0 = sList[k], j1 = sList[has1 ? k - 1 : k];
           const float4 a0 = sA[j0], b0 = sB[j0], a1 = sA[j1], b1 = sB[j1];
           float dx0, dy0, dx1, dy1;
-          const float qf0 = alpha_qform<!kCamera>(a0, b0, qx, qy, t, dx0, dy0);
-          const float qf1 = alpha_qform<!kCamera>(a1, b1, qx, qy, t, dx1, dy1);
+          const float qf0 = alpha_qform<!kCamera>(a0, b0, qx, qy, t, dx0, dy0, wrap);
+          const float qf1 = alpha_qform<!kCamera>(a1, b1, qx, qy, t, dx1, dy1, wrap);
           AlphaEval ev;
           bool valid = (bstart + j0 < last) && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
           if (__any_sync(0xffffffffu, valid)) park(j0, valid, ev);
@@ -312,7 +314,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     }
     if (n_slots > 0) {  // drain what is left of this pass
       __syncwarp();
-      reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local);
+      reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
       n_slots = 0;
     }
     __syncthreads();  // patch boxes / staging / per-query rows are reused by the next ray pass
