@@ -184,6 +184,14 @@ int splatb200_view_sensor_grads(splatb200_view* v, splatb200_sensor_grads* out);
  * to HOST memory; copies are issued on the ctx stream. Any pointer may be NULL to skip it. */
 int splatb200_view_download(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib);
 int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, const float* g_alpha);
+/* Overlapped variants of the two calls above for PINNED host buffers: the copies run on the view's own copy
+ * streams (one per direction) beside the compute stream, ordered by events. download_async returns at once; the host buffers
+ * are complete after splatb200_ctx_sync (or any later stream-ordered call that synchronises, e.g. grads_download of a
+ * backward that depended on them). backward_host_overlapped uploads the upstream gradients on the host-to-device copy
+ * stream — after this view's pending download_async, because upstream gradients are a function of the rendered
+ * outputs — and runs the backward kernels once they have arrived; other views' kernels keep the GPU busy meanwhile. */
+int splatb200_view_download_async(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib);
+int splatb200_view_backward_host_overlapped(splatb200_view* v, const float* g_blend16, const float* g_alpha);
 
 /* ---- reference-granularity entry points --------------------------------------------------------
  * One call per function the reference ships as code, HOST buffers in and out, for callers that switch

@@ -33,7 +33,7 @@ struct splatb200_ctx {
   int64_t launches = 0;      // hand-written kernels
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
-  cudaStream_t aux = nullptr;  // independent small kernels of the binning stage run beside the depth sort
+  cudaStream_t aux = nullptr;  // spare non-blocking stream (binning fork experiment; unused on the hot path)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // scene
@@ -119,6 +119,10 @@ struct splatb200_view {
   uint32_t* to_vals0 = nullptr;
   RasterOutDev out{};
   float *g_blend_stage = nullptr, *g_alpha_stage = nullptr;
+  // overlapped host-buffer calls: forward done (compute -> d2h), download done, upload done, backward done
+  cudaEvent_t ev_fwd = nullptr, ev_dl = nullptr, ev_up = nullptr, ev_bwd = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // this view's copy streams (views overlap each other's transfers)
+  bool dl_pending = false, bwd_recorded = false;
   float* sensor_grads = nullptr;  // 6 + d_time_offset
   // actors
   ActorState* d_actors = nullptr;
@@ -220,6 +224,10 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
+  for (cudaEvent_t* e : {&v->ev_fwd, &v->ev_dl, &v->ev_up, &v->ev_bwd})
+    if (*e) { cudaEventDestroy(*e); *e = nullptr; }
+  for (cudaStream_t* q : {&v->s_h2d, &v->s_d2h})
+    if (*q) { cudaStreamSynchronize(*q); cudaStreamDestroy(*q); *q = nullptr; }
   for (auto& e : v->ev)
     for (auto& x : e)
       if (x) { cudaEventDestroy(x); x = nullptr; }
@@ -429,6 +437,10 @@ extern "C" const char* splatb200_last_error(const splatb200_ctx* c) { return c ?
 
 extern "C" int splatb200_ctx_sync(splatb200_ctx* c) {
   CU_TRY(c, cudaStreamSynchronize(c->stream));
+  for (auto* v : c->views) {  // copy streams of the overlapped host-buffer calls
+    if (v->s_h2d) CU_TRY(c, cudaStreamSynchronize(v->s_h2d));
+    if (v->s_d2h) CU_TRY(c, cudaStreamSynchronize(v->s_d2h));
+  }
   return SPLATB200_OK;
 }
 
@@ -898,6 +910,10 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   v->stage = 2;
   if (stop_after == 2) return SPLATB200_OK;
 
+  if (v->dl_pending) {  // an overlapped download of the previous render still reads the output buffers
+    CU_TRY(c, cudaStreamWaitEvent(st, v->ev_dl, 0));
+    v->dl_pending = false;
+  }
   v->out.hit_or = v->multi_pass ? 1 : 0;
   if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
   {
@@ -989,6 +1005,59 @@ extern "C" int splatb200_view_backward_host(splatb200_view* v, const float* g_bl
   CU_TRY(c, cudaMemcpyAsync(v->g_blend_stage, g_blend16, sizeof(float) * 16 * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
   CU_TRY(c, cudaMemcpyAsync(v->g_alpha_stage, g_alpha, sizeof(float) * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
   return splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
+}
+
+namespace {
+int ensure_copy_events(splatb200_view* v) {
+  splatb200_ctx* c = v->ctx;
+  for (cudaEvent_t* e : {&v->ev_fwd, &v->ev_dl, &v->ev_up, &v->ev_bwd})
+    if (!*e) CU_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaStream_t* q : {&v->s_h2d, &v->s_d2h})
+    if (!*q) CU_TRY(c, cudaStreamCreateWithFlags(q, cudaStreamNonBlocking));
+  return SPLATB200_OK;
+}
+}  // namespace
+
+extern "C" int splatb200_view_download_async(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib) {
+  splatb200_ctx* c = v->ctx;
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "download before forward");
+  int rc = ensure_copy_events(v);
+  if (rc) return rc;
+  const size_t P = (size_t)v->P;
+  CU_TRY(c, cudaEventRecord(v->ev_fwd, c->stream));
+  CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, v->ev_fwd, 0));
+  if (blend16 && P) CU_TRY(c, cudaMemcpyAsync(blend16, v->out.blend, sizeof(float) * 16 * P, cudaMemcpyDeviceToHost, v->s_d2h));
+  if (alpha && P) CU_TRY(c, cudaMemcpyAsync(alpha, v->out.alpha, sizeof(float) * P, cudaMemcpyDeviceToHost, v->s_d2h));
+  if (n_contrib && P) CU_TRY(c, cudaMemcpyAsync(n_contrib, v->out.n_contrib, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, v->s_d2h));
+  CU_TRY(c, cudaEventRecord(v->ev_dl, v->s_d2h));
+  v->dl_pending = true;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_backward_host_overlapped(splatb200_view* v, const float* g_blend16, const float* g_alpha) {
+  splatb200_ctx* c = v->ctx;
+  if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
+  int rc = ensure_copy_events(v);
+  if (rc) return rc;
+  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  if (!v->g_blend_stage) {
+    CU_TRY(c, cudaMalloc(&v->g_blend_stage, sizeof(float) * 16 * P));
+    CU_TRY(c, cudaMalloc(&v->g_alpha_stage, sizeof(float) * P));
+  }
+  // the upstream gradients are a function of the rendered outputs: their upload follows this view's download;
+  // the staging buffers may still be read by this view's previous backward
+  if (v->dl_pending) CU_TRY(c, cudaStreamWaitEvent(v->s_h2d, v->ev_dl, 0));
+  if (v->bwd_recorded) CU_TRY(c, cudaStreamWaitEvent(v->s_h2d, v->ev_bwd, 0));
+  CU_TRY(c, cudaMemcpyAsync(v->g_blend_stage, g_blend16, sizeof(float) * 16 * (size_t)v->P, cudaMemcpyHostToDevice, v->s_h2d));
+  CU_TRY(c, cudaMemcpyAsync(v->g_alpha_stage, g_alpha, sizeof(float) * (size_t)v->P, cudaMemcpyHostToDevice, v->s_h2d));
+  CU_TRY(c, cudaEventRecord(v->ev_up, v->s_h2d));
+  CU_TRY(c, cudaStreamWaitEvent(c->stream, v->ev_up, 0));
+  rc = splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
+  if (rc) return rc;
+  CU_TRY(c, cudaEventRecord(v->ev_bwd, c->stream));
+  v->bwd_recorded = true;
+  return SPLATB200_OK;
 }
 
 // ---- reference-granularity entry points ------------------------------------------------------------
