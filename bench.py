@@ -57,6 +57,7 @@ def workload_config(world: int):
                     "expected+median range",
         "n_gaussians": N_GAUSS, "lidar_rays": 128 * 1800, "camera_pixels": 1920 * 1080,
         "frames_per_step": world, "parallelism": f"frames x{world} (scene replicated, grads all-reduced)" if world > 1 else "single GPU",
+        "streams": "one per sensor view + the ctx stream",
         "l2_policy": "inputs larger than L2 (scene 112 MB + per-view records and worklists > 500 MB, L2 126 MB); no explicit flush",
     }
 
@@ -322,6 +323,7 @@ def run_b200(args):
             vl.backward_device(g_dev["l"][0].data_ptr(), g_dev["l"][1].data_ptr())
             vc.forward(0.0)
             vc.backward_device(g_dev["c"][0].data_ptr(), g_dev["c"][1].data_ptr())
+            ctx.join()      # view streams: order the ctx stream (NCCL, the timing event) after both sensors
             sdist.allreduce_grads(grads_t)
 
         def step_e2e():
@@ -341,6 +343,7 @@ def run_b200(args):
             for name, v in (("l", vl), ("c", vc)):
                 _, _, gb, ga = g_host[name]
                 v.backward_host_overlapped(gb, ga)
+            ctx.join()
             sdist.allreduce_grads(grads_t)
             ctx.grads_into(*gh_parts)
             ctx.sync()
@@ -361,17 +364,25 @@ def run_b200(args):
             return float(ms.item()), t0, t1
 
         # ---- device-resident timing ------------------------------------------------------------
+        # the two sensors of a frame run on their own streams (the lidar's latency-bound binning and the tail of its
+        # compositing grid overlap the camera's kernels); --serial keeps everything on one stream
+        ctx.set_view_streams(not args.serial)
         for _ in range(max(args.warmup, 0)):
             step_device()
-        ctx.set_profiling(True)
         l0, ll0 = ctx.launch_count, ctx.library_launch_count
         sampler = ClockSampler(local) if rank == 0 else None
         ms_dev, t0, t1 = timed(step_device, args.steps)
         clocks = sampler.stop(t0, t1) if sampler else None
         launches, lib_launches = ctx.launch_count - l0, ctx.library_launch_count - ll0
+        # per-stage CUDA-event times: a separate, serialised pass (one stream), so that a stage's time is its own
+        ctx.set_view_streams(False)
+        ctx.set_profiling(True)
+        ms_serial, _, _ = timed(step_device, max(3, min(args.steps, 10)))
+        ms_serial /= max(3, min(args.steps, 10))
         stage_l, stage_c = vl.stage_ms(), vc.stage_ms()
         ctx.set_profiling(False)
         stats_l, stats_c = vl.stats(), vc.stats()
+        ctx.set_view_streams(not args.serial)
 
         # per-sensor rates (each sensor's fwd+bwd timed alone, device-resident)
         def only(v, g):
@@ -435,6 +446,8 @@ def run_b200(args):
         "kernel_ms": ms_k, "kernel_bytes": bytes_k, "kernel_share_of_step": ms_k / stage_total if stage_total else None,
         "frame_algorithmic_bytes": frame_bytes, "frame_frac": frame_bytes / (per_step * 1e-3) / 1e9 / peak,
         "stage_ms": {"lidar": stage_l, "camera": stage_c},
+        "stage_ms_note": "per-stage CUDA-event times from a serialised pass (one stream, %.3f ms per frame); the timed "
+                         "region runs the two sensors on their own streams" % ms_serial if not args.serial else "single stream",
         "note": "compositing is fp32-issue bound (~120 flop/B, SURVEY.md §8(d)), so its HBM fraction is low by construction; "
                 "frame_frac = algorithmic bytes of the whole frame / step time / peak",
     }
@@ -473,6 +486,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", default="auto", choices=["auto", "full", "quarter"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--serial", action="store_true", help="one stream for both sensors (default: one stream per sensor view)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

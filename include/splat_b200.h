@@ -108,6 +108,13 @@ int64_t splatb200_ctx_library_launch_count(const splatb200_ctx* ctx);
  * synchronisation point, so enabling profiling adds no host-device synchronisation to a timed region.
  * This is the measurement hook bench.py's roofline uses. */
 int splatb200_ctx_set_profiling(splatb200_ctx* ctx, int32_t on);
+/* View streams (off by default). On: every view enqueues its forward / backward on its own stream, so one sensor's
+ * latency-bound binning kernels and the tail of its compositing grid overlap another sensor's kernels. A view's work is
+ * ordered after everything asked of the ctx stream before the call; the ctx stream is ordered after the views' work by
+ * zero / upload / download / sync calls, by every other call on that view, and by splatb200_ctx_join — call it before
+ * work you enqueue yourself on the ctx stream (e.g. an NCCL all-reduce of the bound gradient buffer) reads the results. */
+int splatb200_ctx_set_view_streams(splatb200_ctx* ctx, int32_t on);
+int splatb200_ctx_join(splatb200_ctx* ctx);
 int splatb200_view_stage_ms(splatb200_view* v, float out_ms[8]);
 
 /* ---- scene: GaussianSet + SceneGraph (scene.hpp:11-45, 171-187) ------------------------------ */

@@ -33,6 +33,8 @@ struct splatb200_ctx {
   int64_t launches = 0;      // hand-written kernels
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
+  bool view_streams = false;   // views run forward / backward on their own streams (splatb200_ctx_set_view_streams)
+  cudaEvent_t ev_ctx = nullptr; // 'everything asked of the ctx stream so far'
   cudaStream_t aux = nullptr;  // spare non-blocking stream (binning fork experiment; unused on the hot path)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
@@ -122,6 +124,10 @@ struct splatb200_view {
   // overlapped host-buffer calls: forward done (compute -> d2h), download done, upload done, backward done
   cudaEvent_t ev_fwd = nullptr, ev_dl = nullptr, ev_up = nullptr, ev_bwd = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // this view's copy streams (views overlap each other's transfers)
+  cudaStream_t vs = nullptr;       // this view's work stream (ctx->view_streams)
+  cudaEvent_t ev_last = nullptr;   // last work enqueued on vs
+  bool busy = false;               // vs holds work the ctx stream has not been ordered after yet
+  bool wait_up = false;            // the next backward waits for ev_up (overlapped upstream-gradient upload)
   bool dl_pending = false, bwd_recorded = false;
   float* sensor_grads = nullptr;  // 6 + d_time_offset
   // actors
@@ -226,8 +232,9 @@ void free_view_buffers(splatb200_view* v) {
   v->h_total = nullptr;
   for (cudaEvent_t* e : {&v->ev_fwd, &v->ev_dl, &v->ev_up, &v->ev_bwd})
     if (*e) { cudaEventDestroy(*e); *e = nullptr; }
-  for (cudaStream_t* q : {&v->s_h2d, &v->s_d2h})
+  for (cudaStream_t* q : {&v->s_h2d, &v->s_d2h, &v->vs})
     if (*q) { cudaStreamSynchronize(*q); cudaStreamDestroy(*q); *q = nullptr; }
+  if (v->ev_last) { cudaEventDestroy(v->ev_last); v->ev_last = nullptr; }
   for (auto& e : v->ev)
     for (auto& x : e)
       if (x) { cudaEventDestroy(x); x = nullptr; }
@@ -245,6 +252,36 @@ void harvest_stage_events(splatb200_view* v) {
     }
     v->ev_valid[k] = false;
   }
+}
+
+// ---- view streams -----------------------------------------------------------------------------------
+// With ctx->view_streams every view enqueues its forward / backward on its own stream, so that one sensor's
+// latency-bound binning kernels and the tail of its compositing grid overlap another sensor's kernels. Ordering:
+//   * a view's work is ordered after everything asked of the ctx stream before the call (scene upload, zero_grads);
+//   * the ctx stream is ordered after the views' work at the ctx-level calls that consume it (zero_grads, uploads,
+//     grads_download, ctx_sync, ctx_join) and at every other view-level call on that view.
+cudaStream_t work_stream(splatb200_view* v) {
+  splatb200_ctx* c = v->ctx;
+  if (!c->view_streams) return c->stream;
+  if (!v->vs) cudaStreamCreateWithFlags(&v->vs, cudaStreamNonBlocking);
+  if (!v->ev_last) cudaEventCreateWithFlags(&v->ev_last, cudaEventDisableTiming);
+  if (!c->ev_ctx) cudaEventCreateWithFlags(&c->ev_ctx, cudaEventDisableTiming);
+  cudaEventRecord(c->ev_ctx, c->stream);
+  cudaStreamWaitEvent(v->vs, c->ev_ctx, 0);
+  return v->vs;
+}
+void mark_busy(splatb200_view* v, cudaStream_t st) {
+  if (st == v->ctx->stream || !v->ev_last) return;
+  cudaEventRecord(v->ev_last, st);
+  v->busy = true;
+}
+void join_view(splatb200_view* v) {
+  if (!v->busy) return;
+  cudaStreamWaitEvent(v->ctx->stream, v->ev_last, 0);
+  v->busy = false;
+}
+void join_all(splatb200_ctx* c) {
+  for (auto* v : c->views) join_view(v);
 }
 
 struct StageTimer {
@@ -430,12 +467,14 @@ extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_ctx) cudaEventDestroy(c->ev_ctx);
   delete c;
 }
 
 extern "C" const char* splatb200_last_error(const splatb200_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
 
 extern "C" int splatb200_ctx_sync(splatb200_ctx* c) {
+  join_all(c);
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   for (auto* v : c->views) {  // copy streams of the overlapped host-buffer calls
     if (v->s_h2d) CU_TRY(c, cudaStreamSynchronize(v->s_h2d));
@@ -449,10 +488,23 @@ extern "C" int64_t splatb200_ctx_launch_count(const splatb200_ctx* c) { return c
 extern "C" int64_t splatb200_ctx_library_launch_count(const splatb200_ctx* c) { return c->lib_launches; }
 
 extern "C" int splatb200_ctx_set_profiling(splatb200_ctx* c, int32_t on) {
+  join_all(c);
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   c->profiling = on != 0;
   for (auto* v : c->views)
     for (int k = 0; k < 8; ++k) { v->ev_valid[k] = false; v->ev_sum_ms[k] = 0.0; v->ev_count[k] = 0; }
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_ctx_set_view_streams(splatb200_ctx* c, int32_t on) {
+  join_all(c);
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  c->view_streams = on != 0;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_ctx_join(splatb200_ctx* c) {
+  join_all(c);
   return SPLATB200_OK;
 }
 
@@ -468,6 +520,7 @@ extern "C" int splatb200_view_stage_ms(splatb200_view* v, float out_ms[8]) {
 extern "C" int splatb200_scene_upload(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
                                       const float* quat, const float* opacity_logit, const float* color,
                                       const float* feature, const int32_t* actor_id) {
+  join_all(c);
   if (n < 0 || d_f < 0 || d_f > 13) return c->fail(SPLATB200_EINVAL, "scene_upload: need n >= 0 and 0 <= d_f <= 13");
   CU_TRY(c, cudaSetDevice(c->device));
   // Same shape as the resident scene (the per-iteration case: parameters change, sizes do not): keep the
@@ -511,6 +564,7 @@ extern "C" int splatb200_scene_bind_device(splatb200_ctx* c, int64_t n, int32_t 
                                            const float* scale_log, const float* quat, const float* opacity_logit,
                                            const float* color, const float* feature, const int32_t* actor_id,
                                            int32_t max_actor_id) {
+  join_all(c);
   if (n < 0 || d_f < 0 || d_f > 13) return c->fail(SPLATB200_EINVAL, "scene_bind_device: need n >= 0 and 0 <= d_f <= 13");
   CU_TRY(c, cudaSetDevice(c->device));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
@@ -567,6 +621,7 @@ extern "C" int splatb200_scene_actor_velocity(splatb200_ctx* c, int32_t track, d
 
 // ---- grads --------------------------------------------------------------------------------------
 extern "C" int splatb200_grads_zero(splatb200_ctx* c) {
+  join_all(c);
   if (c->grads) CU_TRY(c, cudaMemsetAsync(c->grads, 0, sizeof(float) * (size_t)c->grads_floats, c->stream));
   for (auto* v : c->views) {
     if (v->actor_pending) {
@@ -580,6 +635,7 @@ extern "C" int splatb200_grads_zero(splatb200_ctx* c) {
 extern "C" int64_t splatb200_grads_size(const splatb200_ctx* c) { return c->grads_floats; }
 extern "C" float* splatb200_grads_device_ptr(splatb200_ctx* c) { return c->grads; }
 extern "C" int splatb200_grads_bind_device(splatb200_ctx* c, float* dev, int64_t n_floats) {
+  join_all(c);
   if (n_floats != (int64_t)(14 + c->d_f) * c->n) return c->fail(SPLATB200_EINVAL, "grads_bind_device: size must be (14 + d_f) * N floats");
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   if (c->owns_grads) dfree(c->grads);
@@ -590,6 +646,7 @@ extern "C" int splatb200_grads_bind_device(splatb200_ctx* c, float* dev, int64_t
 }
 extern "C" int splatb200_grads_download(splatb200_ctx* c, float* d_mean, float* d_scale_log, float* d_quat,
                                         float* d_opacity_logit, float* d_color, float* d_feature) {
+  join_all(c);
   const ParamGradDev g = c->pg();
   const size_t n = (size_t)c->n;
   auto dl = [&](float* dst, const float* src, size_t w) -> cudaError_t {
@@ -606,6 +663,7 @@ extern "C" int splatb200_grads_download(splatb200_ctx* c, float* d_mean, float* 
   return SPLATB200_OK;
 }
 extern "C" int splatb200_grads_download_actor(splatb200_ctx* c, int32_t track, double* d_pose_offset, double* d_vel_offset6) {
+  join_all(c);
   if (track < 0 || track >= (int)c->tracks.size()) return c->fail(SPLATB200_EINVAL, "track index out of range");
   for (auto* v : c->views) {
     int rc = finalize_actor_grads(v);
@@ -753,6 +811,7 @@ extern "C" int splatb200_view_create_lidar(splatb200_ctx* c, const splatb200_lid
 }
 
 extern "C" void splatb200_view_destroy(splatb200_view* v) {
+  if (v && v->vs) cudaStreamSynchronize(v->vs);
   if (!v) return;
   splatb200_ctx* c = v->ctx;
   cudaSetDevice(c->device);
@@ -811,6 +870,7 @@ static int prepare_actors(splatb200_view* v, float t_scene) {
   }
   // the previous frame's kernels may still read d_actors: order the overwrite after them
   CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (v->vs) CU_TRY(c, cudaStreamSynchronize(v->vs));
   CU_TRY(c, cudaMemcpy(v->d_actors, st.data(), sizeof(ActorState) * na, cudaMemcpyHostToDevice));
   return SPLATB200_OK;
 }
@@ -827,12 +887,13 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   if (rc) return rc;
   v->s.d_f = c->d_f;
   v->s.channels = v->s.is_camera ? 3 + c->d_f : c->d_f;
-  cudaStream_t st = c->stream;
+  cudaStream_t st = work_stream(v);
+  struct Busy { splatb200_view* v; cudaStream_t st; ~Busy() { mark_busy(v, st); } } busy_guard{v, st};
   const SceneDev sc = c->scene_dev(v->d_actors);
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, st));
 
   {
-    StageTimer tm(v, 0);
+    StageTimer tm(v, 0, st);
     launch_project(v->s, sc, v->proj, st);
   }
   CHECK_LAUNCH(c, "k_project");
@@ -860,7 +921,7 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     }
     CHECK_LAUNCH(c, "k_tile_hist / k_tile_scan");
     {
-      StageTimer tm(v, 1);
+      StageTimer tm(v, 1, st);
       // depth order of the Gaussians (stable: ties in ascending source index), then offsets in that order
       v->order_sel = 0;
       c->launches += launch_depth_sort_scan(v->proj.dkey, v->dkey_alt, v->order0, v->order1,
@@ -892,7 +953,7 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
 
   v->sorted_sel = 0;
   if (v->I > 0) {
-    StageTimer tm(v, 3);
+    StageTimer tm(v, 3, st);
     int nl = 0;
     if (!v->two_level) {
       v->sorted_sel = launch_tile_sort(c->n, v->I, v->offsets, v->order(), v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x,
@@ -917,7 +978,7 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   v->out.hit_or = v->multi_pass ? 1 : 0;
   if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
   {
-    StageTimer tm(v, 5);
+    StageTimer tm(v, 5, st);
     launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
                       v->out, st);
   }
@@ -929,6 +990,7 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
 
 extern "C" int splatb200_view_stats_get(splatb200_view* v, splatb200_view_stats* out) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "stats before forward");
   std::vector<uint32_t> cnt((size_t)c->n);
   if (c->n) CU_TRY(c, cudaMemcpyAsync(cnt.data(), v->proj.count, sizeof(uint32_t) * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
@@ -953,18 +1015,23 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
   CU_TRY(c, cudaSetDevice(c->device));
   if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
   if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
-  cudaStream_t st = c->stream;
+  cudaStream_t st = work_stream(v);
+  struct Busy { splatb200_view* v; cudaStream_t st; ~Busy() { mark_busy(v, st); } } busy_guard{v, st};
+  if (v->wait_up) {  // overlapped upload of the upstream gradients (backward_host_overlapped)
+    CU_TRY(c, cudaStreamWaitEvent(st, v->ev_up, 0));
+    v->wait_up = false;
+  }
   RasterGradDev rg{v->rg};
   const ParamGradDev pg = c->pg();
   if (v->I > 0) {
-    StageTimer tm(v, 6);
+    StageTimer tm(v, 6, st);
     launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
                       v->out, g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
     CHECK_LAUNCH(c, "k_raster_bwd");
     c->launches += 1;
   }
   {
-    StageTimer tm(v, 7);
+    StageTimer tm(v, 7, st);
     launch_project_bwd(v->s, c->scene_dev(v->d_actors), v->proj, rg, pg, v->sensor_grads, v->actor_acc, st);
   }
   CHECK_LAUNCH(c, "k_project_bwd");
@@ -975,6 +1042,7 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
 
 extern "C" int splatb200_view_sensor_grads(splatb200_view* v, splatb200_sensor_grads* out) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   float h[8];
   CU_TRY(c, cudaMemcpyAsync(h, v->sensor_grads, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
@@ -985,6 +1053,7 @@ extern "C" int splatb200_view_sensor_grads(splatb200_view* v, splatb200_sensor_g
 
 extern "C" int splatb200_view_download(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "download before forward");
   const size_t P = (size_t)v->P;
   if (blend16 && P) CU_TRY(c, cudaMemcpyAsync(blend16, v->out.blend, sizeof(float) * 16 * P, cudaMemcpyDeviceToHost, c->stream));
@@ -996,6 +1065,7 @@ extern "C" int splatb200_view_download(splatb200_view* v, float* blend16, float*
 
 extern "C" int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, const float* g_alpha) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
   const size_t P = (size_t)std::max<int64_t>(1, v->P);
   if (!v->g_blend_stage) {
@@ -1024,8 +1094,12 @@ extern "C" int splatb200_view_download_async(splatb200_view* v, float* blend16, 
   int rc = ensure_copy_events(v);
   if (rc) return rc;
   const size_t P = (size_t)v->P;
-  CU_TRY(c, cudaEventRecord(v->ev_fwd, c->stream));
-  CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, v->ev_fwd, 0));
+  if (v->busy) {  // the forward ran on the view's own stream
+    CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, v->ev_last, 0));
+  } else {
+    CU_TRY(c, cudaEventRecord(v->ev_fwd, c->stream));
+    CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, v->ev_fwd, 0));
+  }
   if (blend16 && P) CU_TRY(c, cudaMemcpyAsync(blend16, v->out.blend, sizeof(float) * 16 * P, cudaMemcpyDeviceToHost, v->s_d2h));
   if (alpha && P) CU_TRY(c, cudaMemcpyAsync(alpha, v->out.alpha, sizeof(float) * P, cudaMemcpyDeviceToHost, v->s_d2h));
   if (n_contrib && P) CU_TRY(c, cudaMemcpyAsync(n_contrib, v->out.n_contrib, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, v->s_d2h));
@@ -1052,10 +1126,10 @@ extern "C" int splatb200_view_backward_host_overlapped(splatb200_view* v, const 
   CU_TRY(c, cudaMemcpyAsync(v->g_blend_stage, g_blend16, sizeof(float) * 16 * (size_t)v->P, cudaMemcpyHostToDevice, v->s_h2d));
   CU_TRY(c, cudaMemcpyAsync(v->g_alpha_stage, g_alpha, sizeof(float) * (size_t)v->P, cudaMemcpyHostToDevice, v->s_h2d));
   CU_TRY(c, cudaEventRecord(v->ev_up, v->s_h2d));
-  CU_TRY(c, cudaStreamWaitEvent(c->stream, v->ev_up, 0));
+  v->wait_up = true;
   rc = splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
   if (rc) return rc;
-  CU_TRY(c, cudaEventRecord(v->ev_bwd, c->stream));
+  CU_TRY(c, cudaEventRecord(v->ev_bwd, (c->view_streams && v->vs) ? v->vs : c->stream));
   v->bwd_recorded = true;
   return SPLATB200_OK;
 }
@@ -1100,6 +1174,7 @@ int run_dump(splatb200_view* v, std::vector<float>& h) {
 
 extern "C" int splatb200_view_composed(splatb200_view* v, float* mean_w, float* cov_w, float* vel_dyn_w, float* opacity) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "view_composed before forward");
   std::vector<float> h;
   int rc = run_dump(v, h);
@@ -1118,6 +1193,7 @@ extern "C" int splatb200_view_composed(splatb200_view* v, float* mean_w, float* 
 
 extern "C" int64_t splatb200_view_projected(splatb200_view* v, int64_t* source_index, float* fields25) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "view_projected before forward");
   std::vector<int64_t> vis;
   int rc = visible_list(v, vis);
@@ -1161,6 +1237,7 @@ extern "C" int splatb200_view_project_backward(splatb200_view* v, const float* g
                                                const float* g_cov2d, const float* g_velocity, int64_t begin, int64_t end,
                                                float* g_mean_w, float* g_cov_w, float* g_vel_dyn_w) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   CU_TRY(c, cudaSetDevice(c->device));
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
   std::vector<int64_t> vis;
@@ -1196,6 +1273,7 @@ extern "C" int splatb200_view_project_backward(splatb200_view* v, const float* g
 extern "C" int splatb200_view_compose_backward(splatb200_view* v, const float* g_mean_w, const float* g_cov_w,
                                                const float* g_vel_dyn_w, const float* g_opacity, int64_t begin, int64_t end) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   CU_TRY(c, cudaSetDevice(c->device));
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
   if (begin < 0 || end > c->n || begin > end) return c->fail(SPLATB200_EINVAL, "compose_backward: [begin, end) outside the scene");
@@ -1228,6 +1306,7 @@ extern "C" int splatb200_view_compose_backward(splatb200_view* v, const float* g
 extern "C" int splatb200_view_backward_projected(splatb200_view* v, const float* g_mean2d, const float* g_range,
                                                  const float* g_cov2d, const float* g_velocity, const float* g_opacity) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   CU_TRY(c, cudaSetDevice(c->device));
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
   if (c->n == 0) return SPLATB200_OK;
@@ -1258,6 +1337,7 @@ template <class T> int fetch(splatb200_ctx* c, std::vector<T>& h, const T* d, si
 
 extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, void* dst) {
   splatb200_ctx* c = v->ctx;
+  join_view(v);  // order the ctx stream after the view's own stream
   const std::string name(name_c ? name_c : "");
   if (v->stage < 1) return c->fail(SPLATB200_ERUNTIME, "view_array before forward");
   const size_t N = (size_t)c->n;

@@ -673,3 +673,43 @@ def test_overlapped_host_buffer_calls(ctx):
             y = y.astype(np.float64).reshape(sc.n, -1)
             rel = np.abs(x - y).max(1) / np.maximum(np.abs(y).max(1), 1e-3 * max(np.abs(y).max(), 1e-30))
             assert np.quantile(rel, 0.99) <= 1e-3, (step, k)
+
+
+def test_view_streams_match_single_stream(ctx):
+    """splatb200_ctx_set_view_streams: two views on their own streams produce the single-stream outputs bit for bit and
+    the same accumulated gradients, over repeated frames (ordering against zero_grads / scene re-upload / download)."""
+    sc = synth.make_scene(30000, seed=41, r_max=40.0, scale_mean=0.1)
+    ctx.upload_scene(sc)
+    lid = synth.lidar32()
+    vl = ctx.lidar_view(lid, synth.grid_rays(lid), ST)
+    vc = ctx.camera_view(synth.make_camera(width=640, height=360), ST)
+    ups = {}
+    for name, v in (("l", vl), ("c", vc)):
+        gb, ga = synth.upstream(v.P, seed=5)
+        if name == "l":
+            gb[:, 14:] = 0
+        ups[name] = (gb, ga)
+
+    def frame():
+        ctx.upload_scene(sc)
+        ctx.zero_grads()
+        for name, v in (("l", vl), ("c", vc)):
+            v.forward(0.0)
+            v.backward(*ups[name])
+        ctx.join()
+        g = {k: x.copy() for k, x in ctx.grads().items() if k != "actors"}
+        return g, {n: (v.array("blend").copy(), v.array("n_contrib").copy()) for n, v in (("l", vl), ("c", vc))}
+
+    g_ref, out_ref = frame()
+    ctx.set_view_streams(True)
+    try:
+        for _ in range(4):
+            g, out = frame()
+            for n in ("l", "c"):
+                assert np.array_equal(out[n][0], out_ref[n][0]) and np.array_equal(out[n][1], out_ref[n][1]), n
+            for k, y in g_ref.items():
+                x, y2 = g[k].astype(np.float64).reshape(sc.n, -1), y.astype(np.float64).reshape(sc.n, -1)
+                rel = np.abs(x - y2).max(1) / np.maximum(np.abs(y2).max(1), 1e-3 * max(np.abs(y2).max(), 1e-30))
+                assert np.quantile(rel, 0.99) <= 1e-3, k
+    finally:
+        ctx.set_view_streams(False)
