@@ -38,6 +38,8 @@ N_GAUSS = 1_000_000
 SCENE_SEED = 3
 METRIC = "lidar Mrays/s + camera MPix/s, fwd+bwd (one frame = 128-beam lidar sweep + 1920x1080 RS camera, 1M Gaussians)"
 UNIT = "Mqueries/s"
+CAMERA_FIRST = os.environ.get("BENCH_CAMERA_FIRST", "0") == "1"   # enqueue order of the two sensors of a frame (no measurable effect)
+HOST_THREADS = os.environ.get("BENCH_HOST_THREADS", "1") == "1"    # one host thread per sensor view (with view streams)
 
 
 def frame_sensors(frame: int):
@@ -57,7 +59,7 @@ def workload_config(world: int):
                     "expected+median range",
         "n_gaussians": N_GAUSS, "lidar_rays": 128 * 1800, "camera_pixels": 1920 * 1080,
         "frames_per_step": world, "parallelism": f"frames x{world} (scene replicated, grads all-reduced)" if world > 1 else "single GPU",
-        "streams": "one per sensor view + the ctx stream",
+        "streams": "one per sensor view + the ctx stream; one host thread per view",
         "l2_policy": "inputs larger than L2 (scene 112 MB + per-view records and worklists > 500 MB, L2 126 MB); no explicit flush",
     }
 
@@ -316,13 +318,25 @@ def run_b200(args):
                 dist.barrier()
             torch.cuda.synchronize()
 
+        pool = None
+        if HOST_THREADS and not args.serial:
+            from concurrent.futures import ThreadPoolExecutor
+            pool = ThreadPoolExecutor(max_workers=2)
+
         def step_device():
             """inputs resident in HBM: scene, rays, upstream gradients"""
             ctx.zero_grads()
-            vl.forward(0.0)
-            vl.backward_device(g_dev["l"][0].data_ptr(), g_dev["l"][1].data_ptr())
-            vc.forward(0.0)
-            vc.backward_device(g_dev["c"][0].data_ptr(), g_dev["c"][1].data_ptr())
+            order = ((vc, "c"), (vl, "l")) if CAMERA_FIRST else ((vl, "l"), (vc, "c"))
+
+            def run_view(v, k):
+                v.forward(0.0)      # contains the one host sync of a render (the worklist size)
+                v.backward_device(g_dev[k][0].data_ptr(), g_dev[k][1].data_ptr())
+            if pool is not None:    # one host thread per view: neither view's host sync delays the other's launches
+                for f in [pool.submit(run_view, v, k) for v, k in order]:
+                    f.result()
+            else:
+                for v, k in order:
+                    run_view(v, k)
             ctx.join()      # view streams: order the ctx stream (NCCL, the timing event) after both sensors
             sdist.allreduce_grads(grads_t)
 
@@ -336,13 +350,23 @@ def run_b200(args):
             # (they are a function of them).
             # (lidar first measured best: its small transfers and its backward then run beside the camera's forward
             # and the camera's 149 MB download; camera first was 0.6 ms slower)
-            for name, v in (("l", vl), ("c", vc)):
+            def run_view(name, v):
                 v.forward(0.0)
                 _, _, _, vb, va, vn = out_host[name]
                 v.download_async(vb, va, vn)
-            for name, v in (("l", vl), ("c", vc)):
                 _, _, gb, ga = g_host[name]
                 v.backward_host_overlapped(gb, ga)
+            if pool is not None:
+                for f in [pool.submit(run_view, name, v) for name, v in (("l", vl), ("c", vc))]:
+                    f.result()
+            else:
+                for name, v in (("l", vl), ("c", vc)):
+                    v.forward(0.0)
+                    _, _, _, vb, va, vn = out_host[name]
+                    v.download_async(vb, va, vn)
+                for name, v in (("l", vl), ("c", vc)):
+                    _, _, gb, ga = g_host[name]
+                    v.backward_host_overlapped(gb, ga)
             ctx.join()
             sdist.allreduce_grads(grads_t)
             ctx.grads_into(*gh_parts)

@@ -112,7 +112,10 @@ int splatb200_ctx_set_profiling(splatb200_ctx* ctx, int32_t on);
  * latency-bound binning kernels and the tail of its compositing grid overlap another sensor's kernels. A view's work is
  * ordered after everything asked of the ctx stream before the call; the ctx stream is ordered after the views' work by
  * zero / upload / download / sync calls, by every other call on that view, and by splatb200_ctx_join — call it before
- * work you enqueue yourself on the ctx stream (e.g. an NCCL all-reduce of the bound gradient buffer) reads the results. */
+ * work you enqueue yourself on the ctx stream (e.g. an NCCL all-reduce of the bound gradient buffer) reads the results.
+ * Threads: with view streams on, DIFFERENT views of one ctx may be driven from different host threads (forward,
+ * backward, download_async, backward_host_overlapped), so that one view's host sync — the worklist size, read once per
+ * forward — does not delay another view's launches; ctx-level calls must not run concurrently with them. */
 int splatb200_ctx_set_view_streams(splatb200_ctx* ctx, int32_t on);
 int splatb200_ctx_join(splatb200_ctx* ctx);
 int splatb200_view_stage_ms(splatb200_view* v, float out_ms[8]);

@@ -3,6 +3,7 @@
 // composite, and its reverse. Host code only; the kernels live in forward.cu / binning.cu /
 // raster_bwd.cu / project_bwd.cu.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -30,11 +31,10 @@ struct splatb200_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string err;
-  int64_t launches = 0;      // hand-written kernels
+  std::atomic<int64_t> launches{0};      // hand-written kernels (views may be driven from several host threads)
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
   bool view_streams = false;   // views run forward / backward on their own streams (splatb200_ctx_set_view_streams)
-  cudaEvent_t ev_ctx = nullptr; // 'everything asked of the ctx stream so far'
   cudaStream_t aux = nullptr;  // spare non-blocking stream (binning fork experiment; unused on the hot path)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
@@ -126,6 +126,7 @@ struct splatb200_view {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // this view's copy streams (views overlap each other's transfers)
   cudaStream_t vs = nullptr;       // this view's work stream (ctx->view_streams)
   cudaEvent_t ev_last = nullptr;   // last work enqueued on vs
+  cudaEvent_t ev_ctx = nullptr;    // 'everything asked of the ctx stream so far', as seen at this view's last call
   bool busy = false;               // vs holds work the ctx stream has not been ordered after yet
   bool wait_up = false;            // the next backward waits for ev_up (overlapped upstream-gradient upload)
   bool dl_pending = false, bwd_recorded = false;
@@ -235,6 +236,7 @@ void free_view_buffers(splatb200_view* v) {
   for (cudaStream_t* q : {&v->s_h2d, &v->s_d2h, &v->vs})
     if (*q) { cudaStreamSynchronize(*q); cudaStreamDestroy(*q); *q = nullptr; }
   if (v->ev_last) { cudaEventDestroy(v->ev_last); v->ev_last = nullptr; }
+  if (v->ev_ctx) { cudaEventDestroy(v->ev_ctx); v->ev_ctx = nullptr; }
   for (auto& e : v->ev)
     for (auto& x : e)
       if (x) { cudaEventDestroy(x); x = nullptr; }
@@ -265,9 +267,9 @@ cudaStream_t work_stream(splatb200_view* v) {
   if (!c->view_streams) return c->stream;
   if (!v->vs) cudaStreamCreateWithFlags(&v->vs, cudaStreamNonBlocking);
   if (!v->ev_last) cudaEventCreateWithFlags(&v->ev_last, cudaEventDisableTiming);
-  if (!c->ev_ctx) cudaEventCreateWithFlags(&c->ev_ctx, cudaEventDisableTiming);
-  cudaEventRecord(c->ev_ctx, c->stream);
-  cudaStreamWaitEvent(v->vs, c->ev_ctx, 0);
+  if (!v->ev_ctx) cudaEventCreateWithFlags(&v->ev_ctx, cudaEventDisableTiming);
+  cudaEventRecord(v->ev_ctx, c->stream);
+  cudaStreamWaitEvent(v->vs, v->ev_ctx, 0);
   return v->vs;
 }
 void mark_busy(splatb200_view* v, cudaStream_t st) {
@@ -467,7 +469,6 @@ extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->ev_ctx) cudaEventDestroy(c->ev_ctx);
   delete c;
 }
 

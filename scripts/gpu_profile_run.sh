@@ -11,10 +11,10 @@ timeout 600 python bench.py > "$OUT/bench_${TAG}.json" 2> "$OUT/bench_${TAG}.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_${TAG}_reference_arm.json" 2>> "$OUT/bench_${TAG}.err"
 # 2. launch list of the same command (shares only; cold-cache, serialised)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file "$OUT/launches_${TAG}.csv" \
-    python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
+    python bench.py --steps 2 --warmup 1 --no-cpu --serial > /dev/null 2>&1
 # 3. full-set capture of every hand-written kernel of one frame (second frame: warm)
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"^(k_|void k_|sb::k_|void sb::k_)" -s 30 -c 30 \
-    -o "$OUT/prof_${TAG}" python bench.py --steps 1 --warmup 1 --no-cpu > "$OUT/ncu_${TAG}.log" 2>&1
+    -o "$OUT/prof_${TAG}" python bench.py --steps 1 --warmup 1 --no-cpu --serial > "$OUT/ncu_${TAG}.log" 2>&1
 # 4. sanitizers on the small parity configs
 timeout 900 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -x -k "config1 or lidar_forward_backward or camera_forward_backward or edge_cases or more_than_256 or one_level" \
     > "$OUT/sanitizer_memcheck_${TAG}.log" 2>&1

@@ -19,7 +19,7 @@ for r in rows[1:]:
         continue
     tot[r[ki][:70]][0] += v / 1000.0; tot[r[ki][:70]][1] += 1
 s = sum(v[0] for v in tot.values())
-print("ncu --metrics gpu__time_duration.sum --clock-control none -c 600 : python bench.py --steps 2 --warmup 1 --no-cpu")
+print("ncu --metrics gpu__time_duration.sum --clock-control none -c 600 : python bench.py --steps 2 --warmup 1 --no-cpu --serial  (one stream: deterministic kernel order; ncu serialises launches anyway)")
 print("per-kernel totals over the captured launches (cold-cache, serialised: compare SHARES with bench.py's roofline.stage_ms)")
 for k, (us, n) in sorted(tot.items(), key=lambda x: -x[1][0]):
     print(f"{us:10.1f} us {n:4d}x {100 * us / s:5.1f}%  {k}")
