@@ -35,8 +35,6 @@ struct splatb200_ctx {
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
   bool view_streams = false;   // views run forward / backward on their own streams (splatb200_ctx_set_view_streams)
-  cudaStream_t aux = nullptr;  // spare non-blocking stream (binning fork experiment; unused on the hot path)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // scene
   int64_t n = 0;
@@ -412,7 +410,7 @@ int alloc_query_buffers(splatb200_view* v) {
   }
   CU_TRY(c, cudaMalloc(&v->sensor_grads, sizeof(float) * 8));
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, c->stream));
-  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t) * 3));
+  CU_TRY(c, cudaMallocHost(&v->h_total, sizeof(int64_t) * 8));
   return SPLATB200_OK;
 }
 
@@ -449,13 +447,6 @@ extern "C" int splatb200_ctx_create(int device, void* cuda_stream, splatb200_ctx
   auto* c = new splatb200_ctx();
   c->device = device;
   c->stream = (cudaStream_t)cuda_stream;
-  if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
-    g_create_error = "cannot create the auxiliary stream";
-    delete c;
-    return SPLATB200_ECUDA;
-  }
   *out = c;
   return SPLATB200_OK;
 }
@@ -466,9 +457,6 @@ extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
   cudaStreamSynchronize(c->stream);
   while (!c->views.empty()) splatb200_view_destroy(c->views.back());
   free_scene(c);
-  if (c->aux) cudaStreamDestroy(c->aux);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
@@ -903,14 +891,10 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   const int sh = v->two_level ? super_shift() : 0;
   {
     // Per-tile list lengths straight from the tile rectangles (tile ranges, compositing CTA order, sort histograms).
-    // Independent of the depth sort; running the two side by side on separate streams was measured and gains nothing
-    // (both are chains of small kernels that already fill the SM slots; the fork/join events cost what the overlap saves).
-    const bool fork = false;
+    // (Independent of the depth sort; forking them onto a second stream was measured and gains nothing — both are
+    // chains of small kernels and the fork/join events cost what the overlap saves. Overlap comes from running the
+    // sensors of a frame on their own streams instead: splatb200_ctx_set_view_streams.)
     cudaStream_t ts = st;
-    if (fork) {
-      CU_TRY(c, cudaEventRecord(c->ev_fork, st));
-      CU_TRY(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    }
     {
       StageTimer tm(v, 2, ts);
       c->launches += launch_tile_counts(c->n, v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin,
@@ -929,19 +913,21 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
                                             v->two_level ? v->proj.ccount : v->proj.count, v->offsets, c->n, v->dsort_temp,
                                             v->dsort_temp_bytes, st);
     }
-    if (fork) {
-      CU_TRY(c, cudaEventRecord(c->ev_join, c->aux));
-      CU_TRY(c, cudaStreamWaitEvent(st, c->ev_join, 0));
-    }
   }
   CHECK_LAUNCH(c, "depth sort + scan");
-  v->h_total[1] = 0;
-  v->h_total[2] = 0;
+  for (int k = 1; k < 8; ++k) v->h_total[k] = 0;
+  // look-back time-out flags (word 16 of each sort workspace): this frame's depth sort, the previous frame's tile sort
+  // and expansion (their workspaces are only cleared when the next one is launched, after this sync)
+  CU_TRY(c, cudaMemcpyAsync(v->h_total + 3, (const uint32_t*)v->dsort_temp + 16, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (v->sort_temp && v->I > 0) CU_TRY(c, cudaMemcpyAsync(v->h_total + 4, (const uint32_t*)v->sort_temp + 16, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (v->expand_temp && v->I > 0) CU_TRY(c, cudaMemcpyAsync(v->h_total + 5, (const uint32_t*)v->expand_temp + 16, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaMemcpyAsync(v->h_total, v->d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaMemcpyAsync(v->h_total + 1, v->offsets + c->n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   if (v->two_level) CU_TRY(c, cudaMemcpyAsync(v->h_total + 2, v->d_total_c, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaStreamSynchronize(st));
   if (c->profiling) harvest_stage_events(v);  // previous step's events have all completed by now
+  if (v->h_total[3] | v->h_total[4] | v->h_total[5])
+    return c->fail(SPLATB200_ERUNTIME, "a decoupled look-back of the tile binning timed out (results of that render are invalid)");
   v->I = v->h_total[0];
   v->I_sort = v->two_level ? v->h_total[2] : v->I;
   v->stage = 1;
