@@ -203,6 +203,14 @@ int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, cons
 int splatb200_view_download_async(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib);
 int splatb200_view_backward_host_overlapped(splatb200_view* v, const float* g_blend16, const float* g_alpha);
 
+/* ---- test hooks -----------------------------------------------------------------------------------
+ * The hand-written depth sort + count scan of the binning stage on caller data (HOST arrays in and out): keys are
+ * sorted as unsigned 32-bit integers, stably; order_out[k] = original position of the k-th smallest key;
+ * offsets_out[k] = sum of counts[order_out[k']] over k' < k, k in [0, n] (mod 2^32). Exists so that the sort can be
+ * tested on adversarial inputs (equal keys, partial tiles, n = 1) independently of the renderer. */
+int splatb200_debug_depth_sort(splatb200_ctx* ctx, int64_t n, const uint32_t* keys, const uint32_t* counts,
+                               uint32_t* order_out, uint32_t* offsets_out);
+
 /* ---- reference-granularity entry points --------------------------------------------------------
  * One call per function the reference ships as code, HOST buffers in and out, for callers that switch
  * function by function (include/splat_b200.hpp wraps them in the reference's own types). All need a

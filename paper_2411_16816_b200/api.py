@@ -28,7 +28,7 @@ INT_ARRAYS = {"raster_stats", "source_index", "rect", "isect_tile", "isect_depth
 SYMBOLS = [
     "splatb200_ctx_create", "splatb200_ctx_destroy", "splatb200_last_error", "splatb200_ctx_sync",
     "splatb200_ctx_launch_count", "splatb200_ctx_library_launch_count",
-    "splatb200_ctx_set_profiling", "splatb200_ctx_set_view_streams", "splatb200_ctx_join", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_bind_device",
+    "splatb200_debug_depth_sort", "splatb200_ctx_set_profiling", "splatb200_ctx_set_view_streams", "splatb200_ctx_join", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_bind_device",
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
@@ -100,6 +100,7 @@ def lib():
         L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
+        L.splatb200_debug_depth_sort.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_stage_ms.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_grads_size.argtypes = [C.c_void_p]
         L.splatb200_grads_device_ptr.argtypes = [C.c_void_p]
@@ -221,6 +222,15 @@ class Context:
     @property
     def library_launch_count(self) -> int:
         return int(self.L.splatb200_ctx_library_launch_count(self.h))
+
+    def debug_depth_sort(self, keys: np.ndarray, counts: np.ndarray):
+        """Test hook: the binning stage's radix sort + count scan on caller data -> (order, offsets)."""
+        keys = np.ascontiguousarray(keys, np.uint32)
+        counts = np.ascontiguousarray(counts, np.uint32)
+        n = len(keys)
+        order, offsets = np.zeros(n, np.uint32), np.zeros(n + 1, np.uint32)
+        self._check(self.L.splatb200_debug_depth_sort(self.h, n, _p(keys), _p(counts), _p(order), _p(offsets)))
+        return order, offsets
 
     def set_view_streams(self, on: bool):
         """Views run forward / backward on their own streams (sensors overlap); see splat_b200.h."""

@@ -1121,6 +1121,37 @@ extern "C" int splatb200_view_backward_host_overlapped(splatb200_view* v, const 
   return SPLATB200_OK;
 }
 
+// ---- test hook: the depth sort + count scan on caller data ----------------------------------------------
+extern "C" int splatb200_debug_depth_sort(splatb200_ctx* c, int64_t n, const uint32_t* keys, const uint32_t* counts,
+                                          uint32_t* order_out, uint32_t* offsets_out) {
+  if (n < 0 || (n > 0 && (!keys || !counts))) return c->fail(SPLATB200_EINVAL, "debug_depth_sort: bad arguments");
+  CU_TRY(c, cudaSetDevice(c->device));
+  const size_t m = (size_t)std::max<int64_t>(1, n);
+  uint32_t *k0 = nullptr, *k1 = nullptr, *o0 = nullptr, *o1 = nullptr, *cnt = nullptr, *off = nullptr;
+  void* temp = nullptr;
+  const size_t temp_bytes = depth_sort_temp_bytes(n);
+  auto fin = [&](int rc) {
+    cudaFree(k0); cudaFree(k1); cudaFree(o0); cudaFree(o1); cudaFree(cnt); cudaFree(off); cudaFree(temp);
+    return rc;
+  };
+  if (cudaMalloc(&k0, 4 * m) || cudaMalloc(&k1, 4 * m) || cudaMalloc(&o0, 4 * m) || cudaMalloc(&o1, 4 * m) ||
+      cudaMalloc(&cnt, 4 * m) || cudaMalloc(&off, 4 * (m + 1)) || cudaMalloc(&temp, temp_bytes))
+    return fin(c->fail(SPLATB200_ENOMEM, "debug_depth_sort: out of device memory"));
+  if (n) {
+    cudaMemcpyAsync(k0, keys, 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(cnt, counts, 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream);
+  }
+  launch_depth_sort_scan(k0, k1, o0, o1, cnt, off, n, temp, temp_bytes, c->stream);
+  if (n && order_out) cudaMemcpyAsync(order_out, o0, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->stream);
+  if (offsets_out) cudaMemcpyAsync(offsets_out, off, 4 * (size_t)(n + 1), cudaMemcpyDeviceToHost, c->stream);
+  uint32_t err = 0;
+  if (n) cudaMemcpyAsync(&err, (const uint32_t*)temp + 16, 4, cudaMemcpyDeviceToHost, c->stream);
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return fin(c->fail(SPLATB200_ECUDA, cudaGetErrorString(e)));
+  if (err) return fin(c->fail(SPLATB200_ERUNTIME, "debug_depth_sort: look-back timed out"));
+  return fin(SPLATB200_OK);
+}
+
 // ---- reference-granularity entry points ------------------------------------------------------------
 // The functions the reference ships as code, one call each, HOST buffers in and out. Not the hot path
 // (the fused forward/backward above is); these exist so that a caller written against

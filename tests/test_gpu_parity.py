@@ -713,3 +713,27 @@ def test_view_streams_match_single_stream(ctx):
                 assert np.quantile(rel, 0.99) <= 1e-3, k
     finally:
         ctx.set_view_streams(False)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 4095, 4096, 4097, 8192, 100_003, 1_000_000])
+def test_radix_sort_and_count_scan(ctx, n):
+    """The hand-written onesweep radix sort + look-back scan against numpy on adversarial inputs: partial and exactly
+    full 4,096-item tiles, all keys equal (stability = identity), two values, sorted / reversed, random 32-bit, keys that
+    differ only in one byte."""
+    rng = np.random.default_rng(n + 7)
+    cases = {
+        "random": rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32),
+        "equal": np.full(n, 0x3f800000, np.uint32),
+        "two": np.where(rng.random(n) < 0.5, 0xffffffff, 0x41200000).astype(np.uint32),
+        "sorted": np.arange(n, dtype=np.uint32) * 3,
+        "reversed": (np.arange(n, dtype=np.uint32)[::-1] * 5).copy(),
+        "byte2": (rng.integers(0, 256, n, dtype=np.uint64).astype(np.uint32) << 16) | 0x40000000,
+        "depths": np.abs(rng.normal(20.0, 15.0, n)).astype(np.float32).view(np.uint32),
+    }
+    counts = rng.integers(0, 1000, n, dtype=np.uint64).astype(np.uint32)   # totals stay below 2^30 (the per-view limit)
+    for name, keys in cases.items():
+        order, offsets = ctx.debug_depth_sort(keys, counts)
+        ref = np.argsort(keys, kind="stable").astype(np.uint32)
+        assert np.array_equal(order, ref), (name, n)
+        ref_off = np.concatenate([[0], np.cumsum(counts[ref].astype(np.uint64))]).astype(np.uint64) & 0xffffffff
+        assert np.array_equal(offsets.astype(np.uint64), ref_off), (name, n)
