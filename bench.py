@@ -319,6 +319,7 @@ def run_b200(args):
             torch.cuda.synchronize()
 
         pool = None
+        threaded = [True]     # cleared for the serialised per-stage timing pass
         if HOST_THREADS and not args.serial:
             from concurrent.futures import ThreadPoolExecutor
             pool = ThreadPoolExecutor(max_workers=2)
@@ -331,7 +332,7 @@ def run_b200(args):
             def run_view(v, k):
                 v.forward(0.0)      # contains the one host sync of a render (the worklist size)
                 v.backward_device(g_dev[k][0].data_ptr(), g_dev[k][1].data_ptr())
-            if pool is not None:    # one host thread per view: neither view's host sync delays the other's launches
+            if pool is not None and threaded[0]:    # one host thread per view: neither view's host sync delays the other's launches
                 for f in [pool.submit(run_view, v, k) for v, k in order]:
                     f.result()
             else:
@@ -356,7 +357,7 @@ def run_b200(args):
                 v.download_async(vb, va, vn)
                 _, _, gb, ga = g_host[name]
                 v.backward_host_overlapped(gb, ga)
-            if pool is not None:
+            if pool is not None and threaded[0]:
                 for f in [pool.submit(run_view, name, v) for name, v in (("l", vl), ("c", vc))]:
                     f.result()
             else:
@@ -400,6 +401,7 @@ def run_b200(args):
         launches, lib_launches = ctx.launch_count - l0, ctx.library_launch_count - ll0
         # per-stage CUDA-event times: a separate, serialised pass (one stream), so that a stage's time is its own
         ctx.set_view_streams(False)
+        threaded[0] = False
         ctx.set_profiling(True)
         ms_serial, _, _ = timed(step_device, max(3, min(args.steps, 10)))
         ms_serial /= max(3, min(args.steps, 10))
@@ -407,6 +409,7 @@ def run_b200(args):
         ctx.set_profiling(False)
         stats_l, stats_c = vl.stats(), vc.stats()
         ctx.set_view_streams(not args.serial)
+        threaded[0] = True
 
         # per-sensor rates (each sensor's fwd+bwd timed alone, device-resident)
         def only(v, g):

@@ -33,6 +33,11 @@
 #include "kernels.h"
 #include "raster_common.cuh"
 
+// Measured alternatives that lost (round 1, same box A/B): 3 CTAs/SM with 80 registers and smaller panels or half-size
+// batches (4-15% slower); a sparse phase B over a saved ballot of the blending lanes (camera 4% slower); fully
+// warp-private staging without any CTA barrier — each warp scanning the hit bytes and gathering its own entries 32 at a
+// time (5% slower: the CTA-wide batch amortises one memory round trip over 256 list entries, the private ring pays one
+// per 32).
 namespace sb {
 
 constexpr int kRed = 26;     // 16 channel grads + conic 3 + mean2d 2 + vel 3 + rho + range
