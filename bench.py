@@ -39,6 +39,7 @@ SCENE_SEED = 3
 METRIC = "lidar Mrays/s + camera MPix/s, fwd+bwd (one frame = 128-beam lidar sweep + 1920x1080 RS camera, 1M Gaussians)"
 UNIT = "Mqueries/s"
 CAMERA_FIRST = os.environ.get("BENCH_CAMERA_FIRST", "0") == "1"   # enqueue order of the two sensors of a frame (no measurable effect)
+E2E_BANDS = int(os.environ.get("BENCH_E2E_BANDS", "0"))      # 0: the library default (4 for a camera)
 HOST_THREADS = os.environ.get("BENCH_HOST_THREADS", "1") == "1"    # one host thread per sensor view (with view streams)
 
 
@@ -352,11 +353,10 @@ def run_b200(args):
             # (lidar first measured best: its small transfers and its backward then run beside the camera's forward
             # and the camera's 149 MB download; camera first was 0.6 ms slower)
             def run_view(name, v):
-                v.forward(0.0)
                 _, _, _, vb, va, vn = out_host[name]
-                v.download_async(vb, va, vn)
+                v.forward_to_host(0.0, vb, va, vn, bands=E2E_BANDS)   # camera: bands of tile rows, each downloaded while the next renders
                 _, _, gb, ga = g_host[name]
-                v.backward_host_overlapped(gb, ga)
+                v.backward_from_host(gb, ga)            # a band's gradients go up after its outputs came down
             if pool is not None and threaded[0]:
                 for f in [pool.submit(run_view, name, v) for name, v in (("l", vl), ("c", vc))]:
                     f.result()

@@ -202,6 +202,14 @@ int splatb200_view_backward_host(splatb200_view* v, const float* g_blend16, cons
  * outputs — and runs the backward kernels once they have arrived; other views' kernels keep the GPU busy meanwhile. */
 int splatb200_view_download_async(splatb200_view* v, float* blend16, float* alpha, int32_t* n_contrib);
 int splatb200_view_backward_host_overlapped(splatb200_view* v, const float* g_blend16, const float* g_alpha);
+/* Fused forms for PINNED host buffers: forward_to_host renders a camera image in `bands` bands of tile rows (0: default,
+ * 4; at most 8; a lidar sweep is one band) and sends each band's outputs to the host on the view's copy stream while the
+ * next band is being composited; backward_from_host uploads the upstream gradients band by band — a band's upload
+ * follows that band's download, because upstream gradients are a function of the rendered outputs — and starts each
+ * band's backward kernel as soon as its gradients have arrived. Host buffers are complete after splatb200_ctx_sync. */
+int splatb200_view_forward_to_host(splatb200_view* v, float t_scene, float* blend16, float* alpha, int32_t* n_contrib,
+                                   int32_t bands);
+int splatb200_view_backward_from_host(splatb200_view* v, const float* g_blend16, const float* g_alpha);
 
 /* ---- test hooks -----------------------------------------------------------------------------------
  * The hand-written depth sort + count scan of the binning stage on caller data (HOST arrays in and out): keys are

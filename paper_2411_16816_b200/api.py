@@ -35,7 +35,7 @@ SYMBOLS = [
     "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
-    "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
+    "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
     "splatb200_view_project_backward", "splatb200_view_compose_backward", "splatb200_view_backward_projected",
 ]
 
@@ -123,6 +123,8 @@ def lib():
         L.splatb200_view_download.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_download_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_backward_host_overlapped.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_view_forward_to_host.argtypes = [C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
+        L.splatb200_view_backward_from_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_stats_get.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_view_sensor_grads.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_view_set_camera.argtypes = [C.c_void_p, C.c_void_p]
@@ -417,6 +419,14 @@ class View:
         """Upstream gradients from PINNED host arrays, uploaded on the host-to-device copy stream (after this view's
         pending download_async), then the backward kernels."""
         self.ctx._check(self.L.splatb200_view_backward_host_overlapped(self.h, _p(gb), _p(ga)))
+
+    def forward_to_host(self, t_scene: float, blend16=None, alpha=None, n_contrib=None, bands: int = 0):
+        """forward + banded, overlapped download into PINNED host arrays (complete after ctx.sync())."""
+        self.ctx._check(self.L.splatb200_view_forward_to_host(self.h, float(t_scene), _p(blend16), _p(alpha), _p(n_contrib), int(bands)))
+
+    def backward_from_host(self, gb: np.ndarray, ga: np.ndarray):
+        """banded, overlapped upload of the upstream gradients from PINNED host arrays + backward."""
+        self.ctx._check(self.L.splatb200_view_backward_from_host(self.h, _p(gb), _p(ga)))
 
     def download(self, blend16=None, alpha=None, n_contrib=None):
         self.ctx._check(self.L.splatb200_view_download(self.h, _p(blend16), _p(alpha), _p(n_contrib)))

@@ -127,6 +127,16 @@ struct splatb200_view {
   cudaEvent_t ev_ctx = nullptr;    // 'everything asked of the ctx stream so far', as seen at this view's last call
   bool busy = false;               // vs holds work the ctx stream has not been ordered after yet
   bool wait_up = false;            // the next backward waits for ev_up (overlapped upstream-gradient upload)
+  // banded host transfers (forward_to_host / backward_from_host): the image is rendered and differentiated in bands of
+  // tile rows, so that a band's download / upload runs beside the next band's kernels
+  struct Band { int tile_first, tile_count; int64_t q0, q1; };
+  std::vector<Band> bands;
+  float* plan_blend = nullptr; float* plan_alpha = nullptr; int32_t* plan_ncontrib = nullptr;  // forward plan (host, pinned)
+  bool plan_fwd = false;
+  const float* plan_gb = nullptr; const float* plan_ga = nullptr;                              // backward plan (host, pinned)
+  bool plan_bwd = false;
+  bool band_dl_valid = false;      // ev_bdl[] hold this render's per-band downloads
+  cudaEvent_t ev_bfwd[8] = {}, ev_bdl[8] = {}, ev_bup[8] = {};
   bool dl_pending = false, bwd_recorded = false;
   float* sensor_grads = nullptr;  // 6 + d_time_offset
   // actors
@@ -235,6 +245,9 @@ void free_view_buffers(splatb200_view* v) {
     if (*q) { cudaStreamSynchronize(*q); cudaStreamDestroy(*q); *q = nullptr; }
   if (v->ev_last) { cudaEventDestroy(v->ev_last); v->ev_last = nullptr; }
   if (v->ev_ctx) { cudaEventDestroy(v->ev_ctx); v->ev_ctx = nullptr; }
+  for (int b = 0; b < 8; ++b)
+    for (cudaEvent_t* e : {&v->ev_bfwd[b], &v->ev_bdl[b], &v->ev_bup[b]})
+      if (*e) { cudaEventDestroy(*e); *e = nullptr; }
   for (auto& e : v->ev)
     for (auto& x : e)
       if (x) { cudaEventDestroy(x); x = nullptr; }
@@ -964,13 +977,38 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   }
   v->out.hit_or = v->multi_pass ? 1 : 0;
   if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
-  {
+  v->band_dl_valid = false;
+  if (!v->plan_fwd) {
     StageTimer tm(v, 5, st);
     launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
                       v->out, st);
+    CHECK_LAUNCH(c, "k_raster_fwd");
+    c->launches += 1;
+  } else {
+    // forward_to_host: band by band, each band's outputs leave on the view's device-to-host stream while the next band
+    // is being composited
+    v->plan_fwd = false;
+    StageTimer tm(v, 5, st);
+    for (size_t b = 0; b < v->bands.size(); ++b) {
+      const auto& bd = v->bands[b];
+      launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr, v->out,
+                        st, bd.tile_first, bd.tile_count);
+      CHECK_LAUNCH(c, "k_raster_fwd (band)");
+      c->launches += 1;
+      CU_TRY(c, cudaEventRecord(v->ev_bfwd[b], st));
+      CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, v->ev_bfwd[b], 0));
+      const size_t q0 = (size_t)bd.q0, nq = (size_t)(bd.q1 - bd.q0);
+      if (nq) {
+        if (v->plan_blend) CU_TRY(c, cudaMemcpyAsync(v->plan_blend + 16 * q0, v->out.blend + 16 * q0, sizeof(float) * 16 * nq, cudaMemcpyDeviceToHost, v->s_d2h));
+        if (v->plan_alpha) CU_TRY(c, cudaMemcpyAsync(v->plan_alpha + q0, v->out.alpha + q0, sizeof(float) * nq, cudaMemcpyDeviceToHost, v->s_d2h));
+        if (v->plan_ncontrib) CU_TRY(c, cudaMemcpyAsync(v->plan_ncontrib + q0, v->out.n_contrib + q0, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, v->s_d2h));
+      }
+      CU_TRY(c, cudaEventRecord(v->ev_bdl[b], v->s_d2h));
+    }
+    CU_TRY(c, cudaEventRecord(v->ev_dl, v->s_d2h));
+    v->dl_pending = true;
+    v->band_dl_valid = true;
   }
-  CHECK_LAUNCH(c, "k_raster_fwd");
-  c->launches += 1;
   v->stage = 3;
   return SPLATB200_OK;
 }
@@ -1010,7 +1048,33 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
   }
   RasterGradDev rg{v->rg};
   const ParamGradDev pg = c->pg();
-  if (v->I > 0) {
+  if (v->plan_bwd) {
+    // backward_from_host: a band's upstream gradients are uploaded after that band's outputs have been downloaded (they
+    // are a function of them) and its backward kernel starts as soon as they have arrived
+    v->plan_bwd = false;
+    StageTimer tm(v, 6, st);
+    if (v->bwd_recorded) CU_TRY(c, cudaStreamWaitEvent(v->s_h2d, v->ev_bwd, 0));  // staging buffers still in use
+    for (size_t b = 0; b < v->bands.size(); ++b) {
+      const auto& bd = v->bands[b];
+      const size_t q0 = (size_t)bd.q0, nq = (size_t)(bd.q1 - bd.q0);
+      if (v->band_dl_valid) CU_TRY(c, cudaStreamWaitEvent(v->s_h2d, v->ev_bdl[b], 0));
+      if (nq) {
+        CU_TRY(c, cudaMemcpyAsync(v->g_blend_stage + 16 * q0, v->plan_gb + 16 * q0, sizeof(float) * 16 * nq, cudaMemcpyHostToDevice, v->s_h2d));
+        CU_TRY(c, cudaMemcpyAsync(v->g_alpha_stage + q0, v->plan_ga + q0, sizeof(float) * nq, cudaMemcpyHostToDevice, v->s_h2d));
+      }
+      CU_TRY(c, cudaEventRecord(v->ev_bup[b], v->s_h2d));
+    }
+    for (size_t b = 0; b < v->bands.size(); ++b) {
+      const auto& bd = v->bands[b];
+      CU_TRY(c, cudaStreamWaitEvent(st, v->ev_bup[b], 0));
+      if (v->I > 0) {
+        launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr, v->out,
+                          g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st, bd.tile_first, bd.tile_count);
+        CHECK_LAUNCH(c, "k_raster_bwd (band)");
+        c->launches += 1;
+      }
+    }
+  } else if (v->I > 0) {
     StageTimer tm(v, 6, st);
     launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
                       v->out, g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
@@ -1115,6 +1179,66 @@ extern "C" int splatb200_view_backward_host_overlapped(splatb200_view* v, const 
   CU_TRY(c, cudaEventRecord(v->ev_up, v->s_h2d));
   v->wait_up = true;
   rc = splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
+  if (rc) return rc;
+  CU_TRY(c, cudaEventRecord(v->ev_bwd, (c->view_streams && v->vs) ? v->vs : c->stream));
+  v->bwd_recorded = true;
+  return SPLATB200_OK;
+}
+
+// ---- fused host-buffer calls with banded, overlapped transfers ------------------------------------------------
+namespace {
+int make_bands(splatb200_view* v, int nb) {
+  splatb200_ctx* c = v->ctx;
+  int rc = ensure_copy_events(v);
+  if (rc) return rc;
+  if (nb <= 0) nb = v->s.is_camera ? 4 : 1;
+  nb = std::min(nb, 8);
+  v->bands.clear();
+  if (v->s.is_camera) {
+    const int rows = v->s.tiles_y, per = (rows + nb - 1) / nb;
+    for (int r0 = 0; r0 < rows; r0 += per) {
+      const int r1 = std::min(rows, r0 + per);
+      const int64_t y0 = std::min<int64_t>(v->s.height, (int64_t)kTile * r0), y1 = std::min<int64_t>(v->s.height, (int64_t)kTile * r1);
+      v->bands.push_back({r0 * v->s.tiles_x, (r1 - r0) * v->s.tiles_x, y0 * v->s.width, y1 * v->s.width});
+    }
+  } else {  // a lidar sweep is small (18 MB of outputs): one band
+    v->bands.push_back({0, (int)v->n_tiles, 0, v->P});
+  }
+  for (size_t b = 0; b < v->bands.size(); ++b)
+    for (cudaEvent_t* e : {&v->ev_bfwd[b], &v->ev_bdl[b], &v->ev_bup[b]})
+      if (!*e) CU_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return SPLATB200_OK;
+}
+}  // namespace
+
+extern "C" int splatb200_view_forward_to_host(splatb200_view* v, float t_scene, float* blend16, float* alpha, int32_t* n_contrib,
+                                              int32_t bands) {
+  int rc = make_bands(v, bands);
+  if (rc) return rc;
+  v->plan_blend = blend16; v->plan_alpha = alpha; v->plan_ncontrib = n_contrib;
+  v->plan_fwd = true;
+  rc = splatb200_view_forward(v, t_scene, 0);
+  v->plan_fwd = false;
+  return rc;
+}
+
+extern "C" int splatb200_view_backward_from_host(splatb200_view* v, const float* g_blend16, const float* g_alpha) {
+  splatb200_ctx* c = v->ctx;
+  if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
+  if (v->bands.empty()) {
+    int rc = make_bands(v, 0);
+    if (rc) return rc;
+  }
+  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  if (!v->g_blend_stage) {
+    CU_TRY(c, cudaMalloc(&v->g_blend_stage, sizeof(float) * 16 * P));
+    CU_TRY(c, cudaMalloc(&v->g_alpha_stage, sizeof(float) * P));
+  }
+  v->plan_gb = g_blend16; v->plan_ga = g_alpha;
+  v->plan_bwd = true;
+  int rc = splatb200_view_backward(v, v->g_blend_stage, v->g_alpha_stage);
+  v->plan_bwd = false;
   if (rc) return rc;
   CU_TRY(c, cudaEventRecord(v->ev_bwd, (c->view_streams && v->vs) ? v->vs : c->stream));
   v->bwd_recorded = true;

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256, kCamera ? 4 : 3)
 k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
              const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
-             const uint32_t* __restrict__ tile_order, RasterOutDev out) {
+             const uint32_t* __restrict__ tile_order, int tile_first, RasterOutDev out) {
   __shared__ float4 sA[256];
   __shared__ float4 sB[256];
   __shared__ float2 sC[256];
@@ -92,7 +92,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   __shared__ __align__(8) uint8_t sHit[8][256];  // [warp][batch entry]: some lane of the warp blended it
   __shared__ PatchBox sBox[8];
 
-  const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+  const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
@@ -260,13 +260,16 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
 
 void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
-                       const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st) {
-  const int tiles = s.tiles_x * s.tiles_y;
-  if (tiles == 0) return;
+                       const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st, int tile_first, int tile_count) {
+  // tile_count < 0: the whole grid in tile_order; otherwise tiles [tile_first, tile_first + tile_count) in id order (a band)
+  const int tiles = tile_count < 0 ? s.tiles_x * s.tiles_y : tile_count;
+  if (tiles <= 0) return;
+  const uint32_t* order = tile_count < 0 ? tile_order : nullptr;
+  if (tile_count < 0) tile_first = 0;
   if (s.is_camera)
-    k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order, out);
+    k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else
-    k_raster_fwd<false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order, out);
+    k_raster_fwd<false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
 }
 
 // ------------------------------------------------------------------------------------------------

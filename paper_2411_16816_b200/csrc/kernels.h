@@ -51,7 +51,7 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
 // worklists first), nullptr = identity
 void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
-                       const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st);
+                       const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st, int tile_first = 0, int tile_count = -1);
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 
@@ -86,7 +86,7 @@ void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, int64_t
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
                        const uint32_t* tile_order, const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha, const RasterGradDev& rg,
-                       const ParamGradDev& pg, float* d_time_offset, cudaStream_t st);
+                       const ParamGradDev& pg, float* d_time_offset, cudaStream_t st, int tile_first = 0, int tile_count = -1);
 
 // project_bwd.cu
 enum BwdMode { kFused = 0, kFromProjected = 1, kProjOnly = 2, kComposeOnly = 3 };

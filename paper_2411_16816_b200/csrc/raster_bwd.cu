@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256, 2)
 k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
              const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
-             const uint32_t* __restrict__ tile_order, RasterOutDev fwd, const float* __restrict__ g_blend16,
+             const uint32_t* __restrict__ tile_order, int tile_first, RasterOutDev fwd, const float* __restrict__ g_blend16,
              const float* __restrict__ g_alpha, RasterGradDev rg, ParamGradDev pg, float* __restrict__ d_time_offset) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float4* sA = reinterpret_cast<float4*>(smem_raw);                    // kBatch
@@ -149,7 +149,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   __shared__ int s_max_last;
   __shared__ float s_dt[8];
 
-  const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+  const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   uint8_t* sList = sListAll + kBatch * warp;
@@ -346,9 +346,12 @@ constexpr size_t kBwdSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBa
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
                        const uint32_t* tile_order, const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha,
-                       const RasterGradDev& rg, const ParamGradDev& pg, float* d_time_offset, cudaStream_t st) {
-  const int tiles = s.tiles_x * s.tiles_y;
-  if (tiles == 0) return;
+                       const RasterGradDev& rg, const ParamGradDev& pg, float* d_time_offset, cudaStream_t st, int tile_first,
+                       int tile_count) {
+  const int tiles = tile_count < 0 ? s.tiles_x * s.tiles_y : tile_count;
+  if (tiles <= 0) return;
+  if (tile_count < 0) tile_first = 0;
+  else tile_order = nullptr;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_raster_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
@@ -357,10 +360,10 @@ void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
   }
   if (s.is_camera)
     k_raster_bwd<true><<<tiles, 256, kBwdSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
-                                                     fwd, g_blend16, g_alpha, rg, pg, d_time_offset);
+                                                     tile_first, fwd, g_blend16, g_alpha, rg, pg, d_time_offset);
   else
     k_raster_bwd<false><<<tiles, 256, kBwdSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
-                                                      fwd, g_blend16, g_alpha, rg, pg, d_time_offset);
+                                                      tile_first, fwd, g_blend16, g_alpha, rg, pg, d_time_offset);
 }
 
 }  // namespace sb

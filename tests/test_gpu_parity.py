@@ -654,15 +654,21 @@ def test_overlapped_host_buffer_calls(ctx):
         ref_out[name] = (vb.copy(), va.copy(), vn.copy())
         v.backward_host_async(hgb, hga)
     g_ref = {k: x.copy() for k, x in ctx.grads().items() if k != "actors"}
-    for step in range(3):
+    for step in range(5):
         ctx.zero_grads()
         for name, v in (("l", vl), ("c", vc)):
             vb, va, vn, _, _ = host[name]
             vb[...] = -1; va[...] = -1; vn[...] = -1
-            v.forward(0.0)
-            v.download_async(vb, va, vn)
+            if step < 2:
+                v.forward(0.0)
+                v.download_async(vb, va, vn)
+            else:       # fused, banded forms (camera: 1, 3 and 8 bands over 23 tile rows)
+                v.forward_to_host(0.0, vb, va, vn, bands=(1, 3, 8)[step - 2])
         for name, v in (("l", vl), ("c", vc)):
-            v.backward_host_overlapped(host[name][3], host[name][4])
+            if step < 2:
+                v.backward_host_overlapped(host[name][3], host[name][4])
+            else:
+                v.backward_from_host(host[name][3], host[name][4])
         g = ctx.grads()          # synchronises the compute stream
         ctx.sync()
         for name in ("l", "c"):
