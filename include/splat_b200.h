@@ -211,6 +211,20 @@ int splatb200_view_forward_to_host(splatb200_view* v, float t_scene, float* blen
                                    int32_t bands);
 int splatb200_view_backward_from_host(splatb200_view* v, const float* g_blend16, const float* g_alpha);
 
+/* ---- lidar returns -> rasterization points (SPEC.md:230-238 assign_points_to_tiles) ----
+ * The producer of splatb200_view_create_lidar's `rays`. points_xyz: n x 3 world coordinates (ego-motion compensated),
+ * timestamps: n capture times; HOST arrays. Each point is re-expressed relative to the sensor pose at its own capture
+ * time (constant linear + angular velocity over the sweep), converted by Eq. 10 and mapped, with zero extent, to one
+ * tile. Outputs (HOST, caller-allocated): tile[n] (-1: rejected — non-finite or at the sensor origin),
+ * sph[n x 4] = (azimuth, elevation, t_l = timestamp - lidar.timestamp, range) per INPUT point, order[<= n] = the kept
+ * points tile-major, ray_begin / ray_end [M_phi * M_omega] = its per-tile slices, counts[3] = kept, rejected, dropped.
+ * train = 0 (evaluation): every valid point is kept, ascending input index inside a tile; tiles may hold more than
+ * 256 points (rendered in additional passes). train = 1: a tile keeps the (at most) 256 points with the smallest
+ * hash(seed, index), in (hash, index) order — the seeded shuffle-and-drop of PAPER.md:512. */
+int splatb200_assign_points(splatb200_ctx* ctx, const splatb200_lidar* lidar, int64_t n, const float* points_xyz,
+                            const float* timestamps, int32_t train, uint32_t seed, int64_t* tile, float* sph,
+                            int64_t* order, int64_t* ray_begin, int64_t* ray_end, int64_t* counts);
+
 /* ---- test hooks -----------------------------------------------------------------------------------
  * The hand-written depth sort + count scan of the binning stage on caller data (HOST arrays in and out): keys are
  * sorted as unsigned 32-bit integers, stably; order_out[k] = original position of the k-th smallest key;

@@ -504,6 +504,21 @@ int view_brute(void* vv, int early_exit, S* blend16, S* alpha, int64_t* n_contri
     *alpha_out = S(0);                                                                                                   \
     return evaluate_alpha<S>(g, qx, qy, t, st, wrap != 0, *alpha_out, dx, dy, ga, cl) ? 1 : 0;                           \
   }                                                                                                                      \
+  extern "C" int64_t orc_assign_points_##SUF(const double* lidar, const double* elev, int n_beams, const S* xyz,           \
+                                             const S* stamps, int64_t n, int train, uint32_t seed, int64_t* tile,         \
+                                             S* sph4 /* n x (phi, omega, t_l, range) */, int64_t* order,                  \
+                                             int64_t* begin, int64_t* end, int64_t* counts3) {                           \
+    const LidarModel<S> l = unpack_lidar<S>(lidar, elev, n_beams);                                                       \
+    const AssignedPoints<S> a = assign_points_to_tiles<S>(xyz, stamps, n, l, train != 0, seed);                          \
+    for (int64_t i = 0; i < n; ++i) {                                                                                    \
+      tile[i] = a.tile[i];                                                                                               \
+      sph4[4 * i] = a.phi[i]; sph4[4 * i + 1] = a.omega[i]; sph4[4 * i + 2] = a.t_l[i]; sph4[4 * i + 3] = a.range[i];    \
+    }                                                                                                                    \
+    for (size_t k = 0; k < a.order.size(); ++k) order[k] = a.order[k];                                                   \
+    for (size_t t = 0; t < a.begin.size(); ++t) { begin[t] = a.begin[t]; end[t] = a.end[t]; }                            \
+    counts3[0] = (int64_t)a.order.size(); counts3[1] = a.rejected; counts3[2] = a.dropped;                               \
+    return (int64_t)a.begin.size();                                                                                      \
+  }                                                                                                                      \
   extern "C" S orc_wrap_pi_##SUF(S a) { return wrap_pi<S>(a); }                                                          \
   extern "C" S orc_wrap_two_pi_##SUF(S a) { return wrap_two_pi<S>(a); }                                                  \
   extern "C" S orc_sigmoid_##SUF(S a) { return Sc<S>::sigmoid(a); }

@@ -162,6 +162,28 @@ class OracleView:
         return self.array("ms").astype(np.float64)
 
 
+def assign_points_to_tiles(lidar, xyz_world, stamps, train=False, seed=0, dtype=np.float32):
+    """lidar returns -> per-tile rasterization points. Returns a dict: tile (n, -1 = rejected),
+    phi / omega / t_l / range (n), order (kept points, tile-major), begin / end (per tile), rejected, dropped."""
+    L = lib()
+    suf = _suf(dtype)
+    xyz = np.ascontiguousarray(xyz_world, dtype).reshape(-1, 3)
+    ts = np.ascontiguousarray(stamps, dtype)
+    n = len(ts)
+    m_phi, m_omega = lidar.grid()
+    T = m_phi * m_omega
+    tile = np.zeros(n, np.int64)
+    sph = np.zeros((n, 4), dtype)
+    order, begin, end, cnt = np.zeros(n, np.int64), np.zeros(T, np.int64), np.zeros(T, np.int64), np.zeros(3, np.int64)
+    elev = lidar.elev(dtype)
+    f = getattr(L, f"orc_assign_points_{suf}")
+    f.restype = C.c_int64
+    f(_p(lidar.packed(dtype)), _p(elev), C.c_int(len(elev)), _p(xyz), _p(ts), C.c_int64(n), C.c_int(int(train)), C.c_uint32(seed),
+      _p(tile), _p(sph), _p(order), _p(begin), _p(end), _p(cnt))
+    return {"tile": tile, "phi": sph[:, 0].copy(), "omega": sph[:, 1].copy(), "t_l": sph[:, 2].copy(), "range": sph[:, 3].copy(),
+            "order": order[:cnt[0]].copy(), "begin": begin, "end": end, "rejected": int(cnt[1]), "dropped": int(cnt[2])}
+
+
 def detmath_eval(fn, x, y=None):
     x = np.ascontiguousarray(x, np.float32)
     y = np.zeros_like(x) if y is None else np.ascontiguousarray(y, np.float32)

@@ -1046,6 +1046,94 @@ template <class S> TileRect lidar_tile_range(const S lo[2], const S hi[2], const
   return r;
 }
 
+// ----------------------------------------------------------------------------
+// assign_points_to_tiles — no reference source exists
+// ----------------------------------------------------------------------------
+/// Result of mapping lidar returns to rasterization points. Per INPUT point: tile (-1 if rejected), spherical
+/// coordinates relative to the sensor pose at the point's own capture time (Eq. 10 after ego-motion removal), the
+/// capture-time offset t_l and the measured range. `order` lists the kept points tile-major (eval: ascending input
+/// index inside a tile; train: ascending (hash, index), at most 256 per tile), `begin/end` are its per-tile slices.
+template <class S> struct AssignedPoints {
+  std::vector<int64_t> tile;
+  std::vector<S> phi, omega, t_l, range;
+  std::vector<int64_t> order, begin, end;
+  int64_t rejected = 0, dropped = 0;
+  int tiles_x = 0, tiles_y = 0;
+};
+
+/// The "seeded shuffle" of PAPER.md:512 (SPEC open question: tie-breaking undefined): a point keeps its place in a
+/// full tile iff its hash is among the 256 smallest of the tile. Counter-based, so any implementation reproduces it.
+inline uint32_t point_hash(uint32_t seed, uint32_t index) {
+  uint32_t h = index * 0x9E3779B9u + seed;
+  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;  // murmur3 finaliser
+  return h;
+}
+
+constexpr int kPointsPerTile = kNphi * kNomega;  // 256
+
+/// One point: sensor-frame position at scan centre -> position at its own capture time under the constant-velocity
+/// assumption (the same first-order motion model the rasterizer applies to Gaussians: u = -w x p - v,
+/// projection.hpp:44-48) -> Eq. 10 (projection.hpp:122-125) -> the tile holding that zero-extent location
+/// (column floor(phi / span); row = number of row boundaries below omega: a point on an edge belongs to the floor
+/// tile). Returns false for non-finite input or a point at the sensor origin.
+template <class S>
+bool assign_one_point(const S* xyz_world, S stamp, const LidarModel<S>& lidar, const LidarGrid<S>& g, int64_t& tile, S& phi,
+                      S& omega, S& t_l, S& range) {
+  tile = -1; phi = omega = t_l = range = S(0);
+  if (!(std::isfinite(xyz_world[0]) && std::isfinite(xyz_world[1]) && std::isfinite(xyz_world[2]) && std::isfinite(stamp)))
+    return false;
+  const V3<S> p0 = lidar.pose.apply(V3<S>{xyz_world[0], xyz_world[1], xyz_world[2]});
+  t_l = stamp - lidar.timestamp;
+  const V3<S> u = relative_velocity_sensor<S>(p0, lidar.vel_lin, lidar.vel_ang, V3<S>{S(0), S(0), S(0)});
+  const V3<S> p{p0.x + u.x * t_l, p0.y + u.y * t_l, p0.z + u.z * t_l};
+  const S r = Sc<S>::sqrt((p.x * p.x + p.y * p.y) + p.z * p.z);
+  if (!(r > S(0)) || !std::isfinite(r)) return false;
+  phi = wrap_two_pi(Sc<S>::atan2(p.y, p.x));
+  omega = Sc<S>::asin(p.z / r);
+  range = r;
+  int col = (int)Sc<S>::floor(phi / g.span);
+  col = std::min(std::max(col, 0), g.m_phi - 1);
+  int row = 0;
+  for (size_t k = 0; k < g.boundaries.size(); ++k)
+    if (g.boundaries[k] < omega) row = (int)k + 1;
+  tile = (int64_t)row * g.m_phi + col;
+  return true;
+}
+
+template <class S>
+AssignedPoints<S> assign_points_to_tiles(const S* xyz_world, const S* stamps, int64_t n, const LidarModel<S>& lidar,
+                                         bool train, uint32_t seed) {
+  AssignedPoints<S> a;
+  const LidarGrid<S> g = make_lidar_grid<S>(lidar);
+  a.tiles_x = g.m_phi; a.tiles_y = g.m_omega;
+  const int64_t T = (int64_t)g.m_phi * g.m_omega;
+  a.tile.resize(n); a.phi.resize(n); a.omega.resize(n); a.t_l.resize(n); a.range.resize(n);
+  std::vector<std::vector<int64_t>> per_tile((size_t)T);
+  for (int64_t i = 0; i < n; ++i) {
+    if (assign_one_point<S>(xyz_world + 3 * i, stamps[i], lidar, g, a.tile[i], a.phi[i], a.omega[i], a.t_l[i], a.range[i]))
+      per_tile[(size_t)a.tile[i]].push_back(i);
+    else
+      ++a.rejected;
+  }
+  a.begin.assign((size_t)T, 0); a.end.assign((size_t)T, 0);
+  for (int64_t t = 0; t < T; ++t) {
+    auto& v = per_tile[(size_t)t];
+    if (train) {  // "shuffle points ... and discard any points beyond 256"
+      std::stable_sort(v.begin(), v.end(), [&](int64_t x, int64_t y) {
+        return point_hash(seed, (uint32_t)x) < point_hash(seed, (uint32_t)y);
+      });
+      if ((int64_t)v.size() > kPointsPerTile) {
+        a.dropped += (int64_t)v.size() - kPointsPerTile;
+        v.resize(kPointsPerTile);
+      }
+    }
+    a.begin[(size_t)t] = (int64_t)a.order.size();
+    a.order.insert(a.order.end(), v.begin(), v.end());
+    a.end[(size_t)t] = (int64_t)a.order.size();
+  }
+  return a;
+}
+
 /// Sort key: tile id major, IEEE bits of the (positive) fp32 depth minor — the
 /// 64-bit key the device radix sort uses. In fp64 mode the depth is compared as a double.
 struct Isect {

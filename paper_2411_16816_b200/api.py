@@ -28,7 +28,7 @@ INT_ARRAYS = {"raster_stats", "source_index", "rect", "isect_tile", "isect_depth
 SYMBOLS = [
     "splatb200_ctx_create", "splatb200_ctx_destroy", "splatb200_last_error", "splatb200_ctx_sync",
     "splatb200_ctx_launch_count", "splatb200_ctx_library_launch_count",
-    "splatb200_debug_depth_sort", "splatb200_ctx_set_profiling", "splatb200_ctx_set_view_streams", "splatb200_ctx_join", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_bind_device",
+    "splatb200_debug_depth_sort", "splatb200_assign_points", "splatb200_ctx_set_profiling", "splatb200_ctx_set_view_streams", "splatb200_ctx_join", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_bind_device",
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
@@ -100,6 +100,7 @@ def lib():
         L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
+        L.splatb200_assign_points.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_uint32] + [C.c_void_p] * 6
         L.splatb200_debug_depth_sort.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_stage_ms.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_grads_size.argtypes = [C.c_void_p]
@@ -224,6 +225,25 @@ class Context:
     @property
     def library_launch_count(self) -> int:
         return int(self.L.splatb200_ctx_library_launch_count(self.h))
+
+    def assign_points_to_tiles(self, lidar: LidarModel, xyz_world: np.ndarray, stamps: np.ndarray, train: bool = False, seed: int = 0):
+        """lidar returns -> per-tile rasterization points (same dict as the oracle's
+        assign_points_to_tiles, plus `rayset`: the RaySet view_create_lidar takes)."""
+        xyz = np.ascontiguousarray(xyz_world, np.float32).reshape(-1, 3)
+        ts = np.ascontiguousarray(stamps, np.float32)
+        n = len(ts)
+        pod, keep = _lidar_pod(lidar)
+        m_phi, m_omega = lidar.grid()
+        T = m_phi * m_omega
+        tile, sph = np.zeros(n, np.int64), np.zeros((n, 4), np.float32)
+        order, begin, end, cnt = np.zeros(n, np.int64), np.zeros(T, np.int64), np.zeros(T, np.int64), np.zeros(3, np.int64)
+        self._check(self.L.splatb200_assign_points(self.h, C.byref(pod), n, _p(xyz), _p(ts), int(train), int(seed) & 0xffffffff,
+                                                   _p(tile), _p(sph), _p(order), _p(begin), _p(end), _p(cnt)))
+        order = order[:cnt[0]].copy()
+        rays = np.ascontiguousarray(sph[order][:, :3])
+        return {"tile": tile, "phi": sph[:, 0].copy(), "omega": sph[:, 1].copy(), "t_l": sph[:, 2].copy(), "range": sph[:, 3].copy(),
+                "order": order, "begin": begin, "end": end, "rejected": int(cnt[1]), "dropped": int(cnt[2]),
+                "rayset": RaySet(rays=rays, begin=begin.copy(), end=end.copy())}
 
     def debug_depth_sort(self, keys: np.ndarray, counts: np.ndarray):
         """Test hook: the binning stage's radix sort + count scan on caller data -> (order, offsets)."""

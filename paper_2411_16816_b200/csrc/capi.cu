@@ -1245,6 +1245,105 @@ extern "C" int splatb200_view_backward_from_host(splatb200_view* v, const float*
   return SPLATB200_OK;
 }
 
+// ---- assign_points_to_tiles -----------------------------------------------------------------
+// Device: per-point geometry + tile key (k_assign_points), stable radix sort by tile (and by shuffle hash first in
+// training mode); host: the per-tile slices and the 256-point cap of the training mode (O(n) over the sorted keys).
+extern "C" int splatb200_assign_points(splatb200_ctx* c, const splatb200_lidar* l, int64_t n, const float* points_xyz,
+                                       const float* timestamps, int32_t train, uint32_t seed, int64_t* tile, float* sph,
+                                       int64_t* order, int64_t* ray_begin, int64_t* ray_end, int64_t* counts) {
+  if (!l || n < 0 || (n > 0 && (!points_xyz || !timestamps)) || !ray_begin || !ray_end || !counts)
+    return c->fail(SPLATB200_EINVAL, "assign_points: null argument");
+  if (l->n_beams < 1 || !(l->azimuth_resolution > 0.0f)) return c->fail(SPLATB200_EINVAL, "lidar needs beams and res_phi > 0");
+  if (n >= (1LL << 30)) return c->fail(SPLATB200_EINVAL, "assign_points: too many points");
+  CU_TRY(c, cudaSetDevice(c->device));
+  int m_phi, m_omega;
+  lidar_grid_of(l->azimuth_resolution, l->n_beams, &m_phi, &m_omega);
+  if (m_omega - 1 > kMaxBoundaries) return c->fail(SPLATB200_EINVAL, "too many beams");
+  const int64_t T = (int64_t)m_phi * m_omega;
+  Sensor s;
+  std::memset(&s, 0, sizeof(Sensor));
+  fill_pose(s, l->R, l->t, l->vel_lin, l->vel_ang);
+  s.tiles_x = m_phi; s.tiles_y = m_omega;
+  s.span = (float)kNphi * l->azimuth_resolution;
+  s.n_boundaries = m_omega - 1;
+  for (int k = 1; k < m_omega; ++k)
+    s.boundaries[k - 1] = 0.5f * (l->elevation_channels[kNomega * k - 1] + l->elevation_channels[kNomega * k]);
+  for (int64_t t = 0; t < T; ++t) ray_begin[t] = ray_end[t] = 0;
+  counts[0] = counts[1] = counts[2] = 0;
+  if (n == 0) return SPLATB200_OK;
+
+  const size_t m = (size_t)n;
+  float *d_xyz = nullptr, *d_ts = nullptr;
+  float4* d_sph = nullptr;
+  uint32_t *d_key = nullptr, *d_hash = nullptr, *d_valid = nullptr, *k0 = nullptr, *k1 = nullptr, *o0 = nullptr, *o1 = nullptr,
+           *oh = nullptr, *off = nullptr;
+  void* temp = nullptr;
+  const size_t temp_bytes = depth_sort_temp_bytes(n);
+  auto fin = [&](int rc) {
+    cudaFree(d_xyz); cudaFree(d_ts); cudaFree(d_sph); cudaFree(d_key); cudaFree(d_hash); cudaFree(d_valid); cudaFree(k0);
+    cudaFree(k1); cudaFree(o0); cudaFree(o1); cudaFree(oh); cudaFree(off); cudaFree(temp);
+    return rc;
+  };
+  if (cudaMalloc(&d_xyz, 12 * m) || cudaMalloc(&d_ts, 4 * m) || cudaMalloc(&d_sph, 16 * m) || cudaMalloc(&d_key, 4 * m) ||
+      cudaMalloc(&d_hash, 4 * m) || cudaMalloc(&d_valid, 4 * m) || cudaMalloc(&k0, 4 * m) || cudaMalloc(&k1, 4 * m) ||
+      cudaMalloc(&o0, 4 * m) || cudaMalloc(&o1, 4 * m) || cudaMalloc(&oh, 4 * m) || cudaMalloc(&off, 4 * (m + 1)) ||
+      cudaMalloc(&temp, temp_bytes))
+    return fin(c->fail(SPLATB200_ENOMEM, "assign_points: out of device memory"));
+  cudaStream_t st = c->stream;
+  cudaMemcpyAsync(d_xyz, points_xyz, 12 * m, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_ts, timestamps, 4 * m, cudaMemcpyHostToDevice, st);
+  launch_assign_points(s, l->timestamp, n, d_xyz, d_ts, seed, d_key, d_sph, d_hash, d_valid, st);
+  c->launches += 1;
+  const uint32_t* final_order = o0;
+  if (!train) {
+    cudaMemcpyAsync(k0, d_key, 4 * m, cudaMemcpyDeviceToDevice, st);
+    c->launches += launch_depth_sort_scan(k0, k1, o0, o1, d_valid, off, n, temp, temp_bytes, st);
+  } else {  // LSD: by hash first, then (stably) by tile
+    cudaMemcpyAsync(k0, d_hash, 4 * m, cudaMemcpyDeviceToDevice, st);
+    c->launches += launch_depth_sort_scan(k0, k1, oh, o1, d_valid, off, n, temp, temp_bytes, st);
+    launch_gather_u32(n, d_key, oh, k0, st);                       // keys in hash order
+    c->launches += 1 + launch_depth_sort_scan(k0, k1, o0, o1, d_valid, off, n, temp, temp_bytes, st);
+    launch_gather_u32(n, oh, o0, o1, st);                          // compose the two permutations
+    c->launches += 1;
+    final_order = o1;
+  }
+  std::vector<uint32_t> h_key(m), h_order(m);
+  std::vector<float4> h_sph(m);
+  cudaMemcpyAsync(h_key.data(), d_key, 4 * m, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(h_order.data(), final_order, 4 * m, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(h_sph.data(), d_sph, 16 * m, cudaMemcpyDeviceToHost, st);
+  uint32_t err = 0;
+  cudaMemcpyAsync(&err, (const uint32_t*)temp + 16, 4, cudaMemcpyDeviceToHost, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fin(c->fail(SPLATB200_ECUDA, cudaGetErrorString(e)));
+  if (err) return fin(c->fail(SPLATB200_ERUNTIME, "assign_points: look-back timed out"));
+  int64_t kept = 0, rejected = 0, dropped = 0;
+  for (size_t i = 0; i < m; ++i) {
+    if (tile) tile[i] = h_key[i] == 0xffffffffu ? -1 : (int64_t)h_key[i];
+    if (sph) { sph[4 * i] = h_sph[i].x; sph[4 * i + 1] = h_sph[i].y; sph[4 * i + 2] = h_sph[i].z; sph[4 * i + 3] = h_sph[i].w; }
+    rejected += h_key[i] == 0xffffffffu;
+  }
+  // per-tile slices of the sorted order; training mode keeps the first 256 of a tile (smallest hashes)
+  size_t k = 0;
+  while (k < m) {
+    const uint32_t t = h_key[h_order[k]];
+    if (t == 0xffffffffu) break;  // rejected points sort last
+    size_t e2 = k;
+    while (e2 < m && h_key[h_order[e2]] == t) ++e2;
+    size_t take = e2 - k;
+    if (train && take > (size_t)(kNphi * kNomega)) { dropped += (int64_t)take - kNphi * kNomega; take = (size_t)(kNphi * kNomega); }
+    ray_begin[t] = kept;
+    for (size_t q = 0; q < take; ++q) {
+      if (order) order[kept] = h_order[k + q];
+      ++kept;
+    }
+    ray_end[t] = kept;
+    k = e2;
+  }
+  counts[0] = kept; counts[1] = rejected; counts[2] = dropped;
+  return fin(SPLATB200_OK);
+}
+
 // ---- test hook: the depth sort + count scan on caller data ----------------------------------------------
 extern "C" int splatb200_debug_depth_sort(splatb200_ctx* c, int64_t n, const uint32_t* keys, const uint32_t* counts,
                                           uint32_t* order_out, uint32_t* offsets_out) {

@@ -55,6 +55,12 @@ void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 
+// assign.cu (assign_points_to_tiles): per-point tile key (0xffffffff = rejected), (phi, omega, t_l, range),
+// shuffle hash, valid flag
+void launch_assign_points(const Sensor& s, float timestamp, int64_t n, const float* xyz, const float* stamps, uint32_t seed,
+                          uint32_t* key, float4* sph, uint32_t* hash, uint32_t* valid, cudaStream_t st);
+void launch_gather_u32(int64_t n, const uint32_t* src, const uint32_t* idx, uint32_t* dst, cudaStream_t st);
+
 // binning.cu (hand-written radix sort, scans, tile histogram — no library kernels)
 size_t depth_sort_temp_bytes(int64_t n);
 // stable sort of (dkey, position) by the 32-bit key; the sorted source indices land in order0 (dkey, dkey_alt, order1

@@ -637,3 +637,97 @@ def test_backward_dynamic_actor_fd(L):
         tr.vel_offset[k] = old
         num = (lp - lm) / (2 * h)
         assert abs(num - ga_vel[k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(ga_vel).max()) + 1e-6, (k, num, ga_vel[k])
+
+
+# ---- assign_points_to_tiles ----------------------------------------------------------
+@pytest.fixture(scope="module")
+def op(oracle_lib):
+    from oracle import oracle_py
+    return oracle_py
+
+
+def _sweep_points(lid, rng, jitter=0.0, n_az=None):
+    """World points on the rays of a grid sweep seen from a STATIC sensor at the lidar pose (range random)."""
+    from paper_2411_16816_b200 import synth
+    rs = synth.grid_rays(lid, n_az)
+    phi, om = rs.rays[:, 0].astype(np.float64), rs.rays[:, 1].astype(np.float64)
+    r = rng.uniform(5.0, 60.0, len(phi))
+    d = np.stack([np.cos(om) * np.cos(phi), np.cos(om) * np.sin(phi), np.sin(om)], 1) * r[:, None]
+    d += jitter * rng.normal(size=d.shape)
+    R, t = np.asarray(lid.R, np.float64), np.asarray(lid.t, np.float64)
+    world = (d - t) @ R          # inverse of p_s = R p_w + t
+    return world, rs
+
+
+def test_assign_points_stationary_sensor_is_identity(op):
+    """SPEC.md:235 'stationary sensor -> ego-motion removal is identity': spherical coordinates of the points equal the
+    ray directions they were generated on, for any timestamp."""
+    from paper_2411_16816_b200 import synth
+    lid = synth.lidar32()
+    rng = np.random.default_rng(0)
+    world, rs = _sweep_points(lid, rng)
+    ts = rng.uniform(-0.05, 0.05, len(world))
+    a = op.assign_points_to_tiles(lid, world, ts, dtype=np.float64)
+    assert a["rejected"] == 0 and a["dropped"] == 0
+    assert np.abs(a["phi"] - rs.rays[:, 0]).max() < 1e-6 and np.abs(a["omega"] - rs.rays[:, 1]).max() < 1e-6
+    assert np.allclose(a["t_l"], ts - lid.timestamp)
+
+
+def test_assign_points_exact_fill_and_bijection(op):
+    """SPEC.md:236 'exactly N_phi*N_omega points per tile -> every tile full, zero overflow' and the point-tile bijection
+    (SPEC.md:243): the union over tiles reproduces the input multiset."""
+    from paper_2411_16816_b200 import synth
+    lid = synth.lidar32()
+    world, rs = _sweep_points(lid, np.random.default_rng(1))
+    a = op.assign_points_to_tiles(lid, world, np.zeros(len(world)), dtype=np.float64)
+    counts = a["end"] - a["begin"]
+    assert (counts == 256).all()
+    assert np.array_equal(np.sort(a["order"]), np.arange(len(world)))
+    # tile-major slices hold exactly the points whose tile id they carry, in ascending input index
+    for t in (0, 17, len(counts) - 1):
+        sl = a["order"][a["begin"][t]:a["end"][t]]
+        assert (a["tile"][sl] == t).all() and (np.diff(sl) > 0).all()
+    # the sweep's own tile layout agrees
+    tile_of_ray = np.repeat(np.arange(len(rs.begin)), rs.end - rs.begin)
+    assert np.array_equal(a["tile"], tile_of_ray)
+
+
+def test_assign_points_overflow_eval_and_train(op):
+    """SPEC.md:237 '257 points landing in one tile, eval mode -> two passes whose concatenation covers all 257'; training
+    mode keeps 256 of them (seeded, reproducible) and reports one dropped point. Non-finite points are rejected."""
+    from paper_2411_16816_b200 import synth
+    lid = synth.lidar32()
+    world, rs = _sweep_points(lid, np.random.default_rng(2))
+    extra = world[5:6] * 1.01                      # one more return on (almost) the same ray: same tile
+    bad = np.array([[np.nan, 0.0, 1.0], [0.0, np.inf, 1.0]])
+    pts = np.concatenate([world, extra, bad])
+    ts = np.zeros(len(pts))
+    a = op.assign_points_to_tiles(lid, pts, ts, dtype=np.float64)
+    t = a["tile"][len(world)]
+    assert a["rejected"] == 2 and (a["tile"][-2:] == -1).all()
+    assert a["end"][t] - a["begin"][t] == 257 and len(a["order"]) == len(world) + 1
+    b = op.assign_points_to_tiles(lid, pts, ts, train=True, seed=7, dtype=np.float64)
+    assert b["dropped"] == 1 and b["end"][t] - b["begin"][t] == 256 and len(b["order"]) == len(world)
+    b2 = op.assign_points_to_tiles(lid, pts, ts, train=True, seed=7, dtype=np.float64)
+    assert np.array_equal(b["order"], b2["order"])
+    c = op.assign_points_to_tiles(lid, pts, ts, train=True, seed=8, dtype=np.float64)
+    assert not np.array_equal(b["order"], c["order"])
+
+
+def test_assign_points_removes_ego_motion(op):
+    """A moving sensor: a static world point observed at t_l appears where first-order ego-motion puts it, i.e. where the
+    rasterizer places a static Gaussian at that capture time (mean2d + velocity * t_l, projection.hpp:44-58, 140-174)."""
+    from paper_2411_16816_b200 import synth
+    lid = synth.lidar128()                        # vel_lin = (15, 0, 0), vel_ang = (0, 0, 0.1)
+    rng = np.random.default_rng(3)
+    pts = rng.normal(0, 15, (2000, 3)) + np.array([0, 0, 1.0])
+    ts = rng.uniform(-0.05, 0.05, len(pts)) + lid.timestamp
+    a = op.assign_points_to_tiles(lid, pts, ts, dtype=np.float64)
+    R, t = np.asarray(lid.R, np.float64), np.asarray(lid.t, np.float64)
+    p0 = pts @ R.T + t
+    u = -np.cross(np.asarray(lid.vel_ang, np.float64), p0) - np.asarray(lid.vel_lin, np.float64)
+    p = p0 + u * (ts - lid.timestamp)[:, None]
+    phi = np.mod(np.arctan2(p[:, 1], p[:, 0]), 2 * np.pi)
+    ok = a["tile"] >= 0
+    assert np.abs(np.angle(np.exp(1j * (a["phi"][ok] - phi[ok])))).max() < 1e-9
+    assert np.abs(a["range"][ok] - np.linalg.norm(p[ok], axis=1)).max() < 1e-9
