@@ -640,12 +640,6 @@ def test_backward_dynamic_actor_fd(L):
 
 
 # ---- assign_points_to_tiles ----------------------------------------------------------
-@pytest.fixture(scope="module")
-def op(oracle_lib):
-    from oracle import oracle_py
-    return oracle_py
-
-
 def _sweep_points(lid, rng, jitter=0.0, n_az=None):
     """World points on the rays of a grid sweep seen from a STATIC sensor at the lidar pose (range random)."""
     from paper_2411_16816_b200 import synth
@@ -659,7 +653,7 @@ def _sweep_points(lid, rng, jitter=0.0, n_az=None):
     return world, rs
 
 
-def test_assign_points_stationary_sensor_is_identity(op):
+def test_assign_points_stationary_sensor_is_identity(oracle_lib):
     """SPEC.md:235 'stationary sensor -> ego-motion removal is identity': spherical coordinates of the points equal the
     ray directions they were generated on, for any timestamp."""
     from paper_2411_16816_b200 import synth
@@ -673,7 +667,7 @@ def test_assign_points_stationary_sensor_is_identity(op):
     assert np.allclose(a["t_l"], ts - lid.timestamp)
 
 
-def test_assign_points_exact_fill_and_bijection(op):
+def test_assign_points_exact_fill_and_bijection(oracle_lib):
     """SPEC.md:236 'exactly N_phi*N_omega points per tile -> every tile full, zero overflow' and the point-tile bijection
     (SPEC.md:243): the union over tiles reproduces the input multiset."""
     from paper_2411_16816_b200 import synth
@@ -692,7 +686,7 @@ def test_assign_points_exact_fill_and_bijection(op):
     assert np.array_equal(a["tile"], tile_of_ray)
 
 
-def test_assign_points_overflow_eval_and_train(op):
+def test_assign_points_overflow_eval_and_train(oracle_lib):
     """SPEC.md:237 '257 points landing in one tile, eval mode -> two passes whose concatenation covers all 257'; training
     mode keeps 256 of them (seeded, reproducible) and reports one dropped point. Non-finite points are rejected."""
     from paper_2411_16816_b200 import synth
@@ -714,7 +708,7 @@ def test_assign_points_overflow_eval_and_train(op):
     assert not np.array_equal(b["order"], c["order"])
 
 
-def test_assign_points_removes_ego_motion(op):
+def test_assign_points_removes_ego_motion(oracle_lib):
     """A moving sensor: a static world point observed at t_l appears where first-order ego-motion puts it, i.e. where the
     rasterizer places a static Gaussian at that capture time (mean2d + velocity * t_l, projection.hpp:44-58, 140-174)."""
     from paper_2411_16816_b200 import synth
