@@ -163,6 +163,10 @@ void splatb200_view_destroy(splatb200_view* v);
 int splatb200_view_set_camera(splatb200_view* v, const splatb200_camera* cam);
 int splatb200_view_set_lidar_pose(splatb200_view* v, const float R[9], const float t[3], const float vel_lin[3],
                                   const float vel_ang[3]);
+/* a new sweep for an existing lidar view — the per-frame output of splatb200_assign_points: same layout as the `rays`
+ * of view_create_lidar, any number of rays (buffers grow as needed); n_tiles must equal the view's */
+int splatb200_view_set_rays(splatb200_view* v, const float* rays, int64_t n_rays, const int64_t* ray_begin,
+                            const int64_t* ray_end, int64_t n_tiles);
 /* lidar tile grid: M_phi, M_omega */
 int splatb200_lidar_grid(const splatb200_lidar* lidar, int32_t* m_phi, int32_t* m_omega);
 

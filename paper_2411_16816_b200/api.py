@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -100,6 +100,7 @@ def lib():
         L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
+        L.splatb200_view_set_rays.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
         L.splatb200_assign_points.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_uint32] + [C.c_void_p] * 6
         L.splatb200_debug_depth_sort.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_view_stage_ms.argtypes = [C.c_void_p, C.c_void_p]
@@ -379,6 +380,13 @@ class View:
             self.close()
         except Exception:
             pass
+
+    def set_rays(self, rayset: RaySet):
+        """A new sweep for this lidar view (e.g. ctx.assign_points_to_tiles(...)["rayset"])."""
+        rays = np.ascontiguousarray(rayset.rays, np.float32)
+        rb, re = np.ascontiguousarray(rayset.begin, np.int64), np.ascontiguousarray(rayset.end, np.int64)
+        self.ctx._check(self.L.splatb200_view_set_rays(self.h, _p(rays), len(rays), _p(rb), _p(re), len(rb)))
+        self.P = len(rays)
 
     def set_camera(self, cam: CameraModel):
         pod = _camera_pod(cam)

@@ -113,6 +113,7 @@ struct splatb200_view {
   int64_t I_sort = 0;             // entries the radix sort handles: block-level intersections, or I
   // queries
   int64_t P = 0, n_tiles = 0;
+  int64_t P_cap = 0;   // queries the per-query buffers are sized for (lidar sweeps change size: view_set_rays)
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
   int64_t *ray_begin = nullptr, *ray_end = nullptr;
   uint32_t* tile_order = nullptr;  // CTA -> tile permutation (longest worklists first), rebuilt every forward
@@ -731,6 +732,57 @@ extern "C" int splatb200_lidar_grid(const splatb200_lidar* l, int32_t* m_phi, in
   return SPLATB200_OK;
 }
 
+namespace {
+// Packs and uploads a lidar view's rays (shared by view_create_lidar and view_set_rays). Within a tile the rays are
+// re-ordered azimuth-major (then by elevation), so that 32 consecutive positions — one warp of the compositing kernels —
+// form a compact patch (4 azimuth bins x 8 beams on a grid sweep) that per-warp culling can exploit. The original index
+// travels in .w; outputs keep the caller's ray order. Needs v->rays capacity >= n_rays (v->P_cap).
+int upload_rays(splatb200_view* v, const float* rays, int64_t n_rays, const int64_t* ray_begin, const int64_t* ray_end) {
+  splatb200_ctx* c = v->ctx;
+  const int64_t n_tiles = v->n_tiles;
+  if (n_rays > 0xffffffffLL) return c->fail(SPLATB200_EINVAL, "more than 2^32-1 rays in one view");
+  if (n_rays > 0 && !rays) return c->fail(SPLATB200_EINVAL, "null rays");
+  for (int64_t t = 0; t < n_tiles; ++t)
+    if (ray_begin[t] < 0 || ray_end[t] < ray_begin[t] || ray_end[t] > n_rays)
+      return c->fail(SPLATB200_EINVAL, "ray_begin/ray_end must delimit slices of the ray array");
+  v->multi_pass = false;
+  for (int64_t t = 0; t < n_tiles; ++t)
+    if (ray_end[t] - ray_begin[t] > 256) v->multi_pass = true;  // several passes over a tile's list (SPEC.md:233)
+  std::vector<float4> packed((size_t)std::max<int64_t>(1, n_rays));
+  {
+    std::vector<std::pair<std::pair<float, float>, int64_t>> keyed;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+      const int64_t b = ray_begin[t], e = ray_end[t];
+      if (e <= b) continue;
+      keyed.clear();
+      const float ref = rays[3 * b];
+      for (int64_t r = b; r < e; ++r) {
+        float rel = std::fmod(rays[3 * r] - ref, 6.283185307179586f);   // wrap to (-pi, pi] around the tile's first ray
+        if (rel > 3.14159265358979f) rel -= 6.283185307179586f;
+        if (rel <= -3.14159265358979f) rel += 6.283185307179586f;
+        keyed.push_back({{rel, rays[3 * r + 1]}, r});
+      }
+      std::stable_sort(keyed.begin(), keyed.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (int64_t k = 0; k < e - b; ++k) {
+        const int64_t r = keyed[(size_t)k].second;
+        const uint32_t bits = (uint32_t)r;
+        float w;
+        std::memcpy(&w, &bits, 4);
+        packed[(size_t)(b + k)] = make_float4(rays[3 * r], rays[3 * r + 1], rays[3 * r + 2], w);
+      }
+    }
+  }
+  if (!v->rays && cudaMalloc(&v->rays, sizeof(float4) * (size_t)v->P_cap) != cudaSuccess)
+    return c->fail(SPLATB200_ENOMEM, "cudaMalloc rays");
+  if (n_rays) cudaMemcpyAsync(v->rays, packed.data(), sizeof(float4) * (size_t)n_rays, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(v->ray_begin, ray_begin, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(v->ray_end, ray_end, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->fail(SPLATB200_ECUDA, "ray upload failed");
+  v->P = n_rays;
+  return SPLATB200_OK;
+}
+}  // namespace
+
 extern "C" int splatb200_view_create_lidar(splatb200_ctx* c, const splatb200_lidar* l, const splatb200_raster_settings* st,
                                            const float* rays, int64_t n_rays, const int64_t* ray_begin,
                                            const int64_t* ray_end, int64_t n_tiles, splatb200_view** out) {
@@ -767,47 +819,11 @@ extern "C" int splatb200_view_create_lidar(splatb200_ctx* c, const splatb200_lid
     return code;
   };
   if (rc) return fin(rc);
-  const size_t P = (size_t)std::max<int64_t>(1, n_rays);
-  if (n_rays > 0xffffffffLL) return fin(c->fail(SPLATB200_EINVAL, "more than 2^32-1 rays in one view"));
-  for (int64_t t = 0; t < n_tiles; ++t)
-    if (ray_begin[t] < 0 || ray_end[t] < ray_begin[t] || ray_end[t] > n_rays)
-      return fin(c->fail(SPLATB200_EINVAL, "ray_begin/ray_end must delimit slices of the ray array"));
-  for (int64_t t = 0; t < n_tiles; ++t)
-    if (ray_end[t] - ray_begin[t] > 256) v->multi_pass = true;  // several passes over a tile's list (SPEC.md:233)
-  // Within a tile the rays are re-ordered azimuth-major (then by elevation), so that 32 consecutive positions — one
-  // warp of the compositing kernels — form a compact patch (4 azimuth bins x 8 beams on a grid sweep) that per-warp
-  // culling can exploit. The original index travels in .w; outputs keep the caller's ray order.
-  std::vector<float4> packed(P);
-  {
-    std::vector<std::pair<std::pair<float, float>, int64_t>> keyed;
-    for (int64_t t = 0; t < n_tiles; ++t) {
-      const int64_t b = ray_begin[t], e = ray_end[t];
-      if (e <= b) continue;
-      keyed.clear();
-      const float ref = rays[3 * b];
-      for (int64_t r = b; r < e; ++r) {
-        float rel = std::fmod(rays[3 * r] - ref, 6.283185307179586f);   // wrap to (-pi, pi] around the tile's first ray
-        if (rel > 3.14159265358979f) rel -= 6.283185307179586f;
-        if (rel <= -3.14159265358979f) rel += 6.283185307179586f;
-        keyed.push_back({{rel, rays[3 * r + 1]}, r});
-      }
-      std::stable_sort(keyed.begin(), keyed.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
-      for (int64_t k = 0; k < e - b; ++k) {
-        const int64_t r = keyed[(size_t)k].second;
-        const uint32_t bits = (uint32_t)r;
-        float w;
-        std::memcpy(&w, &bits, 4);
-        packed[(size_t)(b + k)] = make_float4(rays[3 * r], rays[3 * r + 1], rays[3 * r + 2], w);
-      }
-    }
-  }
-  if (cudaMalloc(&v->rays, sizeof(float4) * P) != cudaSuccess || cudaMalloc(&v->ray_begin, sizeof(int64_t) * n_tiles) != cudaSuccess ||
-      cudaMalloc(&v->ray_end, sizeof(int64_t) * n_tiles) != cudaSuccess)
-    return fin(c->fail(SPLATB200_ENOMEM, "cudaMalloc rays"));
-  if (n_rays) cudaMemcpyAsync(v->rays, packed.data(), sizeof(float4) * (size_t)n_rays, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(v->ray_begin, ray_begin, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(v->ray_end, ray_end, sizeof(int64_t) * n_tiles, cudaMemcpyHostToDevice, c->stream);
-  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fin(c->fail(SPLATB200_ECUDA, "ray upload failed"));
+  if (cudaMalloc(&v->ray_begin, sizeof(int64_t) * n_tiles) != cudaSuccess || cudaMalloc(&v->ray_end, sizeof(int64_t) * n_tiles) != cudaSuccess)
+    return fin(c->fail(SPLATB200_ENOMEM, "cudaMalloc ray slices"));
+  v->P_cap = std::max<int64_t>(1, n_rays);
+  rc = upload_rays(v, rays, n_rays, ray_begin, ray_end);
+  if (rc) return fin(rc);
   *out = v;
   return SPLATB200_OK;
 }
@@ -826,6 +842,36 @@ extern "C" void splatb200_view_destroy(splatb200_view* v) {
       break;
     }
   delete v;
+}
+
+// A new sweep for an existing lidar view (the per-frame output of splatb200_assign_points): same tile grid, any number
+// of rays. Buffers grow when the sweep is larger than any before.
+extern "C" int splatb200_view_set_rays(splatb200_view* v, const float* rays, int64_t n_rays, const int64_t* ray_begin,
+                                       const int64_t* ray_end, int64_t n_tiles) {
+  splatb200_ctx* c = v->ctx;
+  if (v->s.is_camera) return c->fail(SPLATB200_EINVAL, "view is not a lidar");
+  if (n_rays < 0 || !ray_begin || !ray_end || n_tiles != v->n_tiles) return c->fail(SPLATB200_EINVAL, "set_rays: bad arguments");
+  CU_TRY(c, cudaSetDevice(c->device));
+  join_view(v);
+  CU_TRY(c, cudaStreamSynchronize(c->stream));  // the previous sweep's kernels and copies are done with the buffers
+  for (cudaStream_t q : {v->s_h2d, v->s_d2h})
+    if (q) CU_TRY(c, cudaStreamSynchronize(q));
+  v->dl_pending = false; v->band_dl_valid = false; v->bwd_recorded = false;
+  if (n_rays > v->P_cap) {
+    dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend); dfree(v->out.n_contrib);
+    dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage); dfree(v->rays);
+    const size_t cap = (size_t)(n_rays + n_rays / 8 + 256);
+    CU_TRY(c, cudaMalloc(&v->out.blend, sizeof(float) * 16 * cap));
+    CU_TRY(c, cudaMalloc(&v->out.alpha, sizeof(float) * cap));
+    CU_TRY(c, cudaMalloc(&v->out.t_final, sizeof(float) * cap));
+    CU_TRY(c, cudaMalloc(&v->out.range_blend, sizeof(float) * cap));
+    CU_TRY(c, cudaMalloc(&v->out.n_contrib, sizeof(int32_t) * cap));
+    CU_TRY(c, cudaMalloc(&v->out.last_idx, sizeof(int32_t) * cap));
+    v->P_cap = (int64_t)cap;
+  }
+  v->stage = 0;
+  v->bands.clear();
+  return upload_rays(v, rays, n_rays, ray_begin, ray_end);
 }
 
 // compose_at_time's host part: actor validation (scene.hpp:297-298) and pose interpolation
@@ -1118,7 +1164,7 @@ extern "C" int splatb200_view_backward_host(splatb200_view* v, const float* g_bl
   splatb200_ctx* c = v->ctx;
   join_view(v);  // order the ctx stream after the view's own stream
   if (!g_blend16 || !g_alpha) return c->fail(SPLATB200_EINVAL, "null upstream gradient");
-  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  const size_t P = (size_t)std::max<int64_t>(1, std::max(v->P, v->P_cap));  // lidar sweeps change size (view_set_rays)
   if (!v->g_blend_stage) {
     CU_TRY(c, cudaMalloc(&v->g_blend_stage, sizeof(float) * 16 * P));
     CU_TRY(c, cudaMalloc(&v->g_alpha_stage, sizeof(float) * P));
@@ -1165,7 +1211,7 @@ extern "C" int splatb200_view_backward_host_overlapped(splatb200_view* v, const 
   if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "backward without saved forward state");
   int rc = ensure_copy_events(v);
   if (rc) return rc;
-  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  const size_t P = (size_t)std::max<int64_t>(1, std::max(v->P, v->P_cap));  // lidar sweeps change size (view_set_rays)
   if (!v->g_blend_stage) {
     CU_TRY(c, cudaMalloc(&v->g_blend_stage, sizeof(float) * 16 * P));
     CU_TRY(c, cudaMalloc(&v->g_alpha_stage, sizeof(float) * P));
@@ -1230,7 +1276,7 @@ extern "C" int splatb200_view_backward_from_host(splatb200_view* v, const float*
     int rc = make_bands(v, 0);
     if (rc) return rc;
   }
-  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  const size_t P = (size_t)std::max<int64_t>(1, std::max(v->P, v->P_cap));  // lidar sweeps change size (view_set_rays)
   if (!v->g_blend_stage) {
     CU_TRY(c, cudaMalloc(&v->g_blend_stage, sizeof(float) * 16 * P));
     CU_TRY(c, cudaMalloc(&v->g_alpha_stage, sizeof(float) * P));
