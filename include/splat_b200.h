@@ -215,6 +215,16 @@ int splatb200_view_forward_to_host(splatb200_view* v, float t_scene, float* blen
                                    int32_t bands);
 int splatb200_view_backward_from_host(splatb200_view* v, const float* g_blend16, const float* g_alpha);
 
+/* ---- line-of-sight channel of a lidar view (SPEC.md:427 loss_total) -----
+ * The one loss term that needs the compositing loop: los[q] = sum of alpha_i over the blended Gaussians whose
+ * rolling-shutter range r_i lies in front of los_cut[q] = r_p - eps ("penalizing opacity before the ground truth lidar
+ * range"; r_p is the `range` column splatb200_assign_points returns). set_los uploads the per-ray cuts (HOST, P floats;
+ * NULL switches the channel off); the next forward fills the accumulator, read back with
+ * splatb200_view_array(v, "los", dst). set_los_grad uploads dL/dlos (HOST, P floats) for the next backward, which adds
+ * it to dL/dalpha_i of exactly those Gaussians. Both arrays are in the caller's ray order. */
+int splatb200_view_set_los(splatb200_view* v, const float* los_cut);
+int splatb200_view_set_los_grad(splatb200_view* v, const float* g_los);
+
 /* ---- lidar returns -> rasterization points (SPEC.md:230-238 assign_points_to_tiles) ----
  * The producer of splatb200_view_create_lidar's `rays`. points_xyz: n x 3 world coordinates (ego-motion compensated),
  * timestamps: n capture times; HOST arrays. Each point is re-expressed relative to the sensor pose at its own capture

@@ -40,6 +40,7 @@ template <class S> struct ViewH {
   Worklist wl;
   std::vector<Ray<S>> rays;
   std::vector<int64_t> ray_begin, ray_end;
+  std::vector<S> los_cut, g_los;   // optional line-of-sight channel: per-ray cut r_p - eps, upstream gradient
   RasterOut<S> out;
   RasterGrads<S> rg;
   ProjectedGrads<S> pg;
@@ -147,7 +148,8 @@ template <class S> void view_forward(ViewH<S>* v, double t_scene, int workers, i
   v->ms[2] = t3 - t2;
   if (stop_after == 2) return;
   if (v->camera) v->out = rasterize_camera<S>(v->wl, v->proj, v->scene, v->cam, v->st, workers);
-  else v->out = rasterize_lidar<S>(v->wl, v->proj, v->scene, v->rays, v->ray_begin, v->ray_end, v->st, workers);
+  else v->out = rasterize_lidar<S>(v->wl, v->proj, v->scene, v->rays, v->ray_begin, v->ray_end, v->st, workers,
+                                   v->los_cut.empty() ? nullptr : &v->los_cut);
   v->ms[3] = now_ms() - t3;
 }
 
@@ -197,8 +199,9 @@ template <class S> int view_backward(void* vv, const S* g_blend16, const S* g_al
   const int64_t P = v->out.P;
   std::vector<S> gb(g_blend16, g_blend16 + 16 * P), ga(g_alpha, g_alpha + P);
   double t0 = now_ms();
+  const bool los = !v->camera && !v->los_cut.empty() && v->g_los.size() == v->los_cut.size();
   v->rg = rasterize_backward<S>(v->wl, v->proj, v->scene, v->camera, &v->cam, &v->rays, &v->ray_begin, &v->ray_end,
-                                v->st, v->out, gb, ga, workers);
+                                v->st, v->out, gb, ga, workers, los ? &v->los_cut : nullptr, los ? &v->g_los : nullptr);
   double t1 = now_ms();
   v->ms[4] = t1 - t0;
   raster_grads_to_projected_grads<S>(v->rg, v->proj, v->scene, v->camera, v->pg);
@@ -295,6 +298,10 @@ template <class S> int64_t view_array(void* vv, const char* name_c, void* dst) {
   if (name == "isect_tile") return ints(v->wl.items.size(), [&](size_t k) { return v->wl.items[k].tile; });
   if (name == "isect_depth_bits") return ints(v->wl.items.size(), [&](size_t k) { return v->wl.items[k].depth_bits; });
   if (name == "isect_src") return ints(v->wl.items.size(), [&](size_t k) { return v->wl.items[k].src; });
+  if (name == "los") {
+    if (dst) std::copy(v->out.los.begin(), v->out.los.end(), (S*)dst);
+    return (int64_t)v->out.los.size();
+  }
   if (name == "tile_begin") return ints(v->wl.tile_begin.size(), [&](size_t k) { return v->wl.tile_begin[k]; });
   if (name == "tile_end") return ints(v->wl.tile_end.size(), [&](size_t k) { return v->wl.tile_end[k]; });
   if (name == "grid") return ints(2, [&](size_t k) { return k == 0 ? v->wl.tiles_x : v->wl.tiles_y; });
@@ -432,6 +439,16 @@ int view_brute(void* vv, int early_exit, S* blend16, S* alpha, int64_t* n_contri
                          workers, stop_after);                                                                           \
   }                                                                                                                      \
   extern "C" void orc_view_free_##SUF(void* v) { delete (ViewH<S>*)v; }                                                  \
+  /* line-of-sight channel: sets the per-ray cut (r_p - eps) and re-runs the compositing so that array "los" exists */   \
+  extern "C" void orc_view_set_los_##SUF(void* vv, const S* cut, int workers) {                                          \
+    auto* v = (ViewH<S>*)vv;                                                                                             \
+    v->los_cut.assign(cut, cut + v->rays.size());                                                                        \
+    v->out = rasterize_lidar<S>(v->wl, v->proj, v->scene, v->rays, v->ray_begin, v->ray_end, v->st, workers, &v->los_cut); \
+  }                                                                                                                      \
+  extern "C" void orc_view_set_los_grad_##SUF(void* vv, const S* g) {                                                    \
+    auto* v = (ViewH<S>*)vv;                                                                                             \
+    v->g_los.assign(g, g + v->rays.size());                                                                              \
+  }                                                  \
   extern "C" int orc_view_backward_##SUF(void* v, const S* g_blend16, const S* g_alpha, int workers) {                   \
     return view_backward<S>(v, g_blend16, g_alpha, workers);                                                             \
   }                                                                                                                      \

@@ -151,6 +151,17 @@ class OracleView:
         assert gb.size == 16 * self.P and ga.size == self.P
         getattr(self.L, f"orc_view_backward_{self.suf}")(self.h, _p(gb), _p(ga), C.c_int(workers))
 
+    def set_los(self, los_cut, workers=1):
+        """Line-of-sight channel: per-ray cut r_p - eps; array("los") holds the accumulator afterwards."""
+        cut = np.ascontiguousarray(los_cut, self.dtype)
+        assert cut.size == self.P and not self.camera
+        getattr(self.L, f"orc_view_set_los_{self.suf}")(self.h, _p(cut), C.c_int(workers))
+
+    def set_los_grad(self, g_los):
+        g = np.ascontiguousarray(g_los, self.dtype)
+        assert g.size == self.P
+        getattr(self.L, f"orc_view_set_los_grad_{self.suf}")(self.h, _p(g))
+
     def brute_force(self, early_exit=True):
         blend = np.empty((self.P, 16), self.dtype)
         alpha = np.empty(self.P, self.dtype)

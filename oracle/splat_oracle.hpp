@@ -1256,6 +1256,7 @@ template <class S> struct RasterOut {
   std::vector<S> range_blend;       // P  lidar: un-normalised sum w * r_rs
   std::vector<int32_t> n_contrib;   // P  number of blended Gaussians
   std::vector<int32_t> last_idx;    // P  list position (1-based, tile-local) of last blended Gaussian
+  std::vector<S> los;               // P  lidar, optional: sum of alpha_i over blended Gaussians with r_i < r_p - eps
   int64_t nonfinite = 0;
 };
 
@@ -1264,7 +1265,12 @@ template <class S> struct Ray { S phi, omega, t; };
 /// Compositing of one query over one depth-ordered list. SPEC.md:295-313 (Eq. 4).
 template <class S, class GetSplat>
 inline void composite_one(int64_t count, GetSplat get, S qx, S qy, S t, bool lidar, const RasterSettings<S>& st, S* acc16,
-                          S& T, S& range_acc, S& median, int32_t& n_contrib, int32_t& last_idx, int channels) {
+                          S& T, S& range_acc, S& median, int32_t& n_contrib, int32_t& last_idx, int channels,
+                          S los_cut = S(0), S* los = nullptr) {
+  // los (lidar, optional): the line-of-sight accumulator of SPEC.md:427 / PAPER.md:532-536 — the sum of alpha_i over the
+  // blended Gaussians whose rolling-shutter range lies in front of los_cut = r_p - eps ("penalizing opacity before the
+  // ground truth lidar range"). It needs the per-Gaussian alphas, hence lives inside the compositing loop.
+  if (los) *los = S(0);
   T = S(1);
   range_acc = S(0);
   median = S(0);
@@ -1285,6 +1291,7 @@ inline void composite_one(int64_t count, GetSplat get, S qx, S qy, S t, bool lid
     if (lidar) {
       const S r_rs = Sc<S>::fma(g.vz, t, g.depth);
       range_acc = Sc<S>::fma(r_rs, w, range_acc);
+      if (los && r_rs < los_cut) *los += alpha;
       if (!med_found && T < S(0.5)) {
         median = r_rs;
         med_found = true;
@@ -1347,9 +1354,10 @@ template <class S>
 RasterOut<S> rasterize_lidar(const Worklist& wl, const std::vector<Projected<S>>& projected,
                              const ComposedScene<S>& scene, const std::vector<Ray<S>>& rays,
                              const std::vector<int64_t>& ray_begin, const std::vector<int64_t>& ray_end,
-                             const RasterSettings<S>& st, int workers = 1) {
+                             const RasterSettings<S>& st, int workers = 1, const std::vector<S>* los_cut = nullptr) {
   RasterOut<S> out;
   out.P = (int64_t)rays.size();
+  if (los_cut) out.los.assign(out.P, S(0));
   out.camera = false;
   out.channels = scene.graph->gaussians.d_f;
   out.blend.assign(out.P * 16, S(0));
@@ -1369,7 +1377,8 @@ RasterOut<S> rasterize_lidar(const Worklist& wl, const std::vector<Projected<S>>
         S Tt, ra, med;
         composite_one<S>(std::max<int64_t>(0, e - b), [&](int64_t j) -> const Splat<S>& { return splats[j]; },
                          rays[p].phi, rays[p].omega, rays[p].t, true, st, &out.blend[16 * p], Tt, ra, med,
-                         out.n_contrib[p], out.last_idx[p], out.channels);
+                         out.n_contrib[p], out.last_idx[p], out.channels, los_cut ? (*los_cut)[p] : S(0),
+                         los_cut ? &out.los[p] : nullptr);
         out.t_final[p] = Tt;
         out.alpha[p] = S(1) - Tt;
         out.range_blend[p] = ra;
@@ -1460,7 +1469,7 @@ template <class S> struct RasterGrads {
 template <class S, class GetSplat, class GetSrc>
 inline void composite_one_backward(GetSplat get, GetSrc src_of, S qx, S qy, S t, bool lidar, const RasterSettings<S>& st,
                                    const S* g_out16, S g_alpha, S t_final, S range_blend, int32_t last_idx, int channels,
-                                   RasterGrads<S>& out) {
+                                   RasterGrads<S>& out, S los_cut = S(0), S g_los = S(0), bool los = false) {
   if (last_idx <= 0) return;
   S g_acc = g_alpha;  // dL/dA, A = 1 - T_final
   S g_D = S(0);       // dL/d(range_blend)
@@ -1498,6 +1507,7 @@ inline void composite_one_backward(GetSplat get, GetSrc src_of, S qx, S qy, S t,
       out.g_vel[3 * i + 2] += g_D * w * t;
       g_a += g_D * (r_rs * T - suffix_r / one_m);
       suffix_r += w * r_rs;
+      if (los && r_rs < los_cut) g_a += g_los;  // d los / d alpha_i = 1 for the Gaussians in front of the cut
     }
     g_a += g_acc * t_final / one_m;
     if (clamped) continue;  // alpha == alpha_clamp is constant in every parameter
@@ -1561,8 +1571,10 @@ RasterGrads<S> rasterize_backward(const Worklist& wl, const std::vector<Projecte
                                   const std::vector<Ray<S>>* rays, const std::vector<int64_t>* ray_begin,
                                   const std::vector<int64_t>* ray_end, const RasterSettings<S>& st,
                                   const RasterOut<S>& fwd, const std::vector<S>& g_blend16,
-                                  const std::vector<S>& g_alpha, int workers = 1) {
+                                  const std::vector<S>& g_alpha, int workers = 1, const std::vector<S>* los_cut = nullptr,
+                                  const std::vector<S>* g_los = nullptr) {
   const int64_t N = scene.size();
+  const bool los = los_cut && g_los;
   const int T = wl.tiles_x * wl.tiles_y;
   workers = std::max(1, workers);
   std::vector<RasterGrads<S>> parts(workers);
@@ -1594,7 +1606,8 @@ RasterGrads<S> rasterize_backward(const Worklist& wl, const std::vector<Projecte
         for (int64_t p = (*ray_begin)[tile]; p < (*ray_end)[tile]; ++p)
           composite_one_backward<S>(get, src, (*rays)[p].phi, (*rays)[p].omega, (*rays)[p].t, true, st,
                                     &g_blend16[16 * p], g_alpha[p], fwd.t_final[p], fwd.range_blend[p],
-                                    fwd.last_idx[p], fwd.channels, out);
+                                    fwd.last_idx[p], fwd.channels, out, los ? (*los_cut)[p] : S(0), los ? (*g_los)[p] : S(0),
+                                    los);
       }
     }
   });

@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -100,6 +100,8 @@ def lib():
         L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
+        L.splatb200_view_set_los.argtypes = [C.c_void_p, C.c_void_p]
+        L.splatb200_view_set_los_grad.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_view_set_rays.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
         L.splatb200_assign_points.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_uint32] + [C.c_void_p] * 6
         L.splatb200_debug_depth_sort.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -380,6 +382,14 @@ class View:
             self.close()
         except Exception:
             pass
+
+    def set_los(self, los_cut):
+        """Line-of-sight channel: per-ray cut r_p - eps (None: off); the next forward fills array("los")."""
+        cut = None if los_cut is None else np.ascontiguousarray(los_cut, np.float32)
+        self.ctx._check(self.L.splatb200_view_set_los(self.h, _p(cut)))
+
+    def set_los_grad(self, g_los):
+        self.ctx._check(self.L.splatb200_view_set_los_grad(self.h, _p(np.ascontiguousarray(g_los, np.float32))))
 
     def set_rays(self, rayset: RaySet):
         """A new sweep for this lidar view (e.g. ctx.assign_points_to_tiles(...)["rayset"])."""

@@ -114,6 +114,7 @@ struct splatb200_view {
   // queries
   int64_t P = 0, n_tiles = 0;
   int64_t P_cap = 0;   // queries the per-query buffers are sized for (lidar sweeps change size: view_set_rays)
+  float *d_los_cut = nullptr, *d_los = nullptr, *d_g_los = nullptr;  // line-of-sight channel (lidar, optional)
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
   int64_t *ray_begin = nullptr, *ray_end = nullptr;
   uint32_t* tile_order = nullptr;  // CTA -> tile permutation (longest worklists first), rebuilt every forward
@@ -236,7 +237,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -844,6 +845,40 @@ extern "C" void splatb200_view_destroy(splatb200_view* v) {
   delete v;
 }
 
+// ---- line-of-sight channel --------------------------------------------------------------------
+extern "C" int splatb200_view_set_los(splatb200_view* v, const float* los_cut) {
+  splatb200_ctx* c = v->ctx;
+  if (v->s.is_camera) return c->fail(SPLATB200_EINVAL, "line of sight is a lidar channel");
+  join_view(v);
+  if (!los_cut) {
+    v->out.los_cut = nullptr; v->out.los = nullptr; v->out.g_los = nullptr;
+    return SPLATB200_OK;
+  }
+  const size_t cap = (size_t)std::max<int64_t>(1, std::max(v->P, v->P_cap));
+  if (!v->d_los_cut) {
+    CU_TRY(c, cudaMalloc(&v->d_los_cut, sizeof(float) * cap));
+    CU_TRY(c, cudaMalloc(&v->d_los, sizeof(float) * cap));
+    CU_TRY(c, cudaMalloc(&v->d_g_los, sizeof(float) * cap));
+    CU_TRY(c, cudaMemsetAsync(v->d_g_los, 0, sizeof(float) * cap, c->stream));
+  }
+  if (v->P) CU_TRY(c, cudaMemcpyAsync(v->d_los_cut, los_cut, sizeof(float) * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemsetAsync(v->d_los, 0, sizeof(float) * cap, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));  // the host array is borrowed for the call only
+  v->out.los_cut = v->d_los_cut; v->out.los = v->d_los; v->out.g_los = v->d_g_los;
+  v->stage = std::min(v->stage, 2);  // the accumulator belongs to a forward with these cuts
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_set_los_grad(splatb200_view* v, const float* g_los) {
+  splatb200_ctx* c = v->ctx;
+  if (!v->out.los_cut) return c->fail(SPLATB200_ERUNTIME, "set_los_grad before set_los");
+  if (!g_los) return c->fail(SPLATB200_EINVAL, "null gradient");
+  join_view(v);
+  if (v->P) CU_TRY(c, cudaMemcpyAsync(v->d_g_los, g_los, sizeof(float) * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
 // A new sweep for an existing lidar view (the per-frame output of splatb200_assign_points): same tile grid, any number
 // of rays. Buffers grow when the sweep is larger than any before.
 extern "C" int splatb200_view_set_rays(splatb200_view* v, const float* rays, int64_t n_rays, const int64_t* ray_begin,
@@ -860,6 +895,7 @@ extern "C" int splatb200_view_set_rays(splatb200_view* v, const float* rays, int
   if (n_rays > v->P_cap) {
     dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend); dfree(v->out.n_contrib);
     dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage); dfree(v->rays);
+    dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los);
     const size_t cap = (size_t)(n_rays + n_rays / 8 + 256);
     CU_TRY(c, cudaMalloc(&v->out.blend, sizeof(float) * 16 * cap));
     CU_TRY(c, cudaMalloc(&v->out.alpha, sizeof(float) * cap));
@@ -871,6 +907,7 @@ extern "C" int splatb200_view_set_rays(splatb200_view* v, const float* rays, int
   }
   v->stage = 0;
   v->bands.clear();
+  v->out.los_cut = nullptr; v->out.los = nullptr; v->out.g_los = nullptr;  // cuts belong to a sweep: set them again
   return upload_rays(v, rays, n_rays, ray_begin, ray_end);
 }
 
@@ -1752,6 +1789,7 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   else if (name == "alpha") src = v->out.alpha;
   else if (name == "t_final") src = v->out.t_final;
   else if (name == "range_blend") src = v->out.range_blend;
+  else if (name == "los") src = v->out.los;
   if (!src) return c->fail(SPLATB200_EINVAL, "unknown array name " + name);
   if (dst && cnt) {
     CU_TRY(c, cudaMemcpyAsync(dst, src, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream));

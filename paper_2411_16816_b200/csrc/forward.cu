@@ -77,7 +77,7 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
 // query of the tile has saturated (T < transmittance_min): one __syncthreads_and per batch; a warp whose
 // 32 queries have all saturated stops evaluating on its own.
 // ------------------------------------------------------------------------------------------------
-template <bool kCamera>
+template <bool kCamera, bool kLos = false>
 __global__ void __launch_bounds__(256, kCamera ? 4 : 3)
 k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
@@ -127,6 +127,9 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     warp_patch_box<!kCamera>(inside, qx, qy, t, lane, &sBox[warp]);
 
     float T = 1.0f, range_acc = 0.0f, median = 0.0f;
+    constexpr bool los_on = !kCamera && kLos;  // a separate instantiation: the plain lidar kernel pays nothing for it
+    float los = 0.0f, los_cut = 0.0f;
+    if (los_on && inside) los_cut = out.los_cut[pix];
     bool med_found = false;
     int n_contrib = 0, last_idx = 0;
     float acc[kChannels];
@@ -198,6 +201,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           const float2 c = sC[j];
           const float r_rs = __fmaf_rn(c.y, t, c.x);
           range_acc = __fmaf_rn(r_rs, w, range_acc);
+          if (los_on && r_rs < los_cut) los = __fadd_rn(los, ev.alpha);  // opacity in front of the measured range
           if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
         }
         if (T < s.transmittance_min) done = true;
@@ -243,6 +247,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         acc[14] = median;
         acc[15] = A;
         out.range_blend[pix] = range_acc;
+        if (los_on) out.los[pix] = los;
       }
       float4* o4 = reinterpret_cast<float4*>(out.blend + 16 * pix);
 #pragma unroll
@@ -268,6 +273,8 @@ void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
   if (tile_count < 0) tile_first = 0;
   if (s.is_camera)
     k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+  else if (out.los_cut)
+    k_raster_fwd<false, true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else
     k_raster_fwd<false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
 }

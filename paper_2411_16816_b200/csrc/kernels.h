@@ -20,6 +20,11 @@ struct RasterOutDev {
   int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
   uint8_t* tile_wrap;  // T  lidar: 1 if some batch of the tile could not certify |azimuth difference| < pi (seam tiles);
                        //    the backward skips the wrap elsewhere. Written by the forward.
+  // optional line-of-sight channel of a lidar view: los[q] = sum of alpha_i over the
+  // blended Gaussians whose rolling-shutter range lies in front of los_cut[q] = r_p - eps; null = off
+  const float* los_cut;  // P
+  float* los;            // P
+  const float* g_los;    // P  upstream gradient (backward)
   unsigned long long* stats;  // debug (SPLATB200_STATS=1), else null: [0] staged entries, [1] per-warp survivors of the cull
 };
 

@@ -129,7 +129,7 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
   __syncwarp();
 }
 
-template <bool kCamera>
+template <bool kCamera, bool kLos = false>
 __global__ void __launch_bounds__(256, 2)
 k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
@@ -187,6 +187,9 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       }
     }
     int last = 0;
+    constexpr bool los_on = !kCamera && kLos;
+    float los_cut = 0.0f, g_los = 0.0f;
+    if (los_on && inside) { los_cut = fwd.los_cut[pix]; g_los = fwd.g_los[pix]; }
     float T = 1.0f, K = 0.0f, g_D = 0.0f;
     float g_out[kChannels];
 #pragma unroll
@@ -280,11 +283,14 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
               d3 = fmaf(g_out[4 * c + 3], f4.w, d3);
             }
             float dotgf = (d0 + d1) + (d2 + d3);
+            float g_extra = 0.0f;
             if (!kCamera) {
               const float2 c2 = sC[jj];
-              dotgf = fmaf(g_D, fmaf(c2.y, t, c2.x), dotgf);  // r_rs = r + v_r t
+              const float r_rs = fmaf(c2.y, t, c2.x);  // r_rs = r + v_r t
+              dotgf = fmaf(g_D, r_rs, dotgf);
+              if (los_on && r_rs < los_cut) g_extra = g_los;  // d los / d alpha_i = 1 in front of the cut
             }
-            const float g_a = dotgf * T + (K - S) * inv;
+            const float g_a = dotgf * T + (K - S) * inv + g_extra;
             S = fmaf(w, dotgf, S);
             if (!ev.clamped) g_sigma = -ev.alpha * g_a;  // alpha = rho exp(-sigma), sigma = qf / 2; clamped: constant
           }
@@ -356,11 +362,15 @@ void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
   if (!attr_set) {
     cudaFuncSetAttribute(k_raster_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
     cudaFuncSetAttribute(k_raster_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+    cudaFuncSetAttribute(k_raster_bwd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
     attr_set = true;
   }
   if (s.is_camera)
     k_raster_bwd<true><<<tiles, 256, kBwdSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
                                                      tile_first, fwd, g_blend16, g_alpha, rg, pg, d_time_offset);
+  else if (fwd.los_cut && fwd.g_los)
+    k_raster_bwd<false, true><<<tiles, 256, kBwdSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
+                                                            tile_first, fwd, g_blend16, g_alpha, rg, pg, d_time_offset);
   else
     k_raster_bwd<false><<<tiles, 256, kBwdSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
                                                       tile_first, fwd, g_blend16, g_alpha, rg, pg, d_time_offset);

@@ -823,3 +823,49 @@ def test_view_set_rays_per_frame_sweeps(ctx, op):
             x, y2 = g2[k].astype(np.float64).reshape(sc.n, -1), y.astype(np.float64).reshape(sc.n, -1)
             rel = np.abs(x - y2).max(1) / np.maximum(np.abs(y2).max(1), 1e-3 * max(np.abs(y2).max(), 1e-30))
             assert np.quantile(rel, 0.99) <= 1e-3, (n_pts, k)
+
+
+# ---- line-of-sight channel ------------------------------------------------
+def test_line_of_sight_channel(ctx, op):
+    """los[q] = sum of alpha_i in front of the per-ray cut: bit-identical to the fp32 oracle (same additions in the same
+    order); its upstream gradient reaches the parameters like the fp64 oracle's; switching the channel off restores the
+    plain render; the cuts come from assign_points' measured ranges."""
+    sc = synth.make_scene(20000, seed=14, r_max=40.0, scale_mean=0.15)
+    ctx.upload_scene(sc)
+    lid = synth.lidar128()
+    rng = np.random.default_rng(9)
+    pts = (rng.normal(0, 20, (50_000, 3)) + np.array([0, 0, 1.0])).astype(np.float32)
+    ts = (rng.uniform(-0.05, 0.05, len(pts)) + lid.timestamp).astype(np.float32)
+    a = ctx.assign_points_to_tiles(lid, pts, ts)
+    rs = a["rayset"]
+    cut = (a["range"][a["order"]] - 0.8).astype(np.float32)       # r_p - eps, in ray order
+    view = ctx.lidar_view(lid, rs, ST)
+    view.set_los(cut)
+    view.forward(0.0)
+    o32, o64 = op.OracleScene(sc, np.float32), op.OracleScene(sc, np.float64)
+    ov32 = o32.render_lidar(lid, rs, ST, workers=8)
+    ov32.set_los(cut, workers=8)
+    los, olos = view.array("los"), ov32.array("los")
+    assert np.count_nonzero(olos) > 1000
+    assert np.array_equal(bits(los), bits(olos))
+    assert_render_close(view, ov32, True)
+    # backward: only the line-of-sight gradient
+    g_los = rng.normal(size=view.P).astype(np.float32)
+    zb, za = np.zeros((view.P, 16), np.float32), np.zeros(view.P, np.float32)
+    ctx.zero_grads()
+    view.set_los_grad(g_los)
+    view.backward(zb, za)
+    for o in (o32, o64):
+        o.zero_grads()
+        ov = o.render_lidar(lid, rs, ST, workers=8)
+        ov.set_los(cut, workers=8)
+        ov.set_los_grad(g_los)
+        ov.backward(zb, za, workers=8)
+    grads_close(ctx.grads(), o64.grads(), o32.grads(), what="los ")
+    assert np.abs(ctx.grads()["d_opacity_logit"]).max() > 0
+    # off again: no accumulator, no gradient from it
+    view.set_los(None)
+    view.forward(0.0)
+    ctx.zero_grads()
+    view.backward(zb, za)
+    assert all(np.count_nonzero(x) == 0 for k, x in ctx.grads().items() if k != "actors")

@@ -725,3 +725,67 @@ def test_assign_points_removes_ego_motion(oracle_lib):
     ok = a["tile"] >= 0
     assert np.abs(np.angle(np.exp(1j * (a["phi"][ok] - phi[ok])))).max() < 1e-9
     assert np.abs(a["range"][ok] - np.linalg.norm(p[ok], axis=1)).max() < 1e-9
+
+
+# ---- line-of-sight accumulator --------------------------------------
+def _los_scene():
+    """Three wide Gaussians on the +x axis of lidar32 at ranges 5, 9.5 and 12 m whose peak alphas are 0.2, 0.3, 0.4."""
+    lid = synth.lidar32()
+    R, t = np.asarray(lid.R, np.float64), np.asarray(lid.t, np.float64)
+    ranges, alphas = [5.0, 9.5, 12.0], [0.2, 0.3, 0.4]
+    mean = np.array([(np.array([r, 0.0, 0.0]) - t) @ R for r in ranges])
+    n = 3
+    # opacity logit such that rho = opacity * det_ratio = alpha at the centre; large isotropic scale => det_ratio ~ 1
+    sc = Scene(mean, np.log(np.full((n, 3), 0.5)), np.tile([1.0, 0, 0, 0], (n, 1)), np.log(np.array(alphas) / (1 - np.array(alphas))),
+               np.zeros((n, 3)), np.ones((n, 13)) * 0.1, np.zeros(n, np.int32))
+    return lid, sc, ranges, alphas
+
+
+def test_los_spec_example(oracle_lib):
+    """'Gaussians at ranges {5, 9.5, 12} with alpha {0.2, 0.3, 0.4}, r_p = 10, eps = 0.8 -> L_los
+    contribution 0.2 (only r = 5 < 9.2)'."""
+    lid, sc, ranges, alphas = _los_scene()
+    lid.vel_lin = np.zeros(3); lid.vel_ang = np.zeros(3)
+    rays = synth.grid_rays(lid)
+    ov = op.OracleScene(sc, np.float64).render_lidar(lid, rays, ST, workers=4)
+    # the ray closest to the +x axis
+    k = int(np.argmin(np.abs(rays.rays[:, 1]) + np.minimum(rays.rays[:, 0], 2 * np.pi - rays.rays[:, 0])))
+    cut = np.full(len(rays.rays), 10.0 - 0.8)
+    ov.set_los(cut, workers=4)
+    los = ov.array("los")
+    assert ov.array("n_contrib")[k] == 3
+    assert abs(los[k] - 0.2) < 2e-3                     # alpha at the ray = 0.2 * exp(-qf/2) with a tiny offset from the centre
+    ov.set_los(np.full(len(rays.rays), 10.0), workers=4)   # eps = 0: r = 5 and 9.5 count
+    assert abs(ov.array("los")[k] - 0.5) < 5e-3
+    ov.set_los(np.full(len(rays.rays), 1.0), workers=4)    # nothing in front of 1 m
+    assert ov.array("los").max() == 0.0
+
+
+def test_los_gradient_matches_finite_differences(oracle_lib):
+    """d(sum_q g_q los_q)/d(every parameter group) analytic == central differences (fp64), SPEC.md:322's bar, on the scene
+    and sensor of the lidar backward check."""
+    rng = np.random.default_rng(24)
+    sc = _f64_scene(synth.make_scene(10, seed=32, r_min=3.0, r_max=6.0, scale_mean=0.3))
+    sc.mean[:, 2] = rng.uniform(-0.5, 1.0, 10)
+    lid = _flat_lidar(n_beams=16, res=2 * np.pi / 128)
+    lid.vel_lin, lid.vel_ang = np.array([5.0, 1.0, 0.2]), np.array([0.0, 0.05, 0.3])
+    rays = synth.grid_rays(lid)
+    P = len(rays.rays)
+    cut = rng.uniform(3.5, 6.5, P)
+    g_los = rng.normal(size=P)
+
+    def loss(scene):
+        ov = op.OracleScene(scene, np.float64).render_lidar(lid, rays, ST)
+        ov.set_los(cut)
+        return float((ov.array("los") * g_los).sum())
+
+    o = op.OracleScene(sc, np.float64)
+    v = o.render_lidar(lid, rays, ST)
+    v.set_los(cut)
+    assert np.count_nonzero(v.array("los")) > 50
+    v.set_los_grad(g_los)
+    v.backward(np.zeros((P, 16)), np.zeros(P))
+    grads = o.grads()
+    assert np.abs(grads["d_opacity_logit"]).max() > 0 and np.abs(grads["d_mean"]).max() > 0
+    assert np.abs(grads["d_feature"]).max() == 0        # the accumulator does not see the features
+    _fd_check(loss, sc, grads, rng)
