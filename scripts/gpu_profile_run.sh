@@ -16,8 +16,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"^(k_|void k_|sb::k_|void sb::k_)" -s 30 -c 30 \
     -o "$OUT/prof_${TAG}" python bench.py --steps 1 --warmup 1 --no-cpu --serial > "$OUT/ncu_${TAG}.log" 2>&1
 # 4. sanitizers on the small parity configs
-timeout 900 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -x -k "config1 or lidar_forward_backward or camera_forward_backward or edge_cases or more_than_256 or one_level" \
+timeout 900 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -x -k "config1 or lidar_forward_backward or camera_forward_backward or edge_cases or more_than_256 or one_level or radix_sort or assign_points or line_of_sight or set_rays or overlapped or view_streams" \
     > "$OUT/sanitizer_memcheck_${TAG}.log" 2>&1
-timeout 900 compute-sanitizer --tool racecheck python -m pytest tests -m gpu -q -x -k "config1 or camera_forward_backward or more_than_256" \
+timeout 900 compute-sanitizer --tool racecheck python -m pytest tests -m gpu -q -x -k "config1 or camera_forward_backward or more_than_256 or line_of_sight or assign_points_matches" \
     > "$OUT/sanitizer_racecheck_${TAG}.log" 2>&1
 ls -la "$OUT"
