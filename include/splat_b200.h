@@ -225,6 +225,18 @@ int splatb200_view_backward_from_host(splatb200_view* v, const float* g_blend16,
 int splatb200_view_set_los(splatb200_view* v, const float* los_cut);
 int splatb200_view_set_los_grad(splatb200_view* v, const float* g_los);
 
+/* ---- lidar head (SPEC.md:366-389 decode_lidar; section 3.3) ----------------------
+ * A 2-layer perceptron (hidden 32, rectified-linear inside, logistic outputs) from the D_f blended features of a ray + its
+ * direction in the sensor frame to (intensity, ray-drop probability). weights: HOST, splatb200_lidar_head_params(d_f)
+ * floats, row-major W1 [32 x (d_f + 3)], b1 [32], W2 [2 x 32], b2 [2]. forward: after splatb200_view_forward of a lidar
+ * view; y: HOST, P x 2 in the caller's ray order. backward: g_y HOST P x 2; g_weights HOST (overwritten with dL/dweights);
+ * g_blend16: DEVICE, P x 16 — dL/dfeature is ADDED to slots [0, d_f) of each ray, so that the buffer (holding any other
+ * upstream gradient of the render) can go straight into splatb200_view_backward. */
+int32_t splatb200_lidar_head_params(int32_t d_f);
+int splatb200_lidar_head_forward(splatb200_view* v, const float* weights, float* y);
+int splatb200_lidar_head_backward(splatb200_view* v, const float* weights, const float* g_y, float* g_weights,
+                                  float* g_blend16);
+
 /* ---- lidar returns -> rasterization points (SPEC.md:230-238 assign_points_to_tiles) ----
  * The producer of splatb200_view_create_lidar's `rays`. points_xyz: n x 3 world coordinates (ego-motion compensated),
  * timestamps: n capture times; HOST arrays. Each point is re-expressed relative to the sensor pose at its own capture

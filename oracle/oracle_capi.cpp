@@ -536,6 +536,23 @@ int view_brute(void* vv, int early_exit, S* blend16, S* alpha, int64_t* n_contri
     counts3[0] = (int64_t)a.order.size(); counts3[1] = a.rejected; counts3[2] = a.dropped;                               \
     return (int64_t)a.begin.size();                                                                                      \
   }                                                                                                                      \
+  /* decode_lidar: n rays; feat n x d_f, sph n x 2 (azimuth, elevation); y n x 2 (intensity, drop) */      \
+  extern "C" void orc_lidar_head_forward_##SUF(const S* w, int d_f, int64_t n, const S* feat, const S* sph, S* y) {      \
+    for (int64_t i = 0; i < n; ++i) {                                                                                    \
+      S d[3], h[kHeadHidden];                                                                                            \
+      ray_direction_sensor<S>(sph[2 * i], sph[2 * i + 1], d);                                                            \
+      lidar_head_forward_one<S>(w, d_f, feat + (int64_t)d_f * i, d, y + 2 * i, h);                                       \
+    }                                                                                                                    \
+  }                                                                                                                      \
+  extern "C" void orc_lidar_head_backward_##SUF(const S* w, int d_f, int64_t n, const S* feat, const S* sph,            \
+                                                const S* g_y, S* gw, S* g_feat) {                                        \
+    for (int k = 0; k < lidar_head_params(d_f); ++k) gw[k] = S(0);                                                       \
+    for (int64_t i = 0; i < n; ++i) {                                                                                    \
+      S d[3];                                                                                                            \
+      ray_direction_sensor<S>(sph[2 * i], sph[2 * i + 1], d);                                                            \
+      lidar_head_backward_one<S>(w, d_f, feat + (int64_t)d_f * i, d, g_y + 2 * i, gw, g_feat + (int64_t)d_f * i);        \
+    }                                                                                                                    \
+  }                                                                                                                      \
   extern "C" S orc_wrap_pi_##SUF(S a) { return wrap_pi<S>(a); }                                                          \
   extern "C" S orc_wrap_two_pi_##SUF(S a) { return wrap_two_pi<S>(a); }                                                  \
   extern "C" S orc_sigmoid_##SUF(S a) { return Sc<S>::sigmoid(a); }

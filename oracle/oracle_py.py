@@ -195,6 +195,36 @@ def assign_points_to_tiles(lidar, xyz_world, stamps, train=False, seed=0, dtype=
             "order": order[:cnt[0]].copy(), "begin": begin, "end": end, "rejected": int(cnt[1]), "dropped": int(cnt[2])}
 
 
+HEAD_HIDDEN = 32
+
+
+def lidar_head_params(d_f):
+    return HEAD_HIDDEN * (d_f + 3) + HEAD_HIDDEN + 2 * HEAD_HIDDEN + 2
+
+
+def lidar_head_forward(w, feat, sph, dtype=np.float32):
+    """decode_lidar: feat n x d_f blended features, sph n x 2 (azimuth, elevation) -> n x 2
+    (intensity, ray-drop probability)."""
+    L, suf = lib(), _suf(dtype)
+    feat = np.ascontiguousarray(feat, dtype); sph = np.ascontiguousarray(sph, dtype); w = np.ascontiguousarray(w, dtype)
+    n, d_f = feat.shape
+    assert w.size == lidar_head_params(d_f)
+    y = np.zeros((n, 2), dtype)
+    getattr(L, f"orc_lidar_head_forward_{suf}")(_p(w), C.c_int(d_f), C.c_int64(n), _p(feat), _p(sph), _p(y))
+    return y
+
+
+def lidar_head_backward(w, feat, sph, g_y, dtype=np.float32):
+    """-> (dL/dw [params], dL/dfeat [n x d_f])"""
+    L, suf = lib(), _suf(dtype)
+    feat = np.ascontiguousarray(feat, dtype); sph = np.ascontiguousarray(sph, dtype); w = np.ascontiguousarray(w, dtype)
+    g_y = np.ascontiguousarray(g_y, dtype)
+    n, d_f = feat.shape
+    gw, gf = np.zeros(w.size, dtype), np.zeros((n, d_f), dtype)
+    getattr(L, f"orc_lidar_head_backward_{suf}")(_p(w), C.c_int(d_f), C.c_int64(n), _p(feat), _p(sph), _p(g_y), _p(gw), _p(gf))
+    return gw, gf
+
+
 def detmath_eval(fn, x, y=None):
     x = np.ascontiguousarray(x, np.float32)
     y = np.zeros_like(x) if y is None else np.ascontiguousarray(y, np.float32)

@@ -59,6 +59,8 @@ template <> struct Sc<float> {
   static float floor(float a) { return std::floor(a); }
   static float ceil(float a) { return std::ceil(a); }
   static float abs(float a) { return std::fabs(a); }
+  static float cos(float a) { return std::cos(a); }   // decoder only (tolerance parity, no bit-exactness contract)
+  static float sin(float a) { return std::sin(a); }
 };
 template <> struct Sc<double> {
   static double exp(double x) { return std::exp(x); }
@@ -76,6 +78,8 @@ template <> struct Sc<double> {
   static double floor(double a) { return std::floor(a); }
   static double ceil(double a) { return std::ceil(a); }
   static double abs(double a) { return std::fabs(a); }
+  static double cos(double a) { return std::cos(a); }
+  static double sin(double a) { return std::sin(a); }
 };
 
 template <class S> constexpr S pi() { return static_cast<S>(3.14159265358979323846L); }  // common.hpp:30
@@ -1044,6 +1048,61 @@ template <class S> TileRect lidar_tile_range(const S lo[2], const S hi[2], const
   lidar_azimuth_tile_range(lo[0], hi[0], g, r.x0, r.x1);
   lidar_elevation_tile_range(lo[1], hi[1], g, r.y0, r.y1);
   return r;
+}
+
+// ----------------------------------------------------------------------------
+// decode_lidar (§3.3, Appendix B) — no reference source exists
+// ----------------------------------------------------------------------------
+/// LidarHead: 2 layers, hidden 32, input = D_f blended features + 3 (ray direction in the sensor frame), outputs
+/// intensity and ray-drop probability through logistic activations, rectified-linear inside.
+/// Parameter block (row-major): W1 [32 x (d_f + 3)], b1 [32], W2 [2 x 32], b2 [2].
+constexpr int kHeadHidden = 32;
+inline int lidar_head_params(int d_f) { return kHeadHidden * (d_f + 3) + kHeadHidden + 2 * kHeadHidden + 2; }
+
+template <class S> void ray_direction_sensor(S phi, S omega, S d[3]) {
+  const S co = Sc<S>::cos(omega);
+  d[0] = co * Sc<S>::cos(phi); d[1] = co * Sc<S>::sin(phi); d[2] = Sc<S>::sin(omega);
+}
+
+/// One ray. x = (features, direction); h = relu(W1 x + b1); y = sigmoid(W2 h + b2). Returns h for the backward.
+template <class S> void lidar_head_forward_one(const S* w, int d_f, const S* feat, const S dir[3], S y[2], S h[kHeadHidden]) {
+  const int in = d_f + 3;
+  const S* W1 = w; const S* b1 = W1 + kHeadHidden * in; const S* W2 = b1 + kHeadHidden; const S* b2 = W2 + 2 * kHeadHidden;
+  for (int j = 0; j < kHeadHidden; ++j) {
+    S a = b1[j];
+    for (int k = 0; k < d_f; ++k) a = Sc<S>::fma(W1[j * in + k], feat[k], a);
+    for (int k = 0; k < 3; ++k) a = Sc<S>::fma(W1[j * in + d_f + k], dir[k], a);
+    h[j] = a > S(0) ? a : S(0);
+  }
+  for (int o = 0; o < 2; ++o) {
+    S a = b2[o];
+    for (int j = 0; j < kHeadHidden; ++j) a = Sc<S>::fma(W2[o * kHeadHidden + j], h[j], a);
+    y[o] = Sc<S>::sigmoid(a);
+  }
+}
+
+/// Backward of one ray: accumulates the parameter gradients into gw (same layout as w) and returns dL/dfeat.
+template <class S>
+void lidar_head_backward_one(const S* w, int d_f, const S* feat, const S dir[3], const S g_y[2], S* gw, S* g_feat) {
+  const int in = d_f + 3;
+  const S* W1 = w; const S* b1 = W1 + kHeadHidden * in; const S* W2 = b1 + kHeadHidden;
+  S* gW1 = gw; S* gb1 = gW1 + kHeadHidden * in; S* gW2 = gb1 + kHeadHidden; S* gb2 = gW2 + 2 * kHeadHidden;
+  S y[2], h[kHeadHidden];
+  lidar_head_forward_one<S>(w, d_f, feat, dir, y, h);
+  S gp2[2];
+  for (int o = 0; o < 2; ++o) {
+    gp2[o] = g_y[o] * y[o] * (S(1) - y[o]);
+    gb2[o] += gp2[o];
+    for (int j = 0; j < kHeadHidden; ++j) gW2[o * kHeadHidden + j] += gp2[o] * h[j];
+  }
+  for (int k = 0; k < d_f; ++k) g_feat[k] = S(0);
+  for (int j = 0; j < kHeadHidden; ++j) {
+    if (!(h[j] > S(0))) continue;
+    const S gp1 = W2[j] * gp2[0] + W2[kHeadHidden + j] * gp2[1];
+    gb1[j] += gp1;
+    for (int k = 0; k < d_f; ++k) { gW1[j * in + k] += gp1 * feat[k]; g_feat[k] += W1[j * in + k] * gp1; }
+    for (int k = 0; k < 3; ++k) gW1[j * in + d_f + k] += gp1 * dir[k];
+  }
 }
 
 // ----------------------------------------------------------------------------

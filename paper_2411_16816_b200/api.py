@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_lidar_head_params", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -100,6 +100,9 @@ def lib():
         L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
+        L.splatb200_lidar_head_params.argtypes = [C.c_int32]
+        L.splatb200_lidar_head_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_lidar_head_backward.argtypes = [C.c_void_p] * 5
         L.splatb200_view_set_los.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_view_set_los_grad.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_view_set_rays.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
@@ -382,6 +385,22 @@ class View:
             self.close()
         except Exception:
             pass
+
+    def lidar_head_forward(self, weights) -> np.ndarray:
+        """decode_lidar over this view's blended features: P x 2 (intensity, ray-drop probability)."""
+        w = np.ascontiguousarray(weights, np.float32)
+        assert w.size == self.L.splatb200_lidar_head_params(self.ctx.d_f)
+        y = np.zeros((self.P, 2), np.float32)
+        self.ctx._check(self.L.splatb200_lidar_head_forward(self.h, _p(w), _p(y)))
+        return y
+
+    def lidar_head_backward(self, weights, g_y, g_blend16_device_ptr: int) -> np.ndarray:
+        """-> dL/dweights; dL/dfeature is added to the DEVICE buffer (P x 16) at g_blend16_device_ptr."""
+        w = np.ascontiguousarray(weights, np.float32)
+        gy = np.ascontiguousarray(g_y, np.float32)
+        gw = np.zeros(w.size, np.float32)
+        self.ctx._check(self.L.splatb200_lidar_head_backward(self.h, _p(w), _p(gy), _p(gw), C.c_void_p(g_blend16_device_ptr)))
+        return gw
 
     def set_los(self, los_cut):
         """Line-of-sight channel: per-ray cut r_p - eps (None: off); the next forward fills array("los")."""

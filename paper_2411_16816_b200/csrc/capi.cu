@@ -25,6 +25,10 @@ template <class T> void dfree(T*& p) {
   if (p) cudaFree(p);
   p = nullptr;
 }
+struct DevScratch {  // a device allocation that lives for one call
+  float* p = nullptr;
+  ~DevScratch() { if (p) cudaFree(p); }
+};
 }  // namespace
 
 struct splatb200_ctx {
@@ -845,6 +849,51 @@ extern "C" void splatb200_view_destroy(splatb200_view* v) {
   delete v;
 }
 
+// ---- lidar head ---------------------------------------------------------------------------
+extern "C" int32_t splatb200_lidar_head_params(int32_t d_f) { return lidar_head_params(d_f); }
+
+extern "C" int splatb200_lidar_head_forward(splatb200_view* v, const float* weights, float* y) {
+  splatb200_ctx* c = v->ctx;
+  if (v->s.is_camera) return c->fail(SPLATB200_EINVAL, "the lidar head decodes a lidar view");
+  if (!weights || !y) return c->fail(SPLATB200_EINVAL, "null argument");
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "lidar head before forward");
+  join_view(v);
+  const int np = lidar_head_params(c->d_f);
+  DevScratch dw, dy;
+  CU_TRY(c, cudaMalloc(&dw.p, sizeof(float) * np));
+  CU_TRY(c, cudaMalloc(&dy.p, sizeof(float) * 2 * (size_t)std::max<int64_t>(1, v->P)));
+  CU_TRY(c, cudaMemcpyAsync(dw.p, weights, sizeof(float) * np, cudaMemcpyHostToDevice, c->stream));
+  launch_lidar_head_fwd(dw.p, c->d_f, v->P, v->rays, v->out.blend, dy.p, c->stream);
+  CHECK_LAUNCH(c, "k_lidar_head_fwd");
+  c->launches += v->P > 0;
+  if (v->P) CU_TRY(c, cudaMemcpyAsync(y, dy.p, sizeof(float) * 2 * (size_t)v->P, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_lidar_head_backward(splatb200_view* v, const float* weights, const float* g_y, float* g_weights,
+                                             float* g_blend16) {
+  splatb200_ctx* c = v->ctx;
+  if (v->s.is_camera) return c->fail(SPLATB200_EINVAL, "the lidar head decodes a lidar view");
+  if (!weights || !g_y || !g_weights || !g_blend16) return c->fail(SPLATB200_EINVAL, "null argument");
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "lidar head before forward");
+  join_view(v);
+  const int np = lidar_head_params(c->d_f);
+  DevScratch dw, dgw, dgy;
+  CU_TRY(c, cudaMalloc(&dw.p, sizeof(float) * np));
+  CU_TRY(c, cudaMalloc(&dgw.p, sizeof(float) * np));
+  CU_TRY(c, cudaMalloc(&dgy.p, sizeof(float) * 2 * (size_t)std::max<int64_t>(1, v->P)));
+  CU_TRY(c, cudaMemcpyAsync(dw.p, weights, sizeof(float) * np, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemsetAsync(dgw.p, 0, sizeof(float) * np, c->stream));
+  if (v->P) CU_TRY(c, cudaMemcpyAsync(dgy.p, g_y, sizeof(float) * 2 * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
+  launch_lidar_head_bwd(dw.p, c->d_f, v->P, v->rays, v->out.blend, dgy.p, g_blend16, dgw.p, c->stream);
+  CHECK_LAUNCH(c, "k_lidar_head_bwd");
+  c->launches += v->P > 0;
+  CU_TRY(c, cudaMemcpyAsync(g_weights, dgw.p, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
 // ---- line-of-sight channel --------------------------------------------------------------------
 extern "C" int splatb200_view_set_los(splatb200_view* v, const float* los_cut) {
   splatb200_ctx* c = v->ctx;
@@ -1474,11 +1523,6 @@ int visible_list(splatb200_view* v, std::vector<int64_t>& vis) {
     if (cnt[i]) vis.push_back((int64_t)i);
   return SPLATB200_OK;
 }
-
-struct DevScratch {
-  float* p = nullptr;
-  ~DevScratch() { if (p) cudaFree(p); }
-};
 
 int run_dump(splatb200_view* v, std::vector<float>& h) {
   splatb200_ctx* c = v->ctx;

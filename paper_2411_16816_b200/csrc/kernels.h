@@ -60,6 +60,13 @@ void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 
+// decode.cu (decode_lidar): the lidar head over a view's blended features
+int lidar_head_params(int d_f);
+void launch_lidar_head_fwd(const float* w, int d_f, int64_t n_rays, const float4* rays, const float* blend16, float* y_out,
+                           cudaStream_t st);
+void launch_lidar_head_bwd(const float* w, int d_f, int64_t n_rays, const float4* rays, const float* blend16, const float* g_y,
+                           float* g_blend16, float* g_w, cudaStream_t st);
+
 // assign.cu (assign_points_to_tiles): per-point tile key (0xffffffff = rejected), (phi, omega, t_l, range),
 // shuffle hash, valid flag
 void launch_assign_points(const Sensor& s, float timestamp, int64_t n, const float* xyz, const float* stamps, uint32_t seed,

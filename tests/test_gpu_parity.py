@@ -869,3 +869,46 @@ def test_line_of_sight_channel(ctx, op):
     ctx.zero_grads()
     view.backward(zb, za)
     assert all(np.count_nonzero(x) == 0 for k, x in ctx.grads().items() if k != "actors")
+
+
+# ---- lidar head ---------------------------------------------------------
+def test_lidar_head_matches_oracle(ctx, op):
+    """decode_lidar over a rendered sweep: intensity / ray-drop within 1e-4 of the fp32 oracle; weight gradients and the
+    feature gradient (added into the compositing upstream buffer) within 1e-3 of the fp64 oracle; the combined backward
+    — head + rasterizer — equals the rasterizer backward fed with the oracle's feature gradient."""
+    import torch
+    sc = synth.make_scene(15000, seed=16, r_max=40.0, scale_mean=0.15)
+    ctx.upload_scene(sc)
+    lid = synth.lidar128()
+    rs = synth.grid_rays(lid)
+    view = ctx.lidar_view(lid, rs, ST)
+    view.forward(0.0)
+    P, d_f = view.P, sc.d_f
+    rng = np.random.default_rng(11)
+    w = rng.normal(0, 0.3, op.lidar_head_params(d_f)).astype(np.float32)
+    feat = view.array("blend").reshape(P, 16)[:, :d_f]
+    sph = rs.rays[:, :2]
+    y = view.lidar_head_forward(w)
+    oy = op.lidar_head_forward(w, feat, sph, np.float32)
+    assert y.min() > 0 and y.max() < 1
+    assert np.abs(y - oy).max() <= RENDER_RTOL
+    g_y = rng.normal(size=(P, 2)).astype(np.float32)
+    g_up = torch.zeros((P, 16), dtype=torch.float32, device="cuda")
+    g_up[:, 3] = 0.25                                   # some other upstream gradient of the render: must be kept
+    gw = view.lidar_head_backward(w, g_y, g_up.data_ptr())
+    ogw, ogf = op.lidar_head_backward(w, feat, sph, g_y, np.float64)
+    assert np.abs(gw - ogw).max() <= GRAD_RTOL * np.abs(ogw).max()
+    gf = g_up.cpu().numpy()
+    exp = np.zeros((P, 16)); exp[:, :d_f] = ogf; exp[:, 3] += 0.25
+    assert np.abs(gf - exp).max() <= GRAD_RTOL * np.abs(exp).max()
+    # head + rasterizer backward in one go
+    ga = torch.zeros(P, dtype=torch.float32, device="cuda")
+    ctx.zero_grads()
+    view.backward_device(g_up.data_ptr(), ga.data_ptr())
+    g1 = {k: x.copy() for k, x in ctx.grads().items() if k != "actors"}
+    ctx.zero_grads()
+    view.backward(exp.astype(np.float32), np.zeros(P, np.float32))
+    g2 = ctx.grads()
+    for k, a in g1.items():
+        b = g2[k]
+        assert np.abs(a - b).max() <= 2e-3 * max(np.abs(b).max(), 1e-30), k

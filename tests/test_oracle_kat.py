@@ -789,3 +789,34 @@ def test_los_gradient_matches_finite_differences(oracle_lib):
     assert np.abs(grads["d_opacity_logit"]).max() > 0 and np.abs(grads["d_mean"]).max() > 0
     assert np.abs(grads["d_feature"]).max() == 0        # the accumulator does not see the features
     _fd_check(loss, sc, grads, rng)
+
+
+# ---- decode_lidar ----------------------------------------------------------------------
+def test_lidar_head_examples_and_fd(oracle_lib):
+    """zero weights and bias -> intensity = drop = sigmoid(0) = 0.5; outputs in (0, 1); every weight tensor
+    and the feature gradient match central differences (fp64, rel err <= 1e-3)."""
+    rng = np.random.default_rng(5)
+    d_f, n = 13, 40
+    feat, sph = rng.normal(size=(n, d_f)), np.stack([rng.uniform(0, 2 * np.pi, n), rng.uniform(-0.4, 0.2, n)], 1)
+    nw = op.lidar_head_params(d_f)
+    assert nw == 32 * 16 + 32 + 64 + 2
+    y0 = op.lidar_head_forward(np.zeros(nw), feat, sph, np.float64)
+    assert np.all(y0 == 0.5)
+    w = rng.normal(0, 0.4, nw)
+    y = op.lidar_head_forward(w, feat, sph, np.float64)
+    assert y.min() > 0 and y.max() < 1
+    g_y = rng.normal(size=(n, 2))
+    gw, gf = op.lidar_head_backward(w, feat, sph, g_y, np.float64)
+    loss = lambda w_, f_: float((op.lidar_head_forward(w_, f_, sph, np.float64) * g_y).sum())
+    h = 1e-6
+    for k in rng.choice(nw, 40, replace=False):
+        wp, wm = w.copy(), w.copy()
+        wp[k] += h; wm[k] -= h
+        num = (loss(wp, feat) - loss(wm, feat)) / (2 * h)
+        assert abs(num - gw[k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(gw).max()) + 1e-8, (k, num, gw[k])
+    for _ in range(20):
+        i, k = rng.integers(n), rng.integers(d_f)
+        fp, fm = feat.copy(), feat.copy()
+        fp[i, k] += h; fm[i, k] -= h
+        num = (loss(w, fp) - loss(w, fm)) / (2 * h)
+        assert abs(num - gf[i, k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(gf).max()) + 1e-8
