@@ -225,6 +225,24 @@ int splatb200_view_backward_from_host(splatb200_view* v, const float* g_blend16,
 int splatb200_view_set_los(splatb200_view* v, const float* los_cut);
 int splatb200_view_set_los_grad(splatb200_view* v, const float* g_los);
 
+/* ---- optimizer step (SPEC.md:439-444 optimizer_step) -------------------------
+ * Adam (beta = 0.9 / 0.999, eps = 1e-15) with per-group scheduled learning rates, in place on the ctx's GaussianSet
+ * (uploaded or bound device arrays), reading the ctx's SceneParamGrads buffer — i.e. what the backward passes, and on
+ * several GPUs the all-reduce, left there. Groups: 0 mean, 1 scale_log, 2 quat, 3 opacity_logit, 4 color, 5 feature.
+ * Learning rate of a group at `step` (0-based): min(1, step / warmup) * lr_init * (lr_final / lr_init)^t with
+ * t = clamp((step - warmup) / (total_steps - warmup), 0, 1) — linear warm-up from 0, then exponential interpolation.
+ * A group whose gradient holds a non-finite value is skipped (parameters and moments untouched); skipped[6] (may be NULL)
+ * receives 1 for such groups. Moments live in the ctx and start at zero (reset by a scene upload of another size). */
+typedef struct {
+  float lr_init[6], lr_final[6];
+  int64_t warmup_steps[6];
+  int64_t total_steps;
+} splatb200_adam_config;
+int splatb200_optimizer_step(splatb200_ctx* ctx, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]);
+/* current parameters back to HOST arrays (any pointer may be NULL) */
+int splatb200_scene_download(splatb200_ctx* ctx, float* mean, float* scale_log, float* quat, float* opacity_logit, float* color,
+                             float* feature);
+
 /* ---- lidar head (SPEC.md:366-389 decode_lidar; section 3.3) ----------------------
  * A 2-layer perceptron (hidden 32, rectified-linear inside, logistic outputs) from the D_f blended features of a ray + its
  * direction in the sensor frame to (intensity, ray-drop probability). weights: HOST, splatb200_lidar_head_params(d_f)

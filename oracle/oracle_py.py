@@ -195,6 +195,35 @@ def assign_points_to_tiles(lidar, xyz_world, stamps, train=False, seed=0, dtype=
             "order": order[:cnt[0]].copy(), "begin": begin, "end": end, "rejected": int(cnt[1]), "dropped": int(cnt[2])}
 
 
+def adam_lr(cfg, group, step):
+    """linear warm-up from 0, then exponential interpolation lr_init -> lr_final."""
+    w = float(cfg["warmup_steps"][group])
+    ramp = min(1.0, step / w) if w > 0 else 1.0
+    denom = float(cfg["total_steps"]) - w
+    t = min(1.0, max(0.0, (step - w) / denom)) if denom > 0 else 1.0
+    return ramp * cfg["lr_init"][group] * (cfg["lr_final"][group] / cfg["lr_init"][group]) ** t
+
+
+def adam_step(params, grads, m, v, cfg, step, dtype=np.float64):
+    """optimizer_step: Adam, beta = (0.9, 0.999), eps = 1e-15, per-group scheduled learning rate; a
+    group with a non-finite gradient is skipped. params / grads / m / v: lists of 6 arrays (mean, scale_log, quat,
+    opacity_logit, color, feature); updated in place. Returns the list of skipped groups."""
+    b1, b2, eps = dtype(0.9), dtype(0.999), dtype(1e-15)
+    t1 = step + 1.0
+    bc1, bc2 = dtype(1.0 / (1.0 - 0.9 ** t1)), dtype(1.0 / (1.0 - 0.999 ** t1))
+    skipped = []
+    for k in range(6):
+        g = grads[k].astype(dtype)
+        if not np.isfinite(g).all():
+            skipped.append(k)
+            continue
+        lr = dtype(adam_lr(cfg, k, step))
+        m[k][...] = b1 * m[k] + (dtype(1) - b1) * g
+        v[k][...] = b2 * v[k] + (dtype(1) - b2) * g * g
+        params[k][...] = params[k] - lr * (m[k] * bc1) / (np.sqrt(v[k] * bc2) + eps)
+    return skipped
+
+
 HEAD_HIDDEN = 32
 
 

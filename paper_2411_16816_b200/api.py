@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_lidar_head_params", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_scene_download", "splatb200_lidar_head_params", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -54,6 +54,10 @@ class CameraPOD(C.Structure):
                 ("height", C.c_int32), ("R", C.c_float * 9), ("t", C.c_float * 3), ("vel_lin", C.c_float * 3),
                 ("vel_ang", C.c_float * 3), ("shutter_duration", C.c_float), ("time_offset", C.c_float),
                 ("timestamp", C.c_float)]
+
+
+class AdamConfigPOD(C.Structure):
+    _fields_ = [("lr_init", C.c_float * 6), ("lr_final", C.c_float * 6), ("warmup_steps", C.c_int64 * 6), ("total_steps", C.c_int64)]
 
 
 class LidarPOD(C.Structure):
@@ -100,6 +104,8 @@ def lib():
         L.splatb200_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
+        L.splatb200_optimizer_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.splatb200_scene_download.argtypes = [C.c_void_p] * 7
         L.splatb200_lidar_head_params.argtypes = [C.c_int32]
         L.splatb200_lidar_head_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_lidar_head_backward.argtypes = [C.c_void_p] * 5
@@ -250,6 +256,25 @@ class Context:
         return {"tile": tile, "phi": sph[:, 0].copy(), "omega": sph[:, 1].copy(), "t_l": sph[:, 2].copy(), "range": sph[:, 3].copy(),
                 "order": order, "begin": begin, "end": end, "rejected": int(cnt[1]), "dropped": int(cnt[2]),
                 "rayset": RaySet(rays=rays, begin=begin.copy(), end=end.copy())}
+
+    def optimizer_step(self, cfg: dict, step: int):
+        """optimizer_step on the resident scene from the resident gradients; cfg: lr_init[6], lr_final[6],
+        warmup_steps[6], total_steps. Returns the skipped groups."""
+        pod = AdamConfigPOD()
+        for k in range(6):
+            pod.lr_init[k], pod.lr_final[k], pod.warmup_steps[k] = cfg["lr_init"][k], cfg["lr_final"][k], int(cfg["warmup_steps"][k])
+        pod.total_steps = int(cfg["total_steps"])
+        skipped = (C.c_int32 * 6)()
+        self._check(self.L.splatb200_optimizer_step(self.h, C.byref(pod), int(step), skipped))
+        return [k for k in range(6) if skipped[k]]
+
+    def download_scene(self):
+        """Current parameters: (mean, scale_log, quat, opacity_logit, color, feature) as float32 arrays."""
+        n, d_f = self.n, self.d_f
+        out = [np.zeros((n, 3), np.float32), np.zeros((n, 3), np.float32), np.zeros((n, 4), np.float32), np.zeros(n, np.float32),
+               np.zeros((n, 3), np.float32), np.zeros((n, d_f), np.float32)]
+        self._check(self.L.splatb200_scene_download(self.h, *[_p(a) for a in out]))
+        return out
 
     def debug_depth_sort(self, keys: np.ndarray, counts: np.ndarray):
         """Test hook: the binning stage's radix sort + count scan on caller data -> (order, offsets)."""

@@ -58,6 +58,10 @@ struct splatb200_ctx {
   std::vector<std::vector<double>> actor_d_pose;  // per track 6 x n_poses
   std::vector<std::vector<double>> actor_d_vel;   // per track 6
   std::vector<splatb200_view*> views;
+  // optimizer state (splatb200_optimizer_step): Adam moments over the gradient buffer's layout, per-group skip flags
+  float *adam_m = nullptr, *adam_v = nullptr;
+  int64_t adam_floats = 0;
+  int* adam_bad = nullptr;
 
   int fail(int code, const std::string& m) {
     err = m;
@@ -194,6 +198,8 @@ void free_scene(splatb200_ctx* c) {
   if (c->owns_grads) dfree(c->grads);
   c->grads = nullptr;
   c->owns_grads = false;
+  dfree(c->adam_m); dfree(c->adam_v); dfree(c->adam_bad);
+  c->adam_floats = 0;
 }
 
 int alloc_grads(splatb200_ctx* c) {
@@ -847,6 +853,66 @@ extern "C" void splatb200_view_destroy(splatb200_view* v) {
       break;
     }
   delete v;
+}
+
+// ---- optimizer step -----------------------------------------------------------------------
+extern "C" int splatb200_optimizer_step(splatb200_ctx* c, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]) {
+  if (!cfg || step < 0) return c->fail(SPLATB200_EINVAL, "optimizer_step: bad arguments");
+  if (!c->mean || !c->grads) return c->fail(SPLATB200_ERUNTIME, "optimizer_step without a scene");
+  CU_TRY(c, cudaSetDevice(c->device));
+  join_all(c);
+  const int64_t n = c->n, total = c->grads_floats;
+  if (c->adam_floats != total) {
+    dfree(c->adam_m); dfree(c->adam_v); dfree(c->adam_bad);
+    CU_TRY(c, cudaMalloc(&c->adam_m, sizeof(float) * (size_t)std::max<int64_t>(1, total)));
+    CU_TRY(c, cudaMalloc(&c->adam_v, sizeof(float) * (size_t)std::max<int64_t>(1, total)));
+    CU_TRY(c, cudaMalloc(&c->adam_bad, sizeof(int) * 6));
+    CU_TRY(c, cudaMemsetAsync(c->adam_m, 0, sizeof(float) * (size_t)total, c->stream));
+    CU_TRY(c, cudaMemsetAsync(c->adam_v, 0, sizeof(float) * (size_t)total, c->stream));
+    c->adam_floats = total;
+  }
+  const int64_t width[6] = {3, 3, 4, 1, 3, c->d_f};
+  float* params[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
+  AdamGroups gr;
+  gr.begin[0] = 0;
+  for (int k = 0; k < 6; ++k) gr.begin[k + 1] = gr.begin[k] + width[k] * n;
+  CU_TRY(c, cudaMemsetAsync(c->adam_bad, 0, sizeof(int) * 6, c->stream));
+  launch_grad_finite(c->grads, total, gr, c->adam_bad, c->stream);
+  const double t1 = (double)step + 1.0;
+  const float bc1 = (float)(1.0 / (1.0 - std::pow(0.9, t1))), bc2 = (float)(1.0 / (1.0 - std::pow(0.999, t1)));
+  for (int k = 0; k < 6; ++k) {
+    const double w = (double)cfg->warmup_steps[k];
+    const double ramp = w > 0 ? std::min(1.0, (double)step / w) : 1.0;
+    const double denom = (double)cfg->total_steps - w;
+    const double t = denom > 0 ? std::min(1.0, std::max(0.0, ((double)step - w) / denom)) : 1.0;
+    const double lr = ramp * (double)cfg->lr_init[k] * std::pow((double)cfg->lr_final[k] / (double)cfg->lr_init[k], t);
+    launch_adam(params[k], c->grads + gr.begin[k], c->adam_m + gr.begin[k], c->adam_v + gr.begin[k], width[k] * n, (float)lr,
+                bc1, bc2, c->adam_bad + k, c->stream);
+  }
+  CHECK_LAUNCH(c, "k_adam");
+  c->launches += 7;
+  if (skipped) {
+    int h[6];
+    CU_TRY(c, cudaMemcpyAsync(h, c->adam_bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < 6; ++k) skipped[k] = h[k] != 0;
+  }
+  for (auto* v : c->views) v->stage = 0;  // renders belong to the old parameters
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_scene_download(splatb200_ctx* c, float* mean, float* scale_log, float* quat, float* opacity_logit,
+                                        float* color, float* feature) {
+  if (!c->mean) return c->fail(SPLATB200_ERUNTIME, "no scene");
+  join_all(c);
+  const size_t n = (size_t)c->n;
+  float* dst[6] = {mean, scale_log, quat, opacity_logit, color, feature};
+  const float* src[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
+  const size_t width[6] = {3, 3, 4, 1, 3, (size_t)c->d_f};
+  for (int k = 0; k < 6; ++k)
+    if (dst[k] && n * width[k]) CU_TRY(c, cudaMemcpyAsync(dst[k], src[k], sizeof(float) * n * width[k], cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
 }
 
 // ---- lidar head ---------------------------------------------------------------------------

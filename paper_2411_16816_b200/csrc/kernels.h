@@ -60,6 +60,12 @@ void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 
+// optim.cu (optimizer_step): Adam over the GaussianSet from the contiguous SceneParamGrads buffer
+struct AdamGroups { int64_t begin[7]; };  // slices of the gradient buffer: mean, scale_log, quat, opacity_logit, color, feature
+void launch_grad_finite(const float* g, int64_t n_floats, const AdamGroups& gr, int* bad6, cudaStream_t st);
+void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float bc1, float bc2, const int* bad,
+                 cudaStream_t st);
+
 // decode.cu (decode_lidar): the lidar head over a view's blended features
 int lidar_head_params(int d_f);
 void launch_lidar_head_fwd(const float* w, int d_f, int64_t n_rays, const float4* rays, const float* blend16, float* y_out,

@@ -820,3 +820,28 @@ def test_lidar_head_examples_and_fd(oracle_lib):
         fp[i, k] += h; fm[i, k] -= h
         num = (loss(w, fp) - loss(w, fm)) / (2 * h)
         assert abs(num - gf[i, k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(gf).max()) + 1e-8
+
+
+# ---- optimizer_step ------------------------------------------------------------------------
+_ADAM_CFG = {"lr_init": [1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-3], "lr_final": [1.6e-6, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-4],
+             "warmup_steps": [0, 0, 0, 0, 0, 100], "total_steps": 30000}
+
+
+def test_optimizer_step_examples():
+    """zero gradient -> unchanged; scalar, constant gradient 1, lr 0.1 -> first step ~ -0.1; the schedule
+    ends on the final learning rate; warm-up ramps linearly from 0; a non-finite gradient skips its group."""
+    z = lambda: [np.zeros((4, w)) for w in (3, 3, 4, 1, 3, 13)]
+    p, g, m, v = [x + 1.0 for x in z()], z(), z(), z()
+    assert op.adam_step(p, g, m, v, _ADAM_CFG, 0) == [] and all((x == 1.0).all() for x in p)
+    cfg = {"lr_init": [0.1] * 6, "lr_final": [0.1] * 6, "warmup_steps": [0] * 6, "total_steps": 10}
+    p, g, m, v = z(), [x + 1.0 for x in z()], z(), z()
+    op.adam_step(p, g, m, v, cfg, 0)
+    assert all(np.allclose(x, -0.1, atol=1e-12) for x in p)
+    for k in range(6):
+        assert abs(op.adam_lr(_ADAM_CFG, k, 30000) - _ADAM_CFG["lr_final"][k]) <= 1e-12
+    assert op.adam_lr(_ADAM_CFG, 5, 0) == 0.0 and abs(op.adam_lr(_ADAM_CFG, 5, 50) - 0.5 * 2.5e-3) < 1e-12
+    assert abs(op.adam_lr(_ADAM_CFG, 0, 15000) - 1.6e-5) < 1e-12        # geometric mean half-way
+    g[2][1, 2] = np.nan
+    before = [x.copy() for x in p]
+    assert op.adam_step(p, g, m, v, cfg, 1) == [2]
+    assert np.array_equal(p[2], before[2]) and not np.array_equal(p[0], before[0])
