@@ -825,7 +825,7 @@ static const uint32_t* tile_ws_hist(const void* ws, int tiles_x, int tiles_y) {
 // *total (device) and the digit histograms a sort by tile id needs (kept in tile_ws).
 int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int tiles_y, int wrap_x, void* tile_ws,
                        uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, uint32_t* seg_first,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool want_hist) {
   const size_t slot_bytes = tile_slot_bytes(tiles_x, tiles_y);
   cudaMemsetAsync(tile_ws, 0, slot_bytes, st);
   int* slots = (int*)tile_ws;
@@ -843,6 +843,7 @@ int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int 
     cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmemMax);
     attr = true;
   }
+  if (!want_hist) hist = nullptr;  // the grid is not sorted on (two-level binning sorts blocks, not tiles)
   k_tile_scan<<<1, 1024, in_smem ? smem : 0, st>>>(tiles_x, tiles_y, slots, in_smem ? nullptr : scratch, tile_begin, tile_end, hist,
                                                    tile_passes((int64_t)tiles_x * tiles_y), tile_order, total, seg_first, kSeg);
   return launches + 1;

@@ -1109,7 +1109,7 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     {
       StageTimer tm(v, 2, ts);
       c->launches += launch_tile_counts(c->n, v->proj, 0, v->s.tiles_x, v->s.tiles_y, wrap_x, v->tile_ws, v->tile_begin,
-                                        v->tile_end, v->to_vals0, v->d_total, nullptr, ts);
+                                        v->tile_end, v->to_vals0, v->d_total, nullptr, ts, !v->two_level);
       v->tile_order = v->to_vals0;
       if (v->two_level)  // the same on the grid of 8 x 8-tile blocks: block ranges, list segments, sort histograms
         c->launches += launch_tile_counts(c->n, v->proj, sh, v->stiles_x, v->stiles_y, 0, v->tile_ws_c, v->super_begin,

@@ -92,7 +92,7 @@ size_t tile_hist_bytes(int tiles_x, int tiles_y);
 // *total (device) and the digit histograms a sort by tile id needs (kept in tile_ws)
 int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int tiles_y, int wrap_x, void* tile_ws,
                        uint32_t* tile_begin, uint32_t* tile_end, uint32_t* tile_order, int64_t* total, uint32_t* seg_first,
-                       cudaStream_t st);
+                       cudaStream_t st, bool want_hist = true);
 size_t tile_sort_temp_bytes(int64_t cap, int64_t n_tiles);
 // duplication (one (tile id, source index) pair per intersection, generated in depth order inside the first pass) +
 // stable sort by tile id, on the grid of 2^shift-tile blocks. Returns which of vals0 / vals1 holds the sorted indices.
