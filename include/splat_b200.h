@@ -251,6 +251,10 @@ int splatb200_scene_download(splatb200_ctx* ctx, float* mean, float* scale_log, 
  * g_blend16: DEVICE, P x 16 — dL/dfeature is ADDED to slots [0, d_f) of each ray, so that the buffer (holding any other
  * upstream gradient of the render) can go straight into splatb200_view_backward. */
 int32_t splatb200_lidar_head_params(int32_t d_f);
+/* fused form of the forward: with weights set (HOST, copied; NULL switches it off) every splatb200_view_forward of the
+ * lidar view also decodes the blended features in the compositing kernel's epilogue, while they are still in registers;
+ * read the P x 2 result with splatb200_view_array(v, "lidar_head", dst). */
+int splatb200_view_set_lidar_head(splatb200_view* v, const float* weights);
 int splatb200_lidar_head_forward(splatb200_view* v, const float* weights, float* y);
 int splatb200_lidar_head_backward(splatb200_view* v, const float* weights, const float* g_y, float* g_weights,
                                   float* g_blend16);

@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_scene_download", "splatb200_lidar_head_params", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_scene_download", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -107,6 +107,7 @@ def lib():
         L.splatb200_optimizer_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.splatb200_scene_download.argtypes = [C.c_void_p] * 7
         L.splatb200_lidar_head_params.argtypes = [C.c_int32]
+        L.splatb200_view_set_lidar_head.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_lidar_head_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_lidar_head_backward.argtypes = [C.c_void_p] * 5
         L.splatb200_view_set_los.argtypes = [C.c_void_p, C.c_void_p]
@@ -410,6 +411,11 @@ class View:
             self.close()
         except Exception:
             pass
+
+    def set_lidar_head(self, weights):
+        """Fused lidar head: every forward also decodes the blended features (array("lidar_head"): P x 2); None: off."""
+        w = None if weights is None else np.ascontiguousarray(weights, np.float32)
+        self.ctx._check(self.L.splatb200_view_set_lidar_head(self.h, _p(w)))
 
     def lidar_head_forward(self, weights) -> np.ndarray:
         """decode_lidar over this view's blended features: P x 2 (intensity, ray-drop probability)."""

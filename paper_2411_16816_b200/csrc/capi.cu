@@ -123,6 +123,7 @@ struct splatb200_view {
   int64_t P = 0, n_tiles = 0;
   int64_t P_cap = 0;   // queries the per-query buffers are sized for (lidar sweeps change size: view_set_rays)
   float *d_los_cut = nullptr, *d_los = nullptr, *d_g_los = nullptr;  // line-of-sight channel (lidar, optional)
+  float *d_head_w = nullptr, *d_head_y = nullptr;                     // fused lidar head (optional)
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
   int64_t *ray_begin = nullptr, *ray_end = nullptr;
   uint32_t* tile_order = nullptr;  // CTA -> tile permutation (longest worklists first), rebuilt every forward
@@ -247,7 +248,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -918,6 +919,23 @@ extern "C" int splatb200_scene_download(splatb200_ctx* c, float* mean, float* sc
 // ---- lidar head ---------------------------------------------------------------------------
 extern "C" int32_t splatb200_lidar_head_params(int32_t d_f) { return lidar_head_params(d_f); }
 
+extern "C" int splatb200_view_set_lidar_head(splatb200_view* v, const float* weights) {
+  splatb200_ctx* c = v->ctx;
+  if (v->s.is_camera) return c->fail(SPLATB200_EINVAL, "the lidar head decodes a lidar view");
+  join_view(v);
+  if (!weights) {
+    v->out.head_w = nullptr; v->out.head_y = nullptr;
+    return SPLATB200_OK;
+  }
+  const int np = lidar_head_params(c->d_f);
+  if (!v->d_head_w) CU_TRY(c, cudaMalloc(&v->d_head_w, sizeof(float) * 640));
+  CU_TRY(c, cudaMemcpyAsync(v->d_head_w, weights, sizeof(float) * np, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  v->out.head_w = v->d_head_w;
+  v->stage = std::min(v->stage, 2);
+  return SPLATB200_OK;
+}
+
 extern "C" int splatb200_lidar_head_forward(splatb200_view* v, const float* weights, float* y) {
   splatb200_ctx* c = v->ctx;
   if (v->s.is_camera) return c->fail(SPLATB200_EINVAL, "the lidar head decodes a lidar view");
@@ -1010,7 +1028,8 @@ extern "C" int splatb200_view_set_rays(splatb200_view* v, const float* rays, int
   if (n_rays > v->P_cap) {
     dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend); dfree(v->out.n_contrib);
     dfree(v->out.last_idx); dfree(v->g_blend_stage); dfree(v->g_alpha_stage); dfree(v->rays);
-    dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los);
+    dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_y);
+    v->out.head_y = nullptr;
     const size_t cap = (size_t)(n_rays + n_rays / 8 + 256);
     CU_TRY(c, cudaMalloc(&v->out.blend, sizeof(float) * 16 * cap));
     CU_TRY(c, cudaMalloc(&v->out.alpha, sizeof(float) * cap));
@@ -1175,6 +1194,9 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   }
   v->out.hit_or = v->multi_pass ? 1 : 0;
   if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
+  if (v->out.head_w && !v->d_head_y)
+    CU_TRY(c, cudaMalloc(&v->d_head_y, sizeof(float) * 2 * (size_t)std::max<int64_t>(1, std::max(v->P, v->P_cap))));
+  v->out.head_y = v->out.head_w ? v->d_head_y : nullptr;
   v->band_dl_valid = false;
   if (!v->plan_fwd) {
     StageTimer tm(v, 5, st);
@@ -1900,6 +1922,7 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   else if (name == "t_final") src = v->out.t_final;
   else if (name == "range_blend") src = v->out.range_blend;
   else if (name == "los") src = v->out.los;
+  else if (name == "lidar_head") { src = v->out.head_y; cnt = 2 * P; }
   if (!src) return c->fail(SPLATB200_EINVAL, "unknown array name " + name);
   if (dst && cnt) {
     CU_TRY(c, cudaMemcpyAsync(dst, src, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream));

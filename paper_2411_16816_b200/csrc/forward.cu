@@ -7,6 +7,7 @@
 //   k_raster_fwd<camera|lidar> per-tile front-to-back compositing (Eq. 3-6).
 #include "kernels.h"
 #include "raster_common.cuh"
+#include "decode_device.cuh"
 
 namespace sb {
 
@@ -77,7 +78,7 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
 // query of the tile has saturated (T < transmittance_min): one __syncthreads_and per batch; a warp whose
 // 32 queries have all saturated stops evaluating on its own.
 // ------------------------------------------------------------------------------------------------
-template <bool kCamera, bool kLos = false>
+template <bool kCamera, bool kLos = false, bool kHead = false>
 __global__ void __launch_bounds__(256, kCamera ? 4 : 3)
 k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
@@ -91,9 +92,14 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   __shared__ uint8_t sList[8][256];
   __shared__ __align__(8) uint8_t sHit[8][256];  // [warp][batch entry]: some lane of the warp blended it
   __shared__ PatchBox sBox[8];
+  __shared__ float sHead[(!kCamera && kHead) ? 640 : 1];  // lidar head parameters (fused epilogue)
 
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
   const int tid = threadIdx.x;
+  if (!kCamera && kHead) {  // visible to everyone after the first barrier below
+    const int np = headdev::kHid * (s.d_f + 3) + headdev::kHid + 2 * headdev::kHid + 2;
+    for (int i = tid; i < np; i += 256) sHead[i] = out.head_w[i];
+  }
   const int lane = tid & 31, warp = tid >> 5;
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
 
@@ -248,6 +254,15 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         acc[15] = A;
         out.range_blend[pix] = range_acc;
         if (los_on) out.los[pix] = los;
+        if (kHead) {  // decode_lidar on the blended features, while they are still in registers
+          float x[headdev::kInMax], y[2], h[headdev::kHid];
+#pragma unroll
+          for (int k = 0; k < 13; ++k) x[k] = acc[k];
+          headdev::ray_dir(qx, qy, x + s.d_f);
+          headdev::head_forward(sHead, s.d_f + 3, x, y, h);
+          out.head_y[2 * pix] = y[0];
+          out.head_y[2 * pix + 1] = y[1];
+        }
       }
       float4* o4 = reinterpret_cast<float4*>(out.blend + 16 * pix);
 #pragma unroll
@@ -273,6 +288,10 @@ void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
   if (tile_count < 0) tile_first = 0;
   if (s.is_camera)
     k_raster_fwd<true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+  else if (out.los_cut && out.head_w)
+    k_raster_fwd<false, true, true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+  else if (out.head_w)
+    k_raster_fwd<false, false, true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else if (out.los_cut)
     k_raster_fwd<false, true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else

@@ -892,6 +892,14 @@ def test_lidar_head_matches_oracle(ctx, op):
     oy = op.lidar_head_forward(w, feat, sph, np.float32)
     assert y.min() > 0 and y.max() < 1
     assert np.abs(y - oy).max() <= RENDER_RTOL
+    # the fused form: decoded in the compositing kernel's epilogue
+    view.set_lidar_head(w)
+    view.forward(0.0)
+    yf = view.array("lidar_head").reshape(P, 2)
+    assert np.abs(yf - oy).max() <= RENDER_RTOL and np.abs(yf - y).max() <= 1e-6
+    assert np.array_equal(view.array("blend").reshape(P, 16)[:, :d_f], feat)
+    view.set_lidar_head(None)
+    view.forward(0.0)
     g_y = rng.normal(size=(P, 2)).astype(np.float32)
     g_up = torch.zeros((P, 16), dtype=torch.float32, device="cuda")
     g_up[:, 3] = 0.25                                   # some other upstream gradient of the render: must be kept
