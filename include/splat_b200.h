@@ -239,6 +239,15 @@ typedef struct {
   int64_t total_steps;
 } splatb200_adam_config;
 int splatb200_optimizer_step(splatb200_ctx* ctx, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]);
+/* The same on the slice [lo, hi) of the gradient buffer's flat layout [mean 3N | scale_log 3N | quat 4N | opacity N |
+ * color 3N | feature d_f N] only — a rank's shard after a reduce-scatter (paper_2411_16816_b200/dist.py
+ * sharded_optimizer_step: reduce-scatter -> this -> all-gather of the parameters). skip_groups[6] (may be NULL): groups to
+ * leave untouched, e.g. because ANOTHER rank's shard of the group held a non-finite gradient; skipped[6] reports the groups
+ * whose gradient is non-finite inside [lo, hi). */
+int splatb200_optimizer_step_range(splatb200_ctx* ctx, const splatb200_adam_config* cfg, int64_t step, int64_t lo, int64_t hi,
+                                   const int32_t skip_groups[6], int32_t skipped[6]);
+/* non-finite check alone, per group, inside [lo, hi) (sharded step: the flags are all-reduced before anyone steps) */
+int splatb200_grads_nonfinite_range(splatb200_ctx* ctx, int64_t lo, int64_t hi, int32_t flags[6]);
 /* current parameters back to HOST arrays (any pointer may be NULL) */
 int splatb200_scene_download(splatb200_ctx* ctx, float* mean, float* scale_log, float* quat, float* opacity_logit, float* color,
                              float* feature);

@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_scene_download", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_optimizer_step_range", "splatb200_grads_nonfinite_range", "splatb200_scene_download", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -105,6 +105,8 @@ def lib():
         L.splatb200_ctx_set_view_streams.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_ctx_join.argtypes = [C.c_void_p]
         L.splatb200_optimizer_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.splatb200_optimizer_step_range.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        L.splatb200_grads_nonfinite_range.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
         L.splatb200_scene_download.argtypes = [C.c_void_p] * 7
         L.splatb200_lidar_head_params.argtypes = [C.c_int32]
         L.splatb200_view_set_lidar_head.argtypes = [C.c_void_p, C.c_void_p]
@@ -267,6 +269,27 @@ class Context:
         pod.total_steps = int(cfg["total_steps"])
         skipped = (C.c_int32 * 6)()
         self._check(self.L.splatb200_optimizer_step(self.h, C.byref(pod), int(step), skipped))
+        return [k for k in range(6) if skipped[k]]
+
+    @staticmethod
+    def _adam_pod(cfg: dict):
+        pod = AdamConfigPOD()
+        for k in range(6):
+            pod.lr_init[k], pod.lr_final[k], pod.warmup_steps[k] = cfg["lr_init"][k], cfg["lr_final"][k], int(cfg["warmup_steps"][k])
+        pod.total_steps = int(cfg["total_steps"])
+        return pod
+
+    def grads_nonfinite_range(self, lo: int, hi: int):
+        flags = (C.c_int32 * 6)()
+        self._check(self.L.splatb200_grads_nonfinite_range(self.h, int(lo), int(hi), flags))
+        return [int(flags[k]) for k in range(6)]
+
+    def optimizer_step_range(self, cfg: dict, step: int, lo: int, hi: int, skip_groups=None):
+        """optimizer_step on the slice [lo, hi) of the flat gradient layout (a rank's shard); skip_groups: 6 flags."""
+        pod = self._adam_pod(cfg)
+        skipped = (C.c_int32 * 6)()
+        skip = None if skip_groups is None else (C.c_int32 * 6)(*[int(x) for x in skip_groups])
+        self._check(self.L.splatb200_optimizer_step_range(self.h, C.byref(pod), int(step), int(lo), int(hi), skip, skipped))
         return [k for k in range(6) if skipped[k]]
 
     def download_scene(self):

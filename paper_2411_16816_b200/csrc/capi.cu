@@ -857,41 +857,91 @@ extern "C" void splatb200_view_destroy(splatb200_view* v) {
 }
 
 // ---- optimizer step -----------------------------------------------------------------------
-extern "C" int splatb200_optimizer_step(splatb200_ctx* c, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]) {
-  if (!cfg || step < 0) return c->fail(SPLATB200_EINVAL, "optimizer_step: bad arguments");
-  if (!c->mean || !c->grads) return c->fail(SPLATB200_ERUNTIME, "optimizer_step without a scene");
-  CU_TRY(c, cudaSetDevice(c->device));
-  join_all(c);
-  const int64_t n = c->n, total = c->grads_floats;
-  if (c->adam_floats != total) {
-    dfree(c->adam_m); dfree(c->adam_v); dfree(c->adam_bad);
-    CU_TRY(c, cudaMalloc(&c->adam_m, sizeof(float) * (size_t)std::max<int64_t>(1, total)));
-    CU_TRY(c, cudaMalloc(&c->adam_v, sizeof(float) * (size_t)std::max<int64_t>(1, total)));
-    CU_TRY(c, cudaMalloc(&c->adam_bad, sizeof(int) * 6));
-    CU_TRY(c, cudaMemsetAsync(c->adam_m, 0, sizeof(float) * (size_t)total, c->stream));
-    CU_TRY(c, cudaMemsetAsync(c->adam_v, 0, sizeof(float) * (size_t)total, c->stream));
-    c->adam_floats = total;
-  }
+namespace {
+int ensure_adam_state(splatb200_ctx* c) {
+  const int64_t total = c->grads_floats;
+  if (c->adam_floats == total && c->adam_m) return SPLATB200_OK;
+  dfree(c->adam_m); dfree(c->adam_v); dfree(c->adam_bad);
+  CU_TRY(c, cudaMalloc(&c->adam_m, sizeof(float) * (size_t)std::max<int64_t>(1, total)));
+  CU_TRY(c, cudaMalloc(&c->adam_v, sizeof(float) * (size_t)std::max<int64_t>(1, total)));
+  CU_TRY(c, cudaMalloc(&c->adam_bad, sizeof(int) * 6));
+  CU_TRY(c, cudaMemsetAsync(c->adam_m, 0, sizeof(float) * (size_t)total, c->stream));
+  CU_TRY(c, cudaMemsetAsync(c->adam_v, 0, sizeof(float) * (size_t)total, c->stream));
+  c->adam_floats = total;
+  return SPLATB200_OK;
+}
+AdamGroups adam_groups(const splatb200_ctx* c) {
   const int64_t width[6] = {3, 3, 4, 1, 3, c->d_f};
-  float* params[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
   AdamGroups gr;
   gr.begin[0] = 0;
-  for (int k = 0; k < 6; ++k) gr.begin[k + 1] = gr.begin[k] + width[k] * n;
+  for (int k = 0; k < 6; ++k) gr.begin[k + 1] = gr.begin[k] + width[k] * c->n;
+  return gr;
+}
+// flags the groups with a non-finite gradient inside [lo, hi) into c->adam_bad (device), after clearing it
+int flag_nonfinite(splatb200_ctx* c, int64_t lo, int64_t hi) {
+  AdamGroups gr = adam_groups(c);
+  for (int k = 0; k <= 6; ++k) gr.begin[k] = std::min(std::max(gr.begin[k], lo), hi) - lo;  // slices relative to lo
   CU_TRY(c, cudaMemsetAsync(c->adam_bad, 0, sizeof(int) * 6, c->stream));
-  launch_grad_finite(c->grads, total, gr, c->adam_bad, c->stream);
+  launch_grad_finite(c->grads + lo, hi - lo, gr, c->adam_bad, c->stream);
+  return SPLATB200_OK;
+}
+}  // namespace
+
+extern "C" int splatb200_grads_nonfinite_range(splatb200_ctx* c, int64_t lo, int64_t hi, int32_t flags[6]) {
+  if (!c->grads || !flags) return c->fail(SPLATB200_ERUNTIME, "grads_nonfinite_range without gradients");
+  if (lo < 0 || hi < lo || hi > c->grads_floats) return c->fail(SPLATB200_EINVAL, "range outside the gradient buffer");
+  CU_TRY(c, cudaSetDevice(c->device));
+  join_all(c);
+  int rc = ensure_adam_state(c);
+  if (!rc) rc = flag_nonfinite(c, lo, hi);
+  if (rc) return rc;
+  int h[6];
+  CU_TRY(c, cudaMemcpyAsync(h, c->adam_bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < 6; ++k) flags[k] = h[k] != 0;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_optimizer_step_range(splatb200_ctx* c, const splatb200_adam_config* cfg, int64_t step, int64_t lo,
+                                              int64_t hi, const int32_t skip_groups[6], int32_t skipped[6]) {
+  if (!cfg || step < 0) return c->fail(SPLATB200_EINVAL, "optimizer_step: bad arguments");
+  if (!c->mean || !c->grads) return c->fail(SPLATB200_ERUNTIME, "optimizer_step without a scene");
+  if (lo < 0 || hi < lo || hi > c->grads_floats) return c->fail(SPLATB200_EINVAL, "range outside the gradient buffer");
+  CU_TRY(c, cudaSetDevice(c->device));
+  join_all(c);
+  int rc = ensure_adam_state(c);
+  if (!rc) rc = flag_nonfinite(c, lo, hi);
+  if (rc) return rc;
+  if (skip_groups) {  // groups another shard found non-finite
+    int h[6], any = 0;
+    for (int k = 0; k < 6; ++k) { h[k] = skip_groups[k] != 0; any |= h[k]; }
+    if (any) {
+      int cur[6];
+      CU_TRY(c, cudaMemcpyAsync(cur, c->adam_bad, sizeof(cur), cudaMemcpyDeviceToHost, c->stream));
+      CU_TRY(c, cudaStreamSynchronize(c->stream));
+      for (int k = 0; k < 6; ++k) cur[k] |= h[k];
+      CU_TRY(c, cudaMemcpy(c->adam_bad, cur, sizeof(cur), cudaMemcpyHostToDevice));
+    }
+  }
+  const AdamGroups gr = adam_groups(c);
+  float* params[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
   const double t1 = (double)step + 1.0;
   const float bc1 = (float)(1.0 / (1.0 - std::pow(0.9, t1))), bc2 = (float)(1.0 / (1.0 - std::pow(0.999, t1)));
+  int launched = 1;
   for (int k = 0; k < 6; ++k) {
+    const int64_t a = std::max(gr.begin[k], lo), b = std::min(gr.begin[k + 1], hi);
+    if (b <= a) continue;
     const double w = (double)cfg->warmup_steps[k];
     const double ramp = w > 0 ? std::min(1.0, (double)step / w) : 1.0;
     const double denom = (double)cfg->total_steps - w;
     const double t = denom > 0 ? std::min(1.0, std::max(0.0, ((double)step - w) / denom)) : 1.0;
     const double lr = ramp * (double)cfg->lr_init[k] * std::pow((double)cfg->lr_final[k] / (double)cfg->lr_init[k], t);
-    launch_adam(params[k], c->grads + gr.begin[k], c->adam_m + gr.begin[k], c->adam_v + gr.begin[k], width[k] * n, (float)lr,
-                bc1, bc2, c->adam_bad + k, c->stream);
+    launch_adam(params[k] + (a - gr.begin[k]), c->grads + a, c->adam_m + a, c->adam_v + a, b - a, (float)lr, bc1, bc2,
+                c->adam_bad + k, c->stream);
+    ++launched;
   }
   CHECK_LAUNCH(c, "k_adam");
-  c->launches += 7;
+  c->launches += launched;
   if (skipped) {
     int h[6];
     CU_TRY(c, cudaMemcpyAsync(h, c->adam_bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -900,6 +950,10 @@ extern "C" int splatb200_optimizer_step(splatb200_ctx* c, const splatb200_adam_c
   }
   for (auto* v : c->views) v->stage = 0;  // renders belong to the old parameters
   return SPLATB200_OK;
+}
+
+extern "C" int splatb200_optimizer_step(splatb200_ctx* c, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]) {
+  return splatb200_optimizer_step_range(c, cfg, step, 0, c->grads_floats, nullptr, skipped);
 }
 
 extern "C" int splatb200_scene_download(splatb200_ctx* c, float* mean, float* scale_log, float* quat, float* opacity_logit,

@@ -48,3 +48,63 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def shard_range(total: int, world: int, rank: int, align: int = 4):
+    """[lo, hi) of a flat buffer of `total` floats owned by `rank`: equal shards (the last one may be shorter), aligned to
+    `align` elements so that 128-bit accesses stay aligned."""
+    per = -(-total // world)
+    per = -(-per // align) * align
+    lo = min(total, rank * per)
+    return lo, min(total, lo + per)
+
+
+def sharded_optimizer_step(ctx, grads, params_flat, cfg, step, group=None):
+    """the optimizer step fused with the gradient collective. Instead of all-reducing the 27*N-float
+    SceneParamGrads buffer and stepping everywhere, every rank (1) reduce-scatters it — each rank ends up with the SUM of
+    its own shard —, (2) agrees on the groups to skip (a non-finite gradient anywhere skips the group everywhere: one
+    6-int all-reduce), (3) runs Adam on its shard only (moments are only ever touched there: optimizer state and work
+    divide by the world size), (4) all-gathers the updated parameters. Same bytes on the wire as the all-reduce.
+    `grads`: the torch tensor bound with ctx.bind_grads_device; `params_flat`: ONE torch tensor holding the scene in the
+    gradient buffer's layout [mean 3N | scale_log 3N | quat 4N | opacity N | color 3N | feature d_f N], whose slices are
+    bound with ctx.bind_scene_device. Returns the skipped groups."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    total = grads.numel()
+    lo, hi = shard_range(total, world, rank)
+    per = shard_range(total, world, 0)[1]
+    gloo = world > 1 and dist.get_backend(group) == "gloo"   # CPU tests: gloo has no reduce-scatter -> all-reduce, keep the shard
+    if gloo:
+        dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
+    elif world > 1:
+        if per * world != total:       # reduce_scatter_tensor wants equal shards: pad through a staging copy
+            padded = torch.zeros(per * world, dtype=grads.dtype, device=grads.device)
+            padded[:total] = grads
+            out = torch.empty(per, dtype=grads.dtype, device=grads.device)
+            dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
+            grads[lo:hi] = out[:hi - lo]
+        else:
+            dist.reduce_scatter_tensor(grads[lo:hi], grads, op=dist.ReduceOp.SUM, group=group)
+    flags = torch.tensor(ctx.grads_nonfinite_range(lo, hi), dtype=torch.int32, device=grads.device)
+    if world > 1:
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    skip = [int(x) for x in flags.tolist()]
+    ctx.optimizer_step_range(cfg, step, lo, hi, skip_groups=skip)
+    if gloo:
+        send = torch.zeros(per, dtype=params_flat.dtype)
+        send[:hi - lo] = params_flat[lo:hi]
+        parts = [torch.empty(per, dtype=params_flat.dtype) for _ in range(world)]
+        dist.all_gather(parts, send, group=group)
+        params_flat.copy_(torch.cat(parts)[:total])
+    elif world > 1:
+        if per * world != total:
+            send = torch.zeros(per, dtype=params_flat.dtype, device=params_flat.device)
+            send[:hi - lo] = params_flat[lo:hi]
+            recv = torch.empty(per * world, dtype=params_flat.dtype, device=params_flat.device)
+            dist.all_gather_into_tensor(recv, send, group=group)
+            params_flat.copy_(recv[:total])
+        else:
+            dist.all_gather_into_tensor(params_flat, params_flat[lo:hi].clone(), group=group)
+    return [k for k in range(6) if skip[k]]

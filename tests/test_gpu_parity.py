@@ -1001,3 +1001,40 @@ def test_training_loop_reduces_the_loss(ctx):
     vis = np.abs(feature - start.feature).max(1) > 1e-4                                                       # Gaussians the sensors blended
     assert vis.sum() > 200
     assert np.isfinite(feature).all() and np.isfinite(opl).all() and np.isfinite(color).all()
+
+
+def test_optimizer_step_range_and_sharded_path(api, op):
+    """optimizer_step_range on two consecutive shards == optimizer_step on the whole buffer (same context state otherwise),
+    including an unaligned boundary; sharded_optimizer_step at world size 1 (no collective) == optimizer_step; a
+    skip flag from 'another rank' leaves the group untouched."""
+    import torch
+    from paper_2411_16816_b200 import dist as sdist
+    cfg = {"lr_init": [1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-3], "lr_final": [1.6e-6, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-4],
+           "warmup_steps": [0] * 6, "total_steps": 10}
+    sc = synth.make_scene(30_011, seed=21)
+    g_all = (np.random.default_rng(3).normal(size=27 * sc.n) * 1e-2).astype(np.float32)
+    results = []
+    for mode in ("full", "two_shards", "sharded_world1", "skip_quat"):
+        c = api.Context(0)
+        try:
+            c.upload_scene(sc)
+            grads_t = torch.from_numpy(g_all.copy()).cuda()
+            c.bind_grads_device(grads_t.data_ptr(), c.grads_size)
+            for step in range(3):
+                if mode == "full":
+                    c.optimizer_step(cfg, step)
+                elif mode == "two_shards":
+                    cut = 13 * sc.n + 1                      # inside the color slice, not a multiple of 4
+                    c.optimizer_step_range(cfg, step, 0, cut)
+                    c.optimizer_step_range(cfg, step, cut, c.grads_size)
+                elif mode == "sharded_world1":
+                    sdist.sharded_optimizer_step(c, grads_t, None, cfg, step)
+                else:
+                    c.optimizer_step_range(cfg, step, 0, c.grads_size, skip_groups=[0, 0, 1, 0, 0, 0])
+            results.append([a.copy() for a in c.download_scene()])
+        finally:
+            c.close()
+    full, two, sh1, skipq = results
+    for a, b, d in zip(full, two, sh1):
+        assert np.array_equal(a, b) and np.array_equal(a, d)
+    assert np.array_equal(skipq[2], np.asarray(sc.quat, np.float32)) and np.array_equal(skipq[0], full[0])
