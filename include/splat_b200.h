@@ -268,6 +268,27 @@ int splatb200_lidar_head_forward(splatb200_view* v, const float* weights, float*
 int splatb200_lidar_head_backward(splatb200_view* v, const float* weights, const float* g_y, float* g_weights,
                                   float* g_blend16);
 
+/* ---- camera ConvDecoder (SPEC.md:362-380 decode_image; Eq. 7-8; ray directions scene.hpp:119-122) ----
+ * Maps a camera view's blended features (+ per-pixel ray direction + the camera's 8-d embedding, broadcast) to a
+ * per-pixel affine colour correction: I = M . F_rgb + b with (M - 1, b) the 6 outputs of a small CNN — two residual
+ * blocks of 3x3 convolutions at width 32 (ReLU inside, reflect padding) and a linear head. The reference ships no
+ * decoder code; the concrete layer list and parameter packing are fixed in oracle/decoder_oracle.hpp:
+ *   x0 = (feature[d_f], ray_direction[3], embedding[8], 0...) (32 ch);  h0 = conv0(x0);
+ *   h1 = h0 + conv2(relu(conv1(relu(h0))));  h2 = h1 + conv4(relu(conv3(relu(h1))));  y = Wh h2 + bh;
+ *   I_c = (1 + y_c) rgb_c + y_{3+c}.
+ * params: HOST, splatb200_conv_decoder_params() floats: for l = 0..4 W_l[co 32][ky 3][kx 3][ci 32] then b_l[32]; then
+ * Wh[6][32], bh[6]. embedding: HOST, 8 floats. image: HOST, P x 3 (may be NULL: read it with
+ * splatb200_view_array(v, "decoded", dst)). device_ms (may be NULL): device time of the decode, CUDA events.
+ * Call after splatb200_view_forward of a camera view. The convolutions run on the tensor cores (tcgen05, tf32 operands
+ * rounded to nearest, fp32 accumulation): results agree with an fp32 evaluation to ~1e-3 relative. */
+int32_t splatb200_conv_decoder_params(void);
+int splatb200_view_decode_image(splatb200_view* v, const float* params, const float* embedding, float* image,
+                                float* device_ms);
+/* test hook: one 3x3, 32 -> 32 convolution of the decoder on HOST arrays (x, y, res: H x W x 32 pixel-interleaved;
+ * w: 9216 weights + 32 bias; res may be NULL). */
+int splatb200_debug_conv3x3(splatb200_ctx* ctx, const float* x, int32_t H, int32_t W, const float* w, int32_t relu_in,
+                            const float* res, float* y);
+
 /* ---- lidar returns -> rasterization points (SPEC.md:230-238 assign_points_to_tiles) ----
  * The producer of splatb200_view_create_lidar's `rays`. points_xyz: n x 3 world coordinates (ego-motion compensated),
  * timestamps: n capture times; HOST arrays. Each point is re-expressed relative to the sensor pose at its own capture

@@ -11,6 +11,7 @@
 #include <map>
 
 #include "splat_oracle.hpp"
+#include "decoder_oracle.hpp"
 
 using namespace orc;
 
@@ -559,6 +560,26 @@ int view_brute(void* vv, int early_exit, S* blend16, S* alpha, int64_t* n_contri
 
 ORC_API(f32, float)
 ORC_API(f64, double)
+
+// decode_image, decoder_oracle.hpp. rgb H x W x 3, feat H x W x d_f, intr = (fx, fy, cx, cy).
+#define ORC_DECODER(SUF, S)                                                                                              \
+  extern "C" void orc_decoder_forward_##SUF(const S* params, int H, int W, int d_f, const S* rgb, const S* feat,         \
+                                            const S* intr, const S* emb, S* image, S* h2, int workers) {                              \
+    DecoderState<S> st;                                                                                                  \
+    decoder_forward<S>(params, H, W, d_f, rgb, feat, intr, emb, image, &st, workers);                                    \
+    if (h2) std::copy(st.h2.begin(), st.h2.end(), h2);                                                                   \
+  }                                                                                                                      \
+  extern "C" void orc_decoder_backward_##SUF(const S* params, int H, int W, int d_f, const S* rgb, const S* feat,        \
+                                             const S* intr, const S* emb, const S* g_image, S* g_params, S* g_rgb,       \
+                                             S* g_feat, S* g_emb) {                                                      \
+    DecoderState<S> st;                                                                                                  \
+    std::vector<S> image((size_t)H * W * 3);                                                                             \
+    decoder_forward<S>(params, H, W, d_f, rgb, feat, intr, emb, image.data(), &st);                                      \
+    decoder_backward<S>(params, st, rgb, g_image, g_params, g_rgb, g_feat, g_emb);                                       \
+  }
+ORC_DECODER(f32, float)
+ORC_DECODER(f64, double)
+extern "C" int orc_decoder_params() { return kDecParams; }
 
 // detmath bit-pattern probes (host build of the header the kernels use)
 extern "C" void orc_detmath_eval(int fn, const float* x, const float* y, float* out, int64_t n) {

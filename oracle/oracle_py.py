@@ -254,6 +254,39 @@ def lidar_head_backward(w, feat, sph, g_y, dtype=np.float32):
     return gw, gf
 
 
+DEC_WIDTH, DEC_CONVS = 32, 5
+DEC_CONV_PARAMS = DEC_WIDTH * 9 * DEC_WIDTH + DEC_WIDTH
+DEC_HEAD_OFFSET = DEC_CONVS * DEC_CONV_PARAMS
+DEC_PARAMS = DEC_HEAD_OFFSET + 6 * DEC_WIDTH + 6
+
+
+def decoder_forward(params, rgb, feat, intr, emb, dtype=np.float32, want_h2=False, workers=1):
+    """decode_image (decoder_oracle.hpp): rgb H x W x 3, feat H x W x d_f, intr (fx, fy, cx, cy),
+    emb[8] -> image H x W x 3 (and the trunk output H x W x 32 when want_h2)."""
+    L, suf = lib(), _suf(dtype)
+    rgb = np.ascontiguousarray(rgb, dtype); feat = np.ascontiguousarray(feat, dtype)
+    params = np.ascontiguousarray(params, dtype); intr = np.ascontiguousarray(intr, dtype); emb = np.ascontiguousarray(emb, dtype)
+    H, W, d_f = feat.shape
+    assert params.size == DEC_PARAMS and rgb.shape == (H, W, 3) and emb.size == 8 and d_f + 11 <= DEC_WIDTH
+    image = np.zeros((H, W, 3), dtype)
+    h2 = np.zeros((H, W, DEC_WIDTH), dtype) if want_h2 else None
+    getattr(L, f"orc_decoder_forward_{suf}")(_p(params), C.c_int(H), C.c_int(W), C.c_int(d_f), _p(rgb), _p(feat), _p(intr),
+                                             _p(emb), _p(image), _p(h2) if want_h2 else None, C.c_int(workers))
+    return (image, h2) if want_h2 else image
+
+
+def decoder_backward(params, rgb, feat, intr, emb, g_image, dtype=np.float64):
+    """-> (dL/dparams, dL/drgb, dL/dfeat, dL/demb)"""
+    L, suf = lib(), _suf(dtype)
+    rgb = np.ascontiguousarray(rgb, dtype); feat = np.ascontiguousarray(feat, dtype); g_image = np.ascontiguousarray(g_image, dtype)
+    params = np.ascontiguousarray(params, dtype); intr = np.ascontiguousarray(intr, dtype); emb = np.ascontiguousarray(emb, dtype)
+    H, W, d_f = feat.shape
+    gp, grgb, gf, ge = np.zeros(DEC_PARAMS, dtype), np.zeros((H, W, 3), dtype), np.zeros((H, W, d_f), dtype), np.zeros(8, dtype)
+    getattr(L, f"orc_decoder_backward_{suf}")(_p(params), C.c_int(H), C.c_int(W), C.c_int(d_f), _p(rgb), _p(feat), _p(intr),
+                                              _p(emb), _p(g_image), _p(gp), _p(grgb), _p(gf), _p(ge))
+    return gp, grgb, gf, ge
+
+
 def detmath_eval(fn, x, y=None):
     x = np.ascontiguousarray(x, np.float32)
     y = np.zeros_like(x) if y is None else np.ascontiguousarray(y, np.float32)

@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_optimizer_step_range", "splatb200_grads_nonfinite_range", "splatb200_scene_download", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_optimizer_step_range", "splatb200_grads_nonfinite_range", "splatb200_scene_download", "splatb200_conv_decoder_params", "splatb200_view_decode_image", "splatb200_debug_conv3x3", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -109,6 +109,10 @@ def lib():
         L.splatb200_grads_nonfinite_range.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
         L.splatb200_scene_download.argtypes = [C.c_void_p] * 7
         L.splatb200_lidar_head_params.argtypes = [C.c_int32]
+        L.splatb200_conv_decoder_params.argtypes = []
+        L.splatb200_conv_decoder_params.restype = C.c_int32
+        L.splatb200_view_decode_image.argtypes = [C.c_void_p] * 5
+        L.splatb200_debug_conv3x3.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.splatb200_view_set_lidar_head.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_lidar_head_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_lidar_head_backward.argtypes = [C.c_void_p] * 5
@@ -309,6 +313,17 @@ class Context:
         self._check(self.L.splatb200_debug_depth_sort(self.h, n, _p(keys), _p(counts), _p(order), _p(offsets)))
         return order, offsets
 
+    def debug_conv3x3(self, x, w, relu_in=False, res=None):
+        """Test hook: one 3x3, 32 -> 32 reflect-padded convolution of the ConvDecoder (tensor cores) on host arrays."""
+        x = np.ascontiguousarray(x, np.float32)
+        w = np.ascontiguousarray(w, np.float32)
+        H, W, ch = x.shape
+        assert ch == 32 and w.size == 9248
+        r = None if res is None else np.ascontiguousarray(res, np.float32)
+        y = np.zeros_like(x)
+        self._check(self.L.splatb200_debug_conv3x3(self.h, _p(x), H, W, _p(w), int(relu_in), _p(r), _p(y)))
+        return y
+
     def set_view_streams(self, on: bool):
         """Views run forward / backward on their own streams (sensors overlap); see splat_b200.h."""
         self._check(self.L.splatb200_ctx_set_view_streams(self.h, int(on)))
@@ -434,6 +449,18 @@ class View:
             self.close()
         except Exception:
             pass
+
+    def decode_image(self, params, embedding, download=True, timed=False):
+        """decode_image: the ConvDecoder over this camera view's blended features -> H*W x 3 image
+        (None with download=False: read array("decoded")). timed=True also returns the device time in ms."""
+        w = np.ascontiguousarray(params, np.float32)
+        e = np.ascontiguousarray(embedding, np.float32)
+        assert w.size == self.L.splatb200_conv_decoder_params() and e.size == 8
+        img = np.zeros((self.P, 3), np.float32) if download else None
+        ms = C.c_float(0)
+        self.ctx._check(self.L.splatb200_view_decode_image(self.h, _p(w), _p(e), _p(img) if download else None,
+                                                           C.byref(ms) if timed else None))
+        return (img, ms.value) if timed else img
 
     def set_lidar_head(self, weights):
         """Fused lidar head: every forward also decodes the blended features (array("lidar_head"): P x 2); None: off."""

@@ -124,6 +124,9 @@ struct splatb200_view {
   int64_t P_cap = 0;   // queries the per-query buffers are sized for (lidar sweeps change size: view_set_rays)
   float *d_los_cut = nullptr, *d_los = nullptr, *d_g_los = nullptr;  // line-of-sight channel (lidar, optional)
   float *d_head_w = nullptr, *d_head_y = nullptr;                     // fused lidar head (optional)
+  float* dec_buf[3] = {nullptr, nullptr, nullptr};                    // ConvDecoder activations, P x 32 each (lazy)
+  float *d_dec_image = nullptr, *d_dec_params = nullptr;              // decoded image P x 3; parameters + embedding
+  int* d_dec_err = nullptr;
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
   int64_t *ray_begin = nullptr, *ray_end = nullptr;
   uint32_t* tile_order = nullptr;  // CTA -> tile permutation (longest worklists first), rebuilt every forward
@@ -248,7 +251,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); dfree(v->dec_buf[0]); dfree(v->dec_buf[1]); dfree(v->dec_buf[2]); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -1029,6 +1032,81 @@ extern "C" int splatb200_lidar_head_backward(splatb200_view* v, const float* wei
   c->launches += v->P > 0;
   CU_TRY(c, cudaMemcpyAsync(g_weights, dgw.p, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return SPLATB200_OK;
+}
+
+// ---- camera ConvDecoder -------------------------------------------------------------------
+extern "C" int32_t splatb200_conv_decoder_params(void) { return conv_decoder_params(); }
+
+extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* params, const float* embedding, float* image,
+                                           float* device_ms) {
+  splatb200_ctx* c = v->ctx;
+  if (!v->s.is_camera) return c->fail(SPLATB200_EINVAL, "decode_image decodes a camera view");
+  if (!params || !embedding) return c->fail(SPLATB200_EINVAL, "null argument");
+  if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "decode_image before forward");
+  if (c->d_f + 11 > 32) return c->fail(SPLATB200_EINVAL, "decode_image: d_f + 3 + 8 input channels must fit the width of 32");
+  if (v->s.width < 2 || v->s.height < 2) return c->fail(SPLATB200_EINVAL, "decode_image: reflect padding needs a 2 x 2 image");
+  join_view(v);
+  const int np = conv_decoder_params();
+  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  for (int k = 0; k < 3; ++k)
+    if (!v->dec_buf[k]) CU_TRY(c, cudaMalloc(&v->dec_buf[k], sizeof(float) * 32 * P));
+  if (!v->d_dec_image) CU_TRY(c, cudaMalloc(&v->d_dec_image, sizeof(float) * 3 * P));
+  if (!v->d_dec_params) CU_TRY(c, cudaMalloc(&v->d_dec_params, sizeof(float) * (np + 8 + 2)));
+  if (!v->d_dec_err) CU_TRY(c, cudaMalloc(&v->d_dec_err, sizeof(int)));
+  float* d_emb = v->d_dec_params + ((np + 3) & ~3);
+  CU_TRY(c, cudaMemcpyAsync(v->d_dec_params, params, sizeof(float) * np, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(d_emb, embedding, sizeof(float) * 8, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemsetAsync(v->d_dec_err, 0, sizeof(int), c->stream));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (device_ms) {
+    CU_TRY(c, cudaEventCreate(&e0));
+    CU_TRY(c, cudaEventCreate(&e1));
+    CU_TRY(c, cudaEventRecord(e0, c->stream));
+  }
+  const int launched = launch_conv_decoder(v->d_dec_params, d_emb, v->s.height, v->s.width, c->d_f, v->s.fx, v->s.fy, v->s.cx,
+                                           v->s.cy, v->out.blend, v->s.channels, v->dec_buf[0], v->dec_buf[1], v->dec_buf[2],
+                                           v->d_dec_image, v->d_dec_err, c->stream);
+  CHECK_LAUNCH(c, "k_conv3x3_tc");
+  c->launches += launched;
+  if (device_ms) CU_TRY(c, cudaEventRecord(e1, c->stream));
+  int err = 0;
+  CU_TRY(c, cudaMemcpyAsync(&err, v->d_dec_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (image && v->P) CU_TRY(c, cudaMemcpyAsync(image, v->d_dec_image, sizeof(float) * 3 * (size_t)v->P, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (device_ms) {
+    CU_TRY(c, cudaEventElapsedTime(device_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (err) return c->fail(SPLATB200_ERUNTIME, "decode_image: tensor-core completion barrier timed out");
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_debug_conv3x3(splatb200_ctx* c, const float* x, int32_t H, int32_t W, const float* w, int32_t relu_in,
+                                       const float* res, float* y) {
+  if (!x || !w || !y || H < 2 || W < 2) return c->fail(SPLATB200_EINVAL, "bad argument");
+  join_all(c);
+  const size_t n = (size_t)H * W * 32;
+  DevScratch dx, dw, dr, dy, de;
+  CU_TRY(c, cudaMalloc(&dx.p, sizeof(float) * n));
+  CU_TRY(c, cudaMalloc(&dy.p, sizeof(float) * n));
+  CU_TRY(c, cudaMalloc(&dw.p, sizeof(float) * 9248));
+  CU_TRY(c, cudaMalloc(&de.p, sizeof(int)));
+  if (res) CU_TRY(c, cudaMalloc(&dr.p, sizeof(float) * n));
+  CU_TRY(c, cudaMemcpyAsync(dx.p, x, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(dw.p, w, sizeof(float) * 9248, cudaMemcpyHostToDevice, c->stream));
+  if (res) CU_TRY(c, cudaMemcpyAsync(dr.p, res, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemsetAsync(de.p, 0, sizeof(int), c->stream));
+  CU_TRY(c, cudaMemsetAsync(dy.p, 0, sizeof(float) * n, c->stream));
+  launch_conv3x3((const float*)dx.p, H, W, (const float*)dw.p, relu_in, (const float*)dr.p, (float*)dy.p, (int*)de.p, c->stream);
+  CHECK_LAUNCH(c, "k_conv3x3_tc");
+  c->launches += 1;
+  int err = 0;
+  CU_TRY(c, cudaMemcpyAsync(&err, de.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(y, dy.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (err) return c->fail(SPLATB200_ERUNTIME, "conv3x3: tensor-core completion barrier timed out");
   return SPLATB200_OK;
 }
 
@@ -1977,6 +2055,7 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   else if (name == "range_blend") src = v->out.range_blend;
   else if (name == "los") src = v->out.los;
   else if (name == "lidar_head") { src = v->out.head_y; cnt = 2 * P; }
+  else if (name == "decoded") { src = v->d_dec_image; cnt = 3 * P; }
   if (!src) return c->fail(SPLATB200_EINVAL, "unknown array name " + name);
   if (dst && cnt) {
     CU_TRY(c, cudaMemcpyAsync(dst, src, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream));

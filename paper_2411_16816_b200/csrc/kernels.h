@@ -76,6 +76,16 @@ void launch_lidar_head_fwd(const float* w, int d_f, int64_t n_rays, const float4
 void launch_lidar_head_bwd(const float* w, int d_f, int64_t n_rays, const float4* rays, const float* blend16, const float* g_y,
                            float* g_blend16, float* g_w, cudaStream_t st);
 
+// conv_decoder.cu (decode_image): the camera ConvDecoder on the tensor cores (tcgen05, tf32)
+int conv_decoder_params();
+// y = conv3x3(relu_in ? relu(x) : x; w[9216] + bias[32], reflect padding) (+ res); x, y, res: H x W x 32
+void launch_conv3x3(const float* x, int H, int W, const float* w, int relu_in, const float* res, float* y, int* err,
+                    cudaStream_t st);
+// blend (P x blend_stride: rgb, features) -> image P x 3; buf_a/b/c: P x 32 scratch each. Returns the launch count.
+int launch_conv_decoder(const float* params, const float* emb, int H, int W, int d_f, float fx, float fy, float cx, float cy,
+                        const float* blend, int blend_stride, float* buf_a, float* buf_b, float* buf_c, float* image,
+                        int* err, cudaStream_t st);
+
 // assign.cu (assign_points_to_tiles): per-point tile key (0xffffffff = rejected), (phi, omega, t_l, range),
 // shuffle hash, valid flag
 void launch_assign_points(const Sensor& s, float timestamp, int64_t n, const float* xyz, const float* stamps, uint32_t seed,

@@ -1038,3 +1038,97 @@ def test_optimizer_step_range_and_sharded_path(api, op):
     for a, b, d in zip(full, two, sh1):
         assert np.array_equal(a, b) and np.array_equal(a, d)
     assert np.array_equal(skipq[2], np.asarray(sc.quat, np.float32)) and np.array_equal(skipq[0], full[0])
+
+
+# ---- camera ConvDecoder: tcgen05 / tf32 implicit-GEMM convolutions -----------------------
+# tf32 operands (10-bit mantissa, rounded to nearest) with fp32 accumulation: 2^-11 relative per operand; over five
+# layers the image agrees with the fp32 oracle to DEC_RTOL of the output scale.
+DEC_RTOL = 3e-3
+
+
+def _conv3x3_numpy(x, w, relu_in, res):
+    H, W, _ = x.shape
+    k = w[:9216].reshape(32, 3, 3, 32).astype(np.float64)
+    xin = np.maximum(x, 0) if relu_in else x
+    xp = np.pad(xin.astype(np.float64), ((1, 1), (1, 1), (0, 0)), mode="reflect")
+    y = np.zeros((H, W, 32)) + w[9216:].astype(np.float64)
+    for ky in range(3):
+        for kx in range(3):
+            y += xp[ky:ky + H, kx:kx + W, :] @ k[:, ky, kx, :].T
+    return y + (0 if res is None else res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("H,W", [(2, 2), (5, 131), (8, 128), (33, 300), (64, 640)])
+def test_conv3x3_tensor_core_matches_numpy(ctx, H, W):
+    """One decoder convolution (partial tiles in both directions, reflect padding, ReLU on the input, residual) against
+    a float64 numpy evaluation, and bit-exactly on small integers (exact in tf32)."""
+    rng = np.random.default_rng(H * 1000 + W)
+    x = rng.normal(0, 1, (H, W, 32)).astype(np.float32)
+    w = rng.normal(0, 0.1, 9248).astype(np.float32)
+    res = rng.normal(0, 1, (H, W, 32)).astype(np.float32)
+    for relu_in, r in ((False, None), (True, res)):
+        y = ctx.debug_conv3x3(x, w, relu_in, r)
+        ref = _conv3x3_numpy(x, w, relu_in, r)
+        assert np.abs(y - ref).max() <= 2e-3 * np.abs(ref).max(), (relu_in, np.abs(y - ref).max(), np.abs(ref).max())
+    # integers up to 2^10 are exact in tf32: bit-exact convolution
+    xi = rng.integers(-8, 9, (H, W, 32)).astype(np.float32)
+    wi = rng.integers(-4, 5, 9248).astype(np.float32)
+    assert np.array_equal(ctx.debug_conv3x3(xi, wi), _conv3x3_numpy(xi, wi, False, None).astype(np.float32))
+
+
+def _decoder_inputs(view, cam, d_f):
+    blend = view.array("blend").reshape(cam.height, cam.width, 3 + d_f)
+    return blend[..., :3], blend[..., 3:], np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float32)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,h", [(320, 192), (203, 77)])
+def test_decode_image_matches_oracle(ctx, op, w, h):
+    sc = synth.make_scene(6000, seed=21, r_max=40.0, scale_mean=0.12)
+    cam = synth.make_camera(width=w, height=h)
+    ctx.upload_scene(sc)
+    view = ctx.camera_view(cam, ST)
+    view.forward(0.0)
+    rgb, feat, intr = _decoder_inputs(view, cam, sc.d_f)
+    rng = np.random.default_rng(5)
+    params = rng.normal(0, 0.08, op.DEC_PARAMS).astype(np.float32)
+    params[op.DEC_HEAD_OFFSET:] = rng.normal(0, 0.3, op.DEC_PARAMS - op.DEC_HEAD_OFFSET)
+    emb = rng.normal(0, 1, 8).astype(np.float32)
+    img = view.decode_image(params, emb).reshape(h, w, 3)
+    ref = op.decoder_forward(params, rgb, feat, intr, emb, np.float32, workers=8)
+    assert np.abs(img - ref).max() <= DEC_RTOL * max(1.0, np.abs(ref).max()), np.abs(img - ref).max()
+    assert np.array_equal(view.array("decoded").reshape(h, w, 3), img)
+    # SPEC.md:374: zero-initialised head -> the decoder is the identity, exactly
+    p0 = params.copy(); p0[op.DEC_HEAD_OFFSET:] = 0
+    assert np.array_equal(view.decode_image(p0, emb).reshape(h, w, 3), rgb)
+    # SPEC.md:375: forced M = 2, b = 0.1
+    p0[-6:] = [1, 1, 1, 0.1, 0.1, 0.1]
+    assert np.allclose(view.decode_image(p0, emb).reshape(h, w, 3), 2 * rgb + np.float32(0.1), rtol=0, atol=1e-6)
+    # a lidar view has no image to decode
+    lv = ctx.lidar_view(synth.lidar32(), synth.grid_rays(synth.lidar32()), ST)
+    lv.forward(0.0)
+    with pytest.raises(Exception):
+        lv.decode_image(params, emb)
+
+
+@pytest.mark.gpu
+def test_decode_image_full_size_1080p(ctx, op):
+    """The north-star camera (1920 x 1080): parity with the threaded fp32 oracle, run-to-run determinism, device time."""
+    sc = synth.make_scene(200_000, seed=22)
+    cam = synth.make_camera()
+    ctx.upload_scene(sc)
+    view = ctx.camera_view(cam, ST)
+    view.forward(0.0)
+    rgb, feat, intr = _decoder_inputs(view, cam, sc.d_f)
+    rng = np.random.default_rng(6)
+    params = rng.normal(0, 0.08, op.DEC_PARAMS).astype(np.float32)
+    params[op.DEC_HEAD_OFFSET:] = rng.normal(0, 0.3, op.DEC_PARAMS - op.DEC_HEAD_OFFSET)
+    emb = rng.normal(0, 1, 8).astype(np.float32)
+    img, _ = view.decode_image(params, emb, timed=True)
+    times = [view.decode_image(params, emb, download=False, timed=True)[1] for _ in range(5)]
+    assert np.array_equal(view.array("decoded").reshape(-1, 3), img)
+    ref = op.decoder_forward(params, rgb, feat, intr, emb, np.float32, workers=16)
+    err = np.abs(img.reshape(ref.shape) - ref).max()
+    print(f"decode_image 1920x1080: {min(times):.3f} ms on the device, max |err| {err:.2e} (scale {np.abs(ref).max():.2f})")
+    assert err <= DEC_RTOL * max(1.0, np.abs(ref).max())

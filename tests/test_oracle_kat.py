@@ -845,3 +845,81 @@ def test_optimizer_step_examples():
     before = [x.copy() for x in p]
     assert op.adam_step(p, g, m, v, cfg, 1) == [2]
     assert np.array_equal(p[2], before[2]) and not np.array_equal(p[0], before[0])
+
+
+# ---- decode_image / ConvDecoder -----------------------------------------------------
+def _decoder_case(seed, H=8, W=8, d_f=13, head_scale=0.3):
+    rng = np.random.default_rng(seed)
+    params = rng.normal(0, 0.08, op.DEC_PARAMS)
+    params[op.DEC_HEAD_OFFSET:] = rng.normal(0, head_scale, op.DEC_PARAMS - op.DEC_HEAD_OFFSET)
+    rgb = rng.uniform(0, 1, (H, W, 3))
+    feat = rng.normal(0, 1, (H, W, d_f))
+    intr = np.array([20.0, 21.0, W / 2 + 0.3, H / 2 - 0.2])
+    emb = rng.normal(0, 1, 8)
+    return params, rgb, feat, intr, emb
+
+
+def test_decoder_spec_examples(oracle_lib):
+    params, rgb, feat, intr, emb = _decoder_case(0)
+    # zero-initialised head -> M = 1, b = 0 -> I = F_rgb
+    p0 = params.copy(); p0[op.DEC_HEAD_OFFSET:] = 0
+    assert np.array_equal(op.decoder_forward(p0, rgb, feat, intr, emb, np.float64), rgb)
+    # forced M = 2, b = 0.1 (head weights zero, bias (1,1,1,.1,.1,.1)) -> I = 2 F_rgb + 0.1
+    p0[-6:] = [1, 1, 1, 0.1, 0.1, 0.1]
+    assert np.allclose(op.decoder_forward(p0, rgb, feat, intr, emb, np.float64), 2 * rgb + 0.1, atol=1e-15)
+    # fp32 instantiation agrees with fp64
+    a = op.decoder_forward(params, rgb, feat, intr, emb, np.float64)
+    b = op.decoder_forward(params, rgb, feat, intr, emb, np.float32)
+    assert np.abs(a - b).max() < 1e-4 * max(1.0, np.abs(a).max())
+
+
+def test_decoder_gradients_match_finite_differences(oracle_lib):
+    """all decoder gradients match finite differences on an 8 x 8 input, rel err <= 1e-3 (64-bit)."""
+    params, rgb, feat, intr, emb = _decoder_case(1)
+    rng = np.random.default_rng(2)
+    g_image = rng.normal(0, 1, rgb.shape)
+    gp, grgb, gf, ge = op.decoder_backward(params, rgb, feat, intr, emb, g_image)
+
+    def loss(p=params, r=rgb, f=feat, e=emb):
+        return float((op.decoder_forward(p, r, f, intr, e, np.float64) * g_image).sum())
+
+    def fd(arr, idx, h=1e-6):
+        a = arr.copy(); a.flat[idx] += h
+        b = arr.copy(); b.flat[idx] -= h
+        return a, b, 2 * h
+
+    scale = np.abs(gp).max()
+    # every weight tensor: 3 random entries of each conv's weights and bias, the head weights and bias
+    probes = []
+    for l in range(op.DEC_CONVS):
+        base = l * op.DEC_CONV_PARAMS
+        probes += list(base + rng.integers(0, 9216, 3)) + [base + 9216 + int(rng.integers(0, 32))]
+    probes += list(op.DEC_HEAD_OFFSET + rng.integers(0, 192, 3)) + [op.DEC_PARAMS - 6 + int(rng.integers(0, 6))]
+    for k in probes:
+        a, b, d = fd(params, k)
+        num = (loss(p=a) - loss(p=b)) / d
+        assert abs(num - gp[k]) <= 1e-3 * max(abs(num), 1e-3 * scale), (k, num, gp[k])
+    for k in rng.integers(0, rgb.size, 4):
+        a, b, d = fd(rgb, k)
+        num = (loss(r=a) - loss(r=b)) / d
+        assert abs(num - grgb.flat[k]) <= 1e-3 * max(abs(num), 1e-6)
+    for k in rng.integers(0, feat.size, 6):
+        a, b, d = fd(feat, k)
+        num = (loss(f=a) - loss(f=b)) / d
+        assert abs(num - gf.flat[k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(gf).max())
+    for k in range(8):
+        a, b, d = fd(emb, k)
+        num = (loss(e=a) - loss(e=b)) / d
+        assert abs(num - ge[k]) <= 1e-3 * max(abs(num), 1e-3 * np.abs(ge).max())
+
+
+def test_decoder_translation_equivariance(oracle_lib):
+    """shifting the trunk input by one pixel shifts the interior output by one pixel. The ray-direction
+    channels depend on the pixel, so the shift is applied with the principal point moved by the same pixel."""
+    params, rgb, feat, intr, emb = _decoder_case(3, H=12, W=14)
+    a = op.decoder_forward(params, rgb, feat, intr, emb, np.float64)
+    rgb_s, feat_s = np.roll(rgb, 1, axis=1), np.roll(feat, 1, axis=1)
+    intr_s = intr.copy(); intr_s[2] += 1.0
+    b = op.decoder_forward(params, rgb_s, feat_s, intr_s, emb, np.float64)
+    # five 3x3 layers: the receptive field reaches 5 px, so compare columns 6 .. W-6
+    assert np.allclose(b[:, 7:-5], a[:, 6:-6], atol=1e-12)
