@@ -284,10 +284,23 @@ int splatb200_lidar_head_backward(splatb200_view* v, const float* weights, const
 int32_t splatb200_conv_decoder_params(void);
 int splatb200_view_decode_image(splatb200_view* v, const float* params, const float* embedding, float* image,
                                 float* device_ms);
+/* Backward of the decode ("Includes their backward passes"; gradient example SPEC.md:376). Needs the state
+ * saved by the splatb200_view_decode_image call that followed the view's last forward (else SPLATB200_ERUNTIME, like
+ * the rasterizer's backward without saved state). g_image: HOST, P x 3 = dL/dI. g_params: HOST,
+ * splatb200_conv_decoder_params() floats, OVERWRITTEN with dL/dparams; g_embedding: HOST, 8 floats, overwritten
+ * (SensorGrads::d_embedding, projection.hpp:207-222). g_blend: DEVICE, P x (3 + d_f) — dL/dF_rgb and dL/dfeature are
+ * ADDED to it, so the buffer goes straight into splatb200_view_backward_device as the upstream gradient of the render.
+ * Weight gradients and input gradients of the five convolutions run on the tensor cores as well. */
+int splatb200_view_decode_image_backward(splatb200_view* v, const float* g_image, float* g_params, float* g_embedding,
+                                         float* g_blend, float* device_ms);
 /* test hook: one 3x3, 32 -> 32 convolution of the decoder on HOST arrays (x, y, res: H x W x 32 pixel-interleaved;
  * w: 9216 weights + 32 bias; res may be NULL). */
 int splatb200_debug_conv3x3(splatb200_ctx* ctx, const float* x, int32_t H, int32_t W, const float* w, int32_t relu_in,
                             const float* res, float* y);
+/* test hook: its gradients. g_y: H x W x 32 -> g_x (H x W x 32, masked by the ReLU of the input when relu_in),
+ * g_w (9216 + 32, overwritten). */
+int splatb200_debug_conv3x3_backward(splatb200_ctx* ctx, const float* x, int32_t H, int32_t W, const float* w,
+                                     int32_t relu_in, const float* g_y, float* g_x, float* g_w);
 
 /* ---- lidar returns -> rasterization points (SPEC.md:230-238 assign_points_to_tiles) ----
  * The producer of splatb200_view_create_lidar's `rays`. points_xyz: n x 3 world coordinates (ego-motion compensated),

@@ -578,7 +578,28 @@ ORC_API(f64, double)
     decoder_backward<S>(params, st, rgb, g_image, g_params, g_rgb, g_feat, g_emb);                                       \
   }
 ORC_DECODER(f32, float)
+// backward of the decode from SAVED activations (x0, h0, t1, h1, t2, h2: P x 32 each, e.g. those of the device path):
+// the ReLU masks then are those of the forward that actually ran
+extern "C" void orc_decoder_backward_state_f64(const double* params, int H, int W, int d_f, const double* rgb,
+                                               const double* acts, const double* g_image, double* g_params, double* g_rgb,
+                                               double* g_feat, double* g_emb) {
+  DecoderState<double> st;
+  st.H = H; st.W = W; st.d_f = d_f;
+  const size_t n = (size_t)H * W * kDecWidth;
+  std::vector<double>* dst[6] = {&st.x0, &st.h0, &st.t1, &st.h1, &st.t2, &st.h2};
+  for (int k = 0; k < 6; ++k) dst[k]->assign(acts + k * n, acts + (k + 1) * n);
+  decoder_backward<double>(params, st, rgb, g_image, g_params, g_rgb, g_feat, g_emb);
+}
 ORC_DECODER(f64, double)
+extern "C" void orc_decoder_activations_f64(const double* params, int H, int W, int d_f, const double* rgb, const double* feat,
+                                            const double* intr, const double* emb, double* acts) {
+  DecoderState<double> st;
+  std::vector<double> image((size_t)H * W * 3);
+  decoder_forward<double>(params, H, W, d_f, rgb, feat, intr, emb, image.data(), &st);
+  const size_t n = (size_t)H * W * kDecWidth;
+  const std::vector<double>* src[6] = {&st.x0, &st.h0, &st.t1, &st.h1, &st.t2, &st.h2};
+  for (int k = 0; k < 6; ++k) std::copy(src[k]->begin(), src[k]->end(), acts + k * n);
+}
 extern "C" int orc_decoder_params() { return kDecParams; }
 
 // detmath bit-pattern probes (host build of the header the kernels use)

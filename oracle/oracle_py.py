@@ -287,6 +287,20 @@ def decoder_backward(params, rgb, feat, intr, emb, g_image, dtype=np.float64):
     return gp, grgb, gf, ge
 
 
+def decoder_backward_from_state(params, rgb, acts, d_f, g_image):
+    """Backward of decode_image from saved activations (6 x H x W x 32: x0, h0, t1, h1, t2, h2), fp64: the ReLU masks
+    are those of the forward that produced `acts`. -> (dL/dparams, dL/drgb, dL/dfeat, dL/demb)"""
+    L, dtype = lib(), np.float64
+    rgb = np.ascontiguousarray(rgb, dtype); acts = np.ascontiguousarray(acts, dtype); g_image = np.ascontiguousarray(g_image, dtype)
+    params = np.ascontiguousarray(params, dtype)
+    H, W, _ = rgb.shape
+    assert acts.shape == (6, H, W, DEC_WIDTH)
+    gp, grgb, gf, ge = np.zeros(DEC_PARAMS, dtype), np.zeros((H, W, 3), dtype), np.zeros((H, W, d_f), dtype), np.zeros(8, dtype)
+    L.orc_decoder_backward_state_f64(_p(params), C.c_int(H), C.c_int(W), C.c_int(d_f), _p(rgb), _p(acts), _p(g_image), _p(gp),
+                                     _p(grgb), _p(gf), _p(ge))
+    return gp, grgb, gf, ge
+
+
 def detmath_eval(fn, x, y=None):
     x = np.ascontiguousarray(x, np.float32)
     y = np.zeros_like(x) if y is None else np.ascontiguousarray(y, np.float32)

@@ -32,7 +32,7 @@ SYMBOLS = [
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
-    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_optimizer_step_range", "splatb200_grads_nonfinite_range", "splatb200_scene_download", "splatb200_conv_decoder_params", "splatb200_view_decode_image", "splatb200_debug_conv3x3", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
+    "splatb200_view_destroy", "splatb200_view_set_camera", "splatb200_view_set_lidar_pose", "splatb200_view_set_rays", "splatb200_optimizer_step", "splatb200_optimizer_step_range", "splatb200_grads_nonfinite_range", "splatb200_scene_download", "splatb200_conv_decoder_params", "splatb200_view_decode_image", "splatb200_debug_conv3x3", "splatb200_view_decode_image_backward", "splatb200_debug_conv3x3_backward", "splatb200_lidar_head_params", "splatb200_view_set_lidar_head", "splatb200_lidar_head_forward", "splatb200_lidar_head_backward", "splatb200_view_set_los", "splatb200_view_set_los_grad", "splatb200_lidar_grid",
     "splatb200_view_forward", "splatb200_view_stats_get", "splatb200_view_blend", "splatb200_view_alpha",
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
@@ -112,6 +112,8 @@ def lib():
         L.splatb200_conv_decoder_params.argtypes = []
         L.splatb200_conv_decoder_params.restype = C.c_int32
         L.splatb200_view_decode_image.argtypes = [C.c_void_p] * 5
+        L.splatb200_view_decode_image_backward.argtypes = [C.c_void_p] * 6
+        L.splatb200_debug_conv3x3_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_debug_conv3x3.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.splatb200_view_set_lidar_head.argtypes = [C.c_void_p, C.c_void_p]
         L.splatb200_lidar_head_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -324,6 +326,14 @@ class Context:
         self._check(self.L.splatb200_debug_conv3x3(self.h, _p(x), H, W, _p(w), int(relu_in), _p(r), _p(y)))
         return y
 
+    def debug_conv3x3_backward(self, x, w, g_y, relu_in=False):
+        """Test hook: (g_x, g_w) of one decoder convolution (tensor cores) on host arrays."""
+        x = np.ascontiguousarray(x, np.float32); w = np.ascontiguousarray(w, np.float32); g_y = np.ascontiguousarray(g_y, np.float32)
+        H, W, _ = x.shape
+        gx, gw = np.zeros_like(x), np.zeros(9248, np.float32)
+        self._check(self.L.splatb200_debug_conv3x3_backward(self.h, _p(x), H, W, _p(w), int(relu_in), _p(g_y), _p(gx), _p(gw)))
+        return gx, gw
+
     def set_view_streams(self, on: bool):
         """Views run forward / backward on their own streams (sensors overlap); see splat_b200.h."""
         self._check(self.L.splatb200_ctx_set_view_streams(self.h, int(on)))
@@ -461,6 +471,18 @@ class View:
         self.ctx._check(self.L.splatb200_view_decode_image(self.h, _p(w), _p(e), _p(img) if download else None,
                                                            C.byref(ms) if timed else None))
         return (img, ms.value) if timed else img
+
+    def decode_image_backward(self, g_image, g_blend_device_ptr: int, timed=False):
+        """Backward of decode_image: dL/dimage (P x 3) -> (dL/dparams, dL/dembedding[8]); dL/dF_rgb and dL/dfeature are
+        added to the DEVICE buffer (P x (3 + d_f)) at g_blend_device_ptr — the upstream gradient of view.backward_device."""
+        g = np.ascontiguousarray(g_image, np.float32)
+        assert g.size == 3 * self.P
+        gp = np.zeros(self.L.splatb200_conv_decoder_params(), np.float32)
+        ge = np.zeros(8, np.float32)
+        ms = C.c_float(0)
+        self.ctx._check(self.L.splatb200_view_decode_image_backward(self.h, _p(g), _p(gp), _p(ge), C.c_void_p(g_blend_device_ptr),
+                                                                    C.byref(ms) if timed else None))
+        return (gp, ge, ms.value) if timed else (gp, ge)
 
     def set_lidar_head(self, weights):
         """Fused lidar head: every forward also decodes the blended features (array("lidar_head"): P x 2); None: off."""

@@ -124,7 +124,10 @@ struct splatb200_view {
   int64_t P_cap = 0;   // queries the per-query buffers are sized for (lidar sweeps change size: view_set_rays)
   float *d_los_cut = nullptr, *d_los = nullptr, *d_g_los = nullptr;  // line-of-sight channel (lidar, optional)
   float *d_head_w = nullptr, *d_head_y = nullptr;                     // fused lidar head (optional)
-  float* dec_buf[3] = {nullptr, nullptr, nullptr};                    // ConvDecoder activations, P x 32 each (lazy)
+  float* dec_act[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // ConvDecoder activations x0 h0 t1 h1 t2 h2 (lazy)
+  float* dec_g[3] = {nullptr, nullptr, nullptr};                      // backward scratch, P x 32 each
+  float *dec_gext = nullptr, *d_dec_gimage = nullptr, *d_dec_gparams = nullptr;  // (H+2)(W+2) x 32; P x 3; params + 8
+  bool dec_ready = false;                                             // activations match the last forward + decode
   float *d_dec_image = nullptr, *d_dec_params = nullptr;              // decoded image P x 3; parameters + embedding
   int* d_dec_err = nullptr;
   float4* rays = nullptr;  // per ray POSITION: azimuth, elevation, t_l, bits of the original ray index (see create_lidar)
@@ -251,7 +254,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); dfree(v->dec_buf[0]); dfree(v->dec_buf[1]); dfree(v->dec_buf[2]); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); for (auto*& b : v->dec_act) dfree(b); for (auto*& b : v->dec_g) dfree(b); dfree(v->dec_gext); dfree(v->d_dec_gimage); dfree(v->d_dec_gparams); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -1049,10 +1052,10 @@ extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* param
   join_view(v);
   const int np = conv_decoder_params();
   const size_t P = (size_t)std::max<int64_t>(1, v->P);
-  for (int k = 0; k < 3; ++k)
-    if (!v->dec_buf[k]) CU_TRY(c, cudaMalloc(&v->dec_buf[k], sizeof(float) * 32 * P));
+  for (int k = 0; k < 6; ++k)
+    if (!v->dec_act[k]) CU_TRY(c, cudaMalloc(&v->dec_act[k], sizeof(float) * 32 * P));
   if (!v->d_dec_image) CU_TRY(c, cudaMalloc(&v->d_dec_image, sizeof(float) * 3 * P));
-  if (!v->d_dec_params) CU_TRY(c, cudaMalloc(&v->d_dec_params, sizeof(float) * (np + 8 + 2)));
+  if (!v->d_dec_params) CU_TRY(c, cudaMalloc(&v->d_dec_params, sizeof(float) * (2 * 9248 + np + 8 + 2)));
   if (!v->d_dec_err) CU_TRY(c, cudaMalloc(&v->d_dec_err, sizeof(int)));
   float* d_emb = v->d_dec_params + ((np + 3) & ~3);
   CU_TRY(c, cudaMemcpyAsync(v->d_dec_params, params, sizeof(float) * np, cudaMemcpyHostToDevice, c->stream));
@@ -1065,8 +1068,8 @@ extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* param
     CU_TRY(c, cudaEventRecord(e0, c->stream));
   }
   const int launched = launch_conv_decoder(v->d_dec_params, d_emb, v->s.height, v->s.width, c->d_f, v->s.fx, v->s.fy, v->s.cx,
-                                           v->s.cy, v->out.blend, v->s.channels, v->dec_buf[0], v->dec_buf[1], v->dec_buf[2],
-                                           v->d_dec_image, v->d_dec_err, c->stream);
+                                           v->s.cy, v->out.blend, v->s.channels, v->dec_act, v->d_dec_image, v->d_dec_err,
+                                           c->stream);
   CHECK_LAUNCH(c, "k_conv3x3_tc");
   c->launches += launched;
   if (device_ms) CU_TRY(c, cudaEventRecord(e1, c->stream));
@@ -1080,6 +1083,83 @@ extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* param
     cudaEventDestroy(e1);
   }
   if (err) return c->fail(SPLATB200_ERUNTIME, "decode_image: tensor-core completion barrier timed out");
+  v->dec_ready = true;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_view_decode_image_backward(splatb200_view* v, const float* g_image, float* g_params,
+                                                    float* g_embedding, float* g_blend, float* device_ms) {
+  splatb200_ctx* c = v->ctx;
+  if (!v->s.is_camera) return c->fail(SPLATB200_EINVAL, "decode_image decodes a camera view");
+  if (!g_image || !g_params || !g_embedding || !g_blend) return c->fail(SPLATB200_EINVAL, "null argument");
+  if (!v->dec_ready || v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "decode_image backward without saved state");
+  join_view(v);
+  const int np = conv_decoder_params();
+  const int H = v->s.height, W = v->s.width;
+  const size_t P = (size_t)std::max<int64_t>(1, v->P);
+  for (int k = 0; k < 3; ++k)
+    if (!v->dec_g[k]) CU_TRY(c, cudaMalloc(&v->dec_g[k], sizeof(float) * 32 * P));
+  if (!v->dec_gext) CU_TRY(c, cudaMalloc(&v->dec_gext, sizeof(float) * 32 * (size_t)(H + 2) * (W + 2)));
+  if (!v->d_dec_gimage) CU_TRY(c, cudaMalloc(&v->d_dec_gimage, sizeof(float) * 3 * P));
+  if (!v->d_dec_gparams) CU_TRY(c, cudaMalloc(&v->d_dec_gparams, sizeof(float) * (np + 8)));
+  float* d_wt = v->d_dec_params + ((np + 3) & ~3) + 8;   // scratch behind the parameters and the embedding
+  CU_TRY(c, cudaMemcpyAsync(v->d_dec_gimage, g_image, sizeof(float) * 3 * (size_t)v->P, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemsetAsync(v->d_dec_gparams, 0, sizeof(float) * (np + 8), c->stream));
+  CU_TRY(c, cudaMemsetAsync(v->d_dec_err, 0, sizeof(int), c->stream));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (device_ms) {
+    CU_TRY(c, cudaEventCreate(&e0));
+    CU_TRY(c, cudaEventCreate(&e1));
+    CU_TRY(c, cudaEventRecord(e0, c->stream));
+  }
+  const int launched = launch_conv_decoder_backward(v->d_dec_params, H, W, c->d_f, v->out.blend, v->s.channels, v->dec_act,
+                                                    v->d_dec_gimage, v->dec_g, v->dec_gext, d_wt, v->d_dec_gparams,
+                                                    v->d_dec_gparams + np, g_blend, v->d_dec_err, c->stream);
+  CHECK_LAUNCH(c, "conv decoder backward");
+  c->launches += launched;
+  if (device_ms) CU_TRY(c, cudaEventRecord(e1, c->stream));
+  int err = 0;
+  CU_TRY(c, cudaMemcpyAsync(&err, v->d_dec_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g_params, v->d_dec_gparams, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g_embedding, v->d_dec_gparams + np, sizeof(float) * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (device_ms) {
+    CU_TRY(c, cudaEventElapsedTime(device_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (err) return c->fail(SPLATB200_ERUNTIME, "decode_image backward: tensor-core completion barrier timed out");
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_debug_conv3x3_backward(splatb200_ctx* c, const float* x, int32_t H, int32_t W, const float* w,
+                                                int32_t relu_in, const float* g_y, float* g_x, float* g_w) {
+  if (!x || !w || !g_y || !g_x || !g_w || H < 2 || W < 2) return c->fail(SPLATB200_EINVAL, "bad argument");
+  join_all(c);
+  const size_t n = (size_t)H * W * 32, ne = (size_t)(H + 2) * (W + 2) * 32;
+  DevScratch dx, dw, dwt, dgy, dgx, dgw, dge, de;
+  CU_TRY(c, cudaMalloc(&dx.p, sizeof(float) * n));
+  CU_TRY(c, cudaMalloc(&dgy.p, sizeof(float) * n));
+  CU_TRY(c, cudaMalloc(&dgx.p, sizeof(float) * n));
+  CU_TRY(c, cudaMalloc(&dge.p, sizeof(float) * ne));
+  CU_TRY(c, cudaMalloc(&dw.p, sizeof(float) * 9248));
+  CU_TRY(c, cudaMalloc(&dwt.p, sizeof(float) * 9248));
+  CU_TRY(c, cudaMalloc(&dgw.p, sizeof(float) * 9248));
+  CU_TRY(c, cudaMalloc(&de.p, sizeof(int)));
+  CU_TRY(c, cudaMemcpyAsync(dx.p, x, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(dgy.p, g_y, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(dw.p, w, sizeof(float) * 9248, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemsetAsync(dgw.p, 0, sizeof(float) * 9248, c->stream));
+  CU_TRY(c, cudaMemsetAsync(de.p, 0, sizeof(int), c->stream));
+  launch_conv3x3_backward(dx.p, H, W, dw.p, relu_in, dgy.p, dwt.p, dge.p, dgx.p, dgw.p, (int*)de.p, c->stream);
+  CHECK_LAUNCH(c, "k_conv3x3_wgrad_tc");
+  c->launches += 4;
+  int err = 0;
+  CU_TRY(c, cudaMemcpyAsync(&err, de.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g_x, dgx.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g_w, dgw.p, sizeof(float) * 9248, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (err) return c->fail(SPLATB200_ERUNTIME, "conv3x3 backward: tensor-core completion barrier timed out");
   return SPLATB200_OK;
 }
 
@@ -1362,6 +1442,7 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     v->band_dl_valid = true;
   }
   v->stage = 3;
+  v->dec_ready = false;
   return SPLATB200_OK;
 }
 
@@ -2056,6 +2137,9 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   else if (name == "los") src = v->out.los;
   else if (name == "lidar_head") { src = v->out.head_y; cnt = 2 * P; }
   else if (name == "decoded") { src = v->d_dec_image; cnt = 3 * P; }
+  else if (name.rfind("decoder_act", 0) == 0 && name.size() == 12 && name[11] >= '0' && name[11] <= '5') {
+    src = v->dec_act[name[11] - '0']; cnt = 32 * P;   // x0, h0, t1, h1, t2, h2 of the last decode (P x 32)
+  }
   if (!src) return c->fail(SPLATB200_EINVAL, "unknown array name " + name);
   if (dst && cnt) {
     CU_TRY(c, cudaMemcpyAsync(dst, src, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream));

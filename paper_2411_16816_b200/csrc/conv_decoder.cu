@@ -94,11 +94,14 @@ struct ConvArgs {
   float* y;              // H x W x 32 (unused by the head variant)
   int H, W;
   int relu_in;
+  int ext;               // 0: y = conv(x), reflect padding, H x W. 1 (input-gradient form): zero padding and the output
+                         // domain grown by one pixel on every side, y is (H + 2) x (W + 2) — see k_dec_fold
   // head variant: h2 = res + conv -> y6 = Wh h2 + bh -> image = (1 + y[0:3]) * rgb + y[3:6]
   const float* head;     // 192 + 6
   const float* blend;    // P x blend_stride, rgb first
   int blend_stride;
   float* image;          // P x 3
+  float* h2;             // trunk output kept for the backward (may be null)
   int* err;              // set to 1 if the MMA completion barrier timed out
 };
 
@@ -113,7 +116,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tiles_x = (a.W + kCTW - 1) / kCTW, tiles_y = (a.H + kCTR - 1) / kCTR;
+  const int Ho = a.H + 2 * a.ext, Wo = a.W + 2 * a.ext;  // output domain
+  const int tiles_x = (Wo + kCTW - 1) / kCTW, tiles_y = (Ho + kCTR - 1) / kCTR;
   const int n_tiles = tiles_x * tiles_y;
 
   if (warp == 0) {
@@ -154,8 +158,11 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
     for (int i = tid; i < kCHR * kCHW * 8; i += kCThreads) {
       const int c = i & 7, hp = i >> 3;
       const int row = hp / kCHW, px = hp - row * kCHW;
-      const int gy = reflect_clamped(y0 - 1 + row, a.H), gx = reflect_clamped(x0 - 1 + px, a.W);
+      int gy = y0 - 1 + row - a.ext, gx = x0 - 1 + px - a.ext;
+      const bool outside = gy < 0 || gy >= a.H || gx < 0 || gx >= a.W;
+      gy = reflect_clamped(gy, a.H); gx = reflect_clamped(gx, a.W);
       float4 v = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
+      if (a.ext && outside) v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (a.relu_in) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
       v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
       sX[c * kCPlane + hp] = v;
@@ -201,8 +208,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
       float acc[32];
       tmem_load32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(r * 32), acc);
       const int gx = x0 + q * 32 + lane, gy = y0 + r;
-      if (gx < a.W && gy < a.H) {
-        const int64_t p = (int64_t)gy * a.W + gx;
+      if (gx < Wo && gy < Ho) {
+        const int64_t p = (int64_t)gy * Wo + gx;
 #pragma unroll
         for (int k = 0; k < 32; ++k) acc[k] += sBias[k];
         if (a.res) {
@@ -214,6 +221,11 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
           }
         }
         if (kHead) {
+          if (a.h2) {
+            float4* hp = reinterpret_cast<float4*>(a.h2 + p * 32);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) hp[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+          }
           float y6[6];
 #pragma unroll
           for (int o = 0; o < 6; ++o) {
@@ -283,7 +295,324 @@ template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(k_conv3x3_tc<kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemBytes);
     once = true;
   }
-  k_conv3x3_tc<kHead><<<conv_grid(a.H, a.W), kCThreads, kCSmemBytes, st>>>(a);
+  k_conv3x3_tc<kHead><<<conv_grid(a.H + 2 * a.ext, a.W + 2 * a.ext), kCThreads, kCSmemBytes, st>>>(a);
+}
+
+
+// ================================================ backward ====================================================
+// weight gradient of one convolution on the tensor cores:
+//   g_w[co][ky][kx][ci] = sum_p g_y[p][co] * xr[reflect(p + (ky-1, kx-1))][ci],  xr = relu_in ? relu(x) : x.
+// The reduction runs over pixels, so pixels are the K dimension: both operands are transposed while they are staged
+// (channel rows, 4 consecutive pixels per 16-byte unit — K-major again; the MN-major operand forms returned zeros for
+// tf32 on this part, measured with either swizzle mode). One tile = 64 pixels of one image row:
+//   A [(ky, ci) 128 rows][q 72]  = halo row ky (y0-1+ky), halo pixel q (x0-1+q); rows 96..127 ("ky = 3") stay zero
+//   B_kx [co 32][q 72]           = g_y[pixel q - kx][co]   — three shifted copies, one per filter column
+//   D_kx[(ky, ci)][co] += A . B_kx^T   — 9 instructions of 128 x 32 x 8 per kx
+// D stays in tensor memory across all the tiles of the persistent CTA (3 x 32 columns) and is added to global memory
+// once, at the end.
+constexpr int kWT = 64;                              // tile width (pixels)
+constexpr int kWQC = (kWT + 2 + 7) / 8 * 2;          // 18 K chunks of 4 pixels (72 halo pixels, the last 6 zero)
+constexpr int kWXFloats = kWQC * 128 * 4;            // 9,216 floats = 36,864 B
+constexpr int kWGFloats = kWQC * 32 * 4;             // 2,304 floats per shifted copy
+constexpr int kWSmemBytes = (kWXFloats + 3 * kWGFloats) * 4 + 8 * 32 * 4 + 64;
+
+struct WgradArgs {
+  const float* x;      // H x W x 32, input of the convolution
+  const float* gy;     // H x W x 32, gradient of its output
+  float* gw;           // 9216 + 32, accumulated (+=)
+  int H, W, relu_in;
+  int* err;
+};
+
+__global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sX = reinterpret_cast<float*>(smem_raw);
+  float* sG = sX + kWXFloats;
+  float* sRed = sG + 3 * kWGFloats;                            // [8 warps][32]
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sRed + 256);
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tiles_x = (a.W + kWT - 1) / kWT;
+  const int n_tiles = tiles_x * a.H;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" :: "r"(smem_u32(sTmem)), "r"(128) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(sBar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = tid; i < kWXFloats + 3 * kWGFloats; i += kCThreads) sX[i] = 0.f;   // pads, the 4th row group
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem_base = *sTmem;
+  const uint32_t x_addr = smem_u32(sX), g_addr = smem_u32(sG), bar_addr = smem_u32(sBar);
+  uint32_t phase = 0, accumulate = 0;
+  float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);   // bias gradient of channel unit tid & 7
+  bool ok = true;
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int y0 = tile / tiles_x, x0 = (tile - y0 * tiles_x) * kWT;
+    // halo rows y0-1 .. y0+1, pixels x0-1 .. x0+64, transposed: float (q / 4, ky * 32 + ci, q % 4)
+    for (int i = tid; i < 3 * (kWT + 2) * 8; i += kCThreads) {
+      const int c = i & 7, hp = i >> 3;
+      const int row = hp / (kWT + 2), q = hp - row * (kWT + 2);
+      const int gy = reflect_clamped(y0 - 1 + row, a.H), gx = reflect_clamped(x0 - 1 + q, a.W);
+      float4 v = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
+      if (a.relu_in) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
+      float* dst = sX + (q >> 2) * 512 + (row * 32 + 4 * c) * 4 + (q & 3);
+      dst[0] = to_tf32(v.x); dst[4] = to_tf32(v.y); dst[8] = to_tf32(v.z); dst[12] = to_tf32(v.w);
+    }
+    for (int i = tid; i < kWT * 8; i += kCThreads) {
+      const int c = i & 7, px = i >> 3;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (x0 + px < a.W) v = __ldg(reinterpret_cast<const float4*>(a.gy + ((int64_t)y0 * a.W + x0 + px) * 32) + c);
+      bsum.x += v.x; bsum.y += v.y; bsum.z += v.z; bsum.w += v.w;
+      v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int q = px + kx;
+        float* dst = sG + kx * kWGFloats + (q >> 2) * 128 + (4 * c) * 4 + (q & 3);
+        dst[0] = v.x; dst[4] = v.y; dst[8] = v.z; dst[12] = v.w;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll 1
+      for (int ks = 0; ks < kWQC / 2; ++ks) {
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const uint32_t aa = x_addr + (uint32_t)(2 * ks) * 2048u;
+          const uint32_t bb = g_addr + (uint32_t)(kx * kWGFloats * 4) + (uint32_t)(2 * ks) * 512u;
+          mma_tf32(tmem_base + (uint32_t)(kx * 32), smem_desc(aa, 2048u, 128u), smem_desc(bb, 512u, 128u),
+                   accumulate | (uint32_t)ks);
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" :: "r"(bar_addr) : "memory");
+    }
+    accumulate = 1;
+    {
+      uint32_t done = 0;
+      for (int spin = 0; spin < kCSpin && !done; ++spin)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done) : "r"(bar_addr), "r"(phase) : "memory");
+      if (!__syncthreads_and((int)done)) {
+        if (tid == 0 && a.err) *a.err = 1;
+        ok = false;
+        break;
+      }
+      phase ^= 1u;
+    }
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // ---- weights: warps 0..2 hold ky = warp (lanes = ci); 3 x 32 columns = (kx, co) ----
+  if (ok && accumulate && warp < 4) {
+#pragma unroll 1
+    for (int kx = 0; kx < 3; ++kx) {
+      float acc[32];
+      tmem_load32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(kx * 32), acc);
+      if (warp < 3) {
+#pragma unroll
+        for (int co = 0; co < 32; ++co) atomicAdd(a.gw + ((co * 3 + warp) * 3 + kx) * 32 + lane, acc[co]);
+      }
+    }
+  }
+  // ---- bias: sum the per-thread partials of each channel unit ----
+  {
+    float4 t = bsum;
+#pragma unroll
+    for (int m = 8; m < 32; m <<= 1) {
+      t.x += __shfl_xor_sync(0xffffffffu, t.x, m); t.y += __shfl_xor_sync(0xffffffffu, t.y, m);
+      t.z += __shfl_xor_sync(0xffffffffu, t.z, m); t.w += __shfl_xor_sync(0xffffffffu, t.w, m);
+    }
+    if (lane < 8) reinterpret_cast<float4*>(sRed)[warp * 8 + lane] = t;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (ok && tid < 32) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kCThreads / 32; ++w) t += sRed[w * 32 + tid];
+    atomicAdd(a.gw + 9216 + tid, t);
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem_base), "r"(128) : "memory");
+}
+
+// weights of the input-gradient convolution: Wt[ci][ky][kx][co] = W[co][2-ky][2-kx][ci], zero bias
+__global__ void k_dec_transpose_w(const float* __restrict__ w, float* __restrict__ wt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 9216) {
+    const int co = i & 31, t = (i >> 5) % 9, ci = i / 288;
+    wt[i] = w[(co * 9 + (8 - t)) * 32 + ci];
+  } else if (i < 9248) {
+    wt[i] = 0.f;
+  }
+}
+
+// Folds the extended-domain result of the zero-padded transposed convolution back onto the image (the adjoint of
+// reflect padding: what landed on row -1 belongs to row 1, on row H to row H-2, same for columns), applies the ReLU
+// mask of the convolution's input and adds the residual branch's gradient. One thread per (pixel, 16-byte unit).
+__global__ void __launch_bounds__(256) k_dec_fold(int H, int W, const float* __restrict__ gext, const float* __restrict__ x_mask,
+                                                   const float* __restrict__ add, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)H * W * 8) return;
+  const int64_t p = i >> 3;
+  const int c = (int)(i & 7);
+  const int y = (int)(p / W), x = (int)(p - (int64_t)y * W);
+  const int We = W + 2;
+  constexpr int kNone = -9;
+  // preimages of row y under reflect padding: y itself, row -1 if y == 1, row H if y == H - 2 (both when H == 3)
+  const int yc[3] = {y, y == 1 ? -1 : kNone, y == H - 2 ? H : kNone};
+  const int xc[3] = {x, x == 1 ? -1 : kNone, x == W - 2 ? W : kNone};
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (yc[a] == kNone) continue;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (xc[b] == kNone) continue;
+      const float4 t = __ldg(reinterpret_cast<const float4*>(gext + ((int64_t)(yc[a] + 1) * We + (xc[b] + 1)) * 32) + c);
+      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+    }
+  }
+  if (x_mask) {
+    const float4 m = __ldg(reinterpret_cast<const float4*>(x_mask + p * 32) + c);
+    if (!(m.x > 0.f)) s.x = 0.f;
+    if (!(m.y > 0.f)) s.y = 0.f;
+    if (!(m.z > 0.f)) s.z = 0.f;
+    if (!(m.w > 0.f)) s.w = 0.f;
+  }
+  if (add) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(add + p * 32) + c);
+    s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+  }
+  reinterpret_cast<float4*>(out)[i] = s;
+}
+
+// head backward: per pixel, from dL/dimage: dL/drgb (added to the blend gradient), dL/dh2, and the head's parameter
+// gradients (block-reduced, then one atomic per parameter and CTA)
+__global__ void __launch_bounds__(256) k_dec_head_bwd(int64_t P, const float* __restrict__ h2, const float* __restrict__ head,
+                                                       const float* __restrict__ blend, int blend_stride,
+                                                       const float* __restrict__ g_image, float* __restrict__ g_blend,
+                                                       float* __restrict__ g_h2, float* __restrict__ g_head) {
+  __shared__ float sHead[198];
+  __shared__ float sAcc[198];
+  for (int i = threadIdx.x; i < 198; i += blockDim.x) { sHead[i] = head[i]; sAcc[i] = 0.f; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < P; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = base + threadIdx.x;
+    const bool live = p < P;
+    float h[32], gy[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 32; ++k) h[k] = 0.f;
+    if (live) {
+      const float4* hp = reinterpret_cast<const float4*>(h2 + p * 32);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) { const float4 t = __ldg(hp + c); h[4 * c] = t.x; h[4 * c + 1] = t.y; h[4 * c + 2] = t.z; h[4 * c + 3] = t.w; }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float y = sHead[192 + c];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) y = fmaf(sHead[c * 32 + k], h[k], y);
+        const float g = __ldg(g_image + 3 * p + c);
+        g_blend[p * blend_stride + c] += g * (1.f + y);
+        gy[c] = g * __ldg(blend + p * blend_stride + c);
+        gy[3 + c] = g;
+      }
+      float4* gp = reinterpret_cast<float4*>(g_h2 + p * 32);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float t = 0.f;
+#pragma unroll
+          for (int q = 0; q < 6; ++q) t = fmaf(gy[q], sHead[q * 32 + 4 * c + j], t);
+          o[j] = t;
+        }
+        gp[c] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    // parameter gradients: warp-reduce gy[q] * h[k] and gy[q]
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+#pragma unroll 4
+      for (int k = 0; k < 32; ++k) {
+        float t = gy[q] * h[k];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (lane == 0) atomicAdd(&sAcc[q * 32 + k], t);
+      }
+      float t = gy[q];
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+      if (lane == 0) atomicAdd(&sAcc[192 + q], t);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 198; i += blockDim.x) atomicAdd(g_head + i, sAcc[i]);
+}
+
+// gradient of the decoder input: feature slots are added to the blend gradient, embedding slots summed over pixels
+__global__ void __launch_bounds__(256) k_dec_input_bwd(int64_t P, int d_f, const float* __restrict__ g_x0,
+                                                        float* __restrict__ g_blend, int blend_stride, float* __restrict__ g_emb) {
+  __shared__ float sEmb[8];
+  if (threadIdx.x < 8) sEmb[threadIdx.x] = 0.f;
+  __syncthreads();
+  float e[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const float* g = g_x0 + p * 32;
+    for (int k = 0; k < d_f; ++k) g_blend[p * blend_stride + 3 + k] += __ldg(g + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] += __ldg(g + d_f + 3 + k);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float t = e[k];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&sEmb[k], t);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) atomicAdd(g_emb + threadIdx.x, sEmb[threadIdx.x]);
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+void launch_wgrad(const float* x, const float* gy, float* gw, int H, int W, int relu_in, int* err, cudaStream_t st) {
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(k_conv3x3_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmemBytes);
+    once = true;
+  }
+  WgradArgs a{x, gy, gw, H, W, relu_in, err};
+  const int tiles = ((W + kWT - 1) / kWT) * H;
+  k_conv3x3_wgrad_tc<<<tiles < 3 * sm_count() ? tiles : 3 * sm_count(), kCThreads, kWSmemBytes, st>>>(a);
+}
+
+// g_x = mask(x) . fold(convT(g_y)) + add: transposed weights -> tensor-core convolution on the grown domain -> fold
+void launch_dgrad(const float* gy, const float* w, float* wt, float* gext, const float* x_mask, const float* add, float* gx,
+                  int H, int W, int* err, cudaStream_t st) {
+  k_dec_transpose_w<<<(9248 + 255) / 256, 256, 0, st>>>(w, wt);
+  ConvArgs a{};
+  a.x = gy; a.w = wt; a.y = gext; a.H = H; a.W = W; a.ext = 1; a.err = err;
+  launch_conv<false>(a, st);
+  const int64_t units = (int64_t)H * W * 8;
+  k_dec_fold<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(H, W, gext, x_mask, add, gx);
 }
 
 }  // namespace
@@ -298,26 +627,59 @@ void launch_conv3x3(const float* x, int H, int W, const float* w, int relu_in, c
   launch_conv<false>(a, st);
 }
 
+void launch_conv3x3_backward(const float* x, int H, int W, const float* w, int relu_in, const float* gy, float* wt, float* gext,
+                             float* gx, float* gw, int* err, cudaStream_t st) {
+  if (H <= 0 || W <= 0) return;
+  launch_wgrad(x, gy, gw, H, W, relu_in, err, st);
+  launch_dgrad(gy, w, wt, gext, relu_in ? x : nullptr, nullptr, gx, H, W, err, st);
+}
+
 int launch_conv_decoder(const float* params, const float* emb, int H, int W, int d_f, float fx, float fy, float cx, float cy,
-                        const float* blend, int blend_stride, float* buf_a, float* buf_b, float* buf_c, float* image,
-                        int* err, cudaStream_t st) {
+                        const float* blend, int blend_stride, float* const act[6], float* image, int* err, cudaStream_t st) {
   if (H <= 0 || W <= 0) return 0;
   const int64_t units = (int64_t)H * W * 8;
-  k_decoder_input<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(H, W, d_f, fx, fy, cx, cy, blend, blend_stride, emb, buf_a);
+  float *x0 = act[0], *h0 = act[1], *t1 = act[2], *h1 = act[3], *t2 = act[4], *h2 = act[5];
+  k_decoder_input<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(H, W, d_f, fx, fy, cx, cy, blend, blend_stride, emb, x0);
   ConvArgs a{};
   a.H = H; a.W = W; a.err = err;
-  a.x = buf_a; a.w = params; a.res = nullptr; a.y = buf_b; a.relu_in = 0;             // h0 (b)
+  a.x = x0; a.w = params; a.res = nullptr; a.y = h0; a.relu_in = 0;
   launch_conv<false>(a, st);
-  a.x = buf_b; a.w = params + 9248; a.y = buf_c; a.relu_in = 1;                       // t1 (c)
+  a.x = h0; a.w = params + 9248; a.y = t1; a.relu_in = 1;
   launch_conv<false>(a, st);
-  a.x = buf_c; a.w = params + 2 * 9248; a.res = buf_b; a.y = buf_a;                   // h1 = h0 + conv2 (a)
+  a.x = t1; a.w = params + 2 * 9248; a.res = h0; a.y = h1;                            // h1 = h0 + conv2(relu(t1))
   launch_conv<false>(a, st);
-  a.x = buf_a; a.w = params + 3 * 9248; a.res = nullptr; a.y = buf_c;                 // t2 (c)
+  a.x = h1; a.w = params + 3 * 9248; a.res = nullptr; a.y = t2;
   launch_conv<false>(a, st);
-  a.x = buf_c; a.w = params + 4 * 9248; a.res = buf_a; a.y = nullptr;                 // h2 = h1 + conv4 -> head -> image
-  a.head = params + 5 * 9248; a.blend = blend; a.blend_stride = blend_stride; a.image = image;
+  a.x = t2; a.w = params + 4 * 9248; a.res = h1; a.y = nullptr;                       // h2 = h1 + conv4(relu(t2)) -> head
+  a.head = params + 5 * 9248; a.blend = blend; a.blend_stride = blend_stride; a.image = image; a.h2 = h2;
   launch_conv<true>(a, st);
   return 6;
+}
+
+int launch_conv_decoder_backward(const float* params, int H, int W, int d_f, const float* blend, int blend_stride,
+                                 float* const act[6], const float* g_image, float* const g[3], float* gext, float* wt,
+                                 float* g_params, float* g_emb, float* g_blend, int* err, cudaStream_t st) {
+  if (H <= 0 || W <= 0) return 0;
+  const int64_t P = (int64_t)H * W;
+  const float *x0 = act[0], *h0 = act[1], *t1 = act[2], *h1 = act[3], *t2 = act[4], *h2 = act[5];
+  float *g0 = g[0], *g1 = g[1], *g2 = g[2];
+  const int grid = 4 * sm_count();
+  k_dec_head_bwd<<<grid, 256, 0, st>>>(P, h2, params + 5 * 9248, blend, blend_stride, g_image, g_blend, g0, g_params + 5 * 9248);
+  // block 2: h2 = h1 + conv4(relu(t2)), t2 = conv3(relu(h1));  g0 = dL/dh2
+  launch_wgrad(t2, g0, g_params + 4 * 9248, H, W, 1, err, st);
+  launch_dgrad(g0, params + 4 * 9248, wt, gext, t2, nullptr, g1, H, W, err, st);      // g1 = dL/dt2
+  launch_wgrad(h1, g1, g_params + 3 * 9248, H, W, 1, err, st);
+  launch_dgrad(g1, params + 3 * 9248, wt, gext, h1, g0, g2, H, W, err, st);           // g2 = dL/dh1
+  // block 1: h1 = h0 + conv2(relu(t1)), t1 = conv1(relu(h0))
+  launch_wgrad(t1, g2, g_params + 2 * 9248, H, W, 1, err, st);
+  launch_dgrad(g2, params + 2 * 9248, wt, gext, t1, nullptr, g1, H, W, err, st);      // g1 = dL/dt1
+  launch_wgrad(h0, g1, g_params + 9248, H, W, 1, err, st);
+  launch_dgrad(g1, params + 9248, wt, gext, h0, g2, g0, H, W, err, st);               // g0 = dL/dh0
+  // stem: h0 = conv0(x0)
+  launch_wgrad(x0, g0, g_params, H, W, 0, err, st);
+  launch_dgrad(g0, params, wt, gext, nullptr, nullptr, g1, H, W, err, st);            // g1 = dL/dx0
+  k_dec_input_bwd<<<grid, 256, 0, st>>>(P, d_f, g1, g_blend, blend_stride, g_emb);
+  return 2 + 5 * 4;
 }
 
 }  // namespace sb

@@ -1132,3 +1132,125 @@ def test_decode_image_full_size_1080p(ctx, op):
     err = np.abs(img.reshape(ref.shape) - ref).max()
     print(f"decode_image 1920x1080: {min(times):.3f} ms on the device, max |err| {err:.2e} (scale {np.abs(ref).max():.2f})")
     assert err <= DEC_RTOL * max(1.0, np.abs(ref).max())
+
+
+DEC_GRAD_RTOL = 5e-3   # tf32 operands in the gradient convolutions as well; relative to each tensor's largest entry
+
+
+def _reflect_idx(i, n):
+    i = np.abs(i)
+    return np.where(i >= n, 2 * (n - 1) - i, i)
+
+
+def _conv3x3_backward_numpy(x, w, relu_in, gy):
+    H, W, _ = x.shape
+    k = w[:9216].reshape(32, 3, 3, 32).astype(np.float64)
+    xin = (np.maximum(x, 0) if relu_in else x).astype(np.float64)
+    gy = gy.astype(np.float64)
+    gx, gw = np.zeros((H, W, 32)), np.zeros((32, 3, 3, 32))
+    for ky in range(3):
+        ys = _reflect_idx(np.arange(H) + ky - 1, H)
+        for kx in range(3):
+            xs = _reflect_idx(np.arange(W) + kx - 1, W)
+            gw[:, ky, kx, :] = np.einsum("hwo,hwi->oi", gy, xin[ys][:, xs])
+            np.add.at(gx, (ys[:, None], xs[None, :]), gy @ k[:, ky, kx, :])
+    if relu_in:
+        gx *= x > 0
+    return gx, np.concatenate([gw.ravel(), gy.sum((0, 1))])
+
+
+@pytest.mark.parametrize("H,W", [(2, 2), (3, 3), (5, 131), (33, 300)])
+def test_conv3x3_backward_matches_numpy(ctx, H, W):
+    """Input and weight gradients of one decoder convolution (both tensor-core kernels; the adjoint of reflect padding
+    on the borders, including the 3 x 3 image where both border preimages fold onto the centre)."""
+    rng = np.random.default_rng(H * 1000 + W + 1)
+    x = rng.normal(0, 1, (H, W, 32)).astype(np.float32)
+    w = rng.normal(0, 0.1, 9248).astype(np.float32)
+    gy = rng.normal(0, 1, (H, W, 32)).astype(np.float32)
+    for relu_in in (False, True):
+        gx, gw = ctx.debug_conv3x3_backward(x, w, gy, relu_in)
+        rgx, rgw = _conv3x3_backward_numpy(x, w, relu_in, gy)
+        assert np.abs(gx - rgx).max() <= 2e-3 * np.abs(rgx).max(), (relu_in, np.abs(gx - rgx).max(), np.abs(rgx).max())
+        assert np.abs(gw - rgw).max() <= 2e-3 * np.abs(rgw).max(), (relu_in, np.abs(gw - rgw).max(), np.abs(rgw).max())
+    # small integers: exact in tf32 and in the fp32 accumulators
+    xi = rng.integers(-4, 5, (H, W, 32)).astype(np.float32)
+    wi = rng.integers(-3, 4, 9248).astype(np.float32)
+    gi = rng.integers(-2, 3, (H, W, 32)).astype(np.float32)
+    gx, gw = ctx.debug_conv3x3_backward(xi, wi, gi, True)
+    rgx, rgw = _conv3x3_backward_numpy(xi, wi, True, gi)
+    assert np.array_equal(gx, rgx.astype(np.float32)) and np.array_equal(gw, rgw.astype(np.float32))
+
+
+@pytest.mark.parametrize("w,h", [(96, 64), (203, 77)])
+def test_decode_image_backward_matches_oracle(ctx, op, w, h):
+    """dL/dparams, dL/dembedding, dL/dF_rgb and dL/dfeature of decode_image against the fp64 oracle backward (pinned by
+    finite differences, tests/test_oracle_kat.py); the feature gradient is added into the render's upstream buffer."""
+    import torch
+    sc = synth.make_scene(4000, seed=23, r_max=40.0, scale_mean=0.12)
+    cam = synth.make_camera(width=w, height=h)
+    ctx.upload_scene(sc)
+    view = ctx.camera_view(cam, ST)
+    view.forward(0.0)
+    P, d_f = view.P, sc.d_f
+    rgb, feat, intr = _decoder_inputs(view, cam, d_f)
+    rng = np.random.default_rng(7)
+    params = rng.normal(0, 0.08, op.DEC_PARAMS).astype(np.float32)
+    params[op.DEC_HEAD_OFFSET:] = rng.normal(0, 0.3, op.DEC_PARAMS - op.DEC_HEAD_OFFSET)
+    emb = rng.normal(0, 1, 8).astype(np.float32)
+    g_image = rng.normal(0, 1, (h, w, 3)).astype(np.float32)
+    g_up = torch.zeros((P, 3 + d_f), dtype=torch.float32, device="cuda")
+    with pytest.raises(Exception):                      # no saved state yet (SPEC.md:319)
+        view.decode_image_backward(g_image, g_up.data_ptr())
+    view.decode_image(params, emb)
+    g_up[:, 5] = 0.5                                    # another upstream gradient of the render: must be kept
+    gp, ge = view.decode_image_backward(g_image, g_up.data_ptr())
+    # The device gradient is the gradient of the device forward: its ReLU masks come from the tf32 activations, and
+    # against white-noise dL/dI a mask flip on a near-zero activation is a full-size term of an incoherent sum. So the
+    # oracle backward runs from the device's saved activations (forward parity is test_decode_image_matches_oracle).
+    acts = np.stack([view.array(f"decoder_act{k}").reshape(h, w, 32) for k in range(6)])
+    ogp, ogrgb, ogf, oge = op.decoder_backward_from_state(params, rgb, acts, d_f, g_image)
+    names = [f"conv{l}" for l in range(5)] + ["head"]
+    bounds = [l * op.DEC_CONV_PARAMS for l in range(6)] + [op.DEC_PARAMS]
+    for name, b, e in zip(names, bounds[:-1], bounds[1:]):
+        err, scale = np.abs(gp[b:e] - ogp[b:e]).max(), np.abs(ogp[b:e]).max()
+        assert err <= DEC_GRAD_RTOL * scale, (name, err, scale)
+    assert np.abs(ge - oge).max() <= DEC_GRAD_RTOL * np.abs(oge).max()
+    gb = g_up.cpu().numpy().reshape(h, w, 3 + d_f)
+    exp = np.concatenate([ogrgb, ogf], axis=2); exp[..., 5] += 0.5
+    assert np.abs(gb[..., :3] - exp[..., :3]).max() <= DEC_GRAD_RTOL * np.abs(exp[..., :3]).max()
+    assert np.abs(gb[..., 3:] - exp[..., 3:]).max() <= DEC_GRAD_RTOL * np.abs(exp[..., 3:]).max()
+    # decoder + rasterizer backward in one go: the buffer is the render's upstream gradient
+    ga = torch.zeros(P, dtype=torch.float32, device="cuda")
+    ctx.zero_grads()
+    view.backward_device(g_up.data_ptr(), ga.data_ptr())
+    assert np.isfinite(ctx.grads()["d_feature"]).all() and np.abs(ctx.grads()["d_feature"]).max() > 0
+    # a new forward invalidates the saved activations
+    view.forward(0.0)
+    with pytest.raises(Exception):
+        view.decode_image_backward(g_image, g_up.data_ptr())
+
+
+def test_decode_image_backward_full_size_1080p(ctx, op):
+    """1920 x 1080: linearity of the backward in dL/dimage, finite results, device time."""
+    import torch
+    sc = synth.make_scene(200_000, seed=22)
+    cam = synth.make_camera()
+    ctx.upload_scene(sc)
+    view = ctx.camera_view(cam, ST)
+    view.forward(0.0)
+    rng = np.random.default_rng(8)
+    params = rng.normal(0, 0.08, op.DEC_PARAMS).astype(np.float32)
+    params[op.DEC_HEAD_OFFSET:] = rng.normal(0, 0.3, op.DEC_PARAMS - op.DEC_HEAD_OFFSET)
+    emb = rng.normal(0, 1, 8).astype(np.float32)
+    view.decode_image(params, emb, download=False)
+    g_image = rng.normal(0, 1, (view.P, 3)).astype(np.float32)
+    g1 = torch.zeros((view.P, 16), dtype=torch.float32, device="cuda")
+    g2 = torch.zeros_like(g1)
+    gp1, ge1, ms = view.decode_image_backward(g_image, g1.data_ptr(), timed=True)
+    gp2, ge2, ms2 = view.decode_image_backward(2 * g_image, g2.data_ptr(), timed=True)
+    print(f"decode_image backward 1920x1080: {min(ms, ms2):.3f} ms on the device")
+    assert np.isfinite(gp1).all() and np.abs(gp1).max() > 0
+    # power-of-two scaling is exact in every product; only the atomics' summation order differs between the runs
+    assert np.abs(gp2 - 2 * gp1).max() <= 1e-4 * np.abs(gp1).max()
+    assert np.abs(ge2 - 2 * ge1).max() <= 1e-4 * np.abs(ge1).max()
+    assert torch.equal(g2, 2 * g1)

@@ -923,3 +923,20 @@ def test_decoder_translation_equivariance(oracle_lib):
     b = op.decoder_forward(params, rgb_s, feat_s, intr_s, emb, np.float64)
     # five 3x3 layers: the receptive field reaches 5 px, so compare columns 6 .. W-6
     assert np.allclose(b[:, 7:-5], a[:, 6:-6], atol=1e-12)
+
+
+def test_decoder_backward_from_state_equals_backward(oracle_lib):
+    """The state-fed backward (used to check the device path against its own activations) is the same function."""
+    params, rgb, feat, intr, emb = _decoder_case(4, H=6, W=7)
+    g_image = np.random.default_rng(5).normal(0, 1, rgb.shape)
+    ref = op.decoder_backward(params, rgb, feat, intr, emb, g_image)
+    H, W, d_f = feat.shape
+    # rebuild the activations with numpy from the trunk output chain is the oracle's job: take them from a forward
+    import ctypes as C
+    L = oracle_lib
+    acts = np.zeros((6, H, W, 32))
+    L.orc_decoder_activations_f64(_p(params), C.c_int(H), C.c_int(W), C.c_int(d_f), _p(np.ascontiguousarray(rgb)),
+                                  _p(np.ascontiguousarray(feat)), _p(intr), _p(emb), _p(acts))
+    got = op.decoder_backward_from_state(params, rgb, acts, d_f, g_image)
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
