@@ -155,17 +155,34 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int x0 = tx * kCTW, y0 = ty * kCTR;
     // ---- stage the halo: 4 rows x 130 pixels x 8 units, reflect padding, optional ReLU, tf32 rounding ----
-    for (int i = tid; i < kCHR * kCHW * 8; i += kCThreads) {
-      const int c = i & 7, hp = i >> 3;
-      const int row = hp / kCHW, px = hp - row * kCHW;
-      int gy = y0 - 1 + row - a.ext, gx = x0 - 1 + px - a.ext;
-      const bool outside = gy < 0 || gy >= a.H || gx < 0 || gx >= a.W;
-      gy = reflect_clamped(gy, a.H); gx = reflect_clamped(gx, a.W);
-      float4 v = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
-      if (a.ext && outside) v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.relu_in) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
-      v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
-      sX[c * kCPlane + hp] = v;
+    // (eight loads in flight per thread: the staging is latency-bound otherwise)
+    constexpr int kItems = kCHR * kCHW * 8;
+#pragma unroll 1
+    for (int i0 = tid; i0 < kItems; i0 += 8 * kCThreads) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kCThreads;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < kItems) {
+          const int c = i & 7, hp = i >> 3;
+          const int row = hp / kCHW, px = hp - row * kCHW;
+          int gy = y0 - 1 + row - a.ext, gx = x0 - 1 + px - a.ext;
+          const bool outside = gy < 0 || gy >= a.H || gx < 0 || gx >= a.W;
+          gy = reflect_clamped(gy, a.H); gx = reflect_clamped(gx, a.W);
+          if (!(a.ext && outside)) v[u] = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kCThreads;
+        if (i < kItems) {
+          float4 t = v[u];
+          if (a.relu_in) { t.x = fmaxf(t.x, 0.f); t.y = fmaxf(t.y, 0.f); t.z = fmaxf(t.z, 0.f); t.w = fmaxf(t.w, 0.f); }
+          t.x = to_tf32(t.x); t.y = to_tf32(t.y); t.z = to_tf32(t.z); t.w = to_tf32(t.w);
+          sX[(i & 7) * kCPlane + (i >> 3)] = t;
+        }
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy stores -> tensor-core reads
     __syncthreads();
@@ -312,8 +329,10 @@ template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
 // once, at the end.
 constexpr int kWT = 64;                              // tile width (pixels)
 constexpr int kWQC = (kWT + 2 + 7) / 8 * 2;          // 18 K chunks of 4 pixels (72 halo pixels, the last 6 zero)
-constexpr int kWXFloats = kWQC * 128 * 4;            // 9,216 floats = 36,864 B
-constexpr int kWGFloats = kWQC * 32 * 4;             // 2,304 floats per shifted copy
+constexpr int kWXChunk = 128 * 4 + 4;                // floats per K chunk of A (+16 B: conflict-free transposed stores)
+constexpr int kWGChunk = 32 * 4 + 4;                 // floats per K chunk of B
+constexpr int kWXFloats = kWQC * kWXChunk;           // 37,152 B
+constexpr int kWGFloats = kWQC * kWGChunk;           // 9,504 B per shifted copy
 constexpr int kWSmemBytes = (kWXFloats + 3 * kWGFloats) * 4 + 8 * 32 * 4 + 64;
 
 struct WgradArgs {
@@ -350,23 +369,44 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
   const uint32_t tmem_base = *sTmem;
   const uint32_t x_addr = smem_u32(sX), g_addr = smem_u32(sG), bar_addr = smem_u32(sBar);
   uint32_t phase = 0, accumulate = 0;
-  float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);   // bias gradient of channel unit tid & 7
+  float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);   // bias gradient of channel unit 2 (warp & 3) + (tid & 1)
   bool ok = true;
 
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int y0 = tile / tiles_x, x0 = (tile - y0 * tiles_x) * kWT;
-    // halo rows y0-1 .. y0+1, pixels x0-1 .. x0+64, transposed: float (q / 4, ky * 32 + ci, q % 4)
-    for (int i = tid; i < 3 * (kWT + 2) * 8; i += kCThreads) {
-      const int c = i & 7, hp = i >> 3;
-      const int row = hp / (kWT + 2), q = hp - row * (kWT + 2);
-      const int gy = reflect_clamped(y0 - 1 + row, a.H), gx = reflect_clamped(x0 - 1 + q, a.W);
-      float4 v = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
-      if (a.relu_in) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
-      float* dst = sX + (q >> 2) * 512 + (row * 32 + 4 * c) * 4 + (q & 3);
-      dst[0] = to_tf32(v.x); dst[4] = to_tf32(v.y); dst[8] = to_tf32(v.z); dst[12] = to_tf32(v.w);
+    // halo rows y0-1 .. y0+1, pixels x0-1 .. x0+64, transposed: float (q / 4, ky * 32 + ci, q % 4). A warp covers
+    // 2 channel units x 16 pixels: 32-byte sectors from global memory, 32 distinct banks per transposed store.
+    {
+      constexpr int kItems = 3 * 5 * 128;   // rows x (5 x 16 pixels, 66 used) x (16 px x 8 units)
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = tid + u * kCThreads;
+        const int c = ((i >> 5) & 3) * 2 + (i & 1), blk = i >> 7;
+        const int row = blk / 5, q = (blk - row * 5) * 16 + ((i >> 1) & 15);
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < kItems && q < kWT + 2) {
+          const int gy = reflect_clamped(y0 - 1 + row, a.H), gx = reflect_clamped(x0 - 1 + q, a.W);
+          v[u] = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = tid + u * kCThreads;
+        const int c = ((i >> 5) & 3) * 2 + (i & 1), blk = i >> 7;
+        const int row = blk / 5, q = (blk - row * 5) * 16 + ((i >> 1) & 15);
+        if (i < kItems && q < kWT + 2) {
+          float4 t = v[u];
+          if (a.relu_in) { t.x = fmaxf(t.x, 0.f); t.y = fmaxf(t.y, 0.f); t.z = fmaxf(t.z, 0.f); t.w = fmaxf(t.w, 0.f); }
+          float* dst = sX + (q >> 2) * kWXChunk + (row * 32 + 4 * c) * 4 + (q & 3);
+          dst[0] = to_tf32(t.x); dst[4] = to_tf32(t.y); dst[8] = to_tf32(t.z); dst[12] = to_tf32(t.w);
+        }
+      }
     }
-    for (int i = tid; i < kWT * 8; i += kCThreads) {
-      const int c = i & 7, px = i >> 3;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = tid + u * kCThreads;
+      const int c = ((i >> 5) & 3) * 2 + (i & 1), px = (i >> 7) * 16 + ((i >> 1) & 15);
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (x0 + px < a.W) v = __ldg(reinterpret_cast<const float4*>(a.gy + ((int64_t)y0 * a.W + x0 + px) * 32) + c);
       bsum.x += v.x; bsum.y += v.y; bsum.z += v.z; bsum.w += v.w;
@@ -374,7 +414,7 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
 #pragma unroll
       for (int kx = 0; kx < 3; ++kx) {
         const int q = px + kx;
-        float* dst = sG + kx * kWGFloats + (q >> 2) * 128 + (4 * c) * 4 + (q & 3);
+        float* dst = sG + kx * kWGFloats + (q >> 2) * kWGChunk + (4 * c) * 4 + (q & 3);
         dst[0] = v.x; dst[4] = v.y; dst[8] = v.z; dst[12] = v.w;
       }
     }
@@ -386,9 +426,9 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
       for (int ks = 0; ks < kWQC / 2; ++ks) {
 #pragma unroll
         for (int kx = 0; kx < 3; ++kx) {
-          const uint32_t aa = x_addr + (uint32_t)(2 * ks) * 2048u;
-          const uint32_t bb = g_addr + (uint32_t)(kx * kWGFloats * 4) + (uint32_t)(2 * ks) * 512u;
-          mma_tf32(tmem_base + (uint32_t)(kx * 32), smem_desc(aa, 2048u, 128u), smem_desc(bb, 512u, 128u),
+          const uint32_t aa = x_addr + (uint32_t)(2 * ks * kWXChunk * 4);
+          const uint32_t bb = g_addr + (uint32_t)(kx * kWGFloats * 4) + (uint32_t)(2 * ks * kWGChunk * 4);
+          mma_tf32(tmem_base + (uint32_t)(kx * 32), smem_desc(aa, kWXChunk * 4u, 128u), smem_desc(bb, kWGChunk * 4u, 128u),
                    accumulate | (uint32_t)ks);
         }
       }
@@ -422,22 +462,21 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
       }
     }
   }
-  // ---- bias: sum the per-thread partials of each channel unit ----
+  // ---- bias: sum the per-thread partials of each channel unit (lanes of equal parity, then warps w and w + 4) ----
   {
     float4 t = bsum;
 #pragma unroll
-    for (int m = 8; m < 32; m <<= 1) {
+    for (int m = 2; m < 32; m <<= 1) {
       t.x += __shfl_xor_sync(0xffffffffu, t.x, m); t.y += __shfl_xor_sync(0xffffffffu, t.y, m);
       t.z += __shfl_xor_sync(0xffffffffu, t.z, m); t.w += __shfl_xor_sync(0xffffffffu, t.w, m);
     }
-    if (lane < 8) reinterpret_cast<float4*>(sRed)[warp * 8 + lane] = t;
+    if (lane < 2) reinterpret_cast<float4*>(sRed)[warp * 2 + lane] = t;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (ok && tid < 32) {
-    float t = 0.f;
-#pragma unroll
-    for (int w = 0; w < kCThreads / 32; ++w) t += sRed[w * 32 + tid];
+    const int c = tid >> 2;   // channel unit: warps (c >> 1) and (c >> 1) + 4, lane c & 1
+    const float t = sRed[(((c >> 1) * 2 + (c & 1)) << 2) + (tid & 3)] + sRed[((((c >> 1) + 4) * 2 + (c & 1)) << 2) + (tid & 3)];
     atomicAdd(a.gw + 9216 + tid, t);
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem_base), "r"(128) : "memory");
@@ -455,18 +494,10 @@ __global__ void k_dec_transpose_w(const float* __restrict__ w, float* __restrict
 }
 
 // Folds the extended-domain result of the zero-padded transposed convolution back onto the image (the adjoint of
-// reflect padding: what landed on row -1 belongs to row 1, on row H to row H-2, same for columns), applies the ReLU
-// mask of the convolution's input and adds the residual branch's gradient. One thread per (pixel, 16-byte unit).
-__global__ void __launch_bounds__(256) k_dec_fold(int H, int W, const float* __restrict__ gext, const float* __restrict__ x_mask,
-                                                   const float* __restrict__ add, float* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)H * W * 8) return;
-  const int64_t p = i >> 3;
-  const int c = (int)(i & 7);
-  const int y = (int)(p / W), x = (int)(p - (int64_t)y * W);
+// reflect padding: what landed on row -1 belongs to row 1, on row H to row H-2, same for columns; both when H == 3).
+__device__ __forceinline__ float4 fold_sum(const float* __restrict__ gext, int H, int W, int y, int x, int c) {
   const int We = W + 2;
   constexpr int kNone = -9;
-  // preimages of row y under reflect padding: y itself, row -1 if y == 1, row H if y == H - 2 (both when H == 3)
   const int yc[3] = {y, y == 1 ? -1 : kNone, y == H - 2 ? H : kNone};
   const int xc[3] = {x, x == 1 ? -1 : kNone, x == W - 2 ? W : kNone};
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -480,6 +511,18 @@ __global__ void __launch_bounds__(256) k_dec_fold(int H, int W, const float* __r
       s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
     }
   }
+  return s;
+}
+
+// g_x = mask(x) . fold(gext) + add. One thread per (pixel, 16-byte unit).
+__global__ void __launch_bounds__(256) k_dec_fold(int H, int W, const float* __restrict__ gext, const float* __restrict__ x_mask,
+                                                   const float* __restrict__ add, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)H * W * 8) return;
+  const int64_t p = i >> 3;
+  const int c = (int)(i & 7);
+  const int y = (int)(p / W), x = (int)(p - (int64_t)y * W);
+  float4 s = fold_sum(gext, H, W, y, x, c);
   if (x_mask) {
     const float4 m = __ldg(reinterpret_cast<const float4*>(x_mask + p * 32) + c);
     if (!(m.x > 0.f)) s.x = 0.f;
@@ -494,93 +537,113 @@ __global__ void __launch_bounds__(256) k_dec_fold(int H, int W, const float* __r
   reinterpret_cast<float4*>(out)[i] = s;
 }
 
-// head backward: per pixel, from dL/dimage: dL/drgb (added to the blend gradient), dL/dh2, and the head's parameter
-// gradients (block-reduced, then one atomic per parameter and CTA)
+// The stem's fold, fused with the gradient of the decoder input: feature slots are added to the blend gradient, the
+// embedding slots are summed over all pixels (registers over the grid-stride loop -> warp -> block -> one atomic).
+__global__ void __launch_bounds__(256) k_dec_fold_input(int H, int W, int d_f, const float* __restrict__ gext,
+                                                         float* __restrict__ g_blend, int blend_stride, float* __restrict__ g_emb) {
+  __shared__ float sEmb[8];
+  if (threadIdx.x < 8) sEmb[threadIdx.x] = 0.f;
+  __syncthreads();
+  const int c = threadIdx.x & 7;
+  const int64_t n = (int64_t)H * W * 8;
+  float e[4] = {0.f, 0.f, 0.f, 0.f};   // channels 4c .. 4c+3 of this thread's unit
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i >> 3;
+    const int y = (int)(p / W), x = (int)(p - (int64_t)y * W);
+    const float4 s = fold_sum(gext, H, W, y, x, c);
+    const float v[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = 4 * c + j;
+      if (k < d_f) g_blend[p * blend_stride + 3 + k] += v[j];
+      e[j] += v[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float t = e[j];
+    t += __shfl_xor_sync(0xffffffffu, t, 8);
+    t += __shfl_xor_sync(0xffffffffu, t, 16);
+    const int k = 4 * c + j - d_f - 3;   // embedding slot
+    if ((threadIdx.x & 31) < 8 && k >= 0 && k < 8) atomicAdd(&sEmb[k], t);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) atomicAdd(g_emb + threadIdx.x, sEmb[threadIdx.x]);
+}
+
+// head backward, 8 threads per pixel (thread = one 16-byte channel unit): from dL/dimage, dL/drgb (added to the blend
+// gradient), dL/dh2, and the head's parameter gradients (kept in registers over the grid-stride loop, then reduced)
 __global__ void __launch_bounds__(256) k_dec_head_bwd(int64_t P, const float* __restrict__ h2, const float* __restrict__ head,
                                                        const float* __restrict__ blend, int blend_stride,
                                                        const float* __restrict__ g_image, float* __restrict__ g_blend,
                                                        float* __restrict__ g_h2, float* __restrict__ g_head) {
-  __shared__ float sHead[198];
   __shared__ float sAcc[198];
-  for (int i = threadIdx.x; i < 198; i += blockDim.x) { sHead[i] = head[i]; sAcc[i] = 0.f; }
+  for (int i = threadIdx.x; i < 198; i += blockDim.x) sAcc[i] = 0.f;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < P; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = base + threadIdx.x;
+  const int c = threadIdx.x & 7;
+  float wh[6][4], bh[3], wacc[6][4], bacc[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    bacc[q] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { wh[q][j] = __ldg(head + q * 32 + 4 * c + j); wacc[q][j] = 0.f; }
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) bh[q] = __ldg(head + 192 + q);
+  const int64_t n_groups = (P + 31) / 32;
+  for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const int64_t p = grp * 32 + (threadIdx.x >> 3);
     const bool live = p < P;
-    float h[32], gy[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) h = __ldg(reinterpret_cast<const float4*>(h2 + p * 32) + c);
+    float gy[6];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) h[k] = 0.f;
-    if (live) {
-      const float4* hp = reinterpret_cast<const float4*>(h2 + p * 32);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) { const float4 t = __ldg(hp + c); h[4 * c] = t.x; h[4 * c + 1] = t.y; h[4 * c + 2] = t.z; h[4 * c + 3] = t.w; }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float y = sHead[192 + c];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) y = fmaf(sHead[c * 32 + k], h[k], y);
-        const float g = __ldg(g_image + 3 * p + c);
-        g_blend[p * blend_stride + c] += g * (1.f + y);
-        gy[c] = g * __ldg(blend + p * blend_stride + c);
-        gy[3 + c] = g;
-      }
-      float4* gp = reinterpret_cast<float4*>(g_h2 + p * 32);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        float o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float t = 0.f;
-#pragma unroll
-          for (int q = 0; q < 6; ++q) t = fmaf(gy[q], sHead[q * 32 + 4 * c + j], t);
-          o[j] = t;
-        }
-        gp[c] = make_float4(o[0], o[1], o[2], o[3]);
-      }
+    for (int q = 0; q < 3; ++q) {
+      float y = wh[q][0] * h.x + wh[q][1] * h.y + wh[q][2] * h.z + wh[q][3] * h.w;
+      y += __shfl_xor_sync(0xffffffffu, y, 1);
+      y += __shfl_xor_sync(0xffffffffu, y, 2);
+      y += __shfl_xor_sync(0xffffffffu, y, 4);
+      y += bh[q];
+      const float g = live ? __ldg(g_image + 3 * p + q) : 0.f;
+      if (live && c == q) g_blend[p * blend_stride + q] += g * (1.f + y);
+      gy[q] = live ? g * __ldg(blend + p * blend_stride + q) : 0.f;
+      gy[3 + q] = g;
     }
-    // parameter gradients: warp-reduce gy[q] * h[k] and gy[q]
+    if (live) {
+      float o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float t = 0.f;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) t = fmaf(gy[q], wh[q][j], t);
+        o[j] = t;
+      }
+      reinterpret_cast<float4*>(g_h2 + p * 32)[c] = make_float4(o[0], o[1], o[2], o[3]);
+    }
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
-#pragma unroll 4
-      for (int k = 0; k < 32; ++k) {
-        float t = gy[q] * h[k];
-#pragma unroll
-        for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-        if (lane == 0) atomicAdd(&sAcc[q * 32 + k], t);
-      }
-      float t = gy[q];
-#pragma unroll
-      for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-      if (lane == 0) atomicAdd(&sAcc[192 + q], t);
+      wacc[q][0] = fmaf(gy[q], h.x, wacc[q][0]); wacc[q][1] = fmaf(gy[q], h.y, wacc[q][1]);
+      wacc[q][2] = fmaf(gy[q], h.z, wacc[q][2]); wacc[q][3] = fmaf(gy[q], h.w, wacc[q][3]);
+      bacc[q] += gy[q];
     }
+  }
+  // lanes of equal channel unit (xor 8, 16), then the block, then one atomic per parameter and CTA
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float t = wacc[q][j];
+      t += __shfl_xor_sync(0xffffffffu, t, 8);
+      t += __shfl_xor_sync(0xffffffffu, t, 16);
+      if ((threadIdx.x & 31) < 8) atomicAdd(&sAcc[q * 32 + 4 * c + j], t);
+    }
+    float t = bacc[q];
+    t += __shfl_xor_sync(0xffffffffu, t, 8);
+    t += __shfl_xor_sync(0xffffffffu, t, 16);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&sAcc[192 + q], t);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 198; i += blockDim.x) atomicAdd(g_head + i, sAcc[i]);
-}
-
-// gradient of the decoder input: feature slots are added to the blend gradient, embedding slots summed over pixels
-__global__ void __launch_bounds__(256) k_dec_input_bwd(int64_t P, int d_f, const float* __restrict__ g_x0,
-                                                        float* __restrict__ g_blend, int blend_stride, float* __restrict__ g_emb) {
-  __shared__ float sEmb[8];
-  if (threadIdx.x < 8) sEmb[threadIdx.x] = 0.f;
-  __syncthreads();
-  float e[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
-    const float* g = g_x0 + p * 32;
-    for (int k = 0; k < d_f; ++k) g_blend[p * blend_stride + 3 + k] += __ldg(g + k);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) e[k] += __ldg(g + d_f + 3 + k);
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    float t = e[k];
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&sEmb[k], t);
-  }
-  __syncthreads();
-  if (threadIdx.x < 8) atomicAdd(g_emb + threadIdx.x, sEmb[threadIdx.x]);
 }
 
 int sm_count() {
@@ -605,12 +668,16 @@ void launch_wgrad(const float* x, const float* gy, float* gw, int H, int W, int 
 }
 
 // g_x = mask(x) . fold(convT(g_y)) + add: transposed weights -> tensor-core convolution on the grown domain -> fold
-void launch_dgrad(const float* gy, const float* w, float* wt, float* gext, const float* x_mask, const float* add, float* gx,
-                  int H, int W, int* err, cudaStream_t st) {
+void launch_dgrad_conv(const float* gy, const float* w, float* wt, float* gext, int H, int W, int* err, cudaStream_t st) {
   k_dec_transpose_w<<<(9248 + 255) / 256, 256, 0, st>>>(w, wt);
   ConvArgs a{};
   a.x = gy; a.w = wt; a.y = gext; a.H = H; a.W = W; a.ext = 1; a.err = err;
   launch_conv<false>(a, st);
+}
+
+void launch_dgrad(const float* gy, const float* w, float* wt, float* gext, const float* x_mask, const float* add, float* gx,
+                  int H, int W, int* err, cudaStream_t st) {
+  launch_dgrad_conv(gy, w, wt, gext, H, W, err, st);
   const int64_t units = (int64_t)H * W * 8;
   k_dec_fold<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(H, W, gext, x_mask, add, gx);
 }
@@ -677,9 +744,9 @@ int launch_conv_decoder_backward(const float* params, int H, int W, int d_f, con
   launch_dgrad(g1, params + 9248, wt, gext, h0, g2, g0, H, W, err, st);               // g0 = dL/dh0
   // stem: h0 = conv0(x0)
   launch_wgrad(x0, g0, g_params, H, W, 0, err, st);
-  launch_dgrad(g0, params, wt, gext, nullptr, nullptr, g1, H, W, err, st);            // g1 = dL/dx0
-  k_dec_input_bwd<<<grid, 256, 0, st>>>(P, d_f, g1, g_blend, blend_stride, g_emb);
-  return 2 + 5 * 4;
+  launch_dgrad_conv(g0, params, wt, gext, H, W, err, st);                             // dL/dx0 on the grown domain
+  k_dec_fold_input<<<grid, 256, 0, st>>>(H, W, d_f, gext, g_blend, blend_stride, g_emb);
+  return 1 + 5 * 4;
 }
 
 }  // namespace sb
