@@ -36,8 +36,7 @@ constexpr int kCXUnits = 8 * kCPlane;          // halo: 66,688 B
 constexpr int kCWUnits = 9 * 8 * 32;           // weights: 36,864 B
 constexpr int kCThreads = 256;                 // warp w: tile row w / 4, TMEM lanes 32 (w % 4) ..
 constexpr int kCTmemCols = 32 * kCTR;          // 64
-constexpr int kCSmemBytes = (kCXUnits + kCWUnits) * 16 + 32 * 4 + 256 * 4 + 64;
-constexpr int kCSpin = 1 << 22;
+constexpr int kCTries = 1 << 14;                // bounded wait on the MMA completion barrier
 
 // tcgen05 instruction descriptor: D = f32 (bits 4-5 = 1), A = B = tf32 (bits 7-9, 10-12 = 2), both K-major (bits 15,
 // 16 = 0), N >> 3 at bit 17, M >> 4 at bit 24
@@ -102,36 +101,79 @@ struct ConvArgs {
   int blend_stride;
   float* image;          // P x 3
   float* h2;             // trunk output kept for the backward (may be null)
-  int* err;              // set to 1 if the MMA completion barrier timed out
+  int* err;              // set to 1 if a pipeline barrier timed out
 };
 
+// ---- mbarrier helpers (bounded waits: a protocol mistake must not hang the device) ----
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 t;\n\tmbarrier.arrive.shared::cta.b64 t, [%0];\n\t}\n" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (int tries = 0; tries < kCTries && !done; ++tries)   // try_wait suspends the warp: no issue slots burnt
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" :: "r"(bar) : "memory");
+}
+
+// Warp-specialised, persistent, one CTA per SM. Three roles run a tile apart from each other:
+//   warps 8..15  producers: stage tile i+1's halo into the other halo buffer          (full[s] / empty[s])
+//   warp 16      one lane issues tile i's 72 MMAs into accumulator set i & 1          (tfull[s] / tempty[s])
+//   warps 0..7   epilogue of tile i-1: TMEM -> registers -> shared-memory transpose -> coalesced global stores
+#ifndef SB_PROD_WARPS
+#define SB_PROD_WARPS 6
+#endif
+constexpr int kWsEpiWarps = 8, kWsProdWarps = SB_PROD_WARPS;   // epilogue warp w: tile row w / 4, TMEM lanes 32 (w % 4) ..
+constexpr int kWsThreads = 32 * (kWsEpiWarps + kWsProdWarps + 1);   // 416
+constexpr int kWsEpiFloats = 32 * 32;                               // per epilogue warp: 32 pixels x 32 channels
+constexpr int kWsSmemBytes = (2 * kCXUnits + kCWUnits) * 16 + kWsEpiWarps * kWsEpiFloats * 4 + 32 * 4 + 256 * 4 + 128;
+
 template <bool kHead>
-__global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
+__global__ void __launch_bounds__(kWsThreads, 1) k_conv3x3_tc(ConvArgs a) {
+  static_assert(kWsEpiWarps == 4 * kCTR, "one epilogue warp per (tile row, TMEM lane quarter)");
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float4* sX = reinterpret_cast<float4*>(smem_raw);
-  float4* sW = sX + kCXUnits;
-  float* sBias = reinterpret_cast<float*>(sW + kCWUnits);
-  float* sHead = sBias + 32;                                    // 198 used
-  uint64_t* sBar = reinterpret_cast<uint64_t*>(sHead + 256);
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 1);
+  float4* sX = reinterpret_cast<float4*>(smem_raw);              // two halo buffers
+  float4* sW = sX + 2 * kCXUnits;
+  float* sEpi = reinterpret_cast<float*>(sW + kCWUnits);         // [4 warps][32 px][32 ch], 16-byte units XOR-swizzled
+  float* sBias = sEpi + kWsEpiWarps * kWsEpiFloats;
+  float* sHead = sBias + 32;                                     // 198 used
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sHead + 256);     // full[2], empty[2], tfull[2], tempty[2]
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Ho = a.H + 2 * a.ext, Wo = a.W + 2 * a.ext;  // output domain
   const int tiles_x = (Wo + kCTW - 1) / kCTW, tiles_y = (Ho + kCTR - 1) / kCTR;
   const int n_tiles = tiles_x * tiles_y;
+  const uint32_t bar0 = smem_u32(sBar);
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 16u + 8u * s; };
+  auto tfull = [&](int s) { return bar0 + 32u + 8u * s; };
+  auto tempty = [&](int s) { return bar0 + 48u + 8u * s; };
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" :: "r"(smem_u32(sTmem)), "r"(kCTmemCols) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" :: "r"(smem_u32(sTmem)), "r"(2 * kCTmemCols) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(sBar)) : "memory");
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(full(s), 32 * kWsProdWarps);
+      mbar_init(empty(s), 1);
+      mbar_init(tfull(s), 1);
+      mbar_init(tempty(s), 32 * kWsEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // the layer's weights, once per CTA: unit ((tap * 8 + c) * 32 + co) = W[co][tap][4c .. 4c+3]
   {
     const float4* gw = reinterpret_cast<const float4*>(a.w);
-    for (int i = tid; i < kCWUnits; i += kCThreads) {
+    for (int i = tid; i < kCWUnits; i += kWsThreads) {
       const int co = i / 72, rem = i - co * 72, tap = rem >> 3, c = rem & 7;
       float4 v = __ldg(gw + i);
       v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
@@ -139,132 +181,170 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_tc(ConvArgs a) {
     }
     if (tid < 32) sBias[tid] = __ldg(a.w + 9216 + tid);
     if (kHead)
-      for (int i = tid; i < 198; i += kCThreads) sHead[i] = __ldg(a.head + i);
+      for (int i = tid; i < 198; i += kWsThreads) sHead[i] = __ldg(a.head + i);
   }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem_base = *sTmem;
-  const uint32_t x_addr = smem_u32(sX), w_addr = smem_u32(sW), bar_addr = smem_u32(sBar);
-  // K-major, no swizzle: leading offset = distance between the two 16-byte K chunks, stride offset = 8-row groups
-  constexpr uint32_t a_lbo = (uint32_t)kCPlane * 16u, a_sbo = 128u;
-  constexpr uint32_t b_lbo = 512u, b_sbo = 128u;
-  uint32_t phase = 0;
+  bool ok = true;
 
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    const int x0 = tx * kCTW, y0 = ty * kCTR;
-    // ---- stage the halo: 4 rows x 130 pixels x 8 units, reflect padding, optional ReLU, tf32 rounding ----
-    // (eight loads in flight per thread: the staging is latency-bound otherwise)
-    constexpr int kItems = kCHR * kCHW * 8;
-#pragma unroll 1
-    for (int i0 = tid; i0 < kItems; i0 += 8 * kCThreads) {
-      float4 v[8];
+  if (warp >= kWsEpiWarps && warp < kWsEpiWarps + kWsProdWarps) {
+    // =============================== producers ===============================
+    const int t = tid - 32 * kWsEpiWarps;
+    const int c = t & 7, pl = t >> 3;
+    const float relu_floor = a.relu_in ? 0.f : -INFINITY;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int s = it & 1;
+      const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+      const int x0 = tx * kCTW, y0 = ty * kCTR;
+      if (!mbar_wait(empty(s), ((it >> 1) & 1) ^ 1)) { ok = false; break; }
+      float4* dstX = sX + s * kCXUnits;
+      constexpr int kPl = 4 * kWsProdWarps;                 // pixel lanes
+      constexpr int kPxIters = (kCHW + kPl - 1) / kPl;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * kCThreads;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < kItems) {
-          const int c = i & 7, hp = i >> 3;
-          const int row = hp / kCHW, px = hp - row * kCHW;
-          int gy = y0 - 1 + row - a.ext, gx = x0 - 1 + px - a.ext;
-          const bool outside = gy < 0 || gy >= a.H || gx < 0 || gx >= a.W;
-          gy = reflect_clamped(gy, a.H); gx = reflect_clamped(gx, a.W);
-          if (!(a.ext && outside)) v[u] = __ldg(reinterpret_cast<const float4*>(a.x + ((int64_t)gy * a.W + gx) * 32) + c);
+      for (int r0 = 0; r0 < kCHR; r0 += 2) {
+        float4 v[2][kPxIters];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          int gy = y0 - 1 + r0 + rr - a.ext;
+          const bool row_out = a.ext && (gy < 0 || gy >= a.H);
+          gy = reflect_clamped(gy, a.H);
+          const float4* rowp = reinterpret_cast<const float4*>(a.x + (int64_t)gy * a.W * 32) + c;
+#pragma unroll
+          for (int k = 0; k < kPxIters; ++k) {
+            const int px = pl + kPl * k;
+            int gx = x0 - 1 + px - a.ext;
+            const bool out = row_out || (a.ext && (gx < 0 || gx >= a.W));
+            gx = reflect_clamped(gx, a.W);
+            v[rr][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (px < kCHW && !out) v[rr][k] = __ldg(rowp + gx * 8);
+          }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * kCThreads;
-        if (i < kItems) {
-          float4 t = v[u];
-          if (a.relu_in) { t.x = fmaxf(t.x, 0.f); t.y = fmaxf(t.y, 0.f); t.z = fmaxf(t.z, 0.f); t.w = fmaxf(t.w, 0.f); }
-          t.x = to_tf32(t.x); t.y = to_tf32(t.y); t.z = to_tf32(t.z); t.w = to_tf32(t.w);
-          sX[(i & 7) * kCPlane + (i >> 3)] = t;
-        }
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy stores -> tensor-core reads
-    __syncthreads();
-    // ---- one thread issues the tile's 2 x 9 x 4 MMAs (128 x 32 x 8 each) and commits them to the barrier ----
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
-      for (int r = 0; r < kCTR; ++r) {
-#pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const int ky = tap / 3, kx = tap - 3 * ky;
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint32_t aa = x_addr + (uint32_t)((2 * ks) * kCPlane + (r + ky) * kCHW + kx) * 16u;
-            const uint32_t bb = w_addr + (uint32_t)((tap * 8 + 2 * ks) * 32) * 16u;
-            mma_tf32(tmem_base + (uint32_t)(r * 32), smem_desc(aa, a_lbo, a_sbo), smem_desc(bb, b_lbo, b_sbo),
-                     (tap | ks) != 0);
+          for (int k = 0; k < kPxIters; ++k) {
+            const int px = pl + kPl * k;
+            if (px < kCHW) {
+              float4 q = v[rr][k];
+              q.x = to_tf32(fmaxf(q.x, relu_floor)); q.y = to_tf32(fmaxf(q.y, relu_floor));
+              q.z = to_tf32(fmaxf(q.z, relu_floor)); q.w = to_tf32(fmaxf(q.w, relu_floor));
+              dstX[c * kCPlane + (r0 + rr) * kCHW + px] = q;
+            }
           }
         }
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" :: "r"(bar_addr) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy stores -> tensor-core reads
+      mbar_arrive(full(s));
     }
-    // ---- wait for the MMAs (bounded: a descriptor mistake must not hang the device) ----
-    {
-      uint32_t done = 0;
-      for (int spin = 0; spin < kCSpin && !done; ++spin)
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-            : "=r"(done) : "r"(bar_addr), "r"(phase) : "memory");
-      if (!__syncthreads_and((int)done)) {
-        if (tid == 0 && a.err) *a.err = 1;
-        break;
+  } else if (warp == kWsEpiWarps + kWsProdWarps) {
+    // =============================== MMA issuer (one lane) ===============================
+    if (lane == 0) {
+      const uint32_t w_addr = smem_u32(sW);
+      constexpr uint32_t a_lbo = (uint32_t)kCPlane * 16u, a_sbo = 128u, b_lbo = 512u, b_sbo = 128u;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int s = it & 1;
+        const uint32_t par = (it >> 1) & 1;
+        if (!mbar_wait(tempty(s), par ^ 1) || !mbar_wait(full(s), par)) { ok = false; break; }
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t x_addr = smem_u32(sX + s * kCXUnits);
+        const uint32_t d_addr = tmem_base + (uint32_t)(s * kCTmemCols);
+#pragma unroll
+        for (int r = 0; r < kCTR; ++r) {
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int ky = tap / 3, kx = tap - 3 * ky;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint32_t aa = x_addr + (uint32_t)((2 * ks) * kCPlane + (r + ky) * kCHW + kx) * 16u;
+              const uint32_t bb = w_addr + (uint32_t)((tap * 8 + 2 * ks) * 32) * 16u;
+              mma_tf32(d_addr + (uint32_t)(r * 32), smem_desc(aa, a_lbo, a_sbo), smem_desc(bb, b_lbo, b_sbo), (tap | ks) != 0);
+            }
+          }
+        }
+        umma_commit(empty(s));    // halo buffer s may be refilled once these MMAs have read it
+        umma_commit(tfull(s));    // accumulator set s is complete
       }
-      phase ^= 1u;
     }
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    // ---- epilogue: warp w reads row w / 4, pixels 32 (w % 4) + lane; one pixel's 32 channels per thread ----
-    {
-      const int r = warp >> 2, q = warp & 3;
-      float acc[32];
-      tmem_load32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(r * 32), acc);
-      const int gx = x0 + q * 32 + lane, gy = y0 + r;
-      if (gx < Wo && gy < Ho) {
-        const int64_t p = (int64_t)gy * Wo + gx;
+    __syncwarp();
+  } else if (warp < kWsEpiWarps) {
+    // =============================== epilogue ===============================
+    float* my = sEpi + warp * kWsEpiFloats;
+    const int cq = lane & 7, pq = lane >> 3;      // coalesced phase: 16-byte unit, pixel within a group of 4
+    const float4 bias4 = reinterpret_cast<const float4*>(sBias)[cq];
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int s = it & 1;
+      const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+      const int x0 = tx * kCTW, y0 = ty * kCTR;
+      if (!mbar_wait(tfull(s), (it >> 1) & 1)) { ok = false; break; }
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      {
+        const int r = warp >> 2, wq = warp & 3;
+        float acc[32];
+        tmem_load32(tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(s * kCTmemCols + r * 32), acc);
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        mbar_arrive(tempty(s));   // the accumulators are in registers: hand the set back
+        // lane = pixel -> shared memory (unit c of pixel l at c ^ (l & 7)) -> lane = (pixel group, unit)
+        __syncwarp();
 #pragma unroll
-        for (int k = 0; k < 32; ++k) acc[k] += sBias[k];
-        if (a.res) {
-          const float4* rp = reinterpret_cast<const float4*>(a.res + p * 32);
+        for (int c = 0; c < 8; ++c)
+          reinterpret_cast<float4*>(my)[lane * 8 + (c ^ (lane & 7))] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+        __syncwarp();
+        const int gy = y0 + r;
+        const int gx0 = x0 + wq * 32;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 t = __ldg(rp + c);
-            acc[4 * c] += t.x; acc[4 * c + 1] += t.y; acc[4 * c + 2] += t.z; acc[4 * c + 3] += t.w;
+        for (int k = 0; k < 8; ++k) {
+          const int l = 4 * k + pq;
+          float4 v = reinterpret_cast<float4*>(my)[l * 8 + (cq ^ (l & 7))];
+          v.x += bias4.x; v.y += bias4.y; v.z += bias4.z; v.w += bias4.w;
+          const int gx = gx0 + l;
+          const bool live = gx < Wo && gy < Ho;
+          const int64_t p = (int64_t)gy * Wo + gx;
+          if (live && a.res) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(a.res + p * 32) + cq);
+            v.x += q.x; v.y += q.y; v.z += q.z; v.w += q.w;
+          }
+          if (kHead) {
+            if (live && a.h2) reinterpret_cast<float4*>(a.h2 + p * 32)[cq] = v;
+            reinterpret_cast<float4*>(my)[l * 8 + (cq ^ (l & 7))] = v;   // back for the per-pixel head
+          } else if (live) {
+            reinterpret_cast<float4*>(a.y + p * 32)[cq] = v;
           }
         }
         if (kHead) {
-          if (a.h2) {
-            float4* hp = reinterpret_cast<float4*>(a.h2 + p * 32);
+          __syncwarp();
+          const int gx = gx0 + lane;
+          if (gx < Wo && gy < Ho) {
+            const int64_t p = (int64_t)gy * Wo + gx;
+            float y6[6];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) hp[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+            for (int o = 0; o < 6; ++o) y6[o] = sHead[192 + o];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 h = reinterpret_cast<float4*>(my)[lane * 8 + (c ^ (lane & 7))];
+#pragma unroll
+              for (int o = 0; o < 6; ++o) {
+                const float4 w4 = reinterpret_cast<const float4*>(sHead + o * 32)[c];
+                y6[o] = fmaf(w4.x, h.x, fmaf(w4.y, h.y, fmaf(w4.z, h.z, fmaf(w4.w, h.w, y6[o]))));
+              }
+            }
+            const float* rgb = a.blend + p * a.blend_stride;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) a.image[3 * p + c] = fmaf(1.f + y6[c], __ldg(rgb + c), y6[3 + c]);
           }
-          float y6[6];
-#pragma unroll
-          for (int o = 0; o < 6; ++o) {
-            float s = sHead[192 + o];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) s = fmaf(sHead[o * 32 + k], acc[k], s);
-            y6[o] = s;
-          }
-          const float* rgb = a.blend + p * a.blend_stride;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) a.image[3 * p + c] = fmaf(1.f + y6[c], __ldg(rgb + c), y6[3 + c]);
-        } else {
-          float4* yp = reinterpret_cast<float4*>(a.y + p * 32);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) yp[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
         }
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();  // accumulators read and halo consumed: both free for the next tile
   }
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem_base), "r"(kCTmemCols) : "memory");
+  if (!ok && a.err) *a.err = 1;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem_base), "r"(2 * kCTmemCols) : "memory");
 }
 
 // x0 = (feature, ray direction, embedding, 0 ...): one thread per (pixel, 16-byte unit)
@@ -303,16 +383,16 @@ int conv_grid(int H, int W) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = ((W + kCTW - 1) / kCTW) * ((H + kCTR - 1) / kCTR);
-  return tiles < 2 * sms ? tiles : 2 * sms;
+  return tiles < sms ? tiles : sms;
 }
 
 template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
   static bool once = false;
   if (!once) {
-    cudaFuncSetAttribute(k_conv3x3_tc<kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemBytes);
+    cudaFuncSetAttribute(k_conv3x3_tc<kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmemBytes);
     once = true;
   }
-  k_conv3x3_tc<kHead><<<conv_grid(a.H + 2 * a.ext, a.W + 2 * a.ext), kCThreads, kCSmemBytes, st>>>(a);
+  k_conv3x3_tc<kHead><<<conv_grid(a.H + 2 * a.ext, a.W + 2 * a.ext), kWsThreads, kWsSmemBytes, st>>>(a);
 }
 
 
@@ -437,9 +517,9 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
     accumulate = 1;
     {
       uint32_t done = 0;
-      for (int spin = 0; spin < kCSpin && !done; ++spin)
+      for (int tries = 0; tries < kCTries && !done; ++tries)   // try_wait suspends the warp: no issue slots burnt
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
             : "=r"(done) : "r"(bar_addr), "r"(phase) : "memory");
       if (!__syncthreads_and((int)done)) {
         if (tid == 0 && a.err) *a.err = 1;
