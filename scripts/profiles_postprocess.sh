@@ -33,6 +33,11 @@ for k in "k_raster_fwd<(bool)0" "k_raster_fwd<(bool)1" "k_raster_bwd<(bool)0" "k
   echo "#### $k" >> "$P/ncu_source_lines_${TAG}.txt"
   python scripts/ncu_lines.py /tmp/prof_${TAG}_src.csv "$k" 25 >> "$P/ncu_source_lines_${TAG}.txt"
 done
+if [ -f "$G/launches_decoder_${TAG}.csv" ]; then
+  cp "$G/launches_decoder_${TAG}.csv" "$G/decoder_${TAG}.txt" "$P/"
+  ncu -i "$G/prof_decoder_${TAG}.ncu-rep" --page raw --csv > /tmp/prof_decoder_${TAG}_raw.csv
+  python scripts/ncu_summary.py /tmp/prof_decoder_${TAG}_raw.csv > "$P/ncu_full_decoder_${TAG}.txt"
+fi
 for t in memcheck racecheck; do
   grep -E "COMPUTE-SANITIZER|passed|failed|ERROR SUMMARY|RACECHECK SUMMARY|hazard" "$G/sanitizer_${t}_${TAG}.log" | tail -6 > "$P/sanitizer_${t}_${TAG}.log" || true
 done
