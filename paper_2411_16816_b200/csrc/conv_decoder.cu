@@ -36,7 +36,7 @@ constexpr int kCXUnits = 8 * kCPlane;          // halo: 66,688 B
 constexpr int kCWUnits = 9 * 8 * 32;           // weights: 36,864 B
 constexpr int kCThreads = 256;                 // warp w: tile row w / 4, TMEM lanes 32 (w % 4) ..
 constexpr int kCTmemCols = 32 * kCTR;          // 64
-constexpr int kCTries = 1 << 14;                // bounded wait on the MMA completion barrier
+constexpr int kCTries = 1 << 18;                // bounded wait on the MMA completion barrier
 
 // tcgen05 instruction descriptor: D = f32 (bits 4-5 = 1), A = B = tf32 (bits 7-9, 10-12 = 2), both K-major (bits 15,
 // 16 = 0), N >> 3 at bit 17, M >> 4 at bit 24
@@ -376,9 +376,12 @@ __global__ void __launch_bounds__(256) k_decoder_input(int H, int W, int d_f, fl
   const int64_t p = i >> 3;
   const int c = (int)(i & 7);
   const int v = (int)(p / W), u = (int)(p - (int64_t)v * W);
-  // scene.hpp:119-122
-  const float da = (float(u) + 0.5f - cx) / fx, db = (float(v) + 0.5f - cy) / fy;
-  const float inv = 1.f / sqrtf(da * da + db * db + 1.f);
+  // scene.hpp:119-122 (only the units that hold a direction channel pay for it)
+  float da = 0.f, db = 0.f, inv = 0.f;
+  if (4 * c + 3 >= d_f && 4 * c < d_f + 3) {
+    da = (float(u) + 0.5f - cx) / fx; db = (float(v) + 0.5f - cy) / fy;
+    inv = 1.f / sqrtf(da * da + db * db + 1.f);
+  }
   float out[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -420,19 +423,21 @@ template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
 //   g_w[co][ky][kx][ci] = sum_p g_y[p][co] * xr[reflect(p + (ky-1, kx-1))][ci],  xr = relu_in ? relu(x) : x.
 // The reduction runs over pixels, so pixels are the K dimension: both operands are transposed while they are staged
 // (channel rows, 4 consecutive pixels per 16-byte unit — K-major again; the MN-major operand forms returned zeros for
-// tf32 on this part, measured with either swizzle mode). One tile = 64 pixels of one image row:
-//   A [(ky, ci) 128 rows][q 72]  = halo row ky (y0-1+ky), halo pixel q (x0-1+q); rows 96..127 ("ky = 3") stay zero
-//   B_kx [co 32][q 72]           = g_y[pixel q - kx][co]   — three shifted copies, one per filter column
-//   D_kx[(ky, ci)][co] += A . B_kx^T   — 9 instructions of 128 x 32 x 8 per kx
-// D stays in tensor memory across all the tiles of the persistent CTA (3 x 32 columns) and is added to global memory
-// once, at the end.
+// tf32 on this part, measured with either swizzle mode). One tile = 64 pixels of two image rows y0, y0+1:
+//   A [(h, ci) 128 rows][q 72]   = halo row h = 0..3 (image row y0-1+h), halo pixel q (x0-1+q)
+//   B_r,kx [co 32][q 72]         = g_y[row y0+r][pixel q - kx][co]   — per output row three shifted copies (filter column)
+//   D_r,kx[(h, ci)][co] += A . B_r,kx^T   — 9 instructions of 128 x 32 x 8 each; halo row h is tap ky = h - r of row r,
+//                                            so three of the four 32-row groups of every D are weight gradients
+// The six D stay in tensor memory across all the tiles of the persistent CTA (6 x 32 columns) and are added to global
+// memory once, at the end (g_w[ky] = D_0[h = ky] + D_1[h = ky + 1]).
 constexpr int kWT = 64;                              // tile width (pixels)
 constexpr int kWQC = (kWT + 2 + 7) / 8 * 2;          // 18 K chunks of 4 pixels (72 halo pixels, the last 6 zero)
 constexpr int kWXChunk = 128 * 4 + 4;                // floats per K chunk of A (+16 B: conflict-free transposed stores)
 constexpr int kWGChunk = 32 * 4 + 4;                 // floats per K chunk of B
 constexpr int kWXFloats = kWQC * kWXChunk;           // 37,152 B
 constexpr int kWGFloats = kWQC * kWGChunk;           // 9,504 B per shifted copy
-constexpr int kWSmemBytes = (kWXFloats + 3 * kWGFloats) * 4 + 8 * 32 * 4 + 64;
+constexpr int kWSmemBytes = (kWXFloats + 6 * kWGFloats) * 4 + 8 * 32 * 4 + 64;   // 94 KB: two CTAs per SM
+constexpr int kWTmemCols = 256;                      // 6 x 32 used
 
 struct WgradArgs {
   const float* x;      // H x W x 32, input of the convolution
@@ -442,26 +447,26 @@ struct WgradArgs {
   int* err;
 };
 
-__global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) {
+__global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sX = reinterpret_cast<float*>(smem_raw);
   float* sG = sX + kWXFloats;
-  float* sRed = sG + 3 * kWGFloats;                            // [8 warps][32]
+  float* sRed = sG + 6 * kWGFloats;                            // [8 warps][32]
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sRed + 256);
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tiles_x = (a.W + kWT - 1) / kWT;
-  const int n_tiles = tiles_x * a.H;
+  const int n_tiles = tiles_x * ((a.H + 1) / 2);
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" :: "r"(smem_u32(sTmem)), "r"(128) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" :: "r"(smem_u32(sTmem)), "r"(kWTmemCols) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(sBar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int i = tid; i < kWXFloats + 3 * kWGFloats; i += kCThreads) sX[i] = 0.f;   // pads, the 4th row group
+  for (int i = tid; i < kWXFloats + 6 * kWGFloats; i += kCThreads) sX[i] = 0.f;   // pads
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -472,14 +477,15 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
   bool ok = true;
 
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int y0 = tile / tiles_x, x0 = (tile - y0 * tiles_x) * kWT;
-    // halo rows y0-1 .. y0+1, pixels x0-1 .. x0+64, transposed: float (q / 4, ky * 32 + ci, q % 4). A warp covers
+    const int ty = tile / tiles_x;
+    const int y0 = 2 * ty, x0 = (tile - ty * tiles_x) * kWT;
+    // halo rows y0-1 .. y0+2, pixels x0-1 .. x0+64, transposed: float (q / 4, h * 32 + ci, q % 4). A warp covers
     // 2 channel units x 16 pixels: 32-byte sectors from global memory, 32 distinct banks per transposed store.
     {
-      constexpr int kItems = 3 * 5 * 128;   // rows x (5 x 16 pixels, 66 used) x (16 px x 8 units)
-      float4 v[8];
+      constexpr int kItems = 4 * 5 * 128;   // rows x (5 x 16 pixels, 66 used) x (16 px x 8 units): 10 per thread
+      float4 v[10];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 10; ++u) {
         const int i = tid + u * kCThreads;
         const int c = ((i >> 5) & 3) * 2 + (i & 1), blk = i >> 7;
         const int row = blk / 5, q = (blk - row * 5) * 16 + ((i >> 1) & 15);
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 10; ++u) {
         const int i = tid + u * kCThreads;
         const int c = ((i >> 5) & 3) * 2 + (i & 1), blk = i >> 7;
         const int row = blk / 5, q = (blk - row * 5) * 16 + ((i >> 1) & 15);
@@ -502,19 +508,28 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
         }
       }
     }
+    {
+      float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = tid + u * kCThreads;
-      const int c = ((i >> 5) & 3) * 2 + (i & 1), px = (i >> 7) * 16 + ((i >> 1) & 15);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (x0 + px < a.W) v = __ldg(reinterpret_cast<const float4*>(a.gy + ((int64_t)y0 * a.W + x0 + px) * 32) + c);
-      bsum.x += v.x; bsum.y += v.y; bsum.z += v.z; bsum.w += v.w;
-      v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
+      for (int u = 0; u < 4; ++u) {
+        const int i = tid + u * kCThreads;
+        const int c = ((i >> 5) & 3) * 2 + (i & 1), px = ((i >> 7) & 3) * 16 + ((i >> 1) & 15), r = i >> 9;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (x0 + px < a.W && y0 + r < a.H) v[u] = __ldg(reinterpret_cast<const float4*>(a.gy + ((int64_t)(y0 + r) * a.W + x0 + px) * 32) + c);
+      }
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) {
-        const int q = px + kx;
-        float* dst = sG + kx * kWGFloats + (q >> 2) * kWGChunk + (4 * c) * 4 + (q & 3);
-        dst[0] = v.x; dst[4] = v.y; dst[8] = v.z; dst[12] = v.w;
+      for (int u = 0; u < 4; ++u) {
+        const int i = tid + u * kCThreads;
+        const int c = ((i >> 5) & 3) * 2 + (i & 1), px = ((i >> 7) & 3) * 16 + ((i >> 1) & 15), r = i >> 9;
+        float4 t = v[u];
+        bsum.x += t.x; bsum.y += t.y; bsum.z += t.z; bsum.w += t.w;
+        t.x = to_tf32(t.x); t.y = to_tf32(t.y); t.z = to_tf32(t.z); t.w = to_tf32(t.w);
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const int q = px + kx;
+          float* dst = sG + (r * 3 + kx) * kWGFloats + (q >> 2) * kWGChunk + (4 * c) * 4 + (q & 3);
+          dst[0] = t.x; dst[4] = t.y; dst[8] = t.z; dst[12] = t.w;
+        }
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -524,7 +539,7 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
 #pragma unroll 1
       for (int ks = 0; ks < kWQC / 2; ++ks) {
 #pragma unroll
-        for (int kx = 0; kx < 3; ++kx) {
+        for (int kx = 0; kx < 6; ++kx) {   // (output row r, filter column kx) = (kx / 3, kx % 3)
           const uint32_t aa = x_addr + (uint32_t)(2 * ks * kWXChunk * 4);
           const uint32_t bb = g_addr + (uint32_t)(kx * kWGFloats * 4) + (uint32_t)(2 * ks * kWGChunk * 4);
           mma_tf32(tmem_base + (uint32_t)(kx * 32), smem_desc(aa, kWXChunk * 4u, 128u), smem_desc(bb, kWGChunk * 4u, 128u),
@@ -549,15 +564,16 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
     }
   }
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  // ---- weights: warps 0..2 hold ky = warp (lanes = ci); 3 x 32 columns = (kx, co) ----
+  // ---- weights: warp h (0..3) holds halo row h (lanes = ci); 6 x 32 columns = (r, kx, co); tap ky = h - r ----
   if (ok && accumulate && warp < 4) {
 #pragma unroll 1
-    for (int kx = 0; kx < 3; ++kx) {
+    for (int rk = 0; rk < 6; ++rk) {
       float acc[32];
-      tmem_load32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(kx * 32), acc);
-      if (warp < 3) {
+      tmem_load32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(rk * 32), acc);
+      const int r = rk / 3, kx = rk - 3 * r, ky = warp - r;
+      if (ky >= 0 && ky < 3) {
 #pragma unroll
-        for (int co = 0; co < 32; ++co) atomicAdd(a.gw + ((co * 3 + warp) * 3 + kx) * 32 + lane, acc[co]);
+        for (int co = 0; co < 32; ++co) atomicAdd(a.gw + ((co * 3 + ky) * 3 + kx) * 32 + lane, acc[co]);
       }
     }
   }
@@ -578,7 +594,7 @@ __global__ void __launch_bounds__(kCThreads, 3) k_conv3x3_wgrad_tc(WgradArgs a) 
     const float t = sRed[(((c >> 1) * 2 + (c & 1)) << 2) + (tid & 3)] + sRed[((((c >> 1) + 4) * 2 + (c & 1)) << 2) + (tid & 3)];
     atomicAdd(a.gw + 9216 + tid, t);
   }
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem_base), "r"(128) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem_base), "r"(kWTmemCols) : "memory");
 }
 
 // weights of the input-gradient convolution: Wt[ci][ky][kx][co] = W[co][2-ky][2-kx][ci], zero bias
@@ -762,8 +778,8 @@ void launch_wgrad(const float* x, const float* gy, float* gw, int H, int W, int 
     once = true;
   }
   WgradArgs a{x, gy, gw, H, W, relu_in, err};
-  const int tiles = ((W + kWT - 1) / kWT) * H;
-  k_conv3x3_wgrad_tc<<<tiles < 3 * sm_count() ? tiles : 3 * sm_count(), kCThreads, kWSmemBytes, st>>>(a);
+  const int tiles = ((W + kWT - 1) / kWT) * ((H + 1) / 2);
+  k_conv3x3_wgrad_tc<<<tiles < 2 * sm_count() ? tiles : 2 * sm_count(), kCThreads, kWSmemBytes, st>>>(a);
 }
 
 // g_x = mask(x) . fold(convT(g_y)) + add: transposed weights -> tensor-core convolution on the grown domain -> fold
