@@ -288,8 +288,8 @@ int splatb200_view_decode_image(splatb200_view* v, const float* params, const fl
  * saved by the splatb200_view_decode_image call that followed the view's last forward (else SPLATB200_ERUNTIME, like
  * the rasterizer's backward without saved state). g_image: HOST, P x 3 = dL/dI. g_params: HOST,
  * splatb200_conv_decoder_params() floats, OVERWRITTEN with dL/dparams; g_embedding: HOST, 8 floats, overwritten
- * (SensorGrads::d_embedding, projection.hpp:207-222). g_blend: DEVICE, P x (3 + d_f) — dL/dF_rgb and dL/dfeature are
- * ADDED to it, so the buffer goes straight into splatb200_view_backward_device as the upstream gradient of the render.
+ * (SensorGrads::d_embedding, projection.hpp:207-222). g_blend: DEVICE, P x 16 (the blend buffer's row pitch: rgb, then d_f features) — dL/dF_rgb and
+ * dL/dfeature are ADDED to it, so the buffer goes straight into splatb200_view_backward_device as the upstream gradient of the render.
  * Weight gradients and input gradients of the five convolutions run on the tensor cores as well. */
 int splatb200_view_decode_image_backward(splatb200_view* v, const float* g_image, float* g_params, float* g_embedding,
                                          float* g_blend, float* device_ms);

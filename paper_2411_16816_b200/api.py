@@ -474,7 +474,7 @@ class View:
 
     def decode_image_backward(self, g_image, g_blend_device_ptr: int, timed=False):
         """Backward of decode_image: dL/dimage (P x 3) -> (dL/dparams, dL/dembedding[8]); dL/dF_rgb and dL/dfeature are
-        added to the DEVICE buffer (P x (3 + d_f)) at g_blend_device_ptr — the upstream gradient of view.backward_device."""
+        added to the DEVICE buffer (P x 16: rgb, then d_f features) at g_blend_device_ptr — the upstream gradient of view.backward_device."""
         g = np.ascontiguousarray(g_image, np.float32)
         assert g.size == 3 * self.P
         gp = np.zeros(self.L.splatb200_conv_decoder_params(), np.float32)

@@ -1068,7 +1068,7 @@ extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* param
     CU_TRY(c, cudaEventRecord(e0, c->stream));
   }
   const int launched = launch_conv_decoder(v->d_dec_params, d_emb, v->s.height, v->s.width, c->d_f, v->s.fx, v->s.fy, v->s.cx,
-                                           v->s.cy, v->out.blend, v->s.channels, v->dec_act, v->d_dec_image, v->d_dec_err,
+                                           v->s.cy, v->out.blend, /*row pitch of the blend buffer*/ 16, v->dec_act, v->d_dec_image, v->d_dec_err,
                                            c->stream);
   CHECK_LAUNCH(c, "k_conv3x3_tc");
   c->launches += launched;
@@ -1112,7 +1112,7 @@ extern "C" int splatb200_view_decode_image_backward(splatb200_view* v, const flo
     CU_TRY(c, cudaEventCreate(&e1));
     CU_TRY(c, cudaEventRecord(e0, c->stream));
   }
-  const int launched = launch_conv_decoder_backward(v->d_dec_params, H, W, c->d_f, v->out.blend, v->s.channels, v->dec_act,
+  const int launched = launch_conv_decoder_backward(v->d_dec_params, H, W, c->d_f, v->out.blend, /*row pitch*/ 16, v->dec_act,
                                                     v->d_dec_gimage, v->dec_g, v->dec_gext, d_wt, v->d_dec_gparams,
                                                     v->d_dec_gparams + np, g_blend, v->d_dec_err, c->stream);
   CHECK_LAUNCH(c, "conv decoder backward");

@@ -1078,8 +1078,8 @@ def test_conv3x3_tensor_core_matches_numpy(ctx, H, W):
 
 
 def _decoder_inputs(view, cam, d_f):
-    blend = view.array("blend").reshape(cam.height, cam.width, 3 + d_f)
-    return blend[..., :3], blend[..., 3:], np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float32)
+    blend = view.array("blend").reshape(cam.height, cam.width, 16)
+    return blend[..., :3], blend[..., 3:3 + d_f], np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float32)
 
 
 @pytest.mark.gpu
@@ -1181,28 +1181,28 @@ def test_conv3x3_backward_matches_numpy(ctx, H, W):
     assert np.array_equal(gx, rgx.astype(np.float32)) and np.array_equal(gw, rgw.astype(np.float32))
 
 
-@pytest.mark.parametrize("w,h", [(96, 64), (203, 77)])
-def test_decode_image_backward_matches_oracle(ctx, op, w, h):
+@pytest.mark.parametrize("w,h,d_f", [(96, 64, 13), (203, 77, 13), (70, 50, 5)])
+def test_decode_image_backward_matches_oracle(ctx, op, w, h, d_f):
     """dL/dparams, dL/dembedding, dL/dF_rgb and dL/dfeature of decode_image against the fp64 oracle backward (pinned by
     finite differences, tests/test_oracle_kat.py); the feature gradient is added into the render's upstream buffer."""
     import torch
-    sc = synth.make_scene(4000, seed=23, r_max=40.0, scale_mean=0.12)
+    sc = synth.make_scene(4000, seed=23, r_max=40.0, scale_mean=0.12, d_f=d_f)
     cam = synth.make_camera(width=w, height=h)
     ctx.upload_scene(sc)
     view = ctx.camera_view(cam, ST)
     view.forward(0.0)
-    P, d_f = view.P, sc.d_f
+    P = view.P
     rgb, feat, intr = _decoder_inputs(view, cam, d_f)
     rng = np.random.default_rng(7)
     params = rng.normal(0, 0.08, op.DEC_PARAMS).astype(np.float32)
     params[op.DEC_HEAD_OFFSET:] = rng.normal(0, 0.3, op.DEC_PARAMS - op.DEC_HEAD_OFFSET)
     emb = rng.normal(0, 1, 8).astype(np.float32)
     g_image = rng.normal(0, 1, (h, w, 3)).astype(np.float32)
-    g_up = torch.zeros((P, 3 + d_f), dtype=torch.float32, device="cuda")
+    g_up = torch.zeros((P, 16), dtype=torch.float32, device="cuda")
     with pytest.raises(Exception):                      # no saved state yet (SPEC.md:319)
         view.decode_image_backward(g_image, g_up.data_ptr())
     view.decode_image(params, emb)
-    g_up[:, 5] = 0.5                                    # another upstream gradient of the render: must be kept
+    g_up[:, 4] = 0.5                                    # another upstream gradient of the render: must be kept
     gp, ge = view.decode_image_backward(g_image, g_up.data_ptr())
     # The device gradient is the gradient of the device forward: its ReLU masks come from the tf32 activations, and
     # against white-noise dL/dI a mask flip on a near-zero activation is a full-size term of an incoherent sum. So the
@@ -1215,10 +1215,11 @@ def test_decode_image_backward_matches_oracle(ctx, op, w, h):
         err, scale = np.abs(gp[b:e] - ogp[b:e]).max(), np.abs(ogp[b:e]).max()
         assert err <= DEC_GRAD_RTOL * scale, (name, err, scale)
     assert np.abs(ge - oge).max() <= DEC_GRAD_RTOL * np.abs(oge).max()
-    gb = g_up.cpu().numpy().reshape(h, w, 3 + d_f)
-    exp = np.concatenate([ogrgb, ogf], axis=2); exp[..., 5] += 0.5
+    gb = g_up.cpu().numpy().reshape(h, w, 16)
+    exp = np.concatenate([ogrgb, ogf], axis=2); exp[..., 4] += 0.5
     assert np.abs(gb[..., :3] - exp[..., :3]).max() <= DEC_GRAD_RTOL * np.abs(exp[..., :3]).max()
-    assert np.abs(gb[..., 3:] - exp[..., 3:]).max() <= DEC_GRAD_RTOL * np.abs(exp[..., 3:]).max()
+    assert np.abs(gb[..., 3:3 + d_f] - exp[..., 3:]).max() <= DEC_GRAD_RTOL * np.abs(exp[..., 3:]).max()
+    assert not gb[..., 3 + d_f:].any()                  # slots behind the features are not touched
     # decoder + rasterizer backward in one go: the buffer is the render's upstream gradient
     ga = torch.zeros(P, dtype=torch.float32, device="cuda")
     ctx.zero_grads()
