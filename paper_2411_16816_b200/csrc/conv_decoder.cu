@@ -433,10 +433,10 @@ template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
 constexpr int kWT = 64;                              // tile width (pixels)
 constexpr int kWQC = (kWT + 2 + 7) / 8 * 2;          // 18 K chunks of 4 pixels (72 halo pixels, the last 6 zero)
 constexpr int kWXChunk = 128 * 4 + 4;                // floats per K chunk of A (+16 B: conflict-free transposed stores)
-constexpr int kWGChunk = 32 * 4 + 4;                 // floats per K chunk of B
+constexpr int kWGChunk = 64 * 4 + 4;                 // floats per K chunk of B (64 rows: output row r, channel co)
 constexpr int kWXFloats = kWQC * kWXChunk;           // 37,152 B
-constexpr int kWGFloats = kWQC * kWGChunk;           // 9,504 B per shifted copy
-constexpr int kWSmemBytes = (kWXFloats + 6 * kWGFloats) * 4 + 8 * 32 * 4 + 64;   // 94 KB: two CTAs per SM
+constexpr int kWGFloats = kWQC * kWGChunk;           // 18,720 B per shifted copy (both output rows)
+constexpr int kWSmemBytes = (kWXFloats + 3 * kWGFloats) * 4 + 8 * 32 * 4 + 64;   // 94 KB: two CTAs per SM
 constexpr int kWTmemCols = 256;                      // 6 x 32 used
 
 struct WgradArgs {
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sX = reinterpret_cast<float*>(smem_raw);
   float* sG = sX + kWXFloats;
-  float* sRed = sG + 6 * kWGFloats;                            // [8 warps][32]
+  float* sRed = sG + 3 * kWGFloats;                            // [8 warps][32]
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sRed + 256);
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(sBar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int i = tid; i < kWXFloats + 6 * kWGFloats; i += kCThreads) sX[i] = 0.f;   // pads
+  for (int i = tid; i < kWXFloats + 3 * kWGFloats; i += kCThreads) sX[i] = 0.f;   // pads
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
 #pragma unroll
         for (int kx = 0; kx < 3; ++kx) {
           const int q = px + kx;
-          float* dst = sG + (r * 3 + kx) * kWGFloats + (q >> 2) * kWGChunk + (4 * c) * 4 + (q & 3);
+          float* dst = sG + kx * kWGFloats + (q >> 2) * kWGChunk + (r * 32 + 4 * c) * 4 + (q & 3);
           dst[0] = t.x; dst[4] = t.y; dst[8] = t.z; dst[12] = t.w;
         }
       }
@@ -539,11 +539,15 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
 #pragma unroll 1
       for (int ks = 0; ks < kWQC / 2; ++ks) {
 #pragma unroll
-        for (int kx = 0; kx < 6; ++kx) {   // (output row r, filter column kx) = (kx / 3, kx % 3)
+        for (int kx = 0; kx < 3; ++kx) {   // one N = 64 instruction per filter column: both output rows' dL/dy stacked
           const uint32_t aa = x_addr + (uint32_t)(2 * ks * kWXChunk * 4);
           const uint32_t bb = g_addr + (uint32_t)(kx * kWGFloats * 4) + (uint32_t)(2 * ks * kWGChunk * 4);
-          mma_tf32(tmem_base + (uint32_t)(kx * 32), smem_desc(aa, kWXChunk * 4u, 128u), smem_desc(bb, kWGChunk * 4u, 128u),
-                   accumulate | (uint32_t)ks);
+          constexpr uint32_t idesc64 = (kIdesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+              :: "r"(tmem_base + (uint32_t)(kx * 64)), "l"(smem_desc(aa, kWXChunk * 4u, 128u)), "l"(smem_desc(bb, kWGChunk * 4u, 128u)),
+                 "r"(idesc64), "r"(accumulate | (uint32_t)ks) : "memory");
         }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" :: "r"(bar_addr) : "memory");
@@ -569,8 +573,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
 #pragma unroll 1
     for (int rk = 0; rk < 6; ++rk) {
       float acc[32];
+      const int kx = rk >> 1, r = rk & 1, ky = warp - r;   // columns: (kx, r, co)
       tmem_load32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(rk * 32), acc);
-      const int r = rk / 3, kx = rk - 3 * r, ky = warp - r;
       if (ky >= 0 && ky < 3) {
 #pragma unroll
         for (int co = 0; co < 32; ++co) atomicAdd(a.gw + ((co * 3 + ky) * 3 + kx) * 32 + lane, acc[co]);
