@@ -1,8 +1,8 @@
 // decode_image — the camera ConvDecoder (Eq. 7-8).
 //
 // The only dense contraction of the system, so the only kernel here that runs on the tensor cores: every 3x3, 32 -> 32
-// convolution is an implicit GEMM issued as tcgen05.mma (kind::tf32, M = 128 pixels, N = 32 output channels, K = 8
-// input channels per instruction) with the accumulator in tensor memory.
+// convolution is an implicit GEMM issued as tcgen05.mma (kind::tf32, M = 128 pixels, N = 32 or 64 output channels —
+// two stacked taps —, K = 8 input channels per instruction) with the accumulator in tensor memory.
 //
 // Layer list (the reference ships no decoder; SPEC fixes width, depth, kernel size, padding and the output map, the
 // rest is fixed in oracle/decoder_oracle.hpp's header and mirrored here):
@@ -17,7 +17,8 @@
 // 16 B apart, 8-row groups 128 B apart, the two 16-byte K chunks of one instruction one plane apart), and in it a
 // filter tap (ky, kx) is nothing but a different start address — the nine taps of a convolution read the one staged
 // halo, no im2col copy, no per-tap reload. The weights of a layer (9 taps x 32 x 32, 36 KB) are staged once per CTA
-// in the same layout; CTAs are persistent (two per SM, so one stages while the other's MMAs and epilogue run).
+// in the same layout; CTAs are persistent (one per SM) and warp-specialised: producer warps stage the next tile while
+// one lane issues the current tile's MMAs and the epilogue warps drain the previous one (k_conv3x3_tc below).
 // Operands are rounded to tf32 (round-to-nearest) while staging; accumulation is fp32.
 #include <cuda_runtime.h>
 
