@@ -227,6 +227,25 @@ class SensorView {
     detail::check(ctx_.handle(), splatb200_view_backward_host(v_, g_blend16.data.data(), g_alpha.data()));
     detail::check(ctx_.handle(), splatb200_ctx_sync(ctx_.handle()));
   }
+  /// decode_image: the ConvDecoder over this camera view's render, with the camera's own embedding
+  /// (CameraModel::embedding, scene.hpp:106). params: splatb200_conv_decoder_params() floats. -> image, H*W x 3.
+  std::vector<float> decode_image(const std::vector<float>& params, const VecX<float>& embedding) {
+    float e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < 8 && k < (int)embedding.size(); ++k) e[k] = embedding(k);
+    std::vector<float> image(3 * (size_t)queries_);
+    detail::check(ctx_.handle(), splatb200_view_decode_image(v_, params.data(), e, image.data(), nullptr));
+    return image;
+  }
+  /// its backward: dL/dimage -> dL/dparams (overwritten), SensorGrads::d_embedding (+=, projection.hpp:207-222); the
+  /// gradient w.r.t. the render is added to the DEVICE buffer g_blend16 (P x 16) that splatb200_view_backward takes
+  void decode_image_backward(const std::vector<float>& g_image, std::vector<float>& g_params, SensorGrads<float>& gsensor,
+                             float* g_blend16_device) {
+    float ge[8];
+    g_params.assign((size_t)splatb200_conv_decoder_params(), 0.0f);
+    detail::check(ctx_.handle(), splatb200_view_decode_image_backward(v_, g_image.data(), g_params.data(), ge, g_blend16_device, nullptr));
+    if (gsensor.d_embedding.size() < 8) gsensor.d_embedding = VecX<float>::Zero(8);
+    for (int k = 0; k < 8; ++k) gsensor.d_embedding(k) += ge[k];
+  }
   void add_sensor_grads(SensorGrads<float>& out) {
     splatb200_sensor_grads g{};
     detail::check(ctx_.handle(), splatb200_view_sensor_grads(v_, &g));
