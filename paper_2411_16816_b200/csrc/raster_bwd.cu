@@ -15,18 +15,19 @@
 // Reduction of the 26 per-pair values to per-Gaussian gradients, in two phases per warp:
 //   A (lane = query): the sequential part. For every list entry that some lane blends, each lane computes
 //     only TWO scalars — w and dL/dsigma (sigma = qf / 2) — and parks them in a [slot][lane] shared-memory
-//     panel (stride 33: conflict-free both ways). Every other one of the 26 values is a product of one of
+//     panel (strides 36 for w, 33 for dL/dsigma: conflict-free for these writes and for phase B's reads). Every other one of the 26 values is a product of one of
 //     those scalars with per-query data (g_c, t, g_D) or per-Gaussian data (conic, mean, velocity); the
 //     dL/drho term is -dL/dsigma / rho (alpha = rho exp(-sigma) when it is not clamped), so its sum over the
 //     queries needs no panel of its own.
-//   B (lane = Gaussian): when the panel holds kChunk entries (or the batch ends) the roles flip: lanes are
-//     spread over the parked entries (32 / E lanes per entry, E = capacity rounded up to a power of two),
-//     each lane loops over its share of the 32 queries — query data is read as shared-memory broadcasts —
-//     and accumulates the 26 sums of ITS Gaussian in registers; log2(32 / E) shuffle steps join the lanes
-//     of one entry. This replaces a 31-shuffle transposing butterfly per (warp, Gaussian) and costs about
-//     half the instructions.
+//   B: when the panel holds kChunk entries (or the batch ends) the roles flip. The 16 channel sums (for the lidar
+//     13 features + range + v_r) are a dense (entries x queries) x (queries x channels) product and run as warp-level
+//     tf32 MMAs with split operands (reduce_panel). For the eight geometric sums lanes are spread over the parked
+//     entries (32 / E lanes per entry, E = capacity rounded up to a power of two), each lane loops over its share of
+//     the 32 queries — query data is read as shared-memory broadcasts — and accumulates the sums of ITS Gaussian in
+//     registers; log2(32 / E) shuffle steps join the lanes of one entry. This replaces a 31-shuffle transposing
+//     butterfly per (warp, Gaussian) and costs about a third of the instructions.
 // The panel carries its own copy of each parked Gaussian's record, so it survives batch boundaries and is
-// (almost) always drained full. The 26 sums of a (warp, Gaussian) leave as 26 fire-and-forget global REDs
+// (almost) always drained full. The 24-26 sums of a (warp, Gaussian) leave as fire-and-forget global REDs
 // (north_star (4): warp-aggregated atomics — 32 queries are folded into one RED per value). Shared-memory
 // float atomics are NOT used: on sm_100a they compile to a compare-and-swap spin loop (ATOMS.CAST.SPIN),
 // which the first version of this kernel showed to be the bottleneck (profiles/).
@@ -40,91 +41,150 @@
 // per 32).
 namespace sb {
 
-constexpr int kRed = 26;     // 16 channel grads + conic 3 + mean2d 2 + vel 3 + rho + range
 constexpr int kBatch = 256;  // list entries staged per batch
 constexpr int kChunk = 16;   // panel capacity per warp (8 with 3 CTAs/SM was measured: 4-15% slower)
-constexpr int kPanelStride = 33;
-constexpr int kPxStride = 20;  // qx qy t g_D | g_out[16]
+constexpr int kPanelStride = 33;  // dL/dsigma panel: read by the per-entry loop (lane = entry)
+constexpr int kWStride = 36;      // w panel: read as the A fragments of the channel product (conflict-free: 4 gid + tig)
+constexpr int kPxStride = 24;     // qx qy t g_D | G[16] | pad (24 tig + gid: conflict-free B fragments)
 
 struct WarpScratch {
-  float w[kChunk * kPanelStride];
+  float w[kChunk * kWStride];
   float gs[kChunk * kPanelStride];
   float px[32 * kPxStride];
   float4 gA[kChunk], gB[kChunk];  // the parked Gaussians' records
   uint32_t src[kChunk];
 };
 
+// D += A B for one m16n8k8 tf32 tile (A row-major 16 x 8, B column-major 8 x 8, fp32 accumulators).
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+constexpr uint32_t kTf32Mask = 0xffffe000u;  // sign, exponent, 10 mantissa bits
+
 // Phase B for `n` parked entries (1 <= n <= kChunk).
+//
+// The 16 channel sums are the one dense contraction of the path: dL/df[e][c] = sum_q w[e][q] G[q][c], a
+// (16 entries x 32 queries) x (32 queries x 16 channels) product per drained panel. It runs as 8 warp-level
+// m16n8k8 tiles with split operands (x = hi + lo, both exactly representable in tf32; hi hi + hi lo + lo hi, the
+// "3xTF32" scheme: products exact, ~2^-21 relative error, fp32 accumulation), replacing 16 FMAs and four
+// 128-bit shared loads per (entry, query) pair. Both operands are split on the fly: keeping pre-split G rows in
+// shared memory was measured and lost (the 20 KB more per CTA push the carve-out to 228 KB and leave the lidar's
+// gathers no L1: +5% on its kernel). For the lidar the two free columns carry g_D and g_D t, which yields d/d range and d/d v_r from the
+// same product. tcgen05 does not fit here: the operand is produced in registers by this warp, 16 rows at a time.
+// The eight geometric sums (conic 3, mean 2, velocity 2, rho) depend on the pair through Delta and stay on the
+// fp32 pipe, lane = entry.
 template <bool kCamera>
 __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int lane, int d_f, const RasterGradDev& rg,
                                              const ParamGradDev& pg, float& dt_local, bool wrap) {
+  {  // channel product
+    const int gid = lane >> 2, tig = lane & 3;
+    float d[2][4], dlh[2][4], dhl[2][4];  // three accumulators per tile: six independent chains of four MMAs
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[nt][k] = dlh[nt][k] = dhl[nt][k] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int q = ks * 8 + tig;
+      const float af[4] = {ws.w[gid * kWStride + q], ws.w[(gid + 8) * kWStride + q], ws.w[gid * kWStride + q + 4],
+                           ws.w[(gid + 8) * kWStride + q + 4]};
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ah[k] = __float_as_uint(af[k]) & kTf32Mask;
+        al[k] = __float_as_uint(af[k] - __uint_as_float(ah[k])) & kTf32Mask;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const float* bp = &ws.px[q * kPxStride + 4 + nt * 8 + gid];
+        const float bf0 = bp[0], bf1 = bp[4 * kPxStride];
+        const uint32_t bh0 = __float_as_uint(bf0) & kTf32Mask, bh1 = __float_as_uint(bf1) & kTf32Mask;
+        const uint32_t bl0 = __float_as_uint(bf0 - __uint_as_float(bh0)) & kTf32Mask;
+        const uint32_t bl1 = __float_as_uint(bf1 - __uint_as_float(bh1)) & kTf32Mask;
+        mma_tf32(dlh[nt], al, bh0, bh1);
+        mma_tf32(dhl[nt], ah, bl0, bl1);
+        mma_tf32(d[nt], ah, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[nt][k] += dlh[nt][k] + dhl[nt][k];
+    // lane holds rows gid, gid + 8 and columns nt * 8 + 2 tig, + 1: one RED per (warp, Gaussian, value)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = gid + 8 * h;
+      if (e < n) {
+        const size_t src = ws.src[e];
+        float* f0 = kCamera ? pg.d_color + 3 * src : pg.d_feature + (size_t)d_f * src;
+        float* f1 = pg.d_feature + (size_t)d_f * src - (kCamera ? 3 : 0);
+        float* r0 = rg.g + kRasterGradStride * src - 16;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = nt * 8 + 2 * tig + j;
+            const float v = d[nt][2 * h + j];
+            if (v != 0.0f) {  // columns >= channels are exactly zero
+              float* dst;
+              if (kCamera) dst = c < 3 ? f0 + c : f1 + c;
+              else dst = c < 13 ? f1 + c : (c == 13 ? r0 + 25 : r0 + 23);  // 13: d/d range, 14: d/d v_r
+              atomicAdd(dst, v);
+            }
+          }
+      }
+    }
+  }
   int E = 1;  // capacity: smallest power of two >= n
   while (E < n) E <<= 1;
   const int e = lane & (E - 1);
   const int g = lane / E;  // which share of the queries
   const bool active = e < n;
   const float4 gA = ws.gA[active ? e : 0], gB = ws.gB[active ? e : 0];
-  float acc[kRed];
+  constexpr int kGeo = 8;  // conic 3 | mean2d 2 | velocity 2 | sum of dL/dsigma
+  float acc[kGeo];
 #pragma unroll
-  for (int c = 0; c < kRed; ++c) acc[c] = 0.0f;
+  for (int c = 0; c < kGeo; ++c) acc[c] = 0.0f;
   float dt = 0.0f;
   const int row = e * kPanelStride;
   // (visiting only the queries that blended the entry — a divergent loop over a saved ballot — was measured: 2% faster
   // for the lidar, 4% slower for the camera, whose entries are blended by a third of the lanes; the dense loop stays)
-#pragma unroll 2
+#pragma unroll 4
   for (int pp = 0; pp < E; ++pp) {  // 32 / (32 / E) queries per lane
     const int q = g * E + pp;
-    const float w = ws.w[row + q], gs = ws.gs[row + q];
+    const float gs = ws.gs[row + q];
     const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);  // qx qy t g_D
-#pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const float4 gq = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride + 4 + 4 * c4]);
-      acc[4 * c4] = fmaf(w, gq.x, acc[4 * c4]);
-      acc[4 * c4 + 1] = fmaf(w, gq.y, acc[4 * c4 + 1]);
-      acc[4 * c4 + 2] = fmaf(w, gq.z, acc[4 * c4 + 2]);
-      acc[4 * c4 + 3] = fmaf(w, gq.w, acc[4 * c4 + 3]);
-    }
     const float t = q0.z;
-    if (!kCamera) {
-      const float gw = q0.w * w;  // g_D w
-      acc[25] += gw;               // d/d range
-      acc[23] = fmaf(gw, t, acc[23]);  // d/d v_r
-    }
     float dx = q0.x - fmaf(gA.z, t, gA.x);
     if (!kCamera && wrap) dx = wrap_pi(dx);
     const float dy = q0.y - fmaf(gA.w, t, gA.y);
     const float hx = 0.5f * gs * dx, hy = 0.5f * gs * dy;
-    acc[16] = fmaf(hx, dx, acc[16]);
-    acc[17] = fmaf(hx, dy, acc[17]);
-    acc[18] = fmaf(hy, dy, acc[18]);
+    acc[0] = fmaf(hx, dx, acc[0]);
+    acc[1] = fmaf(hx, dy, acc[1]);
+    acc[2] = fmaf(hy, dy, acc[2]);
     const float gdx = gs * fmaf(0.5f * gB.y, dy, gB.x * dx);
     const float gdy = gs * fmaf(0.5f * gB.y, dx, gB.z * dy);
-    acc[19] -= gdx;
-    acc[20] -= gdy;
-    acc[21] = fmaf(-t, gdx, acc[21]);
-    acc[22] = fmaf(-t, gdy, acc[22]);
-    acc[24] -= gs;  // sum of dL/dsigma; scaled by 1 / rho below
+    acc[3] -= gdx;
+    acc[4] -= gdy;
+    acc[5] = fmaf(-t, gdx, acc[5]);
+    acc[6] = fmaf(-t, gdy, acc[6]);
+    acc[7] -= gs;  // sum of dL/dsigma; scaled by 1 / rho below
     if (kCamera) dt -= fmaf(gA.z, gdx, gA.w * gdy);
   }
-  acc[24] = acc[24] / gB.w;  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
+  acc[7] = acc[7] / gB.w;  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
   // join the 32 / E lanes that worked on the same entry
   for (int o = E; o < 32; o <<= 1) {
 #pragma unroll
-    for (int c = 0; c < kRed; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    for (int c = 0; c < kGeo; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
   }
   if (active) dt_local += dt;
   if (active && g == 0) {  // one RED per (warp, Gaussian, value)
-    const size_t src = ws.src[e];
-    float* f0 = kCamera ? pg.d_color + 3 * src : pg.d_feature + (size_t)d_f * src;
-    float* f1 = pg.d_feature + (size_t)d_f * src - (kCamera ? 3 : 0);
-    float* r0 = rg.g + kRasterGradStride * src - 16;
+    float* r0 = rg.g + kRasterGradStride * (size_t)ws.src[e];
 #pragma unroll
-    for (int c = 0; c < kRed; ++c) {
-      if (acc[c] != 0.0f) {
-        float* dst = (c >= 16) ? r0 + c : ((kCamera && c < 3) ? f0 + c : f1 + c);
-        atomicAdd(dst, acc[c]);
-      }
-    }
+    for (int c = 0; c < kGeo; ++c)
+      if (acc[c] != 0.0f) atomicAdd(r0 + (c < 7 ? c : 8), acc[c]);  // slots 0-6, rho at 8 (7: v_r, 9: range)
   }
   __syncwarp();
 }
@@ -224,9 +284,14 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     {
       float* row = &ws.px[lane * kPxStride];
       *reinterpret_cast<float4*>(row) = make_float4(qx, qy, t, g_D);
+      // the B operand of the channel product (reduce_panel); lidar: columns 13, 14 = g_D, g_D t
+      float gcol[kChannels];
+#pragma unroll
+      for (int k = 0; k < kChannels; ++k) gcol[k] = g_out[k];
+      if (!kCamera) { gcol[13] = g_D; gcol[14] = g_D * t; gcol[15] = 0.0f; }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        *reinterpret_cast<float4*>(row + 4 + 4 * k) = make_float4(g_out[4 * k], g_out[4 * k + 1], g_out[4 * k + 2], g_out[4 * k + 3]);
+        *reinterpret_cast<float4*>(row + 4 + 4 * k) = make_float4(gcol[4 * k], gcol[4 * k + 1], gcol[4 * k + 2], gcol[4 * k + 3]);
     }
 
     // warp and block maxima of `last`
@@ -294,9 +359,8 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
             S = fmaf(w, dotgf, S);
             if (!ev.clamped) g_sigma = -ev.alpha * g_a;  // alpha = rho exp(-sigma), sigma = qf / 2; clamped: constant
           }
-          const int o = n_slots * kPanelStride + lane;
-          ws.w[o] = w;
-          ws.gs[o] = g_sigma;
+          ws.w[n_slots * kWStride + lane] = w;
+          ws.gs[n_slots * kPanelStride + lane] = g_sigma;
           if (lane == 0) {
             ws.gA[n_slots] = sA[jj];
             ws.gB[n_slots] = sB[jj];
