@@ -143,11 +143,13 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
   const int g = lane / E;  // which share of the queries
   const bool active = e < n;
   const float4 gA = ws.gA[active ? e : 0], gB = ws.gB[active ? e : 0];
-  constexpr int kGeo = 8;  // conic 3 | mean2d 2 | velocity 2 | sum of dL/dsigma
-  float acc[kGeo];
+  // The eight geometric sums are linear in eight raw moments of g = dL/dsigma over the queries —
+  // {1, dx, dy, dx dx, dx dy, dy dy, t dx, t dy} — so the loop accumulates those (14 fp32 instructions per pair) and
+  // the conic / velocity factors are applied once per entry after the join.
+  constexpr int kGeo = 8;
+  float m[kGeo];  // S0 Sx Sy Sxx Sxy Syy Stx Sty
 #pragma unroll
-  for (int c = 0; c < kGeo; ++c) acc[c] = 0.0f;
-  float dt = 0.0f;
+  for (int c = 0; c < kGeo; ++c) m[c] = 0.0f;
   const int row = e * kPanelStride;
   // (visiting only the queries that blended the entry — a divergent loop over a saved ballot — was measured: 2% faster
   // for the lidar, 4% slower for the camera, whose entries are blended by a third of the lanes; the dense loop stays)
@@ -160,27 +162,35 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
     float dx = q0.x - fmaf(gA.z, t, gA.x);
     if (!kCamera && wrap) dx = wrap_pi(dx);
     const float dy = q0.y - fmaf(gA.w, t, gA.y);
-    const float hx = 0.5f * gs * dx, hy = 0.5f * gs * dy;
-    acc[0] = fmaf(hx, dx, acc[0]);
-    acc[1] = fmaf(hx, dy, acc[1]);
-    acc[2] = fmaf(hy, dy, acc[2]);
-    const float gdx = gs * fmaf(0.5f * gB.y, dy, gB.x * dx);
-    const float gdy = gs * fmaf(0.5f * gB.y, dx, gB.z * dy);
-    acc[3] -= gdx;
-    acc[4] -= gdy;
-    acc[5] = fmaf(-t, gdx, acc[5]);
-    acc[6] = fmaf(-t, gdy, acc[6]);
-    acc[7] -= gs;  // sum of dL/dsigma; scaled by 1 / rho below
-    if (kCamera) dt -= fmaf(gA.z, gdx, gA.w * gdy);
+    const float a = gs * dx, b = gs * dy;
+    m[0] += gs;
+    m[1] += a;
+    m[2] += b;
+    m[3] = fmaf(a, dx, m[3]);
+    m[4] = fmaf(a, dy, m[4]);
+    m[5] = fmaf(b, dy, m[5]);
+    m[6] = fmaf(t, a, m[6]);
+    m[7] = fmaf(t, b, m[7]);
   }
-  acc[7] = acc[7] / gB.w;  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
   // join the 32 / E lanes that worked on the same entry
   for (int o = E; o < 32; o <<= 1) {
 #pragma unroll
-    for (int c = 0; c < kGeo; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    for (int c = 0; c < kGeo; ++c) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
   }
-  if (active) dt_local += dt;
   if (active && g == 0) {  // one RED per (warp, Gaussian, value)
+    const float hb = 0.5f * gB.y;
+    const float gx = fmaf(hb, m[2], gB.x * m[1]), gy = fmaf(hb, m[1], gB.z * m[2]);     // sum of dL/dDelta
+    const float gtx = fmaf(hb, m[7], gB.x * m[6]), gty = fmaf(hb, m[6], gB.z * m[7]);   // sum of t dL/dDelta
+    float acc[kGeo];
+    acc[0] = 0.5f * m[3];  // dL/dconic
+    acc[1] = 0.5f * m[4];
+    acc[2] = 0.5f * m[5];
+    acc[3] = -gx;  // dL/dmean2d
+    acc[4] = -gy;
+    acc[5] = -gtx;  // dL/dvelocity (first two components)
+    acc[6] = -gty;
+    acc[7] = -m[0] / gB.w;  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
+    if (kCamera) dt_local -= fmaf(gA.z, gx, gA.w * gy);  // SensorGrads.d_time_offset
     float* r0 = rg.g + kRasterGradStride * (size_t)ws.src[e];
 #pragma unroll
     for (int c = 0; c < kGeo; ++c)
