@@ -51,7 +51,7 @@ struct WarpScratch {
   float w[kChunk * kWStride];
   float gs[kChunk * kPanelStride];
   float px[32 * kPxStride];
-  float4 gA[kChunk], gB[kChunk];  // the parked Gaussians' records
+  float4 gAB[2 * kChunk];  // the parked Gaussians' records: geomA | geomB
   uint32_t src[kChunk];
 };
 
@@ -142,7 +142,7 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
   const int e = lane & (E - 1);
   const int g = lane / E;  // which share of the queries
   const bool active = e < n;
-  const float4 gA = ws.gA[active ? e : 0], gB = ws.gB[active ? e : 0];
+  const float4 gA = ws.gAB[active ? e : 0], gB = ws.gAB[kChunk + (active ? e : 0)];
   // The eight geometric sums are linear in eight raw moments of g = dL/dsigma over the queries —
   // {1, dx, dy, dx dx, dx dy, dy dy, t dx, t dy} — so the loop accumulates those (14 fp32 instructions per pair) and
   // the conic / velocity factors are applied once per entry after the join.
@@ -371,11 +371,9 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           }
           ws.w[n_slots * kWStride + lane] = w;
           ws.gs[n_slots * kPanelStride + lane] = g_sigma;
-          if (lane == 0) {
-            ws.gA[n_slots] = sA[jj];
-            ws.gB[n_slots] = sB[jj];
-            ws.src[n_slots] = sSrc[jj];
-          }
+          // the record travels with the entry: lanes 0 / 1 copy geomA / geomB (sB follows sA), lane 2 the index
+          if (lane < 2) ws.gAB[lane * kChunk + n_slots] = sA[lane * kBatch + jj];
+          else if (lane == 2) ws.src[n_slots] = sSrc[jj];
           if (++n_slots == kChunk) {
             __syncwarp();
             reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
