@@ -91,6 +91,31 @@ DM_HD float exp(float x) {
   return DM_MUL(DM_MUL(p, s1), s2);
 }
 
+/// e^x for x <= 88 whose caller guarantees x >= -87 (the compositing kernels: x = -qf / 2 with qf <= qform_max).
+/// Bit-identical to exp() on [-87, 88]: the same reduction and kernel; 2^n is then a normal number, so one exact
+/// power-of-two multiply replaces the two-step scaling, the exponent comes from the low mantissa bits of the
+/// magic-number sum instead of a float-to-int conversion, and both range branches go. Arguments above 88 (a
+/// quadratic form below -176: not reachable with a positive-definite conic) evaluate as e^88, which the alpha clamp
+/// treats like +inf.
+DM_HD float exp_bounded(float x) {
+  x = x < 88.0f ? x : 88.0f;
+  const float kMagic = 12582912.0f;
+  const float tmp = DM_ADD(DM_MUL(x, 1.44269504088896341f), kMagic);
+  const float n = DM_SUB(tmp, kMagic);
+  float r = DM_FMA(n, -0.693359375f, x);
+  r = DM_FMA(n, 2.12194440e-4f, r);
+  const float z = DM_MUL(r, r);
+  float p = 1.9875691500e-4f;
+  p = DM_FMA(p, r, 1.3981999507e-3f);
+  p = DM_FMA(p, r, 8.3334519073e-3f);
+  p = DM_FMA(p, r, 4.1665795894e-2f);
+  p = DM_FMA(p, r, 1.6666665459e-1f);
+  p = DM_FMA(p, r, 5.0000001201e-1f);
+  p = DM_ADD(DM_FMA(p, z, r), 1.0f);
+  const float s = bits_to_float((float_to_bits(tmp) << 23) + 0x3f800000u);  // 2^n, n in [-126, 127]
+  return DM_MUL(p, s);
+}
+
 /// Numerically stable logistic, same branch structure as the reference
 /// (common.hpp:54-58).
 DM_HD float sigmoid(float x) {

@@ -50,7 +50,7 @@ __device__ __forceinline__ float alpha_qform(const float4 gA /* mx my vx vy */, 
 __device__ __forceinline__ bool alpha_finish(float qf, float rho, float dx, float dy, float qform_max, float alpha_clamp,
                                              float alpha_min, AlphaEval& o) {
   if (!(qf <= qform_max)) return false;
-  const float gauss = detmath::exp(__fmul_rn(-0.5f, qf));
+  const float gauss = detmath::exp_bounded(__fmul_rn(-0.5f, qf));  // == detmath::exp: qf <= qform_max bounds the argument
   float alpha = __fmul_rn(rho, gauss);
   const bool clamped = alpha > alpha_clamp;
   if (clamped) alpha = alpha_clamp;
