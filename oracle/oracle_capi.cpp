@@ -610,6 +610,7 @@ extern "C" void orc_detmath_eval(int fn, const float* x, const float* y, float* 
       case 1: out[i] = detmath::sigmoid(x[i]); break;
       case 2: out[i] = detmath::atan2(y[i], x[i]); break;
       case 3: out[i] = detmath::asin(x[i]); break;
+      case 4: out[i] = detmath::exp_bounded(x[i]); break;  // the compositing kernels' form of exp
       default: out[i] = 0.0f;
     }
   }

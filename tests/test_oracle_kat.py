@@ -473,6 +473,21 @@ def test_detmath_accuracy():
     assert op.detmath_eval(2, np.array([-1.0], np.float32), np.array([0.0], np.float32))[0] == np.float32(np.pi)
 
 
+def test_detmath_exp_bounded_is_bit_identical_to_exp():
+    """The compositing kernels evaluate exp(-qf / 2) through detmath::exp_bounded (no range branches, one power-of-two
+    scale): on its domain [-87, 88] it must return the very bits of detmath::exp, which the CPU oracle calls — the
+    bit-exact contributor counts rest on it."""
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.uniform(-87, 88, 2_000_000), rng.uniform(-4.5, 0.0, 2_000_000),
+                        -np.exp(rng.uniform(-100, 4.4, 500_000)), np.exp(rng.uniform(-100, 4.4, 500_000)),
+                        [0.0, -0.0, -87.0, 88.0, -4.5, 1e-45, -1e-45]]).astype(np.float32)
+    a = op.detmath_eval(0, x)
+    b = op.detmath_eval(4, x)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    # above the domain the result saturates at e^88 (the alpha clamp treats it like +inf)
+    assert op.detmath_eval(4, np.array([100.0], np.float32))[0] == op.detmath_eval(0, np.array([88.0], np.float32))[0]
+
+
 # ---- KA16: backward (SPEC.md:321-323) ---------------------------------------------------------
 def _loss_camera(sc, cam, gb, ga, t_scene=0.0):
     v = op.OracleScene(sc, np.float64).render_camera(cam, ST, t_scene=t_scene)
