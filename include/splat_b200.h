@@ -97,8 +97,8 @@ int splatb200_ctx_create(int device, void* cuda_stream /* cudaStream_t or NULL *
 void splatb200_ctx_destroy(splatb200_ctx* ctx);
 const char* splatb200_last_error(const splatb200_ctx* ctx); /* ctx may be NULL: last create error */
 int splatb200_ctx_sync(splatb200_ctx* ctx);
-/* number of hand-written kernels launched by this ctx since creation (bench.py's gpu_launches), and
- * the number of library (CUB scan / radix sort) kernels launched beside them */
+/* number of hand-written kernels launched by this ctx since creation (bench.py's gpu_launches), and the number of
+ * library kernels launched beside them (always 0: the radix sorts and scans of the binning stage are hand-written) */
 int64_t splatb200_ctx_launch_count(const splatb200_ctx* ctx);
 int64_t splatb200_ctx_library_launch_count(const splatb200_ctx* ctx);
 /* per-stage CUDA-event timing on the ctx stream (off by default). Stages: 0 project, 1 depth sort + scan, 2 tile counts
@@ -119,6 +119,24 @@ int splatb200_ctx_set_profiling(splatb200_ctx* ctx, int32_t on);
 int splatb200_ctx_set_view_streams(splatb200_ctx* ctx, int32_t on);
 int splatb200_ctx_join(splatb200_ctx* ctx);
 int splatb200_view_stage_ms(splatb200_view* v, float out_ms[8]);
+
+/* ---- multi-GPU: the one collective of the path ("parallel per sensor view" over an immutable scene,
+ * SPEC.md:90; per-worker SceneParamGrads summed, scene.hpp:351-362 SceneParamGrads::add) ---------------------------
+ * One process (and one ctx) per GPU; frames / sensors are sharded over ranks with the scene replicated; after a rank
+ * has accumulated the gradients of its own work items, splatb200_allreduce_grads sums the contiguous
+ * (14 + d_f) * N-float SceneParamGrads buffer (and the per-actor ActorGrad slots) over all ranks, in place, with NCCL.
+ * NCCL is bound at run time from the process's own libnccl.so.2 (the one a trainer or torch already loaded), so the
+ * library itself has no link-time NCCL dependency; without it these calls return SPLATB200_ERUNTIME.
+ *   comm_init: rank 0 obtains a 128-byte id (splatb200_nccl_unique_id), every rank receives it out of band (MPI,
+ *              torch.distributed, a file) and calls comm_init(ctx, id, rank, world) — ncclCommInitRank.
+ *   comm_bind: a C++ trainer that already owns an ncclComm_t hands it over (not destroyed by the library).
+ * allreduce_grads orders itself after every view stream (splatb200_ctx_join) and runs on the ctx stream. */
+int splatb200_nccl_unique_id(void* id128);
+int splatb200_ctx_comm_init(splatb200_ctx* ctx, const void* id128, int32_t rank, int32_t world);
+int splatb200_ctx_comm_bind(splatb200_ctx* ctx, void* nccl_comm /* ncclComm_t */, int32_t rank, int32_t world);
+int splatb200_ctx_comm_destroy(splatb200_ctx* ctx);
+int splatb200_ctx_comm_info(const splatb200_ctx* ctx, int32_t* rank, int32_t* world); /* world = 0: no communicator */
+int splatb200_allreduce_grads(splatb200_ctx* ctx);
 
 /* ---- scene: GaussianSet + SceneGraph (scene.hpp:11-45, 171-187) ------------------------------ */
 /* host arrays are copied to the device; actor_id is validated lazily against the tracks at
@@ -239,6 +257,14 @@ typedef struct {
   int64_t total_steps;
 } splatb200_adam_config;
 int splatb200_optimizer_step(splatb200_ctx* ctx, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]);
+/* forget the Adam moments and step state (splatb200_scene_upload of the SAME shape keeps them — the per-iteration
+ * parameter refresh —; a new shape or splatb200_scene_bind_device drops them) */
+int splatb200_optimizer_reset(splatb200_ctx* ctx);
+/* optimizer_step fused with the collective (every rank steps only its shard of the flat gradient layout):
+ * reduce (sum) of each rank's shard to its owner, agreement on the groups to skip (a non-finite gradient anywhere skips
+ * the group everywhere), Adam on the shard, broadcast of the updated parameters. Same bytes on the wire as the
+ * all-reduce; optimizer work and state divide by the world size. */
+int splatb200_sharded_optimizer_step(splatb200_ctx* ctx, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]);
 /* The same on the slice [lo, hi) of the gradient buffer's flat layout [mean 3N | scale_log 3N | quat 4N | opacity N |
  * color 3N | feature d_f N] only — a rank's shard after a reduce-scatter (paper_2411_16816_b200/dist.py
  * sharded_optimizer_step: reduce-scatter -> this -> all-gather of the parameters). skip_groups[6] (may be NULL): groups to
@@ -357,7 +383,9 @@ int splatb200_view_backward_projected(splatb200_view* v, const float* g_mean2d, 
  * n_contrib, last_idx. float arrays: mean2d(2), depth_key, cov2d(4), velocity(3), aabb(4), conic(4),
  * det_ratio, mu_sensor(3), rel_vel_sensor(3), blend(16), alpha, t_final, range_blend — projected
  * fields are compacted in ascending source_index like the reference's std::vector<ProjectedGaussian>
- * (projection.hpp:115,171). */
+ * (projection.hpp:115,171). "packed_record" (26 floats per visible Gaussian, source order) is the record k_project
+ * STORED for the compositing kernels, read back as it lies in HBM: mean2d.xy, velocity.xy | conic a, 2b, c,
+ * rho = det_ratio * opacity | depth key, v_r | the 16 channel slots (camera: rgb + features; lidar: features). */
 int64_t splatb200_view_array(splatb200_view* v, const char* name, void* dst);
 
 #ifdef __cplusplus

@@ -408,6 +408,55 @@ int view_brute(void* vv, int early_exit, S* blend16, S* alpha, int64_t* n_contri
   return 0;
 }
 
+// Contributor introspection for the gradient parity gate (tests only). For every query: the sequence of (source index,
+// clamped) it blends. hash (P, optional): a 64-bit signature of that sequence. gauss_flag (N, optional): a query that
+// blends a flagged Gaussian gets query_flag = 1. Every Gaussian blended by a query with query_flag = 1 is marked in
+// gauss_mask (N, optional).
+template <class S>
+int view_contrib(void* vv, const uint8_t* gauss_flag, uint8_t* query_flag, uint8_t* gauss_mask, uint64_t* hash, int workers) {
+  auto* v = (ViewH<S>*)vv;
+  const Worklist& wl = v->wl;
+  const int T = wl.tiles_x * wl.tiles_y;
+  const bool camera = v->camera;
+  const int W = camera ? v->cam.width : 0, H = camera ? v->cam.height : 0;
+  parallel_chunks(T, workers, [&](int, int64_t tb, int64_t te) {
+    std::vector<Splat<S>> splats;
+    std::vector<int32_t> pos;
+    std::vector<uint8_t> cl;
+    for (int64_t tile = tb; tile < te; ++tile) {
+      const int64_t b = wl.tile_begin[tile], e = std::max<int64_t>(wl.tile_begin[tile], wl.tile_end[tile]);
+      splats.resize(e - b);
+      for (int64_t j = b; j < e; ++j) splats[j - b] = make_splat(v->proj[wl.items[j].pidx], v->scene, camera);
+      auto one = [&](int64_t p, S qx, S qy, S t) {
+        contributors_one<S>(e - b, [&](int64_t j) -> const Splat<S>& { return splats[j]; }, qx, qy, t, !camera, v->st, pos, cl);
+        uint64_t hsh = 0xcbf29ce484222325ull;
+        bool flagged = query_flag && query_flag[p];
+        for (size_t k = 0; k < pos.size(); ++k) {
+          const int64_t src = wl.items[b + pos[k]].src;
+          hsh = (hsh ^ (uint64_t)(2 * src + cl[k])) * 0x100000001b3ull;
+          if (gauss_flag && gauss_flag[src]) flagged = true;
+        }
+        if (hash) hash[p] = hsh;
+        if (flagged) {
+          if (query_flag) query_flag[p] = 1;
+          if (gauss_mask)
+            for (size_t k = 0; k < pos.size(); ++k) gauss_mask[wl.items[b + pos[k]].src] = 1;
+        }
+      };
+      if (camera) {
+        const int tx = (int)(tile % wl.tiles_x), ty = (int)(tile / wl.tiles_x);
+        for (int py = ty * kTile; py < std::min(H, (ty + 1) * kTile); ++py) {
+          const S t = pixel_capture_offset<S>(py, H, v->cam.shutter_duration, v->cam.time_offset);
+          for (int px = tx * kTile; px < std::min(W, (tx + 1) * kTile); ++px) one((int64_t)py * W + px, S(px) + S(0.5), S(py) + S(0.5), t);
+        }
+      } else {
+        for (int64_t p = v->ray_begin[tile]; p < v->ray_end[tile]; ++p) one(p, v->rays[p].phi, v->rays[p].omega, v->rays[p].t);
+      }
+    }
+  });
+  return 0;
+}
+
 }  // namespace
 
 #define ORC_API(SUF, S)                                                                                                  \
@@ -456,6 +505,10 @@ int view_brute(void* vv, int early_exit, S* blend16, S* alpha, int64_t* n_contri
   extern "C" int64_t orc_view_array_##SUF(void* v, const char* name, void* dst) { return view_array<S>(v, name, dst); }  \
   extern "C" int orc_view_brute_##SUF(void* v, int early_exit, S* blend16, S* alpha, int64_t* n_contrib) {               \
     return view_brute<S>(v, early_exit, blend16, alpha, n_contrib);                                                      \
+  }                                                                                                                      \
+  extern "C" int orc_view_contrib_##SUF(void* v, const uint8_t* gauss_flag, uint8_t* query_flag, uint8_t* gauss_mask,     \
+                                        uint64_t* hash, int workers) {                                                   \
+    return view_contrib<S>(v, gauss_flag, query_flag, gauss_mask, hash, workers);                                        \
   }                                                                                                                      \
   /* ---- known-answer helpers (SPEC examples) ---- */                                                                   \
   extern "C" void orc_covariance_from_scale_quat_##SUF(const S* scale_log, const S* quat, S* out9) {                     \

@@ -169,6 +169,19 @@ class OracleView:
         getattr(self.L, f"orc_view_brute_{self.suf}")(self.h, C.c_int(int(early_exit)), _p(blend), _p(alpha), _p(nc))
         return blend, alpha, nc
 
+    def contrib(self, gauss_flag=None, query_flag=None, want_hash=False, workers=1):
+        """Contributor introspection (gradient parity gate): per-query signature of the blended (source index, clamped)
+        sequence; a query blending a Gaussian with gauss_flag set is added to query_flag; every Gaussian blended by a
+        flagged query is marked. Returns (hash or None, query_flag, gauss_mask)."""
+        n = self.scene.n
+        gf = None if gauss_flag is None else np.ascontiguousarray(gauss_flag, np.uint8)
+        qf = np.zeros(self.P, np.uint8) if query_flag is None else np.ascontiguousarray(query_flag, np.uint8).copy()
+        gm = np.zeros(n, np.uint8)
+        h = np.zeros(self.P, np.uint64) if want_hash else None
+        getattr(self.L, f"orc_view_contrib_{self.suf}")(self.h, _p(gf) if gf is not None else None, _p(qf), _p(gm),
+                                                        _p(h) if h is not None else None, C.c_int(workers))
+        return h, qf, gm
+
     def ms(self):
         return self.array("ms").astype(np.float64)
 

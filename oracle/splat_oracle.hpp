@@ -1360,6 +1360,28 @@ inline void composite_one(int64_t count, GetSplat get, S qx, S qy, S t, bool lid
   }
 }
 
+/// Test-only introspection: the list positions (0-based, tile-local) a query blends, found by the very loop of
+/// composite_one (same skip rules, same transmittance cut-off). Used by the gradient parity gate to find the
+/// queries on which the fp32 and the fp64 forward passes take different discrete decisions, and the Gaussians those
+/// queries touch.
+template <class S, class GetSplat>
+inline void contributors_one(int64_t count, GetSplat get, S qx, S qy, S t, bool lidar, const RasterSettings<S>& st,
+                             std::vector<int32_t>& pos, std::vector<uint8_t>& was_clamped) {
+  pos.clear();
+  was_clamped.clear();
+  S T = S(1);
+  for (int64_t j = 0; j < count; ++j) {
+    const Splat<S>& g = get(j);
+    S alpha, dx, dy, gauss;
+    bool clamped;
+    if (!evaluate_alpha(g, qx, qy, t, st, lidar, alpha, dx, dy, gauss, clamped)) continue;
+    T = T * (S(1) - alpha);
+    pos.push_back((int32_t)j);
+    was_clamped.push_back(clamped ? 1 : 0);
+    if (T < st.transmittance_min) break;
+  }
+}
+
 template <class S> void finish_lidar(S* px, S T, S range_acc, S median) {
   const S A = S(1) - T;
   px[13] = (A > S(1e-6)) ? range_acc / A : range_acc;

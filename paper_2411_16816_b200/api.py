@@ -37,6 +37,8 @@ SYMBOLS = [
     "splatb200_view_n_contrib", "splatb200_view_backward", "splatb200_view_sensor_grads", "splatb200_view_download",
     "splatb200_view_backward_host", "splatb200_view_download_async", "splatb200_view_forward_to_host", "splatb200_view_backward_from_host", "splatb200_view_backward_host_overlapped", "splatb200_view_array", "splatb200_view_composed", "splatb200_view_projected",
     "splatb200_view_project_backward", "splatb200_view_compose_backward", "splatb200_view_backward_projected",
+    "splatb200_optimizer_reset", "splatb200_nccl_unique_id", "splatb200_ctx_comm_init", "splatb200_ctx_comm_bind",
+    "splatb200_ctx_comm_destroy", "splatb200_ctx_comm_info", "splatb200_allreduce_grads", "splatb200_sharded_optimizer_step",
 ]
 
 
@@ -163,12 +165,28 @@ def lib():
                                                   C.c_void_p, C.c_int64, C.c_void_p]
         L.splatb200_ctx_create.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
         L.splatb200_lidar_grid.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_optimizer_reset.argtypes = [C.c_void_p]
+        L.splatb200_nccl_unique_id.argtypes = [C.c_void_p]
+        L.splatb200_ctx_comm_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
+        L.splatb200_ctx_comm_bind.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
+        L.splatb200_ctx_comm_destroy.argtypes = [C.c_void_p]
+        L.splatb200_ctx_comm_info.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.splatb200_allreduce_grads.argtypes = [C.c_void_p]
+        L.splatb200_sharded_optimizer_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         _LIB = L
     return _LIB
 
 
 def _p(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library's run-time NCCL binding: 128 bytes rank 0 hands to every rank."""
+    buf = C.create_string_buffer(128)
+    if lib().splatb200_nccl_unique_id(buf) != 0:
+        raise SplatError("NCCL is not available (libnccl.so.2 could not be bound)")
+    return buf.raw
 
 
 def _f32(a):
@@ -296,6 +314,40 @@ class Context:
         skipped = (C.c_int32 * 6)()
         skip = None if skip_groups is None else (C.c_int32 * 6)(*[int(x) for x in skip_groups])
         self._check(self.L.splatb200_optimizer_step_range(self.h, C.byref(pod), int(step), int(lo), int(hi), skip, skipped))
+        return [k for k in range(6) if skipped[k]]
+
+    def optimizer_reset(self):
+        """Forget the Adam moments (an upload_scene of the same shape keeps them)."""
+        self._check(self.L.splatb200_optimizer_reset(self.h))
+
+    # ---- multi-GPU (SPEC.md:471; scene.hpp:351-362): the gradient all-reduce through the C ABI --------------------
+    def comm_init(self, unique_id: bytes, rank: int, world: int):
+        """ncclCommInitRank with the id from nccl_unique_id() (created on rank 0, distributed out of band)."""
+        assert len(unique_id) == 128
+        self._check(self.L.splatb200_ctx_comm_init(self.h, C.c_char_p(unique_id), int(rank), int(world)))
+
+    def comm_bind(self, nccl_comm_ptr: int, rank: int, world: int):
+        self._check(self.L.splatb200_ctx_comm_bind(self.h, C.c_void_p(nccl_comm_ptr), int(rank), int(world)))
+
+    def comm_destroy(self):
+        self._check(self.L.splatb200_ctx_comm_destroy(self.h))
+
+    @property
+    def comm_world(self) -> int:
+        w = C.c_int32(0)
+        self.L.splatb200_ctx_comm_info(self.h, None, C.byref(w))
+        return int(w.value)
+
+    def allreduce_grads(self):
+        """In-place SUM of SceneParamGrads (and the ActorGrad slots) over the ranks of the ctx's communicator; ordered
+        after every view stream, enqueued on the ctx stream."""
+        self._check(self.L.splatb200_allreduce_grads(self.h))
+
+    def sharded_optimizer_step(self, cfg: dict, step: int):
+        """optimizer_step fused with the collective: reduce each shard to its owner, Adam on the shard, broadcast."""
+        pod = self._adam_pod(cfg)
+        skipped = (C.c_int32 * 6)()
+        self._check(self.L.splatb200_sharded_optimizer_step(self.h, C.byref(pod), int(step), skipped))
         return [k for k in range(6) if skipped[k]]
 
     def download_scene(self):

@@ -745,11 +745,8 @@ constexpr size_t kHdrWords = 64;  // tickets [0..15], error flag [16]
 template <int kSrc, bool kWriteKeys>
 void launch_pass(const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, int64_t n, int shift, int bits,
                  const uint32_t* hist, uint32_t* state, uint32_t* ticket, uint32_t* err, const EmitSrc& em, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_radix_pass<kSrc, kWriteKeys>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRadixSmem);
-    attr = true;
-  }
+  static DeviceOnce once;
+  once.run([] { cudaFuncSetAttribute(k_radix_pass<kSrc, kWriteKeys>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRadixSmem); });
   k_radix_pass<kSrc, kWriteKeys><<<(unsigned)radix_tiles(n), kRThreads, kRadixSmem, st>>>(ki, vi, ko, vo, n, shift, bits, hist,
                                                                                           state, ticket, err, em);
 }
@@ -838,11 +835,8 @@ int launch_tile_counts(int64_t n, const ProjDev& p, int shift, int tiles_x, int 
   }
   const size_t smem = tile_scratch_bytes(tiles_x, tiles_y);
   const bool in_smem = smem <= kScanSmemMax;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmemMax);
-    attr = true;
-  }
+  static DeviceOnce once;
+  once.run([] { cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmemMax); });
   if (!want_hist) hist = nullptr;  // the grid is not sorted on (two-level binning sorts blocks, not tiles)
   k_tile_scan<<<1, 1024, in_smem ? smem : 0, st>>>(tiles_x, tiles_y, slots, in_smem ? nullptr : scratch, tile_begin, tile_end, hist,
                                                    tile_passes((int64_t)tiles_x * tiles_y), tile_order, total, seg_first, kSeg);

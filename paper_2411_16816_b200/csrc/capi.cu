@@ -9,8 +9,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "../../include/splat_b200.h"
 #include "kernels.h"
@@ -62,6 +66,12 @@ struct splatb200_ctx {
   float *adam_m = nullptr, *adam_v = nullptr;
   int64_t adam_floats = 0;
   int* adam_bad = nullptr;
+  // NCCL communicator of the gradient all-reduce (splatb200_ctx_comm_init / _comm_bind); void*: ncclComm_t
+  void* comm = nullptr;
+  bool owns_comm = false;
+  int comm_rank = 0, comm_world = 0;
+  double* comm_stage = nullptr;  // device staging of the ActorGrad slots
+  size_t comm_stage_bytes = 0;
 
   int fail(int code, const std::string& m) {
     err = m;
@@ -488,6 +498,7 @@ extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   while (!c->views.empty()) splatb200_view_destroy(c->views.back());
+  splatb200_ctx_comm_destroy(c);
   free_scene(c);
   delete c;
 }
@@ -600,6 +611,23 @@ extern "C" int splatb200_scene_bind_device(splatb200_ctx* c, int64_t n, int32_t 
   c->actor_first.clear();
   c->bound_max_actor = max_actor_id;
   for (auto* v : c->views) v->stage = 0;
+  if (n > 0 && actor_id) {
+    // the caller's max_actor_id is a claim: ids outside [0, max_actor_id] would index the actor table out of bounds on
+    // the device (scene_upload checks the same on the host)
+    int h[2] = {0x7fffffff, -0x7fffffff - 1};
+    int* d = nullptr;
+    CU_TRY(c, cudaMalloc(&d, sizeof(h)));
+    cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, c->stream);
+    launch_actor_id_range(actor_id, n, d, c->stream);
+    cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return c->fail(SPLATB200_ECUDA, std::string("scene_bind_device: ") + cudaGetErrorString(e));
+    c->launches += 1;
+    if (h[0] < 0 || h[1] > max_actor_id)
+      return c->fail(SPLATB200_EOUTOFRANGE, "scene_bind_device: actor_id values span [" + std::to_string(h[0]) + ", " +
+                                                std::to_string(h[1]) + "], outside [0, max_actor_id = " + std::to_string(max_actor_id) + "]");
+  }
   if (keep_grads && keep_floats == (int64_t)(14 + d_f) * n) {
     c->grads = keep_grads;
     c->grads_floats = keep_floats;
@@ -929,6 +957,11 @@ extern "C" int splatb200_optimizer_step_range(splatb200_ctx* c, const splatb200_
       CU_TRY(c, cudaMemcpy(c->adam_bad, cur, sizeof(cur), cudaMemcpyHostToDevice));
     }
   }
+  for (int k = 0; k < 6; ++k) {  // lr_init == 0 freezes a group; anything else must be a valid exponential schedule
+    if (!(cfg->lr_init[k] >= 0.0f) || (cfg->lr_init[k] > 0.0f && !(cfg->lr_final[k] > 0.0f)) || !std::isfinite(cfg->lr_init[k]) ||
+        !std::isfinite(cfg->lr_final[k]))
+      return c->fail(SPLATB200_EINVAL, "optimizer_step: group " + std::to_string(k) + " needs lr_init >= 0 and, unless frozen (lr_init == 0), lr_final > 0");
+  }
   const AdamGroups gr = adam_groups(c);
   float* params[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
   const double t1 = (double)step + 1.0;
@@ -941,6 +974,7 @@ extern "C" int splatb200_optimizer_step_range(splatb200_ctx* c, const splatb200_
     const double ramp = w > 0 ? std::min(1.0, (double)step / w) : 1.0;
     const double denom = (double)cfg->total_steps - w;
     const double t = denom > 0 ? std::min(1.0, std::max(0.0, ((double)step - w) / denom)) : 1.0;
+    if (cfg->lr_init[k] == 0.0f) continue;  // frozen group: parameters and moments untouched
     const double lr = ramp * (double)cfg->lr_init[k] * std::pow((double)cfg->lr_final[k] / (double)cfg->lr_init[k], t);
     launch_adam(params[k] + (a - gr.begin[k]), c->grads + a, c->adam_m + a, c->adam_v + a, b - a, (float)lr, bc1, bc2,
                 c->adam_bad + k, c->stream);
@@ -960,6 +994,229 @@ extern "C" int splatb200_optimizer_step_range(splatb200_ctx* c, const splatb200_
 
 extern "C" int splatb200_optimizer_step(splatb200_ctx* c, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]) {
   return splatb200_optimizer_step_range(c, cfg, step, 0, c->grads_floats, nullptr, skipped);
+}
+
+extern "C" int splatb200_optimizer_reset(splatb200_ctx* c) {
+  // forget the Adam moments (a scene_upload of the same shape keeps them: that is the per-iteration parameter refresh)
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(c->adam_m); dfree(c->adam_v); dfree(c->adam_bad);
+  c->adam_floats = 0;
+  return SPLATB200_OK;
+}
+
+// ---- multi-GPU: NCCL all-reduce of SceneParamGrads (scene.hpp:351-362) ----------------------------------
+// NCCL is bound at run time: a trainer (or torch) has its own libnccl.so.2 in the process, and a second copy linked into
+// this library could not share its communicators.
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string why;
+};
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if (!api.h) api.h = dlopen(n, RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);  // the copy the process already uses
+    for (const char* n : names)
+      if (!api.h) api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (!api.h) { api.why = std::string("libnccl.so.2 not found: ") + dlerror(); return; }
+    auto sym = [&](const char* s) { void* p = dlsym(api.h, s); if (!p && api.why.empty()) api.why = std::string("missing NCCL symbol ") + s; return p; };
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.Reduce = (decltype(api.Reduce))sym("ncclReduce");
+    api.Broadcast = (decltype(api.Broadcast))sym("ncclBroadcast");
+    api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+  });
+  return api.why.empty() ? &api : nullptr;
+}
+#define NCCL_TRY(ctx, api, call)                                                                                   \
+  do {                                                                                                             \
+    ncclResult_t r__ = (call);                                                                                     \
+    if (r__ != ncclSuccess) return (ctx)->fail(SPLATB200_ERUNTIME, std::string(#call) + ": " + (api)->GetErrorString(r__)); \
+  } while (0)
+
+// [lo, hi) of the flat gradient layout owned by `rank`: equal shards aligned to 4 floats (the last may be shorter)
+void shard_of(int64_t total, int world, int rank, int64_t& lo, int64_t& hi) {
+  int64_t per = (total + world - 1) / world;
+  per = (per + 3) / 4 * 4;
+  lo = std::min<int64_t>(total, (int64_t)rank * per);
+  hi = std::min<int64_t>(total, lo + per);
+}
+}  // namespace
+
+extern "C" int splatb200_nccl_unique_id(void* id128) {
+  NcclApi* a = nccl_api();
+  if (!a || !id128) return SPLATB200_ERUNTIME;
+  ncclUniqueId id;
+  if (a->GetUniqueId(&id) != ncclSuccess) return SPLATB200_ERUNTIME;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id128, &id, 128);
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_ctx_comm_destroy(splatb200_ctx* c) {
+  if (c->comm && c->owns_comm) {
+    NcclApi* a = nccl_api();
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (a) a->CommDestroy((ncclComm_t)c->comm);
+  }
+  c->comm = nullptr;
+  c->owns_comm = false;
+  c->comm_rank = 0;
+  c->comm_world = 0;
+  dfree(c->comm_stage);
+  c->comm_stage_bytes = 0;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_ctx_comm_init(splatb200_ctx* c, const void* id128, int32_t rank, int32_t world) {
+  NcclApi* a = nccl_api();
+  if (!a) return c->fail(SPLATB200_ERUNTIME, "comm_init: libnccl.so.2 could not be bound at run time");
+  if (!id128 || world < 1 || rank < 0 || rank >= world) return c->fail(SPLATB200_EINVAL, "comm_init: need 0 <= rank < world and an id");
+  splatb200_ctx_comm_destroy(c);
+  CU_TRY(c, cudaSetDevice(c->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  ncclComm_t comm = nullptr;
+  NCCL_TRY(c, a, a->CommInitRank(&comm, world, id, rank));
+  c->comm = comm;
+  c->owns_comm = true;
+  c->comm_rank = rank;
+  c->comm_world = world;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_ctx_comm_bind(splatb200_ctx* c, void* nccl_comm, int32_t rank, int32_t world) {
+  if (!nccl_api()) return c->fail(SPLATB200_ERUNTIME, "comm_bind: libnccl.so.2 could not be bound at run time");
+  if (!nccl_comm || world < 1 || rank < 0 || rank >= world) return c->fail(SPLATB200_EINVAL, "comm_bind: need a communicator and 0 <= rank < world");
+  splatb200_ctx_comm_destroy(c);
+  c->comm = nccl_comm;
+  c->owns_comm = false;
+  c->comm_rank = rank;
+  c->comm_world = world;
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_ctx_comm_info(const splatb200_ctx* c, int32_t* rank, int32_t* world) {
+  if (rank) *rank = c->comm_rank;
+  if (world) *world = c->comm ? c->comm_world : 0;
+  return SPLATB200_OK;
+}
+
+// ActorGrad slots (host doubles) packed into one device buffer and summed over ranks with the same communicator
+static int allreduce_actor_grads(splatb200_ctx* c, NcclApi* a) {
+  const size_t na = c->tracks.size();
+  if (na == 0) return SPLATB200_OK;
+  for (auto* v : c->views) {
+    int rc = finalize_actor_grads(v);
+    if (rc) return rc;
+  }
+  if (c->actor_d_pose.size() != na) reset_actor_grads(c);
+  std::vector<double> flat;
+  for (size_t t = 0; t < na; ++t) {
+    flat.insert(flat.end(), c->actor_d_pose[t].begin(), c->actor_d_pose[t].end());
+    flat.insert(flat.end(), c->actor_d_vel[t].begin(), c->actor_d_vel[t].end());
+  }
+  if (c->comm_stage_bytes < flat.size() * sizeof(double)) {
+    dfree(c->comm_stage);
+    CU_TRY(c, cudaMalloc(&c->comm_stage, flat.size() * sizeof(double)));
+    c->comm_stage_bytes = flat.size() * sizeof(double);
+  }
+  CU_TRY(c, cudaMemcpyAsync(c->comm_stage, flat.data(), flat.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, a, a->AllReduce(c->comm_stage, c->comm_stage, flat.size(), ncclDouble, ncclSum, (ncclComm_t)c->comm, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(flat.data(), c->comm_stage, flat.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  size_t o = 0;
+  for (size_t t = 0; t < na; ++t) {
+    std::copy(flat.begin() + o, flat.begin() + o + c->actor_d_pose[t].size(), c->actor_d_pose[t].begin());
+    o += c->actor_d_pose[t].size();
+    std::copy(flat.begin() + o, flat.begin() + o + 6, c->actor_d_vel[t].begin());
+    o += 6;
+  }
+  return SPLATB200_OK;
+}
+
+extern "C" int splatb200_allreduce_grads(splatb200_ctx* c) {
+  if (!c->comm) return c->fail(SPLATB200_ERUNTIME, "allreduce_grads without a communicator (splatb200_ctx_comm_init / _comm_bind)");
+  NcclApi* a = nccl_api();
+  if (!a) return c->fail(SPLATB200_ERUNTIME, "allreduce_grads: NCCL is not available");
+  if (!c->grads) return c->fail(SPLATB200_ERUNTIME, "allreduce_grads without a scene");
+  CU_TRY(c, cudaSetDevice(c->device));
+  join_all(c);  // every view's backward (on its own stream) precedes the collective on the ctx stream
+  if (c->grads_floats > 0)
+    NCCL_TRY(c, a, a->AllReduce(c->grads, c->grads, (size_t)c->grads_floats, ncclFloat, ncclSum, (ncclComm_t)c->comm, c->stream));
+  return allreduce_actor_grads(c, a);
+}
+
+extern "C" int splatb200_sharded_optimizer_step(splatb200_ctx* c, const splatb200_adam_config* cfg, int64_t step, int32_t skipped[6]) {
+  if (!c->comm) return c->fail(SPLATB200_ERUNTIME, "sharded_optimizer_step without a communicator");
+  NcclApi* a = nccl_api();
+  if (!a) return c->fail(SPLATB200_ERUNTIME, "sharded_optimizer_step: NCCL is not available");
+  if (!cfg || step < 0) return c->fail(SPLATB200_EINVAL, "optimizer_step: bad arguments");
+  if (!c->mean || !c->grads) return c->fail(SPLATB200_ERUNTIME, "optimizer_step without a scene");
+  CU_TRY(c, cudaSetDevice(c->device));
+  join_all(c);
+  const int world = c->comm_world, rank = c->comm_rank;
+  const int64_t total = c->grads_floats;
+  ncclComm_t comm = (ncclComm_t)c->comm;
+  // (1) each shard is summed onto its owner (a reduce-scatter with ragged shards, one fused NCCL group)
+  NCCL_TRY(c, a, a->GroupStart());
+  for (int r = 0; r < world; ++r) {
+    int64_t lo, hi;
+    shard_of(total, world, r, lo, hi);
+    if (hi > lo) NCCL_TRY(c, a, a->Reduce(c->grads + lo, c->grads + lo, (size_t)(hi - lo), ncclFloat, ncclSum, r, comm, c->stream));
+  }
+  NCCL_TRY(c, a, a->GroupEnd());
+  // (2) groups to skip: a non-finite gradient in any shard skips the group on every rank
+  int64_t lo, hi;
+  shard_of(total, world, rank, lo, hi);
+  int rc = ensure_adam_state(c);
+  if (!rc) rc = flag_nonfinite(c, lo, hi);
+  if (rc) return rc;
+  NCCL_TRY(c, a, a->AllReduce(c->adam_bad, c->adam_bad, 6, ncclInt32, ncclMax, comm, c->stream));
+  int h[6];
+  CU_TRY(c, cudaMemcpyAsync(h, c->adam_bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  int32_t skip[6];
+  for (int k = 0; k < 6; ++k) skip[k] = h[k] != 0;
+  // (3) Adam on this rank's shard only
+  rc = splatb200_optimizer_step_range(c, cfg, step, lo, hi, skip, skipped);
+  if (rc) return rc;
+  // (4) every owner broadcasts its updated slice of each parameter group (an all-gather with ragged shards)
+  const AdamGroups gr = adam_groups(c);
+  float* params[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
+  NCCL_TRY(c, a, a->GroupStart());
+  for (int r = 0; r < world; ++r) {
+    int64_t rlo, rhi;
+    shard_of(total, world, r, rlo, rhi);
+    for (int k = 0; k < 6; ++k) {
+      const int64_t b0 = std::max(gr.begin[k], rlo), b1 = std::min(gr.begin[k + 1], rhi);
+      if (b1 <= b0) continue;
+      float* ptr = params[k] + (b0 - gr.begin[k]);
+      NCCL_TRY(c, a, a->Broadcast(ptr, ptr, (size_t)(b1 - b0), ncclFloat, r, comm, c->stream));
+    }
+  }
+  NCCL_TRY(c, a, a->GroupEnd());
+  if (skipped)
+    for (int k = 0; k < 6; ++k) skipped[k] = skip[k];
+  return SPLATB200_OK;
 }
 
 extern "C" int splatb200_scene_download(splatb200_ctx* c, float* mean, float* scale_log, float* quat, float* opacity_logit,
@@ -2060,6 +2317,35 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
       for (int w = 0; w < df->width; ++w) d[k * df->width + w] = h[i * kDumpStride + df->off + w];
     }
     return (int64_t)rows * df->width;
+  }
+
+  if (name == "packed_record") {
+    // what k_project STORED for the compositing kernels (not a recomputation): per visible Gaussian, in source order,
+    // geomA (mean2d.xy, velocity.xy) | geomB (conic a, 2b, c, rho) | geomC (depth key, v_r) | the 16 channel slots
+    std::vector<uint32_t> cnt;
+    int rc = fetch(c, cnt, v->proj.count, N);
+    if (rc) return rc;
+    std::vector<size_t> vis;
+    for (size_t i = 0; i < N; ++i) if (cnt[i]) vis.push_back(i);
+    constexpr int kW = 26;
+    if (!dst) return (int64_t)vis.size() * kW;
+    std::vector<float4> gA, gB, gF;
+    std::vector<float2> gC;
+    rc = fetch(c, gA, (const float4*)v->proj.geomA, N);
+    if (!rc) rc = fetch(c, gB, (const float4*)v->proj.geomB, N);
+    if (!rc) rc = fetch(c, gC, (const float2*)v->proj.geomC, N);
+    if (!rc) rc = fetch(c, gF, (const float4*)v->proj.feat, 4 * N);
+    if (rc) return rc;
+    float* d = (float*)dst;
+    for (size_t k = 0; k < vis.size(); ++k) {
+      const size_t i = vis[k];
+      float* o = d + kW * k;
+      o[0] = gA[i].x; o[1] = gA[i].y; o[2] = gA[i].z; o[3] = gA[i].w;
+      o[4] = gB[i].x; o[5] = gB[i].y; o[6] = gB[i].z; o[7] = gB[i].w;
+      o[8] = gC[i].x; o[9] = gC[i].y;
+      for (int q = 0; q < 4; ++q) { o[10 + 4 * q] = gF[4 * i + q].x; o[11 + 4 * q] = gF[4 * i + q].y; o[12 + 4 * q] = gF[4 * i + q].z; o[13 + 4 * q] = gF[4 * i + q].w; }
+    }
+    return (int64_t)vis.size() * kW;
   }
 
   if (name == "isect_tile" || name == "isect_depth_bits" || name == "isect_src") {

@@ -399,22 +399,14 @@ __global__ void __launch_bounds__(256) k_decoder_input(int H, int W, int d_f, fl
 }
 
 int conv_grid(int H, int W) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   const int tiles = ((W + kCTW - 1) / kCTW) * ((H + kCTR - 1) / kCTR);
   return tiles < sms ? tiles : sms;
 }
 
 template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(k_conv3x3_tc<kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmemBytes);
-    once = true;
-  }
+  static DeviceOnce once;
+  once.run([] { cudaFuncSetAttribute(k_conv3x3_tc<kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmemBytes); });
   k_conv3x3_tc<kHead><<<conv_grid(a.H + 2 * a.ext, a.W + 2 * a.ext), kWsThreads, kWsSmemBytes, st>>>(a);
 }
 
@@ -766,22 +758,11 @@ __global__ void __launch_bounds__(256) k_dec_head_bwd(int64_t P, const float* __
   for (int i = threadIdx.x; i < 198; i += blockDim.x) atomicAdd(g_head + i, sAcc[i]);
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+int sm_count() { return device_sm_count(); }
 
 void launch_wgrad(const float* x, const float* gy, float* gw, int H, int W, int relu_in, int* err, cudaStream_t st) {
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(k_conv3x3_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmemBytes);
-    once = true;
-  }
+  static DeviceOnce once;
+  once.run([] { cudaFuncSetAttribute(k_conv3x3_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmemBytes); });
   WgradArgs a{x, gy, gw, H, W, relu_in, err};
   const int tiles = ((W + kWT - 1) / kWT) * ((H + 1) / 2);
   k_conv3x3_wgrad_tc<<<tiles < 2 * sm_count() ? tiles : 2 * sm_count(), kCThreads, kWSmemBytes, st>>>(a);

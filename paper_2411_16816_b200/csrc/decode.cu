@@ -153,12 +153,11 @@ void launch_lidar_head_bwd(const float* w, int d_f, int64_t n_rays, const float4
   if (n_rays <= 0) return;
   const int np = lidar_head_params(d_f);
   const size_t smem = sizeof(float) * (((np + 3) & ~3) + 8 * (32 * 33 + 32 * 17));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_lidar_head_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  const unsigned blocks = (unsigned)std::min<int64_t>(148 * 2, (n_rays + 255) / 256);
+  // opt in once per device to the largest size any d_f needs (kInMax inputs), not to the first call's
+  constexpr size_t smem_max = sizeof(float) * (((kHid * kInMax + kHid + 2 * kHid + 2 + 3) & ~3) + 8 * (32 * 33 + 32 * 17));
+  static DeviceOnce once;
+  once.run([] { cudaFuncSetAttribute(k_lidar_head_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max); });
+  const unsigned blocks = (unsigned)std::min<int64_t>(2 * (int64_t)device_sm_count(), (n_rays + 255) / 256);
   k_lidar_head_bwd<<<blocks, 256, smem, st>>>(w, np, d_f, n_rays, rays, blend16, g_y, g_blend16, g_w);
 }
 

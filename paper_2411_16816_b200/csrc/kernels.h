@@ -4,9 +4,39 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "splat_device.cuh"
 
 namespace sb {
+
+// Per-device one-time setup of a kernel (cudaFuncSetAttribute is per device; a ctx may live on any GPU and views may be
+// driven from several host threads): runs f() once for every device the calling site is reached on.
+struct DeviceOnce {
+  std::mutex m;
+  uint64_t done[4] = {0, 0, 0, 0};  // up to 256 devices
+  template <class F> void run(F&& f) {
+    int d = 0;
+    cudaGetDevice(&d);
+    d &= 255;
+    std::lock_guard<std::mutex> g(m);
+    if (!((done[d >> 6] >> (d & 63)) & 1ull)) {
+      f();
+      done[d >> 6] |= 1ull << (d & 63);
+    }
+  }
+};
+// SM count of the current device (cached per device)
+inline int device_sm_count() {
+  static std::mutex m;
+  static int sms[256] = {0};
+  int d = 0;
+  cudaGetDevice(&d);
+  d &= 255;
+  std::lock_guard<std::mutex> g(m);
+  if (!sms[d]) cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d);
+  return sms[d];
+}
 
 struct RasterOutDev {
   float* blend;        // P x 16
@@ -66,6 +96,7 @@ void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaS
 // optim.cu (optimizer_step): Adam over the GaussianSet from the contiguous SceneParamGrads buffer
 struct AdamGroups { int64_t begin[7]; };  // slices of the gradient buffer: mean, scale_log, quat, opacity_logit, color, feature
 void launch_grad_finite(const float* g, int64_t n_floats, const AdamGroups& gr, int* bad6, cudaStream_t st);
+void launch_actor_id_range(const int32_t* id, int64_t n, int* mn_mx /* device, preset to {INT_MAX, INT_MIN} */, cudaStream_t st);
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float bc1, float bc2, const int* bad,
                  cudaStream_t st);
 

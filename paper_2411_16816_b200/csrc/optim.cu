@@ -50,6 +50,26 @@ k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m
   }
 }
 
+// min / max of a bound actor_id array (scene_bind_device validates what scene_upload checks on the host)
+__global__ void __launch_bounds__(256) k_actor_id_range(const int32_t* __restrict__ id, int64_t n, int* __restrict__ mn_mx) {
+  int lo = 0x7fffffff, hi = -0x7fffffff - 1;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+    const int v = id[i];
+    lo = min(lo, v); hi = max(hi, v);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) { atomicMin(&mn_mx[0], lo); atomicMax(&mn_mx[1], hi); }
+}
+void launch_actor_id_range(const int32_t* id, int64_t n, int* mn_mx, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>(148 * 4, (n + 255) / 256);
+  k_actor_id_range<<<blocks, 256, 0, st>>>(id, n, mn_mx);
+}
+
 void launch_grad_finite(const float* g, int64_t n_floats, const AdamGroups& gr, int* bad, cudaStream_t st) {
   if (n_floats <= 0) return;
   const unsigned blocks = (unsigned)std::min<int64_t>(148 * 8, (n_floats + 255) / 256);

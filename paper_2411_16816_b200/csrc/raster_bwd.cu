@@ -437,13 +437,12 @@ void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
   if (tiles <= 0) return;
   if (tile_count < 0) tile_first = 0;
   else tile_order = nullptr;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceOnce once;
+  once.run([] {
     cudaFuncSetAttribute(k_raster_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
     cudaFuncSetAttribute(k_raster_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
     cudaFuncSetAttribute(k_raster_bwd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
-    attr_set = true;
-  }
+  });
   if (s.is_camera)
     k_raster_bwd<true><<<tiles, 256, kBwdSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
                                                      tile_first, fwd, g_blend16, g_alpha, rg, pg, d_time_offset);

@@ -29,12 +29,33 @@ def assign_frames(n_frames: int, world: int, rank: int, costs: Sequence[float] |
     return sorted(mine)
 
 
-def allreduce_grads(grads, group=None):
-    """In-place SUM of the contiguous 27*N-float SceneParamGrads buffer over all ranks (one collective per step).
-    `grads` is a torch tensor: on the GPU it is the buffer bound with splatb200_grads_bind_device, so NCCL reduces the
-    kernels' output in place."""
+def init_comm(ctx, group=None):
+    """Create the library's own NCCL communicator over the ranks of `group` (torch.distributed is only the out-of-band
+    channel for the 128-byte id, exactly what MPI_Bcast is in a C++ trainer). Returns the world size (1: nothing to do)."""
     import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return 1
+    from . import api
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [api.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    ctx.comm_init(box[0], rank, world)
+    return world
+
+
+def allreduce_grads(grads, group=None, ctx=None):
+    """In-place SUM of the contiguous 27*N-float SceneParamGrads buffer over all ranks (one collective per step).
+    With a ctx that owns a communicator (init_comm) the collective is the library's splatb200_allreduce_grads: ncclAllReduce
+    on the ctx stream, ordered after the view streams, ActorGrad slots included. Otherwise `grads` (the torch tensor bound
+    with splatb200_grads_bind_device) is reduced by torch.distributed — the CPU / gloo tests and callers that keep
+    their own process group."""
+    import torch.distributed as dist
+    if ctx is not None and ctx.comm_world > 1:
+        ctx.allreduce_grads()
+        return grads
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if ctx is not None:
+            ctx.join()
         dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
     return grads
 
@@ -72,6 +93,13 @@ def sharded_optimizer_step(ctx, grads, params_flat, cfg, step, group=None):
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
+    if ctx.comm_world > 1:     # the library's own communicator: the whole step is one C-ABI call
+        return ctx.sharded_optimizer_step(cfg, step)
+    # torch collectives run on torch's current stream, the library's kernels on the ctx stream (and the view streams):
+    # order the collectives after the backward kernels, and the library's reads after the collectives
+    ctx.join()
+    if grads.is_cuda:
+        ctx.sync()
     total = grads.numel()
     lo, hi = shard_range(total, world, rank)
     per = shard_range(total, world, 0)[1]
@@ -87,11 +115,15 @@ def sharded_optimizer_step(ctx, grads, params_flat, cfg, step, group=None):
             grads[lo:hi] = out[:hi - lo]
         else:
             dist.reduce_scatter_tensor(grads[lo:hi], grads, op=dist.ReduceOp.SUM, group=group)
+    if grads.is_cuda:
+        torch.cuda.current_stream(grads.device).synchronize()
     flags = torch.tensor(ctx.grads_nonfinite_range(lo, hi), dtype=torch.int32, device=grads.device)
     if world > 1:
         dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
     skip = [int(x) for x in flags.tolist()]
     ctx.optimizer_step_range(cfg, step, lo, hi, skip_groups=skip)
+    if params_flat is not None and params_flat.is_cuda:
+        ctx.sync()      # the all-gather below (torch's stream) reads what k_adam wrote on the ctx stream
     if gloo:
         send = torch.zeros(per, dtype=params_flat.dtype)
         send[:hi - lo] = params_flat[lo:hi]

@@ -107,6 +107,14 @@ class _NumpyAdamCtx:
         w = [3, 3, 4, 1, 3, d_f]
         self.begin = np.concatenate([[0], np.cumsum([x * n for x in w])])
 
+    comm_world = 0      # no library communicator on CPU: the torch.distributed (gloo) branch is under test
+
+    def join(self):
+        pass
+
+    def sync(self):
+        pass
+
     def _slices(self, lo, hi):
         for k in range(6):
             a, b = max(self.begin[k], lo), min(self.begin[k + 1], hi)
