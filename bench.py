@@ -11,10 +11,15 @@ libsplat_b200.so (compose -> project -> tile-bin + radix sort -> composite, and 
 
   python bench.py [--gpus N] [--steps K] [--warmup W]            the sm_100a path
   python bench.py --impl reference ...                           the reference's CPU path (the oracle port)
+  python bench.py --config cfg4 | cfg5 [--frames-per-rank F]     BASELINE configs 4 / 5 (3M dynamic Gaussians, 6 cameras + lidar)
 
-N > 1 (torchrun, one rank per GPU): the scene is replicated, rank r renders frame r (ego pose advanced
-1.5 m and camera yawed 60 degrees per frame: independent frames, no data-path collective), and the
-per-Gaussian SceneParamGrads buffer (27 N floats) is all-reduced with NCCL every step — "weak" scaling.
+N > 1: one rank per GPU. Under torchrun (RANK / WORLD_SIZE in the environment) this process is one rank; without it
+`--gpus N` re-executes itself under `python -m torch.distributed.run --nproc-per-node N` (rendezvous on 127.0.0.1).
+The scene is replicated, rank r renders its own frames (ego pose advanced 1.5 m and the camera yawed 60 degrees per
+frame: independent frames, no data-path collective), gradients accumulate on the rank across its frames, and the
+per-Gaussian SceneParamGrads buffer (27 N floats) is summed over ranks ONCE per step by the library's own
+splatb200_allreduce_grads (ncclAllReduce on the ctx stream) — "weak" scaling. `--dry-launch` only starts the ranks and
+lets them rendezvous (gloo without GPUs): the launch path can be checked on a CPU box.
 
 oracle/ is used here only as the CPU baseline (cpu_baseline leg, --impl reference), never on the GPU path.
 """
@@ -52,14 +57,35 @@ def frame_sensors(frame: int):
     return lid, cam
 
 
-def workload_config(world: int):
+def rig_sensors(frame: int):
+    """Frame `frame` of BASELINE config 4 / 5: the 6-camera rig (yaw k*60 deg) + the lidar, ego advanced 1.5 m per frame."""
+    from paper_2411_16816_b200 import synth
+    x = 1.5 * frame
+    lid = synth.lidar128(position=(x, 0.0, 1.8))
+    cams = [synth.make_camera(position=(x, 0.0, 1.5), yaw=k * np.pi / 3.0) for k in range(6)]
+    return lid, cams
+
+
+def workload_config(world: int, config: str = "northstar", frames_per_rank: int = 1):
+    if config != "northstar":
+        return {
+            "workload": f"BASELINE config {'4' if config == 'cfg4' else '5'}: synth-v1 scene N=3,000,000 Gaussians, 32 moving actors "
+                        "(2 % dynamic), one frame = 6 x 1920x1080 rolling-shutter cameras (yaw k*60 deg) + lidar-128 sweep, "
+                        "forward+backward, gradients accumulated over a rank's frames, ONE all-reduce per step",
+            "n_gaussians": 3_000_000, "lidar_rays": 128 * 1800, "camera_pixels": 6 * 1920 * 1080,
+            "frames_per_rank": frames_per_rank, "frames_per_step": frames_per_rank * world,
+            "parallelism": f"frames x{world} (scene replicated, SceneParamGrads all-reduced by splatb200_allreduce_grads)" if world > 1 else "single GPU",
+            "streams": "one per sensor view (7) + the ctx stream; one host thread per view",
+            "l2_policy": "inputs larger than L2 (scene 336 MB, > 1 GB of records and worklists per view); no explicit flush",
+        }
     return {
         "workload": "north-star frame: synth-v1 scene N=1,000,000 static Gaussians (d_f=13), lidar-128 "
                     "(1800 bins, non-uniform elevation, 0.1 s sweep, moving sensor) + 1920x1080 pinhole camera "
                     "(30 ms rolling shutter, moving sensor), forward+backward incl. features/intensity/ray-drop, "
                     "expected+median range",
         "n_gaussians": N_GAUSS, "lidar_rays": 128 * 1800, "camera_pixels": 1920 * 1080,
-        "frames_per_step": world, "parallelism": f"frames x{world} (scene replicated, grads all-reduced)" if world > 1 else "single GPU",
+        "frames_per_rank": frames_per_rank, "frames_per_step": frames_per_rank * world,
+        "parallelism": f"frames x{world} (scene replicated, SceneParamGrads all-reduced by splatb200_allreduce_grads)" if world > 1 else "single GPU",
         "streams": "one per sensor view + the ctx stream; one host thread per view",
         "l2_policy": "inputs larger than L2 (scene 112 MB + per-view records and worklists > 500 MB, L2 126 MB); no explicit flush",
     }
@@ -247,11 +273,69 @@ def pinned(shape, dtype):
     return t, t.numpy()
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks of this very command under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry_launch(args) -> int:
+    """The launch path without the workload: ranks rendezvous (NCCL with GPUs, gloo without), agree on who is there,
+    take the max over ranks of a per-rank number exactly as the timed run does, and rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2411_16816_b200 import dist as sdist
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cuda = torch.cuda.is_available() and torch.cuda.device_count() >= world
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dev = torch.device("cuda", local) if cuda else torch.device("cpu")
+    if cuda:
+        torch.cuda.set_device(local)
+    dist.init_process_group("nccl" if cuda else "gloo", rank=rank, world_size=world, **({"device_id": dev} if cuda else {}))
+    seen = torch.zeros(world, dtype=torch.int64, device=dev)
+    seen[rank] = 1
+    dist.all_reduce(seen)
+    mx = sdist.max_over_ranks(float(rank + 1), device=dev)
+    frames = sdist.assign_frames(args.frames_per_rank * world if args.frames_per_rank else world, world, rank)
+    cnt = torch.tensor([len(frames)], dtype=torch.int64, device=dev)
+    dist.all_reduce(cnt)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_launch": True, "n_gpus": world, "requested_gpus": args.gpus, "backend": "nccl" if cuda else "gloo",
+                          "ranks_seen": int(seen.sum().item()), "max_over_ranks": mx, "frames_assigned": int(cnt.item())}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def load_counters():
+    """Utilisation counters of the committed ncu --set full capture (profiles/counters.json, made by
+    scripts/make_counters_json.py from the same command with --serial). Measured under the profiler: they explain the
+    live CUDA-event times, they are not bench values."""
+    path = os.path.join(ROOT, "profiles", "counters.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
 
     from paper_2411_16816_b200 import api, synth
+    from paper_2411_16816_b200 import dist as sdist
     from paper_2411_16816_b200.model import RasterSettings, Scene
 
     rank = int(os.environ.get("RANK", "0"))
@@ -259,17 +343,28 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the sm_100a path has no CPU fallback; use --impl reference for the CPU path)")
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: reporting n_gpus={world}", file=sys.stderr)
+    if torch.cuda.device_count() < world // max(1, int(os.environ.get("NNODES", "1"))):
+        raise SystemExit(f"bench.py: {world} ranks asked for, {torch.cuda.device_count()} GPUs visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.nccl_log:
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_FILE"] = args.nccl_log + ".%h.%p"
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(device=dev)
     st = RasterSettings()
+    config = args.config
+    rig = config != "northstar"
+    n_gauss = 3_000_000 if rig else N_GAUSS
+    fpr = args.frames_per_rank or (8 if config == "cfg5" else 1)
 
     with torch.cuda.stream(stream):
         ctx = api.Context(local, stream.cuda_stream)
-        scene = synth.make_scene(N_GAUSS, seed=SCENE_SEED)
+        scene = synth.make_scene(n_gauss, seed=4, n_actors=32, dynamic_fraction=0.02) if rig else synth.make_scene(N_GAUSS, seed=SCENE_SEED)
         # host-side (pinned) copy of the GaussianSet: the e2e path uploads it every step
         keep, arrs = [], []
         for a in (scene.mean, scene.scale_log, scene.quat, scene.opacity_logit, scene.color, scene.feature):
@@ -279,18 +374,24 @@ def run_b200(args):
         t_id, v_id = pinned(scene.actor_id.shape, torch.int32)
         v_id[...] = scene.actor_id
         keep.append(t_id)
-        pscene = Scene(*arrs, v_id, [])
+        pscene = Scene(*arrs, v_id, scene.tracks)
         ctx.upload_scene(pscene)
         n_grad = ctx.grads_size
         grads_t = torch.zeros(n_grad, dtype=torch.float32, device=dev)
         ctx.bind_grads_device(grads_t.data_ptr(), n_grad)
+        # the library's own communicator (ncclCommInitRank; torch.distributed only carries the 128-byte id)
+        comm_world = sdist.init_comm(ctx) if world > 1 else 1
 
-        from paper_2411_16816_b200 import dist as sdist
-        (frame,) = sdist.assign_frames(world, world, rank)      # one frame per rank and step: weak scaling
-        lid, cam = frame_sensors(frame)
+        frames = sdist.assign_frames(fpr * world, world, rank)      # fpr frames per rank and step: weak scaling
+        if rig:
+            lid, cams = rig_sensors(frames[0])
+        else:
+            lid, cam0 = frame_sensors(frames[0])
+            cams = [cam0]
         rays = synth.grid_rays(lid)
         vl = ctx.lidar_view(lid, rays, st)
-        vc = ctx.camera_view(cam, st)
+        vcs = [ctx.camera_view(c, st) for c in cams]
+        vc = vcs[0]
         P_l, P_c = vl.P, vc.P
         # upstream gradients: N(0,1) (seeded), pinned on the host and resident on the device
         g_host, g_dev = {}, {}
@@ -310,7 +411,7 @@ def run_b200(args):
             tn, vn = pinned((P,), torch.int32)
             out_host[name] = (tb, ta, tn, vb, va, vn)
         gh_t, gh = pinned((n_grad,), torch.float32)
-        n = N_GAUSS
+        n = n_gauss
         gh_parts = [gh[0:3 * n], gh[3 * n:6 * n], gh[6 * n:10 * n], gh[10 * n:11 * n], gh[11 * n:14 * n], gh[14 * n:]]
         stream.synchronize()
 
@@ -323,24 +424,46 @@ def run_b200(args):
         threaded = [True]     # cleared for the serialised per-stage timing pass
         if HOST_THREADS and not args.serial:
             from concurrent.futures import ThreadPoolExecutor
-            pool = ThreadPoolExecutor(max_workers=2)
+            pool = ThreadPoolExecutor(max_workers=1 + len(vcs))
+
+        def set_frame(f):
+            """point the views at frame f of the drive (no-op when a rank renders one fixed frame)"""
+            if fpr == 1:
+                return 0.0
+            if rig:
+                l, cs = rig_sensors(f)
+            else:
+                l, c0 = frame_sensors(f)
+                cs = [c0]
+            vl.set_lidar_pose(l)
+            for v, c in zip(vcs, cs):
+                v.set_camera(c)
+            return 0.02 * (f % 5) if rig else 0.0      # scene time of the frame (actor tracks span [-0.1, 0.1] s)
 
         def step_device():
             """inputs resident in HBM: scene, rays, upstream gradients"""
             ctx.zero_grads()
-            order = ((vc, "c"), (vl, "l")) if CAMERA_FIRST else ((vl, "l"), (vc, "c"))
+            for f in frames:
+                t_scene = set_frame(f)
+                order = [(vl, "l")] + [(v, "c") for v in vcs]
+                if CAMERA_FIRST:
+                    order = order[1:] + order[:1]
 
-            def run_view(v, k):
-                v.forward(0.0)      # contains the one host sync of a render (the worklist size)
-                v.backward_device(g_dev[k][0].data_ptr(), g_dev[k][1].data_ptr())
-            if pool is not None and threaded[0]:    # one host thread per view: neither view's host sync delays the other's launches
-                for f in [pool.submit(run_view, v, k) for v, k in order]:
-                    f.result()
+                def run_view(v, k):
+                    v.forward(t_scene)      # contains the one host sync of a render (the worklist size)
+                    v.backward_device(g_dev[k][0].data_ptr(), g_dev[k][1].data_ptr())
+                if pool is not None and threaded[0]:    # one host thread per view: neither view's host sync delays the other's launches
+                    for fu in [pool.submit(run_view, v, k) for v, k in order]:
+                        fu.result()
+                else:
+                    for v, k in order:
+                        run_view(v, k)
+            # ONE collective per step, after the rank's last frame: splatb200_allreduce_grads orders the ctx stream after
+            # every view stream and enqueues ncclAllReduce (in place on the bound buffer) there
+            if comm_world > 1:
+                ctx.allreduce_grads()
             else:
-                for v, k in order:
-                    run_view(v, k)
-            ctx.join()      # view streams: order the ctx stream (NCCL, the timing event) after both sensors
-            sdist.allreduce_grads(grads_t)
+                ctx.join()
 
         def step_e2e():
             """the reference-facing call with HOST buffers: GaussianSet up, rendered images down, upstream
@@ -352,24 +475,35 @@ def run_b200(args):
             # (they are a function of them).
             # (lidar first measured best: its small transfers and its backward then run beside the camera's forward
             # and the camera's 149 MB download; camera first was 0.6 ms slower)
-            def run_view(name, v):
-                _, _, _, vb, va, vn = out_host[name]
-                v.forward_to_host(0.0, vb, va, vn, bands=E2E_BANDS)   # camera: bands of tile rows, each downloaded while the next renders
-                _, _, gb, ga = g_host[name]
-                v.backward_from_host(gb, ga)            # a band's gradients go up after its outputs came down
-            if pool is not None and threaded[0]:
-                for f in [pool.submit(run_view, name, v) for name, v in (("l", vl), ("c", vc))]:
-                    f.result()
-            else:
-                for name, v in (("l", vl), ("c", vc)):
-                    v.forward(0.0)
+            for f in frames:
+                t_scene = set_frame(f)
+
+                def run_view(name, v):
                     _, _, _, vb, va, vn = out_host[name]
-                    v.download_async(vb, va, vn)
-                for name, v in (("l", vl), ("c", vc)):
+                    v.forward_to_host(t_scene, vb, va, vn, bands=E2E_BANDS)   # camera: bands of tile rows, each downloaded while the next renders
                     _, _, gb, ga = g_host[name]
-                    v.backward_host_overlapped(gb, ga)
-            ctx.join()
-            sdist.allreduce_grads(grads_t)
+                    v.backward_from_host(gb, ga)            # a band's gradients go up after its outputs came down
+                views = [("l", vl)] + [("c", v) for v in vcs]
+                if pool is not None and threaded[0] and not rig:
+                    for fu in [pool.submit(run_view, name, v) for name, v in views]:
+                        fu.result()
+                elif rig:       # the six cameras share one pinned output / upstream buffer: one camera at a time
+                    run_view("l", vl)
+                    for v in vcs:
+                        run_view("c", v)
+                        ctx.sync()
+                else:
+                    for name, v in views:
+                        v.forward(t_scene)
+                        _, _, _, vb, va, vn = out_host[name]
+                        v.download_async(vb, va, vn)
+                    for name, v in views:
+                        _, _, gb, ga = g_host[name]
+                        v.backward_host_overlapped(gb, ga)
+            if comm_world > 1:
+                ctx.allreduce_grads()
+            else:
+                ctx.join()
             ctx.grads_into(*gh_parts)
             ctx.sync()
 
@@ -383,13 +517,11 @@ def run_b200(args):
             e1.record(stream)
             barrier()
             t1 = time.time()
-            ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-            return float(ms.item()), t0, t1
+            ms = sdist.max_over_ranks(e0.elapsed_time(e1), device=dev)     # a multi-GPU time is the MAX over ranks
+            return ms, t0, t1
 
         # ---- device-resident timing ------------------------------------------------------------
-        # the two sensors of a frame run on their own streams (the lidar's latency-bound binning and the tail of its
+        # the sensors of a frame run on their own streams (the lidar's latency-bound binning and the tail of its
         # compositing grid overlap the camera's kernels); --serial keeps everything on one stream
         ctx.set_view_streams(not args.serial)
         for _ in range(max(args.warmup, 0)):
@@ -399,15 +531,22 @@ def run_b200(args):
         ms_dev, t0, t1 = timed(step_device, args.steps)
         clocks = sampler.stop(t0, t1) if sampler else None
         launches, lib_launches = ctx.launch_count - l0, ctx.library_launch_count - ll0
+        # the collective alone (same buffer, same stream): what one step pays for it
+        ms_allreduce = None
+        if comm_world > 1:
+            ms_ar, _, _ = timed(ctx.allreduce_grads, 5)
+            ms_allreduce = ms_ar / 5
         # per-stage CUDA-event times: a separate, serialised pass (one stream), so that a stage's time is its own
         ctx.set_view_streams(False)
         threaded[0] = False
         ctx.set_profiling(True)
-        ms_serial, _, _ = timed(step_device, max(3, min(args.steps, 10)))
-        ms_serial /= max(3, min(args.steps, 10))
+        k_ser = max(1, min(args.steps, 10 if not rig else 2))
+        ms_serial, _, _ = timed(step_device, k_ser)
+        ms_serial /= k_ser * len(frames)
         stage_l, stage_c = vl.stage_ms(), vc.stage_ms()
         ctx.set_profiling(False)
         stats_l, stats_c = vl.stats(), vc.stats()
+        stats_cams = [v.stats() for v in vcs]
         ctx.set_view_streams(not args.serial)
         threaded[0] = True
 
@@ -422,24 +561,29 @@ def run_b200(args):
         ms_c, _, _ = timed(only(vc, g_dev["c"]), k_br)
 
         # ---- end to end through the host-buffer API -------------------------------------------
-        for _ in range(min(max(args.warmup, 1), 3)):
+        for _ in range(min(max(args.warmup, 1), 3) if not rig else 1):
             step_e2e()
-        ms_e2e, _, _ = timed(step_e2e, args.steps)
+        k_e2e = args.steps if not rig else max(1, min(args.steps, 3))
+        ms_e2e, _, _ = timed(step_e2e, k_e2e)
+        ms_e2e /= k_e2e
         checksum = float(np.abs(gh[:1024]).sum())   # the downloaded result is really there
+        peak_mem = torch.cuda.mem_get_info(dev)
 
     if world > 1:
         dist.barrier()
     if rank != 0:
         if world > 1:
+            ctx.comm_destroy()
             dist.destroy_process_group()
         return 0
 
-    queries = (P_l + P_c) * world
+    n_cam = len(vcs)
+    queries = (P_l + n_cam * P_c) * len(frames) * world
     per_step = ms_dev / args.steps
     value = queries / (per_step * 1e-3) / 1e6
-    e2e_value = queries / (ms_e2e / args.steps * 1e-3) / 1e6
-    h2d = 112 * N_GAUSS + 68 * (P_l + P_c)
-    d2h = 72 * (P_l + P_c) + 4 * n_grad
+    e2e_value = queries / (ms_e2e * 1e-3) / 1e6
+    h2d = 112 * n_gauss + 68 * (P_l + n_cam * P_c) * len(frames)
+    d2h = 72 * (P_l + n_cam * P_c) * len(frames) + 4 * n_grad
 
     # roofline of the dominant kernel
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -447,53 +591,77 @@ def run_b200(args):
         peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     else:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    cand = []
+    counters = load_counters() if not rig else {}
+    kname = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project", "project_bwd": "k_project_bwd",
+             "tile_counts": "k_tile_hist+k_tile_scan", "tile_sort": "k_radix_pass<emit>(+k_expand)", "depth_sort_scan": "k_radix_pass+k_count_scan"}
+    ckeys = {"raster_fwd": ["k_raster_fwd"], "raster_bwd": ["k_raster_bwd"], "project": ["k_project"], "project_bwd": ["k_project_bwd"],
+             "tile_counts": ["k_tile_hist", "k_tile_scan"], "tile_sort": ["k_expand"], "depth_sort_scan": ["k_radix_hist", "k_radix_pass", "k_count_scan"]}
+    cand, per_kernel = [], {}
     for sensor, stg, sts, camera in (("lidar", stage_l, stats_l, False), ("camera", stage_c, stats_c, True)):
         by = stage_bytes(sts, camera)
         for k, ms in stg.items():
             cand.append((ms, sensor, k, by[k]))
+            cs = [counters.get(f"{b}<{sensor}>") for b in ckeys[k]]
+            cs = [c for c in cs if c]
+            dram = sum(c["dram_bytes"] for c in cs) if cs else None
+            e = {"ms": ms, "algorithmic_bytes": by[k], "frac": by[k] / (ms * 1e-3) / 1e9 / peak if ms > 0 else None,
+                 "dram_bytes": dram, "dram_frac": dram / (ms * 1e-3) / 1e9 / peak if (dram and ms > 0) else None}
+            if len(cs) == 1:
+                e.update({"issue_frac": cs[0]["issue_active_pct"] / 100.0 if cs[0].get("issue_active_pct") is not None else None,
+                          "sm_throughput_frac": cs[0]["sm_throughput_pct"] / 100.0 if cs[0].get("sm_throughput_pct") is not None else None,
+                          "warps_active_frac": cs[0]["warps_active_pct"] / 100.0 if cs[0].get("warps_active_pct") is not None else None})
+            per_kernel[f"{kname[k]}<{sensor}>"] = e
     cand.sort(reverse=True)
     ms_k, sensor_k, stage_k, bytes_k = cand[0]
-    kernel_name = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project", "project_bwd": "k_project_bwd",
-                   "tile_counts": "k_tile_hist+k_tile_scan", "tile_sort": "k_radix_pass",
-                   "depth_sort_scan": "k_radix_pass+k_count_scan"}[stage_k] + ("<camera>" if sensor_k == "camera" else "<lidar>")
+    kernel_name = kname[stage_k] + f"<{sensor_k}>"
+    dom = per_kernel[kernel_name]
     achieved = bytes_k / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")   # per-launch dram bytes from the committed ncu --set full capture
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(kernel_name)
-        except Exception:
-            traffic = None
-    stage_total = sum(stage_l.values()) + sum(stage_c.values())
-    frame_bytes = sum(stage_bytes(stats_l, False).values()) + sum(stage_bytes(stats_c, True).values())
+    stage_total = sum(stage_l.values()) + n_cam * sum(stage_c.values())
+    bytes_l, bytes_c = sum(stage_bytes(stats_l, False).values()), sum(sum(stage_bytes(s_, True).values()) for s_ in stats_cams)
+    frame_bytes = bytes_l + bytes_c
+    compositing = stage_k in ("raster_fwd", "raster_bwd")
     roofline = {
-        "bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+        # what bounds the dominant kernel: the compositing kernels stage L2-resident records through shared memory and
+        # spend ~120 flop per algorithmic byte: issue slots / latency, not HBM
+        "bound": "issue" if compositing else "hbm",
+        "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "frac_kind": "ALGORITHMIC bytes (SURVEY 8(d): every input read once, every output written once) / CUDA-event kernel time / measured HBM peak",
+        "traffic": dom["dram_bytes"], "dram_frac": dom["dram_frac"], "issue_frac": dom.get("issue_frac"),
+        "sm_throughput_frac": dom.get("sm_throughput_frac"), "warps_active_frac": dom.get("warps_active_frac"),
+        "counters_source": "profiles/counters.json (ncu --set full of this command with --serial; dram_frac = its DRAM bytes / the LIVE kernel time / peak)" if counters else None,
+        "peak_source": peak_src,
         "kernel_ms": ms_k, "kernel_bytes": bytes_k, "kernel_share_of_step": ms_k / stage_total if stage_total else None,
-        "frame_algorithmic_bytes": frame_bytes, "frame_frac": frame_bytes / (per_step * 1e-3) / 1e9 / peak,
+        "per_sensor": {"lidar": {"ms_fwd_bwd": ms_l / k_br, "algorithmic_bytes": bytes_l, "frac": bytes_l / (ms_l / k_br * 1e-3) / 1e9 / peak},
+                       "camera": {"ms_fwd_bwd": ms_c / k_br, "algorithmic_bytes": bytes_c / n_cam, "frac": bytes_c / n_cam / (ms_c / k_br * 1e-3) / 1e9 / peak}},
+        "per_kernel": per_kernel,
+        "frame_algorithmic_bytes": frame_bytes, "frame_frac": frame_bytes * len(frames) / (per_step * 1e-3) / 1e9 / peak,
         "stage_ms": {"lidar": stage_l, "camera": stage_c},
         "stage_ms_note": "per-stage CUDA-event times from a serialised pass (one stream, %.3f ms per frame); the timed "
-                         "region runs the two sensors on their own streams" % ms_serial if not args.serial else "single stream",
-        "note": "compositing is fp32-issue bound (~120 flop/B, SURVEY.md §8(d)), so its HBM fraction is low by construction; "
-                "frame_frac = algorithmic bytes of the whole frame / step time / peak",
+                         "region runs the sensors on their own streams" % ms_serial if not args.serial else "single stream",
+        "note": "frac is the contract's number (algorithmic bytes over the HBM peak); dram_frac is the DRAM traffic ncu measured for "
+                "the same kernel over the live kernel time; issue_frac is the share of issue slots used. Compositing is "
+                "issue / latency bound (records are L2-resident, ~120 flop per algorithmic byte), so dram_frac is small by construction",
     }
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": METRIC if not rig else "lidar Mrays/s + camera MPix/s, fwd+bwd (config %s: 3M dynamic Gaussians, 6 cameras + lidar-128 per frame)" % config[3:],
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": workload_config(world),
+        "data": "synthetic", "config": workload_config(world, config, len(frames)),
         "breakdown": {"lidar_mrays_s": P_l / (ms_l / k_br * 1e-3) / 1e6, "camera_mpix_s": P_c / (ms_c / k_br * 1e-3) / 1e6,
-                      "lidar_ms": ms_l / k_br, "camera_ms": ms_c / k_br,
-                      "lidar": stats_l, "camera": stats_c},
+                      "lidar_ms": ms_l / k_br, "camera_ms": ms_c / k_br, "ms_per_frame": per_step / len(frames),
+                      "allreduce_ms": ms_allreduce, "allreduce_bytes": 4 * n_grad if comm_world > 1 else 0,
+                      "collective": "splatb200_allreduce_grads (ncclAllReduce, library communicator)" if comm_world > 1 else None,
+                      "lidar": stats_l, "camera": stats_c, "cameras_intersections": [s_["n_intersections"] for s_ in stats_cams],
+                      "device_memory_used_gb": (peak_mem[1] - peak_mem[0]) / 1e9},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": ms_e2e / args.steps, "result_checksum": checksum},
+                "ms_per_step": ms_e2e, "result_checksum": checksum},
         "gpu_launches": launches, "library_launches": lib_launches,
         "roofline": roofline,
     }
 
-    if world == 1 and not args.no_cpu:
+    if world == 1 and not args.no_cpu and not rig:
         fr = CpuFrame(scene, quarter=False)
         tl, tc = fr.step()
         line["cpu_baseline"] = {"value": (fr.P_l + fr.P_c) / (tl + tc) / 1e6, "unit": UNIT, "cores": fr.workers, "kind": "port",
@@ -501,6 +669,7 @@ def run_b200(args):
                                 "camera_mpix_s": fr.P_c / tc / 1e6, "seconds": tl + tc}
     print(json.dumps(line), flush=True)
     if world > 1:
+        ctx.comm_destroy()
         dist.destroy_process_group()
     return 0
 
@@ -511,12 +680,21 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="northstar", choices=["northstar", "cfg4", "cfg5"],
+                    help="northstar: 1M Gaussians, lidar-128 + one 1080p camera per frame (the headline); cfg4 / cfg5: BASELINE configs 4 / 5")
+    ap.add_argument("--frames-per-rank", type=int, default=0, help="frames a rank renders per step (default 1; cfg5: 8)")
     ap.add_argument("--ref-sample", default="auto", choices=["auto", "full", "quarter"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--serial", action="store_true", help="one stream for both sensors (default: one stream per sensor view)")
+    ap.add_argument("--dry-launch", action="store_true", help="start the ranks and rendezvous only (works without GPUs)")
+    ap.add_argument("--nccl-log", default="", help="write NCCL_DEBUG=INFO output to this path (.host.pid appended)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)         # N ranks of this very command, one per GPU
+    if args.dry_launch:
+        return run_dry_launch(args)
     return run_b200(args)
 
 

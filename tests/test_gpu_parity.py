@@ -44,13 +44,42 @@ def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
 
-def assert_projection_bit_exact(gv, ov):
+def assert_projection_bit_exact(gv, ov, sc=None):
     assert np.array_equal(gv.array("source_index"), ov.array("source_index"))
     for f in PROJ_FIELDS:
         a, b = gv.array(f), ov.array(f)
         assert a.shape == b.shape, f
         same = bits(a) == bits(b)
         assert same.all(), f"{f}: {np.count_nonzero(~same)} of {same.size} values differ bitwise (max abs {np.abs(a - b).max()})"
+    assert_packed_record_bit_exact(gv, ov, sc)
+
+
+def assert_packed_record_bit_exact(gv, ov, sc=None):
+    """The record k_project STORED in HBM for the compositing kernels (geomA | geomB | geomC | 16 channel slots), read
+    back as it lies — not the twin kernel's recomputation — against the oracle's make_splat (splat_oracle.hpp), in fp32
+    arithmetic: b2 = conic01 + conic10, rho = det_ratio * opacity."""
+    rec = gv.array("packed_record").reshape(-1, 26)
+    src = ov.array("source_index")
+    assert len(rec) == len(src)
+    f32 = np.float32
+    m, vel, con = ov.array("mean2d").reshape(-1, 2), ov.array("velocity").reshape(-1, 3), ov.array("conic").reshape(-1, 4)
+    dr, dk, op_ = ov.array("det_ratio"), ov.array("depth_key"), ov.array("opacity")[src]
+    want = np.zeros((len(src), 10), f32)
+    want[:, 0:2], want[:, 2:4] = m, vel[:, :2]
+    want[:, 4], want[:, 5], want[:, 6] = con[:, 0], (con[:, 1].astype(f32) + con[:, 2].astype(f32)), con[:, 3]
+    want[:, 7] = dr.astype(f32) * op_.astype(f32)
+    want[:, 8], want[:, 9] = dk, vel[:, 2]
+    same = bits(rec[:, :10]) == bits(want)
+    assert same.all(), f"packed record: {np.count_nonzero(~same)} geometry values differ bitwise (columns {np.unique(np.nonzero(~same)[1])})"
+    if sc is not None:      # channel slots: camera rgb + features, lidar features, zero padded
+        camera = gv.camera
+        ch = np.zeros((len(src), 16), f32)
+        o = 0
+        if camera:
+            ch[:, :3] = sc.color[src]
+            o = 3
+        ch[:, o:o + sc.d_f] = sc.feature[src]
+        assert np.array_equal(bits(rec[:, 10:]), bits(ch)), "packed record: channel slots differ"
 
 
 def assert_worklist_bit_exact(gv, ov):
@@ -71,40 +100,21 @@ def assert_render_close(gv, ov, lidar):
     assert np.abs(gv.array("t_final") - ov.array("t_final")).max() <= RENDER_RTOL
 
 
-def grads_close(g, og64, og32=None, rtol=GRAD_RTOL, what=""):
-    """Gradient parity gate. Per Gaussian (row) the error against the fp64 oracle must be <= rtol of that
-    row's magnitude. fp32 arithmetic cannot meet that on the ill-conditioned grazing Gaussians of the
-    synthetic scenes (camera depth ~ near plane => |mean2d| ~ 1e5 px, cov2d ~ 1e10 px^2: the reference's own
-    fp32 mode is off by up to 20% there). So: (a) at least 94% of the rows meet the
-    bar, (b) no more rows miss it than in the reference's own fp32 mode (x1.5), (c) every row that misses it
-    is one where the reference's fp32 mode is visibly ill-conditioned too, and stays within 20x its error."""
-    for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_color", "d_feature"):
-        a = np.asarray(g[k], np.float64)
-        n = a.shape[0]
-        a = a.reshape(n, -1)
-        b = np.asarray(og64[k], np.float64).reshape(n, -1)
-        scale = np.abs(b).max() if b.size else 0.0
-        if scale == 0:
-            assert np.abs(a).max(initial=0.0) == 0, k
-            continue
-        rowscale = np.maximum(np.abs(b).max(1), 1e-3 * scale)
-        e_gpu = np.abs(a - b).max(1) / rowscale
-        if og32 is None:
-            assert e_gpu.max() <= rtol, f"{what}{k}: {e_gpu.max():.3e}"
-            continue
-        r = np.asarray(og32[k], np.float64).reshape(n, -1)
-        e_ref = np.abs(r - b).max(1) / rowscale
-        live = np.abs(b).max(1) > 0
-        bad_gpu, bad_ref = e_gpu > rtol, e_ref > rtol
-        msg = (f"{what}{k}: rows beyond {rtol}: gpu {bad_gpu.sum()} / ref-fp32 {bad_ref.sum()} of {live.sum()}; "
-               f"worst gpu {e_gpu.max():.2e} ref {e_ref.max():.2e}; median gpu {np.median(e_gpu[live]):.1e}")
-        # (a) the bulk meets the bar
-        assert bad_gpu.sum() <= 0.06 * live.sum() + 2, msg
-        # (b) the GPU path is no less accurate than the reference's own fp32 mode
-        assert bad_gpu.sum() <= 1.5 * bad_ref.sum() + 3, msg
-        # (c) every offender is a row on which the reference's fp32 mode shows the same ill-conditioning
-        assert np.all(e_ref[bad_gpu] > 0.05 * rtol), msg
-        assert np.all(e_gpu[bad_gpu] <= 20 * e_ref[bad_gpu] + rtol), msg
+def grads_gate(ctx, og, sensor, n, what="", **kw):
+    """tests/grad_gate.py: G1 (100 % of the rows within 1e-3 of the reference algorithm in fp32, minus the rows an input
+    rule marks ill-conditioned) and G2 (vs fp64 on the rows without an fp32/fp64 forward flip)."""
+    import grad_gate
+    (g32, v32), (g64, v64) = og
+    return grad_gate.grad_gate(ctx.grads(), g32, g64, v32, v64, sensor, n, what=what, **kw)
+
+
+def assert_sensor_grads(gv, og):
+    """SensorGrads (projection.hpp:207-222): all seven entries against the reference algorithm in fp32 (same forward
+    bits) at 1e-3, and against fp64 at 5e-3 of the largest entry."""
+    (_, v32), (_, v64) = og
+    sg, s32, s64 = gv.sensor_grads().astype(np.float64), v32.array("sensor_grads").astype(np.float64), v64.array("sensor_grads")
+    assert np.abs(sg - s32).max() <= GRAD_RTOL * np.abs(s32).max(), (sg, s32)
+    assert np.abs(sg - s64).max() <= 5 * GRAD_RTOL * np.abs(s64).max(), (sg, s64)
 
 
 def oracle_grads(op, sc, render, gb, ga):
@@ -125,7 +135,7 @@ def test_config1_lidar32_forward(ctx, op):
     ctx.upload_scene(sc)
     gv = ctx.render_lidar(lid, rays, ST)
     ov = op.OracleScene(sc, np.float32).render_lidar(lid, rays, ST, workers=8)
-    assert_projection_bit_exact(gv, ov)
+    assert_projection_bit_exact(gv, ov, sc)
     assert_worklist_bit_exact(gv, ov)
     assert_render_close(gv, ov, True)
     st = gv.stats()
@@ -159,12 +169,11 @@ def test_lidar_forward_backward(ctx, op, n, seed):
     assert_render_close(gv, ov, True)
     gb, ga = synth.upstream(gv.P, seed=seed)
     gb[:, 14:] = 0
-    (g32, _), (g64, ov64) = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rays, ST, workers=8), gb, ga)
+    og = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rays, ST, workers=8), gb, ga)
     ctx.zero_grads()
     gv.backward(gb, ga)
-    grads_close(ctx.grads(), g64, g32, what="lidar ")
-    sg, osg = gv.sensor_grads(), ov64.array("sensor_grads")
-    assert np.abs(sg[:6] - osg[:6]).max() <= 5 * GRAD_RTOL * np.abs(osg[:6]).max()
+    grads_gate(ctx, og, lid, n, what="lidar ")
+    assert_sensor_grads(gv, og)
 
 
 @pytest.mark.parametrize("w,h,n,seed", [(320, 192, 4000, 4), (640, 360, 30000, 5), (100, 70, 800, 6)])
@@ -178,10 +187,11 @@ def test_camera_forward_backward(ctx, op, w, h, n, seed):
     assert_worklist_bit_exact(gv, ov)
     assert_render_close(gv, ov, False)
     gb, ga = synth.upstream(gv.P, seed=seed)
-    (g32, ov32), (g64, ov64) = oracle_grads(op, sc, lambda o: o.render_camera(cam, ST, workers=8), gb, ga)
+    og = oracle_grads(op, sc, lambda o: o.render_camera(cam, ST, workers=8), gb, ga)
+    (g32, ov32), (g64, ov64) = og
     ctx.zero_grads()
     gv.backward(gb, ga)
-    grads_close(ctx.grads(), g64, g32, what="camera ")
+    grads_gate(ctx, og, cam, n, what="camera ")
     # SensorGrads are sums over all Gaussians, dominated by the ill-conditioned grazing ones: the bar is the
     # fp32 reference's own distance from the fp64 result
     sg, osg, osg32 = gv.sensor_grads(), ov64.array("sensor_grads"), ov32.array("sensor_grads")
@@ -221,11 +231,12 @@ def test_dynamic_scene_actors(ctx, op):
     dyn = np.isin(gv.array("source_index"), np.nonzero(sc.actor_id)[0]).sum()
     assert dyn > 100
     gb, ga = synth.upstream(gv.P, seed=7)
-    (g32, _), (og, _) = oracle_grads(op, sc, lambda o: o.render_camera(cam, ST, t_scene=t_scene, workers=8), gb, ga)
+    ogs = oracle_grads(op, sc, lambda o: o.render_camera(cam, ST, t_scene=t_scene, workers=8), gb, ga)
+    (g32, _), (og, _) = ogs
     ctx.zero_grads()
     gv.backward(gb, ga)
     g = ctx.grads()
-    grads_close(g, og, g32, what="dynamic ")
+    grads_gate(ctx, ogs, cam, sc.n, what="dynamic ")
     for a in range(4):
         for k in ("d_pose_offset", "d_vel_offset"):
             x, y = g["actors"][a][k], og["actors"][a][k].reshape(g["actors"][a][k].shape)
@@ -247,7 +258,7 @@ def _golden_names():
 
 
 @pytest.mark.parametrize("name", _golden_names())
-def test_cuda_path_matches_reference_golden(ctx, name):
+def test_cuda_path_matches_reference_golden(ctx, op, name):
     """The sm_100a path against outputs of the reference's OWN code (unmodified headers compiled against the Eigen
     shim; tests/golden/ref_*.npz): fp32 kernels vs the reference's fp64 instantiation, so tolerances, not bits."""
     import golden_util as gu
@@ -276,12 +287,25 @@ def test_cuda_path_matches_reference_golden(ctx, name):
     ctx.zero_grads()
     gv.backward(gb, ga)
     g = ctx.grads()
+    # the gate's G2 (tests/grad_gate.py) against the REFERENCE's values: rows no fp32/fp64 forward flip touches and the
+    # input rule does not mark: 100 % within 5e-2, at most 10 % beyond 1e-3, group-level relative L2 <= 1e-3
+    import grad_gate
+    rays = None if camera else synth.grid_rays(sensor)
+    ovs = [(op.OracleScene(sc, dt).render_camera(sensor, st, t_scene=t, workers=8) if camera else
+            op.OracleScene(sc, dt).render_lidar(sensor, rays, st, t_scene=t, workers=8)) for dt in (np.float32, np.float64)]
+    n_flips, fm = grad_gate.flip_mask(ovs[0], ovs[1])
+    ok = ~(fm | grad_gate.ill_conditioned(ovs[1], sensor, sc.n))
     for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit"):
         a = g[k].reshape(sc.n, -1).astype(np.float64)
         b = z["ref_" + k].reshape(sc.n, -1)
         rowscale = np.maximum(np.abs(b).max(1), 1e-3 * np.abs(b).max())
         err = np.abs(a - b).max(1) / rowscale
-        assert np.quantile(err, 0.95) <= GRAD_RTOL, (k, np.quantile(err, 0.95))
+        u = ok & (np.abs(b).max(1) > 0)
+        msg = (f"{name} {k}: rows checked {u.sum()} of {(np.abs(b).max(1) > 0).sum()} live ({n_flips} flipped queries), beyond 1e-3: "
+               f"{(err[u] > GRAD_RTOL).sum()}, worst {err[u].max(initial=0.0):.1e}")
+        print(msg)
+        assert err[u].max(initial=0.0) <= 5e-2 and (err[u] > GRAD_RTOL).sum() <= 0.10 * u.sum() + 1, msg
+        assert np.linalg.norm((a - b)[ok]) <= 1e-3 * np.linalg.norm(b[ok]), msg
     sg = gv.sensor_grads()[:6].astype(np.float64)
     assert np.abs(sg - z["ref_sensor_grads"][:6]).max() <= 2e-2 * np.abs(z["ref_sensor_grads"][:6]).max()
 
@@ -391,29 +415,37 @@ def test_more_than_256_rays_per_tile(ctx, op):
     assert_render_close(gv, ov, True)
     gb, ga = synth.upstream(gv.P, seed=3)
     gb[:, 14:] = 0
-    (g32, _), (g64, _) = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rs2, ST, workers=8), gb, ga)
+    og = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rs2, ST, workers=8), gb, ga)
     ctx.zero_grads()
     gv.backward(gb, ga)
-    grads_close(ctx.grads(), g64, g32, what="multipass ")
+    grads_gate(ctx, og, lid, sc.n, what="multipass ")
 
 
 def test_multi_sensor_accumulation_and_reuse(ctx, op):
     """Several sensors over one scene accumulate into one SceneParamGrads; views are reusable across frames."""
+    import grad_gate
     sc = synth.make_scene(5000, seed=14, r_max=40.0, scale_mean=0.1)
     ctx.upload_scene(sc)
     o64, o32 = op.OracleScene(sc, np.float64), op.OracleScene(sc, np.float32)
     cams = [synth.make_camera(width=160, height=96, yaw=k * np.pi / 3) for k in range(3)]
     view = ctx.camera_view(cams[0], ST)
     ctx.zero_grads()
+    fm, ill = np.zeros(sc.n, bool), np.zeros(sc.n, bool)
     for k, cam in enumerate(cams):
         view.set_camera(cam)
         view.forward(0.0)
         gb, ga = synth.upstream(view.P, seed=20 + k)
         view.backward(gb, ga)
+        vs = []
         for o in (o32, o64):
             ov = o.render_camera(cam, ST, workers=8)
             ov.backward(gb, ga, workers=8)
-    grads_close(ctx.grads(), o64.grads(), o32.grads(), what="multi-sensor ")
+            vs.append(ov)
+        if k < len(cams) - 1:       # masks of the earlier sensors (the gate adds the last one's itself)
+            fm |= grad_gate.flip_mask(vs[0], vs[1])[1]
+            ill |= grad_gate.ill_conditioned(vs[1], cam, sc.n)
+    grad_gate.grad_gate(ctx.grads(), o32.grads(), o64.grads(), vs[0], vs[1], cams[-1], sc.n, what="multi-sensor ",
+                        extra_mask=(fm, ill))
 
 
 # ---- BASELINE.json full sizes ------------------------------------------------------------------------
@@ -483,6 +515,103 @@ def test_full_size_1m_gaussians(ctx, op, sensor):
         assert np.quantile(rel, 0.99) <= 1e-3 and np.isfinite(x).all(), (k, np.quantile(rel, 0.99))
 
 
+# ---- gradient parity at the BASELINE sizes --------------------------------------------------
+@pytest.mark.parametrize("near_plane", [None, 1.0])
+def test_cfg2_camera_100k_forward_backward(ctx, op, near_plane):
+    """BASELINE config 2: 100k Gaussians, 1920x1080 rolling-shutter camera, forward + backward, against the oracle at
+    full size: projection, stored records, worklist and contributor counts bit-exact, render <= 1e-4, SceneParamGrads
+    through the gradient gate. near_plane = None is synth-v1 as specified: ~2 % of the visible Gaussians lie at grazing
+    depth and cover every tile (no tan-FOV clamp in the reference), so most pixels see an fp32/fp64 forward flip and G2
+    has few rows left — G1 (100 % of the rows against the reference algorithm in fp32) carries that case. With
+    near_plane = 1 m (the same code path; the grazing Gaussians are culled by the reference's own rule,
+    projection.hpp:99) G2 covers >= 90 % of the live rows."""
+    import dataclasses
+    st = ST if near_plane is None else dataclasses.replace(ST, near_plane=near_plane)
+    n = 100_000
+    sc = synth.make_scene(n, seed=3)
+    cam = synth.make_camera()
+    ctx.upload_scene(sc)
+    gv = ctx.render_camera(cam, st)
+    W = op.hardware_threads()
+    ov = op.OracleScene(sc, np.float32).render_camera(cam, st, workers=W)
+    assert_projection_bit_exact(gv, ov, sc)
+    assert_worklist_bit_exact(gv, ov)
+    assert_render_close(gv, ov, False)
+    gb, ga = synth.upstream(gv.P, seed=1)
+    og = oracle_grads(op, sc, lambda o: o.render_camera(cam, st, workers=W), gb, ga)
+    ctx.zero_grads()
+    gv.backward(gb, ga)
+    grads_gate(ctx, og, cam, n, what=f"cfg2 near_plane={near_plane} ", workers=W, max_ill_frac=0.03,
+               max_flip_frac=None if near_plane is None else 0.10)
+    if near_plane is not None:
+        assert_sensor_grads(gv, og)
+
+
+def test_cfg3_lidar128_1m_forward_backward(ctx, op):
+    """BASELINE config 3: 1M Gaussians, 128-beam lidar with non-uniform elevation and rolling shutter, forward + backward
+    incl. the feature channels standing in for intensity and ray-drop: SceneParamGrads and SensorGrads of the full-size
+    sweep against the oracle (the worklist / contributor counts of this configuration are in
+    test_full_size_1m_gaussians)."""
+    n = 1_000_000
+    sc = synth.make_scene(n, seed=3)
+    lid = synth.lidar128()
+    rays = synth.grid_rays(lid)
+    ctx.upload_scene(sc)
+    gv = ctx.render_lidar(lid, rays, ST)
+    gb, ga = synth.upstream(gv.P, seed=1)
+    gb[:, 14:] = 0
+    W = op.hardware_threads()
+    og = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rays, ST, workers=W), gb, ga)
+    assert np.array_equal(gv.array("n_contrib"), og[0][1].array("n_contrib"))
+    ctx.zero_grads()
+    gv.backward(gb, ga)
+    grads_gate(ctx, og, lid, n, what="cfg3 ", workers=W, max_flip_frac=0.05)
+    assert_sensor_grads(gv, og)
+
+
+def test_cfg4_dynamic_3m_cropped_sensors_match_oracle(ctx, op):
+    """BASELINE config 4's scene (3M Gaussians, 32 moving actors) against the oracle on sensors small enough for the CPU:
+    a 480 x 270 camera of the rig (same field of view) and the 32-beam lidar. Everything the small dynamic test checks,
+    at 3M: composed fields, projection, stored records, worklists and contributor counts bit-exact; render <= 1e-4;
+    SceneParamGrads through the gate; actor pose / velocity offset gradients."""
+    n = 3_000_000
+    sc = synth.make_scene(n, seed=4, n_actors=32, dynamic_fraction=0.02)
+    t_scene = 0.05
+    ctx.upload_scene(sc)
+    W = op.hardware_threads()
+    cam = synth.make_camera(width=480, height=270, yaw=np.pi / 3.0)
+    lid = synth.lidar32()
+    lid.vel_lin, lid.vel_ang = np.array([12.0, 1.0, 0.0]), np.array([0.0, 0.02, 0.3])
+    rays = synth.grid_rays(lid)
+    for name, sensor in (("camera", cam), ("lidar", lid)):
+        camera = name == "camera"
+        gv = ctx.render_camera(cam, ST, t_scene=t_scene) if camera else ctx.render_lidar(lid, rays, ST, t_scene=t_scene)
+        render = (lambda o: o.render_camera(cam, ST, t_scene=t_scene, workers=W)) if camera else \
+                 (lambda o: o.render_lidar(lid, rays, ST, t_scene=t_scene, workers=W))
+        gb, ga = synth.upstream(gv.P, seed=7)
+        if not camera:
+            gb[:, 14:] = 0
+        og = oracle_grads(op, sc, render, gb, ga)
+        ov = og[0][1]
+        if camera:
+            for f in ("mean_w", "vel_dyn_w", "opacity", "cov_w"):
+                assert np.array_equal(bits(gv.array(f)), bits(ov.array(f))), f
+        assert_projection_bit_exact(gv, ov, sc)
+        assert_worklist_bit_exact(gv, ov)
+        assert_render_close(gv, ov, not camera)
+        dyn = np.isin(gv.array("source_index"), np.nonzero(sc.actor_id)[0]).sum()
+        assert dyn > 100, dyn
+        ctx.zero_grads()
+        gv.backward(gb, ga)
+        grads_gate(ctx, og, sensor, n, what=f"cfg4 {name} ", workers=W, max_ill_frac=0.03, max_flip_frac=None if camera else 0.05)
+        g, (g32, _), (g64, _) = ctx.grads(), og[0], og[1]
+        for a in range(len(sc.tracks)):
+            for k in ("d_pose_offset", "d_vel_offset"):
+                x, r, y = g["actors"][a][k], g32["actors"][a][k].reshape(g["actors"][a][k].shape), g64["actors"][a][k].reshape(g["actors"][a][k].shape)
+                assert np.abs(x - y).max() <= 2e-3 * max(np.abs(y).max(), 1e-6) + 5 * np.abs(r - y).max(), (name, a, k)
+        del gv, og, ov
+
+
 @pytest.mark.parametrize("scale_mean,speed", [(0.01, 30.0), (0.3, 60.0), (1.5, 5.0)])
 def test_per_warp_culling_is_sound(ctx, op, scale_mean, speed):
     """The compositing kernels drop (Gaussian, patch) pairs with a conservative bound before evaluating them
@@ -512,10 +641,10 @@ def test_per_warp_culling_is_sound(ctx, op, scale_mean, speed):
         return
     gb, ga = synth.upstream(gl.P, seed=9)
     gb[:, 14:] = 0
-    (g32, _), (g64, _) = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rays, ST, workers=8), gb, ga)
+    og = oracle_grads(op, sc, lambda o: o.render_lidar(lid, rays, ST, workers=8), gb, ga)
     ctx.zero_grads()
     gl.backward(gb, ga)
-    grads_close(ctx.grads(), g64, g32, what=f"cull lidar s={scale_mean} ")
+    grads_gate(ctx, og, lid, sc.n, what=f"cull lidar s={scale_mean} ")
 
 
 # ---- binning variants --------------------------------------------------------------------------------
@@ -571,12 +700,11 @@ def test_backward_is_repeatable_after_new_forward(ctx, op):
         o64.zero_grads()
         ov = o64.render_camera(cam2, ST, workers=8)
         ov.backward(gb, ga, workers=8)
-        assert np.array_equal(view.array("n_contrib"), op.OracleScene(sc, np.float32).render_camera(cam2, ST, workers=8).array("n_contrib"))
-        g, og = ctx.grads(), o64.grads()
-        for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_color", "d_feature"):
-            a, b = g[k].reshape(sc.n, -1).astype(np.float64), og[k].reshape(sc.n, -1)
-            rel = np.abs(a - b).max(1) / np.maximum(np.abs(b).max(1), 1e-3 * np.abs(b).max())
-            assert np.quantile(rel, 0.97) <= GRAD_RTOL, (yaw, k, np.quantile(rel, 0.97))
+        o32 = op.OracleScene(sc, np.float32)
+        ov32 = o32.render_camera(cam2, ST, workers=8)
+        ov32.backward(gb, ga, workers=8)
+        assert np.array_equal(view.array("n_contrib"), ov32.array("n_contrib"))
+        grads_gate(ctx, [(o32.grads(), ov32), (o64.grads(), ov)], cam2, sc.n, what=f"yaw {yaw} ")
 
 
 def test_config4_scale_dynamic_3m(ctx):
@@ -855,13 +983,15 @@ def test_line_of_sight_channel(ctx, op):
     ctx.zero_grads()
     view.set_los_grad(g_los)
     view.backward(zb, za)
+    ovs = []
     for o in (o32, o64):
         o.zero_grads()
         ov = o.render_lidar(lid, rs, ST, workers=8)
         ov.set_los(cut, workers=8)
         ov.set_los_grad(g_los)
         ov.backward(zb, za, workers=8)
-    grads_close(ctx.grads(), o64.grads(), o32.grads(), what="los ")
+        ovs.append(ov)
+    grads_gate(ctx, [(o32.grads(), ovs[0]), (o64.grads(), ovs[1])], lid, sc.n, what="los ")
     assert np.abs(ctx.grads()["d_opacity_logit"]).max() > 0
     # off again: no accumulator, no gradient from it
     view.set_los(None)
