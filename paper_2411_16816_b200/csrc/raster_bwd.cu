@@ -318,16 +318,30 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     const int max_last = s_max_last;
     int n_slots = 0;  // parked entries (warp-uniform); the panel persists across batches
 
+    // hit byte and list entry of a batch are fetched one batch ahead and its records prefetched into L2: a batch's staging
+    // then starts with the record loads instead of a chain of three dependent global loads
+    uint32_t mask_next = 0u, src_next = 0u;
+    if (max_last > 0) {
+      const int b0 = ((max_last - 1) / kBatch) * kBatch;
+      if (b0 + tid < max_last) {
+        mask_next = fwd.hit[lb + b0 + tid];
+        src_next = vals[lb + b0 + tid];
+      }
+    }
     for (int batch = (max_last - 1) / kBatch; batch >= 0 && max_last > 0; --batch) {
       const int bstart = batch * kBatch;
       const int cnt = min(kBatch, max_last - bstart);
       // the forward pass saved, per list entry, which warps blended it: only those entries are staged and revisited
       {
-        uint32_t mask = 0u;
+        const uint32_t mask = mask_next;
+        const uint32_t src = src_next;
+        mask_next = 0u;
+        if (batch > 0) {  // the batch in front of this one is always full
+          mask_next = fwd.hit[lb + bstart - kBatch + tid];
+          src_next = vals[lb + bstart - kBatch + tid];  // unconditional: two independent loads, no wait on the hit byte here
+        }
         if (tid < cnt) {
-          mask = fwd.hit[lb + bstart + tid];
           if (mask) {
-            const uint32_t src = vals[lb + bstart + tid];
             sSrc[tid] = src;
             sA[tid] = p.geomA[src];
             sB[tid] = p.geomB[src];
@@ -401,6 +415,12 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           valid = has1 && (bstart + j1 < last) && alpha_finish(qf1, b1.w, dx1, dy1, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
           if ((sure && has1) || __any_sync(0xffffffffu, valid)) park(j1, valid, ev);
         }
+      }
+      if (mask_next) {  // next batch's records -> L2
+        prefetch_l2(&p.geomA[src_next]);
+        prefetch_l2(&p.geomB[src_next]);
+        prefetch_l2(&p.feat[4 * (size_t)src_next]);
+        if (!kCamera) prefetch_l2(&p.geomC[src_next]);
       }
       __syncthreads();  // every warp is done with the staged batch
     }

@@ -26,6 +26,10 @@ __device__ __forceinline__ float wrap_pi(float a) {
   return a;
 }
 
+// L2 prefetch of a record the NEXT batch will stage: turns its DRAM round trip into an L2 hit (the compositing kernels
+// are latency-bound: a batch is a chain of dependent global loads — list entry, record — in front of the compute)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 struct AlphaEval {
   float alpha, dx, dy, gauss;
   bool clamped;
@@ -220,6 +224,56 @@ __device__ __forceinline__ void warp_patch_box(bool inside, float qx, float qy, 
     if (!(b.hx2 == b.hx2 && b.hy2 == b.hy2 && b.th2 == b.th2)) b.enabled = 0;
   }
   if (lane == 0) *out = b;
+}
+
+// Bounding boxes of the warp's four 8-lane GROUPS (lanes 8g .. 8g + 7), written by the first lane of each group to
+// out[g]: the second level of the culling hierarchy (k_raster_fwd walks one list per group, see there). Same
+// construction and padding as warp_patch_box, reduced over the group only.
+template <bool kLidar>
+__device__ __forceinline__ void group_patch_box(bool inside, float qx, float qy, float t, int lane, PatchBox* out) {
+  const unsigned act = __ballot_sync(0xffffffffu, inside);
+  const int g = lane >> 3;
+  const unsigned gact = (act >> (8 * g)) & 0xffu;
+  PatchBox b;
+  b.cx = b.cy = b.tc = b.hx2 = b.hy2 = b.th2 = 0.0f;
+  b.enabled = 0;
+  b.straddle = 1;
+  // every lane takes part in the shuffles; groups without a valid lane produce a disabled box
+  const int first = gact ? 8 * g + __ffs(gact) - 1 : lane;
+  const float ref = __shfl_sync(0xffffffffu, qx, first);
+  int strad = (kLidar && inside && !(fabsf(qx - ref) < kPi - 1e-3f)) ? 1 : 0;
+  float rx = kLidar ? wrap_pi(qx - ref) : qx;
+  const float big = 3.0e38f;
+  float x0 = inside ? rx : big, x1 = inside ? rx : -big;
+  float y0 = inside ? qy : big, y1 = inside ? qy : -big;
+  float t0 = inside ? t : big, t1 = inside ? t : -big;
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+    x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o)); x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+    y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o)); y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    t0 = fminf(t0, __shfl_xor_sync(0xffffffffu, t0, o)); t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, o));
+    strad |= __shfl_xor_sync(0xffffffffu, strad, o);
+  }
+  if (gact != 0u) {
+    b.straddle = kLidar ? strad : 0;
+    b.cx = 0.5f * (x0 + x1);
+    b.cy = 0.5f * (y0 + y1);
+    b.tc = 0.5f * (t0 + t1);
+    float hx = 0.5f * (x1 - x0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(x0) + fabsf(x1)) + 1e-30f;
+    const float hy = 0.5f * (y1 - y0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(y0) + fabsf(y1)) + 1e-30f;
+    const float th = 0.5f * (t1 - t0) * (1.0f + 1e-6f) + 1e-6f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
+    b.enabled = 1;
+    if (kLidar) {
+      b.cx += ref;
+      hx += 1e-6f * (fabsf(ref) + 8.0f);
+      if (!(hx < 0.5f * kPi)) b.enabled = 0;
+    }
+    b.hx2 = hx + kSlackUlp * (fabsf(b.cx) + hx);
+    b.hy2 = hy + kSlackUlp * (fabsf(b.cy) + hy);
+    b.th2 = th + kSlackUlp * (fabsf(b.tc) + th);
+    if (!(b.hx2 == b.hx2 && b.hy2 == b.hy2 && b.th2 == b.th2)) b.enabled = 0;
+  }
+  if ((lane & 7) == 0) out[g] = b;
 }
 
 // Order-preserving compaction of the batch entries whose mask has this warp's bit. Returns the count.
