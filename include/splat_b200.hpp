@@ -25,6 +25,7 @@
 #pragma once
 
 #include <cstring>
+#include <array>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -116,6 +117,23 @@ class Context {
     if (graph_ != &graph) upload(graph);
   }
   void zero_grads() { detail::check(c_, splatb200_grads_zero(c_)); }
+
+  // ---- multi-GPU ("parallel per sensor view"; scene.hpp:351-362 SceneParamGrads::add across workers) ----
+  /// 128-byte NCCL id: rank 0 creates it, every rank receives it out of band (MPI_Bcast, a file, ...).
+  static std::array<char, 128> nccl_unique_id() {
+    std::array<char, 128> id{};
+    if (splatb200_nccl_unique_id(id.data()) != 0) throw std::runtime_error("splatb200_nccl_unique_id: NCCL is not available");
+    return id;
+  }
+  /// One rank per GPU: ncclCommInitRank over `world` ranks.
+  void comm_init(const std::array<char, 128>& id, int rank, int world) {
+    detail::check(c_, splatb200_ctx_comm_init(c_, id.data(), rank, world));
+  }
+  /// A trainer that already owns an ncclComm_t hands it over (it stays the trainer's).
+  void comm_bind(void* nccl_comm, int rank, int world) { detail::check(c_, splatb200_ctx_comm_bind(c_, nccl_comm, rank, world)); }
+  /// SceneParamGrads (and ActorGrad) summed over all ranks, in place on the device: the per-worker `add` of
+  /// scene.hpp:351-362 as ONE ncclAllReduce per step, after this rank's last backward.
+  void allreduce_grads() { detail::check(c_, splatb200_allreduce_grads(c_)); }
 
   /// SceneParamGrads += device gradients (scene.hpp:325-363), then the device buffer is zeroed, so that the
   /// reference's "accumulate into the caller's struct" contract holds call by call.

@@ -1170,6 +1170,63 @@ def test_optimizer_step_range_and_sharded_path(api, op):
     assert np.array_equal(skipq[2], np.asarray(sc.quat, np.float32)) and np.array_equal(skipq[0], full[0])
 
 
+def test_library_nccl_collective_world1(api, op):
+    """The C-ABI collective (splatb200_ctx_comm_init -> ncclCommInitRank, splatb200_allreduce_grads ->
+    ncclAllReduce on the ctx stream after a join of the view streams, splatb200_sharded_optimizer_step) on the one GPU a
+    test box has: a communicator of world size 1. The sum over one rank is the identity, so gradients (incl. the ActorGrad
+    slots) must come back bit-identical, and the sharded step must equal the plain one. (Two ranks need two GPUs: NCCL
+    refuses two ranks on one device; the two-rank host logic runs on gloo in tests/test_dist_gloo.py, and bench.py
+    --gpus N drives this very call on N GPUs.)"""
+    cfg = {"lr_init": [1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-3], "lr_final": [1.6e-6, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-4],
+           "warmup_steps": [0] * 6, "total_steps": 10}
+    sc = synth.make_scene(20_003, seed=31, n_actors=3, dynamic_fraction=0.2, r_max=30.0, scale_mean=0.1)
+    for k, tr in enumerate(sc.tracks):
+        tr.t[:] = np.array([8.0 + 3 * k, -3.0 + 2 * k, 1.0]) + np.outer(tr.stamps, [6.0, 1.0, 0.0])
+    cam = synth.make_camera(width=320, height=192)
+    import torch
+    uid = api.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    c, c2 = api.Context(0), api.Context(0)
+    try:
+        for x in (c, c2):
+            x.upload_scene(sc)
+        assert c.comm_world == 0
+        with pytest.raises(api.SplatError, match="without a communicator"):
+            c.allreduce_grads()
+        c.comm_init(uid, 0, 1)
+        assert c.comm_world == 1
+        grads_t = torch.zeros(c.grads_size, dtype=torch.float32, device="cuda")
+        c.bind_grads_device(grads_t.data_ptr(), c.grads_size)
+        c.set_view_streams(True)
+        v = c.render_camera(cam, ST, t_scene=0.03)
+        gb, ga = synth.upstream(v.P, seed=3)
+        c.zero_grads()
+        v.backward(gb, ga)
+        g0 = c.grads()
+        assert np.abs(g0["d_mean"]).max() > 0 and any(np.abs(a["d_pose_offset"]).max() > 0 for a in g0["actors"])
+        c.allreduce_grads()          # ordered after the view's stream inside the library; the sum over one rank is the identity
+        g1 = c.grads()
+        for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_color", "d_feature"):
+            assert np.array_equal(g0[k], g1[k]), k
+        for a in range(3):
+            for k in ("d_pose_offset", "d_vel_offset"):
+                assert np.array_equal(g0["actors"][a][k], g1["actors"][a][k]), (a, k)
+        # the sharded step on the communicator == the plain step on a second context fed the same gradient bits
+        g2_t = grads_t.clone()
+        c2.bind_grads_device(g2_t.data_ptr(), c2.grads_size)
+        for step in range(2):
+            assert c.sharded_optimizer_step(cfg, step) == []
+            assert c2.optimizer_step(cfg, step) == []
+        for a, b in zip(c.download_scene(), c2.download_scene()):
+            assert np.array_equal(a, b)
+        assert not np.array_equal(c.download_scene()[0], np.asarray(sc.mean, np.float32))
+        c.comm_destroy()
+        assert c.comm_world == 0
+    finally:
+        c.close()
+        c2.close()
+
+
 # ---- camera ConvDecoder (SURVEY.md §8(f) rank 3): tcgen05 / tf32 implicit-GEMM convolutions -----------------------
 # tf32 operands (10-bit mantissa, rounded to nearest) with fp32 accumulation: 2^-11 relative per operand; over five
 # layers the image agrees with the fp32 oracle to DEC_RTOL of the output scale.
