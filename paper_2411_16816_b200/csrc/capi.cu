@@ -436,8 +436,8 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->tile_ws, tile_hist_bytes(v->s.tiles_x, v->s.tiles_y)));
   CU_TRY(c, cudaMalloc(&v->d_total, sizeof(int64_t)));
   if (std::getenv("SPLATB200_STATS")) {  // debug counters of the compositing kernels (read through view_array "raster_stats")
-    CU_TRY(c, cudaMalloc(&v->out.stats, sizeof(unsigned long long) * 4));
-    CU_TRY(c, cudaMemsetAsync(v->out.stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    CU_TRY(c, cudaMalloc(&v->out.stats, sizeof(unsigned long long) * 8));
+    CU_TRY(c, cudaMemsetAsync(v->out.stats, 0, sizeof(unsigned long long) * 8, c->stream));
   }
   if (v->two_level) {
     const int sh = super_shift();
@@ -2455,14 +2455,16 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   }
   if (name == "raster_stats") {  // cumulative since view creation; zeros unless SPLATB200_STATS is set
     if (dst) {
-      unsigned long long h[4] = {0, 0, 0, 0};
+      // [0] staged entries, [1] per-warp survivors of the first-level cull, [2] group-list entries (lidar), [3] loop
+      // iterations (lidar: max over the warp's groups), [4] staged entries with a non-finite record
+      unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (v->out.stats) {
         CU_TRY(c, cudaMemcpyAsync(h, v->out.stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         CU_TRY(c, cudaStreamSynchronize(c->stream));
       }
-      for (int k = 0; k < 4; ++k) ((int64_t*)dst)[k] = (int64_t)h[k];
+      for (int k = 0; k < 8; ++k) ((int64_t*)dst)[k] = (int64_t)h[k];
     }
-    return 4;
+    return 8;
   }
   if (name == "grid") {
     if (dst) { ((int64_t*)dst)[0] = v->s.tiles_x; ((int64_t*)dst)[1] = v->s.tiles_y; }

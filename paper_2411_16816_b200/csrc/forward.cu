@@ -180,6 +180,11 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         const uint32_t src = vals[idx];
         const float4 gA = p.geomA[src], gB = p.geomB[src];
         mask = patch_mask<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min, &wrapm);
+        // SPEC.md:289 "non-finite alpha -> Gaussian skipped, counter incremented": a record with a non-finite field makes
+        // every alpha it produces non-finite (skipped by the !(qf <= qform_max) / !(alpha >= alpha_min) tests); counted per
+        // staged entry when the debug counters are on
+        if (out.stats && !(fabsf(gA.x) + fabsf(gA.y) + fabsf(gA.z) + fabsf(gA.w) + fabsf(gB.x) + fabsf(gB.y) + fabsf(gB.z) + fabsf(gB.w) < 3.0e38f))
+          atomicAdd(&out.stats[4], 1ull);
         if (mask) {
           sA[tid] = gA;
           sB[tid] = gB;

@@ -58,7 +58,7 @@ struct RasterOutDev {
   // optional fused lidar head: decode_lidar of the blended features as the compositing epilogue
   const float* head_w;   // lidar_head_params(d_f) parameters (device); null = off
   float* head_y;         // P x 2 (intensity, ray-drop probability)
-  unsigned long long* stats;  // debug (SPLATB200_STATS=1), else null: [0] staged entries, [1] per-warp survivors of the cull
+  unsigned long long* stats;  // debug (SPLATB200_STATS=1), else null: 8 counters, see view_array "raster_stats"
 };
 
 // Raw per-Gaussian sums of the compositing backward, indexed by source index; consumed (and re-zeroed)

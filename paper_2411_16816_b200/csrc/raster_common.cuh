@@ -54,7 +54,11 @@ __device__ __forceinline__ float alpha_qform(const float4 gA /* mx my vx vy */, 
 __device__ __forceinline__ bool alpha_finish(float qf, float rho, float dx, float dy, float qform_max, float alpha_clamp,
                                              float alpha_min, AlphaEval& o) {
   if (!(qf <= qform_max)) return false;
-  const float gauss = detmath::exp_bounded(__fmul_rn(-0.5f, qf));  // == detmath::exp: qf <= qform_max bounds the argument
+  // exp_bounded == detmath::exp on [-87, 88] (bit-identical, tests/test_oracle_kat.py). qf <= qform_max bounds the
+  // argument from below; a numerically non-PSD conic can make qf hugely negative, so the argument is clamped at 88 from
+  // above: there exp() is 1.65e38 (or inf beyond), rho * gauss exceeds alpha_clamp either way and the pair is blended
+  // with the clamped alpha exactly as the oracle does (tests: test_near_singular_conics)
+  const float gauss = detmath::exp_bounded(fminf(__fmul_rn(-0.5f, qf), 88.0f));
   float alpha = __fmul_rn(rho, gauss);
   const bool clamped = alpha > alpha_clamp;
   if (clamped) alpha = alpha_clamp;

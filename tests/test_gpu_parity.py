@@ -647,6 +647,45 @@ def test_per_warp_culling_is_sound(ctx, op, scale_mean, speed):
     grads_gate(ctx, og, lid, sc.n, what=f"cull lidar s={scale_mean} ")
 
 
+def test_near_singular_conics(api, op, monkeypatch):
+    """Adversarial numerics (raster_common.cuh alpha_finish): needle Gaussians (one axis 1e-4 of the others) with almost
+    no dilation give near-singular 2-D covariances, conic entries ~1e8 with cancelling terms, and quadratic forms whose
+    fp32 evaluation is noise of either sign — including hugely negative ones, outside exp_bounded's proven range unless
+    the argument is clamped. Contributor counts, last-blended positions and the blend must still follow the oracle bit for
+    bit / to 1e-4; a record with non-finite fields is counted and never blended."""
+    import dataclasses
+    monkeypatch.setenv("SPLATB200_STATS", "1")
+    st = dataclasses.replace(ST, dilation=1e-7)
+    sc = synth.make_scene(4000, seed=41, r_max=25.0, scale_mean=0.3)
+    sc.scale_log[:, 0] += 2.0
+    sc.scale_log[:, 1] -= 9.0            # needles
+    sc.opacity_logit[:] = 4.0
+    sc.mean[7] = np.array([np.inf, 0.0, 0.0], np.float32)     # a Gaussian whose record is non-finite
+    sc.mean[8] = np.array([np.nan, 2.0, 1.0], np.float32)
+    c = api.Context(0)
+    try:
+        c.upload_scene(sc)
+        cam = synth.make_camera(width=256, height=160)
+        gv = c.render_camera(cam, st)
+        ov = op.OracleScene(sc, np.float32).render_camera(cam, st, workers=8)
+        assert_worklist_bit_exact(gv, ov)
+        assert_render_close(gv, ov, False)
+        qneg = 0
+        lid = synth.lidar32()
+        rays = synth.grid_rays(lid)
+        gl = c.render_lidar(lid, rays, st)
+        ol = op.OracleScene(sc, np.float32).render_lidar(lid, rays, st, workers=8)
+        assert_worklist_bit_exact(gl, ol)
+        assert_render_close(gl, ol, True)
+        assert np.isfinite(gv.array("blend")).all() and np.isfinite(gl.array("blend")).all()
+        assert gv.array("n_contrib").max() > 3
+        src = set(gv.array("source_index").tolist()) | set(gl.array("source_index").tolist())
+        assert 7 not in src and 8 not in src        # culled by the projection (non-finite depth), never staged
+        assert gv.array("raster_stats")[4] == 0
+    finally:
+        c.close()
+
+
 # ---- binning variants --------------------------------------------------------------------------------
 def test_camera_one_level_binning_matches_two_level(api, op, monkeypatch):
     """Cameras bin in two levels (8x8-tile blocks sorted, then expanded into tile lists); SPLATB200_ONE_LEVEL selects the
