@@ -308,6 +308,12 @@ int splatb200_lidar_head_backward(splatb200_view* v, const float* weights, const
  * Call after splatb200_view_forward of a camera view. The convolutions run on the tensor cores (tcgen05, tf32 operands
  * rounded to nearest, fp32 accumulation): results agree with an fp32 evaluation to ~1e-3 relative. */
 int32_t splatb200_conv_decoder_params(void);
+/* Arithmetic of the decoder's convolutions (they run on the tf32 tensor cores). 0 (default): operands rounded to tf32,
+ * fp32 accumulation — the image agrees with an fp32 evaluation to ~3e-3 of its scale. 1: split-tf32 ("3xTF32": every
+ * convolution as three passes hi*hi + lo*hi + hi*lo accumulated in fp32) — fp32 accuracy (1e-4 against the fp32 reference
+ * evaluation, gradients within 1e-3 of an fp64 backward) at three times the convolution time. Applies to
+ * decode_image, its backward and the debug convolution hooks of this ctx. */
+int splatb200_ctx_set_decoder_precise(splatb200_ctx* ctx, int32_t on);
 int splatb200_view_decode_image(splatb200_view* v, const float* params, const float* embedding, float* image,
                                 float* device_ms);
 /* Backward of the decode ("Includes their backward passes"; gradient example SPEC.md:376). Needs the state

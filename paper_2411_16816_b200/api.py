@@ -39,6 +39,7 @@ SYMBOLS = [
     "splatb200_view_project_backward", "splatb200_view_compose_backward", "splatb200_view_backward_projected",
     "splatb200_optimizer_reset", "splatb200_nccl_unique_id", "splatb200_ctx_comm_init", "splatb200_ctx_comm_bind",
     "splatb200_ctx_comm_destroy", "splatb200_ctx_comm_info", "splatb200_allreduce_grads", "splatb200_sharded_optimizer_step",
+    "splatb200_ctx_set_decoder_precise",
 ]
 
 
@@ -166,6 +167,7 @@ def lib():
         L.splatb200_ctx_create.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
         L.splatb200_lidar_grid.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.splatb200_optimizer_reset.argtypes = [C.c_void_p]
+        L.splatb200_ctx_set_decoder_precise.argtypes = [C.c_void_p, C.c_int32]
         L.splatb200_nccl_unique_id.argtypes = [C.c_void_p]
         L.splatb200_ctx_comm_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
         L.splatb200_ctx_comm_bind.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
@@ -385,6 +387,10 @@ class Context:
         gx, gw = np.zeros_like(x), np.zeros(9248, np.float32)
         self._check(self.L.splatb200_debug_conv3x3_backward(self.h, _p(x), H, W, _p(w), int(relu_in), _p(g_y), _p(gx), _p(gw)))
         return gx, gw
+
+    def set_decoder_precise(self, on: bool):
+        """ConvDecoder convolutions in split-tf32 (three passes, fp32 accuracy) instead of plain tf32 (default)."""
+        self._check(self.L.splatb200_ctx_set_decoder_precise(self.h, int(on)))
 
     def set_view_streams(self, on: bool):
         """Views run forward / backward on their own streams (sensors overlap); see splat_b200.h."""

@@ -43,6 +43,7 @@ struct splatb200_ctx {
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
   bool view_streams = false;   // views run forward / backward on their own streams (splatb200_ctx_set_view_streams)
+  int decoder_precise = 0;     // ConvDecoder convolutions in split-tf32 (three passes: fp32 accuracy) instead of plain tf32
 
   // scene
   int64_t n = 0;
@@ -1362,6 +1363,11 @@ extern "C" int splatb200_lidar_head_backward(splatb200_view* v, const float* wei
 // ---- camera ConvDecoder -------------------------------------------------------------------
 extern "C" int32_t splatb200_conv_decoder_params(void) { return conv_decoder_params(); }
 
+extern "C" int splatb200_ctx_set_decoder_precise(splatb200_ctx* c, int32_t on) {
+  c->decoder_precise = on != 0;
+  return SPLATB200_OK;
+}
+
 extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* params, const float* embedding, float* image,
                                            float* device_ms) {
   splatb200_ctx* c = v->ctx;
@@ -1390,7 +1396,7 @@ extern "C" int splatb200_view_decode_image(splatb200_view* v, const float* param
   }
   const int launched = launch_conv_decoder(v->d_dec_params, d_emb, v->s.height, v->s.width, c->d_f, v->s.fx, v->s.fy, v->s.cx,
                                            v->s.cy, v->out.blend, /*row pitch of the blend buffer*/ 16, v->dec_act, v->d_dec_image, v->d_dec_err,
-                                           c->stream);
+                                           c->stream, c->decoder_precise);
   CHECK_LAUNCH(c, "k_conv3x3_tc");
   c->launches += launched;
   if (device_ms) CU_TRY(c, cudaEventRecord(e1, c->stream));
@@ -1435,7 +1441,7 @@ extern "C" int splatb200_view_decode_image_backward(splatb200_view* v, const flo
   }
   const int launched = launch_conv_decoder_backward(v->d_dec_params, H, W, c->d_f, v->out.blend, /*row pitch*/ 16, v->dec_act,
                                                     v->d_dec_gimage, v->dec_g, v->dec_gext, d_wt, v->d_dec_gparams,
-                                                    v->d_dec_gparams + np, g_blend, v->d_dec_err, c->stream);
+                                                    v->d_dec_gparams + np, g_blend, v->d_dec_err, c->stream, c->decoder_precise);
   CHECK_LAUNCH(c, "conv decoder backward");
   c->launches += launched;
   if (device_ms) CU_TRY(c, cudaEventRecord(e1, c->stream));
@@ -1472,7 +1478,7 @@ extern "C" int splatb200_debug_conv3x3_backward(splatb200_ctx* c, const float* x
   CU_TRY(c, cudaMemcpyAsync(dw.p, w, sizeof(float) * 9248, cudaMemcpyHostToDevice, c->stream));
   CU_TRY(c, cudaMemsetAsync(dgw.p, 0, sizeof(float) * 9248, c->stream));
   CU_TRY(c, cudaMemsetAsync(de.p, 0, sizeof(int), c->stream));
-  launch_conv3x3_backward(dx.p, H, W, dw.p, relu_in, dgy.p, dwt.p, dge.p, dgx.p, dgw.p, (int*)de.p, c->stream);
+  launch_conv3x3_backward(dx.p, H, W, dw.p, relu_in, dgy.p, dwt.p, dge.p, dgx.p, dgw.p, (int*)de.p, c->stream, c->decoder_precise);
   CHECK_LAUNCH(c, "k_conv3x3_wgrad_tc");
   c->launches += 4;
   int err = 0;
@@ -1500,7 +1506,7 @@ extern "C" int splatb200_debug_conv3x3(splatb200_ctx* c, const float* x, int32_t
   if (res) CU_TRY(c, cudaMemcpyAsync(dr.p, res, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
   CU_TRY(c, cudaMemsetAsync(de.p, 0, sizeof(int), c->stream));
   CU_TRY(c, cudaMemsetAsync(dy.p, 0, sizeof(float) * n, c->stream));
-  launch_conv3x3((const float*)dx.p, H, W, (const float*)dw.p, relu_in, (const float*)dr.p, (float*)dy.p, (int*)de.p, c->stream);
+  launch_conv3x3((const float*)dx.p, H, W, (const float*)dw.p, relu_in, (const float*)dr.p, (float*)dy.p, (int*)de.p, c->stream, c->decoder_precise);
   CHECK_LAUNCH(c, "k_conv3x3_tc");
   c->launches += 1;
   int err = 0;

@@ -58,6 +58,14 @@ __device__ __forceinline__ float to_tf32(float x) {
   return __uint_as_float(u);
 }
 
+// Split-tf32 ("3xTF32") operands for the precise mode: part 0 = hi = tf32(x), part 1 = lo = tf32(x - hi). A product
+// x w = hi hi + lo hi + hi lo + O(2^-22 |x w|): three passes of the same kernel, accumulated in fp32 through the
+// residual input, reach fp32 accuracy on the tf32 tensor cores.
+__device__ __forceinline__ float tf32_part(float x, int part) {
+  const float hi = to_tf32(x);
+  return part ? to_tf32(x - hi) : hi;
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -103,6 +111,8 @@ struct ConvArgs {
   float* image;          // P x 3
   float* h2;             // trunk output kept for the backward (may be null)
   int* err;              // set to 1 if a pipeline barrier timed out
+  int xpart, wpart;      // which tf32 part of the activations / weights is staged (0 hi, 1 lo; tf32_part)
+  int no_bias;           // passes 2 and 3 of the precise mode: the bias went in with pass 1
 };
 
 // ---- mbarrier helpers (bounded waits: a protocol mistake must not hang the device) ----
@@ -180,10 +190,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_conv3x3_tc(ConvArgs a) {
       const int co = i / 72, rem = i - co * 72, tap = rem >> 3, c = rem & 7;
       const int ky = tap / 3, kx = tap - 3 * ky;
       float4 v = __ldg(gw + i);
-      v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
+      v.x = tf32_part(v.x, a.wpart); v.y = tf32_part(v.y, a.wpart); v.z = tf32_part(v.z, a.wpart); v.w = tf32_part(v.w, a.wpart);
       sW[((kx * 8 + c) * 3 + (2 - ky)) * 32 + co] = v;
     }
-    if (tid < 32) sBias[tid] = __ldg(a.w + 9216 + tid);
+    if (tid < 32) sBias[tid] = a.no_bias ? 0.f : __ldg(a.w + 9216 + tid);
     if (kHead)
       for (int i = tid; i < 198; i += kWsThreads) sHead[i] = __ldg(a.head + i);
   }
@@ -236,8 +246,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_conv3x3_tc(ConvArgs a) {
             const int px = pl + kPl * k;
             if (px < kCHW) {
               float4 q = v[rr][k];
-              q.x = to_tf32(fmaxf(q.x, relu_floor)); q.y = to_tf32(fmaxf(q.y, relu_floor));
-              q.z = to_tf32(fmaxf(q.z, relu_floor)); q.w = to_tf32(fmaxf(q.w, relu_floor));
+              q.x = tf32_part(fmaxf(q.x, relu_floor), a.xpart); q.y = tf32_part(fmaxf(q.y, relu_floor), a.xpart);
+              q.z = tf32_part(fmaxf(q.z, relu_floor), a.xpart); q.w = tf32_part(fmaxf(q.w, relu_floor), a.xpart);
               dstX[c * kCPlane + (r0 + rr) * kCHW + px] = q;
             }
           }
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_conv3x3_tc(ConvArgs a) {
           const bool live = gx < Wo && gy < Ho;
           const int64_t p = (int64_t)gy * Wo + gx;
           if (live && a.res) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(a.res + p * 32) + cq);
+            const float4 q = *(reinterpret_cast<const float4*>(a.res + p * 32) + cq);  // plain load: res may alias y (precise mode)
             v.x += q.x; v.y += q.y; v.z += q.z; v.w += q.w;
           }
           if (kHead) {
@@ -411,6 +421,26 @@ template <bool kHead> void launch_conv(const ConvArgs& a, cudaStream_t st) {
 }
 
 
+// precise mode: three passes (hi hi, lo hi, hi lo), accumulated in fp32 through the residual input. The head variant
+// runs its first two passes as plain convolutions into h2 and applies the head in the third.
+template <bool kHead> void launch_conv_p(const ConvArgs& a, int precise, cudaStream_t st) {
+  if (!precise) { launch_conv<kHead>(a, st); return; }
+  float* acc = kHead ? a.h2 : a.y;
+  ConvArgs p = a;
+  p.y = acc; p.xpart = 0; p.wpart = 0; p.no_bias = 0;
+  launch_conv<false>(p, st);
+  p.res = acc; p.no_bias = 1; p.xpart = 1; p.wpart = 0;
+  launch_conv<false>(p, st);
+  p.xpart = 0; p.wpart = 1;
+  if (kHead) {
+    ConvArgs q = a;
+    q.res = acc; q.no_bias = 1; q.xpart = 0; q.wpart = 1;
+    launch_conv<true>(q, st);
+  } else {
+    launch_conv<false>(p, st);
+  }
+}
+
 // ================================================ backward ====================================================
 // weight gradient of one convolution on the tensor cores:
 //   g_w[co][ky][kx][ci] = sum_p g_y[p][co] * xr[reflect(p + (ky-1, kx-1))][ci],  xr = relu_in ? relu(x) : x.
@@ -438,6 +468,8 @@ struct WgradArgs {
   float* gw;           // 9216 + 32, accumulated (+=)
   int H, W, relu_in;
   int* err;
+  int xpart, gpart;    // tf32 parts staged (precise mode: three passes, see tf32_part)
+  int no_bias;         // passes 2 and 3: the bias gradient went in with pass 1
 };
 
 __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) {
@@ -497,7 +529,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
           float4 t = v[u];
           if (a.relu_in) { t.x = fmaxf(t.x, 0.f); t.y = fmaxf(t.y, 0.f); t.z = fmaxf(t.z, 0.f); t.w = fmaxf(t.w, 0.f); }
           float* dst = sX + (q >> 2) * kWXChunk + (row * 32 + 4 * c) * 4 + (q & 3);
-          dst[0] = to_tf32(t.x); dst[4] = to_tf32(t.y); dst[8] = to_tf32(t.z); dst[12] = to_tf32(t.w);
+          dst[0] = tf32_part(t.x, a.xpart); dst[4] = tf32_part(t.y, a.xpart); dst[8] = tf32_part(t.z, a.xpart); dst[12] = tf32_part(t.w, a.xpart);
         }
       }
     }
@@ -515,8 +547,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k_conv3x3_wgrad_tc(WgradArgs a) 
         const int i = tid + u * kCThreads;
         const int c = ((i >> 5) & 3) * 2 + (i & 1), px = ((i >> 7) & 3) * 16 + ((i >> 1) & 15), r = i >> 9;
         float4 t = v[u];
-        bsum.x += t.x; bsum.y += t.y; bsum.z += t.z; bsum.w += t.w;
-        t.x = to_tf32(t.x); t.y = to_tf32(t.y); t.z = to_tf32(t.z); t.w = to_tf32(t.w);
+        if (!a.no_bias) { bsum.x += t.x; bsum.y += t.y; bsum.z += t.z; bsum.w += t.w; }
+        t.x = tf32_part(t.x, a.gpart); t.y = tf32_part(t.y, a.gpart); t.z = tf32_part(t.z, a.gpart); t.w = tf32_part(t.w, a.gpart);
 #pragma unroll
         for (int kx = 0; kx < 3; ++kx) {
           const int q = px + kx;
@@ -760,25 +792,32 @@ __global__ void __launch_bounds__(256) k_dec_head_bwd(int64_t P, const float* __
 
 int sm_count() { return device_sm_count(); }
 
-void launch_wgrad(const float* x, const float* gy, float* gw, int H, int W, int relu_in, int* err, cudaStream_t st) {
+void launch_wgrad(const float* x, const float* gy, float* gw, int H, int W, int relu_in, int* err, cudaStream_t st, int precise) {
   static DeviceOnce once;
   once.run([] { cudaFuncSetAttribute(k_conv3x3_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmemBytes); });
-  WgradArgs a{x, gy, gw, H, W, relu_in, err};
   const int tiles = ((W + kWT - 1) / kWT) * ((H + 1) / 2);
-  k_conv3x3_wgrad_tc<<<tiles < 2 * sm_count() ? tiles : 2 * sm_count(), kCThreads, kWSmemBytes, st>>>(a);
+  const int grid = tiles < 2 * sm_count() ? tiles : 2 * sm_count();
+  WgradArgs a{x, gy, gw, H, W, relu_in, err, 0, 0, 0};
+  k_conv3x3_wgrad_tc<<<grid, kCThreads, kWSmemBytes, st>>>(a);
+  if (precise) {  // + lo(x) hi(g) + hi(x) lo(g), accumulated by the kernel's own +=
+    a.no_bias = 1; a.xpart = 1; a.gpart = 0;
+    k_conv3x3_wgrad_tc<<<grid, kCThreads, kWSmemBytes, st>>>(a);
+    a.xpart = 0; a.gpart = 1;
+    k_conv3x3_wgrad_tc<<<grid, kCThreads, kWSmemBytes, st>>>(a);
+  }
 }
 
 // g_x = mask(x) . fold(convT(g_y)) + add: transposed weights -> tensor-core convolution on the grown domain -> fold
-void launch_dgrad_conv(const float* gy, const float* w, float* wt, float* gext, int H, int W, int* err, cudaStream_t st) {
+void launch_dgrad_conv(const float* gy, const float* w, float* wt, float* gext, int H, int W, int* err, cudaStream_t st, int precise) {
   k_dec_transpose_w<<<(9248 + 255) / 256, 256, 0, st>>>(w, wt);
   ConvArgs a{};
   a.x = gy; a.w = wt; a.y = gext; a.H = H; a.W = W; a.ext = 1; a.err = err;
-  launch_conv<false>(a, st);
+  launch_conv_p<false>(a, precise, st);
 }
 
 void launch_dgrad(const float* gy, const float* w, float* wt, float* gext, const float* x_mask, const float* add, float* gx,
-                  int H, int W, int* err, cudaStream_t st) {
-  launch_dgrad_conv(gy, w, wt, gext, H, W, err, st);
+                  int H, int W, int* err, cudaStream_t st, int precise) {
+  launch_dgrad_conv(gy, w, wt, gext, H, W, err, st, precise);
   const int64_t units = (int64_t)H * W * 8;
   k_dec_fold<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(H, W, gext, x_mask, add, gx);
 }
@@ -788,22 +827,23 @@ void launch_dgrad(const float* gy, const float* w, float* wt, float* gext, const
 int conv_decoder_params() { return 5 * 9248 + 198; }
 
 void launch_conv3x3(const float* x, int H, int W, const float* w, int relu_in, const float* res, float* y, int* err,
-                    cudaStream_t st) {
+                    cudaStream_t st, int precise) {
   if (H <= 0 || W <= 0) return;
   ConvArgs a{};
   a.x = x; a.w = w; a.res = res; a.y = y; a.H = H; a.W = W; a.relu_in = relu_in; a.err = err;
-  launch_conv<false>(a, st);
+  launch_conv_p<false>(a, precise, st);
 }
 
 void launch_conv3x3_backward(const float* x, int H, int W, const float* w, int relu_in, const float* gy, float* wt, float* gext,
-                             float* gx, float* gw, int* err, cudaStream_t st) {
+                             float* gx, float* gw, int* err, cudaStream_t st, int precise) {
   if (H <= 0 || W <= 0) return;
-  launch_wgrad(x, gy, gw, H, W, relu_in, err, st);
-  launch_dgrad(gy, w, wt, gext, relu_in ? x : nullptr, nullptr, gx, H, W, err, st);
+  launch_wgrad(x, gy, gw, H, W, relu_in, err, st, precise);
+  launch_dgrad(gy, w, wt, gext, relu_in ? x : nullptr, nullptr, gx, H, W, err, st, precise);
 }
 
 int launch_conv_decoder(const float* params, const float* emb, int H, int W, int d_f, float fx, float fy, float cx, float cy,
-                        const float* blend, int blend_stride, float* const act[6], float* image, int* err, cudaStream_t st) {
+                        const float* blend, int blend_stride, float* const act[6], float* image, int* err, cudaStream_t st,
+                        int precise) {
   if (H <= 0 || W <= 0) return 0;
   const int64_t units = (int64_t)H * W * 8;
   float *x0 = act[0], *h0 = act[1], *t1 = act[2], *h1 = act[3], *t2 = act[4], *h2 = act[5];
@@ -811,22 +851,22 @@ int launch_conv_decoder(const float* params, const float* emb, int H, int W, int
   ConvArgs a{};
   a.H = H; a.W = W; a.err = err;
   a.x = x0; a.w = params; a.res = nullptr; a.y = h0; a.relu_in = 0;
-  launch_conv<false>(a, st);
+  launch_conv_p<false>(a, precise, st);
   a.x = h0; a.w = params + 9248; a.y = t1; a.relu_in = 1;
-  launch_conv<false>(a, st);
+  launch_conv_p<false>(a, precise, st);
   a.x = t1; a.w = params + 2 * 9248; a.res = h0; a.y = h1;                            // h1 = h0 + conv2(relu(t1))
-  launch_conv<false>(a, st);
+  launch_conv_p<false>(a, precise, st);
   a.x = h1; a.w = params + 3 * 9248; a.res = nullptr; a.y = t2;
-  launch_conv<false>(a, st);
+  launch_conv_p<false>(a, precise, st);
   a.x = t2; a.w = params + 4 * 9248; a.res = h1; a.y = nullptr;                       // h2 = h1 + conv4(relu(t2)) -> head
   a.head = params + 5 * 9248; a.blend = blend; a.blend_stride = blend_stride; a.image = image; a.h2 = h2;
-  launch_conv<true>(a, st);
-  return 6;
+  launch_conv_p<true>(a, precise, st);
+  return precise ? 16 : 6;
 }
 
 int launch_conv_decoder_backward(const float* params, int H, int W, int d_f, const float* blend, int blend_stride,
                                  float* const act[6], const float* g_image, float* const g[3], float* gext, float* wt,
-                                 float* g_params, float* g_emb, float* g_blend, int* err, cudaStream_t st) {
+                                 float* g_params, float* g_emb, float* g_blend, int* err, cudaStream_t st, int precise) {
   if (H <= 0 || W <= 0) return 0;
   const int64_t P = (int64_t)H * W;
   const float *x0 = act[0], *h0 = act[1], *t1 = act[2], *h1 = act[3], *t2 = act[4], *h2 = act[5];
@@ -834,20 +874,20 @@ int launch_conv_decoder_backward(const float* params, int H, int W, int d_f, con
   const int grid = 4 * sm_count();
   k_dec_head_bwd<<<grid, 256, 0, st>>>(P, h2, params + 5 * 9248, blend, blend_stride, g_image, g_blend, g0, g_params + 5 * 9248);
   // block 2: h2 = h1 + conv4(relu(t2)), t2 = conv3(relu(h1));  g0 = dL/dh2
-  launch_wgrad(t2, g0, g_params + 4 * 9248, H, W, 1, err, st);
-  launch_dgrad(g0, params + 4 * 9248, wt, gext, t2, nullptr, g1, H, W, err, st);      // g1 = dL/dt2
-  launch_wgrad(h1, g1, g_params + 3 * 9248, H, W, 1, err, st);
-  launch_dgrad(g1, params + 3 * 9248, wt, gext, h1, g0, g2, H, W, err, st);           // g2 = dL/dh1
+  launch_wgrad(t2, g0, g_params + 4 * 9248, H, W, 1, err, st, precise);
+  launch_dgrad(g0, params + 4 * 9248, wt, gext, t2, nullptr, g1, H, W, err, st, precise);      // g1 = dL/dt2
+  launch_wgrad(h1, g1, g_params + 3 * 9248, H, W, 1, err, st, precise);
+  launch_dgrad(g1, params + 3 * 9248, wt, gext, h1, g0, g2, H, W, err, st, precise);           // g2 = dL/dh1
   // block 1: h1 = h0 + conv2(relu(t1)), t1 = conv1(relu(h0))
-  launch_wgrad(t1, g2, g_params + 2 * 9248, H, W, 1, err, st);
-  launch_dgrad(g2, params + 2 * 9248, wt, gext, t1, nullptr, g1, H, W, err, st);      // g1 = dL/dt1
-  launch_wgrad(h0, g1, g_params + 9248, H, W, 1, err, st);
-  launch_dgrad(g1, params + 9248, wt, gext, h0, g2, g0, H, W, err, st);               // g0 = dL/dh0
+  launch_wgrad(t1, g2, g_params + 2 * 9248, H, W, 1, err, st, precise);
+  launch_dgrad(g2, params + 2 * 9248, wt, gext, t1, nullptr, g1, H, W, err, st, precise);      // g1 = dL/dt1
+  launch_wgrad(h0, g1, g_params + 9248, H, W, 1, err, st, precise);
+  launch_dgrad(g1, params + 9248, wt, gext, h0, g2, g0, H, W, err, st, precise);               // g0 = dL/dh0
   // stem: h0 = conv0(x0)
-  launch_wgrad(x0, g0, g_params, H, W, 0, err, st);
-  launch_dgrad_conv(g0, params, wt, gext, H, W, err, st);                             // dL/dx0 on the grown domain
+  launch_wgrad(x0, g0, g_params, H, W, 0, err, st, precise);
+  launch_dgrad_conv(g0, params, wt, gext, H, W, err, st, precise);                             // dL/dx0 on the grown domain
   k_dec_fold_input<<<grid, 256, 0, st>>>(H, W, d_f, gext, g_blend, blend_stride, g_emb);
-  return 1 + 5 * 4;
+  return precise ? 1 + 5 * 8 : 1 + 5 * 4;
 }
 
 }  // namespace sb

@@ -110,20 +110,22 @@ void launch_lidar_head_bwd(const float* w, int d_f, int64_t n_rays, const float4
 // conv_decoder.cu (decode_image): the camera ConvDecoder on the tensor cores (tcgen05, tf32)
 int conv_decoder_params();
 // y = conv3x3(relu_in ? relu(x) : x; w[9216] + bias[32], reflect padding) (+ res); x, y, res: H x W x 32
+// precise: split-tf32 ("3xTF32": hi hi + lo hi + hi lo in three passes) -> fp32 accuracy on the tf32 tensor cores
 void launch_conv3x3(const float* x, int H, int W, const float* w, int relu_in, const float* res, float* y, int* err,
-                    cudaStream_t st);
+                    cudaStream_t st, int precise = 0);
 // test hook: gradients of one convolution. gw (9248, +=), gx H x W x 32; wt: 9248 scratch, gext: (H+2)(W+2) x 32 scratch
 void launch_conv3x3_backward(const float* x, int H, int W, const float* w, int relu_in, const float* gy, float* wt, float* gext,
-                             float* gx, float* gw, int* err, cudaStream_t st);
+                             float* gx, float* gw, int* err, cudaStream_t st, int precise = 0);
 // blend (P x blend_stride: rgb, features) -> image P x 3; act: the six activations x0, h0, t1, h1, t2, h2 (P x 32 each,
 // kept for the backward). Returns the launch count.
 int launch_conv_decoder(const float* params, const float* emb, int H, int W, int d_f, float fx, float fy, float cx, float cy,
-                        const float* blend, int blend_stride, float* const act[6], float* image, int* err, cudaStream_t st);
+                        const float* blend, int blend_stride, float* const act[6], float* image, int* err, cudaStream_t st,
+                        int precise = 0);
 // g_image P x 3 -> g_params (+=), g_emb[8] (+=), g_blend P x blend_stride (+=: rgb and feature slots); g: three P x 32
 // scratch buffers, gext: (H+2)(W+2) x 32, wt: 9248
 int launch_conv_decoder_backward(const float* params, int H, int W, int d_f, const float* blend, int blend_stride,
                                  float* const act[6], const float* g_image, float* const g[3], float* gext, float* wt,
-                                 float* g_params, float* g_emb, float* g_blend, int* err, cudaStream_t st);
+                                 float* g_params, float* g_emb, float* g_blend, int* err, cudaStream_t st, int precise = 0);
 
 // assign.cu (assign_points_to_tiles): per-point tile key (0xffffffff = rejected), (phi, omega, t_l, range),
 // shuffle hash, valid flag

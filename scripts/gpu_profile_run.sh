@@ -11,7 +11,8 @@ mkdir -p "$OUT"
 if [ "$PART" = "main" ]; then
 # 1. the bench lines (not under a profiler)
 timeout 600 python bench.py > "$OUT/bench_${TAG}.json" 2> "$OUT/bench_${TAG}.err"
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_${TAG}_reference_arm.json" 2>> "$OUT/bench_${TAG}.err"
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_${TAG}_reference_arm.json" 2>> "$OUT/bench_${TAG}.err"
+timeout 900 python bench.py --config cfg4 --steps 3 --warmup 1 > "$OUT/bench_${TAG}_cfg4.json" 2>> "$OUT/bench_${TAG}.err"
 # 2. launch list of the same command (shares only; cold-cache, serialised)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file "$OUT/launches_${TAG}.csv" \
     python bench.py --steps 2 --warmup 1 --no-cpu --serial > /dev/null 2>&1

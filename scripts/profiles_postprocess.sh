@@ -5,6 +5,7 @@ TAG="${1:-r1}"
 G=gpurun_out
 P=profiles
 cp "$G/bench_${TAG}.json" "$G/bench_${TAG}_reference_arm.json" "$P/"
+[ -f "$G/bench_${TAG}_cfg4.json" ] && cp "$G/bench_${TAG}_cfg4.json" "$P/"
 cp "$G/launches_${TAG}.csv" "$P/"
 python - "$G/launches_${TAG}.csv" > "$P/launches_${TAG}_summary.txt" <<'PY'
 import csv, sys
@@ -26,7 +27,7 @@ for k, (us, n) in sorted(tot.items(), key=lambda x: -x[1][0]):
 PY
 ncu -i "$G/prof_${TAG}.ncu-rep" --page raw --csv > /tmp/prof_${TAG}_raw.csv
 python scripts/ncu_summary.py /tmp/prof_${TAG}_raw.csv > "$P/ncu_full_${TAG}.txt"
-python scripts/make_traffic_json.py /tmp/prof_${TAG}_raw.csv "$P/traffic.json" > /dev/null
+python scripts/make_counters_json.py /tmp/prof_${TAG}_raw.csv "$P/counters.json" "$P/traffic.json" > /dev/null
 ncu -i "$G/prof_${TAG}.ncu-rep" --page source --csv --print-source cuda,sass > /tmp/prof_${TAG}_src.csv
 : > "$P/ncu_source_lines_${TAG}.txt"
 for k in "k_raster_fwd<(bool)0" "k_raster_fwd<(bool)1" "k_raster_bwd<(bool)0" "k_raster_bwd<(bool)1" "k_expand" "k_radix_pass<(int)2"; do
