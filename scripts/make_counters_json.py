@@ -17,12 +17,12 @@ hdr, units, data = rows[0], rows[1], rows[2:]
 ix = {h: i for i, h in enumerate(hdr)}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
          "second": 1e3, "nsecond": 1e-6, "%": 1.0, "": 1.0}
-PCT = {"issue_active_pct": "smsp__issue_active.avg.pct", "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+PCT = {"issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
        "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
        "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
        "fma_pipe_pct": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
        "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
-       "lanes_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio"}
+       "lanes_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio", "warp_instructions": "smsp__inst_executed.sum"}
 
 
 def val(d, name):
@@ -55,9 +55,11 @@ for d in data:
     for k, metric in PCT.items():
         v = val(d, metric)
         if v is not None:
-            e[k] += v * t
+            e[k] += v if k == "warp_instructions" else v * t
 for e in out.values():
     for k in PCT:
+        if k == "warp_instructions":
+            continue
         e[k] = e[k] / e["time_ms"] if e["time_ms"] > 0 else None
 json.dump(out, open(sys.argv[2], "w"), indent=1)
 if len(sys.argv) > 3:
