@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsplat_b200.so")
 _LIB = None
 
-INT_ARRAYS = {"raster_stats", "source_index", "rect", "isect_tile", "isect_depth_bits", "isect_src", "tile_begin", "tile_end",
+INT_ARRAYS = {"raster_stats", "hit_bits", "source_index", "rect", "isect_tile", "isect_depth_bits", "isect_src", "tile_begin", "tile_end",
               "grid", "n_contrib", "last_idx"}
 
 # every symbol include/splat_b200.h declares

@@ -2459,6 +2459,15 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
     for (int64_t k = 0; k < v->n_tiles; ++k) ((int64_t*)dst)[k] = h[k];
     return v->n_tiles;
   }
+  if (name == "hit_bits") {  // per list entry: which warps of the tile's CTA blended it in the last forward (saved for the backward)
+    if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "not rasterized");
+    if (!dst) return v->I;
+    std::vector<uint8_t> h;
+    int rc = fetch(c, h, v->out.hit, (size_t)v->I);
+    if (rc) return rc;
+    for (int64_t k = 0; k < v->I; ++k) ((int64_t*)dst)[k] = h[k];
+    return v->I;
+  }
   if (name == "raster_stats") {  // cumulative since view creation; zeros unless SPLATB200_STATS is set
     if (dst) {
       // [0] staged entries, [1] per-warp survivors of the first-level cull, [2] group-list entries (lidar), [3] loop
