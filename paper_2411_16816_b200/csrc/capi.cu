@@ -129,6 +129,9 @@ struct splatb200_view {
   int64_t fine_cap = 0;
   int64_t hit_cap = 0;            // out.hit: one byte per tile-list entry
   bool multi_pass = false;        // some lidar tile holds more than 256 rays
+  int64_t rows_cap = 0;           // out.hit_rows capacity in words (lidar v2 kernels)
+  // lidar: the v2 compositing kernels (raster_lidar.cu) unless a tile needs several ray passes or SPLATB200_LIDAR_V1 is set
+  bool lidar_v2() const { static const bool off = std::getenv("SPLATB200_LIDAR_V1") != nullptr; return !s.is_camera && !multi_pass && !off; }
   int64_t I_sort = 0;             // entries the radix sort handles: block-level intersections, or I
   // queries
   int64_t P = 0, n_tiles = 0;
@@ -265,7 +268,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); for (auto*& b : v->dec_act) dfree(b); for (auto*& b : v->dec_g) dfree(b); dfree(v->dec_gext); dfree(v->d_dec_gimage); dfree(v->d_dec_gparams); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.hit_rows); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); for (auto*& b : v->dec_act) dfree(b); for (auto*& b : v->dec_g) dfree(b); dfree(v->dec_gext); dfree(v->d_dec_gimage); dfree(v->d_dec_gparams); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -400,6 +403,15 @@ int ensure_isect_capacity(splatb200_view* v, int64_t n_sort, int64_t n_fine) {
     const int64_t cap = n_fine + n_fine / 4 + 1024;
     CU_TRY(c, cudaMalloc(&v->out.hit, (size_t)cap));
     v->hit_cap = cap;
+  }
+  if (v->lidar_v2()) {
+    const int64_t need = (int64_t)lidar_hit_rows_words(n_fine, v->n_tiles);
+    if (need > v->rows_cap) {
+      dfree(v->out.hit_rows);
+      const int64_t cap = need + need / 4;
+      CU_TRY(c, cudaMalloc(&v->out.hit_rows, sizeof(uint32_t) * (size_t)cap));
+      v->rows_cap = cap;
+    }
   }
   if (v->two_level && n_fine > v->fine_cap) {
     dfree(v->vals_fine);
@@ -1739,8 +1751,12 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   v->band_dl_valid = false;
   if (!v->plan_fwd) {
     StageTimer tm(v, 5, st);
-    launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
-                      v->out, st);
+    if (v->lidar_v2())
+      launch_raster_fwd_lidar(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end,
+                              v->tile_order, v->out, st);
+    else
+      launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
+                        v->out, st);
     CHECK_LAUNCH(c, "k_raster_fwd");
     c->launches += 1;
   } else {
@@ -1750,8 +1766,12 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     StageTimer tm(v, 5, st);
     for (size_t b = 0; b < v->bands.size(); ++b) {
       const auto& bd = v->bands[b];
-      launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr, v->out,
-                        st, bd.tile_first, bd.tile_count);
+      if (v->lidar_v2())
+        launch_raster_fwd_lidar(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr,
+                                v->out, st, bd.tile_first, bd.tile_count);
+      else
+        launch_raster_fwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr, v->out,
+                          st, bd.tile_first, bd.tile_count);
       CHECK_LAUNCH(c, "k_raster_fwd (band)");
       c->launches += 1;
       CU_TRY(c, cudaEventRecord(v->ev_bfwd[b], st));

@@ -48,6 +48,10 @@ struct RasterOutDev {
   uint8_t* hit;        // I  per list entry: bit w set if some query of warp w of the tile's CTA blended it (saved for
                        //    the backward pass, which then revisits only those entries)
   int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
+  uint32_t* hit_rows;  // lidar v2 kernels (raster_lidar.cu), else null: per-LANE hit bits. One 2048-word block per 256-entry
+                       //    batch of a tile's list, block (tile_begin >> 8) + tile + batch, laid out [warp][word][lane]: bit
+                       //    (j & 31) of word (j >> 5) = that ray blended batch entry j. Words of a (warp, word) pair without
+                       //    any hit are not written (the hit bytes say which).
   uint8_t* tile_wrap;  // T  lidar: 1 if some batch of the tile could not certify |azimuth difference| < pi (seam tiles);
                        //    the backward skips the wrap elsewhere. Written by the forward.
   // optional line-of-sight channel of a lidar view: los[q] = sum of alpha_i over the
@@ -90,6 +94,12 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
 void launch_raster_fwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
                        const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st, int tile_first = 0, int tile_count = -1);
+// raster_lidar.cu: the lidar forward kernel, version 2 (lane = entry cull, bit transpose, lane = ray walk over its own
+// candidates); needs out.hit_rows (lidar_hit_rows_words words) and tiles of at most 256 rays
+size_t lidar_hit_rows_words(int64_t n_isect, int64_t n_tiles);
+void launch_raster_fwd_lidar(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
+                             const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                             const uint32_t* tile_order, const RasterOutDev& out, cudaStream_t st, int tile_first = 0, int tile_count = -1);
 constexpr int kDumpStride = 42;
 void launch_project_dump(const Sensor& s, const SceneDev& sc, float* dump, cudaStream_t st);
 

@@ -30,6 +30,31 @@ __device__ __forceinline__ float wrap_pi(float a) {
 // are latency-bound: a batch is a chain of dependent global loads — list entry, record — in front of the compute)
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// ------------------------------------------------------------------------------------------------
+// Packed fp32 pairs (sm_100a: FFMA2 / FMUL2 / FADD2 execute two IEEE-754 round-to-nearest operations per issue slot;
+// each half is bit-identical to the scalar __f*_rn operation, so the parity contract is untouched). The compositing
+// kernels are issue-bound, not FMA-pipe-bound: halving the fp32 instruction count of the inner loops is the point.
+// ------------------------------------------------------------------------------------------------
+typedef unsigned long long f32x2;  // .x in the low half
+__device__ __forceinline__ f32x2 pack2(float x, float y) { f32x2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y)); return r; }
+__device__ __forceinline__ void unpack2(f32x2 v, float& x, float& y) { asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v)); }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) { f32x2 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) { f32x2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) { f32x2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) { f32x2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+
+// alpha_qform without the azimuth wrap, on packed pairs: the same operations in the same order as the scalar form
+// (mx my = fma(v, t, m); d = q - m; qf = fma(a, dx dx, fma(c, dy dy, b2 (dx dy)))), 7 issue slots instead of 10.
+// m0 = (mean2d.x, mean2d.y), v = (vel.x, vel.y), q = (qx, qy), tt = (t, t).
+__device__ __forceinline__ float alpha_qform_packed(f32x2 m0, f32x2 v, const float4 gB, f32x2 q, f32x2 tt, float& dx, float& dy) {
+  const f32x2 d = sub2(q, fma2(v, tt, m0));
+  const f32x2 dd = mul2(d, d);
+  unpack2(d, dx, dy);
+  float dxx, dyy;
+  unpack2(dd, dxx, dyy);
+  return __fmaf_rn(gB.x, dxx, __fmaf_rn(gB.z, dyy, __fmul_rn(gB.y, __fmul_rn(dx, dy))));
+}
+
 struct AlphaEval {
   float alpha, dx, dy, gauss;
   bool clamped;
