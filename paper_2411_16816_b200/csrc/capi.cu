@@ -444,8 +444,8 @@ int alloc_query_buffers(splatb200_view* v) {
   CU_TRY(c, cudaMalloc(&v->tile_begin, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->tile_end, sizeof(uint32_t) * T));
   CU_TRY(c, cudaMalloc(&v->to_vals0, sizeof(uint32_t) * T));
-  CU_TRY(c, cudaMalloc(&v->out.tile_wrap, T));
-  CU_TRY(c, cudaMemsetAsync(v->out.tile_wrap, 1, T, c->stream));
+  CU_TRY(c, cudaMalloc(&v->out.tile_wrap, 8 * T));  // per tile (shared kernels) or per (tile, warp) (lidar v2 kernels)
+  CU_TRY(c, cudaMemsetAsync(v->out.tile_wrap, 1, 8 * T, c->stream));
   CU_TRY(c, cudaMalloc(&v->tile_ws, tile_hist_bytes(v->s.tiles_x, v->s.tiles_y)));
   CU_TRY(c, cudaMalloc(&v->d_total, sizeof(int64_t)));
   if (std::getenv("SPLATB200_STATS")) {  // debug counters of the compositing kernels (read through view_array "raster_stats")
@@ -1848,16 +1848,24 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
       const auto& bd = v->bands[b];
       CU_TRY(c, cudaStreamWaitEvent(st, v->ev_bup[b], 0));
       if (v->I > 0) {
-        launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr, v->out,
-                          g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st, bd.tile_first, bd.tile_count);
+        if (v->lidar_v2())
+          launch_raster_bwd_lidar(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr,
+                                  v->out, g_blend16, g_alpha, rg, pg, st, bd.tile_first, bd.tile_count);
+        else
+          launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, nullptr, v->out,
+                            g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st, bd.tile_first, bd.tile_count);
         CHECK_LAUNCH(c, "k_raster_bwd (band)");
         c->launches += 1;
       }
     }
   } else if (v->I > 0) {
     StageTimer tm(v, 6, st);
-    launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
-                      v->out, g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
+    if (v->lidar_v2())
+      launch_raster_bwd_lidar(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end,
+                              v->tile_order, v->out, g_blend16, g_alpha, rg, pg, st);
+    else
+      launch_raster_bwd(v->s, v->proj, v->vals(), v->tile_begin, v->tile_end, v->rays, v->ray_begin, v->ray_end, v->tile_order,
+                        v->out, g_blend16, g_alpha, rg, pg, v->sensor_grads + 6, st);
     CHECK_LAUNCH(c, "k_raster_bwd");
     c->launches += 1;
   }

@@ -48,10 +48,10 @@ struct RasterOutDev {
   uint8_t* hit;        // I  per list entry: bit w set if some query of warp w of the tile's CTA blended it (saved for
                        //    the backward pass, which then revisits only those entries)
   int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
-  uint32_t* hit_rows;  // lidar v2 kernels (raster_lidar.cu), else null: per-LANE hit bits. One 2048-word block per 256-entry
-                       //    batch of a tile's list, block (tile_begin >> 8) + tile + batch, laid out [warp][word][lane]: bit
-                       //    (j & 31) of word (j >> 5) = that ray blended batch entry j. Words of a (warp, word) pair without
-                       //    any hit are not written (the hit bytes say which).
+  uint32_t* hit_rows;  // lidar v2 kernels (raster_lidar.cu), else null: the RAYS that blended each list entry, one 32-bit
+                       //    word per (entry, warp of the tile's CTA) instead of the hit byte. One 2048-word block per 256
+                       //    entries of a tile's list, block (tile_begin >> 8) + tile + (entry >> 8), laid out
+                       //    [warp][entry & 255]; written up to each warp's last blended entry
   uint8_t* tile_wrap;  // T  lidar: 1 if some batch of the tile could not certify |azimuth difference| < pi (seam tiles);
                        //    the backward skips the wrap elsewhere. Written by the forward.
   // optional line-of-sight channel of a lidar view: los[q] = sum of alpha_i over the
@@ -175,6 +175,12 @@ void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, 
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
                        const uint32_t* tile_order, const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha, const RasterGradDev& rg,
                        const ParamGradDev& pg, float* d_time_offset, cudaStream_t st, int tile_first = 0, int tile_count = -1);
+
+// the lidar backward that pairs with launch_raster_fwd_lidar (reads fwd.hit_rows; tiles of at most 256 rays)
+void launch_raster_bwd_lidar(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
+                             const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                             const uint32_t* tile_order, const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha,
+                             const RasterGradDev& rg, const ParamGradDev& pg, cudaStream_t st, int tile_first = 0, int tile_count = -1);
 
 // project_bwd.cu
 enum BwdMode { kFused = 0, kFromProjected = 1, kProjOnly = 2, kComposeOnly = 3 };

@@ -445,6 +445,248 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Lidar compositing backward, version 2 (pairs with raster_lidar.cu's forward).
+//
+// A lidar list entry is blended by ~8 of a warp's 32 rays and needed by 1.06 of the tile's 8 warps. The shared kernel
+// above walks a warp's hit entries one at a time with all 32 lanes (phase A: ~140 instructions per entry for ~8 useful
+// lanes) behind CTA-wide staging barriers. Here
+//   * every warp works on its own: it reads ITS hit words (one per list entry: the rays that blended it, saved by the
+//     forward), fetches the records of the entries it blended into a private ring — no CTA barrier anywhere;
+//   * phase A is lane-divergent: a lane walks only the entries ITS ray blended (bits of the hit words, kept per lane in
+//     ring order), back to front, so different lanes are at different entries of the 16-entry chunk — about half the
+//     trips of the entry-by-entry walk — and parks (w, dL/dsigma) in the [slot][lane] panel (zero-filled first);
+//   * phase B (channel product as split-tf32 MMAs, raw moments, REDs) is reduce_panel above, unchanged.
+// ------------------------------------------------------------------------------------------------
+template <bool kLos>
+__global__ void __launch_bounds__(256, 2)
+k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
+                   const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
+                   const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
+                   const uint32_t* __restrict__ tile_order, int tile_first, RasterOutDev fwd, const float* __restrict__ g_blend16,
+                   const float* __restrict__ g_alpha, RasterGradDev rg, ParamGradDev pg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* sA = reinterpret_cast<float4*>(smem_raw);                    // kBatch
+  float4* sB = sA + kBatch;                                            // kBatch
+  float4* sF = sB + kBatch;                                            // 4 kBatch, PLANAR: sF[c * kBatch + j]
+  float2* sC = reinterpret_cast<float2*>(sF + 4 * kBatch);             // kBatch
+  uint32_t* sSrc = reinterpret_cast<uint32_t*>(sC + kBatch);           // kBatch
+  uint32_t* sHw = sSrc + kBatch;                                       // 8 x kBatch: [warp][entry] hit words of the batch
+  WarpScratch* sWs = reinterpret_cast<WarpScratch*>(sHw + 8 * kBatch); // 8
+  uint8_t* sListAll = reinterpret_cast<uint8_t*>(sWs + 8);             // 8 x kBatch
+  __shared__ int s_max_last;
+
+  const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  uint8_t* sList = sListAll + kBatch * warp;
+  const uint32_t* myHw = sHw + kBatch * warp;
+  WarpScratch& ws = sWs[warp];
+  const uint32_t lb = tile_begin[tile], le = tile_end[tile];
+  if (le <= lb) return;
+  const bool wrap = fwd.tile_wrap[tile] != 0;  // certified per tile by the forward (raster_common.cuh)
+  const int64_t qpos = ray_begin[tile] + tid;
+  const bool inside = qpos < ray_end[tile];
+  float qx = 0.0f, qy = 0.0f, t = 0.0f;
+  int64_t pix = 0;
+  if (inside) {
+    const float4 r = rays[qpos];
+    qx = r.x; qy = r.y; t = r.z;
+    pix = (int64_t)__float_as_uint(r.w);
+  }
+  int last = 0;
+  float los_cut = 0.0f, g_los = 0.0f;
+  if (kLos && inside) { los_cut = fwd.los_cut[pix]; g_los = fwd.g_los[pix]; }
+  float T = 1.0f, K = 0.0f, g_D = 0.0f;
+  float g_out[kChannels];
+#pragma unroll
+  for (int k = 0; k < kChannels; ++k) g_out[k] = 0.0f;
+  if (inside) {
+    last = fwd.last_idx[pix];
+    T = fwd.t_final[pix];
+    const float4* g4 = reinterpret_cast<const float4*>(g_blend16 + 16 * pix);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 g = g4[k];
+      g_out[4 * k] = g.x; g_out[4 * k + 1] = g.y; g_out[4 * k + 2] = g.z; g_out[4 * k + 3] = g.w;
+    }
+    float g_acc = g_alpha[pix];
+    const float A = 1.0f - T;
+    if (A > 1e-6f) {  // expected = D / A
+      g_D = g_out[13] / A;
+      g_acc += -g_out[13] * (fwd.range_blend[pix] / A) / A;
+    } else {
+      g_D = g_out[13];
+    }
+#pragma unroll
+    for (int k = 0; k < kChannels; ++k)
+      if (k >= s.channels) g_out[k] = 0.0f;
+    K = g_acc * T;
+  }
+  float S = 0.0f;  // sum_c g_c * suffix_c + g_D * suffix_r
+  {  // per-query data for phase B (read there as broadcasts)
+    float* row = &ws.px[lane * kPxStride];
+    *reinterpret_cast<float4*>(row) = make_float4(qx, qy, t, g_D);
+    float gcol[kChannels];
+#pragma unroll
+    for (int k = 0; k < kChannels; ++k) gcol[k] = g_out[k];
+    gcol[13] = g_D; gcol[14] = g_D * t; gcol[15] = 0.0f;  // columns 13, 14 of the channel product: d/d range, d/d v_r
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<float4*>(row + 4 + 4 * k) = make_float4(gcol[4 * k], gcol[4 * k + 1], gcol[4 * k + 2], gcol[4 * k + 3]);
+  }
+  auto zero_panel = [&]() {  // lanes that did not blend an entry contribute nothing
+    float4* w4 = reinterpret_cast<float4*>(ws.w);
+    float4* g4 = reinterpret_cast<float4*>(ws.gs);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = lane; i < kChunk * kWStride / 4; i += 32) w4[i] = z;
+    for (int i = lane; i < kChunk * kPanelStride / 4; i += 32) g4[i] = z;
+  };
+  zero_panel();
+  if (tid == 0) s_max_last = 0;
+  __syncthreads();
+  int warp_last = last;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
+  if (lane == 0 && warp_last > 0) atomicMax(&s_max_last, warp_last);
+  __syncthreads();
+  const int max_last = s_max_last;
+  if (max_last == 0) return;
+
+  const uint32_t* const hitw = fwd.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u;  // [batch][warp][entry]
+  int n_slots = 0;  // parked entries (warp-uniform); the panel persists across batches
+  float dt_unused = 0.0f;
+
+  for (int batch = (max_last - 1) / kBatch; batch >= 0; --batch) {
+    const int bstart = batch * kBatch;
+    const int cnt = min(kBatch, max_last - bstart);
+    // thread = list entry: the hit words of the 8 warps (each valid up to that warp's last blended entry: the forward
+    // wrote every word in front of it), records only for entries some warp blended
+    {
+      uint32_t any = 0u;
+      if (tid < cnt) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          uint32_t hw = hitw[(size_t)batch * 2048u + w * 256 + tid];
+          sHw[w * kBatch + tid] = hw;
+          any |= hw;
+        }
+        if (any) {
+          const uint32_t src = vals[lb + bstart + tid];
+          sSrc[tid] = src;
+          sA[tid] = p.geomA[src];
+          sB[tid] = p.geomB[src];
+          sC[tid] = p.geomC[src];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sF[k * kBatch + tid] = p.feat[4 * (size_t)src + k];
+        }
+      }
+    }
+    __syncthreads();
+
+    if (warp_last > bstart) {
+      // the warp's hit entries of this batch, back to front. A word beyond this warp's last blended entry was never
+      // written by the forward: masked by position.
+      int n_w = 0;
+      for (int c0 = (cnt - 1) & ~31; c0 >= 0; c0 -= 32) {
+        const int j = c0 + (31 - lane);  // lane 0 takes the highest entry: ballot ranks are back-to-front ranks
+        const bool bit = j < cnt && bstart + j < warp_last && myHw[j] != 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        if (bit) sList[n_w + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)j;
+        n_w += __popc(bal);
+      }
+      __syncwarp();
+      for (int k0 = 0; k0 < n_w;) {
+        const int g = min(kChunk - n_slots, n_w - k0);
+        // my ray's bit of each of the g entries; their records for phase B
+        uint32_t mybits = 0u;
+        for (int e = 0; e < g; ++e) {
+          const int j = sList[k0 + e];
+          mybits |= ((bstart + j < last ? myHw[j] >> lane : 0u) & 1u) << e;
+        }
+        if (lane < g) {
+          const int j = sList[k0 + lane];
+          ws.gAB[n_slots + lane] = sA[j];
+          ws.gAB[kChunk + n_slots + lane] = sB[j];
+          ws.src[n_slots + lane] = sSrc[j];
+        }
+        // ---- phase A: every lane walks the entries ITS ray blended, back to front ---------------
+        while (mybits != 0u) {
+          const int e = __ffs(mybits) - 1;
+          mybits &= mybits - 1u;
+          const int j = sList[k0 + e];
+          const float4 gA = sA[j], gB = sB[j];
+          float dx, dy;
+          const float qf = alpha_qform<true>(gA, gB, qx, qy, t, dx, dy, wrap);
+          AlphaEval ev;
+          if (!alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) continue;  // (the bit says blended)
+          const float one_m = 1.0f - ev.alpha;
+          float inv;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));  // [1 - alpha_clamp, 1]: 1 ulp, no range fix-up needed
+          T = T * inv;  // transmittance in front of this Gaussian
+          const float w = ev.alpha * T;
+          float d0 = 0.0f, d1 = 0.0f, d2 = 0.0f, d3 = 0.0f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float4 f4 = sF[c * kBatch + j];
+            d0 = fmaf(g_out[4 * c], f4.x, d0);
+            d1 = fmaf(g_out[4 * c + 1], f4.y, d1);
+            d2 = fmaf(g_out[4 * c + 2], f4.z, d2);
+            d3 = fmaf(g_out[4 * c + 3], f4.w, d3);
+          }
+          float dotgf = (d0 + d1) + (d2 + d3);
+          const float2 c2 = sC[j];
+          const float r_rs = fmaf(c2.y, t, c2.x);  // r_rs = r + v_r t
+          dotgf = fmaf(g_D, r_rs, dotgf);
+          float g_extra = 0.0f;
+          if (kLos && r_rs < los_cut) g_extra = g_los;  // d los / d alpha_i = 1 in front of the cut
+          const float g_a = dotgf * T + (K - S) * inv + g_extra;
+          S = fmaf(w, dotgf, S);
+          ws.w[(n_slots + e) * kWStride + lane] = w;
+          if (!ev.clamped) ws.gs[(n_slots + e) * kPanelStride + lane] = -ev.alpha * g_a;  // alpha = rho exp(-sigma); clamped: constant
+        }
+        n_slots += g;
+        k0 += g;
+        __syncwarp();
+        if (n_slots == kChunk) {
+          reduce_panel<false>(ws, n_slots, lane, s.d_f, rg, pg, dt_unused, wrap);
+          zero_panel();
+          __syncwarp();
+          n_slots = 0;
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with the staged batch
+  }
+  if (n_slots > 0) {
+    __syncwarp();
+    reduce_panel<false>(ws, n_slots, lane, s.d_f, rg, pg, dt_unused, wrap);
+  }
+}
+
+constexpr size_t kBwdLidarSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBatch * 4 + 8 * kBatch * 4 + 8 * sizeof(WarpScratch) + 8 * kBatch;
+
+void launch_raster_bwd_lidar(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
+                             const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
+                             const uint32_t* tile_order, const RasterOutDev& fwd, const float* g_blend16, const float* g_alpha,
+                             const RasterGradDev& rg, const ParamGradDev& pg, cudaStream_t st, int tile_first, int tile_count) {
+  const int tiles = tile_count < 0 ? s.tiles_x * s.tiles_y : tile_count;
+  if (tiles <= 0) return;
+  if (tile_count < 0) tile_first = 0;
+  else tile_order = nullptr;
+  static DeviceOnce once;
+  once.run([] {
+    cudaFuncSetAttribute(k_raster_bwd_lidar<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdLidarSmem);
+    cudaFuncSetAttribute(k_raster_bwd_lidar<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdLidarSmem);
+  });
+  if (fwd.los_cut && fwd.g_los)
+    k_raster_bwd_lidar<true><<<tiles, 256, kBwdLidarSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
+                                                               tile_first, fwd, g_blend16, g_alpha, rg, pg);
+  else
+    k_raster_bwd_lidar<false><<<tiles, 256, kBwdLidarSmem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, tile_order,
+                                                                tile_first, fwd, g_blend16, g_alpha, rg, pg);
+}
+
 constexpr size_t kBwdSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBatch * 4 + 8 * sizeof(PatchBox) +
                             8 * sizeof(WarpScratch) + kBatch + 8 * kBatch;
 

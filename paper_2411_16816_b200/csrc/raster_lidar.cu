@@ -39,21 +39,32 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
+constexpr int kSlots = 256 + 8 * 32;  // staged batch entries, then 32 carry slots per warp
+constexpr int kListCap = 32 + 256;
+
+// Batch staging is CTA-wide (thread = list entry: the record loads and the 8-box test are done once per entry); the
+// walk is per warp in FULL rounds of 32 survivors: what is left of a batch (< 32 survivors) is copied to the warp's
+// carry slots and opens the first round of the next batch, so only a list's very last round runs partially filled.
+// (Measured alternatives: partial rounds per batch, 1.6 rounds per 32.4 survivors: 0.406 ms; every warp scanning the
+// whole list on its own without CTA barriers: 0.62 ms — the 8-fold test work and the unhidden load chains cost more
+// than the barriers.)
+// The lanes that blended each entry leave as one 32-bit word per (entry, warp) in hit_rows[block][warp][entry & 255]
+// (block = (tile_begin >> 8) + tile + (entry >> 8): never shared between tiles), 0 for an entry the warp culled.
 template <bool kLos, bool kHead>
 __global__ void __launch_bounds__(256, 3)
 k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
                    const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
                    const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
                    const uint32_t* __restrict__ tile_order, int tile_first, RasterOutDev out) {
-  __shared__ float4 sA[256];
-  __shared__ float4 sB[256];
-  __shared__ float2 sC[256];
-  __shared__ float4 sF[4 * 256];   // PLANAR: sF[c * 256 + j] (phase 2 gathers: 16-byte stride between entries)
-  __shared__ float4 sRay[256];     // azimuth, elevation, t of the tile's rays (phase 1 broadcasts)
-  __shared__ uint8_t sMask[256];
-  __shared__ uint8_t sList[8][256];
-  __shared__ uint32_t sRow[8][8][32];  // [warp][word][lane]: bit (j & 31) of word (j >> 5) = this lane blended batch entry j
-  __shared__ uint32_t sHitW[8][8];     // [warp][word]: OR of the warp's rows
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* sA = reinterpret_cast<float4*>(smem_raw);              // kSlots: mean2d.xy, velocity.xy
+  float4* sB = sA + kSlots;                                      // kSlots: conic a, 2b, c; rho
+  float4* sF = sB + kSlots;                                      // 4 x kSlots, PLANAR (gathers by slot: 16-byte stride)
+  float4* sRay = sF + 4 * kSlots;                                // 256: azimuth, elevation, t, t (phase 1 broadcasts)
+  float2* sC = reinterpret_cast<float2*>(sRay + 256);            // kSlots: range, v_r
+  uint32_t* sPos = reinterpret_cast<uint32_t*>(sC + kSlots);     // kSlots: tile-local list position
+  uint16_t* sListAll = reinterpret_cast<uint16_t*>(sPos + kSlots);  // 8 x kListCap
+  uint8_t* sMask = reinterpret_cast<uint8_t*>(sListAll + 8 * kListCap);  // 256
   __shared__ PatchBox sBox[8];
   __shared__ float sHead[kHead ? 640 : 1];  // lidar head parameters (fused epilogue)
 
@@ -64,16 +75,16 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
     for (int i = tid; i < np; i += 256) sHead[i] = out.head_w[i];
   }
   const int lane = tid & 31, warp = tid >> 5;
+  uint16_t* lst = sListAll + kListCap * warp;
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
   const int64_t q_begin = ray_begin[tile], q_end = ray_end[tile];  // at most 256 rays (the host guarantees it)
-  bool any_wrap = false;
 
-  const int64_t pos = q_begin + tid;
-  const bool inside = pos < q_end;
+  const int64_t qpos = q_begin + tid;
+  const bool inside = qpos < q_end;
   float qx = 0.0f, qy = 0.0f, t = 0.0f;
   int64_t pix = 0;
   if (inside) {
-    const float4 r = rays[pos];
+    const float4 r = rays[qpos];
     qx = r.x; qy = r.y; t = r.z;
     pix = (int64_t)__float_as_uint(r.w);  // original ray index
   }
@@ -90,27 +101,106 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
   for (int k = 0; k < kChannels / 2; ++k) acc2[k] = pack2(0.0f, 0.0f);
   const f32x2 q2 = pack2(qx, qy), t2 = pack2(t, t);
   bool done = !inside;
-  __syncthreads();  // patch boxes, rays visible
+  __syncthreads();  // patch boxes, rays, head parameters visible
 
-  // rows of hit bits: 2048 words per 256-entry batch, [warp][word][lane]; block index (lb >> 8) + tile + batch never
-  // collides between tiles (a partial last batch still owns a whole block)
-  uint32_t* const rows_tile = out.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u;
-
-  int64_t pending = -1;  // list position of the batch whose hit bytes are still to be written (CTA-uniform)
-  auto flush_hits = [&]() {
-    if (pending >= 0 && (uint32_t)pending + tid < le) {
-      uint32_t h = 0u;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) h |= ((sHitW[w][tid >> 5] >> (tid & 31)) & 1u) << w;
-      out.hit[pending + tid] = (uint8_t)h;
-    }
-    pending = -1;
-  };
+  uint32_t* const hitw = out.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u + warp * 256;
+  const float4* wray = sRay + 32 * warp;
+  const unsigned lt = (1u << lane) - 1u;
+  const int carry0 = 256 + 32 * warp;  // this warp's carry slots
+  int ncarry = 0;
+  bool carry_wrap = false, any_wrap = false;
+  unsigned live = __ballot_sync(0xffffffffu, !done);
   unsigned long long st_cand = 0ull, st_iter = 0ull;
+
+  // one round: list entries k0 .. k0 + n - 1 (n <= 32); rw: some of them may need the azimuth wrap
+  auto do_round = [&](int k0, int n, bool rw) {
+    // ---- phase 1: lane = entry -----------------------------------------------------------------
+    uint32_t m = 0u;
+    int myslot = 0;
+    if (lane < n) {
+      myslot = lst[k0 + lane];
+      const float4 gA = sA[myslot], gB = sB[myslot];
+      // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min); margins: 1% on rho, 0.02 on qf (the
+      // evaluation's exp and this log are accurate to ~1e-6)
+      float qcut = s.qform_max;
+      const float rho = gB.w;
+      if (s.alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qcut = fminf(qcut, 2.0f * __logf(rho * 1.01f / s.alpha_min) + 0.02f);
+      if (!rw) {  // certified: no azimuth difference leaves (-pi, pi) — packed pairs, 10 issue slots per ray
+        const f32x2 m0 = pack2(gA.x, gA.y), vv = pack2(gA.z, gA.w);
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const float4 ry = wray[r];  // qx qy t t
+          float dx, dy;
+          const float qf = alpha_qform_packed(m0, vv, gB, pack2(ry.x, ry.y), pack2(ry.z, ry.w), dx, dy);
+          if (qf <= qcut) m |= 1u << r;
+        }
+      } else {
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const float4 ry = wray[r];
+          float dx, dy;
+          const float qf = alpha_qform<true>(gA, gB, ry.x, ry.y, ry.z, dx, dy, true);
+          if (qf <= qcut) m |= 1u << r;
+        }
+      }
+      m &= live;
+    }
+    uint32_t bits = transpose32(m, lane);  // bit kk: list entry k0 + kk may blend with MY ray
+    if (out.stats) st_cand += __popc(bits);
+    // ---- phase 2: lane = ray, every lane walks its own candidates front to back ----------------
+    uint32_t hitk = 0u;
+    int trips = 0;
+    while (bits != 0u) {
+      const uint32_t b = bits & (0u - bits);
+      const int slot = lst[k0 + __ffs(bits) - 1];
+      bits ^= b;
+      ++trips;
+      const float4 gA = sA[slot], gB = sB[slot];
+      float dx, dy;
+      const float qf = rw ? alpha_qform<true>(gA, gB, qx, qy, t, dx, dy, true)
+                          : alpha_qform_packed(pack2(gA.x, gA.y), pack2(gA.z, gA.w), gB, q2, t2, dx, dy);
+      AlphaEval ev;
+      if (alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) {
+        const float w = __fmul_rn(ev.alpha, T);
+        const f32x2 ww = pack2(w, w);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 f4 = sF[c * kSlots + slot];
+          acc2[2 * c] = fma2(pack2(f4.x, f4.y), ww, acc2[2 * c]);
+          acc2[2 * c + 1] = fma2(pack2(f4.z, f4.w), ww, acc2[2 * c + 1]);
+        }
+        T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
+        ++n_contrib;
+        last_idx = (int)sPos[slot] + 1;
+        hitk |= b;
+        const float2 c2 = sC[slot];
+        const float r_rs = __fmaf_rn(c2.y, t, c2.x);
+        range_acc = __fmaf_rn(r_rs, w, range_acc);
+        if (kLos && r_rs < los_cut) los = __fadd_rn(los, ev.alpha);  // opacity in front of the measured range
+        if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
+        if (T < s.transmittance_min) { done = true; bits = 0u; }
+      }
+    }
+    if (out.stats) st_iter += (unsigned long long)__reduce_max_sync(0xffffffffu, trips);
+    // the rays that blended each entry: back to entry-major, one word per (entry, warp)
+    const uint32_t hw = transpose32(hitk, lane);
+    if (lane < n) {
+      const uint32_t ps = sPos[myslot];
+      hitw[(size_t)(ps >> 8) * 2048u + (ps & 255u)] = hw;
+    }
+    live = __ballot_sync(0xffffffffu, !done);
+  };
+  auto copy_slot = [&](int from, int to) {
+    sA[to] = sA[from];
+    sB[to] = sB[from];
+    sC[to] = sC[from];
+    sPos[to] = sPos[from];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sF[c * kSlots + to] = sF[c * kSlots + from];
+  };
+
   for (uint32_t base = lb; base < le; base += 256) {
-    const bool all_done = __syncthreads_and(done);
-    flush_hits();
-    if (all_done) break;
+    if (__syncthreads_and(done)) break;  // also: every warp is through with the staged batch
     const uint32_t idx = base + tid;
     uint32_t mask = 0u, wrapm = 0u;
     if (idx < le) {
@@ -123,114 +213,64 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
         sA[tid] = gA;
         sB[tid] = gB;
         sC[tid] = p.geomC[src];
+        sPos[tid] = idx - lb;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) sF[k * 256 + tid] = p.feat[4 * (size_t)src + k];
+        for (int k = 0; k < 4; ++k) sF[k * kSlots + tid] = p.feat[4 * (size_t)src + k];
       }
     }
     sMask[tid] = (uint8_t)mask;
     const bool wrap = __syncthreads_or((mask & wrapm) != 0u) != 0;
     any_wrap |= wrap;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) sRow[warp][w][lane] = 0u;
-    pending = (int64_t)base;
-    const unsigned live = __ballot_sync(0xffffffffu, !done);
-    if (live == 0u) {  // this warp's 32 rays have saturated
-      if (lane < 8) sHitW[warp][lane] = 0u;
-      continue;
-    }
+    if (live == 0u) { ncarry = 0; continue; }  // this warp's 32 rays have saturated
     const int cnt = min(256u, le - base);
-    const int n_w = warp_compact(sMask, cnt, warp, lane, sList[warp]);
-    const uint8_t* lst = sList[warp];
-    const float4* wray = &sRay[32 * warp];
-    for (int k0 = 0; k0 < n_w; k0 += 32) {
-      // ---- phase 1: lane = entry -------------------------------------------------------------
-      uint32_t m = 0u;
-      const int k = k0 + lane;
-      if (k < n_w) {
-        const int j = lst[k];
-        const float4 gA = sA[j], gB = sB[j];
-        // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min); margins: 1% on rho, 0.02 on qf (the
-        // evaluation's exp and this log are accurate to ~1e-6)
-        float qcut = s.qform_max;
-        const float rho = gB.w;
-        if (s.alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qcut = fminf(qcut, 2.0f * __logf(rho * 1.01f / s.alpha_min) + 0.02f);
-        if (!wrap) {  // certified: no azimuth difference of this batch leaves (-pi, pi) — packed pairs, 10 issue slots per ray
-          const f32x2 m0 = pack2(gA.x, gA.y), vv = pack2(gA.z, gA.w);
-#pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            const float4 ry = wray[r];  // qx qy t t
-            float dx, dy;
-            const float qf = alpha_qform_packed(m0, vv, gB, pack2(ry.x, ry.y), pack2(ry.z, ry.w), dx, dy);
-            if (qf <= qcut) m |= 1u << r;
-          }
-        } else {
-#pragma unroll 4
-          for (int r = 0; r < 32; ++r) {
-            const float4 ry = wray[r];
-            float dx, dy;
-            const float qf = alpha_qform<true>(gA, gB, ry.x, ry.y, ry.z, dx, dy, true);
-            if (qf <= qcut) m |= 1u << r;
-          }
-        }
-        m &= live;
+    // the warp's list: what the last batch left over, then this batch's survivors (order preserved); the culled
+    // entries' hit words are zeroed on the way
+    if (lane < ncarry) lst[lane] = (uint16_t)(carry0 + lane);
+    int n = ncarry;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int j = c0 + lane;
+      const bool in = j < cnt;
+      const bool bit = in && ((sMask[j] >> warp) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      if (bit) lst[n + __popc(bal & lt)] = (uint16_t)j;
+      else if (in) {
+        const uint32_t ps = base - lb + j;
+        hitw[(size_t)(ps >> 8) * 2048u + (ps & 255u)] = 0u;
       }
-      uint32_t bits = transpose32(m, lane);  // bit kk: list entry k0 + kk may blend with MY ray
-      if (done) bits = 0u;                   // saturated in an earlier round of this batch (`live` is per batch)
-      if (out.stats) st_cand += __popc(bits);
-      // ---- phase 2: lane = ray, every lane walks its own candidates front to back ------------
-      int trips = 0;
-      while (bits != 0u) {
-        const int kk = __ffs(bits) - 1;
-        bits &= bits - 1u;
-        ++trips;
-        const int j = lst[k0 + kk];
-        const float4 gA = sA[j], gB = sB[j];
-        float dx, dy;
-        const float qf = wrap ? alpha_qform<true>(gA, gB, qx, qy, t, dx, dy, true)
-                              : alpha_qform_packed(pack2(gA.x, gA.y), pack2(gA.z, gA.w), gB, q2, t2, dx, dy);
-        AlphaEval ev;
-        if (alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) {
-          const float w = __fmul_rn(ev.alpha, T);
-          const f32x2 ww = pack2(w, w);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float4 f4 = sF[c * 256 + j];
-            acc2[2 * c] = fma2(pack2(f4.x, f4.y), ww, acc2[2 * c]);
-            acc2[2 * c + 1] = fma2(pack2(f4.z, f4.w), ww, acc2[2 * c + 1]);
-          }
-          T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
-          ++n_contrib;
-          last_idx = (int)(base - lb) + j + 1;
-          sRow[warp][j >> 5][lane] |= 1u << (j & 31);
-          const float2 c2 = sC[j];
-          const float r_rs = __fmaf_rn(c2.y, t, c2.x);
-          range_acc = __fmaf_rn(r_rs, w, range_acc);
-          if (kLos && r_rs < los_cut) los = __fadd_rn(los, ev.alpha);  // opacity in front of the measured range
-          if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
-          if (T < s.transmittance_min) { done = true; bits = 0u; }
-        }
-      }
-      if (out.stats) st_iter += (unsigned long long)__reduce_max_sync(0xffffffffu, trips);
-      __syncwarp();
+      n += __popc(bal);
     }
-    // the warp's rows of this batch -> global, their OR -> the hit bytes
-    uint32_t* rows_b = rows_tile + (size_t)((base - lb) >> 8) * 2048u + warp * 256;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const uint32_t v = sRow[warp][w][lane];
-      const uint32_t o = __reduce_or_sync(0xffffffffu, v);
-      if (o) rows_b[w * 32 + lane] = v;
-      if (lane == 0) sHitW[warp][w] = o;
-    }
+    __syncwarp();
     if (out.stats && lane == 0) {
-      atomicAdd(&out.stats[1], (unsigned long long)n_w);
+      atomicAdd(&out.stats[1], (unsigned long long)(n - ncarry));
       if (warp == 0) atomicAdd(&out.stats[0], (unsigned long long)cnt);
     }
+    const bool rw = wrap || carry_wrap;
+    int k0 = 0;
+    for (; k0 + 32 <= n && live != 0u; k0 += 32) {
+      do_round(k0, 32, rw);
+      __syncwarp();
+    }
+    // what is left moves to the carry slots (it is either all new, or nothing was processed and the old carry stays)
+    const int r = live != 0u ? n - k0 : 0;
+    if (k0 == 0) {
+      if (lane >= ncarry && lane < r) copy_slot(lst[lane], carry0 + lane);
+      carry_wrap = r > 0 && rw;
+    } else {
+      if (lane < r) copy_slot(lst[k0 + lane], carry0 + lane);
+      carry_wrap = r > 0 && wrap;
+    }
+    ncarry = r;
+    __syncwarp();
+  }
+  if (ncarry > 0 && live != 0u) {  // the list's last, partial round
+    if (lane < ncarry) lst[lane] = (uint16_t)(carry0 + lane);
+    __syncwarp();
+    do_round(0, ncarry, carry_wrap);
   }
   if (out.stats) {
-    st_cand = __reduce_add_sync(0xffffffffu, (unsigned)st_cand);
+    const unsigned tot = __reduce_add_sync(0xffffffffu, (unsigned)st_cand);
     if (lane == 0) {
-      atomicAdd(&out.stats[2], st_cand);
+      atomicAdd(&out.stats[2], (unsigned long long)tot);
       atomicAdd(&out.stats[3], st_iter);
     }
   }
@@ -262,10 +302,11 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
     out.n_contrib[pix] = n_contrib;
     out.last_idx[pix] = last_idx;
   }
-  __syncthreads();
-  flush_hits();  // the last batch of a list that ended before every ray saturated
-  if (tid == 0) out.tile_wrap[tile] = any_wrap ? 1 : 0;
+  if (tid == 0) out.tile_wrap[tile] = any_wrap ? 1 : 0;  // CTA-uniform: the backward skips the wrap elsewhere
 }
+
+constexpr size_t kLidarFwdSmem = sizeof(float4) * (2 * kSlots + 4 * kSlots + 256) + sizeof(float2) * kSlots +
+                                 sizeof(uint32_t) * kSlots + sizeof(uint16_t) * 8 * kListCap + 256;
 
 size_t lidar_hit_rows_words(int64_t n_isect, int64_t n_tiles) { return (size_t)((n_isect >> 8) + n_tiles + 2) * 2048u; }
 
@@ -276,14 +317,22 @@ void launch_raster_fwd_lidar(const Sensor& s, const ProjDev& p, const uint32_t* 
   if (tiles <= 0) return;
   const uint32_t* order = tile_count < 0 ? tile_order : nullptr;
   if (tile_count < 0) tile_first = 0;
+  constexpr size_t smem = kLidarFwdSmem;
+  static DeviceOnce once;
+  once.run([] {
+    cudaFuncSetAttribute(k_raster_fwd_lidar<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fwd_lidar<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fwd_lidar<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fwd_lidar<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
   if (out.los_cut && out.head_w)
-    k_raster_fwd_lidar<true, true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+    k_raster_fwd_lidar<true, true><<<tiles, 256, smem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else if (out.head_w)
-    k_raster_fwd_lidar<false, true><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+    k_raster_fwd_lidar<false, true><<<tiles, 256, smem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else if (out.los_cut)
-    k_raster_fwd_lidar<true, false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+    k_raster_fwd_lidar<true, false><<<tiles, 256, smem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
   else
-    k_raster_fwd_lidar<false, false><<<tiles, 256, 0, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
+    k_raster_fwd_lidar<false, false><<<tiles, 256, smem, st>>>(s, p, vals, tile_begin, tile_end, rays, ray_begin, ray_end, order, tile_first, out);
 }
 
 }  // namespace sb
