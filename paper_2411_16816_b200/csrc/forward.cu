@@ -152,9 +152,10 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     if (los_on && inside) los_cut = out.los_cut[pix];
     bool med_found = false;
     int n_contrib = 0, last_idx = 0;
-    float acc[kChannels];
+    f32x2 acc2[kChannels / 2];  // the 16 blended channels as packed pairs (FFMA2: two IEEE fmas per issue slot)
 #pragma unroll
-    for (int k = 0; k < kChannels; ++k) acc[k] = 0.0f;
+    for (int k = 0; k < kChannels / 2; ++k) acc2[k] = pack2(0.0f, 0.0f);
+    const f32x2 q2 = pack2(qx, qy), t2 = pack2(t, t);
     bool done = !inside;
     __syncthreads();  // patch boxes visible
 
@@ -247,13 +248,12 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       }
       auto blend = [&](int j, const AlphaEval& ev) {
         const float w = __fmul_rn(ev.alpha, T);
+        const f32x2 ww = pack2(w, w);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const float4 f4 = sF[4 * j + c];
-          acc[4 * c] = __fmaf_rn(f4.x, w, acc[4 * c]);
-          acc[4 * c + 1] = __fmaf_rn(f4.y, w, acc[4 * c + 1]);
-          acc[4 * c + 2] = __fmaf_rn(f4.z, w, acc[4 * c + 2]);
-          acc[4 * c + 3] = __fmaf_rn(f4.w, w, acc[4 * c + 3]);
+          acc2[2 * c] = fma2(pack2(f4.x, f4.y), ww, acc2[2 * c]);
+          acc2[2 * c + 1] = fma2(pack2(f4.z, f4.w), ww, acc2[2 * c + 1]);
         }
         T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
         ++n_contrib;
@@ -275,8 +275,11 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         for (int k = 0; k < n_w; ++k) {
           if ((k & 3) == 0 && __all_sync(0xffffffffu, done)) break;
           const int j = lst[k];
+          const float4 gA = sA[j], gB = sB[j];
+          float dx, dy;
+          const float qf = alpha_qform_packed(pack2(gA.x, gA.y), pack2(gA.z, gA.w), gB, q2, t2, dx, dy);  // same operations, 7 issue slots
           AlphaEval ev;
-          if (!done && evaluate_alpha<false>(sA[j], sB[j], qx, qy, t, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j, ev);
+          if (!done && alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j, ev);
         }
       } else {
         // the lidar kernel is latency-bound (wrap + fewer resident warps' worth of work per tile): two entries per
@@ -301,6 +304,9 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     }
 
     if (inside) {
+      float acc[kChannels];
+#pragma unroll
+      for (int k = 0; k < kChannels / 2; ++k) unpack2(acc2[k], acc[2 * k], acc[2 * k + 1]);
       const float A = __fsub_rn(1.0f, T);
       if (!kCamera) {
         acc[13] = (A > 1e-6f) ? __fdiv_rn(range_acc, A) : range_acc;

@@ -148,29 +148,57 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
   // the conic / velocity factors are applied once per entry after the join.
   constexpr int kGeo = 8;
   float m[kGeo];  // S0 Sx Sy Sxx Sxy Syy Stx Sty
-#pragma unroll
-  for (int c = 0; c < kGeo; ++c) m[c] = 0.0f;
   const int row = e * kPanelStride;
   // (visiting only the queries that blended the entry — a divergent loop over a saved ballot — was measured: 2% faster
   // for the lidar, 4% slower for the camera, whose entries are blended by a third of the lanes; the dense loop stays)
+  if (kCamera || !wrap) {
+    // packed pairs (FFMA2 / FMUL2 / FADD2: two fp32 operations per issue slot): 9 issue slots per pair instead of 14
+    const f32x2 m0 = pack2(gA.x, gA.y), vv = pack2(gA.z, gA.w);
+    f32x2 sxy = pack2(0.0f, 0.0f), sq = sxy, st = sxy;  // (Sx, Sy), (Sxx, Syy), (Stx, Sty)
+    float s0 = 0.0f, sxy_c = 0.0f;
 #pragma unroll 4
-  for (int pp = 0; pp < E; ++pp) {  // 32 / (32 / E) queries per lane
-    const int q = g * E + pp;
-    const float gs = ws.gs[row + q];
-    const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);  // qx qy t g_D
-    const float t = q0.z;
-    float dx = q0.x - fmaf(gA.z, t, gA.x);
-    if (!kCamera && wrap) dx = wrap_pi(dx);
-    const float dy = q0.y - fmaf(gA.w, t, gA.y);
-    const float a = gs * dx, b = gs * dy;
-    m[0] += gs;
-    m[1] += a;
-    m[2] += b;
-    m[3] = fmaf(a, dx, m[3]);
-    m[4] = fmaf(a, dy, m[4]);
-    m[5] = fmaf(b, dy, m[5]);
-    m[6] = fmaf(t, a, m[6]);
-    m[7] = fmaf(t, b, m[7]);
+    for (int pp = 0; pp < E; ++pp) {  // 32 / (32 / E) queries per lane
+      const int q = g * E + pp;
+      const float gs = ws.gs[row + q];
+      const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);  // qx qy t g_D
+      const f32x2 tt = pack2(q0.z, q0.z);
+      const f32x2 d = sub2(pack2(q0.x, q0.y), fma2(vv, tt, m0));  // (dx, dy)
+      const f32x2 ab = mul2(pack2(gs, gs), d);                     // (gs dx, gs dy)
+      float dxs, dys, as, bs;
+      unpack2(d, dxs, dys);
+      unpack2(ab, as, bs);
+      s0 += gs;
+      sxy = add2(sxy, ab);
+      sq = fma2(ab, d, sq);
+      sxy_c = fmaf(as, dys, sxy_c);
+      st = fma2(tt, ab, st);
+    }
+    m[0] = s0;
+    unpack2(sxy, m[1], m[2]);
+    unpack2(sq, m[3], m[5]);
+    m[4] = sxy_c;
+    unpack2(st, m[6], m[7]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < kGeo; ++c) m[c] = 0.0f;
+#pragma unroll 4
+    for (int pp = 0; pp < E; ++pp) {
+      const int q = g * E + pp;
+      const float gs = ws.gs[row + q];
+      const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);  // qx qy t g_D
+      const float t = q0.z;
+      const float dx = wrap_pi(q0.x - fmaf(gA.z, t, gA.x));
+      const float dy = q0.y - fmaf(gA.w, t, gA.y);
+      const float a = gs * dx, b = gs * dy;
+      m[0] += gs;
+      m[1] += a;
+      m[2] += b;
+      m[3] = fmaf(a, dx, m[3]);
+      m[4] = fmaf(a, dy, m[4]);
+      m[5] = fmaf(b, dy, m[5]);
+      m[6] = fmaf(t, a, m[6]);
+      m[7] = fmaf(t, b, m[7]);
+    }
   }
   // join the 32 / E lanes that worked on the same entry
   for (int o = E; o < 32; o <<= 1) {
@@ -292,6 +320,9 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       K = g_acc * T;
     }
     float S = 0.0f;  // sum_c g_c * suffix_c (+ g_D * suffix_r)
+    f32x2 g2[kChannels / 2];  // the upstream gradient as packed pairs (phase A's dot product)
+#pragma unroll
+    for (int k = 0; k < kChannels / 2; ++k) g2[k] = pack2(g_out[2 * k], g_out[2 * k + 1]);
 
     // per-query data for phase B (read there as broadcasts)
     {
@@ -368,15 +399,16 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
             T = T * inv;  // transmittance in front of this Gaussian
             w = ev.alpha * T;
             // four partial sums: a 16-long dependent FMA chain is 64 cycles of latency in a latency-bound loop
-            float d0 = 0.0f, d1 = 0.0f, d2 = 0.0f, d3 = 0.0f;
+            f32x2 d01 = pack2(0.0f, 0.0f), d23 = d01;  // packed pairs: 8 FFMA2 instead of 16 FFMA
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const float4 f4 = sF[4 * jj + c];
-              d0 = fmaf(g_out[4 * c], f4.x, d0);
-              d1 = fmaf(g_out[4 * c + 1], f4.y, d1);
-              d2 = fmaf(g_out[4 * c + 2], f4.z, d2);
-              d3 = fmaf(g_out[4 * c + 3], f4.w, d3);
+              d01 = fma2(g2[2 * c], pack2(f4.x, f4.y), d01);
+              d23 = fma2(g2[2 * c + 1], pack2(f4.z, f4.w), d23);
             }
+            float d0, d1, d2, d3;
+            unpack2(d01, d0, d1);
+            unpack2(d23, d2, d3);
             float dotgf = (d0 + d1) + (d2 + d3);
             float g_extra = 0.0f;
             if (!kCamera) {
@@ -524,6 +556,9 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
     K = g_acc * T;
   }
   float S = 0.0f;  // sum_c g_c * suffix_c + g_D * suffix_r
+  f32x2 g2[kChannels / 2];  // the upstream gradient as packed pairs (phase A's dot product)
+#pragma unroll
+  for (int k = 0; k < kChannels / 2; ++k) g2[k] = pack2(g_out[2 * k], g_out[2 * k + 1]);
   {  // per-query data for phase B (read there as broadcasts)
     float* row = &ws.px[lane * kPxStride];
     *reinterpret_cast<float4*>(row) = make_float4(qx, qy, t, g_D);
@@ -599,17 +634,15 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
       for (int k0 = 0; k0 < n_w;) {
         const int g = min(kChunk - n_slots, n_w - k0);
         // my ray's bit of each of the g entries; their records for phase B
-        uint32_t mybits = 0u;
-        for (int e = 0; e < g; ++e) {
-          const int j = sList[k0 + e];
-          mybits |= ((bstart + j < last ? myHw[j] >> lane : 0u) & 1u) << e;
-        }
+        uint32_t hw_e = 0u;
         if (lane < g) {
           const int j = sList[k0 + lane];
+          hw_e = myHw[j];
           ws.gAB[n_slots + lane] = sA[j];
           ws.gAB[kChunk + n_slots + lane] = sB[j];
           ws.src[n_slots + lane] = sSrc[j];
         }
+        uint32_t mybits = transpose32(hw_e, lane);  // bit e: my ray blended entry k0 + e
         // ---- phase A: every lane walks the entries ITS ray blended, back to front ---------------
         while (mybits != 0u) {
           const int e = __ffs(mybits) - 1;
@@ -625,15 +658,16 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));  // [1 - alpha_clamp, 1]: 1 ulp, no range fix-up needed
           T = T * inv;  // transmittance in front of this Gaussian
           const float w = ev.alpha * T;
-          float d0 = 0.0f, d1 = 0.0f, d2 = 0.0f, d3 = 0.0f;
+          f32x2 d01 = pack2(0.0f, 0.0f), d23 = d01;  // packed pairs: 8 FFMA2 instead of 16 FFMA
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const float4 f4 = sF[c * kBatch + j];
-            d0 = fmaf(g_out[4 * c], f4.x, d0);
-            d1 = fmaf(g_out[4 * c + 1], f4.y, d1);
-            d2 = fmaf(g_out[4 * c + 2], f4.z, d2);
-            d3 = fmaf(g_out[4 * c + 3], f4.w, d3);
+            d01 = fma2(g2[2 * c], pack2(f4.x, f4.y), d01);
+            d23 = fma2(g2[2 * c + 1], pack2(f4.z, f4.w), d23);
           }
+          float d0, d1, d2, d3;
+          unpack2(d01, d0, d1);
+          unpack2(d23, d2, d3);
           float dotgf = (d0 + d1) + (d2 + d3);
           const float2 c2 = sC[j];
           const float r_rs = fmaf(c2.y, t, c2.x);  // r_rs = r + v_r t

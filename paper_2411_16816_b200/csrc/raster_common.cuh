@@ -55,6 +55,17 @@ __device__ __forceinline__ float alpha_qform_packed(f32x2 m0, f32x2 v, const flo
   return __fmaf_rn(gB.x, dxx, __fmaf_rn(gB.z, dyy, __fmul_rn(gB.y, __fmul_rn(dx, dy))));
 }
 
+// 32 x 32 bit-matrix transpose across the warp: lane l passes row l, receives column l.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? (((y & ~m) >> s) | (x & ~m)) : ((x & m) | ((y & m) << s));
+  }
+  return x;
+}
+
 struct AlphaEval {
   float alpha, dx, dy, gauss;
   bool clamped;

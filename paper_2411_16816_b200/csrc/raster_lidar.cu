@@ -28,17 +28,6 @@
 
 namespace sb {
 
-// 32 x 32 bit-matrix transpose across the warp: lane l passes row l, receives column l.
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu : s == 2 ? 0x33333333u : 0x55555555u;
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
-    x = (lane & s) ? (((y & ~m) >> s) | (x & ~m)) : ((x & m) | ((y & m) << s));
-  }
-  return x;
-}
-
 constexpr int kSlots = 256 + 8 * 32;  // staged batch entries, then 32 carry slots per warp
 constexpr int kListCap = 32 + 256;
 
