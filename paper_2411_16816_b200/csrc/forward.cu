@@ -99,7 +99,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   __shared__ uint8_t sList[8][256];
   __shared__ __align__(8) uint8_t sHit[8][256];  // [warp][batch entry]: some lane of the warp blended it
   __shared__ uint8_t sSub[kCamera ? 1 : 8][4][kCamera ? 1 : 256];  // lidar, [warp][group]: the group's entries of the batch, in list order
-  __shared__ PatchBox sBox[8];
+  __shared__ PatchBox sBox[9];  // 8 warp patches + the tile's box (patch_mask_fast)
   __shared__ PatchBox sGBox[kCamera ? 1 : 8][4];                   // lidar: boxes of the 8-lane groups
   __shared__ float sHead[(!kCamera && kHead) ? 640 : 1];  // lidar head parameters (fused epilogue)
 
@@ -158,6 +158,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     const f32x2 q2 = pack2(qx, qy), t2 = pack2(t, t);
     bool done = !inside;
     __syncthreads();  // patch boxes visible
+    if (tid == 0) tile_patch_box(sBox);  // published by the first barrier of the batch loop
 
     // the hit bytes of a batch are folded and written once every warp is through it, i.e. after the next barrier
     int64_t pending = -1;  // list position of the batch whose hit bytes are still in shared memory (CTA-uniform)
@@ -180,7 +181,7 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       if (idx < le) {
         const uint32_t src = vals[idx];
         const float4 gA = p.geomA[src], gB = p.geomB[src];
-        mask = patch_mask<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min, &wrapm);
+        mask = patch_mask_fast<!kCamera>(gA, gB, sBox, s.qform_max, s.alpha_min, &wrapm);
         // SPEC.md:289 "non-finite alpha -> Gaussian skipped, counter incremented": a record with a non-finite field makes
         // every alpha it produces non-finite (skipped by the !(qf <= qform_max) / !(alpha >= alpha_min) tests); counted per
         // staged entry when the debug counters are on

@@ -54,7 +54,7 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
   uint32_t* sPos = reinterpret_cast<uint32_t*>(sC + kSlots);     // kSlots: tile-local list position
   uint16_t* sListAll = reinterpret_cast<uint16_t*>(sPos + kSlots);  // 8 x kListCap
   uint8_t* sMask = reinterpret_cast<uint8_t*>(sListAll + 8 * kListCap);  // 256
-  __shared__ PatchBox sBox[8];
+  __shared__ PatchBox sBox[9];  // 8 warp patches + the tile's box (patch_mask_fast)
   __shared__ float sHead[kHead ? 640 : 1];  // lidar head parameters (fused epilogue)
 
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
@@ -91,6 +91,7 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
   const f32x2 q2 = pack2(qx, qy), t2 = pack2(t, t);
   bool done = !inside;
   __syncthreads();  // patch boxes, rays, head parameters visible
+  if (tid == 0) tile_patch_box(sBox);  // published by the first barrier of the batch loop
 
   uint32_t* const hitw = out.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u + warp * 256;
   const float4* wray = sRay + 32 * warp;
@@ -195,7 +196,7 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
     if (idx < le) {
       const uint32_t src = vals[idx];
       const float4 gA = p.geomA[src], gB = p.geomB[src];
-      mask = patch_mask<true>(gA, gB, sBox, s.qform_max, s.alpha_min, &wrapm);
+      mask = patch_mask_fast<true>(gA, gB, sBox, s.qform_max, s.alpha_min, &wrapm);
       if (out.stats && !(fabsf(gA.x) + fabsf(gA.y) + fabsf(gA.z) + fabsf(gA.w) + fabsf(gB.x) + fabsf(gB.y) + fabsf(gB.z) + fabsf(gB.w) < 3.0e38f))
         atomicAdd(&out.stats[4], 1ull);  // SPEC.md:289 non-finite record counter
       if (mask) {
