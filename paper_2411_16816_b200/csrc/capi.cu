@@ -130,6 +130,7 @@ struct splatb200_view {
   int64_t hit_cap = 0;            // out.hit: one byte per tile-list entry
   bool multi_pass = false;        // some lidar tile holds more than 256 rays
   int64_t rows_cap = 0;           // out.hit_rows capacity in words (lidar v2 kernels)
+  int64_t list_cap = 0;           // out.hit_list capacity in entries (shared backward kernel)
   // lidar: the v2 compositing kernels (raster_lidar.cu) unless a tile needs several ray passes or SPLATB200_LIDAR_V1 is set
   bool lidar_v2() const { static const bool off = std::getenv("SPLATB200_LIDAR_V1") != nullptr; return !s.is_camera && !multi_pass && !off; }
   int64_t I_sort = 0;             // entries the radix sort handles: block-level intersections, or I
@@ -268,7 +269,7 @@ void free_view_buffers(splatb200_view* v) {
   dfree(v->vals_fine); dfree(v->proj.ccount);
   v->tile_order = nullptr;
   dfree(v->out.blend); dfree(v->out.alpha); dfree(v->out.t_final); dfree(v->out.range_blend);
-  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.hit_rows); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); for (auto*& b : v->dec_act) dfree(b); for (auto*& b : v->dec_g) dfree(b); dfree(v->dec_gext); dfree(v->d_dec_gimage); dfree(v->d_dec_gparams); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
+  dfree(v->out.n_contrib); dfree(v->out.last_idx); dfree(v->out.hit); dfree(v->out.hit_list); dfree(v->out.hit_rows); dfree(v->out.stats); dfree(v->out.tile_wrap); dfree(v->d_los_cut); dfree(v->d_los); dfree(v->d_g_los); dfree(v->d_head_w); dfree(v->d_head_y); for (auto*& b : v->dec_act) dfree(b); for (auto*& b : v->dec_g) dfree(b); dfree(v->dec_gext); dfree(v->d_dec_gimage); dfree(v->d_dec_gparams); dfree(v->d_dec_image); dfree(v->d_dec_params); dfree(v->d_dec_err); dfree(v->g_blend_stage); dfree(v->g_alpha_stage);
   dfree(v->sensor_grads); dfree(v->actor_acc); dfree(v->d_actors);
   if (v->h_total) cudaFreeHost(v->h_total);
   v->h_total = nullptr;
@@ -400,9 +401,15 @@ int ensure_isect_capacity(splatb200_view* v, int64_t n_sort, int64_t n_fine) {
   }
   if (n_fine > v->hit_cap) {
     dfree(v->out.hit);
-    const int64_t cap = n_fine + n_fine / 4 + 1024;
+    const int64_t cap = n_fine + n_fine / 4 + 2048;  // padded: the backward reads the hit bytes as aligned 4-byte words
     CU_TRY(c, cudaMalloc(&v->out.hit, (size_t)cap));
     v->hit_cap = cap;
+  }
+  if (!v->lidar_v2() && n_fine > v->list_cap) {  // (a lidar view changes kernels when a sweep brings a tile above 256 rays)
+    dfree(v->out.hit_list);
+    const int64_t cap = n_fine + n_fine / 4 + 2048;
+    CU_TRY(c, cudaMalloc(&v->out.hit_list, sizeof(uint32_t) * (size_t)cap));
+    v->list_cap = cap;
   }
   if (v->lidar_v2()) {
     const int64_t need = (int64_t)lidar_hit_rows_words(n_fine, v->n_tiles);

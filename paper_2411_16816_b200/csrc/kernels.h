@@ -47,6 +47,7 @@ struct RasterOutDev {
   int32_t* last_idx;   // P  1-based tile-local list position of the last blended Gaussian
   uint8_t* hit;        // I  per list entry: bit w set if some query of warp w of the tile's CTA blended it (saved for
                        //    the backward pass, which then revisits only those entries)
+  uint32_t* hit_list;  // I  scratch of the shared backward kernel: per tile the (position << 8 | hit byte) of its blended entries
   int hit_or;          // tiles with more than one ray pass: OR into (pre-zeroed) hit bytes instead of storing
   uint32_t* hit_rows;  // lidar v2 kernels (raster_lidar.cu), else null: the RAYS that blended each list entry, one 32-bit
                        //    word per (entry, warp of the tile's CTA) instead of the hit byte. One 2048-word block per 256

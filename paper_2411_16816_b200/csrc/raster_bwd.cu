@@ -31,6 +31,8 @@
 // (north_star (4): warp-aggregated atomics — 32 queries are folded into one RED per value). Shared-memory
 // float atomics are NOT used: on sm_100a they compile to a compare-and-swap spin loop (ATOMS.CAST.SPIN),
 // which the first version of this kernel showed to be the bottleneck (profiles/).
+#include <cstdlib>
+
 #include "kernels.h"
 #include "raster_common.cuh"
 
@@ -240,11 +242,13 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   float4* sF = sB + kBatch;                                            // 4 kBatch
   float2* sC = reinterpret_cast<float2*>(sF + 4 * kBatch);             // kBatch
   uint32_t* sSrc = reinterpret_cast<uint32_t*>(sC + kBatch);           // kBatch
-  PatchBox* sBox = reinterpret_cast<PatchBox*>(sSrc + kBatch);         // 8
+  uint32_t* sPos = sSrc + kBatch;                                      // kBatch: tile-local list position
+  PatchBox* sBox = reinterpret_cast<PatchBox*>(sPos + kBatch);         // 8
   WarpScratch* sWs = reinterpret_cast<WarpScratch*>(sBox + 8);         // 8
   uint8_t* sMask = reinterpret_cast<uint8_t*>(sWs + 8);                // kBatch
   uint8_t* sListAll = sMask + kBatch;                                  // 8 x kBatch
   __shared__ int s_max_last;
+  __shared__ int s_wcnt[8];
   __shared__ float s_dt[8];
 
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
@@ -349,43 +353,84 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     const int max_last = s_max_last;
     int n_slots = 0;  // parked entries (warp-uniform); the panel persists across batches
 
-    // hit byte and list entry of a batch are fetched one batch ahead and its records prefetched into L2: a batch's staging
-    // then starts with the record loads instead of a chain of three dependent global loads
-    uint32_t mask_next = 0u, src_next = 0u;
-    if (max_last > 0) {
-      const int b0 = ((max_last - 1) / kBatch) * kBatch;
-      if (b0 + tid < max_last) {
-        mask_next = fwd.hit[lb + b0 + tid];
-        src_next = vals[lb + b0 + tid];
+    // Compact hit list. On the north-star camera 6% of the list entries a tile's forward pass visited were blended by
+    // anyone (the rest are culled grazing footprints): walking the raw list in batches of 256 meant ~5 batches per tile
+    // — two barriers and a chain of dependent loads each — for ~16 useful entries apiece. The CTA therefore first scans
+    // its hit bytes (4 per thread and load, 1,024 per step) and writes (position << 8 | warp mask) of the entries that
+    // were blended, in list order, to its slice of fwd.hit_list; the batches below are then dense.
+    uint32_t* const hl = fwd.hit_list + lb;
+    int n_hit = 0;  // CTA-uniform
+    {
+      const uint32_t w0 = lb >> 2;  // absolute 4-byte word of the tile's first hit byte (the buffer is padded)
+      const uint32_t* hit4 = reinterpret_cast<const uint32_t*>(fwd.hit);
+      for (uint32_t wbase = w0; 4u * wbase < lb + (uint32_t)max_last; wbase += 256u) {
+        const uint32_t word = hit4[wbase + tid];
+        const int pos0 = (int)(4u * (wbase + tid)) - (int)lb;  // tile-local position of the word's first byte
+        uint32_t ent[4];
+        int c4 = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t m = (word >> (8 * i)) & 0xffu;
+          const int ps = pos0 + i;
+          if (m != 0u && ps >= 0 && ps < max_last) ent[c4++] = ((uint32_t)ps << 8) | m;
+        }
+        int incl = c4;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (lane == 31) s_wcnt[warp] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int c = s_wcnt[w];
+          if (w < warp) before += c;
+          total += c;
+        }
+        uint32_t* dst = hl + n_hit + before + (incl - c4);
+        for (int i = 0; i < c4; ++i) dst[i] = ent[i];
+        n_hit += total;
+        __syncthreads();  // s_wcnt is reused; after the last step: the list is visible to the whole CTA
       }
     }
-    for (int batch = (max_last - 1) / kBatch; batch >= 0 && max_last > 0; --batch) {
-      const int bstart = batch * kBatch;
-      const int cnt = min(kBatch, max_last - bstart);
-      // the forward pass saved, per list entry, which warps blended it: only those entries are staged and revisited
+
+    // list entry and record index of a batch are fetched one batch ahead and its records prefetched into L2: a batch's
+    // staging then starts with the record loads instead of a chain of dependent global loads
+    uint32_t ent_next = 0u, src_next = 0u;
+    const int nbat = (n_hit + kBatch - 1) / kBatch;
+    if (nbat > 0) {
+      const int i0 = (nbat - 1) * kBatch + tid;
+      if (i0 < n_hit) {
+        ent_next = hl[i0];
+        src_next = vals[lb + (ent_next >> 8)];
+      }
+    }
+    for (int batch = nbat - 1; batch >= 0; --batch) {
+      const int cnt = min(kBatch, n_hit - batch * kBatch);
       {
-        const uint32_t mask = mask_next;
+        const uint32_t ent = ent_next;
         const uint32_t src = src_next;
-        mask_next = 0u;
+        ent_next = 0u;
         if (batch > 0) {  // the batch in front of this one is always full
-          mask_next = fwd.hit[lb + bstart - kBatch + tid];
-          src_next = vals[lb + bstart - kBatch + tid];  // unconditional: two independent loads, no wait on the hit byte here
+          ent_next = hl[(batch - 1) * kBatch + tid];
+          src_next = vals[lb + (ent_next >> 8)];
         }
         if (tid < cnt) {
-          if (mask) {
-            sSrc[tid] = src;
-            sA[tid] = p.geomA[src];
-            sB[tid] = p.geomB[src];
-            if (!kCamera) sC[tid] = p.geomC[src];
+          sSrc[tid] = src;
+          sPos[tid] = ent >> 8;
+          sA[tid] = p.geomA[src];
+          sB[tid] = p.geomB[src];
+          if (!kCamera) sC[tid] = p.geomC[src];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) sF[4 * tid + k] = p.feat[4 * (size_t)src + k];
-          }
+          for (int k = 0; k < 4; ++k) sF[4 * tid + k] = p.feat[4 * (size_t)src + k];
         }
-        sMask[tid] = (uint8_t)mask;
+        sMask[tid] = tid < cnt ? (uint8_t)(ent & 0xffu) : (uint8_t)0;
       }
       __syncthreads();
 
-      if (warp_last > bstart) {
+      if ((uint32_t)warp_last > sPos[0]) {  // the batch's first entry is its closest
         const int n_w = warp_compact(sMask, cnt, warp, lane, sList);
         // park one list entry (phase A); `valid`: this lane blended it in the forward pass
         auto park = [&](int jj, bool valid, const AlphaEval& ev) {
@@ -442,13 +487,13 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           const float qf0 = alpha_qform<!kCamera>(a0, b0, qx, qy, t, dx0, dy0, wrap);
           const float qf1 = alpha_qform<!kCamera>(a1, b1, qx, qy, t, dx1, dy1, wrap);
           AlphaEval ev;
-          bool valid = (bstart + j0 < last) && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
+          bool valid = ((int)sPos[j0] < last) && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
           if (sure || __any_sync(0xffffffffu, valid)) park(j0, valid, ev);
-          valid = has1 && (bstart + j1 < last) && alpha_finish(qf1, b1.w, dx1, dy1, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
+          valid = has1 && ((int)sPos[j1] < last) && alpha_finish(qf1, b1.w, dx1, dy1, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
           if ((sure && has1) || __any_sync(0xffffffffu, valid)) park(j1, valid, ev);
         }
       }
-      if (mask_next) {  // next batch's records -> L2
+      if (batch > 0) {  // next batch's records -> L2
         prefetch_l2(&p.geomA[src_next]);
         prefetch_l2(&p.geomB[src_next]);
         prefetch_l2(&p.feat[4 * (size_t)src_next]);
@@ -721,7 +766,7 @@ void launch_raster_bwd_lidar(const Sensor& s, const ProjDev& p, const uint32_t* 
                                                                 tile_first, fwd, g_blend16, g_alpha, rg, pg);
 }
 
-constexpr size_t kBwdSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBatch * 4 + 8 * sizeof(PatchBox) +
+constexpr size_t kBwdSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBatch * 4 * 2 + 8 * sizeof(PatchBox) +
                             8 * sizeof(WarpScratch) + kBatch + 8 * kBatch;
 
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
