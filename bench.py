@@ -594,9 +594,15 @@ def run_b200(args):
     counters = load_counters() if not rig else {}
     kname = {"raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project": "k_project", "project_bwd": "k_project_bwd",
              "tile_counts": "k_tile_hist+k_tile_scan", "tile_sort": "k_radix_pass<emit>(+k_expand)", "depth_sort_scan": "k_radix_pass+k_count_scan"}
-    ckeys = {"raster_fwd": ["k_raster_fwd"], "raster_bwd": ["k_raster_bwd"], "project": ["k_project"], "project_bwd": ["k_project_bwd"],
+    ckeys = {"raster_fwd": ["k_raster_fwd", "k_raster_fwd_lidar"], "raster_bwd": ["k_raster_bwd", "k_raster_bwd_lidar"], "project": ["k_project"], "project_bwd": ["k_project_bwd"],
              "tile_counts": ["k_tile_hist", "k_tile_scan"], "tile_sort": ["k_expand"], "depth_sort_scan": ["k_radix_hist", "k_radix_pass", "k_count_scan"]}
     cand, per_kernel = [], {}
+
+    def kernel_label(stage, sensor):
+        # the lidar's single-pass views composite with their own kernel pair (raster_lidar.cu, k_raster_bwd_lidar)
+        if sensor == "lidar" and stage in ("raster_fwd", "raster_bwd") and not os.environ.get("SPLATB200_LIDAR_V1"):
+            return kname[stage] + "_lidar<lidar>"
+        return f"{kname[stage]}<{sensor}>"
     for sensor, stg, sts, camera in (("lidar", stage_l, stats_l, False), ("camera", stage_c, stats_c, True)):
         by = stage_bytes(sts, camera)
         for k, ms in stg.items():
@@ -610,10 +616,10 @@ def run_b200(args):
                 e.update({"issue_frac": cs[0]["issue_active_pct"] / 100.0 if cs[0].get("issue_active_pct") is not None else None,
                           "sm_throughput_frac": cs[0]["sm_throughput_pct"] / 100.0 if cs[0].get("sm_throughput_pct") is not None else None,
                           "warps_active_frac": cs[0]["warps_active_pct"] / 100.0 if cs[0].get("warps_active_pct") is not None else None})
-            per_kernel[f"{kname[k]}<{sensor}>"] = e
+            per_kernel[kernel_label(k, sensor)] = e
     cand.sort(reverse=True)
     ms_k, sensor_k, stage_k, bytes_k = cand[0]
-    kernel_name = kname[stage_k] + f"<{sensor_k}>"
+    kernel_name = kernel_label(stage_k, sensor_k)
     dom = per_kernel[kernel_name]
     achieved = bytes_k / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
     stage_total = sum(stage_l.values()) + n_cam * sum(stage_c.values())

@@ -81,7 +81,8 @@ def _lidar_header(l: LidarModel) -> dict:
 
 def _track_header(t: ActorTrack) -> dict:
     return {"stamps": _vec(t.stamps), "R": _vec(t.R), "t": _vec(t.t), "pose_offset": _vec(t.pose_offset), "vel_lin": _vec(t.vel_lin),
-            "vel_ang": _vec(t.vel_ang), "vel_offset": _vec(t.vel_offset), "init_velocity_from_poses": bool(t.init_velocity_from_poses)}
+            "vel_ang": _vec(t.vel_ang), "vel_offset": _vec(t.vel_offset), "init_velocity_from_poses": bool(t.init_velocity_from_poses),
+            "box_size": _vec(t.box_size)}
 
 
 def save_spz1(path, scene: Scene, cameras: Sequence[CameraModel] = (), lidars: Sequence[LidarModel] = (),
@@ -120,7 +121,8 @@ def load_spz1(path) -> dict:
             tracks = [ActorTrack(stamps=np.array(t["stamps"]), R=np.array(t["R"]), t=np.array(t["t"]),
                                  pose_offset=np.array(t["pose_offset"]), vel_lin=np.array(t["vel_lin"]),
                                  vel_ang=np.array(t["vel_ang"]), vel_offset=np.array(t["vel_offset"]),
-                                 init_velocity_from_poses=bool(t["init_velocity_from_poses"])) for t in h["actor_tracks"]]
+                                 init_velocity_from_poses=bool(t["init_velocity_from_poses"]),
+                                 box_size=np.array(t.get("box_size", [0.0, 0.0, 0.0]))) for t in h["actor_tracks"]]
             cams, embs = [], []
             for c in h["cameras"]:
                 cams.append(CameraModel(fx=c["fx"], fy=c["fy"], cx=c["cx"], cy=c["cy"], width=c["width"], height=c["height"],

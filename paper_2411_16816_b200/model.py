@@ -45,6 +45,7 @@ class ActorTrack:
     vel_ang: np.ndarray = None
     vel_offset: np.ndarray = None      # (6,)
     init_velocity_from_poses: bool = False
+    box_size: np.ndarray = None        # (3,) actor box (scene.hpp:51); not used by the rasterizer, carried through SPZ1
 
     def __post_init__(self):
         n = len(self.stamps)
@@ -55,6 +56,7 @@ class ActorTrack:
         self.vel_lin = np.zeros(3) if self.vel_lin is None else np.asarray(self.vel_lin, np.float64)
         self.vel_ang = np.zeros(3) if self.vel_ang is None else np.asarray(self.vel_ang, np.float64)
         self.vel_offset = np.zeros(6) if self.vel_offset is None else np.asarray(self.vel_offset, np.float64)
+        self.box_size = np.zeros(3) if self.box_size is None else np.asarray(self.box_size, np.float64).reshape(3)
 
 
 @dataclass

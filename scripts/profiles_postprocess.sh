@@ -30,7 +30,7 @@ python scripts/ncu_summary.py /tmp/prof_${TAG}_raw.csv > "$P/ncu_full_${TAG}.txt
 python scripts/make_counters_json.py /tmp/prof_${TAG}_raw.csv "$P/counters.json" "$P/traffic.json" > /dev/null
 ncu -i "$G/prof_${TAG}.ncu-rep" --page source --csv --print-source cuda,sass > /tmp/prof_${TAG}_src.csv
 : > "$P/ncu_source_lines_${TAG}.txt"
-for k in "k_raster_fwd<(bool)0" "k_raster_fwd<(bool)1" "k_raster_bwd<(bool)0" "k_raster_bwd<(bool)1" "k_expand" "k_radix_pass<(int)2"; do
+for k in "k_raster_fwd_lidar" "k_raster_fwd<(bool)1" "k_raster_bwd_lidar" "k_raster_bwd<(bool)1" "k_expand" "k_radix_pass<(int)2"; do
   echo "#### $k" >> "$P/ncu_source_lines_${TAG}.txt"
   python scripts/ncu_lines.py /tmp/prof_${TAG}_src.csv "$k" 25 >> "$P/ncu_source_lines_${TAG}.txt"
 done

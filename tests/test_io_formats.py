@@ -17,6 +17,8 @@ def test_spz1_round_trip_is_bit_exact(tmp_path):
     cams = [synth.make_camera(width=320, height=192, yaw=0.3), synth.make_camera()]
     lids = [synth.lidar128()]
     rng = np.random.default_rng(0)
+    if sc.tracks:
+        sc.tracks[0].box_size = np.array([4.5, 1.9, 1.6])     # ActorTrack::box_size (scene.hpp:51) travels with the track
     weights = {"conv_decoder": rng.normal(size=46438).astype(np.float32), "lidar_head": rng.normal(size=610).astype(np.float32)}
     embs = [rng.normal(size=8).astype(np.float32) for _ in cams]
     p = tmp_path / "scene.spz1"
@@ -28,7 +30,7 @@ def test_spz1_round_trip_is_bit_exact(tmp_path):
         assert a.shape == b.shape and a.dtype == b.dtype and np.array_equal(_bits(a), _bits(b)), k
     assert len(g.tracks) == 3
     for a, b in zip(sc.tracks, g.tracks):
-        for k in ("stamps", "R", "t", "pose_offset", "vel_lin", "vel_ang", "vel_offset"):
+        for k in ("stamps", "R", "t", "pose_offset", "vel_lin", "vel_ang", "vel_offset", "box_size"):
             assert np.array_equal(getattr(a, k), getattr(b, k)), k      # doubles through JSON repr: exact
         assert a.init_velocity_from_poses == b.init_velocity_from_poses
     for a, b in zip(cams, got["cameras"]):
