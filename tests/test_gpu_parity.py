@@ -421,6 +421,55 @@ def test_more_than_256_rays_per_tile(ctx, op):
     grads_gate(ctx, og, lid, sc.n, what="multipass ")
 
 
+_LIDAR_PAIR_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+from paper_2411_16816_b200 import api, synth
+from paper_2411_16816_b200.model import RasterSettings
+sc = synth.make_scene(20000, seed=21, r_max=50.0, scale_mean=0.08)
+lid = synth.lidar128()
+lid.vel_lin = np.array([8.0, 1.0, 0.0])
+rays = synth.grid_rays(lid)
+ctx = api.Context(0)
+ctx.upload_scene(sc)
+v = ctx.render_lidar(lid, rays, RasterSettings())
+gb, ga = synth.upstream(v.P, seed=21)
+gb[:, 14:] = 0
+ctx.zero_grads()
+v.backward(gb, ga)
+g = ctx.grads()
+np.savez(sys.argv[1], blend=v.array("blend"), alpha=v.array("alpha"), n_contrib=v.array("n_contrib"), last_idx=v.array("last_idx"),
+         **{k: g[k] for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_feature")})
+"""
+
+
+@pytest.mark.gpu
+def test_lidar_kernel_pairs_agree(tmp_path):
+    """The lidar's own compositing kernels (raster_lidar.cu + k_raster_bwd_lidar: lane = entry prefilter, bit transpose,
+    lane = ray walk; default for tiles of at most 256 rays) against the shared kernels (SPLATB200_LIDAR_V1=1), each in
+    its own process: every forward output bit-identical (same per-ray blending order, same IEEE operations), gradients
+    equal up to the order of the atomic additions."""
+    import os
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tag, env in (("v2", {}), ("v1", {"SPLATB200_LIDAR_V1": "1"})):
+        out = str(tmp_path / f"{tag}.npz")
+        e = dict(os.environ, **env)
+        e.pop("SPLATB200_LIDAR_V1", None) if not env else None
+        subprocess.run([_sys.executable, "-c", _LIDAR_PAIR_SCRIPT, out], cwd=root, env=e, check=True, timeout=600)
+        outs.append(np.load(out))
+    a, b = outs
+    assert a["n_contrib"].sum() > 10000
+    for k in ("blend", "alpha", "n_contrib", "last_idx"):
+        assert np.array_equal(a[k], b[k]), f"{k}: the two kernel pairs differ"
+    for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_feature"):
+        scale = np.abs(b[k]).max()
+        assert np.abs(a[k].astype(np.float64) - b[k]).max() <= 1e-4 * scale, k
+
+
 def test_multi_sensor_accumulation_and_reuse(ctx, op):
     """Several sensors over one scene accumulate into one SceneParamGrads; views are reusable across frames."""
     import grad_gate
