@@ -49,13 +49,16 @@ constexpr int kPanelStride = 33;  // dL/dsigma panel: read by the per-entry loop
 constexpr int kWStride = 36;      // w panel: read as the A fragments of the channel product (conflict-free: 4 gid + tig)
 constexpr int kPxStride = 24;     // qx qy t g_D | G[16] | pad (24 tig + gid: conflict-free B fragments)
 
-struct WarpScratch {
-  float w[kChunk * kWStride];
-  float gs[kChunk * kPanelStride];
+template <int kC>
+struct WarpScratchT {
+  float w[kC * kWStride];
+  float gs[kC * kPanelStride];
   float px[32 * kPxStride];
-  float4 gAB[2 * kChunk];  // the parked Gaussians' records: geomA | geomB
-  uint32_t src[kChunk];
+  float4 gAB[2 * kC];  // the parked Gaussians' records: geomA | geomB
+  uint32_t src[kC];
 };
+using WarpScratch = WarpScratchT<kChunk>;
+constexpr int kChunkS = 8;  // panel capacity of the shared kernel (k_raster_bwd): 8 entries -> 75.8 KB per CTA, 3 CTAs per SM
 
 // D += A B for one m16n8k8 tf32 tile (A row-major 16 x 8, B column-major 8 x 8, fp32 accumulators).
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -229,8 +232,144 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
   __syncwarp();
 }
 
+// Phase B for the n <= 8 entries of an 8-entry panel. The channel product is transposed — D[c][e] = sum_q G[q][c] w[e][q],
+// M = 16 channels, N = 8 entries, K = 32 queries — so that an 8-entry panel fills the m16n8k8 tile: 12 split-tf32 MMAs
+// and 12 accumulator registers (the 16-entry form: 24 and 24; half of its A rows would be empty here). Raw moments: 4
+// lanes per entry, 8 queries each.
+template <bool kCamera>
+__device__ __forceinline__ void reduce_panel8(const WarpScratchT<kChunkS>& ws, int n, int lane, int d_f, const RasterGradDev& rg,
+                                              const ParamGradDev& pg, float& dt_local, bool wrap) {
+  {
+    const int gid = lane >> 2, tig = lane & 3;
+    float d[4], dlh[4], dhl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = dlh[k] = dhl[k] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int q = ks * 8 + tig;
+      // A[m = channel][k = query] = G[q][c]: rows gid, gid + 8; columns tig, tig + 4 (banks 24 tig + gid: conflict-free)
+      const float* ap = &ws.px[q * kPxStride + 4 + gid];
+      const float af[4] = {ap[0], ap[8], ap[4 * kPxStride], ap[4 * kPxStride + 8]};
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ah[k] = __float_as_uint(af[k]) & kTf32Mask;
+        al[k] = __float_as_uint(af[k] - __uint_as_float(ah[k])) & kTf32Mask;
+      }
+      // B[k = query][n = entry] = w[e][q]: rows tig, tig + 4; column gid (banks 4 gid + tig: conflict-free)
+      const float bf0 = ws.w[gid * kWStride + q], bf1 = ws.w[gid * kWStride + q + 4];
+      const uint32_t bh0 = __float_as_uint(bf0) & kTf32Mask, bh1 = __float_as_uint(bf1) & kTf32Mask;
+      const uint32_t bl0 = __float_as_uint(bf0 - __uint_as_float(bh0)) & kTf32Mask;
+      const uint32_t bl1 = __float_as_uint(bf1 - __uint_as_float(bh1)) & kTf32Mask;
+      mma_tf32(dlh, al, bh0, bh1);
+      mma_tf32(dhl, ah, bl0, bl1);
+      mma_tf32(d, ah, bh0, bh1);
+    }
+    // lane holds channels gid, gid + 8 of entries 2 tig, 2 tig + 1: one RED per (warp, Gaussian, value)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int e = 2 * tig + j;
+      if (e < n) {
+        const size_t src = ws.src[e];
+        float* f0 = kCamera ? pg.d_color + 3 * src : pg.d_feature + (size_t)d_f * src;
+        float* f1 = pg.d_feature + (size_t)d_f * src - (kCamera ? 3 : 0);
+        float* r0 = rg.g + kRasterGradStride * src - 16;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = gid + 8 * h;
+          const float v = d[2 * h + j] + dlh[2 * h + j] + dhl[2 * h + j];
+          if (v != 0.0f) {  // channels >= the sensor's are exactly zero
+            float* dst;
+            if (kCamera) dst = c < 3 ? f0 + c : f1 + c;
+            else dst = c < 13 ? f1 + c : (c == 13 ? r0 + 25 : r0 + 23);  // 13: d/d range, 14: d/d v_r
+            atomicAdd(dst, v);
+          }
+        }
+      }
+    }
+  }
+  const int e = lane & 7, g = lane >> 3;
+  const bool active = e < n;
+  const float4 gA = ws.gAB[active ? e : 0], gB = ws.gAB[kChunkS + (active ? e : 0)];
+  float m[8];  // S0 Sx Sy Sxx Sxy Syy Stx Sty
+  const int row = e * kPanelStride;
+  if (kCamera || !wrap) {
+    const f32x2 m0 = pack2(gA.x, gA.y), vv = pack2(gA.z, gA.w);
+    f32x2 sxy = pack2(0.0f, 0.0f), sq = sxy, st = sxy;  // (Sx, Sy), (Sxx, Syy), (Stx, Sty)
+    float s0 = 0.0f, sxy_c = 0.0f;
+#pragma unroll 4
+    for (int pp = 0; pp < 8; ++pp) {
+      const int q = g * 8 + pp;
+      const float gs = ws.gs[row + q];
+      const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);  // qx qy t g_D
+      const f32x2 tt = pack2(q0.z, q0.z);
+      const f32x2 dd = sub2(pack2(q0.x, q0.y), fma2(vv, tt, m0));  // (dx, dy)
+      const f32x2 ab = mul2(pack2(gs, gs), dd);                     // (gs dx, gs dy)
+      float dxs, dys, as, bs;
+      unpack2(dd, dxs, dys);
+      unpack2(ab, as, bs);
+      s0 += gs;
+      sxy = add2(sxy, ab);
+      sq = fma2(ab, dd, sq);
+      sxy_c = fmaf(as, dys, sxy_c);
+      st = fma2(tt, ab, st);
+    }
+    m[0] = s0;
+    unpack2(sxy, m[1], m[2]);
+    unpack2(sq, m[3], m[5]);
+    m[4] = sxy_c;
+    unpack2(st, m[6], m[7]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) m[c] = 0.0f;
+#pragma unroll 4
+    for (int pp = 0; pp < 8; ++pp) {
+      const int q = g * 8 + pp;
+      const float gs = ws.gs[row + q];
+      const float4 q0 = *reinterpret_cast<const float4*>(&ws.px[q * kPxStride]);
+      const float t = q0.z;
+      const float dx = wrap_pi(q0.x - fmaf(gA.z, t, gA.x));
+      const float dy = q0.y - fmaf(gA.w, t, gA.y);
+      const float a = gs * dx, b = gs * dy;
+      m[0] += gs;
+      m[1] += a;
+      m[2] += b;
+      m[3] = fmaf(a, dx, m[3]);
+      m[4] = fmaf(a, dy, m[4]);
+      m[5] = fmaf(b, dy, m[5]);
+      m[6] = fmaf(t, a, m[6]);
+      m[7] = fmaf(t, b, m[7]);
+    }
+  }
+#pragma unroll
+  for (int o = 8; o < 32; o <<= 1) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
+  }
+  if (active && g == 0) {  // one RED per (warp, Gaussian, value)
+    const float hb = 0.5f * gB.y;
+    const float gx = fmaf(hb, m[2], gB.x * m[1]), gy = fmaf(hb, m[1], gB.z * m[2]);     // sum of dL/dDelta
+    const float gtx = fmaf(hb, m[7], gB.x * m[6]), gty = fmaf(hb, m[6], gB.z * m[7]);   // sum of t dL/dDelta
+    float acc[8];
+    acc[0] = 0.5f * m[3];  // dL/dconic
+    acc[1] = 0.5f * m[4];
+    acc[2] = 0.5f * m[5];
+    acc[3] = -gx;  // dL/dmean2d
+    acc[4] = -gy;
+    acc[5] = -gtx;  // dL/dvelocity (first two components)
+    acc[6] = -gty;
+    acc[7] = __fdividef(-m[0], gB.w);  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
+    if (kCamera) dt_local -= fmaf(gA.z, gx, gA.w * gy);  // SensorGrads.d_time_offset
+    float* r0 = rg.g + kRasterGradStride * (size_t)ws.src[e];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (acc[c] != 0.0f) atomicAdd(r0 + (c < 7 ? c : 8), acc[c]);  // slots 0-6, rho at 8 (7: v_r, 9: range)
+  }
+  __syncwarp();
+}
+
 template <bool kCamera, bool kLos = false>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
              const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
@@ -244,7 +383,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   uint32_t* sSrc = reinterpret_cast<uint32_t*>(sC + kBatch);           // kBatch
   uint32_t* sPos = sSrc + kBatch;                                      // kBatch: tile-local list position
   PatchBox* sBox = reinterpret_cast<PatchBox*>(sPos + kBatch);         // 8
-  WarpScratch* sWs = reinterpret_cast<WarpScratch*>(sBox + 8);         // 8
+  WarpScratchT<kChunkS>* sWs = reinterpret_cast<WarpScratchT<kChunkS>*>(sBox + 8);         // 8
   uint8_t* sMask = reinterpret_cast<uint8_t*>(sWs + 8);                // kBatch
   uint8_t* sListAll = sMask + kBatch;                                  // 8 x kBatch
   __shared__ int s_max_last;
@@ -255,7 +394,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   uint8_t* sList = sListAll + kBatch * warp;
-  WarpScratch& ws = sWs[warp];
+  WarpScratchT<kChunkS>& ws = sWs[warp];
   const uint32_t lb = tile_begin[tile], le = tile_end[tile];
   if (le <= lb) return;
   // lidar: the forward pass certified, per tile, whether any azimuth difference can leave (-pi, pi) (raster_common.cuh)
@@ -469,11 +608,11 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           ws.w[n_slots * kWStride + lane] = w;
           ws.gs[n_slots * kPanelStride + lane] = g_sigma;
           // the record travels with the entry: lanes 0 / 1 copy geomA / geomB (sB follows sA), lane 2 the index
-          if (lane < 2) ws.gAB[lane * kChunk + n_slots] = sA[lane * kBatch + jj];
+          if (lane < 2) ws.gAB[lane * kChunkS + n_slots] = sA[lane * kBatch + jj];
           else if (lane == 2) ws.src[n_slots] = sSrc[jj];
-          if (++n_slots == kChunk) {
+          if (++n_slots == kChunkS) {
             __syncwarp();
-            reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
+            reduce_panel8<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
             n_slots = 0;
           }
         };
@@ -503,7 +642,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     }
     if (n_slots > 0) {  // drain what is left of this pass
       __syncwarp();
-      reduce_panel<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
+      reduce_panel8<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
       n_slots = 0;
     }
     __syncthreads();  // patch boxes / staging / per-query rows are reused by the next ray pass
@@ -767,7 +906,7 @@ void launch_raster_bwd_lidar(const Sensor& s, const ProjDev& p, const uint32_t* 
 }
 
 constexpr size_t kBwdSmem = kBatch * 16 * 2 + 4 * kBatch * 16 + kBatch * 8 + kBatch * 4 * 2 + 8 * sizeof(PatchBox) +
-                            8 * sizeof(WarpScratch) + kBatch + 8 * kBatch;
+                            8 * sizeof(WarpScratchT<kChunkS>) + kBatch + 8 * kBatch;
 
 void launch_raster_bwd(const Sensor& s, const ProjDev& p, const uint32_t* vals, const uint32_t* tile_begin,
                        const uint32_t* tile_end, const float4* rays, const int64_t* ray_begin, const int64_t* ray_end,
