@@ -12,6 +12,8 @@
 
 namespace sb {
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // projection.hpp:294-318
 __device__ __forceinline__ void spherical_jacobian_point_grad(const float* p, const float* gJ, float* o) {
   const float x = p[0], y = p[1], z = p[2];
@@ -143,6 +145,19 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
   const int total = s_total;
   for (int slot = tid; slot < total; slot += 256) {
   const int64_t i = base + s_list[slot];
+  if (slot + 256 < total) {
+    // the kernel is bound by its own load latency (ncu: long-scoreboard stalls at the first use of every parameter row):
+    // the next Gaussian's rows are pulled into L1 while this one is computed
+    const int64_t in = base + s_list[slot + 256];
+    prefetch_l1(sc.mean + 3 * in);
+    prefetch_l1(sc.scale_log + 3 * in);
+    prefetch_l1(sc.quat + 4 * in);
+    prefetch_l1(sc.opacity_logit + in);
+    if (kMode == kFused) {
+      prefetch_l1(rg.g + kRasterGradStride * in);
+      prefetch_l1(rg.g + kRasterGradStride * in + 8);
+    }
+  }
   {
     Fwd f;
     compose_one(sc, i, f);
