@@ -468,7 +468,12 @@ def run_b200(args):
         def step_e2e():
             """the reference-facing call with HOST buffers: GaussianSet up, rendered images down, upstream
             gradients up, SceneParamGrads down — all inside the timed region, from/to pinned memory"""
-            ctx.upload_scene(pscene)
+            # geometry first, colour / features behind it on their own copy stream: projection + binning of both sensors
+            # run while the appearance arrays are still on the link (same bytes, all inside the timed region)
+            if os.environ.get("SPLATB200_SYNC_UPLOAD"):
+                ctx.upload_scene(pscene)        # A/B: the blocking upload
+            else:
+                ctx.upload_scene_async(pscene)
             ctx.zero_grads()
             # every copy is inside the timed region; the library's copy streams overlap a view's transfers with the
             # other view's kernels. A view's upstream gradients are uploaded only after its outputs have been downloaded

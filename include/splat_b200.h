@@ -144,6 +144,15 @@ int splatb200_allreduce_grads(splatb200_ctx* ctx);
 int splatb200_scene_upload(splatb200_ctx* ctx, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
                            const float* quat, const float* opacity_logit, const float* color, const float* feature,
                            const int32_t* actor_id);
+/* The per-iteration upload without the wait (a resident scene of the same shape; anything else takes the blocking path).
+ * Geometry first: mean, scale_log, quat, opacity_logit and actor_id (48 B per Gaussian) go up on the ctx stream, colour
+ * and features (12 + 4 d_f B) follow behind them on a copy stream of their own. A view's projection, depth sort and tile
+ * binning need the geometry only and run while the appearance arrays are still in flight; its forward waits for them
+ * in front of the compositing kernel. The host arrays must stay valid (and should be pinned) until the next
+ * splatb200_ctx_sync. Same GaussianSet fields as scene.hpp:137-168. */
+int splatb200_scene_upload_async(splatb200_ctx* ctx, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
+                                 const float* quat, const float* opacity_logit, const float* color, const float* feature,
+                                 const int32_t* actor_id);
 /* zero-copy variant: DEVICE pointers owned by the caller (e.g. optimiser state); must outlive use */
 int splatb200_scene_bind_device(splatb200_ctx* ctx, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
                                 const float* quat, const float* opacity_logit, const float* color,

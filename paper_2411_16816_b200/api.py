@@ -28,7 +28,7 @@ INT_ARRAYS = {"raster_stats", "hit_bits", "source_index", "rect", "isect_tile", 
 SYMBOLS = [
     "splatb200_ctx_create", "splatb200_ctx_destroy", "splatb200_last_error", "splatb200_ctx_sync",
     "splatb200_ctx_launch_count", "splatb200_ctx_library_launch_count",
-    "splatb200_debug_depth_sort", "splatb200_assign_points", "splatb200_ctx_set_profiling", "splatb200_ctx_set_view_streams", "splatb200_ctx_join", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_bind_device",
+    "splatb200_debug_depth_sort", "splatb200_assign_points", "splatb200_ctx_set_profiling", "splatb200_ctx_set_view_streams", "splatb200_ctx_join", "splatb200_view_stage_ms", "splatb200_scene_upload", "splatb200_scene_upload_async", "splatb200_scene_bind_device",
     "splatb200_scene_set_tracks", "splatb200_scene_actor_velocity", "splatb200_grads_zero", "splatb200_grads_size",
     "splatb200_grads_device_ptr", "splatb200_grads_bind_device", "splatb200_grads_download",
     "splatb200_grads_download_actor", "splatb200_view_create_camera", "splatb200_view_create_lidar",
@@ -159,6 +159,7 @@ def lib():
         L.splatb200_grads_download_actor.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.splatb200_scene_actor_velocity.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
         L.splatb200_scene_upload.argtypes = [C.c_void_p, C.c_int64, C.c_int32] + [C.c_void_p] * 7
+        L.splatb200_scene_upload_async.argtypes = [C.c_void_p, C.c_int64, C.c_int32] + [C.c_void_p] * 7
         L.splatb200_scene_bind_device.argtypes = [C.c_void_p, C.c_int64, C.c_int32] + [C.c_void_p] * 7 + [C.c_int32]
         L.splatb200_scene_set_tracks.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
         L.splatb200_view_create_camera.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -410,6 +411,19 @@ class Context:
         self._check(self.L.splatb200_scene_upload(self.h, s.n, s.d_f, _p(s.mean), _p(s.scale_log), _p(s.quat),
                                                   _p(s.opacity_logit), _p(s.color), _p(s.feature), _p(s.actor_id)))
         self.set_tracks(scene.tracks)
+
+    def upload_scene_async(self, scene: Scene):
+        """Geometry-first upload without the wait (splatb200_scene_upload_async): `scene` must already hold float32 /
+        int32 arrays (pinned for a truly asynchronous copy) that stay alive and unchanged until the next sync(); tracks
+        are not touched."""
+        for a in (scene.mean, scene.scale_log, scene.quat, scene.opacity_logit, scene.color, scene.feature):
+            if a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError("upload_scene_async needs contiguous float32 arrays")
+        if scene.actor_id.dtype != np.int32:
+            raise ValueError("upload_scene_async needs an int32 actor_id array")
+        self._keep_scene = scene
+        self._check(self.L.splatb200_scene_upload_async(self.h, scene.n, scene.d_f, _p(scene.mean), _p(scene.scale_log), _p(scene.quat),
+                                                        _p(scene.opacity_logit), _p(scene.color), _p(scene.feature), _p(scene.actor_id)))
 
     def bind_scene_device(self, n, d_f, mean, scale_log, quat, opacity_logit, color, feature, actor_id, max_actor_id=0):
         """Zero-copy: arguments are raw device addresses (e.g. torch.Tensor.data_ptr())."""

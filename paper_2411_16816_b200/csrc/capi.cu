@@ -43,6 +43,11 @@ struct splatb200_ctx {
   int64_t lib_launches = 0;  // library kernels on the hot path (none since the radix sort is hand-written)
   bool profiling = false;
   bool view_streams = false;   // views run forward / backward on their own streams (splatb200_ctx_set_view_streams)
+  // geometry-first upload (splatb200_scene_upload_async): colour / features follow on their own copy stream; a view's
+  // forward waits for them only in front of its compositing kernel
+  cudaStream_t s_app = nullptr;
+  cudaEvent_t ev_geo = nullptr, ev_app = nullptr;
+  bool app_pending = false;
   int decoder_precise = 0;     // ConvDecoder convolutions in split-tf32 (three passes: fp32 accuracy) instead of plain tf32
 
   // scene
@@ -330,6 +335,10 @@ void join_view(splatb200_view* v) {
 void join_all(splatb200_ctx* c) {
   for (auto* v : c->views) join_view(v);
 }
+// ctx-stream consumers of the colour / feature arrays order themselves after a geometry-first upload still in flight
+void wait_appearance(splatb200_ctx* c) {
+  if (c->app_pending) cudaStreamWaitEvent(c->stream, c->ev_app, 0);
+}
 
 struct StageTimer {
   splatb200_view* v;
@@ -517,6 +526,12 @@ extern "C" void splatb200_ctx_destroy(splatb200_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->s_app) {
+    cudaStreamSynchronize(c->s_app);
+    cudaStreamDestroy(c->s_app);
+    cudaEventDestroy(c->ev_geo);
+    cudaEventDestroy(c->ev_app);
+  }
   while (!c->views.empty()) splatb200_view_destroy(c->views.back());
   splatb200_ctx_comm_destroy(c);
   free_scene(c);
@@ -528,6 +543,10 @@ extern "C" const char* splatb200_last_error(const splatb200_ctx* c) { return c ?
 extern "C" int splatb200_ctx_sync(splatb200_ctx* c) {
   join_all(c);
   CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->s_app) {
+    CU_TRY(c, cudaStreamSynchronize(c->s_app));
+    c->app_pending = false;
+  }
   for (auto* v : c->views) {  // copy streams of the overlapped host-buffer calls
     if (v->s_h2d) CU_TRY(c, cudaStreamSynchronize(v->s_h2d));
     if (v->s_d2h) CU_TRY(c, cudaStreamSynchronize(v->s_d2h));
@@ -575,6 +594,10 @@ extern "C" int splatb200_scene_upload(splatb200_ctx* c, int64_t n, int32_t d_f, 
   join_all(c);
   if (n < 0 || d_f < 0 || d_f > 13) return c->fail(SPLATB200_EINVAL, "scene_upload: need n >= 0 and 0 <= d_f <= 13");
   CU_TRY(c, cudaSetDevice(c->device));
+  if (c->s_app) {  // an asynchronous upload still in flight writes the same buffers
+    CU_TRY(c, cudaStreamSynchronize(c->s_app));
+    c->app_pending = false;
+  }
   // Same shape as the resident scene (the per-iteration case: parameters change, sizes do not): keep the
   // device buffers and the SceneParamGrads buffer (owned or bound), only refresh the contents.
   const bool reuse = c->owns_scene && c->n == n && c->d_f == d_f && c->grads;
@@ -610,6 +633,43 @@ extern "C" int splatb200_scene_upload(splatb200_ctx* c, int64_t n, int32_t d_f, 
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   for (auto* v : c->views) v->stage = 0;
   return reuse ? SPLATB200_OK : alloc_grads(c);
+}
+
+extern "C" int splatb200_scene_upload_async(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean, const float* scale_log,
+                                            const float* quat, const float* opacity_logit, const float* color,
+                                            const float* feature, const int32_t* actor_id) {
+  // only the per-iteration case (same shape as the resident scene, buffers owned): anything else takes the blocking path
+  if (!(c->owns_scene && c->n == n && c->d_f == d_f && c->grads) || n == 0)
+    return splatb200_scene_upload(c, n, d_f, mean, scale_log, quat, opacity_logit, color, feature, actor_id);
+  join_all(c);
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (!c->s_app) {
+    CU_TRY(c, cudaStreamCreateWithFlags(&c->s_app, cudaStreamNonBlocking));
+    CU_TRY(c, cudaEventCreateWithFlags(&c->ev_geo, cudaEventDisableTiming));
+    CU_TRY(c, cudaEventCreateWithFlags(&c->ev_app, cudaEventDisableTiming));
+  }
+  auto up = [&](void* dst, const void* src, size_t bytes, cudaStream_t st) { return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st); };
+  const size_t fn = sizeof(float) * (size_t)n;
+  // geometry (48 B per Gaussian) on the ctx stream: everything up to the tile lists needs nothing else
+  CU_TRY(c, up(c->mean, mean, 3 * fn, c->stream));
+  CU_TRY(c, up(c->scale_log, scale_log, 3 * fn, c->stream));
+  CU_TRY(c, up(c->quat, quat, 4 * fn, c->stream));
+  CU_TRY(c, up(c->opacity_logit, opacity_logit, fn, c->stream));
+  CU_TRY(c, up(c->actor_id, actor_id, sizeof(int32_t) * (size_t)n, c->stream));
+  CU_TRY(c, cudaEventRecord(c->ev_geo, c->stream));
+  // appearance (12 + 4 d_f B per Gaussian) behind it on the link, but on its own stream: the views' projection and
+  // binning kernels run while it is in flight
+  CU_TRY(c, cudaStreamWaitEvent(c->s_app, c->ev_geo, 0));
+  CU_TRY(c, up(c->color, color, 3 * fn, c->s_app));
+  if (d_f) CU_TRY(c, up(c->feature, feature, (size_t)d_f * fn, c->s_app));
+  CU_TRY(c, cudaEventRecord(c->ev_app, c->s_app));
+  c->app_pending = true;
+  c->actor_first.clear();
+  for (int64_t i = 0; i < n; ++i)
+    if (actor_id[i] != 0) c->actor_first.emplace(actor_id[i], i);
+  c->bound_max_actor = 0;
+  for (auto* v : c->views) v->stage = 0;
+  return SPLATB200_OK;
 }
 
 extern "C" int splatb200_scene_bind_device(splatb200_ctx* c, int64_t n, int32_t d_f, const float* mean,
@@ -1027,6 +1087,7 @@ extern "C" int splatb200_optimizer_step_range(splatb200_ctx* c, const splatb200_
   if (lo < 0 || hi < lo || hi > c->grads_floats) return c->fail(SPLATB200_EINVAL, "range outside the gradient buffer");
   CU_TRY(c, cudaSetDevice(c->device));
   join_all(c);
+  wait_appearance(c);
   int rc = ensure_adam_state(c);
   if (!rc) rc = flag_nonfinite(c, lo, hi);
   if (rc) return rc;
@@ -1307,6 +1368,7 @@ extern "C" int splatb200_scene_download(splatb200_ctx* c, float* mean, float* sc
                                         float* color, float* feature) {
   if (!c->mean) return c->fail(SPLATB200_ERUNTIME, "no scene");
   join_all(c);
+  wait_appearance(c);
   const size_t n = (size_t)c->n;
   float* dst[6] = {mean, scale_log, quat, opacity_logit, color, feature};
   const float* src[6] = {c->mean, c->scale_log, c->quat, c->opacity_logit, c->color, c->feature};
@@ -1669,6 +1731,8 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   const SceneDev sc = c->scene_dev(v->d_actors);
   CU_TRY(c, cudaMemsetAsync(v->sensor_grads, 0, sizeof(float) * 8, st));
 
+  const bool late_app = c->app_pending;
+  v->proj.skip_feat = late_app ? 1 : 0;
   {
     StageTimer tm(v, 0, st);
     launch_project(v->s, sc, v->proj, st);
@@ -1749,6 +1813,12 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
   if (v->dl_pending) {  // an overlapped download of the previous render still reads the output buffers
     CU_TRY(c, cudaStreamWaitEvent(st, v->ev_dl, 0));
     v->dl_pending = false;
+  }
+  if (late_app) {  // colour / features are needed from here on
+    CU_TRY(c, cudaStreamWaitEvent(st, c->ev_app, 0));
+    launch_pack_feat(v->s, sc, v->proj, st);
+    CHECK_LAUNCH(c, "k_pack_feat");
+    c->launches += c->n > 0;
   }
   v->out.hit_or = v->multi_pass ? 1 : 0;
   if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));

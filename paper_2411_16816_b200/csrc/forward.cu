@@ -15,6 +15,21 @@ namespace sb {
 // K1/K2: fused compose + projection + tile rectangle
 // ------------------------------------------------------------------------------------------------
 template <bool kCamera>
+__device__ __forceinline__ void pack_channels(const SceneDev& sc, const ProjDev& p, int64_t i) {
+  float ch[kChannels];
+#pragma unroll
+  for (int k = 0; k < kChannels; ++k) ch[k] = 0.0f;
+  int o = 0;
+  if (kCamera) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ch[o++] = sc.color[3 * i + k];
+  }
+  for (int k = 0; k < sc.d_f; ++k) ch[o + k] = sc.feature[(int64_t)sc.d_f * i + k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p.feat[4 * i + k] = make_float4(ch[4 * k], ch[4 * k + 1], ch[4 * k + 2], ch[4 * k + 3]);
+}
+
+template <bool kCamera>
 __global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= sc.n) return;
@@ -42,17 +57,17 @@ __global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor 
   p.geomA[i] = make_float4(f.mean2d[0], f.mean2d[1], f.vel[0], f.vel[1]);
   p.geomB[i] = make_float4(f.conic[0], f.conic[1] + f.conic[2], f.conic[3], f.det_ratio * f.opacity);
   p.geomC[i] = make_float2(f.depth, f.vel[2]);
-  float ch[kChannels];
-#pragma unroll
-  for (int k = 0; k < kChannels; ++k) ch[k] = 0.0f;
-  int o = 0;
-  if (kCamera) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) ch[o++] = sc.color[3 * i + k];
-  }
-  for (int k = 0; k < sc.d_f; ++k) ch[o + k] = sc.feature[(int64_t)sc.d_f * i + k];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) p.feat[4 * i + k] = make_float4(ch[4 * k], ch[4 * k + 1], ch[4 * k + 2], ch[4 * k + 3]);
+  if (!p.skip_feat) pack_channels<kCamera>(sc, p, i);
+}
+
+// The blended channels of one visible Gaussian (camera: rgb + features, lidar: features; zero padded to 16), packed next
+// to its compositing record. Part of k_project, or on its own (k_pack_feat) when the scene's colour / feature arrays
+// arrive after its geometry (splatb200_scene_upload_async).
+template <bool kCamera>
+__global__ void __launch_bounds__(256) k_pack_feat(SceneDev sc, ProjDev p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sc.n || p.count[i] == 0u) return;
+  pack_channels<kCamera>(sc, p, i);
 }
 
 void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st) {
@@ -61,6 +76,12 @@ void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaS
   const unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
   if (s.is_camera) k_project<true><<<blocks, threads, 0, st>>>(s, sc, p);
   else k_project<false><<<blocks, threads, 0, st>>>(s, sc, p);
+}
+void launch_pack_feat(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st) {
+  if (sc.n == 0) return;
+  const unsigned blocks = (unsigned)((sc.n + 255) / 256);
+  if (s.is_camera) k_pack_feat<true><<<blocks, 256, 0, st>>>(sc, p);
+  else k_pack_feat<false><<<blocks, 256, 0, st>>>(sc, p);
 }
 
 // ------------------------------------------------------------------------------------------------

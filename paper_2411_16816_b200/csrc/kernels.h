@@ -89,6 +89,8 @@ constexpr int kActorAccStride = 12;
 
 // forward.cu
 void launch_project(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st);
+// p.skip_feat = 1 in launch_project, then this once the colour / feature arrays are on the device
+void launch_pack_feat(const Sensor& s, const SceneDev& sc, const ProjDev& p, cudaStream_t st);
 // rays: one float4 per ray POSITION (azimuth, elevation, t_l, bit pattern of the original ray index), tile-major and
 // azimuth-major inside a tile (prepared at view creation); tile_order: optional CTA -> tile permutation (longest
 // worklists first), nullptr = identity

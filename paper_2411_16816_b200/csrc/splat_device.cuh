@@ -85,6 +85,7 @@ struct ProjDev {
   uint32_t* dkey;   // fp32 bits of the (positive) depth key; 0xffffffff for culled Gaussians: the depth-sort key
   uint32_t* ccount; // two-level binning (camera): blocks of 2^cshift x 2^cshift tiles touched; null otherwise
   int cshift;
+  int skip_feat;    // k_project leaves `feat` to k_pack_feat (geometry-first scene upload: colour / features still in flight)
 };
 
 __device__ __forceinline__ float wrap_two_pi(float a) {  // common.hpp:34-38
