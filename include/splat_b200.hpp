@@ -83,6 +83,15 @@ class Context {
   Context& operator=(const Context&) = delete;
   splatb200_ctx* handle() const { return c_; }
 
+  /// The per-iteration refresh of the GaussianSet without the wait (same shape as the resident scene; tracks untouched):
+  /// geometry first, colour / features behind it, projection and binning of the next views overlap the rest of the
+  /// copy. `g` must stay alive and unchanged until the next sync().
+  void upload_parameters_async(const GaussianSet<float>& g) {
+    detail::check(c_, splatb200_scene_upload_async(c_, (int64_t)g.size(), g.feature_dim(), g.mean.data(), g.scale_log.data(),
+                                                   g.quat.data(), g.opacity_logit.data(), g.color.data(), g.feature.data(),
+                                                   g.actor_id.data()));
+  }
+
   /// Copy GaussianSet + tracks to the device (Eigen's column-major kxN is the ABI's N rows of k floats).
   void upload(const SceneGraph<float>& graph) {
     const auto& g = graph.gaussians;
