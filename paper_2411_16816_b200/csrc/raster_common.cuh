@@ -170,7 +170,9 @@ __device__ __forceinline__ uint32_t patch_mask(const float4 gA, const float4 gB,
   const bool psd = a > 0.0f && c > 0.0f && det4 >= 0.0f;
   if (!psd) return ((1u << kNP) - 1u) << kP0;
   // slab bounds: Q >= dx^2 kx and Q >= dy^2 ky, both factors rounded down
-  const float kx = __fdiv_rd(det4, 4.0f * c) * (1.0f - 1e-5f), ky = __fdiv_rd(det4, 4.0f * a) * (1.0f - 1e-5f);
+  // (approximate division, 2 ulp, under a 1.1e-5 safety factor: the directed-rounding intrinsics are ~70-instruction
+  // subroutines — 6% of the camera forward's instructions went there)
+  const float kx = __fdividef(det4, 4.0f * c) * (1.0f - 1.1e-5f), ky = __fdividef(det4, 4.0f * a) * (1.0f - 1.1e-5f);
   // alpha = rho exp(-qf/2) < alpha_min  <=>  qf > 2 ln(rho / alpha_min)
   float qmax = qform_max;
   if (alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qmax = fminf(qmax, 2.0f * __logf(rho * 1.01f / alpha_min) + 0.02f);
@@ -238,7 +240,9 @@ __device__ __forceinline__ uint32_t patch_mask_fast(const float4 gA, const float
   const bool psd = a > 0.0f && c > 0.0f && det4 >= 0.0f;
   const PatchBox tb = box[8];
   if (!psd || !tb.enabled) return 0xffu;
-  const float kx = __fdiv_rd(det4, 4.0f * c) * (1.0f - 1e-5f), ky = __fdiv_rd(det4, 4.0f * a) * (1.0f - 1e-5f);
+  // (approximate division, 2 ulp, under a 1.1e-5 safety factor: the directed-rounding intrinsics are ~70-instruction
+  // subroutines — 6% of the camera forward's instructions went there)
+  const float kx = __fdividef(det4, 4.0f * c) * (1.0f - 1.1e-5f), ky = __fdividef(det4, 4.0f * a) * (1.0f - 1.1e-5f);
   float qmax = qform_max;
   if (alpha_min > 0.0f && rho > 0.0f && rho < 1e30f) qmax = fminf(qmax, 2.0f * __logf(rho * 1.01f / alpha_min) + 0.02f);
   const float avx = fabsf(gA.z), avy = fabsf(gA.w);
@@ -250,8 +254,8 @@ __device__ __forceinline__ uint32_t patch_mask_fast(const float4 gA, const float
   const float qe = (qmax + E) * (1.0f + 2e-5f);
   // qe < 0: even the lowest qf rounding allows is beyond the alpha cut-off -> radii below any gap. k == 0 -> r = inf
   // (never dropped along that axis); NaN compares false (kept).
-  const float rx = qe < 0.0f ? -3.0e38f : sqrt_up(__fdiv_ru(qe, kx)) + 2.0f * slack_x;
-  const float ry = qe < 0.0f ? -3.0e38f : sqrt_up(__fdiv_ru(qe, ky)) + 2.0f * slack_y;
+  const float rx = qe < 0.0f ? -3.0e38f : sqrt_up(__fdividef(qe, kx) * (1.0f + 2e-6f)) + 2.0f * slack_x;
+  const float ry = qe < 0.0f ? -3.0e38f : sqrt_up(__fdividef(qe, ky) * (1.0f + 2e-6f)) + 2.0f * slack_y;
   uint32_t mask = 0u, wm = 0u;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {

@@ -31,7 +31,7 @@ fi
 if [ "$PART" = "sanitize" ]; then
 # 4. sanitizers on the small parity configs (racecheck without the tensor-core kernels: their bounded barrier waits
 #    expire under its instrumentation)
-timeout 900 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -x -k "config1 or lidar_forward_backward or camera_forward_backward or edge_cases or more_than_256 or one_level or radix_sort or assign_points or line_of_sight or set_rays or overlapped or view_streams or conv3x3 or decode_image_matches or decode_image_backward_matches" \
+timeout 900 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -x -k "config1 or lidar_forward_backward or camera_forward_backward or edge_cases or more_than_256 or one_level or radix_sort or assign_points or line_of_sight or set_rays or overlapped or view_streams or conv3x3 or decode_image_matches or decode_image_backward_matches or kernel_pairs or async_scene" \
     > "$OUT/sanitizer_memcheck_${TAG}.log" 2>&1
 timeout 900 compute-sanitizer --tool racecheck python -m pytest tests -m gpu -q -x -k "config1 or camera_forward_backward or more_than_256 or line_of_sight or assign_points_matches" \
     > "$OUT/sanitizer_racecheck_${TAG}.log" 2>&1
