@@ -491,6 +491,20 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
     __syncthreads();  // also publishes the patch boxes and the per-query rows
     const int max_last = s_max_last;
     int n_slots = 0;  // parked entries (warp-uniform); the panel persists across batches
+    unsigned long long jpack = 0ull;  // batch index of each parked slot (8 bits each)
+    uint32_t pend = 0u;               // slots whose record has not been copied into the panel yet
+    // records of the slots parked since the last copy: lane 8 w + e copies part w (geomA, geomB, index) of slot e
+    auto copy_pending = [&]() {
+      const int e = lane & 7, part = lane >> 3;
+      if (part < 3 && ((pend >> e) & 1u)) {
+        const int j = (int)((jpack >> (8 * e)) & 0xffull);
+        if (part == 0) ws.gAB[e] = sA[j];
+        else if (part == 1) ws.gAB[kChunkS + e] = sB[j];
+        else ws.src[e] = sSrc[j];
+      }
+      pend = 0u;
+      __syncwarp();
+    };
 
     // Compact hit list. On the north-star camera 6% of the list entries a tile's forward pass visited were blended by
     // anyone (the rest are culled grazing footprints): walking the raw list in batches of 256 meant ~5 batches per tile
@@ -607,13 +621,15 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           }
           ws.w[n_slots * kWStride + lane] = w;
           ws.gs[n_slots * kPanelStride + lane] = g_sigma;
-          // the record travels with the entry: lanes 0 / 1 copy geomA / geomB (sB follows sA), lane 2 the index
-          if (lane < 2) ws.gAB[lane * kChunkS + n_slots] = sA[lane * kBatch + jj];
-          else if (lane == 2) ws.src[n_slots] = sSrc[jj];
+          // the record travels with the entry — copied for all pending slots at once (copy_pending: 24 lanes, one
+          // record part each) when the panel is full or the batch ends, instead of by three lanes per entry
+          jpack |= (unsigned long long)jj << (8 * n_slots);
+          pend |= 1u << n_slots;
           if (++n_slots == kChunkS) {
-            __syncwarp();
+            copy_pending();
             reduce_panel8<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
             n_slots = 0;
+            jpack = 0ull;
           }
         };
         // two entries per iteration: independent quadratic forms (ILP), parked in back-to-front order; the camera
@@ -632,6 +648,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           if ((sure && has1) || __any_sync(0xffffffffu, valid)) park(j1, valid, ev);
         }
       }
+      if (pend) copy_pending();  // the staged records go away with the batch
       if (batch > 0) {  // next batch's records -> L2
         prefetch_l2(&p.geomA[src_next]);
         prefetch_l2(&p.geomB[src_next]);
@@ -645,6 +662,7 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
       reduce_panel8<kCamera>(ws, n_slots, lane, s.d_f, rg, pg, dt_local, wrap);
       n_slots = 0;
     }
+    jpack = 0ull;
     __syncthreads();  // patch boxes / staging / per-query rows are reused by the next ray pass
   }
 
