@@ -143,20 +143,26 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     __syncthreads();
   }
   const int total = s_total;
+  auto prefetch_rows = [&](int64_t in) {
+    prefetch_l1(sc.mean + 3 * in);
+    prefetch_l1(sc.scale_log + 3 * in);
+    prefetch_l1(sc.quat + 4 * in);
+    prefetch_l1(sc.opacity_logit + in);
+    prefetch_l1(sc.actor_id + in);
+    if (kMode == kFused) {
+      prefetch_l1(rg.g + kRasterGradStride * in);
+      prefetch_l1(rg.g + kRasterGradStride * in + 8);
+    }
+  };
+  // the first Gaussian of this thread: its rows are requested together, so that the loads spread over the code below
+  // (each at its first use) find them in L1 instead of paying an L2 round trip apiece
+  if (tid < total) prefetch_rows(base + s_list[tid]);
   for (int slot = tid; slot < total; slot += 256) {
   const int64_t i = base + s_list[slot];
   if (slot + 256 < total) {
     // the kernel is bound by its own load latency (ncu: long-scoreboard stalls at the first use of every parameter row):
     // the next Gaussian's rows are pulled into L1 while this one is computed
-    const int64_t in = base + s_list[slot + 256];
-    prefetch_l1(sc.mean + 3 * in);
-    prefetch_l1(sc.scale_log + 3 * in);
-    prefetch_l1(sc.quat + 4 * in);
-    prefetch_l1(sc.opacity_logit + in);
-    if (kMode == kFused) {
-      prefetch_l1(rg.g + kRasterGradStride * in);
-      prefetch_l1(rg.g + kRasterGradStride * in + 8);
-    }
+    prefetch_rows(base + s_list[slot + 256]);
   }
   {
     Fwd f;
