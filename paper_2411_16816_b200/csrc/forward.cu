@@ -11,6 +11,8 @@
 
 namespace sb {
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // ------------------------------------------------------------------------------------------------
 // K1/K2: fused compose + projection + tile rectangle
 // ------------------------------------------------------------------------------------------------
@@ -33,6 +35,12 @@ template <bool kCamera>
 __global__ void __launch_bounds__(256) k_project(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= sc.n) return;
+  // every parameter row of this Gaussian is requested up front: the loads below sit at their first uses, spread over
+  // the projection arithmetic, and would otherwise pay one L2 / DRAM round trip each
+  prefetch_l1(sc.scale_log + 3 * i);
+  prefetch_l1(sc.quat + 4 * i);
+  prefetch_l1(sc.opacity_logit + i);
+  prefetch_l1(sc.actor_id + i);
   Fwd f;
   compose_one(sc, i, f);
   if (kCamera) project_camera_one(s, f);
