@@ -361,35 +361,37 @@ k_count_scan(const uint32_t* __restrict__ count, const uint32_t* __restrict__ or
   for (int u = 0; u < kSItems; ++u) mine += c[u];
   uint32_t total;
   const uint32_t excl_in_tile = block_excl_scan<8>(mine, s_warp, total);
-  if (tid == 0) {
+  if (tid < 32) {
+    // Look-back by one WARP, 32 predecessors per step (one load per lane, ballots, one warp sum). Every tile of the scan
+    // is resident at once (489 at 1M Gaussians), so a late tile sums most of its predecessors' aggregates: one thread
+    // reading 8 per step left the other 255 threads of every CTA at the barrier below (ncu: 41 barrier-stall cycles
+    // per issued instruction).
+    const int lane = tid;
     uint32_t excl = 0u;
-    if (tile == 0) {
-      st_volatile(&state[0], kFlagPrefix | total);
-    } else {
-      st_volatile(&state[tile], kFlagAgg | total);
-      int64_t t = (int64_t)tile - 1;
-      uint32_t spins = 0u;
-      bool done = false;
-      while (!done) {  // 8 preceding tiles per step (independent loads)
-        uint32_t w[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) w[u] = (t - u >= 0) ? ld_volatile(&state[t - u]) : kFlagPrefix;
-        bool stall = false;
-        int used = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (!done && !stall) {
-            const uint32_t f = w[u] >> 30;
-            if (f == 0u) stall = true;
-            else { excl += w[u] & kValMask; ++used; done = f != 1u; }
-          }
-        }
-        t -= used;
-        if (stall && ++spins > kSpinLimit) { *err = 1u; done = true; }
+    if (lane == 0) st_volatile(&state[tile], (tile == 0 ? kFlagPrefix : kFlagAgg) | total);
+    int64_t t = (int64_t)tile - 1;
+    uint32_t spins = 0u;
+    bool done = tile == 0;
+    while (!done) {
+      const int64_t idx = t - lane;
+      const uint32_t w = idx >= 0 ? ld_volatile(&state[idx]) : kFlagPrefix;
+      const uint32_t f = w >> 30;
+      const unsigned notready = __ballot_sync(0xffffffffu, f == 0u);
+      const unsigned pref = __ballot_sync(0xffffffffu, f != 0u && f != 1u);
+      const int fp = pref ? __ffs(pref) - 1 : 31;              // lanes 0 .. fp are needed
+      const unsigned need = fp >= 31 ? 0xffffffffu : ((2u << fp) - 1u);
+      if (notready & need) {                                     // a needed predecessor has not published yet
+        if (++spins > kSpinLimit) { if (lane == 0) *err = 1u; done = true; }
+        continue;
       }
-      st_volatile(&state[tile], kFlagPrefix | ((excl + total) & kValMask));
+      excl += __reduce_add_sync(0xffffffffu, ((need >> lane) & 1u) ? (w & kValMask) : 0u);
+      if (pref) done = true;
+      else t -= 32;
     }
-    s_base = excl;
+    if (lane == 0) {
+      if (tile != 0) st_volatile(&state[tile], kFlagPrefix | ((excl + total) & kValMask));
+      s_base = excl;
+    }
   }
   __syncthreads();
   uint32_t run = s_base + excl_in_tile;
