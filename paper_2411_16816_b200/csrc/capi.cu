@@ -2567,6 +2567,39 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   if (name == "hit_bits") {  // per list entry: which warps of the tile's CTA blended it in the last forward (saved for the backward)
     if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "not rasterized");
     if (!dst) return v->I;
+    if (v->lidar_v2()) {
+      // the lidar kernel pair keeps one 32-bit word per (entry, warp) — the rays that blended it — instead of the byte:
+      // bit w of the byte = word w is non-zero. Words are valid up to each warp's last blended entry (last_idx).
+      std::vector<uint32_t> rows, tb, te;
+      std::vector<int32_t> last;
+      std::vector<int64_t> rb(v->n_tiles), re(v->n_tiles);
+      std::vector<float4> rays;
+      int rc = fetch(c, rows, v->out.hit_rows, lidar_hit_rows_words(v->I, v->n_tiles));
+      if (!rc) rc = fetch(c, tb, v->tile_begin, (size_t)v->n_tiles);
+      if (!rc) rc = fetch(c, te, v->tile_end, (size_t)v->n_tiles);
+      if (!rc) rc = fetch(c, last, v->out.last_idx, (size_t)v->P);
+      if (!rc) rc = fetch(c, rays, v->rays, (size_t)v->P);
+      if (rc) return rc;
+      CU_TRY(c, cudaMemcpy(rb.data(), v->ray_begin, sizeof(int64_t) * v->n_tiles, cudaMemcpyDeviceToHost));
+      CU_TRY(c, cudaMemcpy(re.data(), v->ray_end, sizeof(int64_t) * v->n_tiles, cudaMemcpyDeviceToHost));
+      for (int64_t k = 0; k < v->I; ++k) ((int64_t*)dst)[k] = 0;
+      for (int64_t t = 0; t < v->n_tiles; ++t) {
+        const uint32_t lb = tb[t], le = te[t];
+        int warp_last[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int64_t q = rb[t]; q < re[t]; ++q) {
+          uint32_t orig;
+          std::memcpy(&orig, &rays[(size_t)q].w, 4);
+          const int w = (int)((q - rb[t]) >> 5);
+          if (w < 8) warp_last[w] = std::max(warp_last[w], (int)last[orig]);
+        }
+        const size_t blk0 = ((size_t)(lb >> 8) + (size_t)t) * 2048u;
+        for (uint32_t pos = 0; lb + pos < le; ++pos)
+          for (int w = 0; w < 8; ++w)
+            if ((int)pos < warp_last[w] && rows[blk0 + (size_t)(pos >> 8) * 2048u + (size_t)w * 256 + (pos & 255u)] != 0u)
+              ((int64_t*)dst)[lb + pos] |= 1ll << w;
+      }
+      return v->I;
+    }
     std::vector<uint8_t> h;
     int rc = fetch(c, h, v->out.hit, (size_t)v->I);
     if (rc) return rc;
@@ -2575,8 +2608,10 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   }
   if (name == "raster_stats") {  // cumulative since view creation; zeros unless SPLATB200_STATS is set
     if (dst) {
-      // [0] staged entries, [1] per-warp survivors of the first-level cull, [2] group-list entries (lidar), [3] loop
-      // iterations (lidar: max over the warp's groups), [4] staged entries with a non-finite record
+      // [0] staged entries, [1] per-warp survivors of the first-level cull, [2] shared lidar kernel: group-list entries;
+      // lidar kernel pair: (entry, ray) candidates of the exact-qf prefilter, [3] shared lidar kernel: loop iterations (max
+      // over the warp's groups); lidar kernel pair: phase-2 trips (longest lane per round), [4] staged entries with a
+      // non-finite record
       unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (v->out.stats) {
         CU_TRY(c, cudaMemcpyAsync(h, v->out.stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));

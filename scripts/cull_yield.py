@@ -16,4 +16,7 @@ for name, v in (("lidar", ctx.lidar_view(lid, rays, st)), ("camera", ctx.camera_
     tb, te = v.array("tile_begin"), v.array("tile_end")
     print(f"{name}: I {len(hb)}, staged {rs[0]}, warp survivors {rs[1]}, (warp, entry) pairs with a blending lane {useful} "
           f"({useful / max(rs[1], 1):.2%} of survivors), entries hit by any warp {(hb != 0).sum()} ({(hb != 0).sum() / max(rs[0], 1):.2%} of staged), "
-          f"blends {nc.sum()} = {nc.sum() / max(useful, 1):.1f} lanes per useful pair, non-finite records {rs[4]}")
+          f"blends {nc.sum()} = {nc.sum() / max(useful, 1):.1f} lanes per useful pair, non-finite records {rs[4]}"
+          + (f"; lidar kernel pair: {rs[2]} (entry, ray) candidates after the exact-qf prefilter ({nc.sum() / max(rs[2], 1):.1%} of them blend), "
+             f"{rs[3]} phase-2 trips (longest lane per round: one trip per {nc.sum() / max(rs[3], 1):.1f} blends)"
+             if name == "lidar" and not os.environ.get("SPLATB200_LIDAR_V1") else ""))

@@ -440,6 +440,7 @@ ctx.zero_grads()
 v.backward(gb, ga)
 g = ctx.grads()
 np.savez(sys.argv[1], blend=v.array("blend"), alpha=v.array("alpha"), n_contrib=v.array("n_contrib"), last_idx=v.array("last_idx"),
+         hit_bits=v.array("hit_bits"),
          **{k: g[k] for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_feature")})
 """
 
@@ -463,7 +464,9 @@ def test_lidar_kernel_pairs_agree(tmp_path):
         outs.append(np.load(out))
     a, b = outs
     assert a["n_contrib"].sum() > 10000
-    for k in ("blend", "alpha", "n_contrib", "last_idx"):
+    # hit_bits: which warps blended each list entry — the shared kernels' hit bytes, and the same thing derived from
+    # the lidar pair's per-(entry, warp) ray masks
+    for k in ("blend", "alpha", "n_contrib", "last_idx", "hit_bits"):
         assert np.array_equal(a[k], b[k]), f"{k}: the two kernel pairs differ"
     for k in ("d_mean", "d_scale_log", "d_quat", "d_opacity_logit", "d_feature"):
         scale = np.abs(b[k]).max()
