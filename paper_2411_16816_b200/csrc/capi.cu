@@ -2569,12 +2569,15 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
     if (!dst) return v->I;
     if (v->lidar_v2()) {
       // the lidar kernel pair keeps one 32-bit word per (entry, warp) — the rays that blended it — instead of the byte:
-      // bit w of the byte = word w is non-zero. Words are valid up to each warp's last blended entry (last_idx).
+      // bit w of the byte = word w is non-zero. Words exist for the warps in the survivor byte (out.hit) and are valid up
+      // to each warp's last blended entry (last_idx).
       std::vector<uint32_t> rows, tb, te;
+      std::vector<uint8_t> surv;  // out.hit: the warps whose patch survived the box test (only they wrote a word)
       std::vector<int32_t> last;
       std::vector<int64_t> rb(v->n_tiles), re(v->n_tiles);
       std::vector<float4> rays;
       int rc = fetch(c, rows, v->out.hit_rows, lidar_hit_rows_words(v->I, v->n_tiles));
+      if (!rc) rc = fetch(c, surv, v->out.hit, (size_t)v->I);
       if (!rc) rc = fetch(c, tb, v->tile_begin, (size_t)v->n_tiles);
       if (!rc) rc = fetch(c, te, v->tile_end, (size_t)v->n_tiles);
       if (!rc) rc = fetch(c, last, v->out.last_idx, (size_t)v->P);
@@ -2595,7 +2598,7 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
         const size_t blk0 = ((size_t)(lb >> 8) + (size_t)t) * 2048u;
         for (uint32_t pos = 0; lb + pos < le; ++pos)
           for (int w = 0; w < 8; ++w)
-            if ((int)pos < warp_last[w] && rows[blk0 + (size_t)(pos >> 8) * 2048u + (size_t)w * 256 + (pos & 255u)] != 0u)
+            if ((int)pos < warp_last[w] && ((surv[lb + pos] >> w) & 1u) && rows[blk0 + (size_t)(pos >> 8) * 2048u + (size_t)w * 256 + (pos & 255u)] != 0u)
               ((int64_t*)dst)[lb + pos] |= 1ll << w;
       }
       return v->I;

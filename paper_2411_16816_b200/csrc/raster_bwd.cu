@@ -803,8 +803,10 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
 #pragma unroll
     for (int w = 0; w < 8; ++w) hw_next[w] = 0u;
     if (b0 * kBatch + tid < max_last) {
+      const uint32_t m = fwd.hit[lb + b0 * kBatch + tid];  // warps whose patch survived the box test: only they wrote a word
 #pragma unroll
-      for (int w = 0; w < 8; ++w) hw_next[w] = hitw[(size_t)b0 * 2048u + w * 256 + tid];
+      for (int w = 0; w < 8; ++w)
+        if ((m >> w) & 1u) hw_next[w] = hitw[(size_t)b0 * 2048u + w * 256 + tid];
       src_next = vals[lb + b0 * kBatch + tid];
     }
   }
@@ -820,8 +822,9 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
       for (int w = 0; w < 8; ++w) hwv[w] = hw_next[w];
       const uint32_t src = src_next;
       if (batch > 0) {  // the batch in front of this one is always full
+        const uint32_t m = fwd.hit[lb + bstart - kBatch + tid];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) hw_next[w] = hitw[(size_t)(batch - 1) * 2048u + w * 256 + tid];
+        for (int w = 0; w < 8; ++w) hw_next[w] = ((m >> w) & 1u) ? hitw[(size_t)(batch - 1) * 2048u + w * 256 + tid] : 0u;
         src_next = vals[lb + bstart - kBatch + tid];
       }
       if (tid < cnt) {

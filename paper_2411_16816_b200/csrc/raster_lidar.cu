@@ -38,7 +38,8 @@ constexpr int kListCap = 32 + 256;
 // whole list on its own without CTA barriers: 0.62 ms — the 8-fold test work and the unhidden load chains cost more
 // than the barriers.)
 // The lanes that blended each entry leave as one 32-bit word per (entry, warp) in hit_rows[block][warp][entry & 255]
-// (block = (tile_begin >> 8) + tile + (entry >> 8): never shared between tiles), 0 for an entry the warp culled.
+// (block = (tile_begin >> 8) + tile + (entry >> 8): never shared between tiles) — written only by the warps whose
+// patch survived the box test; RasterOutDev::hit keeps that survivor mask (one byte per entry) for the backward.
 template <bool kLos, bool kHead>
 __global__ void __launch_bounds__(256, 3)
 k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
@@ -209,24 +210,21 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
       }
     }
     sMask[tid] = (uint8_t)mask;
+    // which warps' patches can see the entry (the box test): only those warps will write a hit word for it; the
+    // backward reads this byte first and fetches just those words
+    if (idx < le) out.hit[idx] = (uint8_t)mask;
     const bool wrap = __syncthreads_or((mask & wrapm) != 0u) != 0;
     any_wrap |= wrap;
     if (live == 0u) { ncarry = 0; continue; }  // this warp's 32 rays have saturated
     const int cnt = min(256u, le - base);
-    // the warp's list: what the last batch left over, then this batch's survivors (order preserved); the culled
-    // entries' hit words are zeroed on the way
+    // the warp's list: what the last batch left over, then this batch's survivors (order preserved)
     if (lane < ncarry) lst[lane] = (uint16_t)(carry0 + lane);
     int n = ncarry;
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       const int j = c0 + lane;
-      const bool in = j < cnt;
-      const bool bit = in && ((sMask[j] >> warp) & 1u);
+      const bool bit = j < cnt && ((sMask[j] >> warp) & 1u);
       const unsigned bal = __ballot_sync(0xffffffffu, bit);
       if (bit) lst[n + __popc(bal & lt)] = (uint16_t)j;
-      else if (in) {
-        const uint32_t ps = base - lb + j;
-        hitw[(size_t)(ps >> 8) * 2048u + (ps & 255u)] = 0u;
-      }
       n += __popc(bal);
     }
     __syncwarp();
