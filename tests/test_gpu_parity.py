@@ -473,6 +473,21 @@ def test_lidar_kernel_pairs_agree(tmp_path):
         assert np.abs(a[k].astype(np.float64) - b[k]).max() <= 1e-4 * scale, k
 
 
+@pytest.mark.gpu
+def test_lidar_kernel_pairs_sweep():
+    """scripts/lidar_pair_fuzz.py: seven scenes (sub-ray to tile-filling footprints, anisotropic, fast sensors, ragged ray
+    sets) through the lidar kernel pair and through the shared kernels, one process each: every forward output and the
+    hit bits bit-identical, gradients equal up to the order of the atomics."""
+    import os
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([_sys.executable, os.path.join(root, "scripts", "lidar_pair_fuzz.py")], cwd=root, capture_output=True,
+                       text=True, timeout=1500, env=dict(os.environ, PYTHONPATH=root))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "all identical" in r.stdout
+
+
 def test_async_scene_upload_matches_blocking(ctx):
     """splatb200_scene_upload_async (geometry first, colour / features behind it on their own copy stream, projection and
     binning overlapping them; k_project + k_pack_feat instead of the fused k_project): bit-identical renders and
