@@ -870,20 +870,21 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
         }
         uint32_t mybits = transpose32(hw_e, lane);  // bit e: my ray blended entry k0 + e
         // ---- phase A: every lane walks the entries ITS ray blended, back to front ---------------
-        while (mybits != 0u) {
-          const int e = __ffs(mybits) - 1;
-          mybits &= mybits - 1u;
+        // Two hits per trip: alpha, 1 / (1 - alpha) and the dot product with the upstream gradient do not depend on the
+        // walk and are evaluated for both first, branch-free, so that the two chains of gathers and arithmetic
+        // interleave (the kernel is latency-bound); the walk itself (T, the suffix scalar) is a few dependent operations.
+        auto eval = [&](int e, float& al, float& inv, float& dot, float& gext, bool& ok, bool& clampd) {
           const int j = sList[k0 + e];
           const float4 gA = sA[j], gB = sB[j];
           float dx, dy;
           const float qf = alpha_qform<true>(gA, gB, qx, qy, t, dx, dy, wrap);
-          AlphaEval ev;
-          if (!alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) continue;  // (the bit says blended)
-          const float one_m = 1.0f - ev.alpha;
-          float inv;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));  // [1 - alpha_clamp, 1]: 1 ulp, no range fix-up needed
-          T = T * inv;  // transmittance in front of this Gaussian
-          const float w = ev.alpha * T;
+          // alpha_finish without its early exits (same operations, same decisions)
+          const float gauss = detmath::exp_bounded(fminf(fmaxf(__fmul_rn(-0.5f, qf), -87.0f), 88.0f));
+          al = __fmul_rn(gB.w, gauss);
+          clampd = al > s.alpha_clamp;
+          if (clampd) al = s.alpha_clamp;
+          ok = (qf <= s.qform_max) && (al >= s.alpha_min);  // (the bit says blended)
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(1.0f - al));  // [1 - alpha_clamp, 1]: 1 ulp, no range fix-up needed
           f32x2 d01 = pack2(0.0f, 0.0f), d23 = d01;  // packed pairs: 8 FFMA2 instead of 16 FFMA
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -894,16 +895,31 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
           float d0, d1, d2, d3;
           unpack2(d01, d0, d1);
           unpack2(d23, d2, d3);
-          float dotgf = (d0 + d1) + (d2 + d3);
           const float2 c2 = sC[j];
           const float r_rs = fmaf(c2.y, t, c2.x);  // r_rs = r + v_r t
-          dotgf = fmaf(g_D, r_rs, dotgf);
-          float g_extra = 0.0f;
-          if (kLos && r_rs < los_cut) g_extra = g_los;  // d los / d alpha_i = 1 in front of the cut
-          const float g_a = dotgf * T + (K - S) * inv + g_extra;
-          S = fmaf(w, dotgf, S);
+          dot = fmaf(g_D, r_rs, (d0 + d1) + (d2 + d3));
+          gext = (kLos && r_rs < los_cut) ? g_los : 0.0f;  // d los / d alpha_i = 1 in front of the cut
+        };
+        auto apply = [&](int e, float al, float inv, float dot, float gext, bool clampd) {
+          T = T * inv;  // transmittance in front of this Gaussian
+          const float w = al * T;
+          const float g_a = dot * T + (K - S) * inv + gext;
+          S = fmaf(w, dot, S);
           ws.w[(n_slots + e) * kWStride + lane] = w;
-          if (!ev.clamped) ws.gs[(n_slots + e) * kPanelStride + lane] = -ev.alpha * g_a;  // alpha = rho exp(-sigma); clamped: constant
+          if (!clampd) ws.gs[(n_slots + e) * kPanelStride + lane] = -al * g_a;  // alpha = rho exp(-sigma); clamped: constant
+        };
+        while (mybits != 0u) {
+          const int e0 = __ffs(mybits) - 1;
+          mybits &= mybits - 1u;
+          const bool has1 = mybits != 0u;
+          const int e1 = has1 ? __ffs(mybits) - 1 : e0;
+          mybits &= mybits - 1u;  // (0 stays 0)
+          float al0, inv0, dot0, gx0, al1, inv1, dot1, gx1;
+          bool ok0, ok1, cl0, cl1;
+          eval(e0, al0, inv0, dot0, gx0, ok0, cl0);
+          eval(e1, al1, inv1, dot1, gx1, ok1, cl1);
+          if (ok0) apply(e0, al0, inv0, dot0, gx0, cl0);
+          if (has1 && ok1) apply(e1, al1, inv1, dot1, gx1, cl1);
         }
         n_slots += g;
         k0 += g;
