@@ -879,7 +879,7 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
           float dx, dy;
           const float qf = alpha_qform<true>(gA, gB, qx, qy, t, dx, dy, wrap);
           // alpha_finish without its early exits (same operations, same decisions)
-          const float gauss = detmath::exp_bounded(fminf(fmaxf(__fmul_rn(-0.5f, qf), -87.0f), 88.0f));
+          const float gauss = detmath::exp_bounded((qf <= s.qform_max) ? fminf(__fmul_rn(-0.5f, qf), 88.0f) : 0.0f);
           al = __fmul_rn(gB.w, gauss);
           clampd = al > s.alpha_clamp;
           if (clampd) al = s.alpha_clamp;

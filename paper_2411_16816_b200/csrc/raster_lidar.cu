@@ -141,36 +141,56 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
     // ---- phase 2: lane = ray, every lane walks its own candidates front to back ----------------
     uint32_t hitk = 0u;
     int trips = 0;
-    while (bits != 0u) {
-      const uint32_t b = bits & (0u - bits);
-      const int slot = lst[k0 + __ffs(bits) - 1];
-      bits ^= b;
-      ++trips;
+    // Two candidates per trip: the records are gathered and alpha evaluated for both first, branch-free (the same
+    // operations as alpha_finish, the same decisions), so that the two chains interleave; then they are blended in order.
+    auto eval = [&](int kk, int& slot, float& al, bool& ok) {
+      slot = lst[k0 + kk];
       const float4 gA = sA[slot], gB = sB[slot];
       float dx, dy;
       const float qf = rw ? alpha_qform<true>(gA, gB, qx, qy, t, dx, dy, true)
                           : alpha_qform_packed(pack2(gA.x, gA.y), pack2(gA.z, gA.w), gB, q2, t2, dx, dy);
-      AlphaEval ev;
-      if (alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) {
-        const float w = __fmul_rn(ev.alpha, T);
-        const f32x2 ww = pack2(w, w);
+      const bool in = qf <= s.qform_max;
+      const float gauss = detmath::exp_bounded(in ? fminf(__fmul_rn(-0.5f, qf), 88.0f) : 0.0f);
+      al = __fmul_rn(gB.w, gauss);
+      if (al > s.alpha_clamp) al = s.alpha_clamp;
+      ok = in && (al >= s.alpha_min);
+    };
+    auto blend = [&](int slot, float al, uint32_t b) {
+      const float w = __fmul_rn(al, T);
+      const f32x2 ww = pack2(w, w);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 f4 = sF[c * kSlots + slot];
-          acc2[2 * c] = fma2(pack2(f4.x, f4.y), ww, acc2[2 * c]);
-          acc2[2 * c + 1] = fma2(pack2(f4.z, f4.w), ww, acc2[2 * c + 1]);
-        }
-        T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
-        ++n_contrib;
-        last_idx = (int)sPos[slot] + 1;
-        hitk |= b;
-        const float2 c2 = sC[slot];
-        const float r_rs = __fmaf_rn(c2.y, t, c2.x);
-        range_acc = __fmaf_rn(r_rs, w, range_acc);
-        if (kLos && r_rs < los_cut) los = __fadd_rn(los, ev.alpha);  // opacity in front of the measured range
-        if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
-        if (T < s.transmittance_min) { done = true; bits = 0u; }
+      for (int c = 0; c < 4; ++c) {
+        const float4 f4 = sF[c * kSlots + slot];
+        acc2[2 * c] = fma2(pack2(f4.x, f4.y), ww, acc2[2 * c]);
+        acc2[2 * c + 1] = fma2(pack2(f4.z, f4.w), ww, acc2[2 * c + 1]);
       }
+      T = __fmul_rn(T, __fsub_rn(1.0f, al));
+      ++n_contrib;
+      last_idx = (int)sPos[slot] + 1;
+      hitk |= b;
+      const float2 c2 = sC[slot];
+      const float r_rs = __fmaf_rn(c2.y, t, c2.x);
+      range_acc = __fmaf_rn(r_rs, w, range_acc);
+      if (kLos && r_rs < los_cut) los = __fadd_rn(los, al);  // opacity in front of the measured range
+      if (!med_found && T < 0.5f) { median = r_rs; med_found = true; }
+      if (T < s.transmittance_min) { done = true; bits = 0u; }
+    };
+    while (bits != 0u) {
+      const uint32_t b0 = bits & (0u - bits);
+      const int kk0 = __ffs(bits) - 1;
+      bits ^= b0;
+      const bool has1 = bits != 0u;
+      const uint32_t b1 = bits & (0u - bits);
+      const int kk1 = has1 ? __ffs(bits) - 1 : kk0;
+      bits ^= b1;
+      ++trips;
+      int slot0, slot1;
+      float al0, al1;
+      bool ok0, ok1;
+      eval(kk0, slot0, al0, ok0);
+      eval(kk1, slot1, al1, ok1);
+      if (ok0) blend(slot0, al0, b0);
+      if (has1 && ok1 && !done) blend(slot1, al1, b1);
     }
     if (out.stats) st_iter += (unsigned long long)__reduce_max_sync(0xffffffffu, trips);
     // the rays that blended each entry: back to entry-major, one word per (entry, warp)
