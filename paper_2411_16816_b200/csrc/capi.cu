@@ -414,7 +414,7 @@ int ensure_isect_capacity(splatb200_view* v, int64_t n_sort, int64_t n_fine) {
     CU_TRY(c, cudaMalloc(&v->out.hit, (size_t)cap));
     v->hit_cap = cap;
   }
-  if (!v->lidar_v2() && n_fine > v->list_cap) {  // (a lidar view changes kernels when a sweep brings a tile above 256 rays)
+  if (n_fine > v->list_cap) {
     dfree(v->out.hit_list);
     const int64_t cap = n_fine + n_fine / 4 + 2048;
     CU_TRY(c, cudaMalloc(&v->out.hit_list, sizeof(uint32_t) * (size_t)cap));
@@ -1821,7 +1821,8 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     c->launches += c->n > 0;
   }
   v->out.hit_or = v->multi_pass ? 1 : 0;
-  if (v->multi_pass && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
+  // hit bytes are OR-ed into: by the shared lidar kernel over several ray passes, by the lidar kernel pair one warp at a time
+  if ((v->multi_pass || v->lidar_v2()) && v->I > 0) CU_TRY(c, cudaMemsetAsync(v->out.hit, 0, (size_t)v->I, st));
   if (v->out.head_w && !v->d_head_y)
     CU_TRY(c, cudaMalloc(&v->d_head_y, sizeof(float) * 2 * (size_t)std::max<int64_t>(1, std::max(v->P, v->P_cap))));
   v->out.head_y = v->out.head_w ? v->d_head_y : nullptr;
@@ -2567,42 +2568,6 @@ extern "C" int64_t splatb200_view_array(splatb200_view* v, const char* name_c, v
   if (name == "hit_bits") {  // per list entry: which warps of the tile's CTA blended it in the last forward (saved for the backward)
     if (v->stage < 3) return c->fail(SPLATB200_ERUNTIME, "not rasterized");
     if (!dst) return v->I;
-    if (v->lidar_v2()) {
-      // the lidar kernel pair keeps one 32-bit word per (entry, warp) — the rays that blended it — instead of the byte:
-      // bit w of the byte = word w is non-zero. Words exist for the warps in the survivor byte (out.hit) and are valid up
-      // to each warp's last blended entry (last_idx).
-      std::vector<uint32_t> rows, tb, te;
-      std::vector<uint8_t> surv;  // out.hit: the warps whose patch survived the box test (only they wrote a word)
-      std::vector<int32_t> last;
-      std::vector<int64_t> rb(v->n_tiles), re(v->n_tiles);
-      std::vector<float4> rays;
-      int rc = fetch(c, rows, v->out.hit_rows, lidar_hit_rows_words(v->I, v->n_tiles));
-      if (!rc) rc = fetch(c, surv, v->out.hit, (size_t)v->I);
-      if (!rc) rc = fetch(c, tb, v->tile_begin, (size_t)v->n_tiles);
-      if (!rc) rc = fetch(c, te, v->tile_end, (size_t)v->n_tiles);
-      if (!rc) rc = fetch(c, last, v->out.last_idx, (size_t)v->P);
-      if (!rc) rc = fetch(c, rays, v->rays, (size_t)v->P);
-      if (rc) return rc;
-      CU_TRY(c, cudaMemcpy(rb.data(), v->ray_begin, sizeof(int64_t) * v->n_tiles, cudaMemcpyDeviceToHost));
-      CU_TRY(c, cudaMemcpy(re.data(), v->ray_end, sizeof(int64_t) * v->n_tiles, cudaMemcpyDeviceToHost));
-      for (int64_t k = 0; k < v->I; ++k) ((int64_t*)dst)[k] = 0;
-      for (int64_t t = 0; t < v->n_tiles; ++t) {
-        const uint32_t lb = tb[t], le = te[t];
-        int warp_last[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int64_t q = rb[t]; q < re[t]; ++q) {
-          uint32_t orig;
-          std::memcpy(&orig, &rays[(size_t)q].w, 4);
-          const int w = (int)((q - rb[t]) >> 5);
-          if (w < 8) warp_last[w] = std::max(warp_last[w], (int)last[orig]);
-        }
-        const size_t blk0 = ((size_t)(lb >> 8) + (size_t)t) * 2048u;
-        for (uint32_t pos = 0; lb + pos < le; ++pos)
-          for (int w = 0; w < 8; ++w)
-            if ((int)pos < warp_last[w] && ((surv[lb + pos] >> w) & 1u) && rows[blk0 + (size_t)(pos >> 8) * 2048u + (size_t)w * 256 + (pos & 255u)] != 0u)
-              ((int64_t*)dst)[lb + pos] |= 1ll << w;
-      }
-      return v->I;
-    }
     std::vector<uint8_t> h;
     int rc = fetch(c, h, v->out.hit, (size_t)v->I);
     if (rc) return rc;

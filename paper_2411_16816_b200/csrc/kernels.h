@@ -52,8 +52,7 @@ struct RasterOutDev {
   uint32_t* hit_rows;  // lidar v2 kernels (raster_lidar.cu), else null: the RAYS that blended each list entry, one 32-bit
                        //    word per (entry, warp of the tile's CTA) instead of the hit byte. One 2048-word block per 256
                        //    entries of a tile's list, block (tile_begin >> 8) + tile + (entry >> 8), laid out
-                       //    [warp][entry & 255]; written up to each warp's last blended entry, and only by the warps whose
-                       //    patch survived the box test: `hit` holds that survivor mask (one byte per entry) for these views
+                       //    [warp][entry & 255]; a word exists where bit `warp` of the entry's hit byte is set
   uint8_t* tile_wrap;  // T  lidar: 1 if some batch of the tile could not certify |azimuth difference| < pi (seam tiles);
                        //    the backward skips the wrap elsewhere. Written by the forward.
   // optional line-of-sight channel of a lidar view: los[q] = sum of alpha_i over the

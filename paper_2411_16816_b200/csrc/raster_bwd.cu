@@ -709,6 +709,7 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
   WarpScratch* sWs = reinterpret_cast<WarpScratch*>(sHw + 8 * kBatch); // 8
   uint8_t* sListAll = reinterpret_cast<uint8_t*>(sWs + 8);             // 8 x kBatch
   __shared__ int s_max_last;
+  __shared__ int s_wcnt[8];
 
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : tile_first + (int)blockIdx.x;
   const int tid = threadIdx.x;
@@ -790,68 +791,94 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
   const int max_last = s_max_last;
   if (max_last == 0) return;
 
-  const uint32_t* const hitw = fwd.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u;  // [batch][warp][entry]
+  const uint32_t* const hitw = fwd.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u;  // [block][warp][entry & 255]
   int n_slots = 0;  // parked entries (warp-uniform); the panel persists across batches
   float dt_unused = 0.0f;
 
-  // hit words and list entry of a batch are fetched one batch ahead and its records prefetched into L2: a batch's staging
-  // then starts with the record loads instead of a chain of three dependent global loads (ncu: a quarter of the stall
-  // samples sat on that chain and on the barrier behind it)
-  uint32_t hw_next[8], src_next = 0u;
+  // Compact hit list (as in k_raster_bwd): half of a lidar tile's entries were blended by some warp. The CTA scans its
+  // hit bytes (bit w: warp w has a hit word for the entry), 1,024 per step, and keeps (position << 8 | byte) of the
+  // non-zero ones, in list order; the batches below are dense.
+  uint32_t* const hl = fwd.hit_list + lb;
+  int n_hit = 0;  // CTA-uniform
   {
-    const int b0 = (max_last - 1) / kBatch;
+    const uint32_t w0 = lb >> 2;
+    const uint32_t* hit4 = reinterpret_cast<const uint32_t*>(fwd.hit);
+    for (uint32_t wbase = w0; 4u * wbase < lb + (uint32_t)max_last; wbase += 256u) {
+      const uint32_t word = hit4[wbase + tid];
+      const int pos0 = (int)(4u * (wbase + tid)) - (int)lb;
+      uint32_t ent[4];
+      int c4 = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) hw_next[w] = 0u;
-    if (b0 * kBatch + tid < max_last) {
-      const uint32_t m = fwd.hit[lb + b0 * kBatch + tid];  // warps whose patch survived the box test: only they wrote a word
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t m = (word >> (8 * i)) & 0xffu;
+        const int ps = pos0 + i;
+        if (m != 0u && ps >= 0 && ps < max_last) ent[c4++] = ((uint32_t)ps << 8) | m;
+      }
+      int incl = c4;
 #pragma unroll
-      for (int w = 0; w < 8; ++w)
-        if ((m >> w) & 1u) hw_next[w] = hitw[(size_t)b0 * 2048u + w * 256 + tid];
-      src_next = vals[lb + b0 * kBatch + tid];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) s_wcnt[warp] = incl;
+      __syncthreads();
+      int before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const int c = s_wcnt[w];
+        if (w < warp) before += c;
+        total += c;
+      }
+      uint32_t* dst = hl + n_hit + before + (incl - c4);
+      for (int i = 0; i < c4; ++i) dst[i] = ent[i];
+      n_hit += total;
+      __syncthreads();  // s_wcnt is reused; after the last step: the list is visible to the whole CTA
     }
   }
-  for (int batch = (max_last - 1) / kBatch; batch >= 0; --batch) {
-    const int bstart = batch * kBatch;
-    const int cnt = min(kBatch, max_last - bstart);
-    // thread = list entry: the hit words of the 8 warps (each valid up to that warp's last blended entry: the forward
-    // wrote every word in front of it), records only for entries some warp blended
+
+  // a batch's list entries, hit words and record indices are fetched one batch ahead and its records prefetched into
+  // L2: staging then starts with the record loads instead of a chain of dependent global loads
+  uint32_t hw_next[8], ent_next = 0u, src_next = 0u;
+  auto fetch = [&](int i) {  // compact entry i of this thread's next batch
+    ent_next = hl[i];
+    const uint32_t ps = ent_next >> 8;
+    src_next = vals[lb + ps];
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      hw_next[w] = ((ent_next >> w) & 1u) ? hitw[(size_t)(ps >> 8) * 2048u + w * 256 + (ps & 255u)] : 0u;
+  };
+#pragma unroll
+  for (int w = 0; w < 8; ++w) hw_next[w] = 0u;
+  const int nbat = (n_hit + kBatch - 1) / kBatch;
+  if (nbat > 0 && (nbat - 1) * kBatch + tid < n_hit) fetch((nbat - 1) * kBatch + tid);
+  for (int batch = nbat - 1; batch >= 0; --batch) {
+    const int cnt = min(kBatch, n_hit - batch * kBatch);
+    // thread = compact entry: the hit words of the warps that blended it, its record
     {
-      uint32_t any = 0u;
       uint32_t hwv[8];
 #pragma unroll
       for (int w = 0; w < 8; ++w) hwv[w] = hw_next[w];
       const uint32_t src = src_next;
-      if (batch > 0) {  // the batch in front of this one is always full
-        const uint32_t m = fwd.hit[lb + bstart - kBatch + tid];
-#pragma unroll
-        for (int w = 0; w < 8; ++w) hw_next[w] = ((m >> w) & 1u) ? hitw[(size_t)(batch - 1) * 2048u + w * 256 + tid] : 0u;
-        src_next = vals[lb + bstart - kBatch + tid];
-      }
+      if (batch > 0) fetch((batch - 1) * kBatch + tid);  // the batch in front of this one is always full
       if (tid < cnt) {
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          sHw[w * kBatch + tid] = hwv[w];
-          any |= hwv[w];
-        }
-        if (any) {
-          sSrc[tid] = src;
-          sA[tid] = p.geomA[src];
-          sB[tid] = p.geomB[src];
-          sC[tid] = p.geomC[src];
+        for (int w = 0; w < 8; ++w) sHw[w * kBatch + tid] = hwv[w];
+        sSrc[tid] = src;
+        sA[tid] = p.geomA[src];
+        sB[tid] = p.geomB[src];
+        sC[tid] = p.geomC[src];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) sF[k * kBatch + tid] = p.feat[4 * (size_t)src + k];
-        }
+        for (int k = 0; k < 4; ++k) sF[k * kBatch + tid] = p.feat[4 * (size_t)src + k];
       }
     }
     __syncthreads();
 
-    if (warp_last > bstart) {
-      // the warp's hit entries of this batch, back to front. A word beyond this warp's last blended entry was never
-      // written by the forward: masked by position.
+    {
+      // the warp's hit entries of this batch, back to front
       int n_w = 0;
       for (int c0 = (cnt - 1) & ~31; c0 >= 0; c0 -= 32) {
         const int j = c0 + (31 - lane);  // lane 0 takes the highest entry: ballot ranks are back-to-front ranks
-        const bool bit = j < cnt && bstart + j < warp_last && myHw[j] != 0u;
+        const bool bit = j < cnt && myHw[j] != 0u;
         const unsigned bal = __ballot_sync(0xffffffffu, bit);
         if (bit) sList[n_w + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)j;
         n_w += __popc(bal);
@@ -933,15 +960,10 @@ k_raster_bwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
       }
     }
     if (batch > 0) {  // next batch's records -> L2
-      uint32_t anyn = 0u;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) anyn |= hw_next[w];
-      if (anyn) {
-        prefetch_l2(&p.geomA[src_next]);
-        prefetch_l2(&p.geomB[src_next]);
-        prefetch_l2(&p.geomC[src_next]);
-        prefetch_l2(&p.feat[4 * (size_t)src_next]);
-      }
+      prefetch_l2(&p.geomA[src_next]);
+      prefetch_l2(&p.geomB[src_next]);
+      prefetch_l2(&p.geomC[src_next]);
+      prefetch_l2(&p.feat[4 * (size_t)src_next]);
     }
     __syncthreads();  // every warp is done with the staged batch
   }

@@ -38,8 +38,9 @@ constexpr int kListCap = 32 + 256;
 // whole list on its own without CTA barriers: 0.62 ms — the 8-fold test work and the unhidden load chains cost more
 // than the barriers.)
 // The lanes that blended each entry leave as one 32-bit word per (entry, warp) in hit_rows[block][warp][entry & 255]
-// (block = (tile_begin >> 8) + tile + (entry >> 8): never shared between tiles) — written only by the warps whose
-// patch survived the box test; RasterOutDev::hit keeps that survivor mask (one byte per entry) for the backward.
+// (block = (tile_begin >> 8) + tile + (entry >> 8): never shared between tiles) — written only where some ray of the
+// warp blended the entry, together with bit `warp` of the entry's hit byte (RasterOutDev::hit, zeroed by the host per
+// forward): the same byte the shared kernels write, here it also says which words exist.
 template <bool kLos, bool kHead>
 __global__ void __launch_bounds__(256, 3)
 k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __restrict__ vals,
@@ -95,6 +96,7 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
   if (tid == 0) tile_patch_box(sBox);  // published by the first barrier of the batch loop
 
   uint32_t* const hitw = out.hit_rows + ((size_t)(lb >> 8) + (size_t)tile) * 2048u + warp * 256;
+  uint32_t* const hit32 = reinterpret_cast<uint32_t*>(out.hit);  // hit bytes, four per word (cudaMalloc-aligned)
   const float4* wray = sRay + 32 * warp;
   const unsigned lt = (1u << lane) - 1u;
   const int carry0 = 256 + 32 * warp;  // this warp's carry slots
@@ -195,9 +197,13 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
     if (out.stats) st_iter += (unsigned long long)__reduce_max_sync(0xffffffffu, trips);
     // the rays that blended each entry: back to entry-major, one word per (entry, warp)
     const uint32_t hw = transpose32(hitk, lane);
-    if (lane < n) {
+    if (lane < n && hw != 0u) {
       const uint32_t ps = sPos[myslot];
       hitw[(size_t)(ps >> 8) * 2048u + (ps & 255u)] = hw;
+      // ... and bit `warp` of the entry's hit byte (pre-zeroed by the host): the backward compacts the non-zero bytes
+      // into a dense list and fetches exactly the words whose bit is set
+      const uint32_t at = lb + ps;
+      atomicOr(hit32 + (at >> 2), (1u << warp) << (8u * (at & 3u)));
     }
     live = __ballot_sync(0xffffffffu, !done);
   };
@@ -230,9 +236,6 @@ k_raster_fwd_lidar(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* 
       }
     }
     sMask[tid] = (uint8_t)mask;
-    // which warps' patches can see the entry (the box test): only those warps will write a hit word for it; the
-    // backward reads this byte first and fetches just those words
-    if (idx < le) out.hit[idx] = (uint8_t)mask;
     const bool wrap = __syncthreads_or((mask & wrapm) != 0u) != 0;
     any_wrap |= wrap;
     if (live == 0u) { ncarry = 0; continue; }  // this warp's 32 rays have saturated
