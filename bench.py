@@ -560,6 +560,7 @@ def run_b200(args):
             def f():
                 v.forward(0.0)
                 v.backward_device(g[0].data_ptr(), g[1].data_ptr())
+                ctx.join()      # the timing events sit on the ctx stream: order it after the view's own stream
             return f
         k_br = max(1, min(args.steps, 5))
         ms_l, _, _ = timed(only(vl, g_dev["l"]), k_br)
