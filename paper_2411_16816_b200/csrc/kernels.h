@@ -67,11 +67,13 @@ struct RasterOutDev {
 };
 
 // Raw per-Gaussian sums of the compositing backward, indexed by source index; consumed (and re-zeroed)
-// by the projection backward. 10 floats per Gaussian: conic (3), mean2d (2), velocity (3), rho, range.
+// by the projection backward. 12 floats = 48 bytes per Gaussian, in three 16-byte groups so that a warp sends each group
+// as one vector RED and the projection backward reads / zeroes rows with 128-bit accesses:
+//   [0..3] conic a, b, c; rho   [4..7] mean2d x, y; velocity x, y   [8..11] v_r, range (lidar), 2 pad
 struct RasterGradDev {
-  float* g;  // N x 10, zero between backward calls
+  float* g;  // N x 12, zero between backward calls
 };
-constexpr int kRasterGradStride = 10;
+constexpr int kRasterGradStride = 12;
 
 // SceneParamGrads (scene.hpp:325-363) as one contiguous device buffer.
 struct ParamGradDev {

@@ -182,11 +182,13 @@ k_project_bwd(const __grid_constant__ Sensor s, SceneDev sc, ProjDev p, RasterGr
     float G2[2][2];
     float gm[3], gv[3];   // g_mean2d + g_range, g_velocity
     if (kMode == kFused) {
-    float r[kRasterGradStride];
-#pragma unroll
-    for (int k = 0; k < kRasterGradStride; ++k) r[k] = rg.g[kRasterGradStride * i + k];  // all loads first: independent
-#pragma unroll
-    for (int k = 0; k < kRasterGradStride; ++k) rg.g[kRasterGradStride * i + k] = 0.0f;  // scratch zero for the next backward
+    // the row (kernels.h: conic + rho | mean2d + velocity.xy | v_r, range) as three 128-bit loads, re-zeroed for the next backward
+    float4* r4 = reinterpret_cast<float4*>(rg.g + kRasterGradStride * i);
+    const float4 R0 = r4[0], R1 = r4[1], R2 = kCamera ? make_float4(0.0f, 0.0f, 0.0f, 0.0f) : r4[2];
+    const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    r4[0] = z4; r4[1] = z4;
+    if (!kCamera) r4[2] = z4;
+    const float r[10] = {R0.x, R0.y, R0.z, R1.x, R1.y, R1.z, R1.w, R2.x, R0.w, R2.y};  // conic 3, mean2d 2, velocity 3, rho, range
     // ---- (1) raw sums -> ProjectedGrads -------------------------------------------------------
     const float g_rho = r[8];
     g_opacity = f.det_ratio * g_rho;

@@ -68,6 +68,14 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
 }
 constexpr uint32_t kTf32Mask = 0xffffe000u;  // sign, exponent, 10 mantissa bits
 
+// One 16-byte fire-and-forget reduction (REDG.E.ADD.F32x4): four adjacent floats of one row in ONE request. The raw
+// geometric sums of an entry used to leave as eight scalar REDs issued value by value — eight instructions, each touching
+// one 32-byte sector per entry (8 sectors per (warp, entry); measured with scripts/red_peak.cu the backward kernels ran
+// at 46-59% of the GPU's RED sector ceiling). The scratch rows are laid out for this (kernels.h: kRasterGradStride).
+__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // Phase B for `n` parked entries (1 <= n <= kChunk).
 //
 // The 16 channel sums are the one dense contraction of the path: dL/df[e][c] = sum_q w[e][q] G[q][c], a
@@ -135,7 +143,7 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
             if (v != 0.0f) {  // columns >= channels are exactly zero
               float* dst;
               if (kCamera) dst = c < 3 ? f0 + c : f1 + c;
-              else dst = c < 13 ? f1 + c : (c == 13 ? r0 + 25 : r0 + 23);  // 13: d/d range, 14: d/d v_r
+              else dst = c < 13 ? f1 + c : (c == 13 ? r0 + 25 : r0 + 24);  // 13: d/d range (slot 9), 14: d/d v_r (slot 8)
               atomicAdd(dst, v);
             }
           }
@@ -210,24 +218,21 @@ __device__ __forceinline__ void reduce_panel(const WarpScratch& ws, int n, int l
 #pragma unroll
     for (int c = 0; c < kGeo; ++c) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
   }
-  if (active && g == 0) {  // one RED per (warp, Gaussian, value)
+  // after the butterfly every lane of an entry holds the full sums (at least two lanes per entry: E <= 16): lane g = 0
+  // sends (conic, rho), lane g = 1 (mean2d, velocity.xy) — two 16-byte REDs per (warp, Gaussian) in one instruction
+  if (active && g < 2) {
     const float hb = 0.5f * gB.y;
-    const float gx = fmaf(hb, m[2], gB.x * m[1]), gy = fmaf(hb, m[1], gB.z * m[2]);     // sum of dL/dDelta
-    const float gtx = fmaf(hb, m[7], gB.x * m[6]), gty = fmaf(hb, m[6], gB.z * m[7]);   // sum of t dL/dDelta
-    float acc[kGeo];
-    acc[0] = 0.5f * m[3];  // dL/dconic
-    acc[1] = 0.5f * m[4];
-    acc[2] = 0.5f * m[5];
-    acc[3] = -gx;  // dL/dmean2d
-    acc[4] = -gy;
-    acc[5] = -gtx;  // dL/dvelocity (first two components)
-    acc[6] = -gty;
-    acc[7] = __fdividef(-m[0], gB.w);  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
-    if (kCamera) dt_local -= fmaf(gA.z, gx, gA.w * gy);  // SensorGrads.d_time_offset
     float* r0 = rg.g + kRasterGradStride * (size_t)ws.src[e];
-#pragma unroll
-    for (int c = 0; c < kGeo; ++c)
-      if (acc[c] != 0.0f) atomicAdd(r0 + (c < 7 ? c : 8), acc[c]);  // slots 0-6, rho at 8 (7: v_r, 9: range)
+    if (g == 0) {
+      const float a0 = 0.5f * m[3], a1 = 0.5f * m[4], a2 = 0.5f * m[5];  // dL/dconic
+      const float a3 = __fdividef(-m[0], gB.w);  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
+      if (a0 != 0.0f || a1 != 0.0f || a2 != 0.0f || a3 != 0.0f) red_add_v4(r0, a0, a1, a2, a3);
+    } else {
+      const float gx = fmaf(hb, m[2], gB.x * m[1]), gy = fmaf(hb, m[1], gB.z * m[2]);     // sum of dL/dDelta
+      const float gtx = fmaf(hb, m[7], gB.x * m[6]), gty = fmaf(hb, m[6], gB.z * m[7]);   // sum of t dL/dDelta
+      if (kCamera) dt_local -= fmaf(gA.z, gx, gA.w * gy);  // SensorGrads.d_time_offset
+      if (gx != 0.0f || gy != 0.0f || gtx != 0.0f || gty != 0.0f) red_add_v4(r0 + 4, -gx, -gy, -gtx, -gty);  // dL/dmean2d, dL/dvelocity.xy
+    }
   }
   __syncwarp();
 }
@@ -281,7 +286,7 @@ __device__ __forceinline__ void reduce_panel8(const WarpScratchT<kChunkS>& ws, i
           if (v != 0.0f) {  // channels >= the sensor's are exactly zero
             float* dst;
             if (kCamera) dst = c < 3 ? f0 + c : f1 + c;
-            else dst = c < 13 ? f1 + c : (c == 13 ? r0 + 25 : r0 + 23);  // 13: d/d range, 14: d/d v_r
+            else dst = c < 13 ? f1 + c : (c == 13 ? r0 + 25 : r0 + 24);  // 13: d/d range (slot 9), 14: d/d v_r (slot 8)
             atomicAdd(dst, v);
           }
         }
@@ -346,24 +351,21 @@ __device__ __forceinline__ void reduce_panel8(const WarpScratchT<kChunkS>& ws, i
 #pragma unroll
     for (int c = 0; c < 8; ++c) m[c] += __shfl_xor_sync(0xffffffffu, m[c], o);
   }
-  if (active && g == 0) {  // one RED per (warp, Gaussian, value)
+  // after the butterfly every lane of an entry holds the full sums (four lanes per entry): lane g = 0
+  // sends (conic, rho), lane g = 1 (mean2d, velocity.xy) — two 16-byte REDs per (warp, Gaussian) in one instruction
+  if (active && g < 2) {
     const float hb = 0.5f * gB.y;
-    const float gx = fmaf(hb, m[2], gB.x * m[1]), gy = fmaf(hb, m[1], gB.z * m[2]);     // sum of dL/dDelta
-    const float gtx = fmaf(hb, m[7], gB.x * m[6]), gty = fmaf(hb, m[6], gB.z * m[7]);   // sum of t dL/dDelta
-    float acc[8];
-    acc[0] = 0.5f * m[3];  // dL/dconic
-    acc[1] = 0.5f * m[4];
-    acc[2] = 0.5f * m[5];
-    acc[3] = -gx;  // dL/dmean2d
-    acc[4] = -gy;
-    acc[5] = -gtx;  // dL/dvelocity (first two components)
-    acc[6] = -gty;
-    acc[7] = __fdividef(-m[0], gB.w);  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
-    if (kCamera) dt_local -= fmaf(gA.z, gx, gA.w * gy);  // SensorGrads.d_time_offset
     float* r0 = rg.g + kRasterGradStride * (size_t)ws.src[e];
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (acc[c] != 0.0f) atomicAdd(r0 + (c < 7 ? c : 8), acc[c]);  // slots 0-6, rho at 8 (7: v_r, 9: range)
+    if (g == 0) {
+      const float a0 = 0.5f * m[3], a1 = 0.5f * m[4], a2 = 0.5f * m[5];  // dL/dconic
+      const float a3 = __fdividef(-m[0], gB.w);  // dL/drho = -dL/dsigma / rho (rho > 0 for every blended entry)
+      if (a0 != 0.0f || a1 != 0.0f || a2 != 0.0f || a3 != 0.0f) red_add_v4(r0, a0, a1, a2, a3);
+    } else {
+      const float gx = fmaf(hb, m[2], gB.x * m[1]), gy = fmaf(hb, m[1], gB.z * m[2]);     // sum of dL/dDelta
+      const float gtx = fmaf(hb, m[7], gB.x * m[6]), gty = fmaf(hb, m[6], gB.z * m[7]);   // sum of t dL/dDelta
+      if (kCamera) dt_local -= fmaf(gA.z, gx, gA.w * gy);  // SensorGrads.d_time_offset
+      if (gx != 0.0f || gy != 0.0f || gtx != 0.0f || gty != 0.0f) red_add_v4(r0 + 4, -gx, -gy, -gtx, -gty);  // dL/dmean2d, dL/dvelocity.xy
+    }
   }
   __syncwarp();
 }
