@@ -603,6 +603,11 @@ def run_b200(args):
     ckeys = {"raster_fwd": ["k_raster_fwd", "k_raster_fwd_lidar"], "raster_bwd": ["k_raster_bwd", "k_raster_bwd_lidar"], "project": ["k_project"], "project_bwd": ["k_project_bwd"],
              "tile_counts": ["k_tile_hist", "k_tile_scan"], "tile_sort": ["k_expand"], "depth_sort_scan": ["k_radix_hist", "k_radix_pass", "k_count_scan"]}
     cand, per_kernel = [], {}
+    red_path = os.path.join(ROOT, "profiles", "red_peak.json")
+    red_peak = None
+    if os.path.exists(red_path):
+        rp = json.load(open(red_path))
+        red_peak = max(v["g_sectors_per_s"] for v in rp.values() if isinstance(v, dict) and "g_sectors_per_s" in v)
 
     def kernel_label(stage, sensor):
         # the lidar's single-pass views composite with their own kernel pair (raster_lidar.cu, k_raster_bwd_lidar)
@@ -618,6 +623,14 @@ def run_b200(args):
             dram = sum(c["dram_bytes"] for c in cs) if cs else None
             e = {"ms": ms, "algorithmic_bytes": by[k], "frac": by[k] / (ms * 1e-3) / 1e9 / peak if ms > 0 else None,
                  "dram_bytes": dram, "dram_frac": dram / (ms * 1e-3) / 1e9 / peak if (dram and ms > 0) else None}
+            # the north star's other two counters: L2 hit rate, and the atomic (RED) sector rate over the LIVE kernel time
+            # against the ceiling scripts/red_peak.cu measured on a B200 (profiles/red_peak.json)
+            reds = sum(c.get("red_sectors") or 0.0 for c in cs) if cs else None
+            if cs and ms > 0:
+                e["l2_hit_frac"] = sum((c.get("l2_hit_pct") or 0.0) * c["time_ms"] for c in cs) / max(sum(c["time_ms"] for c in cs), 1e-12) / 100.0
+                e["red_sectors"] = reds
+                e["red_gsectors_s"] = reds / (ms * 1e-3) / 1e9 if reds else 0.0
+                e["red_frac"] = e["red_gsectors_s"] / red_peak if red_peak else None
             if len(cs) == 1:
                 e.update({"issue_frac": cs[0]["issue_active_pct"] / 100.0 if cs[0].get("issue_active_pct") is not None else None,
                           "sm_throughput_frac": cs[0]["sm_throughput_pct"] / 100.0 if cs[0].get("sm_throughput_pct") is not None else None,
@@ -640,6 +653,9 @@ def run_b200(args):
         "frac": achieved / peak, "frac_kind": "ALGORITHMIC bytes (SURVEY 8(d): every input read once, every output written once) / CUDA-event kernel time / measured HBM peak",
         "traffic": dom["dram_bytes"], "dram_frac": dom["dram_frac"], "issue_frac": dom.get("issue_frac"),
         "sm_throughput_frac": dom.get("sm_throughput_frac"), "warps_active_frac": dom.get("warps_active_frac"),
+        "l2_hit_frac": dom.get("l2_hit_frac"),
+        "atomic": {"red_sectors": dom.get("red_sectors"), "achieved": dom.get("red_gsectors_s"), "peak": red_peak, "unit": "G sectors/s",
+                   "frac": dom.get("red_frac"), "peak_source": "scripts/red_peak.cu on a B200 (profiles/red_peak.json: scattered 4-byte REDs over a 108 MB buffer)"} if red_peak else None,
         "counters_source": "profiles/counters.json (ncu --set full of this command with --serial; dram_frac = its DRAM bytes / the LIVE kernel time / peak)" if counters else None,
         "peak_source": peak_src,
         "kernel_ms": ms_k, "kernel_bytes": bytes_k, "kernel_share_of_step": ms_k / stage_total if stage_total else None,

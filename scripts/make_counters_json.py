@@ -22,7 +22,9 @@ PCT = {"issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active"
        "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
        "fma_pipe_pct": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
        "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
-       "lanes_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio", "warp_instructions": "smsp__inst_executed.sum"}
+       "lanes_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio", "warp_instructions": "smsp__inst_executed.sum",
+       "l2_hit_pct": "lts__t_sector_hit_rate.pct", "red_sectors": "lts__t_sectors_srcunit_tex_op_red.sum"}
+SUMS = ("warp_instructions", "red_sectors")   # summed over a kernel's launches; everything else is a duration-weighted mean
 
 
 def val(d, name):
@@ -55,10 +57,10 @@ for d in data:
     for k, metric in PCT.items():
         v = val(d, metric)
         if v is not None:
-            e[k] += v if k == "warp_instructions" else v * t
+            e[k] += v if k in SUMS else v * t
 for e in out.values():
     for k in PCT:
-        if k == "warp_instructions":
+        if k in SUMS:
             continue
         e[k] = e[k] / e["time_ms"] if e["time_ms"] > 0 else None
 json.dump(out, open(sys.argv[2], "w"), indent=1)
