@@ -5,6 +5,8 @@
 //                             tile rectangle and the packed compositing record.
 //   (tile binning — depth sort, duplication, tile sort, tile ranges — lives in binning.cu)
 //   k_raster_fwd<camera|lidar> per-tile front-to-back compositing (Eq. 3-6).
+#include <cstddef>
+
 #include "kernels.h"
 #include "raster_common.cuh"
 #include "decode_device.cuh"
@@ -120,13 +122,24 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
              const uint32_t* __restrict__ tile_begin, const uint32_t* __restrict__ tile_end,
              const float4* __restrict__ rays, const int64_t* __restrict__ ray_begin, const int64_t* __restrict__ ray_end,
              const uint32_t* __restrict__ tile_order, int tile_first, RasterOutDev out) {
-  __shared__ float4 sA[256];
-  __shared__ float4 sB[256];
-  __shared__ float2 sC[256];
-  __shared__ float4 sF[256 * 4];
-  __shared__ uint8_t sMask[256];
-  __shared__ uint8_t sList[8][256];
-  __shared__ __align__(8) uint8_t sHit[8][256];  // [warp][batch entry]: some lane of the warp blended it
+  // one struct: the camera's walk addresses every array relative to ONE pinned base register (raster_common.cuh: smem_addr)
+  struct Staged {
+    float4 sA[256];
+    float4 sB[256];
+    float4 sF[256 * 4];
+    float2 sC[256];
+    alignas(8) uint8_t sHit[8][256];  // [warp][batch entry]: some lane of the warp blended it
+    uint8_t sList[8][256];
+    uint8_t sMask[256];
+  };
+  __shared__ __align__(16) Staged sm;
+  auto& sA = sm.sA;
+  auto& sB = sm.sB;
+  auto& sC = sm.sC;
+  auto& sF = sm.sF;
+  auto& sMask = sm.sMask;
+  auto& sList = sm.sList;
+  auto& sHit = sm.sHit;
   __shared__ uint8_t sSub[kCamera ? 1 : 8][4][kCamera ? 1 : 256];  // lidar, [warp][group]: the group's entries of the batch, in list order
   __shared__ PatchBox sBox[9];  // 8 warp patches + the tile's box (patch_mask_fast)
   __shared__ PatchBox sGBox[kCamera ? 1 : 8][4];                   // lidar: boxes of the 8-lane groups
@@ -302,14 +315,32 @@ k_raster_fwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
         // the camera kernel is issue-bound: the plain loop has the fewest instructions
         // (group lists were measured on the camera as well: 0.98 -> 1.34 ms. Its footprints span the 8 x 4 patch, every
         // group keeps most entries, and the second-level cull is pure overhead: the camera walks the warp list)
+        // Shared memory by window address (raster_common.cuh: smem_addr): no per-iteration address re-materialisation.
+        const uint32_t aA = smem_addr_pinned(&sm);
+        const uint32_t aB = aA + (uint32_t)offsetof(Staged, sB), aF = aA + (uint32_t)offsetof(Staged, sF);
+        const uint32_t aL = aA + (uint32_t)offsetof(Staged, sList) + 256u * warp, aH = aA + (uint32_t)offsetof(Staged, sHit) + 256u * warp;
         for (int k = 0; k < n_w; ++k) {
           if ((k & 3) == 0 && __all_sync(0xffffffffu, done)) break;
-          const int j = lst[k];
-          const float4 gA = sA[j], gB = sB[j];
+          const uint32_t j = lds_u8(aL + k);
+          const float4 gA = lds_f4(aA + 16u * j), gB = lds_f4(aB + 16u * j);
           float dx, dy;
           const float qf = alpha_qform_packed(pack2(gA.x, gA.y), pack2(gA.z, gA.w), gB, q2, t2, dx, dy);  // same operations, 7 issue slots
           AlphaEval ev;
-          if (!done && alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) blend(j, ev);
+          if (!done && alpha_finish(qf, gB.w, dx, dy, s.qform_max, s.alpha_clamp, s.alpha_min, ev)) {
+            const float w = __fmul_rn(ev.alpha, T);
+            const f32x2 ww = pack2(w, w);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float4 f4 = lds_f4(aF + 64u * j + 16u * c);
+              acc2[2 * c] = fma2(pack2(f4.x, f4.y), ww, acc2[2 * c]);
+              acc2[2 * c + 1] = fma2(pack2(f4.z, f4.w), ww, acc2[2 * c + 1]);
+            }
+            T = __fmul_rn(T, __fsub_rn(1.0f, ev.alpha));
+            ++n_contrib;
+            last_idx = (int)(base - lb) + (int)j + 1;
+            sts_u8(aH + j, 1u);
+            if (T < s.transmittance_min) done = true;
+          }
         }
       } else {
         // the lidar kernel is latency-bound (wrap + fewer resident warps' worth of work per tile): two entries per

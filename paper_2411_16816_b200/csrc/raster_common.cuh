@@ -31,6 +31,32 @@ __device__ __forceinline__ float wrap_pi(float a) {
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // ------------------------------------------------------------------------------------------------
+// Shared-memory accesses by 32-bit window address. nvcc forms the address of a __shared__ array as
+// (SR_CgaCtaId << 24) + offset (S2R + MOV + LEA) and, in the register-capped compositing loops, re-materialises it on
+// every iteration instead of keeping it in a register: 6 of the ~33 instructions the camera forward spends per
+// evaluated list entry. One base address is therefore pinned in a register (an opaque mov) and every array of the loop is
+// addressed relative to it (the differences between the arrays' addresses are compile-time constants).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// the same address as an opaque register value: the compiler cannot re-derive it, so it stays in a register across a loop
+__device__ __forceinline__ uint32_t smem_addr_pinned(const void* p) {
+  uint32_t a = smem_addr(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+
+// ------------------------------------------------------------------------------------------------
 // Packed fp32 pairs (sm_100a: FFMA2 / FMUL2 / FADD2 execute two IEEE-754 round-to-nearest operations per issue slot;
 // each half is bit-identical to the scalar __f*_rn operation, so the parity contract is untouched). The compositing
 // kernels are issue-bound, not FMA-pipe-bound: halving the fp32 instruction count of the inner loops is the point.
