@@ -641,8 +641,10 @@ k_raster_bwd(const __grid_constant__ Sensor s, ProjDev p, const uint32_t* __rest
           const int j0 = sList[k], j1 = sList[has1 ? k - 1 : k];
           const float4 a0 = sA[j0], b0 = sB[j0], a1 = sA[j1], b1 = sB[j1];
           float dx0, dy0, dx1, dy1;
-          const float qf0 = alpha_qform<!kCamera>(a0, b0, qx, qy, t, dx0, dy0, wrap);
-          const float qf1 = alpha_qform<!kCamera>(a1, b1, qx, qy, t, dx1, dy1, wrap);
+          const float qf0 = kCamera ? alpha_qform_packed(pack2(a0.x, a0.y), pack2(a0.z, a0.w), b0, pack2(qx, qy), pack2(t, t), dx0, dy0)
+                                    : alpha_qform<!kCamera>(a0, b0, qx, qy, t, dx0, dy0, wrap);
+          const float qf1 = kCamera ? alpha_qform_packed(pack2(a1.x, a1.y), pack2(a1.z, a1.w), b1, pack2(qx, qy), pack2(t, t), dx1, dy1)
+                                    : alpha_qform<!kCamera>(a1, b1, qx, qy, t, dx1, dy1, wrap);
           AlphaEval ev;
           bool valid = ((int)sPos[j0] < last) && alpha_finish(qf0, b0.w, dx0, dy0, s.qform_max, s.alpha_clamp, s.alpha_min, ev);
           if (sure || __any_sync(0xffffffffu, valid)) park(j0, valid, ev);
