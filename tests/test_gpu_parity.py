@@ -1378,6 +1378,69 @@ def test_library_nccl_collective_world1(api, op):
         c2.close()
 
 
+def _nccl_world2_worker(rank, uid, out_dir):
+    """One rank of test_library_nccl_collective_world2 (its own process and its own GPU)."""
+    import os
+    import torch
+    from paper_2411_16816_b200 import api as _api
+    cfg = {"lr_init": [1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-3], "lr_final": [1.6e-6, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-4],
+           "warmup_steps": [0] * 6, "total_steps": 10}
+    torch.cuda.set_device(rank)
+    sc = synth.make_scene(5_003, seed=31, r_max=30.0, scale_mean=0.1)   # 27 * 5003 floats: not a multiple of 2 * 4
+    c = _api.Context(rank)
+    try:
+        c.upload_scene(sc)
+        c.comm_init(uid, rank, 2)
+        assert c.comm_world == 2
+        g = np.random.default_rng(100 + rank).normal(size=c.grads_size).astype(np.float32)
+        grads_t = torch.from_numpy(g.copy()).cuda()
+        c.bind_grads_device(grads_t.data_ptr(), c.grads_size)
+        c.allreduce_grads()
+        c.sync()
+        np.save(os.path.join(out_dir, f"sum_{rank}.npy"), grads_t.cpu().numpy())
+        # second step's local gradients, reduced inside the sharded step (reduce-scatter -> Adam on the shard -> all-gather)
+        grads_t.copy_(torch.from_numpy(g))
+        skipped = c.sharded_optimizer_step(cfg, 0)
+        assert skipped == []
+        for k, a in enumerate(c.download_scene()):
+            np.save(os.path.join(out_dir, f"param{k}_{rank}.npy"), a)
+        c.comm_destroy()
+    finally:
+        c.close()
+
+
+def test_library_nccl_collective_world2(api, tmp_path):
+    """Two ranks on two GPUs through the library's own communicator (skipped on a one-GPU box: NCCL refuses two ranks
+    on one device): the all-reduced gradient buffer is the same on both ranks and equals the fp32 sum of the two local
+    buffers, and the sharded optimizer step (total not divisible by world * 4) leaves both ranks with the parameters
+    an all-reduce followed by the plain step gives a single context."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    import torch.multiprocessing as mp
+    uid = api.nccl_unique_id()
+    mp.spawn(_nccl_world2_worker, args=(uid, str(tmp_path)), nprocs=2, join=True)
+    s0, s1 = np.load(tmp_path / "sum_0.npy"), np.load(tmp_path / "sum_1.npy")
+    g0 = np.random.default_rng(100).normal(size=s0.size).astype(np.float32)
+    g1 = np.random.default_rng(101).normal(size=s0.size).astype(np.float32)
+    assert np.array_equal(s0, s1) and np.array_equal(s0, g0 + g1)     # two-operand fp32 sum: order-free, bit-exact
+    cfg = {"lr_init": [1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-3], "lr_final": [1.6e-6, 5e-3, 1e-3, 5e-2, 2.5e-3, 2.5e-4],
+           "warmup_steps": [0] * 6, "total_steps": 10}
+    sc = synth.make_scene(5_003, seed=31, r_max=30.0, scale_mean=0.1)
+    c = api.Context(0)
+    try:
+        c.upload_scene(sc)
+        t = torch.from_numpy(g0 + g1).cuda()
+        c.bind_grads_device(t.data_ptr(), c.grads_size)
+        assert c.optimizer_step(cfg, 0) == []
+        want = c.download_scene()
+    finally:
+        c.close()
+    for k, a in enumerate(want):
+        for r in range(2):
+            assert np.array_equal(a, np.load(tmp_path / f"param{k}_{r}.npy")), (k, r)
+
+
 # ---- camera ConvDecoder (SURVEY.md §8(f) rank 3): tcgen05 / tf32 implicit-GEMM convolutions -----------------------
 # tf32 operands (10-bit mantissa, rounded to nearest) with fp32 accumulation: 2^-11 relative per operand; over five
 # layers the image agrees with the fp32 oracle to DEC_RTOL of the output scale.
