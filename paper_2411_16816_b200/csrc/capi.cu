@@ -48,6 +48,13 @@ struct splatb200_ctx {
   cudaStream_t s_app = nullptr;
   cudaEvent_t ev_geo = nullptr, ev_app = nullptr;
   bool app_pending = false;
+  // Small transfers first (banded host-buffer calls). The copy engines were seen (CUPTI timeline of the north-star
+  // frame, scripts/e2e_probe.py) to take a lidar view's one 15 MB download only after ALL ~150 MB of band copies a
+  // camera view had queued — although it was submitted first and ready 3 ms earlier —, so the lidar's upload,
+  // compositing backward and k_project_bwd ran alone at the end of the step. A single-band view therefore publishes
+  // its pending download / upload event here, and a multi-band view lets it pass in front of its second band.
+  std::mutex xfer_mu;  // views may be driven from several host threads
+  cudaEvent_t yield_dl = nullptr, yield_ul = nullptr;
   int decoder_precise = 0;     // ConvDecoder convolutions in split-tf32 (three passes: fp32 accuracy) instead of plain tf32
 
   // scene
@@ -1025,6 +1032,11 @@ extern "C" void splatb200_view_destroy(splatb200_view* v) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   finalize_actor_grads(v);
+  {
+    std::lock_guard<std::mutex> lk(c->xfer_mu);  // the yield slots may hold this view's events
+    c->yield_dl = nullptr;
+    c->yield_ul = nullptr;
+  }
   free_view_buffers(v);
   for (size_t k = 0; k < c->views.size(); ++k)
     if (c->views[k] == v) {
@@ -1854,6 +1866,15 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
       c->launches += 1;
       CU_TRY(c, cudaEventRecord(v->ev_bfwd[b], st));
       CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, v->ev_bfwd[b], 0));
+      if (b >= 1 && !getenv("SPLATB200_NO_YIELD")) {  // small transfers first (splatb200_ctx::yield_dl)
+        cudaEvent_t e = nullptr;
+        {
+          std::lock_guard<std::mutex> lk(c->xfer_mu);
+          e = c->yield_dl;
+          c->yield_dl = nullptr;
+        }
+        if (e) CU_TRY(c, cudaStreamWaitEvent(v->s_d2h, e, 0));
+      }
       const size_t q0 = (size_t)bd.q0, nq = (size_t)(bd.q1 - bd.q0);
       if (nq) {
         if (v->plan_blend) CU_TRY(c, cudaMemcpyAsync(v->plan_blend + 16 * q0, v->out.blend + 16 * q0, sizeof(float) * 16 * nq, cudaMemcpyDeviceToHost, v->s_d2h));
@@ -1863,6 +1884,10 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
       CU_TRY(c, cudaEventRecord(v->ev_bdl[b], v->s_d2h));
     }
     CU_TRY(c, cudaEventRecord(v->ev_dl, v->s_d2h));
+    if (v->bands.size() == 1) {
+      std::lock_guard<std::mutex> lk(c->xfer_mu);
+      c->yield_dl = v->ev_dl;
+    }
     v->dl_pending = true;
     v->band_dl_valid = true;
   }
@@ -1916,11 +1941,24 @@ extern "C" int splatb200_view_backward(splatb200_view* v, const float* g_blend16
       const auto& bd = v->bands[b];
       const size_t q0 = (size_t)bd.q0, nq = (size_t)(bd.q1 - bd.q0);
       if (v->band_dl_valid) CU_TRY(c, cudaStreamWaitEvent(v->s_h2d, v->ev_bdl[b], 0));
+      if (b >= 1 && !getenv("SPLATB200_NO_YIELD")) {  // small transfers first (splatb200_ctx::yield_ul)
+        cudaEvent_t e = nullptr;
+        {
+          std::lock_guard<std::mutex> lk(c->xfer_mu);
+          e = c->yield_ul;
+          c->yield_ul = nullptr;
+        }
+        if (e) CU_TRY(c, cudaStreamWaitEvent(v->s_h2d, e, 0));
+      }
       if (nq) {
         CU_TRY(c, cudaMemcpyAsync(v->g_blend_stage + 16 * q0, v->plan_gb + 16 * q0, sizeof(float) * 16 * nq, cudaMemcpyHostToDevice, v->s_h2d));
         CU_TRY(c, cudaMemcpyAsync(v->g_alpha_stage + q0, v->plan_ga + q0, sizeof(float) * nq, cudaMemcpyHostToDevice, v->s_h2d));
       }
       CU_TRY(c, cudaEventRecord(v->ev_bup[b], v->s_h2d));
+      if (v->bands.size() == 1) {
+        std::lock_guard<std::mutex> lk(c->xfer_mu);
+        c->yield_ul = v->ev_bup[b];
+      }
     }
     for (size_t b = 0; b < v->bands.size(); ++b) {
       const auto& bd = v->bands[b];

@@ -70,6 +70,35 @@ with torch.cuda.stream(stream):
         torch.cuda.synchronize()
         print(f"{label:50s} {(time.perf_counter() - t0) * 100:.3f} ms", flush=True)
 
+    if os.environ.get("E2E_TRACE"):
+        # timeline of one end-to-end step (CUPTI through torch.profiler): every kernel and copy with its stream, start
+        # and duration, relative to the step's first activity -> gpurun_out/e2e_trace.txt
+        from torch.profiler import ProfilerActivity, profile
+        kw = dict(upload=os.environ["E2E_TRACE"] != "mid", download=os.environ["E2E_TRACE"] != "mid")
+        for _ in range(3):
+            step(**kw)
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+            for _ in range(3):          # the first profiled steps pay CUPTI's lazy set-up: keep the last one
+                step(**kw)
+                torch.cuda.synchronize()
+        prof.export_chrome_trace("gpurun_out/e2e_trace.json")
+        import json
+        ev = [e for e in json.load(open("gpurun_out/e2e_trace.json"))["traceEvents"]
+              if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset", "cuda_runtime", "cuda_driver")]
+        ev.sort(key=lambda e: e["ts"])
+        big = [e for e in ev if e["cat"] == "gpu_memset" and e.get("args", {}).get("bytes", 0) > 50_000_000]
+        last0 = big[-1]["ts"] - 400.0       # zero_grads of the last step (its host call starts a little earlier)
+        ev = [e for e in ev if e["ts"] >= last0]
+        t0 = ev[0]["ts"]
+        with open("gpurun_out/e2e_trace.txt", "w") as f:
+            for e in ev:
+                a = e.get("args", {})
+                f.write("%9.1f %8.1f %s s%-3s %s %s\n" % (e["ts"] - t0, e["dur"], "host t%s" % e.get("tid") if e["cat"].startswith("cuda_") else "gpu", a.get("stream", "?"), e["name"][:60].replace("\n", " "),
+                                                     a.get("bytes", "")))
+        os.remove("gpurun_out/e2e_trace.json")
+        print("trace written:", len(ev), "activities, span %.3f ms" % ((ev[-1]["ts"] + ev[-1]["dur"] - t0) / 1e3))
+        sys.exit(0)
     timeit("full e2e, 4 bands")
     timeit("full e2e, 8 bands", bands=8)
     timeit("full e2e, 2 bands", bands=2)
