@@ -70,6 +70,24 @@ with torch.cuda.stream(stream):
         torch.cuda.synchronize()
         print(f"{label:50s} {(time.perf_counter() - t0) * 100:.3f} ms", flush=True)
 
+    g_dev = {}
+    for name in ("l", "c"):
+        g_dev[name] = (torch.from_numpy(np.ascontiguousarray(g_host[name][2])).to(dev), torch.from_numpy(np.ascontiguousarray(g_host[name][3])).to(dev))
+
+    def step_dev(upload=False, download=False):
+        """the device-resident frame bench.py times as `value`"""
+        ctx.zero_grads()
+
+        def run_view(name, v):
+            v.forward(0.0)
+            v.backward_device(g_dev[name][0].data_ptr(), g_dev[name][1].data_ptr())
+        for f in [pool.submit(run_view, name, v) for name, v in (("l", vl), ("c", vc))]:
+            f.result()
+        ctx.join()
+        ctx.sync()
+
+    if os.environ.get("E2E_TRACE") == "dev":
+        step = step_dev
     if os.environ.get("E2E_TRACE"):
         # timeline of one end-to-end step (CUPTI through torch.profiler): every kernel and copy with its stream, start
         # and duration, relative to the step's first activity -> gpurun_out/e2e_trace.txt
