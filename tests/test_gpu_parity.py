@@ -912,7 +912,7 @@ def test_overlapped_host_buffer_calls(ctx):
     ctx.upload_scene(sc)
     lid = synth.lidar32()
     vl = ctx.lidar_view(lid, synth.grid_rays(lid), ST)
-    vc = ctx.camera_view(synth.make_camera(width=640, height=360), ST)
+    vc = ctx.camera_view(synth.make_camera(width=640, height=528), ST)
     keep, host = [], {}
     for name, v in (("l", vl), ("c", vc)):
         gb, ga = synth.upstream(v.P, seed=3)
@@ -941,7 +941,7 @@ def test_overlapped_host_buffer_calls(ctx):
             if step < 2:
                 v.forward(0.0)
                 v.download_async(vb, va, vn)
-            else:       # fused, banded forms (camera: 1, 3 and 8 bands over 23 tile rows)
+            else:       # fused, banded forms (camera: 1, 3 and 8 bands over 33 tile rows)
                 v.forward_to_host(0.0, vb, va, vn, bands=(1, 3, 8)[step - 2])
         for name, v in (("l", vl), ("c", vc)):
             if step < 2:
