@@ -957,25 +957,4 @@ void launch_expand(int stiles_x, int stiles_y, int tiles_x, int tiles_y, int64_t
                                                tile_begin, hdr + kHdrWords, hdr, hdr + 16, vals);
 }
 
-// ------------------------------------------------------------------------------------------------
-// The host's one read per render: see kernels.h.
-// ------------------------------------------------------------------------------------------------
-__global__ void k_gather_totals(const int64_t* __restrict__ total, const uint32_t* __restrict__ scan_total,
-                                const int64_t* __restrict__ total_c, const uint32_t* err0, const uint32_t* err1,
-                                const uint32_t* err2, volatile int64_t* out_host) {
-  if (threadIdx.x != 0) return;
-  out_host[0] = *total;
-  out_host[1] = (int64_t)*scan_total;
-  out_host[2] = total_c ? *total_c : 0;
-  out_host[3] = err0 ? (int64_t)ld_volatile(err0) : 0;
-  out_host[4] = err1 ? (int64_t)ld_volatile(err1) : 0;
-  out_host[5] = err2 ? (int64_t)ld_volatile(err2) : 0;
-  __threadfence_system();
-}
-
-void launch_gather_totals(const int64_t* total, const uint32_t* scan_total, const int64_t* total_c, const uint32_t* err0,
-                          const uint32_t* err1, const uint32_t* err2, int64_t* out_host, cudaStream_t st) {
-  k_gather_totals<<<1, 32, 0, st>>>(total, scan_total, total_c, err0, err1, err2, out_host);
-}
-
 }  // namespace sb

@@ -1779,16 +1779,15 @@ extern "C" int splatb200_view_forward(splatb200_view* v, float t_scene, int32_t 
     }
   }
   CHECK_LAUNCH(c, "depth sort + scan");
-  for (int k = 0; k < 8; ++k) v->h_total[k] = 0;
+  for (int k = 1; k < 8; ++k) v->h_total[k] = 0;
   // look-back time-out flags (word 16 of each sort workspace): this frame's depth sort, the previous frame's tile sort
   // and expansion (their workspaces are only cleared when the next one is launched, after this sync)
-  // one single-thread kernel writes all six words into the pinned, mapped h_total (kernels.h): up to six 4- and 8-byte
-  // engine copies of ~7 us each sat here, on the critical path of the latency-bound binning chain
-  launch_gather_totals(v->d_total, v->offsets + c->n, v->two_level ? v->d_total_c : nullptr, (const uint32_t*)v->dsort_temp + 16,
-                       (v->sort_temp && v->I > 0) ? (const uint32_t*)v->sort_temp + 16 : nullptr,
-                       (v->expand_temp && v->I > 0) ? (const uint32_t*)v->expand_temp + 16 : nullptr, v->h_total, st);
-  CHECK_LAUNCH(c, "k_gather_totals");
-  c->launches += 1;
+  CU_TRY(c, cudaMemcpyAsync(v->h_total + 3, (const uint32_t*)v->dsort_temp + 16, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (v->sort_temp && v->I > 0) CU_TRY(c, cudaMemcpyAsync(v->h_total + 4, (const uint32_t*)v->sort_temp + 16, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (v->expand_temp && v->I > 0) CU_TRY(c, cudaMemcpyAsync(v->h_total + 5, (const uint32_t*)v->expand_temp + 16, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU_TRY(c, cudaMemcpyAsync(v->h_total, v->d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU_TRY(c, cudaMemcpyAsync(v->h_total + 1, v->offsets + c->n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (v->two_level) CU_TRY(c, cudaMemcpyAsync(v->h_total + 2, v->d_total_c, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU_TRY(c, cudaStreamSynchronize(st));
   if (c->profiling) harvest_stage_events(v);  // previous step's events have all completed by now
   if (v->h_total[3] | v->h_total[4] | v->h_total[5])

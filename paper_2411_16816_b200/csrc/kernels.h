@@ -152,12 +152,6 @@ void launch_gather_u32(int64_t n, const uint32_t* src, const uint32_t* idx, uint
 size_t depth_sort_temp_bytes(int64_t n);
 // stable sort of (dkey, position) by the 32-bit key; the sorted source indices land in order0 (dkey, dkey_alt, order1
 // are scratch), then offsets[k] = sum_{k' < k} count[order0[k']] for k in [0, n]. Returns the number of kernels launched.
-// The scalars the host reads at the one sync of a render, gathered by ONE single-thread kernel that writes them into
-// the (pinned, mapped) host words out[0..5]: the intersection total, the count scan's total, the block-grid total
-// (or 0) and three look-back time-out flags (null -> 0). Replaces up to six 4- and 8-byte engine copies of ~7 us each
-// on the critical path of the latency-bound binning chain.
-void launch_gather_totals(const int64_t* total, const uint32_t* scan_total, const int64_t* total_c, const uint32_t* err0,
-                          const uint32_t* err1, const uint32_t* err2, int64_t* out_host, cudaStream_t st);
 int launch_depth_sort_scan(uint32_t* dkey, uint32_t* dkey_alt, uint32_t* order0, uint32_t* order1, const uint32_t* count,
                            uint32_t* offsets, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
 int super_shift();  // log2 of the block edge (in tiles) of the camera's two-level binning
